@@ -1,0 +1,199 @@
+// ref_driver.cpp — extern "C" shim over the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file together
+// with the reference's own sources (/root/reference/proj/src/*.cpp, read in
+// place, never copied) into oracle/_ref/libreplab_ref.so.  Python tests use
+// it to pin the C restatement (oracle/replay_oracle.c) and to generate the
+// golden fixtures under tests/golden/; bench.py uses it as the CPU
+// reference arm.  Every call below goes straight into the reference API:
+//   replab::Rng                 rng.hpp:22-69
+//   replab::ShardedReplayBuffer replay_buffer.hpp:57-108
+//   replab::group_advantages    bandit.hpp:106
+//   replab::grpo_loss_grad / asymre_loss_grad  bandit.hpp:133-139
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "replab/bandit.hpp"
+#include "replab/metrics.hpp"
+#include "replab/replay_buffer.hpp"
+#include "replab/rng.hpp"
+#include "replab/rollout.hpp"
+
+using namespace replab;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+RetentionPolicy retention_of(int kind, double delta) {
+    return kind == 1 ? RetentionPolicy::positive_bias(delta) : RetentionPolicy::plain_fifo();
+}
+SamplingStrategy strategy_of(int s) {
+    switch (s) {
+        case 1: return SamplingStrategy::uniform_without_replacement;
+        case 2: return SamplingStrategy::unused_first_without_replacement;
+        default: return SamplingStrategy::uniform_with_replacement;
+    }
+}
+static_assert(sizeof(RolloutRecord) == 80, "record layout must match rb_record");
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ---- Rng ---------------------------------------------------------------
+void* ref_rng_new(uint64_t seed) { return new Rng(seed); }
+void ref_rng_free(void* r) { delete static_cast<Rng*>(r); }
+void* ref_rng_stream(void* r, const char* name) {
+    return new Rng(static_cast<Rng*>(r)->stream(name));
+}
+void* ref_rng_stream_idx(void* r, const char* name, uint64_t idx) {
+    return new Rng(static_cast<Rng*>(r)->stream(name, idx));
+}
+uint64_t ref_rng_seed(void* r) { return static_cast<Rng*>(r)->seed(); }
+uint64_t ref_rng_next(void* r) { return static_cast<Rng*>(r)->next_u64(); }
+int ref_rng_below(void* r, uint64_t b, uint64_t* out) {
+    return guard([&] { *out = static_cast<Rng*>(r)->below(b); });
+}
+double ref_rng_uniform01(void* r) { return static_cast<Rng*>(r)->uniform01(); }
+double ref_rng_normal(void* r) { return static_cast<Rng*>(r)->normal(); }
+int ref_rng_swor(void* r, uint64_t n, uint64_t k, uint64_t* out) {
+    return guard([&] {
+        auto v = static_cast<Rng*>(r)->sample_without_replacement(n, k);
+        for (size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+    });
+}
+uint64_t ref_hash_name(const char* name) { return hash_name(name); }
+
+// ---- ShardedReplayBuffer -----------------------------------------------
+void* ref_buf_new(uint64_t shards, uint64_t cap, int strategy, int retention, double delta) {
+    ShardedReplayBuffer* out = nullptr;
+    int st = guard([&] {
+        out = new ShardedReplayBuffer(shards, cap, strategy_of(strategy),
+                                      retention_of(retention, delta));
+    });
+    return st == 0 ? out : nullptr;
+}
+void ref_buf_free(void* b) { delete static_cast<ShardedReplayBuffer*>(b); }
+int ref_buf_push(void* b, const RolloutRecord* rec, RolloutRecord* evicted, int* has_evicted) {
+    return guard([&] {
+        *has_evicted = 0;
+        auto ev = static_cast<ShardedReplayBuffer*>(b)->push(*rec);
+        if (ev) {
+            *evicted = *ev;
+            *has_evicted = 1;
+        }
+    });
+}
+// events (optional): 5 int64 per selection {id, creation_step, use_step, batch_id, rank}
+int ref_buf_sample(void* b, uint64_t batch, void* rng, RolloutRecord* out, int64_t* events,
+                   int64_t batch_id, int64_t use_step) {
+    return guard([&] {
+        MetricsLedger ledger;
+        auto v = static_cast<ShardedReplayBuffer*>(b)->sample(
+            batch, *static_cast<Rng*>(rng), events ? &ledger : nullptr, batch_id, use_step);
+        for (size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+        if (events) {
+            const auto& ev = ledger.events();
+            for (size_t i = 0; i < ev.size(); ++i) {
+                events[5 * i + 0] = static_cast<int64_t>(ev[i].rollout_id);
+                events[5 * i + 1] = ev[i].creation_step;
+                events[5 * i + 2] = ev[i].use_step;
+                events[5 * i + 3] = ev[i].batch_id;
+                events[5 * i + 4] = ev[i].within_batch_rank;
+            }
+        }
+    });
+}
+uint64_t ref_buf_size(void* b) { return static_cast<ShardedReplayBuffer*>(b)->size(); }
+uint64_t ref_buf_shard_size(void* b, uint64_t s) {
+    return static_cast<ShardedReplayBuffer*>(b)->shard_size(s);
+}
+uint64_t ref_buf_shard_contents(void* b, uint64_t s, RolloutRecord* out) {
+    auto v = static_cast<ShardedReplayBuffer*>(b)->shard_contents(s);
+    for (size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+    return v.size();
+}
+// Writes the dump into out (capacity cap incl. NUL); returns the full length.
+uint64_t ref_buf_dump(void* b, char* out, uint64_t cap) {
+    std::string d = static_cast<ShardedReplayBuffer*>(b)->dump();
+    if (out && cap) {
+        size_t n = d.size() < cap - 1 ? d.size() : cap - 1;
+        std::memcpy(out, d.data(), n);
+        out[n] = 0;
+    }
+    return d.size();
+}
+void* ref_buf_load(const char* text) {
+    ShardedReplayBuffer* out = nullptr;
+    int st = guard([&] { out = new ShardedReplayBuffer(ShardedReplayBuffer::load(text)); });
+    return st == 0 ? out : nullptr;
+}
+
+// ---- advantages and losses ---------------------------------------------
+int ref_group_advantages(const double* r, uint64_t n, double* out) {
+    return guard([&] {
+        auto v = group_advantages(std::vector<double>(r, r + n));
+        for (size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+    });
+}
+
+// Record-level losses through the reference's own grpo_loss_grad /
+// asymre_loss_grad.  Each record i gets its own prompt row with two arms and
+// logits (log(p/(1-p)), 0), p = exp(logp_want[i]), so the reference's
+// logprob(i, arm 0) ~= logp_want[i]; the value the reference actually used
+// is returned in logp_used.  Per-record dL/dlogp is recovered from the logit
+// gradient: grad[i,0] = dL/dlogp * (1 - p_i) / tau with tau = 1.
+int ref_loss_records(int kind, const double* logp_want, const RolloutRecord* recs,
+                     const double* group_mean, uint64_t n, double eps_low, double eps_high,
+                     double delta_v, double* logp_used, double* dlogp, double* objective,
+                     uint64_t* excluded) {
+    return guard([&] {
+        SoftmaxPolicy pol = SoftmaxPolicy::uniform(n, 2);
+        RolloutSideTables tables;
+        std::vector<RolloutRecord> batch(recs, recs + n);
+        for (uint64_t i = 0; i < n; ++i) {
+            const double p = std::exp(logp_want[i]);
+            pol.logit(i, 0) = std::log(p / (1.0 - p));
+            pol.logit(i, 1) = 0.0;
+            batch[i].prompt_id = i;
+            batch[i].rollout_id = i;  // side tables are keyed by our row index
+            batch[i].group_id = i;
+            tables.arm_of[i] = 0;
+            tables.group_mean_reward[i] = group_mean ? group_mean[i] : 0.0;
+            logp_used[i] = pol.logprob(i, 0, 1.0);
+        }
+        LossSpec spec = kind == 0 ? LossSpec::grpo(eps_low, eps_high, 2)
+                                  : LossSpec::asymre(delta_v, 2);
+        LossResult res = loss_grad(pol, batch, tables, spec);
+        for (uint64_t i = 0; i < n; ++i) {
+            const double p0 = pol.probs(i, 1.0)[0];
+            dlogp[i] = res.grad[2 * i] / (1.0 - p0);
+        }
+        *objective = res.objective;
+        *excluded = res.excluded;
+    });
+}
+
+}  // extern "C"
