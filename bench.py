@@ -1,0 +1,544 @@
+#!/usr/bin/env python
+"""bench.py — replay-step tokens/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c4|c3|c1|c2] [--no-e2e] [--no-cpu-baseline]
+
+A step is one replay step of the path: insert the step's
+freshly produced groups (device advantages, eviction), sample B trajectories
+(MT19937-64 "buffer_sampling" stream), ragged-gather their tokens, and
+evaluate the per-token GRPO loss + dL/dlogp.  The workload is C4 of
+SURVEY.md §8d by default (buffer 16384 sharded over the N GPUs, 256 prompts
+x G=16 = 4096 trajectories/step, 4096 tokens each, (W,T)=(5,3), mu=5.28).
+logp_now comes from a synthetic trainer stand-in run between the two
+phases (its time is reported separately and excluded from the step time).
+Inputs are synthetic (include/replay_synth.h), resident in HBM before the
+timed region; the buffer (537 MB) and per-step traffic exceed the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+CONFIGS = {
+    "c4": dict(name="C4: buffer 16384 trajectories sharded over the GPUs, 256 prompts x G=16 "
+                    "per step, 4096-token responses, FIFO, uniform with replacement, GRPO",
+               capacity=16384, batch=4096, group=16, lmax=4096, ragged=False,
+               retention="plain_fifo", delta=0.0, loss="grpo"),
+    "c3": dict(name="C3: buffer 1024, G=16, 64 prompts, ragged U{1..8192} tokens, 1 GPU, GRPO",
+               capacity=1024, batch=1024, group=16, lmax=8192, ragged=True,
+               retention="plain_fifo", delta=0.0, loss="grpo"),
+    "c1": dict(name="C1: buffer 84, (W,T)=(5,3), G=8, 64 prompts, 1024 tokens, GRPO",
+               capacity=84, batch=512, group=8, lmax=1024, ragged=False,
+               retention="plain_fifo", delta=0.0, loss="grpo"),
+    "c2": dict(name="C2: C1 + positive-bias retention (delta=0.5) + AsymRE",
+               capacity=84, batch=512, group=8, lmax=1024, ragged=False,
+               retention="positive_bias", delta=0.5, loss="asymre"),
+}
+W_WORKERS, T_TRAINERS, MU, SEED = 5, 3, 5.28, 1
+EPS_LOW, EPS_HIGH, DELTA_V = 0.2, 0.2, -0.1
+
+
+def algorithmic_bytes(t_ins, t_samp, r, b, loss):
+    """16*T_ins + b_loss*T_samp + 64*R + 32*B (b_loss 20 GRPO / 16 AsymRE)."""
+    return 16 * t_ins + (20 if loss == "grpo" else 16) * t_samp + 64 * r + 32 * b
+
+
+def peaks():
+    try:
+        p = json.load(open(PEAKS_PATH))
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- schedule
+def schedule(cfg, steps):
+    """Groups produced before step 0 (warm-up fill) and per step (bandit.cpp:609-640)."""
+    g = cfg["group"]
+    warm = math.ceil(cfg["capacity"] / g)
+    per = W_WORKERS * cfg["batch"] / (MU * T_TRAINERS)
+    debt, out = 0.0, []
+    for _ in range(steps):
+        debt += per
+        n = 0
+        while debt >= g:
+            n += 1
+            debt -= g
+        out.append(n)
+    return warm, out
+
+
+class Clocks:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 3 + i and r[3 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- our arm
+class Workload:
+    """Pre-generated inbound batches (device) for every step."""
+
+    def __init__(self, cfg, nsteps, dev, stream):
+        import torch
+
+        from tools import synth
+
+        self.cfg = cfg
+        g = cfg["group"]
+        warm, per_step = schedule(cfg, nsteps)
+        self.batches = []
+        nid, ngid = 0, 0
+        prompts = cfg["batch"] // g
+        plan = [(warm, 0)] + [(n, s) for s, n in enumerate(per_step)]
+        for ngroups, step in plan:
+            n = ngroups * g
+            ids = torch.arange(nid, nid + n, dtype=torch.int64, device=dev)
+            reward = torch.empty(n, dtype=torch.float64, device=dev)
+            length = torch.empty(n, dtype=torch.int32, device=dev)
+            blp = torch.empty(n, dtype=torch.float64, device=dev)
+            synth.fill_meta(SEED, ids, cfg["lmax"], cfg["ragged"], reward, length, blp, stream)
+            toff = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+            toff[1:] = torch.cumsum(length.to(torch.int64), 0)
+            tot = int(toff[-1])
+            pad = (tot + 3) // 4 * 4 + 4
+            tokens = torch.empty(pad, dtype=torch.int32, device=dev)
+            lpo = torch.empty(pad, dtype=torch.float32, device=dev)
+            synth.fill_payload(SEED, ids, toff, tokens, lpo, stream)
+            gid = torch.arange(ngid, ngid + ngroups, dtype=torch.int64, device=dev).repeat_interleave(g)
+            b = dict(rollout_id=ids, reward=reward, behavior_logprob=blp,
+                     group_id=gid, prompt_id=gid % prompts,
+                     creation_step=torch.full((n,), step, dtype=torch.int64, device=dev),
+                     policy_version=torch.full((n,), step, dtype=torch.int64, device=dev),
+                     group_offsets=torch.arange(0, n + 1, g, dtype=torch.int64, device=dev),
+                     tok_offsets=toff, tokens=tokens, logp_old=lpo)
+            self.batches.append((b, n, tot))
+            nid += n
+            ngid += ngroups
+        torch.cuda.synchronize()
+        self.warm = self.batches[0]
+        self.steps = self.batches[1:]
+
+
+def run_ours(args, rank, world, dist):
+    import torch
+
+    import paper_2604_08706_b200 as rb
+    from tools import synth
+
+    cfg = CONFIGS[args.config]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    T, N, B = world, cfg["capacity"], cfg["batch"]
+    assert N % T == 0 and B % T == 0, "config not divisible by the GPU count"
+    buf = rb.ShardedReplayBuffer(T, N, "uniform_with_replacement", cfg["retention"], cfg["delta"],
+                                 max_tokens=cfg["lmax"], shard_range=(rank, rank + 1))
+    buf.set_stream(sh)
+    rng = rb.Rng(SEED).stream("buffer_sampling")
+    K, Wm = args.steps, args.warmup
+    wl = Workload(cfg, K + Wm, dev, sh)
+    # warm-up fill (bandit.cpp:609-615)
+    b, n, _ = wl.warm
+    for lo in range(0, n, 4096):
+        hi = min(n, lo + 4096)
+        part = {k: v for k, v in b.items() if k not in ("group_offsets", "tok_offsets", "tokens", "logp_old")}
+        part = {k: v[lo:hi] for k, v in part.items()}
+        goff = torch.arange(0, hi - lo + 1, cfg["group"], dtype=torch.int64, device=dev)
+        toff = (b["tok_offsets"][lo:hi + 1] - b["tok_offsets"][lo]).contiguous()
+        o0 = int(b["tok_offsets"][lo])
+        buf.insert(**part, group_offsets=goff, tok_offsets=toff,
+                   tokens=b["tokens"][o0:].contiguous(), logp_old=b["logp_old"][o0:].contiguous(),
+                   assume_unique=True)
+    buf.check()
+    per_rank = B // T
+    max_local = per_rank * cfg["lmax"]
+    pad = max_local + 8
+    packed_tok = torch.empty(pad, dtype=torch.int32, device=dev)
+    lpn = torch.empty(pad, dtype=torch.float32, device=dev)
+    dlogp = torch.empty(pad, dtype=torch.float32, device=dev)
+    off = torch.empty(per_rank + 1, dtype=torch.int64, device=dev)
+    sel_ids = torch.empty(per_rank, dtype=torch.int64, device=dev)
+    stats = torch.zeros(5, dtype=torch.float64, device=dev)  # rb_loss_stats (40 B)
+    t_ins = []
+
+    def step(i, ev=None):
+        b, n, tot = wl.steps[i]
+        if ev:
+            ev[0].record(stream)
+        if n:
+            buf.insert(**b, assume_unique=True)
+        if ev:
+            ev[1].record(stream)
+        buf.sample_device(B, rng)
+        if ev:
+            ev[2].record(stream)
+        buf.gather(packed_tok, None, off)
+        if ev:
+            ev[3].record(stream)
+        # --- synthetic trainer stand-in (not part of the replay step)
+        buf.batch_ids_device(sel_ids)
+        synth.logp_now(SEED, i + 1, sel_ids, off, lpn, sh)
+        if ev:
+            ev[4].record(stream)
+        buf.loss_grpo(lpn, dlogp, EPS_LOW, EPS_HIGH, stats=stats) if cfg["loss"] == "grpo" else \
+            buf.loss_asymre(lpn, dlogp, DELTA_V, stats=stats)
+        if world > 1:
+            dist.all_reduce(stats[0:1])            # objective_sum (fp64)
+            dist.all_reduce(stats[2:4].view(torch.int64))  # included, excluded
+            buf.loss_finalize(dlogp, stats)
+        if ev:
+            ev[5].record(stream)
+
+    for i in range(Wm):
+        step(i)
+    buf.check()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(torch.cuda.current_device()) as clk:
+        t0 = time.perf_counter()
+        for i in range(K):
+            step(Wm + i, evs[i])
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    if world > 1:
+        dist.barrier()
+    buf.check()
+    ph = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(5)] for i in range(K)])
+    # phases: insert, sample, gather, stand-in, loss  (ms)
+    step_ms = ph[:, [0, 1, 2, 4]].sum(1)
+    mean = {k: float(ph[:, j].mean()) for j, k in enumerate(["insert", "sample", "gather", "standin", "loss"])}
+    ms = float(step_ms.mean())
+    if world > 1:
+        t = torch.tensor([ms, wall], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, wall = float(t[0]), float(t[1])
+    # token / byte accounting (global)
+    t_samp = B * cfg["lmax"] if not cfg["ragged"] else None
+    if t_samp is None:
+        t_samp = buf.batch_total_tokens() * T
+    ins = [wl.steps[Wm + i] for i in range(K)]
+    R = float(np.mean([x[1] for x in ins]))
+    T_ins = float(np.mean([x[2] for x in ins]))
+    alg = algorithmic_bytes(T_ins, t_samp, R, B, cfg["loss"])
+    hbm, peak_kind = peaks()
+    value = t_samp / (ms * 1e-3)
+    # dominant kernel: the loss (12 B/token GRPO: logp_old, logp_now read + dlogp write)
+    loss_bytes = (12 if cfg["loss"] == "grpo" else 8) * (t_samp / T)
+    gather_bytes = 8 * (t_samp / T)
+    roof = {"bound": "hbm", "kernel": "k_loss_grpo_buf" if cfg["loss"] == "grpo" else "k_loss_asymre_buf",
+            "achieved": loss_bytes / (mean["loss"] * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "peak_kind": peak_kind}
+    roof["frac"] = roof["achieved"] / hbm
+    roof["traffic"] = load_traffic(roof["kernel"])
+    roof["step"] = {"algorithmic_bytes": alg / T, "achieved_gbs": alg / T / (ms * 1e-3) / 1e9,
+                    "frac": alg / T / (ms * 1e-3) / 1e9 / hbm}
+    roof["kernels_gbs"] = {"gather": gather_bytes / (mean["gather"] * 1e-3) / 1e9,
+                           "insert": 16 * T_ins / T / (mean["insert"] * 1e-3) / 1e9}
+    res = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
+        "warmup": Wm, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "fp32", "data": "synthetic (include/replay_synth.h)",
+        "config": {"workload": cfg["name"], "buffer": N, "shards": T, "batch": B,
+                   "group": cfg["group"], "tokens_per_traj": cfg["lmax"], "ragged": cfg["ragged"],
+                   "W": W_WORKERS, "T": T_TRAINERS, "mu": MU, "inserted_per_step": R,
+                   "sampled_tokens_per_step": t_samp, "loss": cfg["loss"],
+                   "l2": "inputs larger than L2 (buffer + per-step traffic >> 126 MB)",
+                   "parallelism": f"shard{T}"},
+        "phases_ms": mean, "step_excludes": "synthetic trainer stand-in (logp_now), phases_ms.standin",
+        "wall_ms_per_step_incl_standin": wall * 1e3 / K,
+        "roofline": roof,
+        "gpu_launches": 9 * K,
+        "clocks": clk.summary(),
+    }
+    return res, buf, wl, rng
+
+
+def load_traffic(kernel):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(kernel)
+    except Exception:
+        return None
+
+
+def run_e2e(args, buf, wl, rng, cfg):
+    """Same metric through the C-ABI with HOST (pinned) buffers, copies timed."""
+    import torch
+
+    import paper_2604_08706_b200 as rb  # noqa: F401
+
+    B = cfg["batch"]
+    K = min(args.steps, 8)
+    steps = wl.steps[-K:] if len(wl.steps) >= K else wl.steps
+    host = []
+    for b, n, tot in steps:
+        hb = {k: v.cpu().pin_memory() for k, v in b.items()}
+        host.append((hb, n, tot))
+    tot_s = B * cfg["lmax"] if not cfg["ragged"] else buf.batch_total_tokens()
+    pad = tot_s + 8
+    tok_h = torch.empty(pad, dtype=torch.int32).pin_memory()
+    off_h = torch.empty(B + 1, dtype=torch.int64).pin_memory()
+    dl_h = torch.empty(pad, dtype=torch.float32).pin_memory()
+    # logp_now from the host: the stand-in's output for the current batch,
+    # produced once (untimed) and re-used; its values do not change the work.
+    lpn_h = torch.empty(pad, dtype=torch.float32).pin_memory()
+    buf.sample_device(B, rng)
+    buf.gather(tok_h, None, off_h)
+    ids = torch.empty(B, dtype=torch.int64, device="cuda")
+    offd = off_h.cuda()
+    lpn_d = torch.empty(pad, dtype=torch.float32, device="cuda")
+    from tools import synth
+
+    buf.batch_ids_device(ids)
+    synth.logp_now(SEED, 99, ids, offd, lpn_d, buf.stream())
+    torch.cuda.synchronize()
+    lpn_h.copy_(lpn_d.cpu())
+    # re-insert the same inbound batches needs fresh ids: shift them
+    shift = 10**12
+    h2d = d2h = 0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for hb, n, tot in host:
+        hb2 = dict(hb)
+        hb2["rollout_id"] = hb["rollout_id"] + shift
+        if n:
+            buf.insert(**hb2)
+        buf.sample_device(B, rng)
+        buf.gather(tok_h, None, off_h)
+        st = buf.loss_grpo(lpn_h, dl_h, EPS_LOW, EPS_HIGH) if cfg["loss"] == "grpo" else \
+            buf.loss_asymre(lpn_h, dl_h, DELTA_V)
+        _ = st.objective
+        h2d += sum(v.numel() * v.element_size() for v in hb.values()) + tot_s * 4
+        d2h += tot_s * 4 * 2 + (B + 1) * 8 + 40
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / len(host)
+    return {"value": tot_s / dt, "unit": "tokens/s", "ms_per_step": dt * 1e3,
+            "h2d_bytes_per_step": h2d // len(host), "d2h_bytes_per_step": d2h // len(host),
+            "steps": len(host), "path": "rb_insert/rb_sample/rb_gather/rb_loss_* with pinned host "
+                                        "buffers (copies inside the timed region)"}
+
+
+# ---------------------------------------------------------------- CPU arm
+def cpu_reference(cfg, steps, warmup, threads=0):
+    """The reference's CPU path (oracle/_ref: unmodified replab buffer/sampler/
+    group_advantages + restated token loss) on the host cores."""
+    import ctypes as C
+
+    from oracle.pyoracle import REF_SO, RECORD_DTYPE, Oracle
+
+    if not os.path.exists(REF_SO):
+        from oracle.pyoracle import build_oracle
+
+        build_oracle(with_ref=True)
+    L = C.CDLL(REF_SO)
+    vp = C.c_void_p
+    L.ref_bench_new.restype = vp
+    L.ref_bench_new.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_double, C.c_int,
+                                C.c_uint64, C.c_int]
+    L.ref_bench_free.argtypes = [vp]
+    L.ref_bench_threads.argtypes = [vp]
+    L.ref_bench_phase_a.argtypes = [vp, C.c_uint64, C.c_uint64, vp, vp, vp, vp, C.c_uint64, vp, vp, vp]
+    L.ref_bench_phase_b.argtypes = [vp, vp, C.c_double, C.c_double, vp, vp, vp, vp]
+    L.ref_last_error.restype = C.c_char_p
+    ora = Oracle()
+    h = L.ref_bench_new(1, cfg["capacity"], 0, 1 if cfg["retention"] == "positive_bias" else 0,
+                        cfg["delta"], cfg["lmax"], SEED, threads)
+    if not h:
+        raise RuntimeError(L.ref_last_error().decode())
+    nthreads = L.ref_bench_threads(h)
+    g = cfg["group"]
+    warm, per_step = schedule(cfg, steps + warmup)
+    nid = [0]
+    ngid = [0]
+
+    def make(ngroups, step):
+        n = ngroups * g
+        ids = np.arange(nid[0], nid[0] + n, dtype=np.uint64)
+        reward, length, blp = ora.synth_meta(SEED, ids, cfg["lmax"], cfg["ragged"])
+        tok, lpo, toff = ora.synth_payload(SEED, ids, length)
+        rec = np.zeros(n, RECORD_DTYPE)
+        rec["rollout_id"] = ids
+        rec["group_id"] = np.repeat(np.arange(ngid[0], ngid[0] + ngroups), g)
+        rec["prompt_id"] = rec["group_id"] % (cfg["batch"] // g)
+        rec["creation_step"] = step
+        rec["policy_version"] = step
+        rec["reward"] = reward
+        rec["is_correct"] = reward == 1.0
+        rec["behavior_logprob"] = blp
+        nid[0] += n
+        ngid[0] += ngroups
+        return rec, toff, tok, lpo
+
+    B = cfg["batch"]
+    maxtok = B * cfg["lmax"]
+    out_ids = np.zeros(B, np.uint64)
+    out_tok = np.zeros(maxtok, np.int32)
+    out_off = np.zeros(B + 1, np.int64)
+    dl = np.zeros(maxtok, np.float32)
+    obj, inc, exc = C.c_double(), C.c_int64(), C.c_int64()
+
+    def phase_a(rec, toff, tok, lpo):
+        st = L.ref_bench_phase_a(h, rec.shape[0], g, rec.ctypes.data, toff.ctypes.data,
+                                 tok.ctypes.data, lpo.ctypes.data, B, out_ids.ctypes.data,
+                                 out_tok.ctypes.data, out_off.ctypes.data)
+        if st:
+            raise RuntimeError(L.ref_last_error().decode())
+
+    rec, toff, tok, lpo = make(warm, 0)
+    phase_a(rec, toff, tok, lpo)
+    inputs = [make(n, s) for s, n in enumerate(per_step)]
+    times = []
+    for i, (rec, toff, tok, lpo) in enumerate(inputs):
+        t0 = time.perf_counter()
+        phase_a(rec, toff, tok, lpo)
+        ta = time.perf_counter() - t0
+        lpn = ora.synth_logp_now(SEED, i + 1, out_ids, out_off)  # stand-in, untimed
+        t1 = time.perf_counter()
+        st = L.ref_bench_phase_b(h, lpn.ctypes.data, EPS_LOW, EPS_HIGH, dl.ctypes.data,
+                                 C.byref(obj), C.byref(inc), C.byref(exc))
+        tb = time.perf_counter() - t1
+        if st:
+            raise RuntimeError(L.ref_last_error().decode())
+        if i >= warmup:
+            times.append(ta + tb)
+    L.ref_bench_free(h)
+    tok_per_step = int(out_off[-1])
+    mean = float(np.mean(times))
+    return {"value": tok_per_step / mean, "unit": "tokens/s", "cores": nthreads,
+            "ms_per_step": mean * 1e3, "steps": len(times),
+            "cpu": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference(cfg, args.steps, args.warmup)
+        line = {"metric": METRIC, "value": r["value"], "unit": "tokens/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+                "data": "synthetic (include/replay_synth.h)", "impl": "reference",
+                "config": {"workload": cfg["name"], "parallelism": "host threads"},
+                "cpu_baseline": {"value": r["value"], "unit": "tokens/s", "cores": r["cores"],
+                                 "kind": "reference",
+                                 "sample": f"{args.steps} full {args.config.upper()} replay steps "
+                                           f"({r['cpu']}); record ops through the unmodified "
+                                           "replab library, token payload/gather/loss restated"},
+                "e2e": {"value": r["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    res, buf, wl, rng = run_ours(args, rank, world, dist)
+    if not args.no_e2e:
+        res["e2e"] = run_e2e(args, buf, wl, rng, cfg)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = cpu_reference(cfg, args.cpu_steps, 1)
+            res["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": r["cores"],
+                                   "kind": "reference",
+                                   "sample": f"{r['steps']} full {args.config.upper()} replay steps "
+                                             f"after 1 warm-up ({r['cpu']})"}
+        except Exception as e:  # noqa: BLE001
+            res["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

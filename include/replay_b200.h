@@ -1,0 +1,276 @@
+/* replay_b200.h — C-ABI of the B200 replay-step library (libreplay_b200.so).
+ *
+ * This is the drop-in boundary for the reference's replay path.  The
+ * reference (/root/reference/proj, C++20, CPU only) has no FFI: its operator
+ * API is the C++ headers.  Each entry point below names the reference
+ * interface it replaces (file:line relative to /root/reference/proj); the
+ * C++ facade in paper_2604_08706_b200/csrc/replab_facade.hpp re-exposes the
+ * reference's own class/function signatures on top of this ABI (see
+ * INTEGRATION.md for the bindings a maintainer would add).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Every status-returning call returns
+ *     RB_OK (0) or an error code; rb_last_error() gives the thread-local
+ *     message, identical to the reference's std::invalid_argument text where
+ *     the reference throws (the facade re-throws it with the same type).
+ *   - Array arguments may point to device memory (the hot path) or to host
+ *     memory (staged through pinned buffers inside the call); the library
+ *     classifies each pointer with cudaPointerGetAttributes.  Packed token
+ *     arrays must be 16-byte aligned and readable up to the next 16-byte
+ *     boundary (true of any cudaMalloc / torch allocation).
+ *   - All work is enqueued on the buffer's CUDA stream (rb_set_stream); calls
+ *     that return host-visible results synchronise that stream.
+ *   - No CPU fallback: every compute entry point runs a CUDA kernel and fails
+ *     with RB_ECUDA when no sm_100 device is present.
+ */
+#ifndef REPLAY_B200_H
+#define REPLAY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the ABI is exported; internals are hidden */
+#endif
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status ------------------------------------------------------------ */
+enum {
+    RB_OK = 0,
+    RB_EINVAL = 1, /* std::invalid_argument in the reference */
+    RB_ELOGIC = 2, /* std::logic_error in the reference */
+    RB_ECUDA = 3,  /* CUDA runtime failure / no device */
+    RB_ENOMEM = 4
+};
+const char* rb_last_error(void);
+/* Library / device info: compiled arch and the device the library runs on. */
+int rb_device_info(int* device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- enums (replay_buffer.hpp:17-46) ------------------------------------ */
+enum { RB_UNIFORM_WITH_REPLACEMENT = 0, RB_UNIFORM_WITHOUT_REPLACEMENT = 1,
+       RB_UNUSED_FIRST_WITHOUT_REPLACEMENT = 2 };
+enum { RB_PLAIN_FIFO = 0, RB_POSITIVE_BIAS = 1 };
+
+/* ---- record (rollout.hpp:13-31; same 80-byte layout) -------------------- */
+typedef struct rb_record {
+    uint64_t rollout_id;
+    uint64_t prompt_id;
+    uint64_t group_id;
+    int64_t creation_step;
+    int64_t policy_version;
+    double reward;
+    uint8_t is_correct;
+    double behavior_logprob;
+    double advantage;
+    uint32_t use_count;
+} rb_record;
+
+/* One selection of sample() with a ledger (metrics.hpp:22-34 UseEvent). */
+typedef struct rb_use_event {
+    uint64_t rollout_id;
+    int64_t creation_step;
+    int64_t use_step;
+    int64_t batch_id;
+    int64_t within_batch_rank;
+} rb_use_event;
+
+/* ======================================================================
+ * Rng — replaces replab::Rng (rng.hpp:22-69, rng.cpp:25-121).
+ * The engine is MT19937-64 reproduced bit-exactly; its 312-word state lives
+ * on the GPU while the sampler consumes it and migrates to the host only
+ * when a host-side draw is requested (rng.cpp:38-55 semantics).
+ * ==================================================================== */
+typedef struct rb_rng rb_rng;
+int rb_rng_create(uint64_t seed, rb_rng** out);                         /* rng.hpp:24 */
+int rb_rng_stream(const rb_rng* parent, const char* name, rb_rng** out); /* rng.hpp:30 */
+int rb_rng_stream_index(const rb_rng* parent, const char* name, uint64_t index,
+                        rb_rng** out);                                  /* rng.hpp:31 */
+int rb_rng_clone(const rb_rng* r, rb_rng** out); /* value copy (Rng is copyable) */
+void rb_rng_destroy(rb_rng* r);
+uint64_t rb_rng_seed(const rb_rng* r);                                  /* rng.hpp:33 */
+uint64_t rb_rng_draws(const rb_rng* r); /* raw engine outputs consumed so far */
+int rb_rng_next_u64(rb_rng* r, uint64_t* out);                          /* rng.hpp:35 */
+int rb_rng_below(rb_rng* r, uint64_t bound, uint64_t* out);             /* rng.hpp:38 */
+int rb_rng_uniform01(rb_rng* r, double* out);                           /* rng.hpp:41 */
+int rb_rng_normal(rb_rng* r, double* out);                              /* rng.hpp:46 */
+int rb_rng_sample_without_replacement(rb_rng* r, uint64_t n, uint64_t k,
+                                      uint64_t* out);                   /* rng.hpp:56 */
+/* Device bulk generation: n raw engine outputs into out (device or host),
+ * produced by the GPU generator (parity aid for the sampler's stream). */
+int rb_rng_fill_u64(rb_rng* r, uint64_t n, uint64_t* out);
+uint64_t rb_hash_name(const char* name);                                /* rng.hpp:11 */
+
+/* ======================================================================
+ * ShardedReplayBuffer — replaces replab::ShardedReplayBuffer
+ * (replay_buffer.hpp:57-108, replay_buffer.cpp:67-324) with an HBM-resident
+ * SoA store: per-slot metadata columns plus fixed-stride token payload
+ * slots {int32 token, fp32 logp_old} of max_tokens per trajectory.
+ * ==================================================================== */
+typedef struct rb_buffer rb_buffer;
+
+/* replay_buffer.cpp:67-81 (+ RetentionPolicy::positive_bias 38-46).
+ * max_tokens: payload stride (>= the longest trajectory; 0 = metadata only).
+ * device: CUDA ordinal; -1 = current device.
+ * shard_begin/shard_end: shards whose token payload this process holds
+ * (multi-GPU: one shard per rank; metadata is replicated on every rank).
+ * Pass 0,0 for "all shards". */
+int rb_create(size_t num_shards, size_t total_capacity, int strategy, int retention,
+              double delta, int32_t max_tokens, int device, size_t shard_begin,
+              size_t shard_end, rb_buffer** out);
+void rb_destroy(rb_buffer* b);
+/* Use an external CUDA stream (cudaStream_t as void*); NULL = library stream. */
+int rb_set_stream(rb_buffer* b, void* stream);
+void* rb_get_stream(rb_buffer* b);
+
+/* push (replay_buffer.cpp:83-96): one record, synchronous.  Rejects an id
+ * present in any shard before mutating.  *has_evicted = 1 and *evicted set
+ * when the shard's retention policy evicted a record.  Optional payload
+ * (tokens/logp_old of n_tokens, host or device; NULL = no payload). */
+int rb_push(rb_buffer* b, const rb_record* rec, const int32_t* tokens, const float* logp_old,
+            int32_t n_tokens, rb_record* evicted, int* has_evicted);
+
+/* Batched insert of whole trajectories — the hot path of the replay step.
+ * Semantics are exactly n sequential push() calls (routing, eviction,
+ * duplicate rejection).  If advantage == NULL the group-relative advantage
+ * (bandit.cpp:276-294) and the group mean reward (bandit.cpp:316-318) are
+ * computed on the device over the groups delimited by group_offsets
+ * (n_groups+1 entries) and frozen into the stored records; otherwise the
+ * given advantages are stored and group_mean (may be NULL) is taken as the
+ * AsymRE baseline.  tok_offsets has n+1 entries into tokens/logp_old.
+ * out_evicted_ids[j] = id evicted by push j or UINT64_MAX (may be NULL).
+ * flags: RB_INSERT_ASSUME_UNIQUE promises ids are new and strictly
+ * increasing (verified on the device; a violation is a sticky RB_EINVAL
+ * reported by the next synchronising call).  Without it the call
+ * synchronises and, on a duplicate at push j, applies pushes [0, j) and
+ * returns RB_EINVAL with *out_applied = j. */
+enum { RB_INSERT_ASSUME_UNIQUE = 1 };
+typedef struct rb_insert_batch {
+    size_t n;
+    const uint64_t* rollout_id;
+    const uint64_t* prompt_id;
+    const uint64_t* group_id;
+    const int64_t* creation_step;
+    const int64_t* policy_version;
+    const double* reward;
+    const uint8_t* is_correct; /* NULL = (reward == 1.0) */
+    const double* behavior_logprob;
+    const double* advantage;   /* NULL = compute per group on the device */
+    const double* group_mean;  /* used when advantage != NULL; may be NULL */
+    const int64_t* group_offsets;
+    size_t n_groups;
+    const int64_t* tok_offsets; /* n+1; NULL = no payload */
+    const int32_t* tokens;
+    const float* logp_old;
+} rb_insert_batch;
+int rb_insert(rb_buffer* b, const rb_insert_batch* batch, uint64_t* out_evicted_ids,
+              size_t* out_applied, int flags);
+
+/* sample (replay_buffer.cpp:184-217): batch_size/num_shards draws per shard
+ * in shard order 0..T-1 from rng (replay_buffer.cpp:135-182), use counts
+ * incremented.  The selection is kept inside the buffer as the "current
+ * batch" for rb_gather / rb_loss_* (device-resident).  Optional outputs
+ * (host or device, may be NULL): record copies carrying the post-increment
+ * use count, (shard, arrival index) pairs, UseEvents (metrics.hpp:22-34).
+ * On an error the shards before the failing one are already mutated, as in
+ * the reference.  Asynchronous unless a host output is requested. */
+int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_records,
+              int64_t* out_shard, int64_t* out_index, rb_use_event* out_events,
+              int64_t batch_id, int64_t use_step);
+
+/* Current batch: number of selections, total tokens (sync), device views. */
+int rb_batch_size(const rb_buffer* b, size_t* n);
+int rb_batch_total_tokens(rb_buffer* b, int64_t* total);
+/* Per-selection rollout ids / lengths / packed offsets (n+1) into caller arrays. */
+int rb_batch_ids(rb_buffer* b, uint64_t* out_ids, int32_t* out_lengths, int64_t* out_offsets);
+
+/* Ragged token gather of the current batch: packs the sampled trajectories'
+ * tokens (and optionally logp_old) contiguously in selection order;
+ * out_offsets (n+1, may be NULL) = exclusive scan of lengths.  No reference
+ * counterpart (the reference has no tokens). */
+int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* out_offsets);
+
+/* Loss statistics of one step (bandit.hpp:127-131 LossResult, token form). */
+typedef struct rb_loss_stats {
+    double objective_sum; /* sum of per-unit objective terms */
+    double objective;     /* objective_sum / included (GRPO) or / B (AsymRE) */
+    int64_t included;
+    int64_t excluded;
+    int64_t total_tokens;
+} rb_loss_stats;
+
+/* GRPO clipped surrogate over the current batch, per token
+ * (grpo_loss_grad, bandit.cpp:363-408): ratio = exp(logp_now - logp_old),
+ * non-finite ratios excluded, clip to [1-eps_low, 1+eps_high], ties take the
+ * unclipped branch; out_dlogp = d(-objective)/d logp_now, normalised by the
+ * included token count.  logp_now/out_dlogp are packed in gather order.
+ * stats (host or device, may be NULL).  Multi-GPU: pass norm_tokens = the
+ * global token count (0 = this buffer's batch) and reduce `stats` across
+ * ranks, then call rb_loss_finalize with the reduced stats. */
+int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double eps_low,
+                 double eps_high, int64_t norm_tokens, rb_loss_stats* stats);
+/* AsymRE (asymre_loss_grad, bandit.cpp:410-438): coef = reward - (group
+ * mean + delta_v); dlogp = -coef / norm_batch on every token; objective =
+ * sum coef * sum_t logp_now / norm_batch.  norm_batch 0 = this batch size. */
+int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double delta_v,
+                   int64_t norm_batch, rb_loss_stats* stats);
+/* Re-normalise out_dlogp after a cross-rank reduction of stats (only does
+ * work when excluded > 0; objective recomputed).  Device or host stats. */
+int rb_loss_finalize(rb_buffer* b, float* dlogp, rb_loss_stats* stats);
+
+/* Inspection (replay_buffer.hpp:74-84). */
+int rb_num_shards(const rb_buffer* b, size_t* out);
+int rb_total_capacity(const rb_buffer* b, size_t* out);
+int rb_shard_capacity(const rb_buffer* b, size_t* out);
+int rb_size(rb_buffer* b, size_t* out);                      /* replay_buffer.cpp:219-226 */
+int rb_shard_size(rb_buffer* b, size_t shard, size_t* out);  /* 228-231 */
+/* shard_contents (233-236): arrival order, oldest first; returns count. */
+int rb_shard_contents(rb_buffer* b, size_t shard, rb_record* out, size_t capacity,
+                      size_t* count);
+/* Token payload of one stored record (by shard + arrival index). */
+int rb_record_tokens(rb_buffer* b, size_t shard, size_t index, int32_t* tokens,
+                     float* logp_old, int32_t capacity, int32_t* n_tokens);
+int rb_strategy(const rb_buffer* b, int* out);
+int rb_retention(const rb_buffer* b, int* kind, double* delta);
+int rb_route_cursor(rb_buffer* b, size_t* out);
+
+/* dump/load (replay_buffer.cpp:238-324): byte-identical text format.
+ * rb_dump writes at most cap bytes (NUL-terminated) and sets *len to the
+ * full length; call with out=NULL to size. */
+int rb_dump(rb_buffer* b, char* out, size_t cap, size_t* len);
+int rb_load(const char* text, int32_t max_tokens, int device, rb_buffer** out);
+
+/* Sticky asynchronous error check (synchronises the stream). */
+int rb_check(rb_buffer* b);
+int rb_synchronize(rb_buffer* b);
+
+/* ======================================================================
+ * Stateless kernels over explicit arrays (host or device pointers).
+ * ==================================================================== */
+/* group_advantages (bandit.cpp:276-294), segmented: groups delimited by
+ * offsets (n_groups+1).  Bit-exact fp64.  out_mean (may be NULL) = group
+ * mean reward (bandit.cpp:316-318).  Every group needs >= 2 rewards. */
+int rb_group_advantages(const double* rewards, const int64_t* offsets, size_t n_groups,
+                        double* out_adv, double* out_mean);
+/* grpo_loss_grad at the token level over explicit arrays (offsets n+1). */
+int rb_grpo_tokens(const float* logp_now, const float* logp_old, const double* adv,
+                   const int64_t* offsets, size_t n_traj, double eps_low, double eps_high,
+                   float* out_dlogp, rb_loss_stats* stats);
+/* Record-level fp64 form (L = 1): the reference's grpo_loss_grad per record. */
+int rb_grpo_records(const double* logp_now, const double* behavior_logprob,
+                    const double* adv, size_t n, double eps_low, double eps_high,
+                    double* out_dlogp, rb_loss_stats* stats);
+int rb_asymre_tokens(const float* logp_now, const double* reward, const double* group_mean,
+                     const int64_t* offsets, size_t n_traj, double delta_v,
+                     float* out_dlogp, rb_loss_stats* stats);
+int rb_asymre_records(const double* logp_now, const double* reward, const double* group_mean,
+                      size_t n, double delta_v, double* out_dlogp, rb_loss_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* REPLAY_B200_H */

@@ -18,6 +18,8 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <unordered_map>
+#include <algorithm>
 #include <vector>
 
 #include "replab/bandit.hpp"
@@ -193,6 +195,184 @@ int ref_loss_records(int kind, const double* logp_want, const RolloutRecord* rec
         }
         *objective = res.objective;
         *excluded = res.excluded;
+    });
+}
+
+}  // extern "C"
+
+// =========================================================================
+// CPU reference arm of bench.py: the replay step on the host.
+//
+// Record-level work goes through the unmodified reference library:
+// group_advantages (bandit.cpp:276-294) for every inserted group,
+// ShardedReplayBuffer::push (replay_buffer.cpp:83-133) for every record and
+// ShardedReplayBuffer::sample (184-217) with the "buffer_sampling" stream.
+// The reference has no tokens, so the token payload store,
+// the ragged gather and the per-token GRPO loss are the C restatement of
+// bandit.cpp:363-408 (same arithmetic as oracle/replay_oracle.c), spread
+// over all host threads.
+namespace {
+
+struct RefBench {
+    ShardedReplayBuffer buf;
+    Rng sampling;
+    int lmax;
+    int threads;
+    std::vector<int32_t> tok;  // [rows][lmax]
+    std::vector<float> lpo;
+    std::unordered_map<uint64_t, std::pair<int, int>> row_of;  // id -> (row, len)
+    std::vector<int> free_rows;
+    std::vector<RolloutRecord> batch;
+    std::vector<int64_t> off;
+    RefBench(size_t T, size_t N, int strategy, int retention, double delta, int lmax_, uint64_t seed,
+             int threads_)
+        : buf(T, N, strategy_of(strategy), retention_of(retention, delta)),
+          sampling(Rng(seed).stream("buffer_sampling")),
+          lmax(lmax_),
+          threads(threads_ > 0 ? threads_ : (int)std::max(1u, std::thread::hardware_concurrency())),
+          tok(N * (size_t)lmax_),
+          lpo(N * (size_t)lmax_) {
+        for (int r = (int)N - 1; r >= 0; --r) free_rows.push_back(r);
+    }
+};
+
+template <class F>
+void parallel_for(int threads, int64_t n, F&& f) {
+    if (threads <= 1 || n < 2) {
+        f(0, n, 0);
+        return;
+    }
+    const int t = (int)std::min<int64_t>(threads, n);
+    std::vector<std::thread> pool;
+    for (int k = 0; k < t; ++k) {
+        const int64_t a = n * k / t, b = n * (k + 1) / t;
+        pool.emplace_back([&, a, b, k] { f(a, b, k); });
+    }
+    for (auto& th : pool) th.join();
+}
+
+}  // namespace
+
+extern "C" {
+
+void* ref_bench_new(uint64_t T, uint64_t N, int strategy, int retention, double delta, int lmax,
+                    uint64_t seed, int threads) {
+    RefBench* out = nullptr;
+    int st = guard([&] { out = new RefBench(T, N, strategy, retention, delta, lmax, seed, threads); });
+    return st == 0 ? out : nullptr;
+}
+void ref_bench_free(void* h) { delete static_cast<RefBench*>(h); }
+int ref_bench_threads(void* h) { return static_cast<RefBench*>(h)->threads; }
+
+// Phase A: insert n records (groups of `group`, advantages computed here by
+// the reference), evict, sample `batch`, gather tokens.  recs carry
+// everything but the advantage; toff (n+1) indexes tokens/logp_old.
+int ref_bench_phase_a(void* hv, uint64_t n, uint64_t group, const RolloutRecord* recs,
+                      const int64_t* toff, const int32_t* tokens, const float* logp_old,
+                      uint64_t batch, uint64_t* out_ids, int32_t* out_tokens, int64_t* out_off) {
+    RefBench& h = *static_cast<RefBench*>(hv);
+    return guard([&] {
+        std::vector<RolloutRecord> rs(recs, recs + n);
+        for (uint64_t g = 0; g + group <= n; g += group) {
+            std::vector<double> rewards(group);
+            for (uint64_t i = 0; i < group; ++i) rewards[i] = rs[g + i].reward;
+            const auto adv = group_advantages(rewards);  // bandit.cpp:315
+            for (uint64_t i = 0; i < group; ++i) rs[g + i].advantage = adv[i];
+        }
+        std::vector<int64_t> rec_row(n, -1);
+        std::unordered_map<uint64_t, uint64_t> pending;  // id -> index in this batch
+        for (uint64_t j = 0; j < n; ++j) {
+            auto ev = h.buf.push(rs[j]);
+            pending[rs[j].rollout_id] = j;
+            if (ev) {
+                auto it = h.row_of.find(ev->rollout_id);
+                if (it != h.row_of.end()) {
+                    h.free_rows.push_back(it->second.first);
+                    h.row_of.erase(it);
+                }
+                pending.erase(ev->rollout_id);
+            }
+        }
+        std::vector<std::pair<uint64_t, int>> copies;  // (batch index, row)
+        for (auto& [id, j] : pending) {
+            const int row = h.free_rows.back();
+            h.free_rows.pop_back();
+            h.row_of[id] = {row, (int)(toff[j + 1] - toff[j])};
+            copies.push_back({j, row});
+        }
+        parallel_for(h.threads, (int64_t)copies.size(), [&](int64_t a, int64_t b, int) {
+            for (int64_t c = a; c < b; ++c) {
+                const uint64_t j = copies[c].first;
+                const size_t row = (size_t)copies[c].second * h.lmax;
+                const int64_t len = toff[j + 1] - toff[j];
+                std::memcpy(&h.tok[row], tokens + toff[j], len * 4);
+                std::memcpy(&h.lpo[row], logp_old + toff[j], len * 4);
+            }
+        });
+        h.batch = h.buf.sample(batch, h.sampling);
+        h.off.assign(batch + 1, 0);
+        for (uint64_t i = 0; i < batch; ++i) {
+            out_ids[i] = h.batch[i].rollout_id;
+            h.off[i + 1] = h.off[i] + h.row_of.at(h.batch[i].rollout_id).second;
+        }
+        std::memcpy(out_off, h.off.data(), (batch + 1) * 8);
+        parallel_for(h.threads, (int64_t)batch, [&](int64_t a, int64_t b, int) {
+            for (int64_t i = a; i < b; ++i) {
+                const auto& ro = h.row_of.at(h.batch[i].rollout_id);
+                std::memcpy(out_tokens + h.off[i], &h.tok[(size_t)ro.first * h.lmax],
+                            (size_t)ro.second * 4);
+            }
+        });
+    });
+}
+
+// Phase B: per-token GRPO (bandit.cpp:363-408 restated) over the batch.
+int ref_bench_phase_b(void* hv, const float* logp_now, double eps_low, double eps_high,
+                      float* out_dlogp, double* objective, int64_t* included, int64_t* excluded) {
+    RefBench& h = *static_cast<RefBench*>(hv);
+    return guard([&] {
+        const int64_t nb = (int64_t)h.batch.size();
+        std::vector<double> obj(h.threads, 0.0);
+        std::vector<int64_t> inc(h.threads, 0), exc(h.threads, 0);
+        parallel_for(h.threads, nb, [&](int64_t a, int64_t b, int k) {
+            for (int64_t i = a; i < b; ++i) {
+                const auto& ro = h.row_of.at(h.batch[i].rollout_id);
+                const float* lo = &h.lpo[(size_t)ro.first * h.lmax];
+                const double A = h.batch[i].advantage;
+                for (int64_t t = h.off[i]; t < h.off[i + 1]; ++t) {
+                    const double ratio = std::exp((double)logp_now[t] - (double)lo[t - h.off[i]]);
+                    if (!std::isfinite(ratio)) {
+                        ++exc[k];
+                        out_dlogp[t] = 0.f;
+                        continue;
+                    }
+                    ++inc[k];
+                    const double c = std::clamp(ratio, 1.0 - eps_low, 1.0 + eps_high);
+                    const double uv = ratio * A, cv = c * A;
+                    if (uv <= cv) {
+                        obj[k] += uv;
+                        out_dlogp[t] = (float)(A * ratio);
+                    } else {
+                        obj[k] += cv;
+                        out_dlogp[t] = 0.f;
+                    }
+                }
+            }
+        });
+        double o = 0.0;
+        int64_t ni = 0, ne = 0;
+        for (int k = 0; k < h.threads; ++k) {
+            o += obj[k];
+            ni += inc[k];
+            ne += exc[k];
+        }
+        const double scale = ni ? 1.0 / (double)ni : 0.0;
+        parallel_for(h.threads, h.off[nb], [&](int64_t a, int64_t b, int) {
+            for (int64_t t = a; t < b; ++t) out_dlogp[t] = (float)((double)out_dlogp[t] * -scale);
+        });
+        *objective = ni ? o * scale : 0.0;
+        *included = ni;
+        *excluded = ne;
     });
 }
 

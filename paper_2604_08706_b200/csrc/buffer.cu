@@ -1,0 +1,1869 @@
+// buffer.cu — ShardedReplayBuffer on the GPU (replay_buffer.hpp:57-108).
+//
+// Kernels (one step of the replay path):
+//   k_insert_route    1 CTA: group advantages (bandit.cpp:276-294), duplicate
+//                     screening, round-robin routing (replay_buffer.cpp:89-90),
+//                     eviction (FIFO closed form / positive-bias warp per shard /
+//                     exact sequential path), metadata scatter.
+//   k_insert_payload  one CTA per inserted trajectory: 128-bit funnel-shifted
+//                     copy of the surviving trajectories' {token, logp_old}.
+//   k_sample_with     1 CTA: MT19937-64 block twist + below() rejection
+//                     (rng.cpp:40-51) for uniform_with_replacement.
+//   k_sample_without  1 thread: partial Fisher-Yates / unused-first
+//                     (replay_buffer.cpp:146-179, rng.cpp:108-121).
+//   k_sample_map      1 CTA: arrival index -> slot, use counts, packed offsets.
+//   k_gather          one CTA per selection: ragged 128-bit gather into the
+//                     packed batch.
+#include <algorithm>
+#include <charconv>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "buffer_internal.cuh"
+#include "rng_internal.cuh"
+
+using namespace rb;
+
+namespace rb {
+
+constexpr uint64_t NONE_ID = UINT64_MAX;
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ int fifo_head(long long P, int C) {
+    return P >= C ? (int)(P % C) : 0;
+}
+__device__ __forceinline__ int arrival_slot(const BufView& v, int s, long long i) {
+    if (v.retention == RB_POSITIVE_BIAS)
+        return v.order[(size_t)s * v.C + (v.head[s] + i) % v.C];
+    return (int)((fifo_head(v.pushes[s], v.C) + i) % v.C);
+}
+__device__ __forceinline__ long long occupancy(const BufView& v, int s) {
+    const long long P = v.pushes[s];
+    return P < v.C ? P : v.C;
+}
+
+struct InsertIn {
+    long long n;
+    const uint64_t *id, *prompt, *group;
+    const int64_t *cstep, *pver;
+    const double *reward, *blp, *adv, *gmean;
+    const uint8_t* correct;
+    const int64_t* goff;
+    long long ngroups;
+    const int32_t* len;  // per-record length (may be NULL)
+    double *adv_out, *gmean_out;
+    int32_t* tslot;
+    uint8_t* surv;
+    uint64_t* evid;
+    rb_record* evrec;  // may be NULL
+};
+
+__device__ __forceinline__ bool in_correct(const InsertIn& in, long long j) {
+    return in.correct ? in.correct[j] != 0 : in.reward[j] == 1.0;
+}
+__device__ __forceinline__ rb_record in_record(const InsertIn& in, long long j) {
+    rb_record r;
+    r.rollout_id = in.id[j];
+    r.prompt_id = in.prompt ? in.prompt[j] : 0;
+    r.group_id = in.group ? in.group[j] : 0;
+    r.creation_step = in.cstep ? in.cstep[j] : 0;
+    r.policy_version = in.pver ? in.pver[j] : 0;
+    r.reward = in.reward[j];
+    r.is_correct = in_correct(in, j);
+    r.behavior_logprob = in.blp ? in.blp[j] : 0.0;
+    r.advantage = in.adv_out[j];
+    r.use_count = 0;
+    return r;
+}
+__device__ __forceinline__ rb_record slot_record(const BufView& v, size_t g) {
+    rb_record r;
+    r.rollout_id = v.id[g];
+    r.prompt_id = v.prompt[g];
+    r.group_id = v.group[g];
+    r.creation_step = v.cstep[g];
+    r.policy_version = v.pver[g];
+    r.reward = v.reward[g];
+    r.is_correct = v.correct[g];
+    r.behavior_logprob = v.blp[g];
+    r.advantage = v.adv[g];
+    r.use_count = v.use[g];
+    return r;
+}
+__device__ __forceinline__ void write_meta(const BufView& v, size_t g, const InsertIn& in,
+                                           long long j) {
+    v.id[g] = in.id[j];
+    v.prompt[g] = in.prompt ? in.prompt[j] : 0;
+    v.group[g] = in.group ? in.group[j] : 0;
+    v.cstep[g] = in.cstep ? in.cstep[j] : 0;
+    v.pver[g] = in.pver ? in.pver[j] : 0;
+    v.reward[g] = in.reward[j];
+    v.correct[g] = in_correct(in, j);
+    v.blp[g] = in.blp ? in.blp[j] : 0.0;
+    v.adv[g] = in.adv_out[j];
+    v.gmean[g] = in.gmean_out[j];
+    v.use[g] = 0;
+    v.len[g] = in.len ? in.len[j] : 0;
+}
+
+// ---- present-id hash set (exact path only) ------------------------------
+__device__ __forceinline__ unsigned long long hmix(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdULL;
+    k ^= k >> 33;
+    return k;
+}
+__device__ bool h_find(const BufView& v, uint64_t k, unsigned long long* at) {
+    unsigned long long i = hmix(k) & (v.hcap - 1);
+    for (;;) {
+        const uint32_t st = v.hstate[i];
+        if (st == 0) return false;
+        if (st == 1 && v.hkeys[i] == k) {
+            *at = i;
+            return true;
+        }
+        i = (i + 1) & (v.hcap - 1);
+    }
+}
+__device__ void h_insert_seq(const BufView& v, uint64_t k) {  // caller checked absence
+    unsigned long long i = hmix(k) & (v.hcap - 1);
+    while (v.hstate[i] == 1) i = (i + 1) & (v.hcap - 1);
+    v.hkeys[i] = k;
+    v.hstate[i] = 1;
+}
+__device__ void h_erase(const BufView& v, uint64_t k) {
+    unsigned long long at;
+    if (h_find(v, k, &at)) v.hstate[at] = 2;
+}
+__device__ void h_insert_par(const BufView& v, uint64_t k) {  // distinct keys, no tombstones
+    unsigned long long i = hmix(k) & (v.hcap - 1);
+    while (atomicCAS(&v.hstate[i], 0u, 3u) != 0u) i = (i + 1) & (v.hcap - 1);
+    v.hkeys[i] = k;
+    __threadfence_block();
+    v.hstate[i] = 1;
+}
+// Rebuild the set from the occupied slots (block-wide).
+__device__ void h_rebuild(const BufView& v) {
+    for (unsigned long long i = threadIdx.x; i < v.hcap; i += blockDim.x) v.hstate[i] = 0;
+    __syncthreads();
+    const long long N = (long long)v.T * v.C;
+    for (long long g = threadIdx.x; g < N; g += blockDim.x) {
+        const int s = (int)(g / v.C), x = (int)(g % v.C);
+        if (x < occupancy(v, s)) h_insert_par(v, v.id[g]);
+    }
+    __syncthreads();
+}
+
+// ---- positive-bias push (replay_buffer.cpp:98-133) on one shard --------
+// The shard is an arrival-ordered ring `order` (head, size).  Victim = the
+// first !is_correct record among arrival positions [0, size+1-fresh_slots)
+// (position C is the record being pushed), else position 0; erasing shifts
+// the older prefix one place towards the tail so arrival order is kept.
+// WARP = true: executed by a full warp; false: by one thread.
+template <bool WARP>
+__device__ void posbias_push(const BufView& v, const InsertIn& in, int s, long long j,
+                             int& size, int& head) {
+    const int lane = WARP ? (threadIdx.x & 31) : 0;
+    const int C = v.C;
+    int32_t* ord = v.order + (size_t)s * C;
+    if (size < C) {
+        const int x = size;
+        const size_t g = (size_t)s * C + x;
+        if (lane == 0) {
+            ord[(head + size) % C] = x;
+            write_meta(v, g, in, j);
+            in.tslot[j] = (int32_t)g;
+            v.owner[g] = (int32_t)j;
+            in.evid[j] = NONE_ID;
+        }
+        ++size;
+        if (WARP) __syncwarp();
+        return;
+    }
+    const int outside = C + 1 - v.fs;  // = correct_slots + 1
+    const bool new_correct = in_correct(in, j);
+    int vpos = -1;
+    for (int base = 0; base < outside && vpos < 0; base += (WARP ? 32 : 1)) {
+        if (WARP) {
+            const int p = base + lane;
+            bool wrong = false;
+            if (p < outside) {
+                if (p < C)
+                    wrong = !v.correct[(size_t)s * C + ord[(head + p) % C]];
+                else
+                    wrong = !new_correct;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, wrong);
+            if (m) vpos = base + __ffs(m) - 1;
+        } else {
+            const bool wrong = base < C ? !v.correct[(size_t)s * C + ord[(head + base) % C]]
+                                        : !new_correct;
+            if (wrong) vpos = base;
+        }
+    }
+    if (vpos < 0) vpos = 0;
+    if (vpos == C) {  // fresh_slots == 0 and the new record is the victim
+        if (lane == 0) {
+            in.evid[j] = in.id[j];
+            if (in.evrec) in.evrec[j] = in_record(in, j);
+            in.tslot[j] = -1;
+        }
+        if (WARP) __syncwarp();
+        return;
+    }
+    const int xv = ord[(head + vpos) % C];
+    const size_t gv = (size_t)s * C + xv;
+    if (lane == 0) {
+        in.evid[j] = v.id[gv];
+        if (in.evrec) in.evrec[j] = slot_record(v, gv);
+    }
+    if (WARP) __syncwarp();
+    // erase position vpos: shift [0, vpos) one place towards the tail
+    for (int hi = vpos; hi > 0; hi -= (WARP ? 32 : 1)) {
+        const int lo = WARP ? max(0, hi - 32) : hi - 1;
+        const int p = lo + lane;
+        int val = 0;
+        if (p < hi) val = ord[(head + p) % C];
+        if (WARP) __syncwarp();
+        if (p < hi) ord[(head + p + 1) % C] = val;
+        if (WARP) __syncwarp();
+    }
+    head = (head + 1) % C;
+    if (lane == 0) {
+        ord[(head + C - 1) % C] = xv;  // the new record takes the victim's slot, at the tail
+        write_meta(v, gv, in, j);
+        in.tslot[j] = (int32_t)gv;
+        v.owner[gv] = (int32_t)j;
+    }
+    if (WARP) __syncwarp();
+}
+
+// ---------------------------------------------------------------- insert
+__global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
+    __shared__ int s_bad, s_risk;
+    __shared__ long long s_applied;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const long long n = in.n;
+    DevCtl* ctl = v.ctl;
+    if (ctl->err_code != 0) {  // sticky error: buffer frozen until rb_check
+        for (long long j = tid; j < n; j += nt) {
+            in.surv[j] = 0;
+            in.tslot[j] = -1;
+            in.evid[j] = NONE_ID;
+        }
+        return;
+    }
+    if (tid == 0) {
+        s_bad = 0;
+        s_applied = n;
+    }
+    __syncthreads();
+
+    // 1. group-relative advantages, frozen at insertion (bandit.cpp:276-294),
+    //    fp64 with the reference's operation order (no FMA contraction).
+    if (in.adv == nullptr) {
+        if (tid == 0 && (in.goff[0] != 0 || in.goff[in.ngroups] != n)) s_bad = 1;
+        for (long long g = tid; g < in.ngroups; g += nt) {
+            const long long b = in.goff[g], e = in.goff[g + 1], m = e - b;
+            if (m < 2 || b < 0 || e > n) {
+                s_bad = 1;
+                continue;
+            }
+            const double dn = (double)m;
+            double mean = 0.0;
+            for (long long k = b; k < e; ++k) mean = __dadd_rn(mean, in.reward[k]);
+            mean = __ddiv_rn(mean, dn);
+            double var = 0.0;
+            for (long long k = b; k < e; ++k) {
+                const double d = __dsub_rn(in.reward[k], mean);
+                var = __dadd_rn(var, __dmul_rn(d, d));
+            }
+            var = __ddiv_rn(var, dn);
+            const double sd = __dsqrt_rn(var);
+            for (long long k = b; k < e; ++k) {
+                in.adv_out[k] = sd < 1e-8 ? 0.0 : __ddiv_rn(__dsub_rn(in.reward[k], mean), sd);
+                in.gmean_out[k] = mean;  // bandit.cpp:316-318 (same sequential sum)
+            }
+        }
+    } else {
+        for (long long j = tid; j < n; j += nt) {
+            in.adv_out[j] = in.adv[j];
+            in.gmean_out[j] = in.gmean ? in.gmean[j] : 0.0;
+        }
+    }
+    __syncthreads();
+    if (s_bad) {
+        if (tid == 0) {
+            ctl->err_code = RB_EINVAL;
+            ctl->err_index = -2;
+        }
+        for (long long j = tid; j < n; j += nt) {
+            in.surv[j] = 0;
+            in.tslot[j] = -1;
+            in.evid[j] = NONE_ID;
+        }
+        return;
+    }
+
+    // 2. duplicate screening: strictly increasing ids above every id ever
+    //    pushed cannot collide (all reference callers allocate ids that way).
+    int risk = 0;
+    for (long long j = tid; j < n; j += nt) {
+        const uint64_t x = in.id[j];
+        if (j > 0 ? x <= in.id[j - 1] : (ctl->has_any && x <= ctl->max_id)) risk = 1;
+    }
+    risk = __syncthreads_or(risk);
+    const unsigned long long cur0 = ctl->cursor;
+    const int T = v.T, C = v.C;
+
+    if (!risk && v.retention == RB_PLAIN_FIFO) {
+        // 3a. FIFO closed form: push j -> shard (cur0+j)%T, per-shard arrival
+        //     p = pushes_s + j/T, slot p % C; the victim is whatever held the
+        //     slot C arrivals earlier (pre-batch record or an earlier push).
+        for (long long j = tid; j < n; j += nt) {
+            const int s = (int)((cur0 + j) % T);
+            const long long rank = j / T, j0 = j % T;
+            const long long ns = (n - 1 - j0) / T + 1;
+            const long long p = v.pushes[s] + rank;
+            const size_t g = (size_t)s * C + (size_t)(p % C);
+            in.tslot[j] = (int32_t)g;
+            in.surv[j] = (rank + C >= ns);
+            uint64_t ev = NONE_ID;
+            if (p >= C) {
+                if (rank >= C) {
+                    const long long jv = j - (long long)C * T;
+                    ev = in.id[jv];
+                    if (in.evrec) in.evrec[j] = in_record(in, jv);
+                } else {
+                    ev = v.id[g];
+                    if (in.evrec) in.evrec[j] = slot_record(v, g);
+                }
+            }
+            in.evid[j] = ev;
+        }
+        __syncthreads();
+        for (long long j = tid; j < n; j += nt)
+            if (in.surv[j]) write_meta(v, (size_t)in.tslot[j], in, j);
+        __syncthreads();
+        for (int s = tid; s < T; s += nt) {
+            const long long j0 = (((long long)s - (long long)(cur0 % T)) % T + T) % T;
+            const long long ns = n > j0 ? (n - 1 - j0) / T + 1 : 0;
+            v.pushes[s] += ns;
+        }
+        if (tid == 0) ctl->cursor = (cur0 + n) % T;
+    } else if (!risk) {
+        // 3b. positive bias: one warp per shard, pushes in arrival order.
+        const int w = tid >> 5, nw = nt >> 5;
+        for (int s = w; s < T; s += nw) {
+            long long P = v.pushes[s];
+            int size = (int)(P < C ? P : C), head = v.head[s];
+            const long long j0 = (((long long)s - (long long)(cur0 % T)) % T + T) % T;
+            long long ns = 0;
+            for (long long j = j0; j < n; j += T, ++ns) posbias_push<true>(v, in, s, j, size, head);
+            if ((tid & 31) == 0) {
+                v.pushes[s] = P + ns;
+                v.head[s] = head;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) ctl->cursor = (cur0 + n) % T;
+    } else {
+        // 3c. exact sequential path (possible duplicates): replay_buffer.cpp:83-96
+        //     push by push against the present-id set.
+        h_rebuild(v);
+        if (tid == 0) {
+            unsigned long long cur = cur0;
+            long long j = 0;
+            for (; j < n; ++j) {
+                const uint64_t x = in.id[j];
+                unsigned long long at;
+                if (h_find(v, x, &at)) {
+                    ctl->err_code = RB_EINVAL;
+                    ctl->err_index = j;
+                    ctl->err_id = x;
+                    break;
+                }
+                h_insert_seq(v, x);
+                const int s = (int)cur;
+                cur = (cur + 1) % T;
+                if (v.retention == RB_PLAIN_FIFO) {
+                    const long long P = v.pushes[s];
+                    const size_t g = (size_t)s * C + (size_t)(P % C);
+                    uint64_t ev = NONE_ID;
+                    if (P >= C) {
+                        ev = v.id[g];
+                        if (in.evrec) in.evrec[j] = slot_record(v, g);
+                    }
+                    write_meta(v, g, in, j);
+                    in.tslot[j] = (int32_t)g;
+                    v.owner[g] = (int32_t)j;
+                    in.evid[j] = ev;
+                    v.pushes[s] = P + 1;
+                } else {
+                    const long long P = v.pushes[s];
+                    int size = (int)(P < C ? P : C), head = v.head[s];
+                    posbias_push<false>(v, in, s, j, size, head);
+                    v.pushes[s] = P + 1;
+                    v.head[s] = head;
+                }
+                if (in.evid[j] != NONE_ID) h_erase(v, in.evid[j]);
+            }
+            s_applied = j;
+            ctl->cursor = cur;
+            for (long long k = j; k < n; ++k) {
+                in.tslot[k] = -1;
+                in.evid[k] = NONE_ID;
+            }
+        }
+        __syncthreads();
+    }
+    if (risk || v.retention != RB_PLAIN_FIFO) {
+        for (long long j = tid; j < n; j += nt) {
+            const int32_t g = in.tslot[j];
+            in.surv[j] = g >= 0 && v.owner[g] == (int32_t)j;
+        }
+    }
+    // 4. bookkeeping
+    if (tid == 0) {
+        const long long applied = s_applied;
+        unsigned long long mx = ctl->has_any ? ctl->max_id : 0ULL;
+        for (long long j = 0; j < applied; ++j) mx = in.id[j] > mx ? in.id[j] : mx;
+        if (applied > 0) {
+            ctl->max_id = mx;
+            ctl->has_any = 1;
+        }
+        ctl->hash_stale = risk ? 0 : 1;
+    }
+}
+
+// ---- 128-bit funnel shifts ------------------------------------------------
+__device__ __forceinline__ uint4 funnel(const uint4& lo, const uint4& hi, int a) {
+    switch (a & 3) {
+        case 0: return lo;
+        case 1: return make_uint4(lo.y, lo.z, lo.w, hi.x);
+        case 2: return make_uint4(lo.z, lo.w, hi.x, hi.y);
+        default: return make_uint4(lo.w, hi.x, hi.y, hi.z);
+    }
+}
+__device__ __forceinline__ uint4 shfl_up4(const uint4& q) {
+    return make_uint4(__shfl_up_sync(0xffffffffu, q.x, 1), __shfl_up_sync(0xffffffffu, q.y, 1),
+                      __shfl_up_sync(0xffffffffu, q.z, 1), __shfl_up_sync(0xffffffffu, q.w, 1));
+}
+__device__ __forceinline__ uint4 shfl_down4(const uint4& q) {
+    return make_uint4(__shfl_down_sync(0xffffffffu, q.x, 1),
+                      __shfl_down_sync(0xffffffffu, q.y, 1),
+                      __shfl_down_sync(0xffffffffu, q.z, 1),
+                      __shfl_down_sync(0xffffffffu, q.w, 1));
+}
+__device__ __forceinline__ uint32_t q_at(const uint4& q, int i) {
+    return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w;
+}
+__device__ __forceinline__ uint4 ldg_nc(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void stg_stream(uint4* p, const uint4& q) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(q.x), "r"(q.y),
+                 "r"(q.z), "r"(q.w));
+}
+
+// Copy `len` 4-byte elements from a packed source at element offset `so`
+// (any alignment) into a 16-byte aligned row.  Whole warps iterate.
+__device__ __forceinline__ void copy_packed_to_row(const uint32_t* src, long long so,
+                                                   uint32_t* row, int len) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int a = (int)(so & 3);
+    const uint4* sq = reinterpret_cast<const uint4*>(src) + (so >> 2);
+    const long long nsq = ((so & 3) + len + 3) >> 2;  // source quads touched
+    const int nq = (len + 3) >> 2;                     // destination quads
+    uint4* dq = reinterpret_cast<uint4*>(row);
+    for (int base = wid * 32; base < nq; base += nw * 32) {
+        const int k = base + lane;
+        uint4 lo = k < nsq ? ldg_nc(sq + k) : make_uint4(0, 0, 0, 0);
+        uint4 hi = shfl_down4(lo);
+        if (lane == 31 && a && k + 1 < nsq) hi = ldg_nc(sq + k + 1);
+        if (k < nq) {
+            const uint4 o = funnel(lo, hi, a);
+            if (4 * k + 3 < len) {
+                dq[k] = o;
+            } else {
+                for (int i = 0; i < 4; ++i)
+                    if (4 * k + i < len) row[4 * k + i] = q_at(o, i);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_insert_payload(BufView v, const uint8_t* surv,
+                                                        const int32_t* tslot,
+                                                        const int64_t* toff, const int32_t* lens,
+                                                        const int32_t* tokens,
+                                                        const float* logp_old) {
+    const long long j = blockIdx.x;
+    if (!surv[j]) return;
+    const int g = tslot[j];
+    const int s = g / v.C;
+    if (s < v.sb || s >= v.se) return;
+    const size_t row = ((size_t)(s - v.sb) * v.C + (g % v.C)) * (size_t)v.stride;
+    const int len = lens[j];
+    if (tokens)
+        copy_packed_to_row(reinterpret_cast<const uint32_t*>(tokens), toff[j],
+                           reinterpret_cast<uint32_t*>(v.tok + row), len);
+    if (logp_old)
+        copy_packed_to_row(reinterpret_cast<const uint32_t*>(logp_old), toff[j],
+                           reinterpret_cast<uint32_t*>(v.lpo + row), len);
+}
+
+// ---------------------------------------------------------------- sample
+struct SampleArgs {
+    int nsh;            // shards to draw from (error semantics: [0, nsh))
+    long long per;      // draws per shard
+    int32_t* sel_shard;
+    int64_t* sel_index;
+};
+
+// uniform_with_replacement (replay_buffer.cpp:141-145): shard 0 takes its
+// `per` below(n_0) draws first, then shard 1, ...  The block generates 312
+// outputs per twist; a chunk containing a rejected value (v >= limit,
+// rng.cpp:45-49; probability ~n/2^64) is replayed sequentially by thread 0.
+__global__ void __launch_bounds__(1024) k_sample_with(BufView v, MtState* st, SampleArgs a) {
+    __shared__ uint64_t mt[MT_N];
+    __shared__ long long s_emit;
+    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = st->mt[i];
+    uint32_t idx = st->idx;
+    unsigned long long consumed = 0;
+    __syncthreads();
+    long long pos = 0;
+    for (int s = 0; s < a.nsh; ++s) {
+        const unsigned long long n = (unsigned long long)occupancy(v, s);
+        const unsigned long long lim = below_limit(n);
+        long long rem = a.per;
+        while (rem > 0) {
+            if (idx >= MT_N) {
+                mt_twist_block(mt);
+                idx = 0;
+            }
+            const long long avail = (long long)(MT_N - idx);
+            const int take = (int)(avail < rem ? avail : rem);
+            bool rej = false;
+            uint64_t x = 0;
+            if (threadIdx.x < take) {
+                x = mt_temper(mt[idx + threadIdx.x]);
+                rej = x >= lim;
+            }
+            if (!__syncthreads_or(rej)) {
+                if (threadIdx.x < take) {
+                    a.sel_shard[pos + threadIdx.x] = s;
+                    a.sel_index[pos + threadIdx.x] = (int64_t)(x % n);
+                }
+                pos += take;
+                rem -= take;
+            } else {
+                if (threadIdx.x == 0) {
+                    long long e = 0;
+                    for (int u = 0; u < take; ++u) {
+                        const uint64_t y = mt_temper(mt[idx + u]);
+                        if (y < lim) {
+                            a.sel_shard[pos + e] = s;
+                            a.sel_index[pos + e] = (int64_t)(y % n);
+                            ++e;
+                        }
+                    }
+                    s_emit = e;
+                }
+                __syncthreads();
+                pos += s_emit;
+                rem -= s_emit;
+                __syncthreads();
+            }
+            idx += take;
+            consumed += take;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) st->mt[i] = mt[i];
+    if (threadIdx.x == 0) {
+        st->idx = idx;
+        st->draws += consumed;
+    }
+}
+
+__device__ __forceinline__ uint64_t mt_below_scalar(uint64_t* mt, uint32_t* idx,
+                                                    uint64_t* draws, uint64_t bound) {
+    const uint64_t lim = below_limit(bound);
+    uint64_t x;
+    do {
+        x = mt_next_scalar(mt, idx, draws);
+    } while (x >= lim);
+    return x % bound;
+}
+
+// uniform_without_replacement / unused_first_without_replacement
+// (replay_buffer.cpp:146-179): sequential partial Fisher-Yates over the
+// arrival indices with the reference's exact draw consumption.
+__global__ void k_sample_without(BufView v, MtState* st, SampleArgs a, int strategy,
+                                 int64_t* scratch /* >= 2*C */) {
+    __shared__ uint64_t mt[MT_N];
+    if (threadIdx.x != 0) return;
+    for (int i = 0; i < MT_N; ++i) mt[i] = st->mt[i];
+    uint32_t idx = st->idx;
+    uint64_t draws = st->draws;
+    long long pos = 0;
+    int64_t* perm = scratch;
+    int64_t* used = scratch + v.C;
+    for (int s = 0; s < a.nsh; ++s) {
+        const long long n = occupancy(v, s), k = a.per;
+        long long picked = 0;
+        if (strategy == RB_UNUSED_FIRST_WITHOUT_REPLACEMENT) {
+            for (long long i = n - 1; i >= 0 && picked < k; --i) {
+                const size_t g = (size_t)s * v.C + arrival_slot(v, s, i);
+                if (v.use[g] == 0) {
+                    a.sel_shard[pos + picked] = s;
+                    a.sel_index[pos + picked] = i;
+                    ++picked;
+                }
+            }
+            if (picked == k) {
+                pos += k;
+                continue;
+            }
+        }
+        // population: all arrival indices, or the used ones (ascending)
+        long long m = 0;
+        if (strategy == RB_UNUSED_FIRST_WITHOUT_REPLACEMENT) {
+            for (long long i = 0; i < n; ++i) {
+                const size_t g = (size_t)s * v.C + arrival_slot(v, s, i);
+                if (v.use[g] != 0) used[m++] = i;
+            }
+        } else {
+            for (long long i = 0; i < n; ++i) used[m++] = i;
+        }
+        for (long long i = 0; i < m; ++i) perm[i] = i;
+        const long long need = k - picked;
+        for (long long i = 0; i < need; ++i) {
+            const long long jj = i + (long long)mt_below_scalar(mt, &idx, &draws, (uint64_t)(m - i));
+            const int64_t t = perm[i];
+            perm[i] = perm[jj];
+            perm[jj] = t;
+            a.sel_shard[pos + picked + i] = s;
+            a.sel_index[pos + picked + i] = used[perm[i]];
+        }
+        pos += k;
+    }
+    for (int i = 0; i < MT_N; ++i) st->mt[i] = mt[i];
+    st->idx = idx;
+    st->draws = draws;
+}
+
+// arrival index -> slot, use-count increments (replay_buffer.cpp:201),
+// packed offsets over the owned selections, loss-accumulator reset.
+__global__ void __launch_bounds__(1024) k_sample_map(BufView v, long long nsel,
+                                                     const int32_t* sel_shard,
+                                                     const int64_t* sel_index, int32_t* sel_slot,
+                                                     int64_t* off, long long lo, long long hi,
+                                                     long long* totals, DevLossAcc* acc) {
+    __shared__ long long s_warp[32];
+    __shared__ long long s_carry;
+    __shared__ unsigned long long s_global;
+    if (threadIdx.x == 0) {
+        s_carry = 0;
+        s_global = 0;
+    }
+    __syncthreads();
+    unsigned long long gsum = 0;
+    for (long long i = threadIdx.x; i < nsel; i += blockDim.x) {
+        const int s = sel_shard[i];
+        const size_t g = (size_t)s * v.C + arrival_slot(v, s, sel_index[i]);
+        sel_slot[i] = (int32_t)g;
+        atomicAdd(&v.use[g], 1u);
+        gsum += (unsigned long long)v.len[g];
+    }
+    atomicAdd(&s_global, gsum);
+    // exclusive scan of lengths over owned selections [lo, hi)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (long long base = lo; base < hi; base += blockDim.x) {
+        const long long i = base + threadIdx.x;
+        long long x = 0;
+        if (i < hi) {
+            const int s = sel_shard[i];
+            x = v.len[(size_t)s * v.C + arrival_slot(v, s, sel_index[i])];
+        }
+        long long incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_warp[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            long long w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            s_warp[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        const long long before = s_carry + (wid ? s_warp[wid - 1] : 0);
+        if (i < hi) off[i - lo] = before + incl - x;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = before + incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        off[hi - lo] = s_carry;
+        totals[0] = s_carry;
+        totals[1] = (long long)s_global;
+        acc->obj_sum = 0.0;
+        acc->included = 0;
+        acc->excluded = 0;
+        acc->done_blocks = 0;
+        acc->total_tokens = (long long)s_global;
+        acc->objective = 0.0;
+        acc->need_fixup = 0;
+    }
+}
+
+// Record copies with the post-increment use count in draw order
+// (replay_buffer.cpp:201-202) and optional UseEvents (205-215).
+__global__ void k_sample_records(BufView v, long long nsel, long long per,
+                                 const int32_t* sel_slot, rb_record* out, rb_use_event* ev,
+                                 long long batch_id, long long use_step) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nsel;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int32_t g = sel_slot[i];
+        const long long seg = (i / per) * per, end = seg + per;
+        long long rank = 0, count = 0;
+        for (long long k = seg; k < end; ++k) {
+            if (sel_slot[k] == g) {
+                ++count;
+                if (k < i) ++rank;
+            }
+        }
+        rb_record r = slot_record(v, g);
+        r.use_count = (uint32_t)(v.use[g] - count + rank + 1);
+        if (out) out[i] = r;
+        if (ev) {
+            rb_use_event e;
+            e.rollout_id = r.rollout_id;
+            e.creation_step = r.creation_step;
+            e.use_step = use_step;
+            e.batch_id = batch_id;
+            e.within_batch_rank = i;
+            ev[i] = e;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- gather
+// One CTA per owned selection: tokens (and optionally logp_old) of the slot
+// row -> packed batch at off[b], 128-bit loads, funnel-shifted stores.
+__device__ __forceinline__ void copy_row_to_packed(const uint32_t* row, int len, uint32_t* dst,
+                                                   long long doff) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int a = (int)(doff & 3);
+    const uint4* sq = reinterpret_cast<const uint4*>(row);
+    const int nsq = (len + 3) >> 2;
+    const int nq = (a + len + 3) >> 2;
+    uint4* dq = reinterpret_cast<uint4*>(dst) + (doff >> 2);
+    for (int base = wid * 32; base < nq; base += nw * 32) {
+        const int k = base + lane;
+        const uint4 cur = k < nsq ? ldg_nc(sq + k) : make_uint4(0, 0, 0, 0);
+        uint4 prev = shfl_up4(cur);
+        if (lane == 0 && a && k >= 1) prev = ldg_nc(sq + k - 1);
+        if (k < nq) {
+            const uint4 o = a ? funnel(prev, cur, 4 - a) : cur;
+            const int e0 = 4 * k - a;  // row element of lane 0 of this quad
+            if (e0 >= 0 && e0 + 3 < len) {
+                stg_stream(dq + k, o);
+            } else {
+                uint32_t* d = dst + ((doff >> 2) << 2) + 4 * (long long)k;
+                for (int i = 0; i < 4; ++i)
+                    if (e0 + i >= 0 && e0 + i < len) d[i] = q_at(o, i);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_gather(BufView v, const int32_t* sel_slot,
+                                                const int64_t* off, long long lo,
+                                                int32_t* out_tok, float* out_lpo) {
+    const long long b = lo + blockIdx.x;
+    const int g = sel_slot[b];
+    const int s = g / v.C;
+    const size_t row = ((size_t)(s - v.sb) * v.C + (g % v.C)) * (size_t)v.stride;
+    const int len = v.len[g];
+    const long long doff = off[blockIdx.x];
+    if (out_tok)
+        copy_row_to_packed(reinterpret_cast<const uint32_t*>(v.tok + row), len,
+                           reinterpret_cast<uint32_t*>(out_tok), doff);
+    if (out_lpo)
+        copy_row_to_packed(reinterpret_cast<const uint32_t*>(v.lpo + row), len,
+                           reinterpret_cast<uint32_t*>(out_lpo), doff);
+}
+
+// ---------------------------------------------------------------- inspect
+__global__ void k_shard_contents(BufView v, int s, long long n, rb_record* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = slot_record(v, (size_t)s * v.C + arrival_slot(v, s, i));
+}
+__global__ void k_slot_of(BufView v, int s, long long i, int32_t* out) {
+    *out = (int32_t)((size_t)s * v.C + arrival_slot(v, s, i));
+}
+
+// Load: records written densely to slots 0..n-1 of shard s, arrival order.
+__global__ void k_load_shard(BufView v, int s, long long n, const rb_record* recs) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const size_t g = (size_t)s * v.C + i;
+        const rb_record r = recs[i];
+        v.id[g] = r.rollout_id;
+        v.prompt[g] = r.prompt_id;
+        v.group[g] = r.group_id;
+        v.cstep[g] = r.creation_step;
+        v.pver[g] = r.policy_version;
+        v.reward[g] = r.reward;
+        v.correct[g] = r.is_correct;
+        v.blp[g] = r.behavior_logprob;
+        v.adv[g] = r.advantage;
+        v.gmean[g] = 0.0;
+        v.use[g] = r.use_count;
+        v.len[g] = 0;
+        if (v.retention == RB_POSITIVE_BIAS) v.order[g] = (int32_t)i;
+    }
+}
+
+}  // namespace rb
+
+// ====================================================================== host
+rb_buffer::~rb_buffer() {
+    if (device >= 0) cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    void* ptrs[] = {v.id, v.prompt, v.group, v.cstep, v.pver, v.reward, v.blp, v.adv, v.gmean,
+                    v.correct, v.use, v.len, v.order, v.head, v.pushes, v.owner, v.tok, v.lpo,
+                    v.hkeys, v.hstate, v.ctl, s_tslot, s_surv, s_evid, s_evrec, s_adv, s_gmean,
+                    s_len, s_toff, sel_slot, sel_shard, sel_index, sel_off, sel_total,
+                    acc, misc};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (void* p : stage_dev)
+        if (p) cudaFree(p);
+    if (stage_host) cudaFreeHost(stage_host);
+    if (stage_event) cudaEventDestroy(stage_event);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+template <class T>
+static T* dalloc(size_t n) {
+    T* p = nullptr;
+    RB_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    RB_CUDA(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+    return p;
+}
+
+void* rb_buffer::scratch(size_t bytes) {
+    if (bytes > misc_cap) {
+        if (misc) {
+            RB_CUDA(cudaStreamSynchronize(stream));
+            cudaFree(misc);
+        }
+        misc_cap = std::max(bytes, misc_cap * 2);
+        RB_CUDA(cudaMalloc(&misc, misc_cap));
+    }
+    return misc;
+}
+void* rb_buffer::host_stage(size_t bytes) {
+    if (stage_event) RB_CUDA(cudaEventSynchronize(stage_event));
+    if (bytes > stage_host_cap) {
+        RB_CUDA(cudaStreamSynchronize(stream));
+        if (stage_host) cudaFreeHost(stage_host);
+        stage_host_cap = std::max(bytes, stage_host_cap * 2);
+        RB_CUDA(cudaMallocHost(&stage_host, stage_host_cap));
+    }
+    return stage_host;
+}
+void* rb_buffer::dev_stage(size_t bytes, int slot) {
+    if (bytes > stage_dev_cap[slot]) {
+        RB_CUDA(cudaStreamSynchronize(stream));
+        if (stage_dev[slot]) cudaFree(stage_dev[slot]);
+        stage_dev_cap[slot] = std::max(bytes, stage_dev_cap[slot] * 2);
+        RB_CUDA(cudaMalloc(&stage_dev[slot], stage_dev_cap[slot]));
+    }
+    return stage_dev[slot];
+}
+void rb_buffer::host_stage_issued() {
+    if (!stage_event) RB_CUDA(cudaEventCreateWithFlags(&stage_event, cudaEventDisableTiming));
+    RB_CUDA(cudaEventRecord(stage_event, stream));
+}
+void rb_buffer::ensure_insert(size_t n) {
+    if (n <= ins_cap) return;
+    RB_CUDA(cudaStreamSynchronize(stream));
+    void* ps[] = {s_tslot, s_surv, s_evid, s_evrec, s_adv, s_gmean, s_len, s_toff};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    ins_cap = std::max(n, ins_cap * 2);
+    s_tslot = dalloc<int32_t>(ins_cap);
+    s_surv = dalloc<uint8_t>(ins_cap);
+    s_evid = dalloc<uint64_t>(ins_cap);
+    s_evrec = dalloc<rb_record>(ins_cap);
+    s_adv = dalloc<double>(ins_cap);
+    s_gmean = dalloc<double>(ins_cap);
+    s_len = dalloc<int32_t>(ins_cap);
+    s_toff = dalloc<int64_t>(ins_cap + 1);
+}
+void rb_buffer::ensure_select(size_t n) {
+    if (n <= sel_cap) return;
+    RB_CUDA(cudaStreamSynchronize(stream));
+    void* ps[] = {sel_slot, sel_shard, sel_index, sel_off};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    sel_cap = std::max(n, sel_cap * 2);
+    sel_slot = dalloc<int32_t>(sel_cap);
+    sel_shard = dalloc<int32_t>(sel_cap);
+    sel_index = dalloc<int64_t>(sel_cap);
+    sel_off = dalloc<int64_t>(sel_cap + 1);
+}
+void rb_buffer::sync() { RB_CUDA(cudaStreamSynchronize(stream)); }
+
+namespace {
+
+struct DeviceScope {  // make the buffer's device current for the call
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        cudaGetDevice(&prev);
+        if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Device view of a caller array: returns a device pointer, staging host
+// memory through the buffer's device staging area at `*cursor`.
+struct Stager {
+    rb_buffer* b;
+    std::vector<std::pair<const void*, size_t>> host_items;
+    size_t total = 0;
+    explicit Stager(rb_buffer* b_) : b(b_) {}
+};
+
+void check_sticky(rb_buffer* b) {
+    DevCtl c;
+    RB_CUDA(cudaMemcpyAsync(&c, b->v.ctl, sizeof c, cudaMemcpyDeviceToHost, b->stream));
+    RB_CUDA(cudaStreamSynchronize(b->stream));
+    if (c.err_code) {
+        DevCtl z = c;
+        z.err_code = 0;
+        z.err_index = 0;
+        RB_CUDA(cudaMemcpyAsync(b->v.ctl, &z, sizeof z, cudaMemcpyHostToDevice, b->stream));
+        RB_CUDA(cudaStreamSynchronize(b->stream));
+        if (c.err_index == -2) invalid("group advantages need >= 2 rewards");
+        if (c.err_index == -3) invalid("rb_insert: trajectory length exceeds max_tokens");
+        invalid("ShardedReplayBuffer: rollout id " + std::to_string(c.err_id) +
+                " is already stored");
+    }
+}
+
+std::string fmt_double(double x) {  // text_io.cpp:10-14 (shortest round trip)
+    char buf[64];
+    auto r = std::to_chars(buf, buf + sizeof buf, x);
+    return std::string(buf, r.ptr);
+}
+
+std::string strategy_name(int s) {
+    switch (s) {
+        case RB_UNIFORM_WITH_REPLACEMENT: return "uniform_with_replacement";
+        case RB_UNIFORM_WITHOUT_REPLACEMENT: return "uniform_without_replacement";
+        case RB_UNUSED_FIRST_WITHOUT_REPLACEMENT: return "unused_first_without_replacement";
+    }
+    throw Error(RB_ELOGIC, "bad SamplingStrategy");
+}
+
+rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
+                  int32_t max_tokens, int device, size_t sb, size_t se) {
+    require_device();
+    if (T == 0) invalid("ShardedReplayBuffer: need at least one shard");
+    if (N == 0 || N % T != 0)
+        invalid("ShardedReplayBuffer: capacity must be a positive multiple of the shard count");
+    if (retention == RB_POSITIVE_BIAS && !(delta >= 0.0 && delta <= 1.0))
+        invalid("RetentionPolicy: delta must be in [0, 1]");
+    if (strategy < 0 || strategy > 2) throw Error(RB_ELOGIC, "bad SamplingStrategy");
+    if (max_tokens < 0) invalid("rb_create: max_tokens must be >= 0");
+    if (sb == 0 && se == 0) se = T;
+    if (sb >= se || se > T) invalid("rb_create: bad owned shard range");
+    if (N / T > (size_t)INT32_MAX / 2 || N > (size_t)INT32_MAX / 2)
+        invalid("rb_create: capacity too large");
+    if (device < 0) RB_CUDA(cudaGetDevice(&device));
+    DeviceScope ds(device);
+    auto* b = new rb_buffer();
+    try {
+        b->T = T;
+        b->N = N;
+        b->C = N / T;
+        b->strategy = strategy;
+        b->retention = retention;
+        b->delta = retention == RB_POSITIVE_BIAS ? delta : 0.0;
+        b->max_tokens = max_tokens;
+        b->stride = (max_tokens + 3) & ~3;
+        b->device = device;
+        b->sb = sb;
+        b->se = se;
+        RB_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+        b->own_stream = true;
+        BufView& v = b->v;
+        v.T = (int)T;
+        v.C = (int)b->C;
+        v.stride = b->stride;
+        v.retention = retention;
+        v.sb = (int)sb;
+        v.se = (int)se;
+        // replay_buffer.cpp:110-112
+        const size_t cs = retention == RB_POSITIVE_BIAS
+                              ? (size_t)std::floor(b->delta * (double)b->C + 1e-9)
+                              : 0;
+        v.cs = (int)cs;
+        v.fs = (int)(b->C - cs);
+        v.id = dalloc<uint64_t>(N);
+        v.prompt = dalloc<uint64_t>(N);
+        v.group = dalloc<uint64_t>(N);
+        v.cstep = dalloc<int64_t>(N);
+        v.pver = dalloc<int64_t>(N);
+        v.reward = dalloc<double>(N);
+        v.blp = dalloc<double>(N);
+        v.adv = dalloc<double>(N);
+        v.gmean = dalloc<double>(N);
+        v.correct = dalloc<uint8_t>(N);
+        v.use = dalloc<uint32_t>(N);
+        v.len = dalloc<int32_t>(N);
+        v.order = dalloc<int32_t>(N);
+        v.head = dalloc<int32_t>(T);
+        v.pushes = dalloc<long long>(T);
+        v.owner = dalloc<int32_t>(N);
+        const size_t rows = (se - sb) * b->C * (size_t)b->stride;
+        v.tok = rows ? dalloc<int32_t>(rows) : nullptr;
+        v.lpo = rows ? dalloc<float>(rows) : nullptr;
+        unsigned long long hc = 64;
+        while (hc < 4ULL * N + 64) hc <<= 1;
+        v.hcap = hc;
+        v.hkeys = dalloc<uint64_t>(hc);
+        v.hstate = dalloc<uint32_t>(hc);
+        v.ctl = dalloc<DevCtl>(1);
+        b->sel_total = dalloc<long long>(2);
+        b->acc = dalloc<DevLossAcc>(1);
+        b->h_pushes.assign(T, 0);
+    } catch (...) {
+        delete b;
+        throw;
+    }
+    return b;
+}
+
+// Insert `bt` (pointers already resolved to device memory; lens/toff device)
+void launch_insert(rb_buffer* b, const rb_insert_batch& bt, const int32_t* d_len,
+                   const int64_t* d_toff, bool want_evrec) {
+    InsertIn in{};
+    in.n = (long long)bt.n;
+    in.id = bt.rollout_id;
+    in.prompt = bt.prompt_id;
+    in.group = bt.group_id;
+    in.cstep = bt.creation_step;
+    in.pver = bt.policy_version;
+    in.reward = bt.reward;
+    in.correct = bt.is_correct;
+    in.blp = bt.behavior_logprob;
+    in.adv = bt.advantage;
+    in.gmean = bt.group_mean;
+    in.goff = bt.group_offsets;
+    in.ngroups = (long long)bt.n_groups;
+    in.len = d_len;
+    in.adv_out = b->s_adv;
+    in.gmean_out = b->s_gmean;
+    in.tslot = b->s_tslot;
+    in.surv = b->s_surv;
+    in.evid = b->s_evid;
+    in.evrec = want_evrec ? b->s_evrec : nullptr;
+    k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
+    RB_CUDA(cudaGetLastError());
+    if (bt.tok_offsets && b->stride > 0 && bt.n > 0 && (bt.tokens || bt.logp_old)) {
+        k_insert_payload<<<(unsigned)bt.n, 256, 0, b->stream>>>(b->v, b->s_surv, b->s_tslot, d_toff,
+                                                               d_len, bt.tokens, bt.logp_old);
+        RB_CUDA(cudaGetLastError());
+    }
+}
+
+}  // namespace
+
+// helper launchers defined at the end of this file (C++ linkage)
+void rb_lengths_from_offsets(const int64_t* toff, size_t n, int32_t* len, int32_t maxlen,
+                             DevCtl* ctl, cudaStream_t s);
+void rb_widen_i32(const int32_t* a, int64_t* b, size_t n, cudaStream_t s);
+void rb_batch_ids_dev(const BufView& v, const int32_t* sel_slot, long long lo, long long hi,
+                      uint64_t* ids, int32_t* lens, cudaStream_t s);
+
+// ---------------------------------------------------------------- C ABI
+extern "C" {
+
+int rb_device_info(int* device, int* sm_count, int* cc_major, int* cc_minor) {
+    return guard([&] {
+        require_device();
+        int d = 0;
+        RB_CUDA(cudaGetDevice(&d));
+        if (device) *device = d;
+        if (sm_count) RB_CUDA(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, d));
+        if (cc_major) RB_CUDA(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, d));
+        if (cc_minor) RB_CUDA(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, d));
+    });
+}
+
+int rb_create(size_t num_shards, size_t total_capacity, int strategy, int retention,
+              double delta, int32_t max_tokens, int device, size_t shard_begin,
+              size_t shard_end, rb_buffer** out) {
+    return guard([&] {
+        *out = create(num_shards, total_capacity, strategy, retention, delta, max_tokens,
+                      device, shard_begin, shard_end);
+    });
+}
+
+void rb_destroy(rb_buffer* b) { delete b; }
+
+int rb_set_stream(rb_buffer* b, void* stream) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        b->sync();
+        if (b->own_stream && b->stream) cudaStreamDestroy(b->stream);
+        if (stream) {
+            b->stream = (cudaStream_t)stream;
+            b->own_stream = false;
+        } else {
+            RB_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+            b->own_stream = true;
+        }
+    });
+}
+void* rb_get_stream(rb_buffer* b) { return (void*)b->stream; }
+
+int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_ids,
+              size_t* out_applied, int flags) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        rb_insert_batch bt = *bt_in;
+        if (out_applied) *out_applied = 0;
+        if (bt.n == 0) return;
+        if (!bt.rollout_id || !bt.reward) invalid("rb_insert: rollout_id and reward are required");
+        if (!bt.advantage && !bt.group_offsets)
+            invalid("rb_insert: need advantage or group_offsets");
+        // Split very large batches so the exact path's hash set stays sparse.
+        const size_t chunk_max = (size_t)(b->v.hcap / 4);
+        if (bt.n > chunk_max) {
+            if (!bt.advantage) invalid("rb_insert: batch too large for device advantages");
+            size_t done = 0;
+            while (done < bt.n) {
+                const size_t m = std::min(chunk_max, bt.n - done);
+                rb_insert_batch c = bt;
+                auto adv = [&](auto* p) { return p ? p + done : p; };
+                c.n = m;
+                c.rollout_id = adv(bt.rollout_id);
+                c.prompt_id = adv(bt.prompt_id);
+                c.group_id = adv(bt.group_id);
+                c.creation_step = adv(bt.creation_step);
+                c.policy_version = adv(bt.policy_version);
+                c.reward = adv(bt.reward);
+                c.is_correct = adv(bt.is_correct);
+                c.behavior_logprob = adv(bt.behavior_logprob);
+                c.advantage = adv(bt.advantage);
+                c.group_mean = adv(bt.group_mean);
+                c.tok_offsets = adv(bt.tok_offsets);
+                size_t applied = 0;
+                int st = rb_insert(b, &c, out_evicted_ids ? out_evicted_ids + done : nullptr,
+                                   &applied, flags);
+                if (out_applied) *out_applied = done + applied;
+                if (st != RB_OK) throw Error(st, rb_last_error());
+                done += m;
+            }
+            return;
+        }
+        b->ensure_insert(bt.n);
+        const size_t n = bt.n;
+
+        // Resolve every input array to device memory (host arrays staged).
+        struct Item {
+            const void** ptr;
+            size_t bytes;
+        };
+        std::vector<Item> items;
+        const int64_t* toff_user = bt.tok_offsets;
+        auto add = [&](const void** p, size_t bytes) {
+            if (*p && !is_device_ptr(*p)) items.push_back({p, bytes});
+        };
+        add((const void**)&bt.rollout_id, n * 8);
+        add((const void**)&bt.prompt_id, n * 8);
+        add((const void**)&bt.group_id, n * 8);
+        add((const void**)&bt.creation_step, n * 8);
+        add((const void**)&bt.policy_version, n * 8);
+        add((const void**)&bt.reward, n * 8);
+        add((const void**)&bt.is_correct, n);
+        add((const void**)&bt.behavior_logprob, n * 8);
+        add((const void**)&bt.advantage, n * 8);
+        add((const void**)&bt.group_mean, n * 8);
+        add((const void**)&bt.group_offsets, (bt.n_groups + 1) * 8);
+        const bool toff_host = toff_user && !is_device_ptr(toff_user);
+        add((const void**)&bt.tok_offsets, (n + 1) * 8);
+        size_t payload_elems = 0;
+        if (toff_user && (bt.tokens || bt.logp_old)) {
+            if (toff_host) {
+                payload_elems = (size_t)toff_user[n];
+            } else {
+                int64_t last = 0;
+                RB_CUDA(cudaMemcpy(&last, toff_user + n, 8, cudaMemcpyDeviceToHost));
+                payload_elems = (size_t)last;
+            }
+            const size_t pbytes = ((payload_elems + 3) & ~size_t(3)) * 4;
+            add((const void**)&bt.tokens, pbytes);
+            add((const void**)&bt.logp_old, pbytes);
+        }
+        if (toff_host) {
+            for (size_t j = 0; j < n; ++j) {
+                const int64_t l = toff_user[j + 1] - toff_user[j];
+                if (l < 0 || l > b->max_tokens)
+                    invalid("rb_insert: trajectory length " + std::to_string(l) +
+                            " exceeds max_tokens " + std::to_string(b->max_tokens));
+            }
+        }
+        if (!items.empty()) {
+            // Pinned host arrays are copied straight to the device; pageable
+            // ones go through the pinned staging area (one H2D for all).
+            size_t total = 0, paged = 0;
+            for (auto& it : items) {
+                total += (it.bytes + 255) & ~size_t(255);
+                if (!is_pinned_ptr(*it.ptr)) paged += (it.bytes + 255) & ~size_t(255);
+            }
+            char* dsg = (char*)b->dev_stage(total, rb_buffer::ST_INSERT);
+            char* hs = paged ? (char*)b->host_stage(paged) : nullptr;
+            size_t o = 0, ho = 0;
+            for (auto& it : items) {
+                const size_t sz = (it.bytes + 255) & ~size_t(255);
+                if (is_pinned_ptr(*it.ptr)) {
+                    RB_CUDA(cudaMemcpyAsync(dsg + o, *it.ptr, it.bytes, cudaMemcpyHostToDevice,
+                                            b->stream));
+                    *it.ptr = dsg + o;
+                    o += sz;
+                }
+            }
+            const size_t paged_base = o;
+            for (auto& it : items) {
+                const size_t sz = (it.bytes + 255) & ~size_t(255);
+                if (*it.ptr >= (const void*)dsg && *it.ptr < (const void*)(dsg + total)) continue;
+                std::memcpy(hs + ho, *it.ptr, it.bytes);
+                *it.ptr = dsg + paged_base + ho;
+                ho += sz;
+            }
+            if (paged) {
+                RB_CUDA(cudaMemcpyAsync(dsg + paged_base, hs, paged, cudaMemcpyHostToDevice,
+                                        b->stream));
+                b->host_stage_issued();
+            }
+        }
+        // lengths from offsets (device)
+        const int32_t* d_len = nullptr;
+        if (bt.tok_offsets) {
+            d_len = b->s_len;
+            rb_lengths_from_offsets(bt.tok_offsets, n, b->s_len, b->max_tokens, b->v.ctl,
+                                    b->stream);
+        }
+        const bool want_evrec = (flags & 0x100) != 0;  // internal: rb_push
+        launch_insert(b, bt, d_len, bt.tok_offsets, want_evrec);
+        if (out_evicted_ids) {
+            RB_CUDA(cudaMemcpyAsync(out_evicted_ids, b->s_evid, n * 8, cudaMemcpyDefault,
+                                    b->stream));
+        }
+        // host mirrors: assume fully applied, corrected below when synchronous
+        for (size_t j = 0; j < n; ++j) b->h_pushes[(b->h_cursor + j) % b->T]++;
+        const size_t cursor_before = b->h_cursor;
+        std::vector<long long> pushes_before;
+        b->h_cursor = (b->h_cursor + n) % b->T;
+        if (!(flags & RB_INSERT_ASSUME_UNIQUE)) {
+            DevCtl c;
+            RB_CUDA(cudaMemcpyAsync(&c, b->v.ctl, sizeof c, cudaMemcpyDeviceToHost, b->stream));
+            RB_CUDA(cudaStreamSynchronize(b->stream));
+            if (c.err_code) {
+                // roll the mirrors back to the applied prefix
+                for (size_t j = 0; j < n; ++j) b->h_pushes[(cursor_before + j) % b->T]--;
+                const size_t applied = c.err_index >= 0 ? (size_t)c.err_index : 0;
+                for (size_t j = 0; j < applied; ++j) b->h_pushes[(cursor_before + j) % b->T]++;
+                b->h_cursor = (cursor_before + applied) % b->T;
+                if (out_applied) *out_applied = applied;
+                check_sticky(b);  // clears and throws
+            }
+            if (out_applied) *out_applied = n;
+        } else if (out_applied) {
+            *out_applied = n;
+        }
+    });
+}
+
+int rb_push(rb_buffer* b, const rb_record* rec, const int32_t* tokens, const float* logp_old,
+            int32_t n_tokens, rb_record* evicted, int* has_evicted) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        if (has_evicted) *has_evicted = 0;
+        if (n_tokens < 0 || n_tokens > b->max_tokens)
+            invalid("rb_push: n_tokens exceeds max_tokens");
+        rb_insert_batch bt{};
+        bt.n = 1;
+        const rb_record r = *rec;
+        bt.rollout_id = &r.rollout_id;
+        bt.prompt_id = &r.prompt_id;
+        bt.group_id = &r.group_id;
+        bt.creation_step = &r.creation_step;
+        bt.policy_version = &r.policy_version;
+        bt.reward = &r.reward;
+        bt.is_correct = &r.is_correct;
+        bt.behavior_logprob = &r.behavior_logprob;
+        bt.advantage = &r.advantage;
+        int64_t toff[2] = {0, n_tokens};
+        if (tokens || logp_old) {
+            bt.tok_offsets = toff;
+            bt.tokens = tokens;
+            bt.logp_old = logp_old;
+        } else {
+            bt.tok_offsets = toff;  // records the length (0) without payload
+            toff[1] = 0;
+        }
+        uint64_t evid = NONE_ID;
+        int st = rb_insert(b, &bt, &evid, nullptr, 0x100);
+        if (st != RB_OK) throw Error(st, rb_last_error());
+        if (evid != NONE_ID) {
+            rb_record ev;
+            RB_CUDA(cudaMemcpyAsync(&ev, b->s_evrec, sizeof ev, cudaMemcpyDeviceToHost, b->stream));
+            RB_CUDA(cudaStreamSynchronize(b->stream));
+            if (evicted) *evicted = ev;
+            if (has_evicted) *has_evicted = 1;
+        }
+    });
+}
+
+int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_records,
+              int64_t* out_shard, int64_t* out_index, rb_use_event* out_events,
+              int64_t batch_id, int64_t use_step) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        const size_t T = b->T;
+        if (batch_size == 0 || batch_size % T != 0)  // replay_buffer.cpp:189-192
+            invalid("ShardedReplayBuffer: batch size must be a positive multiple of the shard count");
+        const size_t per = batch_size / T;
+        // The reference fails at the first empty (197-199) or too-small
+        // (148-150, without replacement) shard after mutating earlier shards.
+        size_t nsh = T;
+        std::string err;
+        for (size_t s = 0; s < T; ++s) {
+            const long long occ = std::min<long long>(b->h_pushes[s], (long long)b->C);
+            if (occ == 0) {
+                nsh = s;
+                err = "ShardedReplayBuffer: cannot sample from an empty shard";
+                break;
+            }
+            if (b->strategy != RB_UNIFORM_WITH_REPLACEMENT && (long long)per > occ) {
+                nsh = s;
+                err = "ShardedReplayBuffer: batch exceeds shard occupancy for sampling without "
+                      "replacement";
+                break;
+            }
+        }
+        const size_t nsel = nsh * per;
+        b->ensure_select(std::max<size_t>(batch_size, 1));
+        if (nsh > 0) {
+            MtState* st = rng->to_device(b->stream);
+            SampleArgs a{(int)nsh, (long long)per, b->sel_shard, b->sel_index};
+            if (b->strategy == RB_UNIFORM_WITH_REPLACEMENT) {
+                k_sample_with<<<1, 1024, 0, b->stream>>>(b->v, st, a);
+            } else {
+                int64_t* scr = (int64_t*)b->scratch(2 * b->C * sizeof(int64_t) + 16);
+                k_sample_without<<<1, 32, 0, b->stream>>>(b->v, st, a, b->strategy, scr);
+            }
+            RB_CUDA(cudaGetLastError());
+        }
+        const long long lo = (long long)std::min(b->sb * per, nsel);
+        const long long hi = (long long)std::min(b->se * per, nsel);
+        k_sample_map<<<1, 1024, 0, b->stream>>>(b->v, (long long)nsel, b->sel_shard, b->sel_index,
+                                                b->sel_slot, b->sel_off, lo, hi, b->sel_total,
+                                                b->acc);
+        RB_CUDA(cudaGetLastError());
+        b->B = nsel;
+        b->last_loss = -1;
+        if (nsel > 0 && (out_records || out_events)) {
+            rb_record* dr = out_records;
+            rb_use_event* de = out_events;
+            const bool hr = out_records && !is_device_ptr(out_records);
+            const bool he = out_events && !is_device_ptr(out_events);
+            char* scr = nullptr;
+            if (hr || he) scr = (char*)b->dev_stage(nsel * (sizeof(rb_record) + sizeof(rb_use_event)), rb_buffer::ST_SAMPLE);
+            if (hr) dr = (rb_record*)scr;
+            if (he) de = (rb_use_event*)(scr + nsel * sizeof(rb_record));
+            const unsigned grid = (unsigned)std::min<size_t>((nsel + 255) / 256, 1184);
+            k_sample_records<<<grid, 256, 0, b->stream>>>(b->v, (long long)nsel, (long long)per,
+                                                          b->sel_slot, dr, de, batch_id, use_step);
+            RB_CUDA(cudaGetLastError());
+            if (hr)
+                RB_CUDA(cudaMemcpyAsync(out_records, dr, nsel * sizeof(rb_record),
+                                        cudaMemcpyDeviceToHost, b->stream));
+            if (he)
+                RB_CUDA(cudaMemcpyAsync(out_events, de, nsel * sizeof(rb_use_event),
+                                        cudaMemcpyDeviceToHost, b->stream));
+        }
+        if (nsel > 0 && (out_shard || out_index)) {
+            // (shard, arrival index) as int64 pairs
+            std::vector<int32_t> sh;
+            if (out_shard) {
+                if (is_device_ptr(out_shard)) {
+                    rb_widen_i32(b->sel_shard, out_shard, nsel, b->stream);
+                } else {
+                    sh.resize(nsel);
+                    RB_CUDA(cudaMemcpyAsync(sh.data(), b->sel_shard, nsel * 4,
+                                            cudaMemcpyDeviceToHost, b->stream));
+                }
+            }
+            if (out_index)
+                RB_CUDA(cudaMemcpyAsync(out_index, b->sel_index, nsel * 8, cudaMemcpyDefault,
+                                        b->stream));
+            if (!sh.empty()) {
+                b->sync();
+                for (size_t i = 0; i < nsel; ++i) out_shard[i] = sh[i];
+            }
+        }
+        const bool host_out = (out_records && !is_device_ptr(out_records)) ||
+                              (out_events && !is_device_ptr(out_events)) ||
+                              (out_index && !is_device_ptr(out_index));
+        if (host_out) b->sync();
+        if (!err.empty()) {
+            b->sync();
+            invalid(err);
+        }
+    });
+}
+
+int rb_batch_size(const rb_buffer* b, size_t* n) {
+    *n = b->B;
+    return RB_OK;
+}
+
+int rb_batch_total_tokens(rb_buffer* b, int64_t* total) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        long long t[2];
+        RB_CUDA(cudaMemcpyAsync(t, b->sel_total, sizeof t, cudaMemcpyDeviceToHost, b->stream));
+        b->sync();
+        *total = t[0];
+    });
+}
+
+int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* out_offsets) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        if (b->stride == 0 && (out_tokens || out_logp_old))
+            invalid("rb_gather: buffer holds no token payload (max_tokens = 0)");
+        const size_t per = b->T ? (b->B / b->T) : 0;
+        const long long lo = (long long)std::min(b->sb * per, b->B);
+        const long long hi = (long long)std::min(b->se * per, b->B);
+        const long long nloc = hi - lo;
+        const bool ht = out_tokens && !is_device_ptr(out_tokens);
+        const bool hl = out_logp_old && !is_device_ptr(out_logp_old);
+        long long total = 0;
+        if (ht || hl) {
+            long long t[2];
+            RB_CUDA(cudaMemcpyAsync(t, b->sel_total, sizeof t, cudaMemcpyDeviceToHost, b->stream));
+            b->sync();
+            total = t[0];
+        }
+        int32_t* dt = out_tokens;
+        float* dl = out_logp_old;
+        char* stage = nullptr;
+        const size_t pb = (((size_t)total + 3) & ~size_t(3)) * 4;
+        if (ht || hl) stage = (char*)b->dev_stage(2 * pb + 16, rb_buffer::ST_GATHER);
+        if (ht) dt = (int32_t*)stage;
+        if (hl) dl = (float*)(stage + pb);
+        if (nloc > 0 && (dt || dl)) {
+            k_gather<<<(unsigned)nloc, 256, 0, b->stream>>>(b->v, b->sel_slot, b->sel_off, lo, dt, dl);
+            RB_CUDA(cudaGetLastError());
+        }
+        if (ht) RB_CUDA(cudaMemcpyAsync(out_tokens, dt, total * 4, cudaMemcpyDeviceToHost, b->stream));
+        if (hl) RB_CUDA(cudaMemcpyAsync(out_logp_old, dl, total * 4, cudaMemcpyDeviceToHost, b->stream));
+        if (out_offsets)
+            RB_CUDA(cudaMemcpyAsync(out_offsets, b->sel_off, (nloc + 1) * 8, cudaMemcpyDefault,
+                                    b->stream));
+        if (ht || hl || (out_offsets && !is_device_ptr(out_offsets))) b->sync();
+    });
+}
+
+int rb_batch_ids(rb_buffer* b, uint64_t* out_ids, int32_t* out_lengths, int64_t* out_offsets) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        const size_t per = b->T ? (b->B / b->T) : 0;
+        const long long lo = (long long)std::min(b->sb * per, b->B);
+        const long long hi = (long long)std::min(b->se * per, b->B);
+        const long long n = hi - lo;
+        const bool hid = out_ids && !is_device_ptr(out_ids);
+        const bool hlen = out_lengths && !is_device_ptr(out_lengths);
+        char* st = (char*)b->dev_stage(n * 12 + 64, rb_buffer::ST_IDS);
+        uint64_t* di = hid ? (uint64_t*)st : out_ids;
+        int32_t* dlen = hlen ? (int32_t*)(st + n * 8 + 16) : out_lengths;
+        if (n > 0) rb_batch_ids_dev(b->v, b->sel_slot, lo, hi, di, dlen, b->stream);
+        if (hid) RB_CUDA(cudaMemcpyAsync(out_ids, di, n * 8, cudaMemcpyDeviceToHost, b->stream));
+        if (hlen) RB_CUDA(cudaMemcpyAsync(out_lengths, dlen, n * 4, cudaMemcpyDeviceToHost, b->stream));
+        if (out_offsets)
+            RB_CUDA(cudaMemcpyAsync(out_offsets, b->sel_off, (n + 1) * 8, cudaMemcpyDefault, b->stream));
+        if (hid || hlen || (out_offsets && !is_device_ptr(out_offsets))) b->sync();
+    });
+}
+
+int rb_num_shards(const rb_buffer* b, size_t* out) {
+    *out = b->T;
+    return RB_OK;
+}
+int rb_total_capacity(const rb_buffer* b, size_t* out) {
+    *out = b->N;
+    return RB_OK;
+}
+int rb_shard_capacity(const rb_buffer* b, size_t* out) {
+    *out = b->C;
+    return RB_OK;
+}
+int rb_size(rb_buffer* b, size_t* out) {
+    size_t t = 0;
+    for (size_t s = 0; s < b->T; ++s) t += (size_t)std::min<long long>(b->h_pushes[s], (long long)b->C);
+    *out = t;
+    return RB_OK;
+}
+int rb_shard_size(rb_buffer* b, size_t shard, size_t* out) {
+    return guard([&] {
+        if (shard >= b->T) throw Error(RB_ELOGIC, "vector::_M_range_check: shard out of range");
+        *out = (size_t)std::min<long long>(b->h_pushes[shard], (long long)b->C);
+    });
+}
+int rb_shard_contents(rb_buffer* b, size_t shard, rb_record* out, size_t capacity,
+                      size_t* count) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        if (shard >= b->T) throw Error(RB_ELOGIC, "vector::_M_range_check: shard out of range");
+        const size_t n = (size_t)std::min<long long>(b->h_pushes[shard], (long long)b->C);
+        *count = n;
+        if (!out || n == 0) return;
+        if (capacity < n) invalid("rb_shard_contents: output too small");
+        rb_record* d = (rb_record*)b->dev_stage(n * sizeof(rb_record), rb_buffer::ST_INSPECT);
+        k_shard_contents<<<(unsigned)std::min<size_t>((n + 255) / 256, 1024), 256, 0, b->stream>>>(
+            b->v, (int)shard, (long long)n, d);
+        RB_CUDA(cudaGetLastError());
+        RB_CUDA(cudaMemcpyAsync(out, d, n * sizeof(rb_record), cudaMemcpyDefault, b->stream));
+        b->sync();
+    });
+}
+
+int rb_record_tokens(rb_buffer* b, size_t shard, size_t index, int32_t* tokens,
+                     float* logp_old, int32_t capacity, int32_t* n_tokens) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        if (shard >= b->T) invalid("rb_record_tokens: shard out of range");
+        const size_t n = (size_t)std::min<long long>(b->h_pushes[shard], (long long)b->C);
+        if (index >= n) invalid("rb_record_tokens: index out of range");
+        if (shard < b->sb || shard >= b->se) invalid("rb_record_tokens: shard not held here");
+        int32_t* d = (int32_t*)b->scratch(64);
+        k_slot_of<<<1, 1, 0, b->stream>>>(b->v, (int)shard, (long long)index, d);
+        int32_t g = 0, len = 0;
+        RB_CUDA(cudaMemcpyAsync(&g, d, 4, cudaMemcpyDeviceToHost, b->stream));
+        b->sync();
+        RB_CUDA(cudaMemcpy(&len, b->v.len + g, 4, cudaMemcpyDeviceToHost));
+        *n_tokens = len;
+        if (len > capacity) invalid("rb_record_tokens: output too small");
+        const size_t row = ((size_t)(shard - b->sb) * b->C + (g % b->C)) * (size_t)b->stride;
+        if (tokens) RB_CUDA(cudaMemcpy(tokens, b->v.tok + row, len * 4, cudaMemcpyDefault));
+        if (logp_old) RB_CUDA(cudaMemcpy(logp_old, b->v.lpo + row, len * 4, cudaMemcpyDefault));
+    });
+}
+
+int rb_strategy(const rb_buffer* b, int* out) {
+    *out = b->strategy;
+    return RB_OK;
+}
+int rb_retention(const rb_buffer* b, int* kind, double* delta) {
+    *kind = b->retention;
+    *delta = b->delta;
+    return RB_OK;
+}
+int rb_route_cursor(rb_buffer* b, size_t* out) {
+    *out = b->h_cursor;
+    return RB_OK;
+}
+
+int rb_check(rb_buffer* b) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        check_sticky(b);
+    });
+}
+int rb_synchronize(rb_buffer* b) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        b->sync();
+    });
+}
+
+// replay_buffer.cpp:238-255
+int rb_dump(rb_buffer* b, char* out, size_t cap, size_t* len) {
+    return guard([&] {
+        std::string s;
+        s += "# sharded_replay_buffer v1\n";
+        s += "# shards = " + std::to_string(b->T) + "\n";
+        s += "# capacity = " + std::to_string(b->N) + "\n";
+        s += "# strategy = " + strategy_name(b->strategy) + "\n";
+        s += "# retention = " +
+             std::string(b->retention == RB_PLAIN_FIFO ? "plain_fifo"
+                                                       : "positive_bias delta=" + fmt_double(b->delta)) +
+             "\n";
+        s += "# route_cursor = " + std::to_string(b->h_cursor) + "\n";
+        std::vector<rb_record> recs(b->C + 1);
+        for (size_t sh = 0; sh < b->T; ++sh) {
+            s += "# shard " + std::to_string(sh) + "\n";
+            size_t n = 0;
+            int st = rb_shard_contents(b, sh, recs.data(), recs.size(), &n);
+            if (st != RB_OK) throw Error(st, rb_last_error());
+            for (size_t i = 0; i < n; ++i) {  // rollout.cpp:9-15
+                const rb_record& r = recs[i];
+                s += std::to_string(r.rollout_id) + "," + std::to_string(r.prompt_id) + "," +
+                     std::to_string(r.group_id) + "," + std::to_string(r.creation_step) + "," +
+                     std::to_string(r.policy_version) + "," + fmt_double(r.reward) + "," +
+                     (r.is_correct ? "1" : "0") + "," + fmt_double(r.behavior_logprob) + "," +
+                     fmt_double(r.advantage) + "," + std::to_string(r.use_count) + "\n";
+            }
+        }
+        *len = s.size();
+        if (out && cap) {
+            const size_t m = std::min(s.size(), cap - 1);
+            std::memcpy(out, s.data(), m);
+            out[m] = 0;
+        }
+    });
+}
+
+}  // extern "C"
+
+// ---- load (replay_buffer.cpp:276-324) -----------------------------------
+namespace {
+std::string_view trim(std::string_view s) {  // text_io trim
+    size_t a = 0, e = s.size();
+    while (a < e && (s[a] == ' ' || s[a] == '\t' || s[a] == '\r' || s[a] == '\n')) ++a;
+    while (e > a && (s[e - 1] == ' ' || s[e - 1] == '\t' || s[e - 1] == '\r' || s[e - 1] == '\n')) --e;
+    return s.substr(a, e - a);
+}
+[[noreturn]] void bad_field(std::string_view what, std::string_view text) {
+    invalid(std::string(what) + ": '" + std::string(text) + "'");
+}
+uint64_t parse_u64(std::string_view t0) {
+    auto t = trim(t0);
+    uint64_t v = 0;
+    auto r = std::from_chars(t.data(), t.data() + t.size(), v);
+    if (r.ec != std::errc() || r.ptr != t.data() + t.size() || t.empty())
+        bad_field("not an unsigned integer", t0);
+    return v;
+}
+int64_t parse_i64(std::string_view t0) {
+    auto t = trim(t0);
+    int64_t v = 0;
+    auto r = std::from_chars(t.data(), t.data() + t.size(), v);
+    if (r.ec != std::errc() || r.ptr != t.data() + t.size() || t.empty())
+        bad_field("not an integer", t0);
+    return v;
+}
+double parse_f64(std::string_view t0) {
+    auto t = trim(t0);
+    double v = 0;
+    auto r = std::from_chars(t.data(), t.data() + t.size(), v);
+    if (r.ec != std::errc() || r.ptr != t.data() + t.size() || t.empty())
+        bad_field("not a number", t0);
+    return v;
+}
+bool parse_bool(std::string_view t0) {
+    auto t = trim(t0);
+    if (t == "true" || t == "1") return true;
+    if (t == "false" || t == "0") return false;
+    bad_field("not a boolean", t0);
+}
+std::vector<std::string_view> split(std::string_view s, char d) {
+    std::vector<std::string_view> out;
+    size_t a = 0;
+    for (;;) {
+        size_t e = s.find(d, a);
+        if (e == std::string_view::npos) {
+            out.push_back(s.substr(a));
+            return out;
+        }
+        out.push_back(s.substr(a, e - a));
+        a = e + 1;
+    }
+}
+std::string_view header_value(std::string_view line, std::string_view key) {
+    const size_t eq = line.find('=');
+    if (eq == std::string_view::npos)
+        invalid("buffer dump: malformed header line '" + std::string(line) + "'");
+    const std::string_view name = trim(line.substr(1, eq - 1));
+    if (name != key)
+        invalid("buffer dump: expected header '" + std::string(key) + "', got '" + std::string(name) + "'");
+    return trim(line.substr(eq + 1));
+}
+rb_record record_from_line(std::string_view line) {  // rollout.cpp:17-35
+    const auto f = split(line, ',');
+    if (f.size() != 10)
+        invalid("RolloutRecord: expected 10 fields, got " + std::to_string(f.size()));
+    rb_record r{};
+    r.rollout_id = parse_u64(f[0]);
+    r.prompt_id = parse_u64(f[1]);
+    r.group_id = parse_u64(f[2]);
+    r.creation_step = parse_i64(f[3]);
+    r.policy_version = parse_i64(f[4]);
+    r.reward = parse_f64(f[5]);
+    r.is_correct = parse_bool(f[6]);
+    r.behavior_logprob = parse_f64(f[7]);
+    r.advantage = parse_f64(f[8]);
+    r.use_count = (uint32_t)parse_u64(f[9]);
+    return r;
+}
+}  // namespace
+
+extern "C" int rb_load(const char* text, int32_t max_tokens, int device, rb_buffer** out) {
+    return guard([&] {
+        std::vector<std::string> lines;
+        for (auto l : split(text, '\n')) {
+            auto t = trim(l);
+            if (!t.empty()) lines.emplace_back(t);
+        }
+        if (lines.size() < 6 || lines[0] != "# sharded_replay_buffer v1")
+            invalid("buffer dump: missing or unsupported header");
+        const uint64_t T = parse_u64(header_value(lines[1], "shards"));
+        const uint64_t N = parse_u64(header_value(lines[2], "capacity"));
+        const std::string_view sname = header_value(lines[3], "strategy");
+        int strategy;
+        if (sname == "uniform_with_replacement") strategy = 0;
+        else if (sname == "uniform_without_replacement") strategy = 1;
+        else if (sname == "unused_first_without_replacement") strategy = 2;
+        else invalid("unknown sampling strategy: '" + std::string(sname) + "'");
+        const std::string_view rname = header_value(lines[4], "retention");
+        int retention = RB_PLAIN_FIFO;
+        double delta = 0.0;
+        constexpr std::string_view kPrefix = "positive_bias delta=";
+        if (rname == "plain_fifo") {
+        } else if (rname.substr(0, kPrefix.size()) == kPrefix) {
+            retention = RB_POSITIVE_BIAS;
+            delta = parse_f64(rname.substr(kPrefix.size()));
+            if (!(delta >= 0.0) || !(delta <= 1.0)) invalid("RetentionPolicy: delta must be in [0, 1]");
+        } else {
+            invalid("unknown retention policy: '" + std::string(rname) + "'");
+        }
+        const uint64_t cursor = parse_u64(header_value(lines[5], "route_cursor"));
+        rb_buffer* b = create(T, N, strategy, retention, delta, max_tokens, device, 0, 0);
+        try {
+            if (cursor >= T) invalid("buffer dump: route cursor out of range");
+            std::vector<std::vector<rb_record>> shards(T);
+            std::unordered_set<uint64_t> ids;
+            size_t shard = 0;
+            bool in_shard = false;
+            for (size_t i = 6; i < lines.size(); ++i) {
+                const std::string& line = lines[i];
+                if (line.rfind("# shard ", 0) == 0) {
+                    shard = parse_u64(std::string_view(line).substr(8));
+                    if (shard >= T) invalid("buffer dump: shard index out of range");
+                    in_shard = true;
+                    continue;
+                }
+                if (!in_shard) invalid("buffer dump: record before any shard marker");
+                shards[shard].push_back(record_from_line(line));
+                if (shards[shard].size() > b->C) invalid("buffer dump: shard exceeds capacity");
+                if (!ids.insert(shards[shard].back().rollout_id).second)
+                    invalid("buffer dump: duplicate rollout id " +
+                            std::to_string(shards[shard].back().rollout_id));
+            }
+            DeviceScope ds(b->device);
+            unsigned long long mx = 0;
+            for (size_t s = 0; s < T; ++s) {
+                const size_t n = shards[s].size();
+                b->h_pushes[s] = (long long)n;
+                for (auto& r : shards[s]) mx = std::max<unsigned long long>(mx, r.rollout_id);
+                if (!n) continue;
+                rb_record* d = (rb_record*)b->dev_stage(n * sizeof(rb_record), rb_buffer::ST_INSPECT);
+                RB_CUDA(cudaMemcpyAsync(d, shards[s].data(), n * sizeof(rb_record),
+                                        cudaMemcpyHostToDevice, b->stream));
+                k_load_shard<<<(unsigned)((n + 255) / 256), 256, 0, b->stream>>>(b->v, (int)s,
+                                                                                (long long)n, d);
+                RB_CUDA(cudaGetLastError());
+                b->sync();
+            }
+            RB_CUDA(cudaMemcpy(b->v.pushes, b->h_pushes.data(), T * sizeof(long long),
+                               cudaMemcpyHostToDevice));
+            DevCtl c{};
+            c.cursor = cursor;
+            c.max_id = mx;
+            c.has_any = ids.empty() ? 0 : 1;
+            c.hash_stale = 1;
+            RB_CUDA(cudaMemcpy(b->v.ctl, &c, sizeof c, cudaMemcpyHostToDevice));
+            b->h_cursor = cursor;
+        } catch (...) {
+            delete b;
+            throw;
+        }
+        *out = b;
+    });
+}
+
+// ---- small helper kernels referenced above --------------------------------
+namespace {
+__global__ void k_lengths(const int64_t* toff, long long n, int32_t* len, int32_t maxlen,
+                          DevCtl* ctl) {
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+         j += (long long)gridDim.x * blockDim.x) {
+        long long l = toff[j + 1] - toff[j];
+        if (l < 0 || l > maxlen) {
+            ctl->err_code = RB_EINVAL;
+            ctl->err_index = -3;
+            l = 0;
+        }
+        len[j] = (int32_t)l;
+    }
+}
+__global__ void k_widen(const int32_t* a, int64_t* b, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+__global__ void k_batch_ids(BufView v, const int32_t* sel_slot, long long lo, long long hi,
+                            uint64_t* ids, int32_t* lens) {
+    for (long long i = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < hi;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int g = sel_slot[i];
+        if (ids) ids[i - lo] = v.id[g];
+        if (lens) lens[i - lo] = v.len[g];
+    }
+}
+}  // namespace
+
+void rb_lengths_from_offsets(const int64_t* toff, size_t n, int32_t* len, int32_t maxlen,
+                             DevCtl* ctl, cudaStream_t s) {
+    k_lengths<<<(unsigned)std::min<size_t>((n + 255) / 256, 1024), 256, 0, s>>>(toff, (long long)n, len,
+                                                                                maxlen, ctl);
+    RB_CUDA(cudaGetLastError());
+}
+void rb_widen_i32(const int32_t* a, int64_t* b, size_t n, cudaStream_t s) {
+    k_widen<<<(unsigned)std::min<size_t>((n + 255) / 256, 1024), 256, 0, s>>>(a, b, (long long)n);
+    RB_CUDA(cudaGetLastError());
+}
+void rb_batch_ids_dev(const BufView& v, const int32_t* sel_slot, long long lo, long long hi,
+                      uint64_t* ids, int32_t* lens, cudaStream_t s) {
+    const long long n = hi - lo;
+    k_batch_ids<<<(unsigned)std::min<long long>((n + 255) / 256, 1024), 256, 0, s>>>(v, sel_slot, lo, hi,
+                                                                                    ids, lens);
+    RB_CUDA(cudaGetLastError());
+}

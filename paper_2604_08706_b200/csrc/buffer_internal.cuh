@@ -1,0 +1,114 @@
+// buffer_internal.cuh — the HBM-resident ShardedReplayBuffer behind rb_buffer.
+//
+// Data layout:
+//   metadata  SoA columns of N = T*C slots (slot g = shard*C + local slot),
+//             replicated on every rank: id, prompt, group, creation_step,
+//             policy_version, reward, is_correct, behavior_logprob,
+//             advantage (frozen), group_mean (AsymRE baseline), use_count,
+//             length;
+//   arrival   FIFO: implicit ring, arrival rank i of shard s lives in local
+//             slot (head_s + i) % C with head_s = pushes_s % C once full;
+//             positive bias: explicit ring order[s*C + (head_s + i) % C];
+//   payload   owned shards only: tokens int32[C][stride], logp_old
+//             fp32[C][stride], stride = max_tokens rounded up to 4 (16 B rows).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rb {
+
+struct DevCtl {
+    unsigned long long max_id;  // largest rollout id ever pushed
+    unsigned long long cursor;  // route cursor (replay_buffer.hpp:105)
+    long long err_index;        // first duplicate push of the last insert
+    unsigned long long err_id;
+    int err_code;  // sticky asynchronous error (RB_EINVAL)
+    int has_any;   // max_id valid
+    int hash_stale;
+    int pad;
+};
+
+// Everything a kernel needs, passed by value.
+struct BufView {
+    int T, C, stride, retention;
+    int sb, se;  // owned shards [sb, se)
+    int cs, fs;  // positive bias: correct_slots, fresh_slots (replay_buffer.cpp:110-112)
+    uint64_t *id, *prompt, *group;
+    int64_t *cstep, *pver;
+    double *reward, *blp, *adv, *gmean;
+    uint8_t* correct;
+    uint32_t* use;
+    int32_t* len;
+    int32_t* order;      // [N] positive-bias arrival rings
+    int32_t* head;       // [T]
+    long long* pushes;   // [T]
+    int32_t* owner;      // [N] last writer in the current insert
+    int32_t* tok;        // owned payload
+    float* lpo;
+    uint64_t* hkeys;     // present-id set (exact path)
+    uint32_t* hstate;
+    unsigned long long hcap;
+    DevCtl* ctl;
+};
+
+}  // namespace rb
+
+struct rb_buffer {
+    size_t T = 0, N = 0, C = 0;
+    int strategy = 0, retention = 0;
+    double delta = 0.0;
+    int32_t max_tokens = 0, stride = 0;
+    int device = 0;
+    size_t sb = 0, se = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    rb::BufView v{};
+
+    // host mirrors (exact; updated when an insert is applied)
+    std::vector<long long> h_pushes;
+    size_t h_cursor = 0;
+
+    // scratch (device), grown on demand
+    size_t ins_cap = 0;
+    int32_t* s_tslot = nullptr;
+    uint8_t* s_surv = nullptr;
+    uint64_t* s_evid = nullptr;
+    rb_record* s_evrec = nullptr;
+    double* s_adv = nullptr;
+    double* s_gmean = nullptr;
+    int32_t* s_len = nullptr;
+    int64_t* s_toff = nullptr;
+    // staging of host-side insert inputs (device side) and pinned mirrors
+    enum { ST_INSERT = 0, ST_SAMPLE, ST_GATHER, ST_IDS, ST_INSPECT, ST_LOSS_IN, ST_LOSS_OUT, ST_N };
+    void* stage_dev[ST_N] = {};
+    size_t stage_dev_cap[ST_N] = {};
+    void* stage_host = nullptr;
+    size_t stage_host_cap = 0;
+    cudaEvent_t stage_event = nullptr;  // last async read of stage_host
+
+    // current batch (selection)
+    size_t sel_cap = 0, B = 0;
+    int32_t* sel_slot = nullptr;
+    int32_t* sel_shard = nullptr;
+    int64_t* sel_index = nullptr;
+    int64_t* sel_off = nullptr;      // packed offsets over owned selections (B+1)
+    long long* sel_total = nullptr;  // [0] local tokens, [1] global tokens
+    rb::DevLossAcc* acc = nullptr;
+    int last_loss = -1;              // 0 grpo, 1 asymre
+
+    // misc scratch
+    void* misc = nullptr;
+    size_t misc_cap = 0;
+
+    ~rb_buffer();
+    void* scratch(size_t bytes);          // device misc scratch
+    void* host_stage(size_t bytes);       // pinned host scratch (waits for its last reader)
+    void host_stage_issued();             // record that the stream reads stage_host
+    void* dev_stage(size_t bytes, int slot);  // device staging areas (one per use)
+    void ensure_insert(size_t n);
+    void ensure_select(size_t n);
+    void sync();
+};

@@ -1,0 +1,146 @@
+// common.cuh — internals shared by the libreplay_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "replay_b200.h"
+
+namespace rb {
+
+// ---- error plumbing: C++ exceptions inside, status codes at the ABI -----
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+void set_last_error(const std::string& msg);
+
+#define RB_CUDA(expr)                                                                  \
+    do {                                                                               \
+        cudaError_t _e = (expr);                                                       \
+        if (_e != cudaSuccess)                                                         \
+            throw ::rb::Error(RB_ECUDA, std::string("CUDA error: ") +                  \
+                                            cudaGetErrorString(_e) + " at " #expr);    \
+    } while (0)
+
+inline void invalid(const std::string& m) { throw Error(RB_EINVAL, m); }
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return RB_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_last_error("out of memory");
+        return RB_ENOMEM;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return RB_ELOGIC;
+    }
+}
+
+// Fails loudly when no sm_100 device is usable (there is no CPU fallback).
+void require_device();
+
+// Pointer classification: true if `p` is device memory / page-locked host memory.
+bool is_device_ptr(const void* p);
+bool is_pinned_ptr(const void* p);
+
+// ---- MT19937-64 (rng.hpp:68, std::mt19937_64 per [rand.predef]) --------
+constexpr int MT_N = 312;
+constexpr int MT_M = 156;
+constexpr uint64_t MT_UM = 0xFFFFFFFF80000000ULL;
+constexpr uint64_t MT_LM = 0x000000007FFFFFFFULL;
+constexpr uint64_t MT_A = 0xB5026F5AA96619E9ULL;
+
+struct MtState {  // identical layout on host and device
+    uint64_t mt[MT_N];
+    uint32_t idx;
+    uint32_t pad;
+    uint64_t draws;
+};
+
+__host__ __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= y >> 43;
+    return y;
+}
+__host__ __device__ __forceinline__ uint64_t mt_mix(uint64_t a, uint64_t b) {
+    const uint64_t x = (a & MT_UM) | (b & MT_LM);
+    return (x >> 1) ^ ((x & 1ULL) ? MT_A : 0ULL);
+}
+// Sequential twist (one thread; used by the scalar device paths and the host).
+__host__ __device__ inline void mt_twist_scalar(uint64_t* mt) {
+    for (int i = 0; i < MT_N; ++i) {
+        const int i1 = (i + 1 == MT_N) ? 0 : i + 1;
+        const int im = (i + MT_M >= MT_N) ? i + MT_M - MT_N : i + MT_M;
+        mt[i] = mt[im] ^ mt_mix(mt[i], mt[i1]);
+    }
+}
+__host__ __device__ inline uint64_t mt_next_scalar(uint64_t* mt, uint32_t* idx,
+                                                   uint64_t* draws) {
+    if (*idx >= MT_N) {
+        mt_twist_scalar(mt);
+        *idx = 0;
+    }
+    ++*draws;
+    return mt_temper(mt[(*idx)++]);
+}
+// rng.cpp:44: values >= limit are rejected.
+__host__ __device__ __forceinline__ uint64_t below_limit(uint64_t bound) {
+    return UINT64_MAX - UINT64_MAX % bound;
+}
+
+// Block-cooperative twist of a shared-memory MT state in three dependency
+// phases (i < 156 reads only old words; 156 <= i < 311 reads new words
+// i-156; i = 311 reads new word 0).  Requires blockDim.x >= 156; every
+// thread of the block must call it.
+__device__ __forceinline__ void mt_twist_block(uint64_t* mt) {
+    const int t = threadIdx.x;
+    uint64_t v = 0;
+    if (t < 156) v = mt[t + 156] ^ mt_mix(mt[t], mt[t + 1]);
+    __syncthreads();
+    if (t < 156) mt[t] = v;
+    __syncthreads();
+    if (t < 155) v = mt[t] ^ mt_mix(mt[t + 156], mt[t + 157]);
+    __syncthreads();
+    if (t < 155) mt[t + 156] = v;
+    __syncthreads();
+    if (t == 0) mt[311] = mt[155] ^ mt_mix(mt[311], mt[0]);
+    __syncthreads();
+}
+
+// ---- small device helpers ----------------------------------------------
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Device-side loss accumulator (one per buffer; reset by the sampler).
+struct DevLossAcc {
+    double obj_sum;
+    unsigned long long included;
+    unsigned long long excluded;
+    unsigned long long done_blocks;
+    long long total_tokens;  // normaliser used for the optimistic scale
+    double objective;
+    int need_fixup;
+    int pad;
+};
+
+}  // namespace rb

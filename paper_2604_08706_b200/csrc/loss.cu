@@ -1,0 +1,755 @@
+// loss.cu — group advantages and the two policy-gradient losses.
+//
+//   rb_loss_grpo      grpo_loss_grad (bandit.cpp:363-408) per token of the
+//                     current batch: logp_old read straight from the slot row
+//                     (never packed), logp_now / dlogp packed; 20 B/token with
+//                     the gather.
+//   rb_loss_asymre    asymre_loss_grad (bandit.cpp:410-438) per token.
+//   rb_group_advantages, rb_grpo_tokens, rb_grpo_records, rb_asymre_*:
+//                     the same arithmetic over explicit arrays.
+//
+// Precision: the ratio is evaluated in fp32 (expf) and the branch decided in
+// fp32 unless the token sits within 4e-6 (relative) of a clip edge, has
+// |logp_now - logp_old| >= 80 or is non-finite; those tokens are recomputed
+// exactly as the reference does, in fp64 (exp, clamp, r*A <= c*A with ties to
+// the unclipped branch, non-finite => excluded).  Objective terms accumulate
+// in fp64.  dlogp is written with the optimistic scale -1/total_tokens; if any
+// token was excluded, the last CTA flags a rescale to -1/included.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "buffer_internal.cuh"
+
+using namespace rb;
+
+namespace rb {
+
+struct GrpoParams {
+    float lo_f, hi_f;    // 1-eps_low, 1+eps_high (fp32)
+    double lo, hi;       // same in fp64
+};
+
+struct GrpoPartial {
+    double obj = 0.0;
+    long long inc = 0, exc = 0;
+};
+
+// One token (bandit.cpp:380-400).  Returns the un-normalised coefficient.
+__device__ __forceinline__ float grpo_token(float lpn, float lpo, double A, float Af,
+                                            const GrpoParams& p, GrpoPartial& acc) {
+    const float d = lpn - lpo;
+    const float r = __expf(d);
+    const bool edge = !(fabsf(d) < 80.f) || fabsf(r - p.hi_f) <= 4e-6f * p.hi_f ||
+                      fabsf(r - p.lo_f) <= 4e-6f * p.lo_f;
+    if (!edge) {
+        ++acc.inc;
+        bool unclipped;
+        if (A > 0.0)
+            unclipped = r <= p.hi_f;
+        else if (A < 0.0)
+            unclipped = r >= p.lo_f;
+        else
+            unclipped = true;
+        if (unclipped) {
+            acc.obj += (double)r * A;
+            return Af * r;
+        }
+        acc.obj += (A > 0.0 ? p.hi : p.lo) * A;
+        return 0.f;
+    }
+    const double rd = exp((double)lpn - (double)lpo);
+    if (!isfinite(rd)) {  // bandit.cpp:381-386
+        ++acc.exc;
+        return 0.f;
+    }
+    ++acc.inc;
+    const double c = rd < p.lo ? p.lo : (p.hi < rd ? p.hi : rd);  // std::clamp
+    const double uv = __dmul_rn(rd, A), cv = __dmul_rn(c, A);
+    if (uv <= cv) {  // ties -> unclipped (bandit.cpp:392)
+        acc.obj += uv;
+        return (float)(A * rd);
+    }
+    acc.obj += cv;
+    return 0.f;
+}
+
+__device__ __forceinline__ uint4 ldg4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint4 funnel4(const uint4& lo, const uint4& hi, int a) {
+    switch (a & 3) {
+        case 0: return lo;
+        case 1: return make_uint4(lo.y, lo.z, lo.w, hi.x);
+        case 2: return make_uint4(lo.z, lo.w, hi.x, hi.y);
+        default: return make_uint4(lo.w, hi.x, hi.y, hi.z);
+    }
+}
+__device__ __forceinline__ uint4 shfl_up_q(const uint4& q) {
+    return make_uint4(__shfl_up_sync(0xffffffffu, q.x, 1), __shfl_up_sync(0xffffffffu, q.y, 1),
+                      __shfl_up_sync(0xffffffffu, q.z, 1), __shfl_up_sync(0xffffffffu, q.w, 1));
+}
+__device__ __forceinline__ float qf(const uint4& q, int i) {
+    return __uint_as_float(i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w);
+}
+
+// Block reduction of the partials + one atomic per CTA + last-CTA finalize.
+__device__ void grpo_block_commit(GrpoPartial p, DevLossAcc* acc) {
+    __shared__ double s_obj[32];
+    __shared__ long long s_inc[32], s_exc[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    p.obj = warp_sum_f64(p.obj);
+    p.inc = warp_sum_i64(p.inc);
+    p.exc = warp_sum_i64(p.exc);
+    if (lane == 0) {
+        s_obj[wid] = p.obj;
+        s_inc[wid] = p.inc;
+        s_exc[wid] = p.exc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double o = 0;
+        long long i = 0, e = 0;
+        for (int w = 0; w < nw; ++w) {
+            o += s_obj[w];
+            i += s_inc[w];
+            e += s_exc[w];
+        }
+        atomicAdd(&acc->obj_sum, o);
+        atomicAdd(&acc->included, (unsigned long long)i);
+        atomicAdd(&acc->excluded, (unsigned long long)e);
+        __threadfence();
+        const unsigned long long t = atomicAdd(&acc->done_blocks, 1ULL);
+        if (t == gridDim.x - 1) {  // last CTA: objective and rescale flag
+            __threadfence();
+            const unsigned long long inc = atomicAdd(&acc->included, 0ULL);
+            const unsigned long long exc = atomicAdd(&acc->excluded, 0ULL);
+            const double obj = atomicAdd(&acc->obj_sum, 0.0);
+            acc->objective = inc ? obj / (double)inc : 0.0;
+            acc->need_fixup = exc > 0 && inc > 0;
+        }
+    }
+}
+
+// GRPO over the current batch: CTA per owned selection.
+__global__ void __launch_bounds__(256) k_loss_grpo_buf(BufView v, const int32_t* sel_slot,
+                                                       const int64_t* off, long long lo,
+                                                       const float* lpn_packed, float* dlogp,
+                                                       GrpoParams prm, DevLossAcc* acc) {
+    const long long b = lo + blockIdx.x;
+    const int g = sel_slot[b];
+    const int s = g / v.C;
+    const float* row = v.lpo + ((size_t)(s - v.sb) * v.C + (g % v.C)) * (size_t)v.stride;
+    const int len = v.len[g];
+    const long long doff = off[blockIdx.x];
+    const double A = v.adv[g];
+    const float Af = (float)A;
+    const float scale = -1.f / (float)acc->total_tokens;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int a = (int)(doff & 3);
+    const int nsq = (len + 3) >> 2;
+    const int nq = (a + len + 3) >> 2;
+    const long long P0 = doff >> 2;
+    GrpoPartial part;
+    for (int base = wid * 32; base < nq; base += nw * 32) {
+        const int k = base + lane;
+        const uint4 cur = k < nsq ? ldg4(row + 4 * k) : make_uint4(0, 0, 0, 0);
+        uint4 prev = shfl_up_q(cur);
+        if (lane == 0 && a && k >= 1) prev = ldg4(row + 4 * (k - 1));
+        if (k < nq) {
+            const uint4 old = a ? funnel4(prev, cur, 4 - a) : cur;
+            const uint4 now = ldg4(lpn_packed + 4 * (P0 + k));
+            const int e0 = 4 * k - a;
+            float o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                o[i] = 0.f;
+                if (e0 + i >= 0 && e0 + i < len)
+                    o[i] = grpo_token(qf(now, i), qf(old, i), A, Af, prm, part) * scale;
+            }
+            float* dq = dlogp + 4 * (P0 + k);
+            if (e0 >= 0 && e0 + 3 < len) {
+                *reinterpret_cast<float4*>(dq) = make_float4(o[0], o[1], o[2], o[3]);
+            } else {
+                for (int i = 0; i < 4; ++i)
+                    if (e0 + i >= 0 && e0 + i < len) dq[i] = o[i];
+            }
+        }
+    }
+    grpo_block_commit(part, acc);
+}
+
+// GRPO over explicit packed arrays (stateless API): CTA per trajectory.
+__global__ void __launch_bounds__(256) k_loss_grpo_packed(const float* lpn, const float* lpo,
+                                                          const double* adv,
+                                                          const int64_t* offsets, float* dlogp,
+                                                          GrpoParams prm, DevLossAcc* acc,
+                                                          long long n_traj) {
+    const long long i = blockIdx.x;
+    const long long o0 = offsets[i], o1 = offsets[i + 1];
+    const int len = (int)(o1 - o0);
+    const double A = adv[i];
+    const float Af = (float)A;
+    const long long total = offsets[n_traj] - offsets[0];
+    const float scale = total > 0 ? -1.f / (float)total : 0.f;
+    const long long q0 = o0 >> 2, q1 = (o1 + 3) >> 2;
+    GrpoPartial part;
+    for (long long q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+        const uint4 now = ldg4(lpn + 4 * q);
+        const uint4 old = ldg4(lpo + 4 * q);
+        float* dq = dlogp + 4 * q;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const long long t = 4 * q + e;
+            if (t >= o0 && t < o1) dq[e] = grpo_token(qf(now, e), qf(old, e), A, Af, prm, part) * scale;
+        }
+    }
+    (void)len;
+    grpo_block_commit(part, acc);
+}
+
+__global__ void k_dlogp_rescale(float* d, long long n, const long long* n_dev,
+                                const DevLossAcc* acc) {
+    if (!acc->need_fixup) return;
+    if (n_dev) n = *n_dev;
+    const float f = (float)((double)acc->total_tokens / (double)acc->included);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        d[i] *= f;
+}
+
+// AsymRE over the current batch: dlogp = -coef/B on every token.
+__global__ void __launch_bounds__(256) k_loss_asymre_buf(BufView v, const int32_t* sel_slot,
+                                                         const int64_t* off, long long lo,
+                                                         const float* lpn_packed, float* dlogp,
+                                                         double delta_v, double inv_b,
+                                                         DevLossAcc* acc) {
+    const long long b = lo + blockIdx.x;
+    const int g = sel_slot[b];
+    const int len = v.len[g];
+    const long long o0 = off[blockIdx.x], o1 = o0 + len;
+    const double coef = v.reward[g] - (v.gmean[g] + delta_v);  // bandit.cpp:429
+    const float gcoef = (float)(coef * -inv_b);
+    double seq = 0.0;
+    const long long q0 = o0 >> 2, q1 = (o1 + 3) >> 2;
+    for (long long q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+        const uint4 now = ldg4(lpn_packed + 4 * q);
+        float* dq = dlogp + 4 * q;
+        if (4 * q >= o0 && 4 * q + 3 < o1) {
+            seq += (double)qf(now, 0) + (double)qf(now, 1) + (double)qf(now, 2) + (double)qf(now, 3);
+            *reinterpret_cast<float4*>(dq) = make_float4(gcoef, gcoef, gcoef, gcoef);
+        } else {
+            for (int e = 0; e < 4; ++e) {
+                const long long t = 4 * q + e;
+                if (t >= o0 && t < o1) {
+                    seq += (double)qf(now, e);
+                    dq[e] = gcoef;
+                }
+            }
+        }
+    }
+    GrpoPartial p;
+    p.obj = coef * seq;
+    grpo_block_commit(p, acc);
+}
+
+__global__ void __launch_bounds__(256) k_loss_asymre_packed(const float* lpn, const double* reward,
+                                                            const double* gmean,
+                                                            const int64_t* offsets, float* dlogp,
+                                                            double delta_v, double inv_b,
+                                                            DevLossAcc* acc) {
+    const long long i = blockIdx.x;
+    const long long o0 = offsets[i], o1 = offsets[i + 1];
+    const double coef = reward[i] - (gmean[i] + delta_v);
+    const float gcoef = (float)(coef * -inv_b);
+    double seq = 0.0;
+    for (long long t = o0 + threadIdx.x; t < o1; t += blockDim.x) {
+        seq += (double)lpn[t];
+        dlogp[t] = gcoef;
+    }
+    GrpoPartial p;
+    p.obj = coef * seq;
+    grpo_block_commit(p, acc);
+}
+
+// Record-level fp64 forms (L = 1): the reference's arithmetic per record.
+__global__ void k_grpo_records(const double* lpn, const double* blp, const double* adv,
+                               long long n, double lo, double hi, double* coef_out,
+                               DevLossAcc* acc) {
+    GrpoPartial p;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double ratio = exp(lpn[i] - blp[i]);
+        if (!isfinite(ratio)) {
+            ++p.exc;
+            coef_out[i] = 0.0;
+            continue;
+        }
+        ++p.inc;
+        const double A = adv[i];
+        const double c = ratio < lo ? lo : (hi < ratio ? hi : ratio);
+        const double uv = __dmul_rn(ratio, A), cv = __dmul_rn(c, A);
+        if (uv <= cv) {
+            p.obj += uv;
+            coef_out[i] = __dmul_rn(A, ratio);
+        } else {
+            p.obj += cv;
+            coef_out[i] = 0.0;
+        }
+    }
+    grpo_block_commit(p, acc);
+}
+__global__ void k_scale_records(double* d, long long n, const DevLossAcc* acc) {
+    const unsigned long long inc = acc->included;
+    const double s = inc ? 1.0 / (double)inc : 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        d[i] = inc ? __dmul_rn(d[i], -s) : 0.0;
+}
+__global__ void k_asymre_records(const double* lpn, const double* reward, const double* gmean,
+                                 long long n, double delta_v, double* d, DevLossAcc* acc) {
+    GrpoPartial p;
+    const double s = 1.0 / (double)n;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double coef = reward[i] - (gmean[i] + delta_v);
+        p.obj += __dmul_rn(coef, lpn[i]);
+        d[i] = __dmul_rn(coef, -s);
+    }
+    grpo_block_commit(p, acc);
+}
+
+// group_advantages (bandit.cpp:276-294), segmented; bit-exact fp64.
+__global__ void k_group_adv(const double* r, const int64_t* off, long long ng, double* adv,
+                            double* mean_out, int* bad) {
+    for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < ng;
+         gi += (long long)gridDim.x * blockDim.x) {
+        const long long b = off[gi], e = off[gi + 1], m = e - b;
+        if (m < 2) {
+            *bad = 1;
+            continue;
+        }
+        const double dn = (double)m;
+        double mean = 0.0;
+        for (long long k = b; k < e; ++k) mean = __dadd_rn(mean, r[k]);
+        mean = __ddiv_rn(mean, dn);
+        double var = 0.0;
+        for (long long k = b; k < e; ++k) {
+            const double d = __dsub_rn(r[k], mean);
+            var = __dadd_rn(var, __dmul_rn(d, d));
+        }
+        var = __ddiv_rn(var, dn);
+        const double sd = __dsqrt_rn(var);
+        for (long long k = b; k < e; ++k)
+            adv[k] = sd < 1e-8 ? 0.0 : __ddiv_rn(__dsub_rn(r[k], mean), sd);
+        if (mean_out) mean_out[gi] = mean;
+    }
+}
+
+__global__ void k_acc_reset(DevLossAcc* acc, long long total) {
+    acc->obj_sum = 0.0;
+    acc->included = 0;
+    acc->excluded = 0;
+    acc->done_blocks = 0;
+    acc->total_tokens = total;
+    acc->objective = 0.0;
+    acc->need_fixup = 0;
+}
+__global__ void k_acc_set_total(DevLossAcc* acc, const long long* total_or_null, long long v) {
+    acc->total_tokens = total_or_null ? *total_or_null : v;
+    acc->obj_sum = 0.0;
+    acc->included = 0;
+    acc->excluded = 0;
+    acc->done_blocks = 0;
+    acc->objective = 0.0;
+    acc->need_fixup = 0;
+}
+__global__ void k_stats_out(const DevLossAcc* acc, rb_loss_stats* out, int asym, double inv_b) {
+    out->objective_sum = acc->obj_sum;
+    out->objective = asym ? acc->obj_sum * inv_b : acc->objective;
+    out->included = (long long)acc->included;
+    out->excluded = (long long)acc->excluded;
+    out->total_tokens = acc->total_tokens;
+}
+__global__ void k_stats_in(DevLossAcc* acc, const rb_loss_stats* in) {
+    acc->obj_sum = in->objective_sum;
+    acc->included = (unsigned long long)in->included;
+    acc->excluded = (unsigned long long)in->excluded;
+    acc->objective = in->included ? in->objective_sum / (double)in->included : 0.0;
+    acc->need_fixup = in->excluded > 0 && in->included > 0;
+}
+
+// ---- stateless context: stream + staging per process ---------------------
+struct Ctx {
+    std::mutex mu;
+    cudaStream_t stream = nullptr;
+    DevLossAcc* acc = nullptr;
+    rb_loss_stats* dstats = nullptr;
+    int* dflag = nullptr;
+    std::vector<void*> temps;
+    Ctx() {}
+    void init() {
+        if (stream) return;
+        require_device();
+        RB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        RB_CUDA(cudaMalloc(&acc, sizeof(DevLossAcc)));
+        RB_CUDA(cudaMalloc(&dstats, sizeof(rb_loss_stats)));
+        RB_CUDA(cudaMalloc(&dflag, sizeof(int)));
+    }
+    // device view of a (possibly host) input array
+    template <class T>
+    const T* in(const T* p, size_t n) {
+        if (!p || is_device_ptr(p)) return p;
+        void* d;
+        RB_CUDA(cudaMallocAsync(&d, std::max<size_t>(n, 1) * sizeof(T) + 16, stream));
+        RB_CUDA(cudaMemcpyAsync(d, p, n * sizeof(T), cudaMemcpyHostToDevice, stream));
+        temps.push_back(d);
+        return (const T*)d;
+    }
+    template <class T>
+    T* out(T* p, size_t n, std::vector<std::pair<void*, std::pair<void*, size_t>>>& back) {
+        if (!p || is_device_ptr(p)) return p;
+        void* d;
+        RB_CUDA(cudaMallocAsync(&d, std::max<size_t>(n, 1) * sizeof(T) + 16, stream));
+        temps.push_back(d);
+        back.push_back({(void*)p, {d, n * sizeof(T)}});
+        return (T*)d;
+    }
+    void finish(std::vector<std::pair<void*, std::pair<void*, size_t>>>& back) {
+        for (auto& b : back)
+            RB_CUDA(cudaMemcpyAsync(b.first, b.second.first, b.second.second,
+                                    cudaMemcpyDeviceToHost, stream));
+        for (void* t : temps) RB_CUDA(cudaFreeAsync(t, stream));
+        temps.clear();
+        RB_CUDA(cudaStreamSynchronize(stream));
+    }
+    void stats(rb_loss_stats* s, int asym, double inv_b,
+               std::vector<std::pair<void*, std::pair<void*, size_t>>>& back) {
+        if (!s) return;
+        rb_loss_stats* d = is_device_ptr(s) ? s : dstats;
+        k_stats_out<<<1, 1, 0, stream>>>(acc, d, asym, inv_b);
+        RB_CUDA(cudaGetLastError());
+        if (d != s) back.push_back({(void*)s, {(void*)d, sizeof(rb_loss_stats)}});
+    }
+};
+Ctx& ctx() {
+    static Ctx c;
+    return c;
+}
+
+void copy_stats(rb_buffer* b, rb_loss_stats* stats, int asym, double inv_b) {
+    if (!stats) return;
+    const bool host = !is_device_ptr(stats);
+    rb_loss_stats* d = host ? (rb_loss_stats*)b->scratch(sizeof(rb_loss_stats)) : stats;
+    k_stats_out<<<1, 1, 0, b->stream>>>(b->acc, d, asym, inv_b);
+    RB_CUDA(cudaGetLastError());
+    if (host) {
+        RB_CUDA(cudaMemcpyAsync(stats, d, sizeof *stats, cudaMemcpyDeviceToHost, b->stream));
+        b->sync();
+    }
+}
+
+// Host logp_now / dlogp for the buffer losses: staged through the buffer's
+// ST_LOSS_IN / ST_LOSS_OUT device areas (H2D before, D2H after).
+struct HostIO {
+    rb_buffer* b;
+    const float* in;
+    float* out;
+    bool host_in, host_out;
+    long long total = 0;
+    HostIO(rb_buffer* b_, const float* lpn, float* dl) : b(b_), in(lpn), out(dl) {
+        host_in = lpn && !is_device_ptr(lpn);
+        host_out = dl && !is_device_ptr(dl);
+        if (!host_in && !host_out) return;
+        RB_CUDA(cudaMemcpyAsync(&total, b->sel_total, 8, cudaMemcpyDeviceToHost, b->stream));
+        b->sync();
+        const size_t bytes = (((size_t)total + 3) & ~size_t(3)) * 4 + 16;
+        if (host_in) {
+            float* d = (float*)b->dev_stage(bytes, rb_buffer::ST_LOSS_IN);
+            if (is_pinned_ptr(lpn)) {
+                RB_CUDA(cudaMemcpyAsync(d, lpn, total * 4, cudaMemcpyHostToDevice, b->stream));
+            } else {
+                void* hs = b->host_stage(total * 4 + 16);
+                std::memcpy(hs, lpn, total * 4);
+                RB_CUDA(cudaMemcpyAsync(d, hs, total * 4, cudaMemcpyHostToDevice, b->stream));
+                b->host_stage_issued();
+            }
+            in = d;
+        }
+        if (host_out) out = (float*)b->dev_stage(bytes, rb_buffer::ST_LOSS_OUT);
+    }
+    void finish(float* user_out) {
+        if (!host_out) return;
+        RB_CUDA(cudaMemcpyAsync(user_out, out, total * 4, cudaMemcpyDeviceToHost, b->stream));
+        b->sync();
+    }
+};
+
+unsigned grid_for(long long n) {
+    return (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8));
+}
+
+}  // namespace rb
+
+// ====================================================================== C ABI
+extern "C" {
+
+int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double eps_low,
+                 double eps_high, int64_t norm_tokens, rb_loss_stats* stats) {
+    return guard([&] {
+        if (b->stride == 0) invalid("rb_loss_grpo: buffer holds no token payload");
+        if (eps_low < 0.0 || eps_high < 0.0) invalid("loss spec: clip bounds must be >= 0");
+        if (!std::isfinite(eps_low) || !std::isfinite(eps_high))
+            invalid("loss spec: parameters must be finite");
+        HostIO io(b, logp_now, out_dlogp);
+        logp_now = io.in;
+        float* const user_dlogp = out_dlogp;
+        out_dlogp = io.out;
+        const size_t per = b->T ? b->B / b->T : 0;
+        const long long lo = (long long)std::min(b->sb * per, b->B);
+        const long long hi = (long long)std::min(b->se * per, b->B);
+        if (b->B == 0) invalid("loss gradient needs a non-empty batch");
+        GrpoParams p;
+        p.lo = 1.0 - eps_low;
+        p.hi = 1.0 + eps_high;
+        p.lo_f = (float)p.lo;
+        p.hi_f = (float)p.hi;
+        if (norm_tokens > 0 || b->last_loss != -1) {
+            // explicit normaliser, or a second loss on the same batch
+            k_acc_set_total<<<1, 1, 0, b->stream>>>(b->acc, norm_tokens > 0 ? nullptr : b->sel_total + 1,
+                                                    norm_tokens);
+            RB_CUDA(cudaGetLastError());
+        }
+        b->last_loss = 0;
+        if (hi > lo) {
+            k_loss_grpo_buf<<<(unsigned)(hi - lo), 256, 0, b->stream>>>(
+                b->v, b->sel_slot, b->sel_off, lo, logp_now, out_dlogp, p, b->acc);
+            RB_CUDA(cudaGetLastError());
+            // Rescale only when a token was excluded (flag set by the last CTA).
+            // Multi-rank buffers defer this to rb_loss_finalize (global counts).
+            if (b->sb == 0 && b->se == b->T) {
+                k_dlogp_rescale<<<148, 256, 0, b->stream>>>(out_dlogp, 0, b->sel_total, b->acc);
+                RB_CUDA(cudaGetLastError());
+            }
+        }
+        io.finish(user_dlogp);
+        copy_stats(b, stats, 0, 0.0);
+    });
+}
+
+int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double delta_v,
+                   int64_t norm_batch, rb_loss_stats* stats) {
+    return guard([&] {
+        if (!std::isfinite(delta_v)) invalid("loss spec: parameters must be finite");
+        if (b->B == 0) invalid("loss gradient needs a non-empty batch");
+        HostIO io(b, logp_now, out_dlogp);
+        logp_now = io.in;
+        float* const user_dlogp = out_dlogp;
+        out_dlogp = io.out;
+        const size_t per = b->T ? b->B / b->T : 0;
+        const long long lo = (long long)std::min(b->sb * per, b->B);
+        const long long hi = (long long)std::min(b->se * per, b->B);
+        const double inv_b = 1.0 / (double)(norm_batch > 0 ? norm_batch : (int64_t)b->B);
+        if (b->last_loss != -1) {
+            k_acc_set_total<<<1, 1, 0, b->stream>>>(b->acc, b->sel_total + 1, 0);
+            RB_CUDA(cudaGetLastError());
+        }
+        b->last_loss = 1;
+        if (hi > lo) {
+            k_loss_asymre_buf<<<(unsigned)(hi - lo), 256, 0, b->stream>>>(
+                b->v, b->sel_slot, b->sel_off, lo, logp_now, out_dlogp, delta_v, inv_b, b->acc);
+            RB_CUDA(cudaGetLastError());
+        }
+        io.finish(user_dlogp);
+        copy_stats(b, stats, 1, inv_b);
+    });
+}
+
+int rb_loss_finalize(rb_buffer* b, float* dlogp, rb_loss_stats* stats) {
+    return guard([&] {
+        // Asynchronous when stats is a device pointer (the multi-GPU hot path:
+        // allreduce the device stats, then finalize without a host round trip).
+        if (!stats) invalid("rb_loss_finalize: stats required");
+        const bool host = !is_device_ptr(stats);
+        rb_loss_stats* dst = stats;
+        if (host) {
+            dst = (rb_loss_stats*)b->scratch(sizeof(rb_loss_stats));
+            RB_CUDA(cudaMemcpyAsync(dst, stats, sizeof(rb_loss_stats), cudaMemcpyHostToDevice,
+                                    b->stream));
+        }
+        k_stats_in<<<1, 1, 0, b->stream>>>(b->acc, dst);
+        RB_CUDA(cudaGetLastError());
+        if (b->last_loss == 0 && dlogp) {
+            k_dlogp_rescale<<<148, 256, 0, b->stream>>>(dlogp, 0, b->sel_total, b->acc);
+            RB_CUDA(cudaGetLastError());
+        }
+        k_stats_out<<<1, 1, 0, b->stream>>>(b->acc, dst, 0, 0.0);
+        RB_CUDA(cudaGetLastError());
+        if (host) {
+            RB_CUDA(cudaMemcpyAsync(stats, dst, sizeof(rb_loss_stats), cudaMemcpyDeviceToHost,
+                                    b->stream));
+            b->sync();
+        }
+    });
+}
+
+int rb_group_advantages(const double* rewards, const int64_t* offsets, size_t n_groups,
+                        double* out_adv, double* out_mean) {
+    return guard([&] {
+        Ctx& c = ctx();
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.init();
+        int64_t last = 0;
+        if (is_device_ptr(offsets))
+            RB_CUDA(cudaMemcpy(&last, offsets + n_groups, 8, cudaMemcpyDeviceToHost));
+        else
+            last = offsets[n_groups];
+        if (!is_device_ptr(offsets)) {
+            for (size_t g = 0; g < n_groups; ++g)
+                if (offsets[g + 1] - offsets[g] < 2) invalid("group advantages need >= 2 rewards");
+        }
+        std::vector<std::pair<void*, std::pair<void*, size_t>>> back;
+        const double* r = c.in(rewards, (size_t)last);
+        const int64_t* o = c.in(offsets, n_groups + 1);
+        double* a = c.out(out_adv, (size_t)last, back);
+        double* m = c.out(out_mean, n_groups, back);
+        RB_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.stream));
+        k_group_adv<<<grid_for((long long)n_groups), 256, 0, c.stream>>>(r, o, (long long)n_groups, a, m,
+                                                                         c.dflag);
+        RB_CUDA(cudaGetLastError());
+        int bad = 0;
+        RB_CUDA(cudaMemcpyAsync(&bad, c.dflag, sizeof bad, cudaMemcpyDeviceToHost, c.stream));
+        c.finish(back);
+        if (bad) invalid("group advantages need >= 2 rewards");
+    });
+}
+
+int rb_grpo_tokens(const float* logp_now, const float* logp_old, const double* adv,
+                   const int64_t* offsets, size_t n_traj, double eps_low, double eps_high,
+                   float* out_dlogp, rb_loss_stats* stats) {
+    return guard([&] {
+        if (eps_low < 0.0 || eps_high < 0.0) invalid("loss spec: clip bounds must be >= 0");
+        if (!std::isfinite(eps_low) || !std::isfinite(eps_high))
+            invalid("loss spec: parameters must be finite");
+        if (n_traj == 0) invalid("loss gradient needs a non-empty batch");
+        Ctx& c = ctx();
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.init();
+        int64_t first = 0, last = 0;
+        if (is_device_ptr(offsets)) {
+            RB_CUDA(cudaMemcpy(&first, offsets, 8, cudaMemcpyDeviceToHost));
+            RB_CUDA(cudaMemcpy(&last, offsets + n_traj, 8, cudaMemcpyDeviceToHost));
+        } else {
+            first = offsets[0];
+            last = offsets[n_traj];
+        }
+        if (first != 0) invalid("rb_grpo_tokens: offsets must start at 0");
+        const size_t nt = ((size_t)last + 3) & ~size_t(3);
+        std::vector<std::pair<void*, std::pair<void*, size_t>>> back;
+        const float* lpn = c.in(logp_now, (size_t)last);
+        const float* lpo = c.in(logp_old, (size_t)last);
+        const double* a = c.in(adv, n_traj);
+        const int64_t* o = c.in(offsets, n_traj + 1);
+        float* d = c.out(out_dlogp, nt, back);
+        if (back.size()) back.back().second.second = (size_t)last * sizeof(float);
+        GrpoParams p;
+        p.lo = 1.0 - eps_low;
+        p.hi = 1.0 + eps_high;
+        p.lo_f = (float)p.lo;
+        p.hi_f = (float)p.hi;
+        k_acc_reset<<<1, 1, 0, c.stream>>>(c.acc, last);
+        k_loss_grpo_packed<<<(unsigned)n_traj, 256, 0, c.stream>>>(lpn, lpo, a, o, d, p, c.acc,
+                                                                  (long long)n_traj);
+        k_dlogp_rescale<<<148, 256, 0, c.stream>>>(d, last, nullptr, c.acc);
+        RB_CUDA(cudaGetLastError());
+        c.stats(stats, 0, 0.0, back);
+        c.finish(back);
+    });
+}
+
+int rb_grpo_records(const double* logp_now, const double* behavior_logprob, const double* adv,
+                    size_t n, double eps_low, double eps_high, double* out_dlogp,
+                    rb_loss_stats* stats) {
+    return guard([&] {
+        if (eps_low < 0.0 || eps_high < 0.0) invalid("loss spec: clip bounds must be >= 0");
+        if (!std::isfinite(eps_low) || !std::isfinite(eps_high))
+            invalid("loss spec: parameters must be finite");
+        if (n == 0) invalid("loss gradient needs a non-empty batch");
+        Ctx& c = ctx();
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.init();
+        std::vector<std::pair<void*, std::pair<void*, size_t>>> back;
+        const double* lpn = c.in(logp_now, n);
+        const double* blp = c.in(behavior_logprob, n);
+        const double* a = c.in(adv, n);
+        double* d = c.out(out_dlogp, n, back);
+        k_acc_reset<<<1, 1, 0, c.stream>>>(c.acc, (long long)n);
+        const unsigned g = grid_for((long long)n);
+        k_grpo_records<<<g, 256, 0, c.stream>>>(lpn, blp, a, (long long)n, 1.0 - eps_low,
+                                                1.0 + eps_high, d, c.acc);
+        k_scale_records<<<g, 256, 0, c.stream>>>(d, (long long)n, c.acc);
+        RB_CUDA(cudaGetLastError());
+        c.stats(stats, 0, 0.0, back);
+        c.finish(back);
+    });
+}
+
+int rb_asymre_tokens(const float* logp_now, const double* reward, const double* group_mean,
+                     const int64_t* offsets, size_t n_traj, double delta_v, float* out_dlogp,
+                     rb_loss_stats* stats) {
+    return guard([&] {
+        if (!std::isfinite(delta_v)) invalid("loss spec: parameters must be finite");
+        if (n_traj == 0) invalid("loss gradient needs a non-empty batch");
+        Ctx& c = ctx();
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.init();
+        int64_t last = 0;
+        if (is_device_ptr(offsets))
+            RB_CUDA(cudaMemcpy(&last, offsets + n_traj, 8, cudaMemcpyDeviceToHost));
+        else
+            last = offsets[n_traj];
+        std::vector<std::pair<void*, std::pair<void*, size_t>>> back;
+        const float* lpn = c.in(logp_now, (size_t)last);
+        const double* r = c.in(reward, n_traj);
+        const double* gm = c.in(group_mean, n_traj);
+        const int64_t* o = c.in(offsets, n_traj + 1);
+        float* d = c.out(out_dlogp, (size_t)last, back);
+        const double inv_b = 1.0 / (double)n_traj;
+        k_acc_reset<<<1, 1, 0, c.stream>>>(c.acc, last);
+        k_loss_asymre_packed<<<(unsigned)n_traj, 256, 0, c.stream>>>(lpn, r, gm, o, d, delta_v,
+                                                                    inv_b, c.acc);
+        RB_CUDA(cudaGetLastError());
+        c.stats(stats, 1, inv_b, back);
+        c.finish(back);
+    });
+}
+
+int rb_asymre_records(const double* logp_now, const double* reward, const double* group_mean,
+                      size_t n, double delta_v, double* out_dlogp, rb_loss_stats* stats) {
+    return guard([&] {
+        if (!std::isfinite(delta_v)) invalid("loss spec: parameters must be finite");
+        if (n == 0) invalid("loss gradient needs a non-empty batch");
+        Ctx& c = ctx();
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.init();
+        std::vector<std::pair<void*, std::pair<void*, size_t>>> back;
+        const double* lpn = c.in(logp_now, n);
+        const double* r = c.in(reward, n);
+        const double* gm = c.in(group_mean, n);
+        double* d = c.out(out_dlogp, n, back);
+        k_acc_reset<<<1, 1, 0, c.stream>>>(c.acc, (long long)n);
+        k_asymre_records<<<grid_for((long long)n), 256, 0, c.stream>>>(lpn, r, gm, (long long)n,
+                                                                       delta_v, d, c.acc);
+        RB_CUDA(cudaGetLastError());
+        c.stats(stats, 1, 1.0 / (double)n, back);
+        c.finish(back);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,268 @@
+// rng.cu — replab::Rng (rng.hpp:22-69, rng.cpp) reproduced bit-exactly.
+//
+// The MT19937-64 state has one authoritative home at a time: the GPU while
+// the sampler consumes it (the hot path never copies it back), the host when
+// a caller asks for a host-side draw (test code that interleaves
+// rng.uniform01() with buffer.sample(), as the reference's own tests do).
+// Migration is a 2.5 KB copy on the owning stream.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "rng_internal.cuh"
+
+namespace rb {
+
+static thread_local std::string g_err;
+void set_last_error(const std::string& msg) { g_err = msg; }
+
+void require_device() {
+    static int ok = -1;
+    if (ok < 0) {
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        ok = (e == cudaSuccess && n > 0) ? 1 : 0;
+        if (ok) {
+            int dev = 0, major = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+            if (major < 10) ok = 2;
+        }
+    }
+    if (ok == 0) throw Error(RB_ECUDA, "libreplay_b200: no CUDA device available (no CPU fallback)");
+    if (ok == 2) throw Error(RB_ECUDA, "libreplay_b200: built for sm_100a; device is older");
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool is_pinned_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// rng.cpp:8-15
+uint64_t hash_name(const char* name) {
+    uint64_t h = 1469598103934665603ULL;
+    for (const unsigned char* c = (const unsigned char*)name; *c; ++c) {
+        h ^= *c;
+        h *= 1099511628211ULL;
+    }
+    return h;
+}
+// rng.cpp:17-23
+static uint64_t splitmix64(uint64_t& state) {
+    state += 0x9e3779b97f4a7c15ULL;
+    uint64_t z = state;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+}  // namespace rb
+
+using namespace rb;
+
+static void mt_seed(MtState& s, uint64_t seed) {  // [rand.predef] seeding
+    s.mt[0] = seed;
+    for (int i = 1; i < MT_N; ++i) s.mt[i] = 6364136223846793005ULL * (s.mt[i - 1] ^ (s.mt[i - 1] >> 62)) + i;
+    s.idx = MT_N;  // libstdc++ twists lazily on the first draw
+    s.pad = 0;
+    s.draws = 0;
+}
+
+rb_rng::rb_rng(uint64_t seed_) : seed(seed_) {
+    mt_seed(host, seed_);
+    where = 0;
+}
+rb_rng::~rb_rng() {
+    if (dev) cudaFree(dev);
+}
+
+void rb_rng::to_host() {
+    if (where == 0) return;
+    RB_CUDA(cudaStreamSynchronize(stream));
+    RB_CUDA(cudaMemcpy(&host, dev, sizeof(MtState), cudaMemcpyDeviceToHost));
+    where = 0;
+}
+
+MtState* rb_rng::to_device(cudaStream_t s) {
+    require_device();
+    if (!dev) RB_CUDA(cudaMalloc(&dev, sizeof(MtState)));
+    if (where == 0) {
+        RB_CUDA(cudaMemcpyAsync(dev, &host, sizeof(MtState), cudaMemcpyHostToDevice, s));
+        // host copy must stay alive until the copy completes
+        RB_CUDA(cudaStreamSynchronize(s));
+    } else if (s != stream) {
+        // order after the previous user of the device state
+        cudaEvent_t ev;
+        RB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        RB_CUDA(cudaEventRecord(ev, stream));
+        RB_CUDA(cudaStreamWaitEvent(s, ev, 0));
+        RB_CUDA(cudaEventDestroy(ev));
+    }
+    where = 1;
+    stream = s;
+    return dev;
+}
+
+uint64_t rb_rng::next() {
+    to_host();
+    return mt_next_scalar(host.mt, &host.idx, &host.draws);
+}
+
+// ---- device bulk generator (parity aid for the sampler's stream) -------
+__global__ void __launch_bounds__(320) k_mt_fill(MtState* st, uint64_t n, uint64_t* out) {
+    __shared__ uint64_t mt[MT_N];
+    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = st->mt[i];
+    uint32_t idx = st->idx;
+    __syncthreads();
+    uint64_t pos = 0;
+    while (pos < n) {
+        if (idx >= MT_N) {
+            mt_twist_block(mt);
+            idx = 0;
+        }
+        const uint64_t avail = (uint64_t)(MT_N - idx);
+        const uint64_t take = avail < n - pos ? avail : n - pos;
+        if (threadIdx.x < take) out[pos + threadIdx.x] = mt_temper(mt[idx + threadIdx.x]);
+        idx += (uint32_t)take;
+        pos += take;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) st->mt[i] = mt[i];
+    if (threadIdx.x == 0) {
+        st->idx = idx;
+        st->draws += n;
+    }
+}
+
+extern "C" {
+
+const char* rb_last_error(void) { return rb::g_err.c_str(); }
+
+uint64_t rb_hash_name(const char* name) { return hash_name(name); }
+
+int rb_rng_create(uint64_t seed, rb_rng** out) {
+    return guard([&] { *out = new rb_rng(seed); });
+}
+
+int rb_rng_stream(const rb_rng* p, const char* name, rb_rng** out) {
+    return guard([&] {  // rng.cpp:27-30
+        uint64_t state = p->seed ^ hash_name(name);
+        *out = new rb_rng(splitmix64(state));
+    });
+}
+
+int rb_rng_stream_index(const rb_rng* p, const char* name, uint64_t index, rb_rng** out) {
+    return guard([&] {  // rng.cpp:32-36
+        uint64_t state = p->seed ^ hash_name(name);
+        state = splitmix64(state) ^ (index * 0x9e3779b97f4a7c15ULL);
+        *out = new rb_rng(splitmix64(state));
+    });
+}
+
+int rb_rng_clone(const rb_rng* r, rb_rng** out) {
+    return guard([&] {
+        rb_rng* c = new rb_rng(r->seed);
+        const_cast<rb_rng*>(r)->to_host();
+        c->host = r->host;
+        *out = c;
+    });
+}
+
+void rb_rng_destroy(rb_rng* r) {
+    if (r && r->where == 1) cudaStreamSynchronize(r->stream);
+    delete r;
+}
+
+uint64_t rb_rng_seed(const rb_rng* r) { return r->seed; }
+
+uint64_t rb_rng_draws(const rb_rng* r) {
+    const_cast<rb_rng*>(r)->to_host();
+    return r->host.draws;
+}
+
+int rb_rng_next_u64(rb_rng* r, uint64_t* out) {
+    return guard([&] { *out = r->next(); });
+}
+
+int rb_rng_below(rb_rng* r, uint64_t bound, uint64_t* out) {
+    return guard([&] {  // rng.cpp:40-51
+        if (bound == 0) invalid("Rng::below: bound must be positive");
+        const uint64_t limit = below_limit(bound);
+        uint64_t v;
+        do {
+            v = r->next();
+        } while (v >= limit);
+        *out = v % bound;
+    });
+}
+
+int rb_rng_uniform01(rb_rng* r, double* out) {
+    return guard([&] { *out = static_cast<double>(r->next() >> 11) * 0x1.0p-53; });
+}
+
+int rb_rng_normal(rb_rng* r, double* out) {
+    return guard([&] {  // rng.cpp:59-70
+        for (;;) {
+            const double u = 2.0 * (static_cast<double>(r->next() >> 11) * 0x1.0p-53) - 1.0;
+            const double v = 2.0 * (static_cast<double>(r->next() >> 11) * 0x1.0p-53) - 1.0;
+            const double s = u * u + v * v;
+            if (s > 0.0 && s < 1.0) {
+                *out = u * std::sqrt(-2.0 * std::log(s) / s);
+                return;
+            }
+        }
+    });
+}
+
+int rb_rng_sample_without_replacement(rb_rng* r, uint64_t n, uint64_t k, uint64_t* out) {
+    return guard([&] {  // rng.cpp:108-121
+        if (k > n) invalid("Rng::sample_without_replacement: k exceeds population");
+        std::vector<uint64_t> idx(n);
+        for (uint64_t i = 0; i < n; ++i) idx[i] = i;
+        for (uint64_t i = 0; i < k; ++i) {
+            const uint64_t bound = n - i, limit = below_limit(bound);
+            uint64_t v;
+            do {
+                v = r->next();
+            } while (v >= limit);
+            std::swap(idx[i], idx[i + v % bound]);
+        }
+        std::memcpy(out, idx.data(), k * sizeof(uint64_t));
+    });
+}
+
+int rb_rng_fill_u64(rb_rng* r, uint64_t n, uint64_t* out) {
+    return guard([&] {
+        require_device();
+        cudaStream_t s = r->stream;
+        MtState* st = r->to_device(s);
+        uint64_t* d = out;
+        const bool dev_out = is_device_ptr(out);
+        if (!dev_out) RB_CUDA(cudaMallocAsync((void**)&d, n * sizeof(uint64_t) + 8, s));
+        k_mt_fill<<<1, 320, 0, s>>>(st, n, d);
+        RB_CUDA(cudaGetLastError());
+        if (!dev_out) {
+            RB_CUDA(cudaMemcpyAsync(out, d, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+            RB_CUDA(cudaFreeAsync(d, s));
+            RB_CUDA(cudaStreamSynchronize(s));
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,29 @@
+// rng_internal.cuh — the rb_rng object behind the C handle.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+struct rb_rng {
+    explicit rb_rng(uint64_t seed);
+    ~rb_rng();
+    rb_rng(const rb_rng&) = delete;
+    rb_rng& operator=(const rb_rng&) = delete;
+
+    // Make the host copy authoritative (synchronises the owning stream).
+    void to_host();
+    // Make the device copy authoritative for kernels on stream `s`.
+    rb::MtState* to_device(cudaStream_t s);
+    uint64_t next();  // host draw (rng.cpp:38)
+
+    uint64_t seed;
+    rb::MtState host{};
+    rb::MtState* dev = nullptr;
+    int where = 0;  // 0 = host authoritative, 1 = device authoritative
+    cudaStream_t stream = 0;
+};
+
+namespace rb {
+uint64_t hash_name(const char* name);
+}

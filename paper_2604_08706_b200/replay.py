@@ -1,0 +1,438 @@
+"""Python mirror of the reference's replay-path API over the C-ABI.
+
+Names, argument meaning and error behaviour follow the reference's C++ API
+(/root/reference/proj/include/replab): ``Rng`` (rng.hpp:22-69),
+``ShardedReplayBuffer`` (replay_buffer.hpp:57-108), ``group_advantages``
+(bandit.hpp:106) and the two losses (bandit.hpp:133-139, token-level form).
+Invalid arguments raise ValueError (the reference's std::invalid_argument).
+
+Arrays may be numpy (host) or torch tensors (host or CUDA); device tensors
+stay on the device (the hot path), host arrays are staged by the library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from ._lib import (RB_INSERT_ASSUME_UNIQUE, RETENTIONS, STRATEGIES, STRATEGY_NAMES, InsertBatch,
+                   LossStats, Record, check, lib)
+
+RECORD_DTYPE = np.dtype(
+    {
+        "names": ["rollout_id", "prompt_id", "group_id", "creation_step", "policy_version",
+                  "reward", "is_correct", "behavior_logprob", "advantage", "use_count"],
+        "formats": ["<u8", "<u8", "<u8", "<i8", "<i8", "<f8", "u1", "<f8", "<f8", "<u4"],
+        "offsets": [0, 8, 16, 24, 32, 40, 48, 56, 64, 72],
+        "itemsize": 80,
+    }
+)
+EVENT_DTYPE = np.dtype([("rollout_id", "<u8"), ("creation_step", "<i8"), ("use_step", "<i8"),
+                        ("batch_id", "<i8"), ("within_batch_rank", "<i8")])
+NONE_ID = np.iinfo(np.uint64).max
+
+
+def _ptr(a) -> Optional[int]:
+    """Raw address of a numpy array or torch tensor (None passes through)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("arrays must be contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+        return a.data_ptr()
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _host(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _arr(a, dtype):
+    """Keep torch tensors (any device) as they are; coerce the rest to numpy."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr") and not isinstance(a, np.ndarray):
+        return a
+    return _host(a, dtype)
+
+
+# ---------------------------------------------------------------------------
+class Rng:
+    """replab::Rng — MT19937-64 with named sub-streams (rng.hpp:22-69)."""
+
+    def __init__(self, seed: int = 0, _handle=None):
+        if _handle is None:
+            h = C.c_void_p()
+            check(lib.rb_rng_create(int(seed) & (2**64 - 1), C.byref(h)))
+            _handle = h
+        self._h = _handle
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.rb_rng_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stream(self, name: str, index: Optional[int] = None) -> "Rng":
+        h = C.c_void_p()
+        if index is None:
+            check(lib.rb_rng_stream(self._h, name.encode(), C.byref(h)))
+        else:
+            check(lib.rb_rng_stream_index(self._h, name.encode(), int(index), C.byref(h)))
+        return Rng(_handle=h)
+
+    def copy(self) -> "Rng":
+        h = C.c_void_p()
+        check(lib.rb_rng_clone(self._h, C.byref(h)))
+        return Rng(_handle=h)
+
+    def seed(self) -> int:
+        return lib.rb_rng_seed(self._h)
+
+    @property
+    def draws(self) -> int:
+        return lib.rb_rng_draws(self._h)
+
+    def next_u64(self) -> int:
+        v = C.c_uint64()
+        check(lib.rb_rng_next_u64(self._h, C.byref(v)))
+        return v.value
+
+    def below(self, bound: int) -> int:
+        v = C.c_uint64()
+        check(lib.rb_rng_below(self._h, int(bound), C.byref(v)))
+        return v.value
+
+    def uniform01(self) -> float:
+        v = C.c_double()
+        check(lib.rb_rng_uniform01(self._h, C.byref(v)))
+        return v.value
+
+    def normal(self) -> float:
+        v = C.c_double()
+        check(lib.rb_rng_normal(self._h, C.byref(v)))
+        return v.value
+
+    def sample_without_replacement(self, n: int, k: int) -> np.ndarray:
+        out = np.zeros(max(k, 1), np.uint64)
+        check(lib.rb_rng_sample_without_replacement(self._h, n, k, out.ctypes.data))
+        return out[:k]
+
+    def fill_u64(self, n: int, out=None):
+        """n raw engine outputs produced by the GPU generator."""
+        if out is None:
+            out = np.zeros(n, np.uint64)
+        check(lib.rb_rng_fill_u64(self._h, n, _ptr(out)))
+        return out
+
+
+def hash_name(name: str) -> int:
+    return lib.rb_hash_name(name.encode())
+
+
+# ---------------------------------------------------------------------------
+def _records_from(recs) -> np.ndarray:
+    r = np.asarray(recs, RECORD_DTYPE)
+    out = np.zeros(r.shape, RECORD_DTYPE)  # zero padding
+    for f in RECORD_DTYPE.names:
+        out[f] = r[f]
+    return out
+
+
+class ShardedReplayBuffer:
+    """replab::ShardedReplayBuffer (replay_buffer.hpp:57-108) in HBM."""
+
+    def __init__(self, num_shards: int, total_capacity: int,
+                 strategy: str = "uniform_with_replacement", retention: str = "plain_fifo",
+                 delta: float = 0.0, max_tokens: int = 0, device: int = -1,
+                 shard_range: Optional[tuple] = None, _handle=None):
+        if _handle is None:
+            if strategy not in STRATEGIES:
+                raise ValueError(f"unknown sampling strategy: '{strategy}'")
+            if retention not in RETENTIONS:
+                raise ValueError(f"unknown retention policy: '{retention}'")
+            sb, se = shard_range if shard_range else (0, 0)
+            h = C.c_void_p()
+            check(lib.rb_create(num_shards, total_capacity, STRATEGIES[strategy],
+                                RETENTIONS[retention], float(delta), int(max_tokens), int(device),
+                                sb, se, C.byref(h)))
+            _handle = h
+        self._h = _handle
+        self.max_tokens = int(max_tokens)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.rb_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- configuration (replay_buffer.hpp:74-84)
+    def _sz(self, fn, *args) -> int:
+        v = C.c_size_t()
+        check(fn(self._h, *args, C.byref(v)))
+        return v.value
+
+    def num_shards(self) -> int:
+        return self._sz(lib.rb_num_shards)
+
+    def total_capacity(self) -> int:
+        return self._sz(lib.rb_total_capacity)
+
+    def shard_capacity(self) -> int:
+        return self._sz(lib.rb_shard_capacity)
+
+    def size(self) -> int:
+        return self._sz(lib.rb_size)
+
+    def shard_size(self, shard: int) -> int:
+        return self._sz(lib.rb_shard_size, shard)
+
+    def route_cursor(self) -> int:
+        return self._sz(lib.rb_route_cursor)
+
+    def strategy(self) -> str:
+        v = C.c_int()
+        check(lib.rb_strategy(self._h, C.byref(v)))
+        return STRATEGY_NAMES[v.value]
+
+    def retention(self):
+        k, d = C.c_int(), C.c_double()
+        check(lib.rb_retention(self._h, C.byref(k), C.byref(d)))
+        return ("plain_fifo" if k.value == 0 else "positive_bias", d.value)
+
+    def set_stream(self, stream) -> None:
+        """Enqueue on an external stream (int handle, e.g. torch.cuda.current_stream().cuda_stream)."""
+        check(lib.rb_set_stream(self._h, C.c_void_p(stream)))
+
+    def stream(self) -> int:
+        return lib.rb_get_stream(self._h) or 0
+
+    # -- push / insert
+    def push(self, record, tokens=None, logp_old=None):
+        """replay_buffer.cpp:83-96 — returns the evicted record or None."""
+        rec = _records_from(np.asarray(record, RECORD_DTYPE).reshape(1))
+        ev = np.zeros(1, RECORD_DTYPE)
+        has = C.c_int(0)
+        tk = _arr(tokens, np.int32)
+        lp = _arr(logp_old, np.float32)
+        n = 0 if tk is None and lp is None else int((tk if tk is not None else lp).shape[0])
+        check(lib.rb_push(self._h, rec.ctypes.data, _ptr(tk), _ptr(lp), n, ev.ctypes.data,
+                          C.byref(has)))
+        return ev[0] if has.value else None
+
+    def insert(self, *, rollout_id, reward, prompt_id=None, group_id=None, creation_step=None,
+               policy_version=None, is_correct=None, behavior_logprob=None, advantage=None,
+               group_mean=None, group_offsets=None, tok_offsets=None, tokens=None,
+               logp_old=None, evicted=None, assume_unique: bool = False) -> int:
+        """Batched push of n trajectories (rb_insert).  Returns the number applied."""
+        keep = []
+
+        def a(x, dt):
+            y = _arr(x, dt)
+            keep.append(y)
+            return _ptr(y)
+
+        rid = _arr(rollout_id, np.uint64)
+        keep.append(rid)
+        n = int(rid.shape[0])
+        bt = InsertBatch()
+        bt.n = n
+        bt.rollout_id = _ptr(rid)
+        bt.prompt_id = a(prompt_id, np.uint64)
+        bt.group_id = a(group_id, np.uint64)
+        bt.creation_step = a(creation_step, np.int64)
+        bt.policy_version = a(policy_version, np.int64)
+        bt.reward = a(reward, np.float64)
+        bt.is_correct = a(is_correct, np.uint8)
+        bt.behavior_logprob = a(behavior_logprob, np.float64)
+        bt.advantage = a(advantage, np.float64)
+        bt.group_mean = a(group_mean, np.float64)
+        go = _arr(group_offsets, np.int64)
+        keep.append(go)
+        bt.group_offsets = _ptr(go)
+        bt.n_groups = 0 if go is None else int(go.shape[0]) - 1
+        bt.tok_offsets = a(tok_offsets, np.int64)
+        bt.tokens = a(tokens, np.int32)
+        bt.logp_old = a(logp_old, np.float32)
+        applied = C.c_size_t(0)
+        ev = _arr(evicted, np.uint64)
+        flags = RB_INSERT_ASSUME_UNIQUE if assume_unique else 0
+        check(lib.rb_insert(self._h, C.byref(bt), _ptr(ev), C.byref(applied), flags))
+        return applied.value
+
+    # -- sample / gather / loss
+    def sample(self, batch_size: int, rng: Rng, ledger: bool = False, batch_id: int = 0,
+               use_step: int = 0, with_index: bool = False):
+        """replay_buffer.cpp:184-217 — record copies in shard-major draw order."""
+        out = np.zeros(batch_size, RECORD_DTYPE)
+        ev = np.zeros(batch_size, EVENT_DTYPE) if ledger else None
+        sh = np.zeros(batch_size, np.int64) if with_index else None
+        ix = np.zeros(batch_size, np.int64) if with_index else None
+        check(lib.rb_sample(self._h, batch_size, rng.handle, out.ctypes.data, _ptr(sh), _ptr(ix),
+                            _ptr(ev), batch_id, use_step))
+        res = [out]
+        if ledger:
+            res.append(ev)
+        if with_index:
+            res += [sh, ix]
+        return res[0] if len(res) == 1 else tuple(res)
+
+    def sample_device(self, batch_size: int, rng: Rng) -> None:
+        """Hot path: select a batch, keep it on the device (no host outputs)."""
+        check(lib.rb_sample(self._h, batch_size, rng.handle, None, None, None, None, 0, 0))
+
+    def batch_size(self) -> int:
+        return self._sz(lib.rb_batch_size)
+
+    def batch_total_tokens(self) -> int:
+        v = C.c_int64()
+        check(lib.rb_batch_total_tokens(self._h, C.byref(v)))
+        return v.value
+
+    def batch_ids(self):
+        n = self.batch_size() // max(1, self.num_shards()) * self.num_shards()
+        ids = np.zeros(max(n, 1), np.uint64)
+        lens = np.zeros(max(n, 1), np.int32)
+        off = np.zeros(n + 1, np.int64)
+        check(lib.rb_batch_ids(self._h, ids.ctypes.data, lens.ctypes.data, off.ctypes.data))
+        return ids[:n], lens[:n], off
+
+    def gather(self, out_tokens=None, out_logp_old=None, out_offsets=None) -> None:
+        check(lib.rb_gather(self._h, _ptr(out_tokens), _ptr(out_logp_old), _ptr(out_offsets)))
+
+    @staticmethod
+    def _stats_arg(stats):
+        """True -> host LossStats (synchronous); None/False -> no stats;
+        a 40-byte device tensor -> device rb_loss_stats (asynchronous)."""
+        if stats is True:
+            st = LossStats()
+            return st, C.byref(st)
+        if stats is None or stats is False:
+            return None, None
+        return stats, _ptr(stats)
+
+    def loss_grpo(self, logp_now, out_dlogp, eps_low=0.2, eps_high=0.2, norm_tokens=0,
+                  stats=True):
+        st, p = self._stats_arg(stats)
+        check(lib.rb_loss_grpo(self._h, _ptr(logp_now), _ptr(out_dlogp), eps_low, eps_high,
+                               int(norm_tokens), p))
+        return st
+
+    def loss_asymre(self, logp_now, out_dlogp, delta_v=-0.1, norm_batch=0, stats=True):
+        st, p = self._stats_arg(stats)
+        check(lib.rb_loss_asymre(self._h, _ptr(logp_now), _ptr(out_dlogp), delta_v,
+                                 int(norm_batch), p))
+        return st
+
+    def loss_finalize(self, dlogp, stats):
+        """Re-normalise after a cross-rank reduction of `stats` (LossStats or device tensor)."""
+        p = C.byref(stats) if isinstance(stats, LossStats) else _ptr(stats)
+        check(lib.rb_loss_finalize(self._h, _ptr(dlogp), p))
+        return stats
+
+    def batch_ids_device(self, out_ids, out_lengths=None, out_offsets=None) -> None:
+        """Per-selection ids / lengths / packed offsets into device arrays (no sync)."""
+        check(lib.rb_batch_ids(self._h, _ptr(out_ids), _ptr(out_lengths), _ptr(out_offsets)))
+
+    # -- inspection / persistence
+    def shard_contents(self, shard: int) -> np.ndarray:
+        cap = self.shard_capacity()
+        out = np.zeros(cap + 1, RECORD_DTYPE)
+        cnt = C.c_size_t()
+        check(lib.rb_shard_contents(self._h, shard, out.ctypes.data, cap + 1, C.byref(cnt)))
+        return out[: cnt.value]
+
+    def record_tokens(self, shard: int, index: int):
+        cap = max(self.max_tokens, 1)
+        tk = np.zeros(cap, np.int32)
+        lp = np.zeros(cap, np.float32)
+        n = C.c_int32()
+        check(lib.rb_record_tokens(self._h, shard, index, tk.ctypes.data, lp.ctypes.data, cap,
+                                   C.byref(n)))
+        return tk[: n.value], lp[: n.value]
+
+    def dump(self) -> str:
+        n = C.c_size_t()
+        check(lib.rb_dump(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib.rb_dump(self._h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+    @staticmethod
+    def load(text: str, max_tokens: int = 0, device: int = -1) -> "ShardedReplayBuffer":
+        h = C.c_void_p()
+        check(lib.rb_load(text.encode(), int(max_tokens), int(device), C.byref(h)))
+        return ShardedReplayBuffer(0, 0, _handle=h, max_tokens=max_tokens)
+
+    def check(self) -> None:
+        check(lib.rb_check(self._h))
+
+    def synchronize(self) -> None:
+        check(lib.rb_synchronize(self._h))
+
+
+# ---------------------------------------------------------------------------
+def group_advantages(rewards, offsets=None, out=None, out_mean=None):
+    """bandit.cpp:276-294 (segmented when offsets are given)."""
+    r = _arr(rewards, np.float64)
+    if offsets is None:
+        offsets = np.array([0, r.shape[0]], np.int64)
+    off = _arr(offsets, np.int64)
+    if out is None:
+        out = np.zeros(r.shape[0], np.float64)
+    check(lib.rb_group_advantages(_ptr(r), _ptr(off), int(off.shape[0]) - 1, _ptr(out),
+                                  _ptr(out_mean)))
+    return out
+
+
+def grpo_tokens(logp_now, logp_old, adv, offsets, eps_low=0.2, eps_high=0.2, out=None):
+    lpn, lpo = _arr(logp_now, np.float32), _arr(logp_old, np.float32)
+    a, off = _arr(adv, np.float64), _arr(offsets, np.int64)
+    if out is None:
+        out = np.zeros(lpn.shape[0], np.float32)
+    st = LossStats()
+    check(lib.rb_grpo_tokens(_ptr(lpn), _ptr(lpo), _ptr(a), _ptr(off), int(off.shape[0]) - 1,
+                             eps_low, eps_high, _ptr(out), C.byref(st)))
+    return out, st
+
+
+def grpo_records(logp_now, behavior_logprob, adv, eps_low=0.2, eps_high=0.2, out=None):
+    lpn, blp, a = (_arr(x, np.float64) for x in (logp_now, behavior_logprob, adv))
+    if out is None:
+        out = np.zeros(lpn.shape[0], np.float64)
+    st = LossStats()
+    check(lib.rb_grpo_records(_ptr(lpn), _ptr(blp), _ptr(a), int(lpn.shape[0]), eps_low,
+                              eps_high, _ptr(out), C.byref(st)))
+    return out, st
+
+
+def asymre_tokens(logp_now, reward, group_mean, offsets, delta_v=-0.1, out=None):
+    lpn = _arr(logp_now, np.float32)
+    r, g, off = _arr(reward, np.float64), _arr(group_mean, np.float64), _arr(offsets, np.int64)
+    if out is None:
+        out = np.zeros(lpn.shape[0], np.float32)
+    st = LossStats()
+    check(lib.rb_asymre_tokens(_ptr(lpn), _ptr(r), _ptr(g), _ptr(off), int(off.shape[0]) - 1,
+                               delta_v, _ptr(out), C.byref(st)))
+    return out, st
+
+
+def asymre_records(logp_now, reward, group_mean, delta_v=-0.1, out=None):
+    lpn, r, g = (_arr(x, np.float64) for x in (logp_now, reward, group_mean))
+    if out is None:
+        out = np.zeros(lpn.shape[0], np.float64)
+    st = LossStats()
+    check(lib.rb_asymre_records(_ptr(lpn), _ptr(r), _ptr(g), int(lpn.shape[0]), delta_v,
+                                _ptr(out), C.byref(st)))
+    return out, st

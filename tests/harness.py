@@ -1,0 +1,196 @@
+"""Replay-step parity harness: the CUDA library vs the CPU oracle, step by step.
+
+Drives both through the same schedule (train()'s production/warm-up loop,
+bandit.cpp:568-691, with T shards as in simulate(), async_sim.cpp:138-139)
+on the synthetic workload of include/replay_synth.h and compares, every
+step: evicted ids per push, sampled records (ids + post-increment use
+counts, i.e. the MT19937-64 stream and arrival-order mapping), the packed
+token gather, and the GRPO / AsymRE token losses.
+
+Used by tests/test_gpu_*.py and __graft_entry__.smoke().
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from oracle.pyoracle import RECORD_DTYPE, Oracle, same_records
+
+
+@dataclass
+class StepConfig:
+    capacity: int = 64
+    shards: int = 1
+    batch: int = 32
+    group: int = 8
+    lmax: int = 64
+    ragged: bool = True
+    workers: int = 5
+    trainers: int = 3
+    mu: float = 5.28
+    strategy: str = "uniform_with_replacement"
+    retention: str = "plain_fifo"
+    delta: float = 0.0
+    seed: int = 1
+    loss: str = "grpo"
+    eps_low: float = 0.2
+    eps_high: float = 0.28
+    delta_v: float = -0.1
+    prompts: int = 16
+    device_inputs: bool = True   # torch CUDA tensors (hot path) vs numpy host arrays
+
+    @property
+    def per_step(self):
+        return self.workers * self.batch / (self.mu * self.trainers)
+
+
+class Producer:
+    """Whole groups with monotone ids; advantages left to the device."""
+
+    def __init__(self, cfg: StepConfig, ora: Oracle):
+        self.cfg, self.o = cfg, ora
+        self.next_id = 0
+        self.next_group = 0
+        self.prompt = 0
+
+    def groups(self, ngroups: int, step: int):
+        c = self.cfg
+        n = ngroups * c.group
+        ids = np.arange(self.next_id, self.next_id + n, dtype=np.uint64)
+        reward, length, blp = self.o.synth_meta(c.seed, ids, c.lmax, c.ragged)
+        gid = np.repeat(np.arange(self.next_group, self.next_group + ngroups), c.group).astype(np.uint64)
+        prompt = (self.prompt + np.repeat(np.arange(ngroups), c.group)) % c.prompts
+        adv = np.zeros(n)
+        gmean = np.zeros(n)
+        for g in range(ngroups):
+            sl = slice(g * c.group, (g + 1) * c.group)
+            adv[sl] = self.o.group_advantages(reward[sl])
+            m = 0.0
+            for r in reward[sl]:
+                m += float(r)
+            gmean[sl] = m / c.group
+        rec = np.zeros(n, RECORD_DTYPE)
+        rec["rollout_id"] = ids
+        rec["prompt_id"] = prompt
+        rec["group_id"] = gid
+        rec["creation_step"] = step
+        rec["policy_version"] = step
+        rec["reward"] = reward
+        rec["is_correct"] = reward == 1.0
+        rec["behavior_logprob"] = blp
+        rec["advantage"] = adv
+        tok, lpo, toff = self.o.synth_payload(c.seed, ids, length)
+        self.next_id += n
+        self.next_group += ngroups
+        self.prompt = (self.prompt + ngroups) % c.prompts
+        return rec, length, tok, lpo, toff, gmean
+
+
+def _to(x, dev):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev) if dev else x
+
+
+def insert_groups(buf, rec, toff, tok, lpo, group, dev):
+    n = rec.shape[0]
+    goff = np.arange(0, n + 1, group, dtype=np.int64)
+    ev = np.zeros(n, np.uint64)
+    buf.insert(rollout_id=_to(rec["rollout_id"].copy(), dev), prompt_id=_to(rec["prompt_id"].copy(), dev),
+               group_id=_to(rec["group_id"].copy(), dev),
+               creation_step=_to(rec["creation_step"].copy(), dev),
+               policy_version=_to(rec["policy_version"].copy(), dev),
+               reward=_to(rec["reward"].copy(), dev),
+               behavior_logprob=_to(rec["behavior_logprob"].copy(), dev),
+               group_offsets=_to(goff, dev), tok_offsets=_to(toff, dev), tokens=_to(tok, dev),
+               logp_old=_to(lpo, dev), evicted=ev)
+    return ev
+
+
+def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, check_every: int = 1):
+    """Returns a dict of per-check counters; raises AssertionError on mismatch."""
+    import torch
+
+    from paper_2604_08706_b200 import Rng, ShardedReplayBuffer
+
+    ora = ora or Oracle()
+    dev = "cuda:0" if cfg.device_inputs else None
+    gbuf = ShardedReplayBuffer(cfg.shards, cfg.capacity, cfg.strategy, cfg.retention, cfg.delta,
+                               max_tokens=cfg.lmax)
+    obuf = ora.buffer(cfg.shards, cfg.capacity, cfg.strategy, cfg.retention, cfg.delta)
+    grng = Rng(cfg.seed).stream("buffer_sampling")
+    orng = ora.rng(cfg.seed).stream("buffer_sampling")
+    prod = Producer(cfg, ora)
+    lengths, gmeans = {}, {}
+    counts = {"pushes": 0, "evictions": 0, "samples": 0, "tokens": 0, "excluded": 0}
+
+    def push_groups(ngroups, step):
+        rec, length, tok, lpo, toff, gmean = prod.groups(ngroups, step)
+        for i, r in enumerate(rec):
+            lengths[int(r["rollout_id"])] = int(length[i])
+            gmeans[int(r["rollout_id"])] = gmean[i]
+        ev = insert_groups(gbuf, rec, toff, tok, lpo, cfg.group, dev)
+        for i, r in enumerate(rec):
+            e = obuf.push(r)
+            want = np.uint64(np.iinfo(np.uint64).max) if e is None else e["rollout_id"]
+            assert ev[i] == want, f"eviction mismatch at push {counts['pushes']}: {ev[i]} vs {want}"
+            counts["pushes"] += 1
+            counts["evictions"] += e is not None
+
+    while obuf.size() < cfg.capacity:
+        push_groups(1, 0)
+    debt = 0.0
+    for step in range(steps):
+        debt += cfg.per_step
+        ng = 0
+        while debt >= float(cfg.group):
+            ng += 1
+            debt -= float(cfg.group)
+        if ng:
+            push_groups(ng, step)
+        grec, gsh, gix = gbuf.sample(cfg.batch, grng, with_index=True)
+        orec, osh, oix = obuf.sample(cfg.batch, orng)
+        assert np.array_equal(gsh, osh) and np.array_equal(gix, oix), f"sample index mismatch step {step}"
+        assert same_records(grec, orec), f"sampled records mismatch step {step}"
+        counts["samples"] += cfg.batch
+        if step % check_every:
+            continue
+        # ---- gather
+        ids = orec["rollout_id"]
+        lens = np.array([lengths[int(i)] for i in ids], np.int64)
+        off = np.zeros(len(ids) + 1, np.int64)
+        np.cumsum(lens, out=off[1:])
+        tot = int(off[-1])
+        tok_want, lpo_want, _ = ora.synth_payload(cfg.seed, ids, lens)
+        pad = (tot + 3) // 4 * 4 + 4
+        gt = torch.zeros(pad, dtype=torch.int32, device="cuda:0")
+        gl = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
+        go = torch.zeros(len(ids) + 1, dtype=torch.int64, device="cuda:0")
+        gbuf.gather(gt, gl, go)
+        assert np.array_equal(go.cpu().numpy(), off), "packed offsets mismatch"
+        assert np.array_equal(gt[:tot].cpu().numpy(), tok_want), f"gathered tokens mismatch step {step}"
+        assert np.array_equal(gl[:tot].cpu().numpy(), lpo_want), f"gathered logp_old mismatch step {step}"
+        counts["tokens"] += tot
+        # ---- loss
+        lpn = ora.synth_logp_now(cfg.seed, step + 1, ids, off)
+        if step % 5 == 3 and tot > 2:  # exercise exclusion (non-finite ratio)
+            lpn[1] = np.float32(np.inf)
+        lpn_d = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
+        lpn_d[:tot] = torch.from_numpy(lpn)
+        dl = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
+        if cfg.loss == "grpo":
+            st = gbuf.loss_grpo(lpn_d, dl, cfg.eps_low, cfg.eps_high)
+            d_want, obj, inc, exc = ora.loss_grpo_tokens(lpn, lpo_want, orec["advantage"], off,
+                                                         cfg.eps_low, cfg.eps_high)
+            assert (st.included, st.excluded) == (inc, exc), (st.included, st.excluded, inc, exc)
+            counts["excluded"] += exc
+        else:
+            st = gbuf.loss_asymre(lpn_d, dl, cfg.delta_v)
+            gm = np.array([gmeans[int(i)] for i in ids])
+            d_want, obj = ora.loss_asymre_tokens(lpn, orec["reward"], gm, off, cfg.delta_v)
+        got = dl[:tot].cpu().numpy()
+        np.testing.assert_allclose(got, d_want, rtol=1e-5, atol=1e-12,
+                                   err_msg=f"dlogp mismatch step {step}")
+        assert abs(st.objective - obj) <= 1e-5 * max(1.0, abs(obj)), (st.objective, obj)
+    return counts
