@@ -522,9 +522,11 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    res, buf, wl, rng = run_ours(args, rank, world, dist)
-    if not args.no_e2e:
-        res["e2e"] = run_e2e(args, buf, wl, rng, cfg)
+    stream = torch.cuda.Stream()  # a real stream handle (not the legacy default)
+    with torch.cuda.stream(stream):
+        res, buf, wl, rng = run_ours(args, rank, world, dist)
+        if not args.no_e2e:
+            res["e2e"] = run_e2e(args, buf, wl, rng, cfg)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             r = cpu_reference(cfg, args.cpu_steps, 1)

@@ -120,7 +120,8 @@ int rb_create(size_t num_shards, size_t total_capacity, int strategy, int retent
               double delta, int32_t max_tokens, int device, size_t shard_begin,
               size_t shard_end, rb_buffer** out);
 void rb_destroy(rb_buffer* b);
-/* Use an external CUDA stream (cudaStream_t as void*); NULL = library stream. */
+/* Enqueue on the given CUDA stream (cudaStream_t as void*; NULL = the legacy
+ * default stream).  Buffers start on a library-owned non-blocking stream. */
 int rb_set_stream(rb_buffer* b, void* stream);
 void* rb_get_stream(rb_buffer* b);
 

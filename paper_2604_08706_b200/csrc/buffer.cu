@@ -1051,7 +1051,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         v.tok = rows ? dalloc<int32_t>(rows) : nullptr;
         v.lpo = rows ? dalloc<float>(rows) : nullptr;
         unsigned long long hc = 64;
-        while (hc < 4ULL * N + 64) hc <<= 1;
+        while (hc < 4ULL * N + 131072) hc <<= 1;  // batches up to hc/4 per kernel
         v.hcap = hc;
         v.hkeys = dalloc<uint64_t>(hc);
         v.hstate = dalloc<uint32_t>(hc);
@@ -1139,13 +1139,9 @@ int rb_set_stream(rb_buffer* b, void* stream) {
         DeviceScope ds(b->device);
         b->sync();
         if (b->own_stream && b->stream) cudaStreamDestroy(b->stream);
-        if (stream) {
-            b->stream = (cudaStream_t)stream;
-            b->own_stream = false;
-        } else {
-            RB_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
-            b->own_stream = true;
-        }
+        // Any handle is taken as given; NULL is the legacy default stream.
+        b->stream = (cudaStream_t)stream;
+        b->own_stream = false;
     });
 }
 void* rb_get_stream(rb_buffer* b) { return (void*)b->stream; }
@@ -1389,6 +1385,7 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 k_sample_without<<<1, 32, 0, b->stream>>>(b->v, st, a, b->strategy, scr);
             }
             RB_CUDA(cudaGetLastError());
+            rng->used_on(b->stream);
         }
         const long long lo = (long long)std::min(b->sb * per, nsel);
         const long long hi = (long long)std::min(b->se * per, nsel);

@@ -89,35 +89,42 @@ rb_rng::rb_rng(uint64_t seed_) : seed(seed_) {
     where = 0;
 }
 rb_rng::~rb_rng() {
+    if (done) {
+        cudaEventSynchronize(done);
+        cudaEventDestroy(done);
+    }
     if (dev) cudaFree(dev);
 }
 
 void rb_rng::to_host() {
     if (where == 0) return;
-    RB_CUDA(cudaStreamSynchronize(stream));
+    if (done) RB_CUDA(cudaEventSynchronize(done));
     RB_CUDA(cudaMemcpy(&host, dev, sizeof(MtState), cudaMemcpyDeviceToHost));
     where = 0;
 }
 
 MtState* rb_rng::to_device(cudaStream_t s) {
     require_device();
-    if (!dev) RB_CUDA(cudaMalloc(&dev, sizeof(MtState)));
+    if (!dev) {
+        RB_CUDA(cudaMalloc(&dev, sizeof(MtState)));
+        RB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        RB_CUDA(cudaGetDevice(&device));
+    }
     if (where == 0) {
+        // the previous device user must be finished before we overwrite
+        RB_CUDA(cudaEventSynchronize(done));
         RB_CUDA(cudaMemcpyAsync(dev, &host, sizeof(MtState), cudaMemcpyHostToDevice, s));
         // host copy must stay alive until the copy completes
         RB_CUDA(cudaStreamSynchronize(s));
-    } else if (s != stream) {
-        // order after the previous user of the device state
-        cudaEvent_t ev;
-        RB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        RB_CUDA(cudaEventRecord(ev, stream));
-        RB_CUDA(cudaStreamWaitEvent(s, ev, 0));
-        RB_CUDA(cudaEventDestroy(ev));
+    } else {
+        // order after the previous user of the device state (any stream)
+        RB_CUDA(cudaStreamWaitEvent(s, done, 0));
     }
     where = 1;
-    stream = s;
     return dev;
 }
+
+void rb_rng::used_on(cudaStream_t s) { RB_CUDA(cudaEventRecord(done, s)); }
 
 uint64_t rb_rng::next() {
     to_host();
@@ -184,10 +191,7 @@ int rb_rng_clone(const rb_rng* r, rb_rng** out) {
     });
 }
 
-void rb_rng_destroy(rb_rng* r) {
-    if (r && r->where == 1) cudaStreamSynchronize(r->stream);
-    delete r;
-}
+void rb_rng_destroy(rb_rng* r) { delete r; }
 
 uint64_t rb_rng_seed(const rb_rng* r) { return r->seed; }
 
@@ -250,13 +254,14 @@ int rb_rng_sample_without_replacement(rb_rng* r, uint64_t n, uint64_t k, uint64_
 int rb_rng_fill_u64(rb_rng* r, uint64_t n, uint64_t* out) {
     return guard([&] {
         require_device();
-        cudaStream_t s = r->stream;
+        cudaStream_t s = 0;  // legacy default stream
         MtState* st = r->to_device(s);
         uint64_t* d = out;
         const bool dev_out = is_device_ptr(out);
         if (!dev_out) RB_CUDA(cudaMallocAsync((void**)&d, n * sizeof(uint64_t) + 8, s));
         k_mt_fill<<<1, 320, 0, s>>>(st, n, d);
         RB_CUDA(cudaGetLastError());
+        r->used_on(s);
         if (!dev_out) {
             RB_CUDA(cudaMemcpyAsync(out, d, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
             RB_CUDA(cudaFreeAsync(d, s));
