@@ -24,6 +24,7 @@
 
 #include "buffer_internal.cuh"
 #include "rng_internal.cuh"
+#include "stream_copy.cuh"
 
 using namespace rb;
 
@@ -35,14 +36,41 @@ constexpr uint64_t NONE_ID = UINT64_MAX;
 __device__ __forceinline__ int fifo_head(long long P, int C) {
     return P >= C ? (int)(P % C) : 0;
 }
+// Arrival head of shard s (FIFO: implicit ring; positive bias: explicit).
+__device__ __forceinline__ int shard_head(const BufView& v, int s) {
+    return v.retention == RB_POSITIVE_BIAS ? v.head[s] : fifo_head(v.pushes[s], v.C);
+}
+// Local slot of arrival rank i (0 = oldest) given the shard's head.
+__device__ __forceinline__ int arrival_slot_h(const BufView& v, int s, long long i, int head) {
+    long long x = head + i;
+    if (x >= v.C) x -= v.C;
+    return v.retention == RB_POSITIVE_BIAS ? v.order[(size_t)s * v.C + x] : (int)x;
+}
 __device__ __forceinline__ int arrival_slot(const BufView& v, int s, long long i) {
-    if (v.retention == RB_POSITIVE_BIAS)
-        return v.order[(size_t)s * v.C + (v.head[s] + i) % v.C];
-    return (int)((fifo_head(v.pushes[s], v.C) + i) % v.C);
+    return arrival_slot_h(v, s, i, shard_head(v, s));
 }
 __device__ __forceinline__ long long occupancy(const BufView& v, int s) {
     const long long P = v.pushes[s];
     return P < v.C ? P : v.C;
+}
+
+// Block-wide: for items [0, n) with count(i) units each, emit(i, first, count)
+// in item order; returns the total.  Items are split into contiguous
+// per-thread runs so one block scan suffices.
+template <class CountF, class EmitF>
+__device__ long long block_build_units(long long n, CountF count, EmitF emit) {
+    const long long per = (n + blockDim.x - 1) / blockDim.x;
+    const long long i0 = threadIdx.x * per, i1 = i0 + per < n ? i0 + per : n;
+    long long local = 0;
+    for (long long i = i0; i < i1; ++i) local += count(i);
+    long long total;
+    long long pos = block_exclusive_scan(local, &total);
+    for (long long i = i0; i < i1; ++i) {
+        const long long c = count(i);
+        emit(i, pos, c);
+        pos += c;
+    }
+    return total;
 }
 
 struct InsertIn {
@@ -53,12 +81,16 @@ struct InsertIn {
     const uint8_t* correct;
     const int64_t* goff;
     long long ngroups;
-    const int32_t* len;  // per-record length (may be NULL)
+    const int64_t* toff;  // n+1 payload offsets (may be NULL: length 0)
+    int32_t maxlen;
+    int32_t* len;         // scratch: per-record length
     double *adv_out, *gmean_out;
     int32_t* tslot;
     uint8_t* surv;
     uint64_t* evid;
-    rb_record* evrec;  // may be NULL
+    rb_record* evrec;     // may be NULL
+    Unit* units;          // payload copy work units (owned survivors)
+    int* n_units;
 };
 
 __device__ __forceinline__ bool in_correct(const InsertIn& in, long long j) {
@@ -248,6 +280,7 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
     const long long n = in.n;
     DevCtl* ctl = v.ctl;
     if (ctl->err_code != 0) {  // sticky error: buffer frozen until rb_check
+        if (tid == 0) *in.n_units = 0;
         for (long long j = tid; j < n; j += nt) {
             in.surv[j] = 0;
             in.tslot[j] = -1;
@@ -260,29 +293,49 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
         s_applied = n;
     }
     __syncthreads();
+    // 0. lengths from the payload offsets
+    for (long long j = tid; j < n; j += nt) {
+        long long l = in.toff ? in.toff[j + 1] - in.toff[j] : 0;
+        if (l < 0 || l > in.maxlen) {
+            s_bad = 3;
+            l = 0;
+        }
+        in.len[j] = (int32_t)l;
+    }
 
     // 1. group-relative advantages, frozen at insertion (bandit.cpp:276-294),
     //    fp64 with the reference's operation order (no FMA contraction).
     if (in.adv == nullptr) {
         if (tid == 0 && (in.goff[0] != 0 || in.goff[in.ngroups] != n)) s_bad = 1;
-        for (long long g = tid; g < in.ngroups; g += nt) {
+        // One warp per group: the rewards are fetched 32 at a time in
+        // parallel and folded in the reference's sequential order by shuffle.
+        const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+        for (long long g = w; g < in.ngroups; g += nw) {
             const long long b = in.goff[g], e = in.goff[g + 1], m = e - b;
             if (m < 2 || b < 0 || e > n) {
-                s_bad = 1;
+                if (lane == 0) s_bad = 1;
                 continue;
             }
             const double dn = (double)m;
             double mean = 0.0;
-            for (long long k = b; k < e; ++k) mean = __dadd_rn(mean, in.reward[k]);
+            for (long long c = b; c < e; c += 32) {
+                const double r = (c + lane < e) ? in.reward[c + lane] : 0.0;
+                const int cnt = (int)(e - c < 32 ? e - c : 32);
+                for (int k = 0; k < cnt; ++k) mean = __dadd_rn(mean, __shfl_sync(0xffffffffu, r, k));
+            }
             mean = __ddiv_rn(mean, dn);
             double var = 0.0;
-            for (long long k = b; k < e; ++k) {
-                const double d = __dsub_rn(in.reward[k], mean);
-                var = __dadd_rn(var, __dmul_rn(d, d));
+            for (long long c = b; c < e; c += 32) {
+                const double r = (c + lane < e) ? in.reward[c + lane] : 0.0;
+                const int cnt = (int)(e - c < 32 ? e - c : 32);
+                for (int k = 0; k < cnt; ++k) {
+                    const double d = __dsub_rn(__shfl_sync(0xffffffffu, r, k), mean);
+                    var = __dadd_rn(var, __dmul_rn(d, d));
+                }
             }
             var = __ddiv_rn(var, dn);
             const double sd = __dsqrt_rn(var);
-            for (long long k = b; k < e; ++k) {
+            for (long long k = b + lane; k < e; k += 32) {
                 in.adv_out[k] = sd < 1e-8 ? 0.0 : __ddiv_rn(__dsub_rn(in.reward[k], mean), sd);
                 in.gmean_out[k] = mean;  // bandit.cpp:316-318 (same sequential sum)
             }
@@ -297,8 +350,9 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
     if (s_bad) {
         if (tid == 0) {
             ctl->err_code = RB_EINVAL;
-            ctl->err_index = -2;
+            ctl->err_index = s_bad == 3 ? -3 : -2;
         }
+        if (tid == 0) *in.n_units = 0;
         for (long long j = tid; j < n; j += nt) {
             in.surv[j] = 0;
             in.tslot[j] = -1;
@@ -425,7 +479,37 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
             in.surv[j] = g >= 0 && v.owner[g] == (int32_t)j;
         }
     }
-    // 4. bookkeeping
+    __syncthreads();
+    // 4. payload work units: surviving records of the shards held here, in
+    //    QPU-quad pieces of their destination row.
+    if (in.toff && v.stride > 0) {
+        auto count = [&](long long j) -> long long {
+            if (!in.surv[j]) return 0;
+            const int g = in.tslot[j], s = g / v.C;
+            if (s < v.sb || s >= v.se) return 0;
+            const int nq = (in.len[j] + 3) >> 2;
+            return (nq + QPU - 1) / QPU;
+        };
+        auto emit = [&](long long j, long long first, long long c) {
+            if (!c) return;
+            const int g = in.tslot[j], s = g / v.C;
+            Unit u;
+            u.row = (s - v.sb) * v.C + (g - s * v.C);
+            u.len = in.len[j];
+            u.g = (int32_t)j;
+            u.off = in.toff[j];
+            u.adv = 0.0;
+            for (long long k = 0; k < c; ++k) {
+                u.k0 = (int32_t)(k * QPU);
+                in.units[first + k] = u;
+            }
+        };
+        const long long total = block_build_units(n, count, emit);
+        if (tid == 0) *in.n_units = (int)total;
+    } else if (tid == 0) {
+        *in.n_units = 0;
+    }
+    // 5. bookkeeping
     if (tid == 0) {
         const long long applied = s_applied;
         unsigned long long mx = ctl->has_any ? ctl->max_id : 0ULL;
@@ -438,85 +522,43 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
     }
 }
 
-// ---- 128-bit funnel shifts ------------------------------------------------
-__device__ __forceinline__ uint4 funnel(const uint4& lo, const uint4& hi, int a) {
-    switch (a & 3) {
-        case 0: return lo;
-        case 1: return make_uint4(lo.y, lo.z, lo.w, hi.x);
-        case 2: return make_uint4(lo.z, lo.w, hi.x, hi.y);
-        default: return make_uint4(lo.w, hi.x, hi.y, hi.z);
-    }
-}
-__device__ __forceinline__ uint4 shfl_up4(const uint4& q) {
-    return make_uint4(__shfl_up_sync(0xffffffffu, q.x, 1), __shfl_up_sync(0xffffffffu, q.y, 1),
-                      __shfl_up_sync(0xffffffffu, q.z, 1), __shfl_up_sync(0xffffffffu, q.w, 1));
-}
-__device__ __forceinline__ uint4 shfl_down4(const uint4& q) {
-    return make_uint4(__shfl_down_sync(0xffffffffu, q.x, 1),
-                      __shfl_down_sync(0xffffffffu, q.y, 1),
-                      __shfl_down_sync(0xffffffffu, q.z, 1),
-                      __shfl_down_sync(0xffffffffu, q.w, 1));
-}
-__device__ __forceinline__ uint32_t q_at(const uint4& q, int i) {
-    return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w;
-}
-__device__ __forceinline__ uint4 ldg_nc(const uint4* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-__device__ __forceinline__ void stg_stream(uint4* p, const uint4& q) {
-    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(q.x), "r"(q.y),
-                 "r"(q.z), "r"(q.w));
-}
-
-// Copy `len` 4-byte elements from a packed source at element offset `so`
-// (any alignment) into a 16-byte aligned row.  Whole warps iterate.
-__device__ __forceinline__ void copy_packed_to_row(const uint32_t* src, long long so,
-                                                   uint32_t* row, int len) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int a = (int)(so & 3);
-    const uint4* sq = reinterpret_cast<const uint4*>(src) + (so >> 2);
-    const long long nsq = ((so & 3) + len + 3) >> 2;  // source quads touched
-    const int nq = (len + 3) >> 2;                     // destination quads
-    uint4* dq = reinterpret_cast<uint4*>(row);
-    for (int base = wid * 32; base < nq; base += nw * 32) {
-        const int k = base + lane;
-        uint4 lo = k < nsq ? ldg_nc(sq + k) : make_uint4(0, 0, 0, 0);
-        uint4 hi = shfl_down4(lo);
-        if (lane == 31 && a && k + 1 < nsq) hi = ldg_nc(sq + k + 1);
-        if (k < nq) {
-            const uint4 o = funnel(lo, hi, a);
-            if (4 * k + 3 < len) {
-                dq[k] = o;
-            } else {
-                for (int i = 0; i < 4; ++i)
-                    if (4 * k + i < len) row[4 * k + i] = q_at(o, i);
+// ---- payload insert: persistent over the route kernel's work units -------
+// Each unit copies QPU quads of one surviving trajectory from the packed
+// inbound batch (any alignment) into its 16-byte aligned slot row, tokens and
+// logp_old interleaved so every thread keeps 2*UNIT_U 16-byte loads in flight.
+__global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, const Unit* units,
+                                                                 const int* n_units,
+                                                                 const int32_t* tokens,
+                                                                 const float* logp_old) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nu = *n_units;
+    for (int u = blockIdx.x; u < nu; u += gridDim.x) {
+        const Unit un = ld_unit(units + u);
+        const int a = (int)(un.off & 3);
+        const int nsq = (a + un.len + 3) >> 2;  // source quads touched
+        const int nq = (un.len + 3) >> 2;        // destination (row) quads
+        const int kw = un.k0 + wid * 32 * UNIT_U;
+        const size_t row = (size_t)un.row * v.stride;
+        uint4 ot[UNIT_U], ol[UNIT_U];
+        if (tokens)
+            packed_to_row_quads<UNIT_U>(reinterpret_cast<const uint4*>(tokens) + (un.off >> 2),
+                                        nsq, a, kw, ot);
+        if (logp_old)
+            packed_to_row_quads<UNIT_U>(reinterpret_cast<const uint4*>(logp_old) + (un.off >> 2),
+                                        nsq, a, kw, ol);
+#pragma unroll
+        for (int s = 0; s < UNIT_U; ++s) {
+            const int k = kw + 32 * s + lane;
+            if (k < nq) {
+                if (tokens)
+                    store_quad_masked(reinterpret_cast<uint32_t*>(v.tok + row), k, ot[s], 4 * k,
+                                      un.len);
+                if (logp_old)
+                    store_quad_masked(reinterpret_cast<uint32_t*>(v.lpo + row), k, ol[s], 4 * k,
+                                      un.len);
             }
         }
     }
-}
-
-__global__ void __launch_bounds__(256) k_insert_payload(BufView v, const uint8_t* surv,
-                                                        const int32_t* tslot,
-                                                        const int64_t* toff, const int32_t* lens,
-                                                        const int32_t* tokens,
-                                                        const float* logp_old) {
-    const long long j = blockIdx.x;
-    if (!surv[j]) return;
-    const int g = tslot[j];
-    const int s = g / v.C;
-    if (s < v.sb || s >= v.se) return;
-    const size_t row = ((size_t)(s - v.sb) * v.C + (g % v.C)) * (size_t)v.stride;
-    const int len = lens[j];
-    if (tokens)
-        copy_packed_to_row(reinterpret_cast<const uint32_t*>(tokens), toff[j],
-                           reinterpret_cast<uint32_t*>(v.tok + row), len);
-    if (logp_old)
-        copy_packed_to_row(reinterpret_cast<const uint32_t*>(logp_old), toff[j],
-                           reinterpret_cast<uint32_t*>(v.lpo + row), len);
 }
 
 // ---------------------------------------------------------------- sample
@@ -525,7 +567,27 @@ struct SampleArgs {
     long long per;      // draws per shard
     int32_t* sel_shard;
     int64_t* sel_index;
+    // map phase
+    long long nsel, lo, hi;  // selections; owned range [lo, hi)
+    int32_t* sel_slot;
+    int32_t* sel_len;
+    int64_t* off;
+    long long* totals;
+    DevLossAcc* acc;
+    Unit* units;
+    int* n_units;
 };
+
+// x % n without a 64-bit division: q from a precomputed reciprocal
+// m = floor((2^64-1)/n) underestimates floor(x/n) by at most 2.
+__device__ __forceinline__ uint64_t fast_mod(uint64_t x, uint64_t n, uint64_t m) {
+    const uint64_t q = __umul64hi(x, m);
+    uint64_t r = x - q * n;
+    while (r >= n) r -= n;
+    return r;
+}
+
+__device__ void sample_map_phase(const BufView& v, const SampleArgs& a);
 
 // uniform_with_replacement (replay_buffer.cpp:141-145): shard 0 takes its
 // `per` below(n_0) draws first, then shard 1, ...  The block generates 312
@@ -542,6 +604,7 @@ __global__ void __launch_bounds__(1024) k_sample_with(BufView v, MtState* st, Sa
     for (int s = 0; s < a.nsh; ++s) {
         const unsigned long long n = (unsigned long long)occupancy(v, s);
         const unsigned long long lim = below_limit(n);
+        const unsigned long long mag = UINT64_MAX / n;
         long long rem = a.per;
         while (rem > 0) {
             if (idx >= MT_N) {
@@ -559,7 +622,7 @@ __global__ void __launch_bounds__(1024) k_sample_with(BufView v, MtState* st, Sa
             if (!__syncthreads_or(rej)) {
                 if (threadIdx.x < take) {
                     a.sel_shard[pos + threadIdx.x] = s;
-                    a.sel_index[pos + threadIdx.x] = (int64_t)(x % n);
+                    a.sel_index[pos + threadIdx.x] = (int64_t)fast_mod(x, n, mag);
                 }
                 pos += take;
                 rem -= take;
@@ -591,6 +654,7 @@ __global__ void __launch_bounds__(1024) k_sample_with(BufView v, MtState* st, Sa
         st->idx = idx;
         st->draws += consumed;
     }
+    sample_map_phase(v, a);  // same CTA: the draws are visible after the barrier
 }
 
 __device__ __forceinline__ uint64_t mt_below_scalar(uint64_t* mt, uint32_t* idx,
@@ -660,67 +724,75 @@ __global__ void k_sample_without(BufView v, MtState* st, SampleArgs a, int strat
     st->draws = draws;
 }
 
-// arrival index -> slot, use-count increments (replay_buffer.cpp:201),
-// packed offsets over the owned selections, loss-accumulator reset.
-__global__ void __launch_bounds__(1024) k_sample_map(BufView v, long long nsel,
-                                                     const int32_t* sel_shard,
-                                                     const int64_t* sel_index, int32_t* sel_slot,
-                                                     int64_t* off, long long lo, long long hi,
-                                                     long long* totals, DevLossAcc* acc) {
-    __shared__ long long s_warp[32];
-    __shared__ long long s_carry;
+// Map phase of every sampler (block-wide): arrival index -> slot, use-count
+// increments (replay_buffer.cpp:201), per-selection lengths, packed offsets
+// over the selections of the shards held here, the gather/loss work units,
+// and the loss-accumulator reset.
+__device__ void sample_map_phase(const BufView& v, const SampleArgs& a) {
     __shared__ unsigned long long s_global;
-    if (threadIdx.x == 0) {
-        s_carry = 0;
-        s_global = 0;
-    }
+    __shared__ int s_head[64];
+    if (threadIdx.x == 0) s_global = 0;
+    const int nsh_h = a.nsh < 64 ? a.nsh : 0;  // cache shard heads when few shards
+    for (int s = threadIdx.x; s < nsh_h; s += blockDim.x) s_head[s] = shard_head(v, s);
     __syncthreads();
     unsigned long long gsum = 0;
-    for (long long i = threadIdx.x; i < nsel; i += blockDim.x) {
-        const int s = sel_shard[i];
-        const size_t g = (size_t)s * v.C + arrival_slot(v, s, sel_index[i]);
-        sel_slot[i] = (int32_t)g;
+    for (long long i = threadIdx.x; i < a.nsel; i += blockDim.x) {
+        const int s = a.sel_shard[i];
+        const int head = nsh_h ? s_head[s] : shard_head(v, s);
+        const int g = s * v.C + arrival_slot_h(v, s, a.sel_index[i], head);
+        a.sel_slot[i] = g;
         atomicAdd(&v.use[g], 1u);
-        gsum += (unsigned long long)v.len[g];
+        const int L = v.len[g];
+        a.sel_len[i] = L;
+        gsum += (unsigned long long)L;
     }
     atomicAdd(&s_global, gsum);
-    // exclusive scan of lengths over owned selections [lo, hi)
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (long long base = lo; base < hi; base += blockDim.x) {
-        const long long i = base + threadIdx.x;
-        long long x = 0;
-        if (i < hi) {
-            const int s = sel_shard[i];
-            x = v.len[(size_t)s * v.C + arrival_slot(v, s, sel_index[i])];
+    __syncthreads();
+    // exclusive scan of the owned selections' lengths -> packed offsets
+    const long long lo = a.lo, nloc = a.hi - a.lo;
+    {
+        const long long per = (nloc + blockDim.x - 1) / blockDim.x;
+        const long long i0 = threadIdx.x * per, i1 = i0 + per < nloc ? i0 + per : nloc;
+        long long local = 0;
+        for (long long i = i0; i < i1; ++i) local += a.sel_len[lo + i];
+        long long total;
+        long long pos = block_exclusive_scan(local, &total);
+        for (long long i = i0; i < i1; ++i) {
+            a.off[i] = pos;
+            pos += a.sel_len[lo + i];
         }
-        long long incl = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+        if (threadIdx.x == 0) {
+            a.off[nloc] = total;
+            a.totals[0] = total;
+            a.totals[1] = (long long)s_global;
         }
-        if (lane == 31) s_warp[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            long long w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const long long y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
-            }
-            s_warp[lane] = w;  // inclusive over warps
-        }
-        __syncthreads();
-        const long long before = s_carry + (wid ? s_warp[wid - 1] : 0);
-        if (i < hi) off[i - lo] = before + incl - x;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) s_carry = before + incl;
-        __syncthreads();
     }
+    __syncthreads();
+    // work units: QPU quads of each selection's destination quad range
+    auto count = [&](long long i) -> long long {
+        const int L = a.sel_len[lo + i];
+        if (L == 0) return 0;
+        const int nq = ((int)(a.off[i] & 3) + L + 3) >> 2;
+        return (nq + QPU - 1) / QPU;
+    };
+    auto emit = [&](long long i, long long first, long long c) {
+        if (!c) return;
+        const int g = a.sel_slot[lo + i], s = g / v.C;
+        Unit u;
+        u.row = (s - v.sb) * v.C + (g - s * v.C);
+        u.len = a.sel_len[lo + i];
+        u.g = g;
+        u.off = a.off[i];
+        u.adv = v.adv[g];
+        for (long long k = 0; k < c; ++k) {
+            u.k0 = (int32_t)(k * QPU);
+            a.units[first + k] = u;
+        }
+    };
+    const long long nu = block_build_units(nloc, count, emit);
     if (threadIdx.x == 0) {
-        off[hi - lo] = s_carry;
-        totals[0] = s_carry;
-        totals[1] = (long long)s_global;
+        *a.n_units = (int)nu;
+        DevLossAcc* acc = a.acc;
         acc->obj_sum = 0.0;
         acc->included = 0;
         acc->excluded = 0;
@@ -729,6 +801,10 @@ __global__ void __launch_bounds__(1024) k_sample_map(BufView v, long long nsel,
         acc->objective = 0.0;
         acc->need_fixup = 0;
     }
+}
+
+__global__ void __launch_bounds__(1024) k_sample_map(BufView v, SampleArgs a) {
+    sample_map_phase(v, a);
 }
 
 // Record copies with the post-increment use count in draw order
@@ -763,50 +839,40 @@ __global__ void k_sample_records(BufView v, long long nsel, long long per,
 }
 
 // ---------------------------------------------------------------- gather
-// One CTA per owned selection: tokens (and optionally logp_old) of the slot
-// row -> packed batch at off[b], 128-bit loads, funnel-shifted stores.
-__device__ __forceinline__ void copy_row_to_packed(const uint32_t* row, int len, uint32_t* dst,
-                                                   long long doff) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int a = (int)(doff & 3);
-    const uint4* sq = reinterpret_cast<const uint4*>(row);
-    const int nsq = (len + 3) >> 2;
-    const int nq = (a + len + 3) >> 2;
-    uint4* dq = reinterpret_cast<uint4*>(dst) + (doff >> 2);
-    for (int base = wid * 32; base < nq; base += nw * 32) {
-        const int k = base + lane;
-        const uint4 cur = k < nsq ? ldg_nc(sq + k) : make_uint4(0, 0, 0, 0);
-        uint4 prev = shfl_up4(cur);
-        if (lane == 0 && a && k >= 1) prev = ldg_nc(sq + k - 1);
-        if (k < nq) {
-            const uint4 o = a ? funnel(prev, cur, 4 - a) : cur;
-            const int e0 = 4 * k - a;  // row element of lane 0 of this quad
-            if (e0 >= 0 && e0 + 3 < len) {
-                stg_stream(dq + k, o);
-            } else {
-                uint32_t* d = dst + ((doff >> 2) << 2) + 4 * (long long)k;
-                for (int i = 0; i < 4; ++i)
-                    if (e0 + i >= 0 && e0 + i < len) d[i] = q_at(o, i);
+// Persistent over the sampler's work units: QPU quads of one selection's
+// slot row -> the packed batch at its offset (funnel-shifted 128-bit stores;
+// boundary quads shared with the neighbouring trajectory use masked stores).
+__global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* units,
+                                                        const int* n_units, int32_t* out_tok,
+                                                        float* out_lpo) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nu = *n_units;
+    for (int u = blockIdx.x; u < nu; u += gridDim.x) {
+        const Unit un = ld_unit(units + u);
+        const int a = (int)(un.off & 3);
+        const int nsq = (un.len + 3) >> 2;
+        const int nq = (a + un.len + 3) >> 2;
+        const long long P0 = un.off >> 2;
+        const int kw = un.k0 + wid * 32 * UNIT_U;
+        const size_t row = (size_t)un.row * v.stride;
+        uint4 ot[UNIT_U], ol[UNIT_U];
+        if (out_tok)
+            row_to_packed_quads<UNIT_U>(reinterpret_cast<const uint4*>(v.tok + row), nsq, a, kw, ot);
+        if (out_lpo)
+            row_to_packed_quads<UNIT_U>(reinterpret_cast<const uint4*>(v.lpo + row), nsq, a, kw, ol);
+#pragma unroll
+        for (int s = 0; s < UNIT_U; ++s) {
+            const int k = kw + 32 * s + lane;
+            if (k < nq) {
+                if (out_tok)
+                    store_quad_masked(reinterpret_cast<uint32_t*>(out_tok), P0 + k, ot[s], 4 * k - a,
+                                      un.len);
+                if (out_lpo)
+                    store_quad_masked(reinterpret_cast<uint32_t*>(out_lpo), P0 + k, ol[s], 4 * k - a,
+                                      un.len);
             }
         }
     }
-}
-
-__global__ void __launch_bounds__(256) k_gather(BufView v, const int32_t* sel_slot,
-                                                const int64_t* off, long long lo,
-                                                int32_t* out_tok, float* out_lpo) {
-    const long long b = lo + blockIdx.x;
-    const int g = sel_slot[b];
-    const int s = g / v.C;
-    const size_t row = ((size_t)(s - v.sb) * v.C + (g % v.C)) * (size_t)v.stride;
-    const int len = v.len[g];
-    const long long doff = off[blockIdx.x];
-    if (out_tok)
-        copy_row_to_packed(reinterpret_cast<const uint32_t*>(v.tok + row), len,
-                           reinterpret_cast<uint32_t*>(out_tok), doff);
-    if (out_lpo)
-        copy_row_to_packed(reinterpret_cast<const uint32_t*>(v.lpo + row), len,
-                           reinterpret_cast<uint32_t*>(out_lpo), doff);
 }
 
 // ---------------------------------------------------------------- inspect
@@ -851,7 +917,7 @@ rb_buffer::~rb_buffer() {
                     v.correct, v.use, v.len, v.order, v.head, v.pushes, v.owner, v.tok, v.lpo,
                     v.hkeys, v.hstate, v.ctl, s_tslot, s_surv, s_evid, s_evrec, s_adv, s_gmean,
                     s_len, s_toff, sel_slot, sel_shard, sel_index, sel_off, sel_total,
-                    acc, misc};
+                    acc, misc, n_units_ins, n_units_sel, loss_partials};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : stage_dev)
@@ -906,10 +972,12 @@ void rb_buffer::host_stage_issued() {
 void rb_buffer::ensure_insert(size_t n) {
     if (n <= ins_cap) return;
     RB_CUDA(cudaStreamSynchronize(stream));
-    void* ps[] = {s_tslot, s_surv, s_evid, s_evrec, s_adv, s_gmean, s_len, s_toff};
+    void* ps[] = {s_tslot, s_surv, s_evid, s_evrec, s_adv, s_gmean, s_len, s_toff, units_ins};
     for (void* p : ps)
         if (p) cudaFree(p);
     ins_cap = std::max(n, ins_cap * 2);
+    units_ins_cap = ins_cap * (size_t)(((stride / 4) + QPU - 1) / QPU + 1);
+    units_ins = dalloc<Unit>(units_ins_cap);
     s_tslot = dalloc<int32_t>(ins_cap);
     s_surv = dalloc<uint8_t>(ins_cap);
     s_evid = dalloc<uint64_t>(ins_cap);
@@ -922,10 +990,13 @@ void rb_buffer::ensure_insert(size_t n) {
 void rb_buffer::ensure_select(size_t n) {
     if (n <= sel_cap) return;
     RB_CUDA(cudaStreamSynchronize(stream));
-    void* ps[] = {sel_slot, sel_shard, sel_index, sel_off};
+    void* ps[] = {sel_slot, sel_shard, sel_index, sel_off, sel_len, units_sel};
     for (void* p : ps)
         if (p) cudaFree(p);
     sel_cap = std::max(n, sel_cap * 2);
+    sel_len = dalloc<int32_t>(sel_cap);
+    units_sel_cap = sel_cap * (size_t)(((stride / 4) + 1 + QPU - 1) / QPU + 1);
+    units_sel = dalloc<Unit>(units_sel_cap);
     sel_slot = dalloc<int32_t>(sel_cap);
     sel_shard = dalloc<int32_t>(sel_cap);
     sel_index = dalloc<int64_t>(sel_cap);
@@ -1058,6 +1129,12 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         v.ctl = dalloc<DevCtl>(1);
         b->sel_total = dalloc<long long>(2);
         b->acc = dalloc<DevLossAcc>(1);
+        int sms = 148;
+        RB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        b->unit_grid = sms * UNIT_CTAS_PER_SM;
+        b->n_units_ins = dalloc<int>(1);
+        b->n_units_sel = dalloc<int>(1);
+        b->loss_partials = dalloc<char>((size_t)b->unit_grid * 32);
         b->h_pushes.assign(T, 0);
     } catch (...) {
         delete b;
@@ -1067,8 +1144,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
 }
 
 // Insert `bt` (pointers already resolved to device memory; lens/toff device)
-void launch_insert(rb_buffer* b, const rb_insert_batch& bt, const int32_t* d_len,
-                   const int64_t* d_toff, bool want_evrec) {
+void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec) {
     InsertIn in{};
     in.n = (long long)bt.n;
     in.id = bt.rollout_id;
@@ -1083,18 +1159,24 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, const int32_t* d_len
     in.gmean = bt.group_mean;
     in.goff = bt.group_offsets;
     in.ngroups = (long long)bt.n_groups;
-    in.len = d_len;
+    in.toff = bt.tok_offsets;
+    in.maxlen = b->max_tokens;
+    in.len = b->s_len;
     in.adv_out = b->s_adv;
     in.gmean_out = b->s_gmean;
     in.tslot = b->s_tslot;
     in.surv = b->s_surv;
     in.evid = b->s_evid;
     in.evrec = want_evrec ? b->s_evrec : nullptr;
+    const bool payload = bt.tok_offsets && b->stride > 0 && (bt.tokens || bt.logp_old);
+    in.units = b->units_ins;
+    in.n_units = b->n_units_ins;
+    if (!payload) in.toff = bt.tok_offsets;  // lengths only
     k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
     RB_CUDA(cudaGetLastError());
-    if (bt.tok_offsets && b->stride > 0 && bt.n > 0 && (bt.tokens || bt.logp_old)) {
-        k_insert_payload<<<(unsigned)bt.n, 256, 0, b->stream>>>(b->v, b->s_surv, b->s_tslot, d_toff,
-                                                               d_len, bt.tokens, bt.logp_old);
+    if (payload) {
+        k_insert_payload<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(
+            b->v, b->units_ins, b->n_units_ins, bt.tokens, bt.logp_old);
         RB_CUDA(cudaGetLastError());
     }
 }
@@ -1267,15 +1349,8 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
                 b->host_stage_issued();
             }
         }
-        // lengths from offsets (device)
-        const int32_t* d_len = nullptr;
-        if (bt.tok_offsets) {
-            d_len = b->s_len;
-            rb_lengths_from_offsets(bt.tok_offsets, n, b->s_len, b->max_tokens, b->v.ctl,
-                                    b->stream);
-        }
         const bool want_evrec = (flags & 0x100) != 0;  // internal: rb_push
-        launch_insert(b, bt, d_len, bt.tok_offsets, want_evrec);
+        launch_insert(b, bt, want_evrec);
         if (out_evicted_ids) {
             RB_CUDA(cudaMemcpyAsync(out_evicted_ids, b->s_evid, n * 8, cudaMemcpyDefault,
                                     b->stream));
@@ -1375,23 +1450,38 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         }
         const size_t nsel = nsh * per;
         b->ensure_select(std::max<size_t>(batch_size, 1));
-        if (nsh > 0) {
-            MtState* st = rng->to_device(b->stream);
-            SampleArgs a{(int)nsh, (long long)per, b->sel_shard, b->sel_index};
-            if (b->strategy == RB_UNIFORM_WITH_REPLACEMENT) {
-                k_sample_with<<<1, 1024, 0, b->stream>>>(b->v, st, a);
-            } else {
-                int64_t* scr = (int64_t*)b->scratch(2 * b->C * sizeof(int64_t) + 16);
-                k_sample_without<<<1, 32, 0, b->stream>>>(b->v, st, a, b->strategy, scr);
-            }
-            RB_CUDA(cudaGetLastError());
-            rng->used_on(b->stream);
-        }
         const long long lo = (long long)std::min(b->sb * per, nsel);
         const long long hi = (long long)std::min(b->se * per, nsel);
-        k_sample_map<<<1, 1024, 0, b->stream>>>(b->v, (long long)nsel, b->sel_shard, b->sel_index,
-                                                b->sel_slot, b->sel_off, lo, hi, b->sel_total,
-                                                b->acc);
+        SampleArgs a{};
+        a.nsh = (int)nsh;
+        a.per = (long long)per;
+        a.sel_shard = b->sel_shard;
+        a.sel_index = b->sel_index;
+        a.nsel = (long long)nsel;
+        a.lo = lo;
+        a.hi = hi;
+        a.sel_slot = b->sel_slot;
+        a.sel_len = b->sel_len;
+        a.off = b->sel_off;
+        a.totals = b->sel_total;
+        a.acc = b->acc;
+        a.units = b->units_sel;
+        a.n_units = b->n_units_sel;
+        if (nsh > 0 && b->strategy == RB_UNIFORM_WITH_REPLACEMENT) {
+            MtState* st = rng->to_device(b->stream);
+            k_sample_with<<<1, 1024, 0, b->stream>>>(b->v, st, a);  // draws + map phase
+            RB_CUDA(cudaGetLastError());
+            rng->used_on(b->stream);
+        } else {
+            if (nsh > 0) {
+                MtState* st = rng->to_device(b->stream);
+                int64_t* scr = (int64_t*)b->scratch(2 * b->C * sizeof(int64_t) + 16);
+                k_sample_without<<<1, 32, 0, b->stream>>>(b->v, st, a, b->strategy, scr);
+                RB_CUDA(cudaGetLastError());
+                rng->used_on(b->stream);
+            }
+            k_sample_map<<<1, 1024, 0, b->stream>>>(b->v, a);
+        }
         RB_CUDA(cudaGetLastError());
         b->B = nsel;
         b->last_loss = -1;
@@ -1487,7 +1577,7 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
         if (ht) dt = (int32_t*)stage;
         if (hl) dl = (float*)(stage + pb);
         if (nloc > 0 && (dt || dl)) {
-            k_gather<<<(unsigned)nloc, 256, 0, b->stream>>>(b->v, b->sel_slot, b->sel_off, lo, dt, dl);
+            k_gather<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(b->v, b->units_sel, b->n_units_sel, dt, dl);
             RB_CUDA(cudaGetLastError());
         }
         if (ht) RB_CUDA(cudaMemcpyAsync(out_tokens, dt, total * 4, cudaMemcpyDeviceToHost, b->stream));

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "stream_copy.cuh"
 
 namespace rb {
 
@@ -88,6 +89,17 @@ struct rb_buffer {
     void* stage_host = nullptr;
     size_t stage_host_cap = 0;
     cudaEvent_t stage_event = nullptr;  // last async read of stage_host
+
+    // persistent-kernel work units (stream_copy.cuh)
+    int unit_grid = 0;                  // SMs * UNIT_CTAS_PER_SM
+    rb::Unit* units_ins = nullptr;      // payload copy units of the last insert
+    int* n_units_ins = nullptr;
+    size_t units_ins_cap = 0;
+    rb::Unit* units_sel = nullptr;      // gather/loss units of the current batch
+    int* n_units_sel = nullptr;
+    size_t units_sel_cap = 0;
+    int32_t* sel_len = nullptr;
+    void* loss_partials = nullptr;      // [unit_grid] per-CTA loss partials
 
     // current batch (selection)
     size_t sel_cap = 0, B = 0;

@@ -37,6 +37,42 @@ struct GrpoPartial {
     long long inc = 0, exc = 0;
 };
 
+// One token of the hot kernel: like grpo_token below, but the fast path adds
+// the (ratio | clip bound) of the objective term to a per-unit fp32 sum that
+// is scaled by A once per unit (no per-token fp64 conversion on the XU pipe).
+__device__ __forceinline__ float grpo_token_unit(float lpn, float lpo, double A, float Af,
+                                                 int sgn, const GrpoParams& p, GrpoPartial& acc,
+                                                 float& fsum) {
+    const float d = lpn - lpo;
+    const float r = __expf(d);
+    const bool edge = !(fabsf(d) < 80.f) || fabsf(r - p.hi_f) <= 4e-6f * p.hi_f ||
+                      fabsf(r - p.lo_f) <= 4e-6f * p.lo_f;
+    if (!edge) {
+        ++acc.inc;
+        const bool unclipped = sgn > 0 ? r <= p.hi_f : (sgn < 0 ? r >= p.lo_f : true);
+        if (unclipped) {
+            fsum += r;
+            return Af * r;
+        }
+        fsum += sgn > 0 ? p.hi_f : p.lo_f;
+        return 0.f;
+    }
+    const double rd = exp((double)lpn - (double)lpo);
+    if (!isfinite(rd)) {  // bandit.cpp:381-386
+        ++acc.exc;
+        return 0.f;
+    }
+    ++acc.inc;
+    const double c = rd < p.lo ? p.lo : (p.hi < rd ? p.hi : rd);  // std::clamp
+    const double uv = __dmul_rn(rd, A), cv = __dmul_rn(c, A);
+    if (uv <= cv) {  // ties -> unclipped (bandit.cpp:392)
+        acc.obj += uv;
+        return (float)(A * rd);
+    }
+    acc.obj += cv;
+    return 0.f;
+}
+
 // One token (bandit.cpp:380-400).  Returns the un-normalised coefficient.
 __device__ __forceinline__ float grpo_token(float lpn, float lpo, double A, float Af,
                                             const GrpoParams& p, GrpoPartial& acc) {
@@ -137,52 +173,147 @@ __device__ void grpo_block_commit(GrpoPartial p, DevLossAcc* acc) {
     }
 }
 
-// GRPO over the current batch: CTA per owned selection.
-__global__ void __launch_bounds__(256) k_loss_grpo_buf(BufView v, const int32_t* sel_slot,
-                                                       const int64_t* off, long long lo,
-                                                       const float* lpn_packed, float* dlogp,
-                                                       GrpoParams prm, DevLossAcc* acc) {
-    const long long b = lo + blockIdx.x;
-    const int g = sel_slot[b];
-    const int s = g / v.C;
-    const float* row = v.lpo + ((size_t)(s - v.sb) * v.C + (g % v.C)) * (size_t)v.stride;
-    const int len = v.len[g];
-    const long long doff = off[blockIdx.x];
-    const double A = v.adv[g];
-    const float Af = (float)A;
-    const float scale = -1.f / (float)acc->total_tokens;
+// Per-CTA loss partial of the persistent kernels (32 B).
+struct Partial {
+    double obj;
+    long long inc, exc, pad;
+};
+
+// Block-reduce the thread partials into parts[blockIdx.x]; the last CTA to
+// finish (one ticket atomic per CTA) folds all partials in a fixed order
+// (bitwise-reproducible objective), writes the accumulator and the optional
+// device stats, and — single-process buffers only — applies the rare
+// -1/total -> -1/included correction itself when a token was excluded.
+__device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
+                            rb_loss_stats* stats, int asym, double inv_b, float* dlogp,
+                            const long long* n_local, int local_fix) {
+    __shared__ double s_obj[32];
+    __shared__ long long s_inc[32], s_exc[32];
+    __shared__ int s_last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int a = (int)(doff & 3);
-    const int nsq = (len + 3) >> 2;
-    const int nq = (a + len + 3) >> 2;
-    const long long P0 = doff >> 2;
+    p.obj = warp_sum_f64(p.obj);
+    p.inc = warp_sum_i64(p.inc);
+    p.exc = warp_sum_i64(p.exc);
+    if (lane == 0) {
+        s_obj[wid] = p.obj;
+        s_inc[wid] = p.inc;
+        s_exc[wid] = p.exc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Partial q{0.0, 0, 0, 0};
+        for (int w = 0; w < nw; ++w) {
+            q.obj += s_obj[w];
+            q.inc += s_inc[w];
+            q.exc += s_exc[w];
+        }
+        parts[blockIdx.x] = q;
+        __threadfence();
+        s_last = atomicAdd(&acc->done_blocks, 1ULL) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double o = 0.0;
+    long long inc = 0, exc = 0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+        o += __ldcg(&parts[i].obj);
+        inc += __ldcg(&parts[i].inc);
+        exc += __ldcg(&parts[i].exc);
+    }
+    o = warp_sum_f64(o);
+    inc = warp_sum_i64(inc);
+    exc = warp_sum_i64(exc);
+    __syncthreads();
+    if (lane == 0) {
+        s_obj[wid] = o;
+        s_inc[wid] = inc;
+        s_exc[wid] = exc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        o = 0.0;
+        inc = exc = 0;
+        for (int w = 0; w < nw; ++w) {
+            o += s_obj[w];
+            inc += s_inc[w];
+            exc += s_exc[w];
+        }
+        acc->obj_sum = o;
+        acc->included = (unsigned long long)inc;
+        acc->excluded = (unsigned long long)exc;
+        acc->objective = asym ? o * inv_b : (inc ? o / (double)inc : 0.0);
+        acc->need_fixup = !asym && exc > 0 && inc > 0;
+        acc->done_blocks = 0;
+        if (stats) {
+            stats->objective_sum = o;
+            stats->objective = acc->objective;
+            stats->included = inc;
+            stats->excluded = exc;
+            stats->total_tokens = acc->total_tokens;
+        }
+        s_last = acc->need_fixup && local_fix;
+    }
+    __syncthreads();
+    if (s_last) {  // rare: some ratio was non-finite
+        const float f = (float)((double)acc->total_tokens / (double)acc->included);
+        const long long n = *n_local;
+        for (long long i = threadIdx.x; i < n; i += blockDim.x) dlogp[i] *= f;
+    }
+}
+
+// GRPO over the current batch: persistent over the sampler's work units.
+// Per token 12 B of compulsory traffic: logp_old (slot row, funnel-shifted to
+// the packed alignment), logp_now (packed) in, dlogp (packed) out.
+__global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
+    BufView v, const Unit* units, const int* n_units, const float* lpn_packed, float* dlogp,
+    GrpoParams prm, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats,
+    const long long* n_local, int local_fix) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const float scale = -1.f / (float)acc->total_tokens;
+    const int nu = *n_units;
     GrpoPartial part;
-    for (int base = wid * 32; base < nq; base += nw * 32) {
-        const int k = base + lane;
-        const uint4 cur = k < nsq ? ldg4(row + 4 * k) : make_uint4(0, 0, 0, 0);
-        uint4 prev = shfl_up_q(cur);
-        if (lane == 0 && a && k >= 1) prev = ldg4(row + 4 * (k - 1));
-        if (k < nq) {
-            const uint4 old = a ? funnel4(prev, cur, 4 - a) : cur;
-            const uint4 now = ldg4(lpn_packed + 4 * (P0 + k));
-            const int e0 = 4 * k - a;
-            float o[4];
+    for (int u = blockIdx.x; u < nu; u += gridDim.x) {
+        const Unit un = ld_unit(units + u);
+        const int a = (int)(un.off & 3);
+        const int nsq = (un.len + 3) >> 2;
+        const int nq = (a + un.len + 3) >> 2;
+        const long long P0 = un.off >> 2;
+        const int kw = un.k0 + wid * 32 * UNIT_U;
+        uint4 now[UNIT_U], old[UNIT_U];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                o[i] = 0.f;
-                if (e0 + i >= 0 && e0 + i < len)
-                    o[i] = grpo_token(qf(now, i), qf(old, i), A, Af, prm, part) * scale;
-            }
-            float* dq = dlogp + 4 * (P0 + k);
-            if (e0 >= 0 && e0 + 3 < len) {
-                *reinterpret_cast<float4*>(dq) = make_float4(o[0], o[1], o[2], o[3]);
-            } else {
-                for (int i = 0; i < 4; ++i)
-                    if (e0 + i >= 0 && e0 + i < len) dq[i] = o[i];
+        for (int s = 0; s < UNIT_U; ++s) {
+            const int k = kw + 32 * s + lane;
+            now[s] = k < nq ? ld_stream(lpn_packed + 4 * (P0 + k)) : make_uint4(0, 0, 0, 0);
+        }
+        row_to_packed_quads<UNIT_U>(
+            reinterpret_cast<const uint4*>(v.lpo + (size_t)un.row * v.stride), nsq, a, kw, old);
+        const double A = un.adv;
+        const float Af = (float)A;
+        const int sgn = A > 0.0 ? 1 : (A < 0.0 ? -1 : 0);
+        float fsum = 0.f;
+#pragma unroll
+        for (int s = 0; s < UNIT_U; ++s) {
+            const int k = kw + 32 * s + lane;
+            if (k < nq) {
+                const int e0 = 4 * k - a;
+                float o[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    o[i] = 0.f;
+                    if (e0 + i >= 0 && e0 + i < un.len)
+                        o[i] = grpo_token_unit(qf(now[s], i), qf(old[s], i), A, Af, sgn, prm, part,
+                                               fsum) * scale;
+                }
+                store_quad_masked(reinterpret_cast<uint32_t*>(dlogp), P0 + k,
+                                  make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]),
+                                             __float_as_uint(o[2]), __float_as_uint(o[3])),
+                                  e0, un.len);
             }
         }
+        part.obj += (double)fsum * A;
     }
-    grpo_block_commit(part, acc);
+    loss_commit(part, parts, acc, stats, 0, 0.0, dlogp, n_local, local_fix);
 }
 
 // GRPO over explicit packed arrays (stateless API): CTA per trajectory.
@@ -225,38 +356,45 @@ __global__ void k_dlogp_rescale(float* d, long long n, const long long* n_dev,
 }
 
 // AsymRE over the current batch: dlogp = -coef/B on every token.
-__global__ void __launch_bounds__(256) k_loss_asymre_buf(BufView v, const int32_t* sel_slot,
-                                                         const int64_t* off, long long lo,
-                                                         const float* lpn_packed, float* dlogp,
-                                                         double delta_v, double inv_b,
-                                                         DevLossAcc* acc) {
-    const long long b = lo + blockIdx.x;
-    const int g = sel_slot[b];
-    const int len = v.len[g];
-    const long long o0 = off[blockIdx.x], o1 = o0 + len;
-    const double coef = v.reward[g] - (v.gmean[g] + delta_v);  // bandit.cpp:429
-    const float gcoef = (float)(coef * -inv_b);
-    double seq = 0.0;
-    const long long q0 = o0 >> 2, q1 = (o1 + 3) >> 2;
-    for (long long q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
-        const uint4 now = ldg4(lpn_packed + 4 * q);
-        float* dq = dlogp + 4 * q;
-        if (4 * q >= o0 && 4 * q + 3 < o1) {
-            seq += (double)qf(now, 0) + (double)qf(now, 1) + (double)qf(now, 2) + (double)qf(now, 3);
-            *reinterpret_cast<float4*>(dq) = make_float4(gcoef, gcoef, gcoef, gcoef);
-        } else {
-            for (int e = 0; e < 4; ++e) {
-                const long long t = 4 * q + e;
-                if (t >= o0 && t < o1) {
-                    seq += (double)qf(now, e);
-                    dq[e] = gcoef;
-                }
+// AsymRE over the current batch (persistent over the work units): 8 B/token,
+// logp_now in, dlogp = -coef/B out; objective sum coef * sum_t logp_now.
+__global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
+    BufView v, const Unit* units, const int* n_units, const float* lpn_packed, float* dlogp,
+    double delta_v, double inv_b, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nu = *n_units;
+    GrpoPartial part;
+    for (int u = blockIdx.x; u < nu; u += gridDim.x) {
+        const Unit un = ld_unit(units + u);
+        const int a = (int)(un.off & 3);
+        const int nq = (a + un.len + 3) >> 2;
+        const long long P0 = un.off >> 2;
+        const int kw = un.k0 + wid * 32 * UNIT_U;
+        const double coef = v.reward[un.g] - (v.gmean[un.g] + delta_v);  // bandit.cpp:429
+        const float gc = (float)(coef * -inv_b);
+        const uint4 gq = make_uint4(__float_as_uint(gc), __float_as_uint(gc), __float_as_uint(gc),
+                                    __float_as_uint(gc));
+        uint4 now[UNIT_U];
+#pragma unroll
+        for (int s = 0; s < UNIT_U; ++s) {
+            const int k = kw + 32 * s + lane;
+            now[s] = k < nq ? ld_stream(lpn_packed + 4 * (P0 + k)) : make_uint4(0, 0, 0, 0);
+        }
+        float fs = 0.f;
+#pragma unroll
+        for (int s = 0; s < UNIT_U; ++s) {
+            const int k = kw + 32 * s + lane;
+            if (k < nq) {
+                const int e0 = 4 * k - a;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (e0 + i >= 0 && e0 + i < un.len) fs += qf(now[s], i);
+                store_quad_masked(reinterpret_cast<uint32_t*>(dlogp), P0 + k, gq, e0, un.len);
             }
         }
+        part.obj += coef * (double)fs;
     }
-    GrpoPartial p;
-    p.obj = coef * seq;
-    grpo_block_commit(p, acc);
+    loss_commit(part, parts, acc, stats, 1, inv_b, dlogp, nullptr, 0);
 }
 
 __global__ void __launch_bounds__(256) k_loss_asymre_packed(const float* lpn, const double* reward,
@@ -527,19 +665,25 @@ int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double e
             RB_CUDA(cudaGetLastError());
         }
         b->last_loss = 0;
+        // Device stats are written by the kernel's last CTA (no extra launch).
+        const bool dev_stats = stats && is_device_ptr(stats);
+        rb_loss_stats* kst = dev_stats ? stats : (stats ? (rb_loss_stats*)b->scratch(64) : nullptr);
         if (hi > lo) {
-            k_loss_grpo_buf<<<(unsigned)(hi - lo), 256, 0, b->stream>>>(
-                b->v, b->sel_slot, b->sel_off, lo, logp_now, out_dlogp, p, b->acc);
+            // Single-process buffers rescale in the last CTA when a token was
+            // excluded; multi-rank buffers defer to rb_loss_finalize.
+            const int local_fix = b->sb == 0 && b->se == b->T;
+            k_loss_grpo_buf<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(
+                b->v, b->units_sel, b->n_units_sel, logp_now, out_dlogp, p, b->acc,
+                (Partial*)b->loss_partials, kst, b->sel_total, local_fix);
             RB_CUDA(cudaGetLastError());
-            // Rescale only when a token was excluded (flag set by the last CTA).
-            // Multi-rank buffers defer this to rb_loss_finalize (global counts).
-            if (b->sb == 0 && b->se == b->T) {
-                k_dlogp_rescale<<<148, 256, 0, b->stream>>>(out_dlogp, 0, b->sel_total, b->acc);
-                RB_CUDA(cudaGetLastError());
-            }
+        } else if (kst) {
+            k_stats_out<<<1, 1, 0, b->stream>>>(b->acc, kst, 0, 0.0);
         }
         io.finish(user_dlogp);
-        copy_stats(b, stats, 0, 0.0);
+        if (stats && !dev_stats) {
+            RB_CUDA(cudaMemcpyAsync(stats, kst, sizeof *stats, cudaMemcpyDeviceToHost, b->stream));
+            b->sync();
+        }
     });
 }
 
@@ -561,13 +705,21 @@ int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double
             RB_CUDA(cudaGetLastError());
         }
         b->last_loss = 1;
+        const bool dev_stats = stats && is_device_ptr(stats);
+        rb_loss_stats* kst = dev_stats ? stats : (stats ? (rb_loss_stats*)b->scratch(64) : nullptr);
         if (hi > lo) {
-            k_loss_asymre_buf<<<(unsigned)(hi - lo), 256, 0, b->stream>>>(
-                b->v, b->sel_slot, b->sel_off, lo, logp_now, out_dlogp, delta_v, inv_b, b->acc);
+            k_loss_asymre_buf<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(
+                b->v, b->units_sel, b->n_units_sel, logp_now, out_dlogp, delta_v, inv_b, b->acc,
+                (Partial*)b->loss_partials, kst);
             RB_CUDA(cudaGetLastError());
+        } else if (kst) {
+            k_stats_out<<<1, 1, 0, b->stream>>>(b->acc, kst, 1, inv_b);
         }
         io.finish(user_dlogp);
-        copy_stats(b, stats, 1, inv_b);
+        if (stats && !dev_stats) {
+            RB_CUDA(cudaMemcpyAsync(stats, kst, sizeof *stats, cudaMemcpyDeviceToHost, b->stream));
+            b->sync();
+        }
     });
 }
 

@@ -174,7 +174,7 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
         counts["tokens"] += tot
         # ---- loss
         lpn = ora.synth_logp_now(cfg.seed, step + 1, ids, off)
-        if step % 5 == 3 and tot > 2:  # exercise exclusion (non-finite ratio)
+        if cfg.loss == "grpo" and step % 5 == 3 and tot > 2:  # exercise exclusion
             lpn[1] = np.float32(np.inf)
         lpn_d = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
         lpn_d[:tot] = torch.from_numpy(lpn)
