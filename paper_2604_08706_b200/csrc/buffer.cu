@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
         s_applied = n;
     }
     __syncthreads();
+    RB_CLOCK(10);
     // 0. lengths from the payload offsets
     for (long long j = tid; j < n; j += nt) {
         long long l = in.toff ? in.toff[j + 1] - in.toff[j] : 0;
@@ -303,40 +304,36 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
         in.len[j] = (int32_t)l;
     }
 
+    RB_CLOCK(11);
     // 1. group-relative advantages, frozen at insertion (bandit.cpp:276-294),
     //    fp64 with the reference's operation order (no FMA contraction).
     if (in.adv == nullptr) {
         if (tid == 0 && (in.goff[0] != 0 || in.goff[in.ngroups] != n)) s_bad = 1;
-        // One warp per group: the rewards are fetched 32 at a time in
-        // parallel and folded in the reference's sequential order by shuffle.
-        const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
-        for (long long g = w; g < in.ngroups; g += nw) {
+        // One thread per group, the reference's sequential fp64 order; the
+        // group's reward loads are independent and pipeline (unrolled).
+        for (long long g = tid; g < in.ngroups; g += nt) {
             const long long b = in.goff[g], e = in.goff[g + 1], m = e - b;
             if (m < 2 || b < 0 || e > n) {
-                if (lane == 0) s_bad = 1;
+                s_bad = 1;
                 continue;
             }
             const double dn = (double)m;
             double mean = 0.0;
-            for (long long c = b; c < e; c += 32) {
-                const double r = (c + lane < e) ? in.reward[c + lane] : 0.0;
-                const int cnt = (int)(e - c < 32 ? e - c : 32);
-                for (int k = 0; k < cnt; ++k) mean = __dadd_rn(mean, __shfl_sync(0xffffffffu, r, k));
-            }
+#pragma unroll 8
+            for (long long k = b; k < e; ++k) mean = __dadd_rn(mean, in.reward[k]);
             mean = __ddiv_rn(mean, dn);
             double var = 0.0;
-            for (long long c = b; c < e; c += 32) {
-                const double r = (c + lane < e) ? in.reward[c + lane] : 0.0;
-                const int cnt = (int)(e - c < 32 ? e - c : 32);
-                for (int k = 0; k < cnt; ++k) {
-                    const double d = __dsub_rn(__shfl_sync(0xffffffffu, r, k), mean);
-                    var = __dadd_rn(var, __dmul_rn(d, d));
-                }
+#pragma unroll 8
+            for (long long k = b; k < e; ++k) {
+                const double d = __dsub_rn(in.reward[k], mean);
+                var = __dadd_rn(var, __dmul_rn(d, d));
             }
             var = __ddiv_rn(var, dn);
             const double sd = __dsqrt_rn(var);
-            for (long long k = b + lane; k < e; k += 32) {
-                in.adv_out[k] = sd < 1e-8 ? 0.0 : __ddiv_rn(__dsub_rn(in.reward[k], mean), sd);
+            const double inv_ok = sd < 1e-8 ? 0.0 : 1.0;
+#pragma unroll 8
+            for (long long k = b; k < e; ++k) {
+                in.adv_out[k] = inv_ok == 0.0 ? 0.0 : __ddiv_rn(__dsub_rn(in.reward[k], mean), sd);
                 in.gmean_out[k] = mean;  // bandit.cpp:316-318 (same sequential sum)
             }
         }
@@ -361,6 +358,7 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
         return;
     }
 
+    RB_CLOCK(12);
     // 2. duplicate screening: strictly increasing ids above every id ever
     //    pushed cannot collide (all reference callers allocate ids that way).
     int risk = 0;
@@ -369,6 +367,7 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
         if (j > 0 ? x <= in.id[j - 1] : (ctl->has_any && x <= ctl->max_id)) risk = 1;
     }
     risk = __syncthreads_or(risk);
+    RB_CLOCK(13);
     const unsigned long long cur0 = ctl->cursor;
     const int T = v.T, C = v.C;
 
@@ -376,12 +375,20 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
         // 3a. FIFO closed form: push j -> shard (cur0+j)%T, per-shard arrival
         //     p = pushes_s + j/T, slot p % C; the victim is whatever held the
         //     slot C arrivals earlier (pre-batch record or an earlier push).
-        for (long long j = tid; j < n; j += nt) {
-            const int s = (int)((cur0 + j) % T);
-            const long long rank = j / T, j0 = j % T;
-            const long long ns = (n - 1 - j0) / T + 1;
-            const long long p = v.pushes[s] + rank;
-            const size_t g = (size_t)s * C + (size_t)(p % C);
+        // 32-bit index arithmetic (n, T, C < 2^31); the 64-bit push counts
+        // enter only through a per-shard P mod C computed once.
+        const int c0 = (int)(cur0 % (unsigned long long)T), n32 = (int)n;
+        for (int j = tid; j < n32; j += nt) {
+            int s = c0 + j % T;
+            if (s >= T) s -= T;
+            const int rank = j / T, j0 = j % T;
+            const int ns = (n32 - 1 - j0) / T + 1;
+            const long long P = v.pushes[s];
+            const long long p = P + rank;
+            const int pm = (int)(P % C);
+            int x = pm + rank % C;
+            if (x >= C) x -= C;
+            const size_t g = (size_t)s * C + (size_t)x;
             in.tslot[j] = (int32_t)g;
             in.surv[j] = (rank + C >= ns);
             uint64_t ev = NONE_ID;
@@ -480,45 +487,64 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
         }
     }
     __syncthreads();
-    // 4. payload work units: surviving records of the shards held here, in
-    //    QPU-quad pieces of their destination row.
-    if (in.toff && v.stride > 0) {
-        auto count = [&](long long j) -> long long {
-            if (!in.surv[j]) return 0;
-            const int g = in.tslot[j], s = g / v.C;
-            if (s < v.sb || s >= v.se) return 0;
-            const int nq = (in.len[j] + 3) >> 2;
-            return (nq + QPU - 1) / QPU;
-        };
-        auto emit = [&](long long j, long long first, long long c) {
-            if (!c) return;
-            const int g = in.tslot[j], s = g / v.C;
-            Unit u;
-            u.row = (s - v.sb) * v.C + (g - s * v.C);
-            u.len = in.len[j];
-            u.g = (int32_t)j;
-            u.off = in.toff[j];
-            u.adv = 0.0;
-            for (long long k = 0; k < c; ++k) {
-                u.k0 = (int32_t)(k * QPU);
-                in.units[first + k] = u;
+    RB_CLOCK(14);
+    // 4. payload descriptors: one per record (row = -1 unless it survived the
+    //    batch in a shard held here) and the max units per record; the
+    //    payload kernel strides over n * ups virtual units.
+    {
+        int ups = 0;
+        if (in.toff && v.stride > 0) {
+            for (long long j = tid; j < n; j += nt) {
+                Unit d;
+                d.row = -1;
+                d.len = in.len[j];
+                d.k0 = 0;
+                d.g = (int32_t)j;
+                d.off = in.toff[j];
+                d.adv = 0.0;
+                if (in.surv[j]) {
+                    const int g = in.tslot[j], s = g / v.C;
+                    if (s >= v.sb && s < v.se && d.len > 0) {
+                        d.row = (s - v.sb) * v.C + (g - s * v.C);
+                        const int u = (((d.len + 3) >> 2) + QPU - 1) / QPU;
+                        ups = u > ups ? u : ups;
+                    }
+                }
+                in.units[j] = d;
             }
-        };
-        const long long total = block_build_units(n, count, emit);
-        if (tid == 0) *in.n_units = (int)total;
-    } else if (tid == 0) {
-        *in.n_units = 0;
+        }
+        ups = __reduce_max_sync(0xffffffffu, ups);
+        __shared__ int s_ups[32];
+        if ((tid & 31) == 0) s_ups[tid >> 5] = ups;
+        __syncthreads();
+        if (tid == 0) {
+            int m = 0;
+            for (int w = 0; w < (nt >> 5); ++w) m = s_ups[w] > m ? s_ups[w] : m;
+            *in.n_units = m;
+        }
     }
-    // 5. bookkeeping
+    RB_CLOCK(15);
+    // 5. bookkeeping: largest id ever pushed (block max over the applied prefix)
+    __shared__ unsigned long long s_mx[32];
+    const long long applied = s_applied;
+    unsigned long long mx = 0;
+    for (long long j = tid; j < applied; j += nt) mx = in.id[j] > mx ? in.id[j] : mx;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
+    }
+    if ((tid & 31) == 0) s_mx[tid >> 5] = mx;
+    __syncthreads();
     if (tid == 0) {
-        const long long applied = s_applied;
-        unsigned long long mx = ctl->has_any ? ctl->max_id : 0ULL;
-        for (long long j = 0; j < applied; ++j) mx = in.id[j] > mx ? in.id[j] : mx;
+        mx = ctl->has_any ? ctl->max_id : 0ULL;
+        for (int w = 0; w < (nt >> 5); ++w) mx = s_mx[w] > mx ? s_mx[w] : mx;
         if (applied > 0) {
             ctl->max_id = mx;
             ctl->has_any = 1;
         }
         ctl->hash_stale = risk ? 0 : 1;
+        RB_CLOCK(16);
     }
 }
 
@@ -526,18 +552,21 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
 // Each unit copies QPU quads of one surviving trajectory from the packed
 // inbound batch (any alignment) into its 16-byte aligned slot row, tokens and
 // logp_old interleaved so every thread keeps 2*UNIT_U 16-byte loads in flight.
-__global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, const Unit* units,
-                                                                 const int* n_units,
+__global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, const Unit* desc,
+                                                                 const int* ups_p, int n,
                                                                  const int32_t* tokens,
                                                                  const float* logp_old) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int nu = *n_units;
+    const int ups = *ups_p;  // units per record (max over the batch)
+    const int nu = n * ups;
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
-        const Unit un = ld_unit(units + u);
+        const int j = u / ups, c = u - j * ups;
+        const Unit un = ld_unit(desc + j);
+        const int nq = (un.len + 3) >> 2;  // destination (row) quads
+        if (un.row < 0 || c * QPU >= nq) continue;
         const int a = (int)(un.off & 3);
         const int nsq = (a + un.len + 3) >> 2;  // source quads touched
-        const int nq = (un.len + 3) >> 2;        // destination (row) quads
-        const int kw = un.k0 + wid * 32 * UNIT_U;
+        const int kw = c * QPU + wid * 32 * UNIT_U;
         const size_t row = (size_t)un.row * v.stride;
         uint4 ot[UNIT_U], ol[UNIT_U];
         if (tokens)
@@ -576,6 +605,8 @@ struct SampleArgs {
     DevLossAcc* acc;
     Unit* units;
     int* n_units;
+    int occ_known;           // occupancies below are valid (T <= 64)
+    long long occ[64];       // per-shard occupancy after the preceding inserts
 };
 
 // x % n without a 64-bit division: q from a precomputed reciprocal
@@ -590,19 +621,25 @@ __device__ __forceinline__ uint64_t fast_mod(uint64_t x, uint64_t n, uint64_t m)
 __device__ void sample_map_phase(const BufView& v, const SampleArgs& a);
 
 // uniform_with_replacement (replay_buffer.cpp:141-145): shard 0 takes its
-// `per` below(n_0) draws first, then shard 1, ...  The block generates 312
-// outputs per twist; a chunk containing a rejected value (v >= limit,
-// rng.cpp:45-49; probability ~n/2^64) is replayed sequentially by thread 0.
-__global__ void __launch_bounds__(1024) k_sample_with(BufView v, MtState* st, SampleArgs a) {
+// `per` below(n_0) draws first, then shard 1, ...  One small CTA (the twist
+// needs 156 threads) generates 312 outputs per block twist; a chunk holding a
+// rejected value (v >= limit, rng.cpp:45-49; probability ~n/2^64) is replayed
+// sequentially by thread 0 so the stream advances exactly as the reference.
+// Occupancies come from the host (a.occ) so the kernel does not depend on
+// the insert and runs on the auxiliary stream, overlapping it.
+constexpr int DRAW_THREADS = 160;
+__global__ void __launch_bounds__(DRAW_THREADS) k_sample_draw(BufView v, MtState* st, SampleArgs a) {
     __shared__ uint64_t mt[MT_N];
     __shared__ long long s_emit;
     for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = st->mt[i];
     uint32_t idx = st->idx;
     unsigned long long consumed = 0;
     __syncthreads();
+    RB_CLOCK(0);
     long long pos = 0;
     for (int s = 0; s < a.nsh; ++s) {
-        const unsigned long long n = (unsigned long long)occupancy(v, s);
+        const unsigned long long n =
+            a.occ_known ? (unsigned long long)a.occ[s] : (unsigned long long)occupancy(v, s);
         const unsigned long long lim = below_limit(n);
         const unsigned long long mag = UINT64_MAX / n;
         long long rem = a.per;
@@ -614,15 +651,11 @@ __global__ void __launch_bounds__(1024) k_sample_with(BufView v, MtState* st, Sa
             const long long avail = (long long)(MT_N - idx);
             const int take = (int)(avail < rem ? avail : rem);
             bool rej = false;
-            uint64_t x = 0;
-            if (threadIdx.x < take) {
-                x = mt_temper(mt[idx + threadIdx.x]);
-                rej = x >= lim;
-            }
+            for (int t = threadIdx.x; t < take; t += blockDim.x) rej |= mt_temper(mt[idx + t]) >= lim;
             if (!__syncthreads_or(rej)) {
-                if (threadIdx.x < take) {
-                    a.sel_shard[pos + threadIdx.x] = s;
-                    a.sel_index[pos + threadIdx.x] = (int64_t)fast_mod(x, n, mag);
+                for (int t = threadIdx.x; t < take; t += blockDim.x) {
+                    a.sel_shard[pos + t] = s;
+                    a.sel_index[pos + t] = (int64_t)fast_mod(mt_temper(mt[idx + t]), n, mag);
                 }
                 pos += take;
                 rem -= take;
@@ -654,7 +687,7 @@ __global__ void __launch_bounds__(1024) k_sample_with(BufView v, MtState* st, Sa
         st->idx = idx;
         st->draws += consumed;
     }
-    sample_map_phase(v, a);  // same CTA: the draws are visible after the barrier
+    RB_CLOCK(1);
 }
 
 __device__ __forceinline__ uint64_t mt_below_scalar(uint64_t* mt, uint32_t* idx,
@@ -732,6 +765,7 @@ __device__ void sample_map_phase(const BufView& v, const SampleArgs& a) {
     __shared__ unsigned long long s_global;
     __shared__ int s_head[64];
     if (threadIdx.x == 0) s_global = 0;
+    RB_CLOCK(2);
     const int nsh_h = a.nsh < 64 ? a.nsh : 0;  // cache shard heads when few shards
     for (int s = threadIdx.x; s < nsh_h; s += blockDim.x) s_head[s] = shard_head(v, s);
     __syncthreads();
@@ -741,65 +775,92 @@ __device__ void sample_map_phase(const BufView& v, const SampleArgs& a) {
         const int head = nsh_h ? s_head[s] : shard_head(v, s);
         const int g = s * v.C + arrival_slot_h(v, s, a.sel_index[i], head);
         a.sel_slot[i] = g;
-        atomicAdd(&v.use[g], 1u);
         const int L = v.len[g];
+        const double adv = v.adv[g];
+        atomicAdd(&v.use[g], 1u);
         a.sel_len[i] = L;
         gsum += (unsigned long long)L;
+        if (i >= a.lo && i < a.hi) {  // descriptor of an owned selection (offset below)
+            Unit d;
+            d.row = (s - v.sb) * v.C + (g - s * v.C);
+            d.len = L;
+            d.k0 = 0;
+            d.g = g;
+            d.off = 0;
+            d.adv = adv;
+            a.units[i - a.lo] = d;
+        }
     }
-    atomicAdd(&s_global, gsum);
+    {  // block sum of the lengths (warp shuffles; no shared-memory atomics)
+        __shared__ unsigned long long s_w[32];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+        if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = gsum;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+            s_global = t;
+        }
+    }
     __syncthreads();
-    // exclusive scan of the owned selections' lengths -> packed offsets
+    RB_CLOCK(3);
+    // exclusive scan of the owned selections' lengths -> packed offsets, the
+    // descriptors' offsets, and the max work units per selection
     const long long lo = a.lo, nloc = a.hi - a.lo;
+    int ups = 0;
     {
         const long long per = (nloc + blockDim.x - 1) / blockDim.x;
         const long long i0 = threadIdx.x * per, i1 = i0 + per < nloc ? i0 + per : nloc;
+        constexpr int R = 8;  // register-resident run (longer runs loop)
+        int Lr[R];
         long long local = 0;
-        for (long long i = i0; i < i1; ++i) local += a.sel_len[lo + i];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            Lr[k] = (i0 + k < i1) ? a.sel_len[lo + i0 + k] : 0;
+            local += Lr[k];
+        }
+        for (long long i = i0 + R; i < i1; ++i) local += a.sel_len[lo + i];
         long long total;
         long long pos = block_exclusive_scan(local, &total);
-        for (long long i = i0; i < i1; ++i) {
+        auto put = [&](long long i, int L) {
             a.off[i] = pos;
-            pos += a.sel_len[lo + i];
-        }
+            reinterpret_cast<long long*>(&a.units[i])[2] = pos;  // Unit::off
+            const int nq = ((int)(pos & 3) + L + 3) >> 2;
+            const int u = L ? (nq + QPU - 1) / QPU : 0;
+            ups = u > ups ? u : ups;
+            pos += L;
+        };
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+            if (i0 + k < i1) put(i0 + k, Lr[k]);
+        for (long long i = i0 + R; i < i1; ++i) put(i, a.sel_len[lo + i]);
         if (threadIdx.x == 0) {
             a.off[nloc] = total;
             a.totals[0] = total;
             a.totals[1] = (long long)s_global;
         }
     }
-    __syncthreads();
-    // work units: QPU quads of each selection's destination quad range
-    auto count = [&](long long i) -> long long {
-        const int L = a.sel_len[lo + i];
-        if (L == 0) return 0;
-        const int nq = ((int)(a.off[i] & 3) + L + 3) >> 2;
-        return (nq + QPU - 1) / QPU;
-    };
-    auto emit = [&](long long i, long long first, long long c) {
-        if (!c) return;
-        const int g = a.sel_slot[lo + i], s = g / v.C;
-        Unit u;
-        u.row = (s - v.sb) * v.C + (g - s * v.C);
-        u.len = a.sel_len[lo + i];
-        u.g = g;
-        u.off = a.off[i];
-        u.adv = v.adv[g];
-        for (long long k = 0; k < c; ++k) {
-            u.k0 = (int32_t)(k * QPU);
-            a.units[first + k] = u;
+    RB_CLOCK(4);
+    {
+        __shared__ int s_u[32];
+        ups = __reduce_max_sync(0xffffffffu, ups);
+        if ((threadIdx.x & 31) == 0) s_u[threadIdx.x >> 5] = ups;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int m = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = s_u[w] > m ? s_u[w] : m;
+            *a.n_units = m;  // units per selection (max over the batch)
+            RB_CLOCK(5);
+            DevLossAcc* acc = a.acc;
+            acc->obj_sum = 0.0;
+            acc->included = 0;
+            acc->excluded = 0;
+            acc->done_blocks = 0;
+            acc->total_tokens = (long long)s_global;
+            acc->objective = 0.0;
+            acc->need_fixup = 0;
         }
-    };
-    const long long nu = block_build_units(nloc, count, emit);
-    if (threadIdx.x == 0) {
-        *a.n_units = (int)nu;
-        DevLossAcc* acc = a.acc;
-        acc->obj_sum = 0.0;
-        acc->included = 0;
-        acc->excluded = 0;
-        acc->done_blocks = 0;
-        acc->total_tokens = (long long)s_global;
-        acc->objective = 0.0;
-        acc->need_fixup = 0;
     }
 }
 
@@ -842,18 +903,21 @@ __global__ void k_sample_records(BufView v, long long nsel, long long per,
 // Persistent over the sampler's work units: QPU quads of one selection's
 // slot row -> the packed batch at its offset (funnel-shifted 128-bit stores;
 // boundary quads shared with the neighbouring trajectory use masked stores).
-__global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* units,
-                                                        const int* n_units, int32_t* out_tok,
-                                                        float* out_lpo) {
+__global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* desc,
+                                                        const int* ups_p, int nloc,
+                                                        int32_t* out_tok, float* out_lpo) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int nu = *n_units;
+    const int ups = *ups_p;  // units per selection (max over the batch)
+    const int nu = nloc * ups;
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
-        const Unit un = ld_unit(units + u);
+        const int b = u / ups, c = u - b * ups;
+        const Unit un = ld_unit(desc + b);
         const int a = (int)(un.off & 3);
-        const int nsq = (un.len + 3) >> 2;
         const int nq = (a + un.len + 3) >> 2;
+        if (c * QPU >= nq) continue;
+        const int nsq = (un.len + 3) >> 2;
         const long long P0 = un.off >> 2;
-        const int kw = un.k0 + wid * 32 * UNIT_U;
+        const int kw = c * QPU + wid * 32 * UNIT_U;
         const size_t row = (size_t)un.row * v.stride;
         uint4 ot[UNIT_U], ol[UNIT_U];
         if (out_tok)
@@ -924,6 +988,10 @@ rb_buffer::~rb_buffer() {
         if (p) cudaFree(p);
     if (stage_host) cudaFreeHost(stage_host);
     if (stage_event) cudaEventDestroy(stage_event);
+    if (aux) cudaStreamSynchronize(aux);
+    if (ev_draw) cudaEventDestroy(ev_draw);
+    if (ev_map) cudaEventDestroy(ev_map);
+    if (aux) cudaStreamDestroy(aux);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -938,7 +1006,7 @@ static T* dalloc(size_t n) {
 void* rb_buffer::scratch(size_t bytes) {
     if (bytes > misc_cap) {
         if (misc) {
-            RB_CUDA(cudaStreamSynchronize(stream));
+            sync();
             cudaFree(misc);
         }
         misc_cap = std::max(bytes, misc_cap * 2);
@@ -949,7 +1017,7 @@ void* rb_buffer::scratch(size_t bytes) {
 void* rb_buffer::host_stage(size_t bytes) {
     if (stage_event) RB_CUDA(cudaEventSynchronize(stage_event));
     if (bytes > stage_host_cap) {
-        RB_CUDA(cudaStreamSynchronize(stream));
+        sync();
         if (stage_host) cudaFreeHost(stage_host);
         stage_host_cap = std::max(bytes, stage_host_cap * 2);
         RB_CUDA(cudaMallocHost(&stage_host, stage_host_cap));
@@ -958,7 +1026,7 @@ void* rb_buffer::host_stage(size_t bytes) {
 }
 void* rb_buffer::dev_stage(size_t bytes, int slot) {
     if (bytes > stage_dev_cap[slot]) {
-        RB_CUDA(cudaStreamSynchronize(stream));
+        sync();
         if (stage_dev[slot]) cudaFree(stage_dev[slot]);
         stage_dev_cap[slot] = std::max(bytes, stage_dev_cap[slot] * 2);
         RB_CUDA(cudaMalloc(&stage_dev[slot], stage_dev_cap[slot]));
@@ -971,12 +1039,12 @@ void rb_buffer::host_stage_issued() {
 }
 void rb_buffer::ensure_insert(size_t n) {
     if (n <= ins_cap) return;
-    RB_CUDA(cudaStreamSynchronize(stream));
+    sync();
     void* ps[] = {s_tslot, s_surv, s_evid, s_evrec, s_adv, s_gmean, s_len, s_toff, units_ins};
     for (void* p : ps)
         if (p) cudaFree(p);
     ins_cap = std::max(n, ins_cap * 2);
-    units_ins_cap = ins_cap * (size_t)(((stride / 4) + QPU - 1) / QPU + 1);
+    units_ins_cap = ins_cap;  // one descriptor per record
     units_ins = dalloc<Unit>(units_ins_cap);
     s_tslot = dalloc<int32_t>(ins_cap);
     s_surv = dalloc<uint8_t>(ins_cap);
@@ -989,20 +1057,23 @@ void rb_buffer::ensure_insert(size_t n) {
 }
 void rb_buffer::ensure_select(size_t n) {
     if (n <= sel_cap) return;
-    RB_CUDA(cudaStreamSynchronize(stream));
+    sync();
     void* ps[] = {sel_slot, sel_shard, sel_index, sel_off, sel_len, units_sel};
     for (void* p : ps)
         if (p) cudaFree(p);
     sel_cap = std::max(n, sel_cap * 2);
     sel_len = dalloc<int32_t>(sel_cap);
-    units_sel_cap = sel_cap * (size_t)(((stride / 4) + 1 + QPU - 1) / QPU + 1);
+    units_sel_cap = sel_cap;  // one descriptor per selection
     units_sel = dalloc<Unit>(units_sel_cap);
     sel_slot = dalloc<int32_t>(sel_cap);
     sel_shard = dalloc<int32_t>(sel_cap);
     sel_index = dalloc<int64_t>(sel_cap);
     sel_off = dalloc<int64_t>(sel_cap + 1);
 }
-void rb_buffer::sync() { RB_CUDA(cudaStreamSynchronize(stream)); }
+void rb_buffer::sync() {
+    sync();
+    if (aux) RB_CUDA(cudaStreamSynchronize(aux));
+}
 
 namespace {
 
@@ -1089,6 +1160,11 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         b->se = se;
         RB_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
         b->own_stream = true;
+        int prio_lo = 0, prio_hi = 0;
+        RB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        RB_CUDA(cudaStreamCreateWithPriority(&b->aux, cudaStreamNonBlocking, prio_hi));
+        RB_CUDA(cudaEventCreateWithFlags(&b->ev_draw, cudaEventDisableTiming));
+        RB_CUDA(cudaEventCreateWithFlags(&b->ev_map, cudaEventDisableTiming));
         BufView& v = b->v;
         v.T = (int)T;
         v.C = (int)b->C;
@@ -1132,6 +1208,8 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         int sms = 148;
         RB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         b->unit_grid = sms * UNIT_CTAS_PER_SM;
+        // the payload copy overlaps the sampler's draw CTA: leave it room
+        b->payload_grid = sms * (UNIT_CTAS_PER_SM - 2);
         b->n_units_ins = dalloc<int>(1);
         b->n_units_sel = dalloc<int>(1);
         b->loss_partials = dalloc<char>((size_t)b->unit_grid * 32);
@@ -1175,8 +1253,8 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec) {
     k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
     RB_CUDA(cudaGetLastError());
     if (payload) {
-        k_insert_payload<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(
-            b->v, b->units_ins, b->n_units_ins, bt.tokens, bt.logp_old);
+        k_insert_payload<<<b->payload_grid, UNIT_THREADS, 0, b->stream>>>(
+            b->v, b->units_ins, b->n_units_ins, (int)bt.n, bt.tokens, bt.logp_old);
         RB_CUDA(cudaGetLastError());
     }
 }
@@ -1468,10 +1546,24 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         a.units = b->units_sel;
         a.n_units = b->n_units_sel;
         if (nsh > 0 && b->strategy == RB_UNIFORM_WITH_REPLACEMENT) {
-            MtState* st = rng->to_device(b->stream);
-            k_sample_with<<<1, 1024, 0, b->stream>>>(b->v, st, a);  // draws + map phase
+            // Draws on the auxiliary stream: they need only the RNG state and
+            // the occupancies (host mirror), so they overlap the insert.
+            a.occ_known = b->T <= 64;
+            for (size_t s = 0; s < b->T && s < 64; ++s)
+                a.occ[s] = std::min<long long>(b->h_pushes[s], (long long)b->C);
+            cudaStream_t ds = a.occ_known ? b->aux : b->stream;
+            if (a.occ_known) RB_CUDA(cudaStreamWaitEvent(b->aux, b->ev_map, 0));
+            MtState* st = rng->to_device(ds);
+            k_sample_draw<<<1, DRAW_THREADS, 0, ds>>>(b->v, st, a);
             RB_CUDA(cudaGetLastError());
-            rng->used_on(b->stream);
+            rng->used_on(ds);
+            if (a.occ_known) {
+                RB_CUDA(cudaEventRecord(b->ev_draw, b->aux));
+                RB_CUDA(cudaStreamWaitEvent(b->stream, b->ev_draw, 0));
+            }
+            k_sample_map<<<1, 1024, 0, b->stream>>>(b->v, a);
+            RB_CUDA(cudaGetLastError());
+            RB_CUDA(cudaEventRecord(b->ev_map, b->stream));
         } else {
             if (nsh > 0) {
                 MtState* st = rng->to_device(b->stream);
@@ -1481,8 +1573,9 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 rng->used_on(b->stream);
             }
             k_sample_map<<<1, 1024, 0, b->stream>>>(b->v, a);
+            RB_CUDA(cudaGetLastError());
+            RB_CUDA(cudaEventRecord(b->ev_map, b->stream));
         }
-        RB_CUDA(cudaGetLastError());
         b->B = nsel;
         b->last_loss = -1;
         if (nsel > 0 && (out_records || out_events)) {
@@ -1577,7 +1670,7 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
         if (ht) dt = (int32_t*)stage;
         if (hl) dl = (float*)(stage + pb);
         if (nloc > 0 && (dt || dl)) {
-            k_gather<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(b->v, b->units_sel, b->n_units_sel, dt, dl);
+            k_gather<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(b->v, b->units_sel, b->n_units_sel, (int)nloc, dt, dl);
             RB_CUDA(cudaGetLastError());
         }
         if (ht) RB_CUDA(cudaMemcpyAsync(out_tokens, dt, total * 4, cudaMemcpyDeviceToHost, b->stream));
@@ -1953,4 +2046,16 @@ void rb_batch_ids_dev(const BufView& v, const int32_t* sel_slot, long long lo, l
     k_batch_ids<<<(unsigned)std::min<long long>((n + 255) / 256, 1024), 256, 0, s>>>(v, sel_slot, lo, hi,
                                                                                     ids, lens);
     RB_CUDA(cudaGetLastError());
+}
+
+// Tuning aid: phase clocks of the single-CTA kernels (zeros unless the
+// library was built with -DRB_PHASE_CLOCKS).
+extern "C" __attribute__((visibility("default"))) int rb_debug_phase_clocks(long long* out) {
+    return guard([&] {
+#ifdef RB_PHASE_CLOCKS
+        RB_CUDA(cudaMemcpyFromSymbol(out, g_phase_clock, 64 * sizeof(long long)));
+#else
+        for (int i = 0; i < 64; ++i) out[i] = 0;
+#endif
+    });
 }

@@ -92,6 +92,9 @@ struct rb_buffer {
 
     // persistent-kernel work units (stream_copy.cuh)
     int unit_grid = 0;                  // SMs * UNIT_CTAS_PER_SM
+    int payload_grid = 0;
+    cudaStream_t aux = nullptr;         // sampler draws (overlap the insert)
+    cudaEvent_t ev_draw = nullptr, ev_map = nullptr;
     rb::Unit* units_ins = nullptr;      // payload copy units of the last insert
     int* n_units_ins = nullptr;
     size_t units_ins_cap = 0;

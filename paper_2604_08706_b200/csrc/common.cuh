@@ -131,6 +131,20 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
     return v;
 }
 
+// Phase clocks for tuning the single-CTA kernels (debug builds only:
+// -DRB_PHASE_CLOCKS; read back with rb_debug_phase_clocks).
+#ifdef RB_PHASE_CLOCKS
+static __device__ long long g_phase_clock[64];
+#define RB_CLOCK(i)                                                  \
+    do {                                                             \
+        if (threadIdx.x == 0 && blockIdx.x == 0) g_phase_clock[i] = clock64(); \
+    } while (0)
+#else
+#define RB_CLOCK(i) \
+    do {            \
+    } while (0)
+#endif
+
 // Device-side loss accumulator (one per buffer; reset by the sampler).
 struct DevLossAcc {
     double obj_sum;

@@ -266,20 +266,23 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
 // Per token 12 B of compulsory traffic: logp_old (slot row, funnel-shifted to
 // the packed alignment), logp_now (packed) in, dlogp (packed) out.
 __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
-    BufView v, const Unit* units, const int* n_units, const float* lpn_packed, float* dlogp,
-    GrpoParams prm, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats,
+    BufView v, const Unit* units, const int* n_units, int nloc, const float* lpn_packed,
+    float* dlogp, GrpoParams prm, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats,
     const long long* n_local, int local_fix) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const float scale = -1.f / (float)acc->total_tokens;
-    const int nu = *n_units;
+    const int ups = *n_units;  // units per selection (max over the batch)
+    const int nu = nloc * ups;
     GrpoPartial part;
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
-        const Unit un = ld_unit(units + u);
+        const int b = u / ups, c = u - b * ups;
+        const Unit un = ld_unit(units + b);
         const int a = (int)(un.off & 3);
-        const int nsq = (un.len + 3) >> 2;
         const int nq = (a + un.len + 3) >> 2;
+        if (c * QPU >= nq) continue;
+        const int nsq = (un.len + 3) >> 2;
         const long long P0 = un.off >> 2;
-        const int kw = un.k0 + wid * 32 * UNIT_U;
+        const int kw = c * QPU + wid * 32 * UNIT_U;
         uint4 now[UNIT_U], old[UNIT_U];
 #pragma unroll
         for (int s = 0; s < UNIT_U; ++s) {
@@ -359,17 +362,20 @@ __global__ void k_dlogp_rescale(float* d, long long n, const long long* n_dev,
 // AsymRE over the current batch (persistent over the work units): 8 B/token,
 // logp_now in, dlogp = -coef/B out; objective sum coef * sum_t logp_now.
 __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
-    BufView v, const Unit* units, const int* n_units, const float* lpn_packed, float* dlogp,
-    double delta_v, double inv_b, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats) {
+    BufView v, const Unit* units, const int* n_units, int nloc, const float* lpn_packed,
+    float* dlogp, double delta_v, double inv_b, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int nu = *n_units;
+    const int ups = *n_units;
+    const int nu = nloc * ups;
     GrpoPartial part;
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
-        const Unit un = ld_unit(units + u);
+        const int b = u / ups, c = u - b * ups;
+        const Unit un = ld_unit(units + b);
         const int a = (int)(un.off & 3);
         const int nq = (a + un.len + 3) >> 2;
+        if (c * QPU >= nq) continue;
         const long long P0 = un.off >> 2;
-        const int kw = un.k0 + wid * 32 * UNIT_U;
+        const int kw = c * QPU + wid * 32 * UNIT_U;
         const double coef = v.reward[un.g] - (v.gmean[un.g] + delta_v);  // bandit.cpp:429
         const float gc = (float)(coef * -inv_b);
         const uint4 gq = make_uint4(__float_as_uint(gc), __float_as_uint(gc), __float_as_uint(gc),
@@ -673,7 +679,7 @@ int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double e
             // excluded; multi-rank buffers defer to rb_loss_finalize.
             const int local_fix = b->sb == 0 && b->se == b->T;
             k_loss_grpo_buf<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(
-                b->v, b->units_sel, b->n_units_sel, logp_now, out_dlogp, p, b->acc,
+                b->v, b->units_sel, b->n_units_sel, (int)(hi - lo), logp_now, out_dlogp, p, b->acc,
                 (Partial*)b->loss_partials, kst, b->sel_total, local_fix);
             RB_CUDA(cudaGetLastError());
         } else if (kst) {
@@ -709,7 +715,8 @@ int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double
         rb_loss_stats* kst = dev_stats ? stats : (stats ? (rb_loss_stats*)b->scratch(64) : nullptr);
         if (hi > lo) {
             k_loss_asymre_buf<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(
-                b->v, b->units_sel, b->n_units_sel, logp_now, out_dlogp, delta_v, inv_b, b->acc,
+                b->v, b->units_sel, b->n_units_sel, (int)(hi - lo), logp_now, out_dlogp, delta_v,
+                inv_b, b->acc,
                 (Partial*)b->loss_partials, kst);
             RB_CUDA(cudaGetLastError());
         } else if (kst) {
