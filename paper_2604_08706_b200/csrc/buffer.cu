@@ -1071,7 +1071,7 @@ void rb_buffer::ensure_select(size_t n) {
     sel_off = dalloc<int64_t>(sel_cap + 1);
 }
 void rb_buffer::sync() {
-    sync();
+    RB_CUDA(cudaStreamSynchronize(stream));
     if (aux) RB_CUDA(cudaStreamSynchronize(aux));
 }
 
