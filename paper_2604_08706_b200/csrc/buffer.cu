@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
                     const int g = in.tslot[j], s = g / v.C;
                     if (s >= v.sb && s < v.se && d.len > 0) {
                         d.row = (s - v.sb) * v.C + (g - s * v.C);
-                        const int u = (((d.len + 3) >> 2) + QPU - 1) / QPU;
+                        const int u = (d.len + 3) >> 2;  // row quads
                         ups = u > ups ? u : ups;
                     }
                 }
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
         if (tid == 0) {
             int m = 0;
             for (int w = 0; w < (nt >> 5); ++w) m = s_ups[w] > m ? s_ups[w] : m;
-            *in.n_units = m;
+            *in.n_units = m;  // max quads per record
         }
     }
     RB_CLOCK(15);
@@ -548,35 +548,37 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
     }
 }
 
-// ---- payload insert: persistent over the route kernel's work units -------
-// Each unit copies QPU quads of one surviving trajectory from the packed
+// ---- payload insert: persistent over n * ceil(max_nq / QPU) virtual units --
+// Each unit copies 128*U quads of one surviving trajectory from the packed
 // inbound batch (any alignment) into its 16-byte aligned slot row, tokens and
-// logp_old interleaved so every thread keeps 2*UNIT_U 16-byte loads in flight.
+// logp_old interleaved so every thread keeps 2*U 16-byte loads in flight.
+template <int U>
 __global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, const Unit* desc,
-                                                                 const int* ups_p, int n,
+                                                                 const int* maxq_p, int n,
                                                                  const int32_t* tokens,
                                                                  const float* logp_old) {
+    constexpr int QU = UNIT_THREADS * U;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int ups = *ups_p;  // units per record (max over the batch)
+    const int ups = (*maxq_p + QU - 1) / QU;  // units per record
     const int nu = n * ups;
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
         const int j = u / ups, c = u - j * ups;
         const Unit un = ld_unit(desc + j);
         const int nq = (un.len + 3) >> 2;  // destination (row) quads
-        if (un.row < 0 || c * QPU >= nq) continue;
+        if (un.row < 0 || c * QU >= nq) continue;
         const int a = (int)(un.off & 3);
         const int nsq = (a + un.len + 3) >> 2;  // source quads touched
-        const int kw = c * QPU + wid * 32 * UNIT_U;
+        const int kw = c * QU + wid * 32 * U;
         const size_t row = (size_t)un.row * v.stride;
-        uint4 ot[UNIT_U], ol[UNIT_U];
+        uint4 ot[U], ol[U];
         if (tokens)
-            packed_to_row_quads<UNIT_U>(reinterpret_cast<const uint4*>(tokens) + (un.off >> 2),
-                                        nsq, a, kw, ot);
+            packed_to_row_quads<U>(reinterpret_cast<const uint4*>(tokens) + (un.off >> 2), nsq, a,
+                                   kw, ot);
         if (logp_old)
-            packed_to_row_quads<UNIT_U>(reinterpret_cast<const uint4*>(logp_old) + (un.off >> 2),
-                                        nsq, a, kw, ol);
+            packed_to_row_quads<U>(reinterpret_cast<const uint4*>(logp_old) + (un.off >> 2), nsq,
+                                   a, kw, ol);
 #pragma unroll
-        for (int s = 0; s < UNIT_U; ++s) {
+        for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
             if (k < nq) {
                 if (tokens)
@@ -589,6 +591,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, cons
         }
     }
 }
+constexpr int PAYLOAD_U = 4;
 
 // ---------------------------------------------------------------- sample
 struct SampleArgs {
@@ -827,7 +830,7 @@ __device__ void sample_map_phase(const BufView& v, const SampleArgs& a) {
             a.off[i] = pos;
             reinterpret_cast<long long*>(&a.units[i])[2] = pos;  // Unit::off
             const int nq = ((int)(pos & 3) + L + 3) >> 2;
-            const int u = L ? (nq + QPU - 1) / QPU : 0;
+            const int u = L ? nq : 0;  // destination quads
             ups = u > ups ? u : ups;
             pos += L;
         };
@@ -850,7 +853,7 @@ __device__ void sample_map_phase(const BufView& v, const SampleArgs& a) {
         if (threadIdx.x == 0) {
             int m = 0;
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = s_u[w] > m ? s_u[w] : m;
-            *a.n_units = m;  // units per selection (max over the batch)
+            *a.n_units = m;  // max destination quads per selection
             RB_CLOCK(5);
             DevLossAcc* acc = a.acc;
             acc->obj_sum = 0.0;
@@ -900,32 +903,35 @@ __global__ void k_sample_records(BufView v, long long nsel, long long per,
 }
 
 // ---------------------------------------------------------------- gather
-// Persistent over the sampler's work units: QPU quads of one selection's
-// slot row -> the packed batch at its offset (funnel-shifted 128-bit stores;
-// boundary quads shared with the neighbouring trajectory use masked stores).
+// Persistent over nloc * ceil(max_nq / (128*U)) virtual units: 128*U quads of
+// one selection's slot row -> the packed batch at its offset (funnel-shifted
+// 128-bit stores; boundary quads shared with the neighbouring trajectory use
+// masked stores).
+template <int U>
 __global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* desc,
-                                                        const int* ups_p, int nloc,
+                                                        const int* maxq_p, int nloc,
                                                         int32_t* out_tok, float* out_lpo) {
+    constexpr int QU = UNIT_THREADS * U;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int ups = *ups_p;  // units per selection (max over the batch)
+    const int ups = (*maxq_p + QU - 1) / QU;  // units per selection
     const int nu = nloc * ups;
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
         const int b = u / ups, c = u - b * ups;
         const Unit un = ld_unit(desc + b);
         const int a = (int)(un.off & 3);
         const int nq = (a + un.len + 3) >> 2;
-        if (c * QPU >= nq) continue;
+        if (c * QU >= nq) continue;
         const int nsq = (un.len + 3) >> 2;
         const long long P0 = un.off >> 2;
-        const int kw = c * QPU + wid * 32 * UNIT_U;
+        const int kw = c * QU + wid * 32 * U;
         const size_t row = (size_t)un.row * v.stride;
-        uint4 ot[UNIT_U], ol[UNIT_U];
+        uint4 ot[U], ol[U];
         if (out_tok)
-            row_to_packed_quads<UNIT_U>(reinterpret_cast<const uint4*>(v.tok + row), nsq, a, kw, ot);
+            row_to_packed_quads<U>(reinterpret_cast<const uint4*>(v.tok + row), nsq, a, kw, ot);
         if (out_lpo)
-            row_to_packed_quads<UNIT_U>(reinterpret_cast<const uint4*>(v.lpo + row), nsq, a, kw, ol);
+            row_to_packed_quads<U>(reinterpret_cast<const uint4*>(v.lpo + row), nsq, a, kw, ol);
 #pragma unroll
-        for (int s = 0; s < UNIT_U; ++s) {
+        for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
             if (k < nq) {
                 if (out_tok)
@@ -938,6 +944,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* 
         }
     }
 }
+constexpr int GATHER_U = 8;
 
 // ---------------------------------------------------------------- inspect
 __global__ void k_shard_contents(BufView v, int s, long long n, rb_record* out) {
@@ -1208,8 +1215,16 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         int sms = 148;
         RB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         b->unit_grid = sms * UNIT_CTAS_PER_SM;
-        // the payload copy overlaps the sampler's draw CTA: leave it room
-        b->payload_grid = sms * (UNIT_CTAS_PER_SM - 2);
+        // Persistent grids: exactly the resident CTAs of each kernel.  The
+        // payload copy overlaps the sampler's draw CTA, so it leaves room.
+        int occ = 0;
+        RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<GATHER_U>,
+                                                              UNIT_THREADS, 0));
+        b->grid_gather = sms * std::max(occ, 1);
+        RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_insert_payload<PAYLOAD_U>,
+                                                              UNIT_THREADS, 0));
+        b->payload_grid = sms * std::max(occ - 2, 1);
+        b->grid_loss = loss_grid(sms);
         b->n_units_ins = dalloc<int>(1);
         b->n_units_sel = dalloc<int>(1);
         b->loss_partials = dalloc<char>((size_t)b->unit_grid * 32);
@@ -1253,7 +1268,7 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec) {
     k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
     RB_CUDA(cudaGetLastError());
     if (payload) {
-        k_insert_payload<<<b->payload_grid, UNIT_THREADS, 0, b->stream>>>(
+        k_insert_payload<PAYLOAD_U><<<b->payload_grid, UNIT_THREADS, 0, b->stream>>>(
             b->v, b->units_ins, b->n_units_ins, (int)bt.n, bt.tokens, bt.logp_old);
         RB_CUDA(cudaGetLastError());
     }
@@ -1670,7 +1685,7 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
         if (ht) dt = (int32_t*)stage;
         if (hl) dl = (float*)(stage + pb);
         if (nloc > 0 && (dt || dl)) {
-            k_gather<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(b->v, b->units_sel, b->n_units_sel, (int)nloc, dt, dl);
+            k_gather<GATHER_U><<<b->grid_gather, UNIT_THREADS, 0, b->stream>>>(b->v, b->units_sel, b->n_units_sel, (int)nloc, dt, dl);
             RB_CUDA(cudaGetLastError());
         }
         if (ht) RB_CUDA(cudaMemcpyAsync(out_tokens, dt, total * 4, cudaMemcpyDeviceToHost, b->stream));

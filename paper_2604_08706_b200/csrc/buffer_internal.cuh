@@ -55,6 +55,8 @@ struct BufView {
     DevCtl* ctl;
 };
 
+int loss_grid(int sms);  // loss.cu: resident CTAs of the loss kernels
+
 }  // namespace rb
 
 struct rb_buffer {
@@ -92,7 +94,7 @@ struct rb_buffer {
 
     // persistent-kernel work units (stream_copy.cuh)
     int unit_grid = 0;                  // SMs * UNIT_CTAS_PER_SM
-    int payload_grid = 0;
+    int payload_grid = 0, grid_gather = 0, grid_loss = 0;
     cudaStream_t aux = nullptr;         // sampler draws (overlap the insert)
     cudaEvent_t ev_draw = nullptr, ev_map = nullptr;
     rb::Unit* units_ins = nullptr;      // payload copy units of the last insert

@@ -262,51 +262,97 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
     }
 }
 
-// GRPO over the current batch: persistent over the sampler's work units.
-// Per token 12 B of compulsory traffic: logp_old (slot row, funnel-shifted to
-// the packed alignment), logp_now (packed) in, dlogp (packed) out.
+// Exact fp64 evaluation of one token, as the reference does (bandit.cpp:380-400).
+__device__ __noinline__ float grpo_token_exact(float lpn, float lpo, double A,
+                                               const GrpoParams& p, GrpoPartial& acc) {
+    const double rd = exp((double)lpn - (double)lpo);
+    if (!isfinite(rd)) {  // bandit.cpp:381-386
+        ++acc.exc;
+        return 0.f;
+    }
+    ++acc.inc;
+    const double c = rd < p.lo ? p.lo : (p.hi < rd ? p.hi : rd);  // std::clamp
+    const double uv = __dmul_rn(rd, A), cv = __dmul_rn(c, A);
+    if (uv <= cv) {  // ties -> unclipped (bandit.cpp:392)
+        acc.obj += uv;
+        return (float)(A * rd);
+    }
+    acc.obj += cv;
+    return 0.f;
+}
+
+// GRPO over the current batch: persistent over nloc * ceil(max_nq/(128*U))
+// virtual units.  Per token 12 B of compulsory traffic: logp_old (slot row,
+// funnel-shifted to the packed alignment) and logp_now (packed) in, dlogp out.
+// Fast path per token: one ex2, the branch as two threshold compares chosen
+// per unit from sign(A), and an fp32 per-unit objective sum; tokens near a
+// clip edge or with |d| >= 80 / non-finite take grpo_token_exact.
+template <int U>
 __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
-    BufView v, const Unit* units, const int* n_units, int nloc, const float* lpn_packed,
+    BufView v, const Unit* units, const int* maxq_p, int nloc, const float* lpn_packed,
     float* dlogp, GrpoParams prm, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats,
     const long long* n_local, int local_fix) {
+    constexpr int QU = UNIT_THREADS * U;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const float scale = -1.f / (float)acc->total_tokens;
-    const int ups = *n_units;  // units per selection (max over the batch)
+    const float tol_hi = 4e-6f * prm.hi_f, tol_lo = 4e-6f * prm.lo_f;
+    const int ups = (*maxq_p + QU - 1) / QU;
     const int nu = nloc * ups;
     GrpoPartial part;
+    long long inc_fast = 0;
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
         const int b = u / ups, c = u - b * ups;
         const Unit un = ld_unit(units + b);
         const int a = (int)(un.off & 3);
         const int nq = (a + un.len + 3) >> 2;
-        if (c * QPU >= nq) continue;
+        if (c * QU >= nq) continue;
         const int nsq = (un.len + 3) >> 2;
         const long long P0 = un.off >> 2;
-        const int kw = c * QPU + wid * 32 * UNIT_U;
-        uint4 now[UNIT_U], old[UNIT_U];
+        const int kw = c * QU + wid * 32 * U;
+        uint4 now[U], old[U];
 #pragma unroll
-        for (int s = 0; s < UNIT_U; ++s) {
+        for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
             now[s] = k < nq ? ld_stream(lpn_packed + 4 * (P0 + k)) : make_uint4(0, 0, 0, 0);
         }
-        row_to_packed_quads<UNIT_U>(
+        row_to_packed_quads<U>(
             reinterpret_cast<const uint4*>(v.lpo + (size_t)un.row * v.stride), nsq, a, kw, old);
         const double A = un.adv;
         const float Af = (float)A;
+        const float Afs = Af * scale;
         const int sgn = A > 0.0 ? 1 : (A < 0.0 ? -1 : 0);
+        const float thr_hi = sgn > 0 ? prm.hi_f : INFINITY;   // unclipped iff thr_lo <= r <= thr_hi
+        const float thr_lo = sgn < 0 ? prm.lo_f : -INFINITY;
+        const float clipv = sgn > 0 ? prm.hi_f : prm.lo_f;
         float fsum = 0.f;
 #pragma unroll
-        for (int s = 0; s < UNIT_U; ++s) {
+        for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
             if (k < nq) {
                 const int e0 = 4 * k - a;
+                const bool full = e0 >= 0 && e0 + 3 < un.len;
                 float o[4];
+                unsigned rare = 0;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    o[i] = 0.f;
-                    if (e0 + i >= 0 && e0 + i < un.len)
-                        o[i] = grpo_token_unit(qf(now[s], i), qf(old[s], i), A, Af, sgn, prm, part,
-                                               fsum) * scale;
+                    const bool valid = full || (e0 + i >= 0 && e0 + i < un.len);
+                    const float d = qf(now[s], i) - qf(old[s], i);
+                    const float r = __expf(d);
+                    const bool edge = !(fabsf(d) < 80.f) || fabsf(r - prm.hi_f) <= tol_hi ||
+                                      fabsf(r - prm.lo_f) <= tol_lo;
+                    const bool unc = r <= thr_hi && r >= thr_lo;
+                    const bool fast = valid && !edge;
+                    o[i] = (fast && unc) ? Afs * r : 0.f;
+                    fsum += fast ? (unc ? r : clipv) : 0.f;
+                    inc_fast += fast;
+                    rare |= (valid && edge) ? (1u << i) : 0u;
+                }
+                if (rare) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (rare & (1u << i))
+                            o[i] = grpo_token_exact(qf(now[s], i), qf(old[s], i), A, prm, part) *
+                                   scale;
                 }
                 store_quad_masked(reinterpret_cast<uint32_t*>(dlogp), P0 + k,
                                   make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]),
@@ -316,7 +362,22 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
         }
         part.obj += (double)fsum * A;
     }
+    part.inc += inc_fast;
     loss_commit(part, parts, acc, stats, 0, 0.0, dlogp, n_local, local_fix);
+}
+constexpr int LOSS_U = 4;
+
+template <int U>
+__global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
+    BufView v, const Unit* units, const int* maxq_p, int nloc, const float* lpn_packed,
+    float* dlogp, double delta_v, double inv_b, DevLossAcc* acc, Partial* parts,
+    rb_loss_stats* stats);
+
+int loss_grid(int sms) {
+    int a = 0, b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_loss_grpo_buf<LOSS_U>, UNIT_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_loss_asymre_buf<LOSS_U>, UNIT_THREADS, 0);
+    return sms * std::max(1, std::min(a, b));
 }
 
 // GRPO over explicit packed arrays (stateless API): CTA per trajectory.
@@ -359,13 +420,16 @@ __global__ void k_dlogp_rescale(float* d, long long n, const long long* n_dev,
 }
 
 // AsymRE over the current batch: dlogp = -coef/B on every token.
-// AsymRE over the current batch (persistent over the work units): 8 B/token,
+// AsymRE over the current batch (persistent over the virtual units): 8 B/token,
 // logp_now in, dlogp = -coef/B out; objective sum coef * sum_t logp_now.
+template <int U>
 __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
-    BufView v, const Unit* units, const int* n_units, int nloc, const float* lpn_packed,
-    float* dlogp, double delta_v, double inv_b, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats) {
+    BufView v, const Unit* units, const int* maxq_p, int nloc, const float* lpn_packed,
+    float* dlogp, double delta_v, double inv_b, DevLossAcc* acc, Partial* parts,
+    rb_loss_stats* stats) {
+    constexpr int QU = UNIT_THREADS * U;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int ups = *n_units;
+    const int ups = (*maxq_p + QU - 1) / QU;
     const int nu = nloc * ups;
     GrpoPartial part;
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
@@ -373,22 +437,22 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
         const Unit un = ld_unit(units + b);
         const int a = (int)(un.off & 3);
         const int nq = (a + un.len + 3) >> 2;
-        if (c * QPU >= nq) continue;
+        if (c * QU >= nq) continue;
         const long long P0 = un.off >> 2;
-        const int kw = c * QPU + wid * 32 * UNIT_U;
+        const int kw = c * QU + wid * 32 * U;
         const double coef = v.reward[un.g] - (v.gmean[un.g] + delta_v);  // bandit.cpp:429
         const float gc = (float)(coef * -inv_b);
         const uint4 gq = make_uint4(__float_as_uint(gc), __float_as_uint(gc), __float_as_uint(gc),
                                     __float_as_uint(gc));
-        uint4 now[UNIT_U];
+        uint4 now[U];
 #pragma unroll
-        for (int s = 0; s < UNIT_U; ++s) {
+        for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
             now[s] = k < nq ? ld_stream(lpn_packed + 4 * (P0 + k)) : make_uint4(0, 0, 0, 0);
         }
         float fs = 0.f;
 #pragma unroll
-        for (int s = 0; s < UNIT_U; ++s) {
+        for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
             if (k < nq) {
                 const int e0 = 4 * k - a;
@@ -678,7 +742,7 @@ int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double e
             // Single-process buffers rescale in the last CTA when a token was
             // excluded; multi-rank buffers defer to rb_loss_finalize.
             const int local_fix = b->sb == 0 && b->se == b->T;
-            k_loss_grpo_buf<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(
+            k_loss_grpo_buf<LOSS_U><<<b->grid_loss, UNIT_THREADS, 0, b->stream>>>(
                 b->v, b->units_sel, b->n_units_sel, (int)(hi - lo), logp_now, out_dlogp, p, b->acc,
                 (Partial*)b->loss_partials, kst, b->sel_total, local_fix);
             RB_CUDA(cudaGetLastError());
@@ -714,7 +778,7 @@ int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double
         const bool dev_stats = stats && is_device_ptr(stats);
         rb_loss_stats* kst = dev_stats ? stats : (stats ? (rb_loss_stats*)b->scratch(64) : nullptr);
         if (hi > lo) {
-            k_loss_asymre_buf<<<b->unit_grid, UNIT_THREADS, 0, b->stream>>>(
+            k_loss_asymre_buf<LOSS_U><<<b->grid_loss, UNIT_THREADS, 0, b->stream>>>(
                 b->v, b->units_sel, b->n_units_sel, (int)(hi - lo), logp_now, out_dlogp, delta_v,
                 inv_b, b->acc,
                 (Partial*)b->loss_partials, kst);
