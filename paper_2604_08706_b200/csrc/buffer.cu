@@ -26,6 +26,8 @@
 #include "rng_internal.cuh"
 #include "stream_copy.cuh"
 
+#include <cooperative_groups.h>
+
 using namespace rb;
 
 namespace rb {
@@ -871,6 +873,257 @@ __global__ void __launch_bounds__(1024) k_sample_map(BufView v, SampleArgs a) {
     sample_map_phase(v, a);
 }
 
+// ---------------------------------------------------------------- cooperative
+// Multi-CTA versions of the two latency-bound steps for the common case
+// (FIFO retention, ids promised unique; uniform sampling).  One record /
+// selection per thread, one grid barrier between the read and write phases,
+// so the dependent-load chains run once per thread instead of serially.
+namespace cg = cooperative_groups;
+constexpr int COOP_THREADS = 256;
+
+// FIFO routing + eviction + group advantages + metadata scatter
+// (replay_buffer.cpp:83-133 closed form; bandit.cpp:276-294 per group).
+__global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, InsertIn in) {
+    cg::grid_group grid = cg::this_grid();
+    const int n = (int)in.n;
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, gn = gridDim.x * blockDim.x;
+    DevCtl* ctl = v.ctl;
+    const int sticky = ctl->err_code;
+    const unsigned long long cur0 = ctl->cursor;
+    const int T = v.T, C = v.C;
+    const int c0 = (int)(cur0 % (unsigned long long)T);
+    int bad = 0;
+    if (!sticky) {
+        for (int j = gt; j < n; j += gn) {
+            long long l = in.toff ? in.toff[j + 1] - in.toff[j] : 0;
+            if (l < 0 || l > in.maxlen) {
+                bad |= 2;
+                l = 0;
+            }
+            in.len[j] = (int32_t)l;
+            const uint64_t x = in.id[j];
+            if (j > 0 ? x <= in.id[j - 1] : (ctl->has_any && x <= ctl->max_id)) bad |= 1;
+            if (in.adv) {
+                in.adv_out[j] = in.adv[j];
+                in.gmean_out[j] = in.gmean ? in.gmean[j] : 0.0;
+            }
+            int s = c0 + j % T;
+            if (s >= T) s -= T;
+            const int rank = j / T, j0 = j % T;
+            const int ns = (n - 1 - j0) / T + 1;
+            const long long P = v.pushes[s];
+            int x2 = (int)(P % C) + rank % C;
+            if (x2 >= C) x2 -= C;
+            const size_t g = (size_t)s * C + (size_t)x2;
+            in.tslot[j] = (int32_t)g;
+            in.surv[j] = (rank + C >= ns);
+            uint64_t ev = NONE_ID;
+            if (P + rank >= C) ev = rank >= C ? in.id[j - C * T] : v.id[g];
+            in.evid[j] = ev;
+        }
+        if (!in.adv) {
+            if (gt == 0 && (in.goff[0] != 0 || in.goff[in.ngroups] != n)) bad |= 4;
+            for (long long gi = gt; gi < in.ngroups; gi += gn) {
+                const long long b = in.goff[gi], e = in.goff[gi + 1], m = e - b;
+                if (m < 2 || b < 0 || e > n) {
+                    bad |= 4;
+                    continue;
+                }
+                const double dn = (double)m;
+                double mean = 0.0;
+#pragma unroll 8
+                for (long long k = b; k < e; ++k) mean = __dadd_rn(mean, in.reward[k]);
+                mean = __ddiv_rn(mean, dn);
+                double var = 0.0;
+#pragma unroll 8
+                for (long long k = b; k < e; ++k) {
+                    const double d = __dsub_rn(in.reward[k], mean);
+                    var = __dadd_rn(var, __dmul_rn(d, d));
+                }
+                var = __ddiv_rn(var, dn);
+                const double sd = __dsqrt_rn(var);
+#pragma unroll 8
+                for (long long k = b; k < e; ++k) {
+                    in.adv_out[k] = sd < 1e-8 ? 0.0 : __ddiv_rn(__dsub_rn(in.reward[k], mean), sd);
+                    in.gmean_out[k] = mean;
+                }
+            }
+        }
+    }
+    if (bad) atomicOr(&ctl->batch_bad, bad);
+    if (gt == 0) *in.n_units = 0;
+    grid.sync();
+    const int bb = sticky ? 8 : *(volatile int*)&ctl->batch_bad;
+    if (bb) {  // nothing is applied; the error is sticky until rb_check
+        for (int j = gt; j < n; j += gn) {
+            in.surv[j] = 0;
+            in.tslot[j] = -1;
+            in.evid[j] = NONE_ID;
+            in.units[j].row = -1;
+        }
+        if (gt == 0 && !sticky) {
+            ctl->err_code = RB_EINVAL;
+            ctl->err_index = (bb & 2) ? -3 : (bb & 4) ? -2 : -4;
+        }
+    } else {
+        int maxq = 0;
+        for (int j = gt; j < n; j += gn) {
+            const int g = in.tslot[j];
+            Unit d;
+            d.row = -1;
+            d.len = in.len[j];
+            d.k0 = 0;
+            d.g = j;
+            d.off = in.toff ? in.toff[j] : 0;
+            d.adv = 0.0;
+            if (in.surv[j]) {
+                write_meta(v, (size_t)g, in, j);
+                const int s = g / C;
+                if (s >= v.sb && s < v.se && d.len > 0 && v.stride > 0) {
+                    d.row = (s - v.sb) * C + (g - s * C);
+                    const int q = (d.len + 3) >> 2;
+                    maxq = q > maxq ? q : maxq;
+                }
+            }
+            in.units[j] = d;
+        }
+        maxq = __reduce_max_sync(0xffffffffu, maxq);
+        if ((threadIdx.x & 31) == 0 && maxq) atomicMax(in.n_units, maxq);
+        for (int s = gt; s < T; s += gn) {
+            const int j0 = ((s - c0) % T + T) % T;
+            const int ns = n > j0 ? (n - 1 - j0) / T + 1 : 0;
+            v.pushes[s] += ns;
+        }
+        if (gt == 0) {
+            ctl->cursor = (cur0 + (unsigned long long)n) % T;
+            ctl->max_id = in.id[n - 1];  // strictly increasing and above the old max
+            ctl->has_any = 1;
+            ctl->hash_stale = 1;
+        }
+    }
+    grid.sync();
+    if (gt == 0) ctl->batch_bad = 0;
+}
+
+// Sampler map phase, cooperative: slots, use counts, lengths, descriptors,
+// packed offsets (per-CTA sums + a grid barrier + per-CTA scan).
+__global__ void __launch_bounds__(COOP_THREADS) k_sample_map_coop(BufView v, SampleArgs a,
+                                                                  long long* cta_sums) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int s_head[64];
+    __shared__ long long s_red[2][32];
+    const int nsh_h = a.nsh < 64 ? a.nsh : 0;
+    for (int s = threadIdx.x; s < nsh_h; s += blockDim.x) s_head[s] = shard_head(v, s);
+    __syncthreads();
+    const long long nsel = a.nsel;
+    const long long per_cta = (nsel + gridDim.x - 1) / gridDim.x;
+    const long long i0 = blockIdx.x * per_cta;
+    const long long i1 = i0 + per_cta < nsel ? i0 + per_cta : nsel;
+    long long own_sum = 0, all_sum = 0;
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const int s = a.sel_shard[i];
+        const int head = nsh_h ? s_head[s] : shard_head(v, s);
+        const int g = s * v.C + arrival_slot_h(v, s, a.sel_index[i], head);
+        a.sel_slot[i] = g;
+        const int L = v.len[g];
+        const double adv = v.adv[g];
+        atomicAdd(&v.use[g], 1u);
+        a.sel_len[i] = L;
+        all_sum += L;
+        if (i >= a.lo && i < a.hi) {
+            own_sum += L;
+            Unit d;
+            d.row = (s - v.sb) * v.C + (g - s * v.C);
+            d.len = L;
+            d.k0 = 0;
+            d.g = g;
+            d.off = 0;
+            d.adv = adv;
+            a.units[i - a.lo] = d;
+        }
+    }
+    own_sum = warp_sum_i64(own_sum);
+    all_sum = warp_sum_i64(all_sum);
+    if ((threadIdx.x & 31) == 0) {
+        s_red[0][threadIdx.x >> 5] = own_sum;
+        s_red[1][threadIdx.x >> 5] = all_sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long o = 0, t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            o += s_red[0][w];
+            t += s_red[1][w];
+        }
+        cta_sums[2 * blockIdx.x] = o;
+        cta_sums[2 * blockIdx.x + 1] = t;
+        if (blockIdx.x == 0) *a.n_units = 0;
+    }
+    grid.sync();
+    // base of this CTA = owned lengths of all earlier CTAs
+    long long base = 0, total = 0, gtotal = 0;
+    for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
+        const long long o = __ldcg(&cta_sums[2 * c]);
+        if (c < (int)blockIdx.x) base += o;
+        total += o;
+        gtotal += __ldcg(&cta_sums[2 * c + 1]);
+    }
+    base = warp_sum_i64(base);
+    total = warp_sum_i64(total);
+    gtotal = warp_sum_i64(gtotal);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        s_red[0][threadIdx.x >> 5] = base;
+        s_red[1][threadIdx.x >> 5] = total;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long b2 = 0, t2 = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            b2 += s_red[0][w];
+            t2 += s_red[1][w];
+        }
+        s_red[0][0] = b2;
+        s_red[1][0] = t2;
+    }
+    __syncthreads();
+    long long carry = s_red[0][0];
+    total = s_red[1][0];
+    int maxq = 0;
+    // scan this CTA's owned selections in chunks of blockDim, carrying across
+    const long long lo = a.lo;
+    const long long o0 = i0 > a.lo ? i0 : a.lo, o1 = i1 < a.hi ? i1 : a.hi;
+    for (long long cb = o0; cb < o1; cb += blockDim.x) {
+        const long long i = cb + threadIdx.x;
+        const long long L = i < o1 ? a.sel_len[i] : 0;
+        long long chunk_total;
+        const long long ex = block_exclusive_scan(L, &chunk_total);
+        if (i < o1) {
+            const long long pos = carry + ex;
+            a.off[i - lo] = pos;
+            reinterpret_cast<long long*>(&a.units[i - lo])[2] = pos;  // Unit::off
+            const int nq = ((int)(pos & 3) + (int)L + 3) >> 2;
+            if (L) maxq = nq > maxq ? nq : maxq;
+        }
+        carry += chunk_total;
+    }
+    maxq = __reduce_max_sync(0xffffffffu, maxq);
+    if ((threadIdx.x & 31) == 0 && maxq) atomicMax(a.n_units, maxq);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.off[a.hi - a.lo] = total;
+        a.totals[0] = total;
+        a.totals[1] = gtotal;
+        DevLossAcc* acc = a.acc;
+        acc->obj_sum = 0.0;
+        acc->included = 0;
+        acc->excluded = 0;
+        acc->done_blocks = 0;
+        acc->total_tokens = gtotal;
+        acc->objective = 0.0;
+        acc->need_fixup = 0;
+    }
+}
+
 // Record copies with the post-increment use count in draw order
 // (replay_buffer.cpp:201-202) and optional UseEvents (205-215).
 __global__ void k_sample_records(BufView v, long long nsel, long long per,
@@ -988,7 +1241,7 @@ rb_buffer::~rb_buffer() {
                     v.correct, v.use, v.len, v.order, v.head, v.pushes, v.owner, v.tok, v.lpo,
                     v.hkeys, v.hstate, v.ctl, s_tslot, s_surv, s_evid, s_evrec, s_adv, s_gmean,
                     s_len, s_toff, sel_slot, sel_shard, sel_index, sel_off, sel_total,
-                    acc, misc, n_units_ins, n_units_sel, loss_partials};
+                    acc, misc, n_units_ins, n_units_sel, loss_partials, coop_sums};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : stage_dev)
@@ -1116,6 +1369,8 @@ void check_sticky(rb_buffer* b) {
         RB_CUDA(cudaStreamSynchronize(b->stream));
         if (c.err_index == -2) invalid("group advantages need >= 2 rewards");
         if (c.err_index == -3) invalid("rb_insert: trajectory length exceeds max_tokens");
+        if (c.err_index == -4)
+            invalid("rb_insert: RB_INSERT_ASSUME_UNIQUE violated (ids not new and strictly increasing)");
         invalid("ShardedReplayBuffer: rollout id " + std::to_string(c.err_id) +
                 " is already stored");
     }
@@ -1225,6 +1480,13 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
                                                               UNIT_THREADS, 0));
         b->payload_grid = sms * std::max(occ - 2, 1);
         b->grid_loss = loss_grid(sms);
+        RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_insert_route_fifo,
+                                                              COOP_THREADS, 0));
+        b->coop_route_max = sms * std::max(occ, 1);
+        RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sample_map_coop,
+                                                              COOP_THREADS, 0));
+        b->coop_map_max = sms * std::max(occ, 1);
+        b->coop_sums = dalloc<long long>(2 * (size_t)b->coop_map_max);
         b->n_units_ins = dalloc<int>(1);
         b->n_units_sel = dalloc<int>(1);
         b->loss_partials = dalloc<char>((size_t)b->unit_grid * 32);
@@ -1237,7 +1499,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
 }
 
 // Insert `bt` (pointers already resolved to device memory; lens/toff device)
-void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec) {
+void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, bool unique) {
     InsertIn in{};
     in.n = (long long)bt.n;
     in.id = bt.rollout_id;
@@ -1265,13 +1527,31 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec) {
     in.units = b->units_ins;
     in.n_units = b->n_units_ins;
     if (!payload) in.toff = bt.tok_offsets;  // lengths only
-    k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
+    if (unique && b->retention == RB_PLAIN_FIFO && !want_evrec && bt.n <= (size_t)INT32_MAX) {
+        // ids promised new and increasing: the cooperative FIFO kernel
+        const int grid = (int)std::min<size_t>((bt.n + COOP_THREADS - 1) / COOP_THREADS,
+                                               (size_t)b->coop_route_max);
+        void* args[] = {(void*)&b->v, (void*)&in};
+        RB_CUDA(cudaLaunchCooperativeKernel((void*)k_insert_route_fifo, dim3(std::max(grid, 1)),
+                                            dim3(COOP_THREADS), args, 0, b->stream));
+    } else {
+        k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
+    }
     RB_CUDA(cudaGetLastError());
     if (payload) {
         k_insert_payload<PAYLOAD_U><<<b->payload_grid, UNIT_THREADS, 0, b->stream>>>(
             b->v, b->units_ins, b->n_units_ins, (int)bt.n, bt.tokens, bt.logp_old);
         RB_CUDA(cudaGetLastError());
     }
+}
+
+void launch_map(rb_buffer* b, SampleArgs& a) {
+    const long long grid =
+        std::max<long long>(1, std::min<long long>((a.nsel + COOP_THREADS - 1) / COOP_THREADS,
+                                                   (long long)b->coop_map_max));
+    void* args[] = {(void*)&b->v, (void*)&a, (void*)&b->coop_sums};
+    RB_CUDA(cudaLaunchCooperativeKernel((void*)k_sample_map_coop, dim3((unsigned)grid),
+                                        dim3(COOP_THREADS), args, 0, b->stream));
 }
 
 }  // namespace
@@ -1443,7 +1723,7 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
             }
         }
         const bool want_evrec = (flags & 0x100) != 0;  // internal: rb_push
-        launch_insert(b, bt, want_evrec);
+        launch_insert(b, bt, want_evrec, (flags & RB_INSERT_ASSUME_UNIQUE) != 0);
         if (out_evicted_ids) {
             RB_CUDA(cudaMemcpyAsync(out_evicted_ids, b->s_evid, n * 8, cudaMemcpyDefault,
                                     b->stream));
@@ -1576,8 +1856,7 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 RB_CUDA(cudaEventRecord(b->ev_draw, b->aux));
                 RB_CUDA(cudaStreamWaitEvent(b->stream, b->ev_draw, 0));
             }
-            k_sample_map<<<1, 1024, 0, b->stream>>>(b->v, a);
-            RB_CUDA(cudaGetLastError());
+            launch_map(b, a);
             RB_CUDA(cudaEventRecord(b->ev_map, b->stream));
         } else {
             if (nsh > 0) {
@@ -1587,8 +1866,7 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 RB_CUDA(cudaGetLastError());
                 rng->used_on(b->stream);
             }
-            k_sample_map<<<1, 1024, 0, b->stream>>>(b->v, a);
-            RB_CUDA(cudaGetLastError());
+            launch_map(b, a);
             RB_CUDA(cudaEventRecord(b->ev_map, b->stream));
         }
         b->B = nsel;

@@ -29,7 +29,7 @@ struct DevCtl {
     int err_code;  // sticky asynchronous error (RB_EINVAL)
     int has_any;   // max_id valid
     int hash_stale;
-    int pad;
+    int batch_bad;  // per-launch error flags of the cooperative insert (reset on exit)
 };
 
 // Everything a kernel needs, passed by value.
@@ -95,6 +95,8 @@ struct rb_buffer {
     // persistent-kernel work units (stream_copy.cuh)
     int unit_grid = 0;                  // SMs * UNIT_CTAS_PER_SM
     int payload_grid = 0, grid_gather = 0, grid_loss = 0;
+    int coop_route_max = 0, coop_map_max = 0;  // co-resident CTAs of the cooperative kernels
+    long long* coop_sums = nullptr;           // [2 * coop_map_max]
     cudaStream_t aux = nullptr;         // sampler draws (overlap the insert)
     cudaEvent_t ev_draw = nullptr, ev_map = nullptr;
     rb::Unit* units_ins = nullptr;      // payload copy units of the last insert

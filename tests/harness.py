@@ -39,6 +39,7 @@ class StepConfig:
     delta_v: float = -0.1
     prompts: int = 16
     device_inputs: bool = True   # torch CUDA tensors (hot path) vs numpy host arrays
+    assume_unique: bool = False  # RB_INSERT_ASSUME_UNIQUE (cooperative FIFO insert kernel)
 
     @property
     def per_step(self):
@@ -93,7 +94,7 @@ def _to(x, dev):
     return torch.from_numpy(np.ascontiguousarray(x)).to(dev) if dev else x
 
 
-def insert_groups(buf, rec, toff, tok, lpo, group, dev):
+def insert_groups(buf, rec, toff, tok, lpo, group, dev, assume_unique=False):
     n = rec.shape[0]
     goff = np.arange(0, n + 1, group, dtype=np.int64)
     ev = np.zeros(n, np.uint64)
@@ -104,7 +105,10 @@ def insert_groups(buf, rec, toff, tok, lpo, group, dev):
                reward=_to(rec["reward"].copy(), dev),
                behavior_logprob=_to(rec["behavior_logprob"].copy(), dev),
                group_offsets=_to(goff, dev), tok_offsets=_to(toff, dev), tokens=_to(tok, dev),
-               logp_old=_to(lpo, dev), evicted=ev)
+               logp_old=_to(lpo, dev), evicted=ev, assume_unique=assume_unique)
+    if assume_unique:
+        buf.synchronize()  # the evicted-id copy is asynchronous
+        buf.check()
     return ev
 
 
@@ -130,7 +134,7 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
         for i, r in enumerate(rec):
             lengths[int(r["rollout_id"])] = int(length[i])
             gmeans[int(r["rollout_id"])] = gmean[i]
-        ev = insert_groups(gbuf, rec, toff, tok, lpo, cfg.group, dev)
+        ev = insert_groups(gbuf, rec, toff, tok, lpo, cfg.group, dev, cfg.assume_unique)
         for i, r in enumerate(rec):
             e = obuf.push(r)
             want = np.uint64(np.iinfo(np.uint64).max) if e is None else e["rollout_id"]
@@ -167,7 +171,9 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
         gt = torch.zeros(pad, dtype=torch.int32, device="cuda:0")
         gl = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
         go = torch.zeros(len(ids) + 1, dtype=torch.int64, device="cuda:0")
+        torch.cuda.synchronize()  # inputs written on torch's stream
         gbuf.gather(gt, gl, go)
+        gbuf.synchronize()  # the library runs on its own stream
         assert np.array_equal(go.cpu().numpy(), off), "packed offsets mismatch"
         assert np.array_equal(gt[:tot].cpu().numpy(), tok_want), f"gathered tokens mismatch step {step}"
         assert np.array_equal(gl[:tot].cpu().numpy(), lpo_want), f"gathered logp_old mismatch step {step}"
@@ -179,6 +185,7 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
         lpn_d = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
         lpn_d[:tot] = torch.from_numpy(lpn)
         dl = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
+        torch.cuda.synchronize()
         if cfg.loss == "grpo":
             st = gbuf.loss_grpo(lpn_d, dl, cfg.eps_low, cfg.eps_high)
             d_want, obj, inc, exc = ora.loss_grpo_tokens(lpn, lpo_want, orec["advantage"], off,
@@ -189,6 +196,7 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
             st = gbuf.loss_asymre(lpn_d, dl, cfg.delta_v)
             gm = np.array([gmeans[int(i)] for i in ids])
             d_want, obj = ora.loss_asymre_tokens(lpn, orec["reward"], gm, off, cfg.delta_v)
+        gbuf.synchronize()
         got = dl[:tot].cpu().numpy()
         np.testing.assert_allclose(got, d_want, rtol=1e-5, atol=1e-12,
                                    err_msg=f"dlogp mismatch step {step}")

@@ -149,6 +149,24 @@ def test_batched_duplicate_applies_prefix(rb):
     assert b.route_cursor() == 1
 
 
+def test_assume_unique_violation_is_sticky(rb):
+    """RB_INSERT_ASSUME_UNIQUE: a broken promise applies nothing and is reported later."""
+    from oracle.pyoracle import RECORD_DTYPE
+
+    b = rb.ShardedReplayBuffer(2, 8)
+    recs = np.array([make_record(i) for i in (1, 2, 3)], RECORD_DTYPE)
+    b.insert(rollout_id=recs["rollout_id"].copy(), reward=recs["reward"].copy(),
+             advantage=recs["advantage"].copy(), assume_unique=True)
+    b.check()
+    bad = np.array([make_record(i) for i in (4, 4)], RECORD_DTYPE)
+    b.insert(rollout_id=bad["rollout_id"].copy(), reward=bad["reward"].copy(),
+             advantage=bad["advantage"].copy(), assume_unique=True)
+    with pytest.raises(ValueError, match="ASSUME_UNIQUE"):
+        b.check()
+    b.check()  # cleared
+    assert sorted(ids(b.shard_contents(0)) + ids(b.shard_contents(1))) == [1, 2, 3]
+
+
 def test_sample_validation(rb):
     """test_buffer_core.cpp:347-359"""
     b = rb.ShardedReplayBuffer(2, 8, strategy="uniform_without_replacement")
@@ -318,6 +336,12 @@ STEP_CASES = {
                               retention="positive_bias", delta=0.5, loss="asymre", seed=2),
     "c3_ragged": dict(capacity=128, shards=1, batch=64, group=16, lmax=257, ragged=True, seed=3),
     "c4_sharded": dict(capacity=256, shards=4, batch=64, group=16, lmax=96, ragged=True, seed=4),
+    "c4_sharded_unique": dict(capacity=256, shards=4, batch=64, group=16, lmax=96, ragged=True,
+                              seed=14, assume_unique=True),
+    "c3_ragged_unique": dict(capacity=128, shards=1, batch=64, group=16, lmax=257, ragged=True,
+                             seed=13, assume_unique=True),
+    "big_batch_unique": dict(capacity=32, shards=2, batch=16, group=8, lmax=12, ragged=True,
+                             seed=18, workers=16, trainers=1, mu=1.0, assume_unique=True),
     "host_inputs": dict(capacity=60, shards=3, batch=30, group=6, lmax=33, ragged=True, seed=5,
                         device_inputs=False),
     "without_repl": dict(capacity=96, shards=2, batch=32, group=8, lmax=20, ragged=True, seed=6,

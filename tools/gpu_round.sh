@@ -9,7 +9,7 @@ mkdir -p $out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active --format=csv > $out/gpu.txt 2>&1
 
 if [[ $what == tests || $what == all ]]; then
-  timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 > $out/pytest_gpu.log 2>&1
+  timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 --durations=8 > $out/pytest_gpu.log 2>&1
   tail -15 $out/pytest_gpu.log
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1
   tail -3 $out/smoke.log
