@@ -1366,7 +1366,12 @@ void check_sticky(rb_buffer* b) {
         z.err_code = 0;
         z.err_index = 0;
         RB_CUDA(cudaMemcpyAsync(b->v.ctl, &z, sizeof z, cudaMemcpyHostToDevice, b->stream));
+        // The host mirrors assumed every asynchronous insert applied: resync
+        // them from the device, which is authoritative.
+        RB_CUDA(cudaMemcpyAsync(b->h_pushes.data(), b->v.pushes, b->T * sizeof(long long),
+                                cudaMemcpyDeviceToHost, b->stream));
         RB_CUDA(cudaStreamSynchronize(b->stream));
+        b->h_cursor = (size_t)c.cursor;
         if (c.err_index == -2) invalid("group advantages need >= 2 rewards");
         if (c.err_index == -3) invalid("rb_insert: trajectory length exceeds max_tokens");
         if (c.err_index == -4)

@@ -28,7 +28,7 @@ if [[ $what == ncu || $what == all ]]; then
       python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $out/ncu_bench.log 2>&1
   echo "launches: $(grep -c k_ $out/launches.csv)"
   # full captures of the heavy kernels in steady state
-  for k in k_loss_grpo_buf k_gather k_insert_payload k_insert_route k_sample_with k_sample_map; do
+  for k in ${NCU_KERNELS:-k_loss_grpo_buf k_gather k_insert_payload k_insert_route_fifo k_sample_draw k_sample_map_coop}; do
     timeout 600 $NCU --set full --clock-control none --import-source on -k regex:"^$k\$" -s 4 -c 1 \
         -o $out/prof_$k -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e \
         > $out/ncu_$k.log 2>&1
