@@ -563,9 +563,12 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, cons
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int ups = (*maxq_p + QU - 1) / QU;  // units per record
     const int nu = n * ups;
+    Unit nxt;  // descriptor of the next unit, loaded one unit ahead
+    if ((int)blockIdx.x < nu) nxt = ld_unit(desc + blockIdx.x / ups);
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
         const int j = u / ups, c = u - j * ups;
-        const Unit un = ld_unit(desc + j);
+        const Unit un = nxt;
+        if (u + (int)gridDim.x < nu) nxt = ld_unit(desc + (u + (int)gridDim.x) / ups);
         const int nq = (un.len + 3) >> 2;  // destination (row) quads
         if (un.row < 0 || c * QU >= nq) continue;
         const int a = (int)(un.off & 3);
@@ -888,6 +891,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
     const int n = (int)in.n;
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, gn = gridDim.x * blockDim.x;
     DevCtl* ctl = v.ctl;
+    RB_CLOCK(20);
     const int sticky = ctl->err_code;
     const unsigned long long cur0 = ctl->cursor;
     const int T = v.T, C = v.C;
@@ -950,9 +954,11 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
             }
         }
     }
+    RB_CLOCK(21);
     if (bad) atomicOr(&ctl->batch_bad, bad);
     if (gt == 0) *in.n_units = 0;
     grid.sync();
+    RB_CLOCK(22);
     const int bb = sticky ? 8 : *(volatile int*)&ctl->batch_bad;
     if (bb) {  // nothing is applied; the error is sticky until rb_check
         for (int j = gt; j < n; j += gn) {
@@ -987,6 +993,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
             }
             in.units[j] = d;
         }
+        RB_CLOCK(23);
         maxq = __reduce_max_sync(0xffffffffu, maxq);
         if ((threadIdx.x & 31) == 0 && maxq) atomicMax(in.n_units, maxq);
         for (int s = gt; s < T; s += gn) {
@@ -1003,6 +1010,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
     }
     grid.sync();
     if (gt == 0) ctl->batch_bad = 0;
+    RB_CLOCK(24);
 }
 
 // Sampler map phase, cooperative: slots, use counts, lengths, descriptors,
@@ -1010,6 +1018,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
 __global__ void __launch_bounds__(COOP_THREADS) k_sample_map_coop(BufView v, SampleArgs a,
                                                                   long long* cta_sums) {
     cg::grid_group grid = cg::this_grid();
+    RB_CLOCK(30);
     __shared__ int s_head[64];
     __shared__ long long s_red[2][32];
     const int nsh_h = a.nsh < 64 ? a.nsh : 0;
@@ -1042,6 +1051,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_sample_map_coop(BufView v, Sam
             a.units[i - a.lo] = d;
         }
     }
+    RB_CLOCK(31);
     own_sum = warp_sum_i64(own_sum);
     all_sum = warp_sum_i64(all_sum);
     if ((threadIdx.x & 31) == 0) {
@@ -1060,6 +1070,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_sample_map_coop(BufView v, Sam
         if (blockIdx.x == 0) *a.n_units = 0;
     }
     grid.sync();
+    RB_CLOCK(32);
     // base of this CTA = owned lengths of all earlier CTAs
     long long base = 0, total = 0, gtotal = 0;
     for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
@@ -1107,6 +1118,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_sample_map_coop(BufView v, Sam
         }
         carry += chunk_total;
     }
+    RB_CLOCK(33);
     maxq = __reduce_max_sync(0xffffffffu, maxq);
     if ((threadIdx.x & 31) == 0 && maxq) atomicMax(a.n_units, maxq);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1168,9 +1180,12 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int ups = (*maxq_p + QU - 1) / QU;  // units per selection
     const int nu = nloc * ups;
+    Unit nxt;  // descriptor of the next unit, loaded one unit ahead
+    if ((int)blockIdx.x < nu) nxt = ld_unit(desc + blockIdx.x / ups);
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
         const int b = u / ups, c = u - b * ups;
-        const Unit un = ld_unit(desc + b);
+        const Unit un = nxt;
+        if (u + (int)gridDim.x < nu) nxt = ld_unit(desc + (u + (int)gridDim.x) / ups);
         const int a = (int)(un.off & 3);
         const int nq = (a + un.len + 3) >> 2;
         if (c * QU >= nq) continue;

@@ -300,9 +300,12 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
     const int nu = nloc * ups;
     GrpoPartial part;
     long long inc_fast = 0;
+    Unit nxt;  // descriptor of the next unit, loaded one unit ahead
+    if ((int)blockIdx.x < nu) nxt = ld_unit(units + blockIdx.x / ups);
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
         const int b = u / ups, c = u - b * ups;
-        const Unit un = ld_unit(units + b);
+        const Unit un = nxt;
+        if (u + (int)gridDim.x < nu) nxt = ld_unit(units + (u + (int)gridDim.x) / ups);
         const int a = (int)(un.off & 3);
         const int nq = (a + un.len + 3) >> 2;
         if (c * QU >= nq) continue;
@@ -320,10 +323,13 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
         const double A = un.adv;
         const float Af = (float)A;
         const float Afs = Af * scale;
+        // Per unit the branch depends on one threshold only: A > 0 clips above
+        // 1+eps_high (r near 1-eps_low is unclipped either way), A < 0 below
+        // 1-eps_low, A = 0 never contributes.  Only tokens within tol of that
+        // threshold, or with d >= 80 / NaN (fp32 overflow vs fp64), go exact.
         const int sgn = A > 0.0 ? 1 : (A < 0.0 ? -1 : 0);
-        const float thr_hi = sgn > 0 ? prm.hi_f : INFINITY;   // unclipped iff thr_lo <= r <= thr_hi
-        const float thr_lo = sgn < 0 ? prm.lo_f : -INFINITY;
-        const float clipv = sgn > 0 ? prm.hi_f : prm.lo_f;
+        const float thr = sgn > 0 ? prm.hi_f : prm.lo_f;
+        const float tol = sgn > 0 ? tol_hi : tol_lo;
         float fsum = 0.f;
 #pragma unroll
         for (int s = 0; s < U; ++s) {
@@ -331,26 +337,42 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
             if (k < nq) {
                 const int e0 = 4 * k - a;
                 const bool full = e0 >= 0 && e0 + 3 < un.len;
-                float o[4];
-                unsigned rare = 0;
+                float o[4] = {0.f, 0.f, 0.f, 0.f};
+                bool slow = !full;
+                if (full) {
+                    float r[4];
+                    bool edge = false;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const bool valid = full || (e0 + i >= 0 && e0 + i < un.len);
-                    const float d = qf(now[s], i) - qf(old[s], i);
-                    const float r = __expf(d);
-                    const bool edge = !(fabsf(d) < 80.f) || fabsf(r - prm.hi_f) <= tol_hi ||
-                                      fabsf(r - prm.lo_f) <= tol_lo;
-                    const bool unc = r <= thr_hi && r >= thr_lo;
-                    const bool fast = valid && !edge;
-                    o[i] = (fast && unc) ? Afs * r : 0.f;
-                    fsum += fast ? (unc ? r : clipv) : 0.f;
-                    inc_fast += fast;
-                    rare |= (valid && edge) ? (1u << i) : 0u;
+                    for (int i = 0; i < 4; ++i) {
+                        const float d = qf(now[s], i) - qf(old[s], i);
+                        r[i] = __expf(d);
+                        edge |= !(d < 80.f) || (sgn != 0 && fabsf(r[i] - thr) <= tol);
+                    }
+                    if (!edge) {
+                        if (sgn > 0) {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const bool unc = r[i] <= thr;
+                                o[i] = unc ? Afs * r[i] : 0.f;
+                                fsum += unc ? r[i] : thr;
+                            }
+                        } else if (sgn < 0) {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const bool unc = r[i] >= thr;
+                                o[i] = unc ? Afs * r[i] : 0.f;
+                                fsum += unc ? r[i] : thr;
+                            }
+                        }
+                        inc_fast += 4;
+                    } else {
+                        slow = true;
+                    }
                 }
-                if (rare) {
+                if (slow) {  // boundary quads and edge tokens: exact fp64, per token
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
-                        if (rare & (1u << i))
+                        if (e0 + i >= 0 && e0 + i < un.len)
                             o[i] = grpo_token_exact(qf(now[s], i), qf(old[s], i), A, prm, part) *
                                    scale;
                 }
@@ -432,9 +454,12 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
     const int ups = (*maxq_p + QU - 1) / QU;
     const int nu = nloc * ups;
     GrpoPartial part;
+    Unit nxt;  // descriptor of the next unit, loaded one unit ahead
+    if ((int)blockIdx.x < nu) nxt = ld_unit(units + blockIdx.x / ups);
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
         const int b = u / ups, c = u - b * ups;
-        const Unit un = ld_unit(units + b);
+        const Unit un = nxt;
+        if (u + (int)gridDim.x < nu) nxt = ld_unit(units + (u + (int)gridDim.x) / ups);
         const int a = (int)(un.off & 3);
         const int nq = (a + un.len + 3) >> 2;
         if (c * QU >= nq) continue;

@@ -27,6 +27,7 @@ def show(name, idx):
     print(name)
     for a, b in zip(idx, idx[1:]):
         print(f"  phase {a}->{b}: {ck[b] - ck[a]:8d} cycles ({(ck[b] - ck[a]) / mhz:7.2f} us @1.9GHz)")
-show("k_sample_with (0 start,1 draws done,2 map start,3 slots,4 offsets,5 units)", [0, 1, 2, 3, 4, 5])
-show("k_insert_route (10 start,11 lengths,12 adv,13 risk,14 route,15 units,16 end)", [10, 11, 12, 13, 14, 15, 16])
+show("k_sample_draw (0 start, 1 end)", [0, 1])
+show("k_insert_route_fifo (20 start,21 phase1,22 after sync,23 metadata,24 end)", [20, 21, 22, 23, 24])
+show("k_sample_map_coop (30 start,31 slots,32 after sync,33 scan)", [30, 31, 32, 33])
 print("phases_ms", res["phases_ms"])
