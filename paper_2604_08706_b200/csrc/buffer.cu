@@ -886,7 +886,13 @@ constexpr int COOP_THREADS = 256;
 
 // FIFO routing + eviction + group advantages + metadata scatter
 // (replay_buffer.cpp:83-133 closed form; bandit.cpp:276-294 per group).
-__global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, InsertIn in) {
+// Phase 1: per record routing/victims; per group (one thread) the reference's
+// sequential fp64 mean and population variance.  Phase 2 (after one grid
+// barrier): per record its advantage (r - mean) / sd and the metadata.  The
+// error flag alternates between two words by launch parity so no second
+// barrier is needed to reset it.
+__global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, InsertIn in,
+                                                                    int parity) {
     cg::grid_group grid = cg::this_grid();
     const int n = (int)in.n;
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, gn = gridDim.x * blockDim.x;
@@ -897,6 +903,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
     const int T = v.T, C = v.C;
     const int c0 = (int)(cur0 % (unsigned long long)T);
     int bad = 0;
+    if (gt == 0) ctl->batch_bad[parity ^ 1] = 0;  // the flag of the next launch
     if (!sticky) {
         for (int j = gt; j < n; j += gn) {
             long long l = in.toff ? in.toff[j + 1] - in.toff[j] : 0;
@@ -946,20 +953,19 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
                 }
                 var = __ddiv_rn(var, dn);
                 const double sd = __dsqrt_rn(var);
-#pragma unroll 8
                 for (long long k = b; k < e; ++k) {
-                    in.adv_out[k] = sd < 1e-8 ? 0.0 : __ddiv_rn(__dsub_rn(in.reward[k], mean), sd);
+                    in.adv_out[k] = sd;  // phase 2 turns it into the advantage
                     in.gmean_out[k] = mean;
                 }
             }
         }
     }
     RB_CLOCK(21);
-    if (bad) atomicOr(&ctl->batch_bad, bad);
+    if (bad) atomicOr(&ctl->batch_bad[parity], bad);
     if (gt == 0) *in.n_units = 0;
     grid.sync();
     RB_CLOCK(22);
-    const int bb = sticky ? 8 : *(volatile int*)&ctl->batch_bad;
+    const int bb = sticky ? 8 : *(volatile int*)&ctl->batch_bad[parity];
     if (bb) {  // nothing is applied; the error is sticky until rb_check
         for (int j = gt; j < n; j += gn) {
             in.surv[j] = 0;
@@ -974,6 +980,11 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
     } else {
         int maxq = 0;
         for (int j = gt; j < n; j += gn) {
+            if (!in.adv) {  // bandit.cpp:289-292: zeros when the population std < 1e-8
+                const double sd = in.adv_out[j];
+                in.adv_out[j] =
+                    sd < 1e-8 ? 0.0 : __ddiv_rn(__dsub_rn(in.reward[j], in.gmean_out[j]), sd);
+            }
             const int g = in.tslot[j];
             Unit d;
             d.row = -1;
@@ -1008,8 +1019,6 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
             ctl->hash_stale = 1;
         }
     }
-    grid.sync();
-    if (gt == 0) ctl->batch_bad = 0;
     RB_CLOCK(24);
 }
 
@@ -1266,6 +1275,7 @@ rb_buffer::~rb_buffer() {
     if (aux) cudaStreamSynchronize(aux);
     if (ev_draw) cudaEventDestroy(ev_draw);
     if (ev_map) cudaEventDestroy(ev_map);
+    if (ev_fork) cudaEventDestroy(ev_fork);
     if (aux) cudaStreamDestroy(aux);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
@@ -1447,6 +1457,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         RB_CUDA(cudaStreamCreateWithPriority(&b->aux, cudaStreamNonBlocking, prio_hi));
         RB_CUDA(cudaEventCreateWithFlags(&b->ev_draw, cudaEventDisableTiming));
         RB_CUDA(cudaEventCreateWithFlags(&b->ev_map, cudaEventDisableTiming));
+        RB_CUDA(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
         BufView& v = b->v;
         v.T = (int)T;
         v.C = (int)b->C;
@@ -1551,13 +1562,19 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         // ids promised new and increasing: the cooperative FIFO kernel
         const int grid = (int)std::min<size_t>((bt.n + COOP_THREADS - 1) / COOP_THREADS,
                                                (size_t)b->coop_route_max);
-        void* args[] = {(void*)&b->v, (void*)&in};
+        int parity = b->route_parity;
+        b->route_parity ^= 1;
+        void* args[] = {(void*)&b->v, (void*)&in, (void*)&parity};
         RB_CUDA(cudaLaunchCooperativeKernel((void*)k_insert_route_fifo, dim3(std::max(grid, 1)),
                                             dim3(COOP_THREADS), args, 0, b->stream));
     } else {
         k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
     }
     RB_CUDA(cudaGetLastError());
+    // The next sampler draws may start here (they need the route's metadata
+    // ordering only, not the payload copy enqueued next).
+    RB_CUDA(cudaEventRecord(b->ev_fork, b->stream));
+    b->fork_valid = true;
     if (payload) {
         k_insert_payload<PAYLOAD_U><<<b->payload_grid, UNIT_THREADS, 0, b->stream>>>(
             b->v, b->units_ins, b->n_units_ins, (int)bt.n, bt.tokens, bt.logp_old);
@@ -1688,7 +1705,9 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
         const bool toff_host = toff_user && !is_device_ptr(toff_user);
         add((const void**)&bt.tok_offsets, (n + 1) * 8);
         size_t payload_elems = 0;
-        if (toff_user && (bt.tokens || bt.logp_old)) {
+        const bool host_payload = (bt.tokens && !is_device_ptr(bt.tokens)) ||
+                                  (bt.logp_old && !is_device_ptr(bt.logp_old));
+        if (toff_user && host_payload) {  // size needed only to stage host payload
             if (toff_host) {
                 payload_elems = (size_t)toff_user[n];
             } else {
@@ -1867,7 +1886,13 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
             for (size_t s = 0; s < b->T && s < 64; ++s)
                 a.occ[s] = std::min<long long>(b->h_pushes[s], (long long)b->C);
             cudaStream_t ds = a.occ_known ? b->aux : b->stream;
-            if (a.occ_known) RB_CUDA(cudaStreamWaitEvent(b->aux, b->ev_map, 0));
+            if (a.occ_known) {
+                // fork the auxiliary stream from the main stream: right after
+                // the last insert's route kernel if nothing else intervened
+                if (!b->fork_valid) RB_CUDA(cudaEventRecord(b->ev_fork, b->stream));
+                RB_CUDA(cudaStreamWaitEvent(b->aux, b->ev_fork, 0));
+            }
+            b->fork_valid = false;
             MtState* st = rng->to_device(ds);
             k_sample_draw<<<1, DRAW_THREADS, 0, ds>>>(b->v, st, a);
             RB_CUDA(cudaGetLastError());

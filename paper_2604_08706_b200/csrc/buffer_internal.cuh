@@ -29,7 +29,8 @@ struct DevCtl {
     int err_code;  // sticky asynchronous error (RB_EINVAL)
     int has_any;   // max_id valid
     int hash_stale;
-    int batch_bad;  // per-launch error flags of the cooperative insert (reset on exit)
+    int batch_bad[2];  // error flags of the cooperative insert, by launch parity
+    int pad;
 };
 
 // Everything a kernel needs, passed by value.
@@ -99,6 +100,9 @@ struct rb_buffer {
     long long* coop_sums = nullptr;           // [2 * coop_map_max]
     cudaStream_t aux = nullptr;         // sampler draws (overlap the insert)
     cudaEvent_t ev_draw = nullptr, ev_map = nullptr;
+    cudaEvent_t ev_fork = nullptr;      // main-stream point the draws may start from
+    bool fork_valid = false;            // ev_fork recorded after the last route kernel
+    int route_parity = 0;
     rb::Unit* units_ins = nullptr;      // payload copy units of the last insert
     int* n_units_ins = nullptr;
     size_t units_ins_cap = 0;

@@ -13,7 +13,7 @@ import bench  # noqa: E402
 from paper_2604_08706_b200 import _lib  # noqa: E402
 
 _lib.lib.rb_debug_phase_clocks.argtypes = [C.c_void_p]
-args = bench.argparse.Namespace(steps=3, warmup=3, config=os.environ.get("CFG", "c4"), no_e2e=True)
+args = bench.argparse.Namespace(steps=3, warmup=3, config=os.environ.get("CFG", "c4"), no_e2e=True, graph=False)
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
     res, buf, wl, rng = bench.run_ours(args, 0, 1, None)
