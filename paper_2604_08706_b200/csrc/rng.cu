@@ -116,15 +116,20 @@ MtState* rb_rng::to_device(cudaStream_t s) {
         RB_CUDA(cudaMemcpyAsync(dev, &host, sizeof(MtState), cudaMemcpyHostToDevice, s));
         // host copy must stay alive until the copy completes
         RB_CUDA(cudaStreamSynchronize(s));
-    } else {
-        // order after the previous user of the device state (any stream)
+    } else if (s != last_stream) {
+        // order after the previous user of the device state on another stream
+        // (same-stream users are ordered already; skipping the wait keeps the
+        // sampler capturable in CUDA graphs)
         RB_CUDA(cudaStreamWaitEvent(s, done, 0));
     }
     where = 1;
     return dev;
 }
 
-void rb_rng::used_on(cudaStream_t s) { RB_CUDA(cudaEventRecord(done, s)); }
+void rb_rng::used_on(cudaStream_t s) {
+    RB_CUDA(cudaEventRecord(done, s));
+    last_stream = s;
+}
 
 uint64_t rb_rng::next() {
     to_host();

@@ -24,6 +24,7 @@ struct rb_rng {
     rb::MtState* dev = nullptr;
     int where = 0;                   // 0 = host authoritative, 1 = device authoritative
     cudaEvent_t done = nullptr;      // completes after the last kernel that used `dev`
+    cudaStream_t last_stream = nullptr;  // stream of that kernel (compared, never used)
     int device = -1;
 };
 
