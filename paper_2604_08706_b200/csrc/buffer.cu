@@ -1221,7 +1221,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* 
         }
     }
 }
-constexpr int GATHER_U = 8;
+constexpr int GATHER_U = 4;
 
 // ---------------------------------------------------------------- inspect
 __global__ void k_shard_contents(BufView v, int s, long long n, rb_record* out) {
