@@ -22,6 +22,7 @@ fi
 
 if [[ $what == ncu || $what == all ]]; then
   NCU=/usr/local/cuda/bin/ncu
+  rm -f $out/prof_*.ncu-rep $out/ncu_*.log
   # launch list of one short bench run (cold-cache, serialised: compare shares)
   timeout 600 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
       --clock-control none -k regex:'^k_' -c 400 --csv --log-file $out/launches.csv \

@@ -23,8 +23,18 @@ def metrics(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
-    h, v = r[0], r[2] if len(r) > 2 else r[1]
-    res = {w: v[h.index(w)] for w in WANT if w in h}
+    h, u, v = r[0], r[1], r[2] if len(r) > 2 else r[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
+             "msecond": 1e6}
+    res = {}
+    for w in WANT:
+        if w in h:
+            i = h.index(w)
+            unit = u[i] if i < len(u) else ""
+            try:
+                res[w] = float(v[i].replace(",", "")) * scale.get(unit, 1)
+            except ValueError:
+                res[w] = v[i]
     stalls = {n.split("smsp__average_warps_issue_stalled_")[1].split("_per")[0]: v[i]
               for i, n in enumerate(h)
               if n.startswith("smsp__average_warps_issue_stalled_") and n.endswith("_per_issue_active.ratio")}
@@ -33,6 +43,7 @@ def metrics(rep):
 
 
 if __name__ == "__main__":
+    # values are normalised to bytes / nanoseconds
     for rep in sys.argv[1:]:
         res, top = metrics(rep)
         print(rep)

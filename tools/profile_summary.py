@@ -46,7 +46,7 @@ for fn in sorted(os.listdir(src)):
     res, top = metrics(rep)
     rd = float(res.get("dram__bytes_read.sum", 0) or 0)
     wr = float(res.get("dram__bytes_write.sum", 0) or 0)
-    traffic[name] = (rd + wr) * 1e6  # ncu reports MB
+    traffic[name] = rd + wr  # bytes (ncu_summary normalises units)
     lines.append(f"## {name}")
     for k, v in res.items():
         lines.append(f"- `{k}` = {v}")
