@@ -42,7 +42,7 @@ def build_oracle(with_ref: bool = True) -> None:
     """Compile the checkers (make -C oracle [ref])."""
     targets = ["all"]
     if with_ref and os.path.isdir(os.environ.get("REPLAB_REF", "/root/reference/proj")):
-        targets.append("ref")
+        targets += ["ref", "reftests"]
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 

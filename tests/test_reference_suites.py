@@ -1,0 +1,40 @@
+"""The reference's OWN test suites (test_buffer_core.cpp, test_rng.cpp),
+compiled unchanged from /root/reference/proj/tests by oracle/Makefile with
+the doctest shim (tests/doctest_shim) against
+  * the unmodified reference library  (*_ref: pins the shim), and
+  * the libreplay_b200 C++ facade      (*_b200: the drop-in, on the GPU).
+The binaries live in oracle/_ref/ (built where the reference sources exist,
+shipped to the GPU box with the snapshot)."""
+import os
+import subprocess
+
+import pytest
+
+REF_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
+
+
+def run(name):
+    path = os.path.join(REF_DIR, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not built (reference sources absent where the repo was built)")
+    r = subprocess.run([path], capture_output=True, text=True, timeout=600)
+    summary = [line for line in r.stdout.splitlines() if line.startswith("[doctest-shim]")]
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-4000:])
+    assert summary and " 0 failed" in summary[-1], summary
+    return summary[-1]
+
+
+@pytest.mark.parametrize("suite", ["test_buffer_core", "test_rng"])
+def test_reference_suite_against_reference(suite):
+    run(f"{suite}_ref")
+
+
+def test_reference_rng_suite_against_facade_host_draws():
+    """test_rng.cpp only draws on the host side of the facade's Rng."""
+    run("test_rng_b200")
+
+
+@pytest.mark.gpu
+def test_reference_buffer_suite_against_b200_facade():
+    """All 20 cases of test_buffer_core.cpp pass against the GPU buffer."""
+    run("test_buffer_core_b200")
