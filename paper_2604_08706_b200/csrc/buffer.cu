@@ -1276,6 +1276,7 @@ rb_buffer::~rb_buffer() {
     if (ev_draw) cudaEventDestroy(ev_draw);
     if (ev_map) cudaEventDestroy(ev_map);
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_pre) cudaEventDestroy(ev_pre);
     if (aux) cudaStreamDestroy(aux);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
@@ -1458,6 +1459,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         RB_CUDA(cudaEventCreateWithFlags(&b->ev_draw, cudaEventDisableTiming));
         RB_CUDA(cudaEventCreateWithFlags(&b->ev_map, cudaEventDisableTiming));
         RB_CUDA(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
+        RB_CUDA(cudaEventCreateWithFlags(&b->ev_pre, cudaEventDisableTiming));
         BufView& v = b->v;
         v.T = (int)T;
         v.C = (int)b->C;
@@ -1558,6 +1560,9 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
     in.units = b->units_ins;
     in.n_units = b->n_units_ins;
     if (!payload) in.toff = bt.tok_offsets;  // lengths only
+    // The next sampler's MT draws may start before the route (they need only
+    // the RNG state and the occupancies); its map phase after it.
+    RB_CUDA(cudaEventRecord(b->ev_pre, b->stream));
     if (unique && b->retention == RB_PLAIN_FIFO && !want_evrec && bt.n <= (size_t)INT32_MAX) {
         // ids promised new and increasing: the cooperative FIFO kernel
         const int grid = (int)std::min<size_t>((bt.n + COOP_THREADS - 1) / COOP_THREADS,
@@ -1571,8 +1576,8 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
     }
     RB_CUDA(cudaGetLastError());
-    // The next sampler draws may start here (they need the route's metadata
-    // ordering only, not the payload copy enqueued next).
+    // The next sampler's map phase may start here: it needs the route's
+    // metadata, not the payload copy enqueued next.
     RB_CUDA(cudaEventRecord(b->ev_fork, b->stream));
     b->fork_valid = true;
     if (payload) {
@@ -1582,13 +1587,13 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
     }
 }
 
-void launch_map(rb_buffer* b, SampleArgs& a) {
+void launch_map(rb_buffer* b, SampleArgs& a, cudaStream_t stream) {
     const long long grid =
         std::max<long long>(1, std::min<long long>((a.nsel + COOP_THREADS - 1) / COOP_THREADS,
                                                    (long long)b->coop_map_max));
     void* args[] = {(void*)&b->v, (void*)&a, (void*)&b->coop_sums};
     RB_CUDA(cudaLaunchCooperativeKernel((void*)k_sample_map_coop, dim3((unsigned)grid),
-                                        dim3(COOP_THREADS), args, 0, b->stream));
+                                        dim3(COOP_THREADS), args, 0, stream));
 }
 
 }  // namespace
@@ -1887,22 +1892,26 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 a.occ[s] = std::min<long long>(b->h_pushes[s], (long long)b->C);
             cudaStream_t ds = a.occ_known ? b->aux : b->stream;
             if (a.occ_known) {
-                // fork the auxiliary stream from the main stream: right after
-                // the last insert's route kernel if nothing else intervened
+                // Fork the auxiliary stream: the draws from just before the
+                // last insert's route kernel (if nothing else intervened), the
+                // map phase after it; both overlap the payload copy.
                 if (!b->fork_valid) RB_CUDA(cudaEventRecord(b->ev_fork, b->stream));
-                RB_CUDA(cudaStreamWaitEvent(b->aux, b->ev_fork, 0));
+                RB_CUDA(cudaStreamWaitEvent(b->aux, b->fork_valid ? b->ev_pre : b->ev_fork, 0));
             }
-            b->fork_valid = false;
             MtState* st = rng->to_device(ds);
             k_sample_draw<<<1, DRAW_THREADS, 0, ds>>>(b->v, st, a);
             RB_CUDA(cudaGetLastError());
             rng->used_on(ds);
             if (a.occ_known) {
-                RB_CUDA(cudaEventRecord(b->ev_draw, b->aux));
-                RB_CUDA(cudaStreamWaitEvent(b->stream, b->ev_draw, 0));
+                if (b->fork_valid) RB_CUDA(cudaStreamWaitEvent(b->aux, b->ev_fork, 0));
+                launch_map(b, a, b->aux);
+                RB_CUDA(cudaEventRecord(b->ev_map, b->aux));
+                RB_CUDA(cudaStreamWaitEvent(b->stream, b->ev_map, 0));
+            } else {
+                launch_map(b, a, b->stream);
+                RB_CUDA(cudaEventRecord(b->ev_map, b->stream));
             }
-            launch_map(b, a);
-            RB_CUDA(cudaEventRecord(b->ev_map, b->stream));
+            b->fork_valid = false;
         } else {
             if (nsh > 0) {
                 MtState* st = rng->to_device(b->stream);
@@ -1911,8 +1920,9 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 RB_CUDA(cudaGetLastError());
                 rng->used_on(b->stream);
             }
-            launch_map(b, a);
+            launch_map(b, a, b->stream);
             RB_CUDA(cudaEventRecord(b->ev_map, b->stream));
+            b->fork_valid = false;
         }
         b->B = nsel;
         b->last_loss = -1;

@@ -100,7 +100,8 @@ struct rb_buffer {
     long long* coop_sums = nullptr;           // [2 * coop_map_max]
     cudaStream_t aux = nullptr;         // sampler draws (overlap the insert)
     cudaEvent_t ev_draw = nullptr, ev_map = nullptr;
-    cudaEvent_t ev_fork = nullptr;      // main-stream point the draws may start from
+    cudaEvent_t ev_fork = nullptr;      // after the last route kernel (map may start)
+    cudaEvent_t ev_pre = nullptr;       // before the last route kernel (draws may start)
     bool fork_valid = false;            // ev_fork recorded after the last route kernel
     int route_parity = 0;
     rb::Unit* units_ins = nullptr;      // payload copy units of the last insert
