@@ -560,6 +560,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, cons
                                                                  const int32_t* tokens,
                                                                  const float* logp_old) {
     constexpr int QU = UNIT_THREADS * U;
+    RB_TSTART(1);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int ups = (*maxq_p + QU - 1) / QU;  // units per record
     const int nu = n * ups;
@@ -595,6 +596,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, cons
             }
         }
     }
+    RB_TEND(1);
 }
 constexpr int PAYLOAD_U = 4;
 
@@ -639,6 +641,7 @@ constexpr int DRAW_THREADS = 160;
 __global__ void __launch_bounds__(DRAW_THREADS) k_sample_draw(BufView v, MtState* st, SampleArgs a) {
     __shared__ uint64_t mt[MT_N];
     __shared__ long long s_emit;
+    RB_TSTART(2);
     for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = st->mt[i];
     uint32_t idx = st->idx;
     unsigned long long consumed = 0;
@@ -696,6 +699,7 @@ __global__ void __launch_bounds__(DRAW_THREADS) k_sample_draw(BufView v, MtState
         st->draws += consumed;
     }
     RB_CLOCK(1);
+    RB_TEND(2);
 }
 
 __device__ __forceinline__ uint64_t mt_below_scalar(uint64_t* mt, uint32_t* idx,
@@ -898,6 +902,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, gn = gridDim.x * blockDim.x;
     DevCtl* ctl = v.ctl;
     RB_CLOCK(20);
+    RB_TSTART(0);
     const int sticky = ctl->err_code;
     const unsigned long long cur0 = ctl->cursor;
     const int T = v.T, C = v.C;
@@ -1020,6 +1025,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, I
         }
     }
     RB_CLOCK(24);
+    RB_TEND(0);
 }
 
 // Sampler map phase, cooperative: slots, use counts, lengths, descriptors,
@@ -1028,6 +1034,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_sample_map_coop(BufView v, Sam
                                                                   long long* cta_sums) {
     cg::grid_group grid = cg::this_grid();
     RB_CLOCK(30);
+    RB_TSTART(3);
     __shared__ int s_head[64];
     __shared__ long long s_red[2][32];
     const int nsh_h = a.nsh < 64 ? a.nsh : 0;
@@ -1143,6 +1150,7 @@ __global__ void __launch_bounds__(COOP_THREADS) k_sample_map_coop(BufView v, Sam
         acc->objective = 0.0;
         acc->need_fixup = 0;
     }
+    RB_TEND(3);
 }
 
 // Record copies with the post-increment use count in draw order
@@ -1186,6 +1194,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* 
                                                         const int* maxq_p, int nloc,
                                                         int32_t* out_tok, float* out_lpo) {
     constexpr int QU = UNIT_THREADS * U;
+    RB_TSTART(4);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int ups = (*maxq_p + QU - 1) / QU;  // units per selection
     const int nu = nloc * ups;
@@ -1220,6 +1229,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* 
             }
         }
     }
+    RB_TEND(4);
 }
 constexpr int GATHER_U = 4;
 
@@ -2398,6 +2408,23 @@ void rb_batch_ids_dev(const BufView& v, const int32_t* sel_slot, long long lo, l
 
 // Tuning aid: phase clocks of the single-CTA kernels (zeros unless the
 // library was built with -DRB_PHASE_CLOCKS).
+extern "C" __attribute__((visibility("default"))) int rb_debug_timeline(unsigned long long* out,
+                                                                        int reset) {
+    return guard([&] {
+#ifdef RB_PHASE_CLOCKS
+        RB_CUDA(cudaDeviceSynchronize());
+        RB_CUDA(cudaMemcpyFromSymbol(out, g_timeline, 64 * sizeof(unsigned long long)));
+        if (reset) {
+            unsigned long long init[64];
+            for (int i = 0; i < 64; ++i) init[i] = (i & 1) ? 0ULL : ~0ULL;
+            RB_CUDA(cudaMemcpyToSymbol(g_timeline, init, sizeof init));
+        }
+#else
+        for (int i = 0; i < 64; ++i) out[i] = 0;
+#endif
+    });
+}
+
 extern "C" __attribute__((visibility("default"))) int rb_debug_phase_clocks(long long* out) {
     return guard([&] {
 #ifdef RB_PHASE_CLOCKS

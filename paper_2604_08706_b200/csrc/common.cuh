@@ -135,13 +135,35 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 // -DRB_PHASE_CLOCKS; read back with rb_debug_phase_clocks).
 #ifdef RB_PHASE_CLOCKS
 static __device__ long long g_phase_clock[64];
+// kernel timeline in global-timer ns: [64 + 2k] = first CTA start, [65 + 2k] = last CTA end
+static __device__ unsigned long long g_timeline[64];
+__device__ __forceinline__ unsigned long long rb_globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 #define RB_CLOCK(i)                                                  \
     do {                                                             \
         if (threadIdx.x == 0 && blockIdx.x == 0) g_phase_clock[i] = clock64(); \
     } while (0)
+#define RB_TSTART(k)                                                           \
+    do {                                                                       \
+        if (threadIdx.x == 0) atomicMin(&g_timeline[2 * (k)], rb_globaltimer()); \
+    } while (0)
+#define RB_TEND(k)                                                                 \
+    do {                                                                           \
+        __syncthreads();                                                           \
+        if (threadIdx.x == 0) atomicMax(&g_timeline[2 * (k) + 1], rb_globaltimer()); \
+    } while (0)
 #else
 #define RB_CLOCK(i) \
     do {            \
+    } while (0)
+#define RB_TSTART(k) \
+    do {             \
+    } while (0)
+#define RB_TEND(k) \
+    do {           \
     } while (0)
 #endif
 

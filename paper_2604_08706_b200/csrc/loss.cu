@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const float scale = -1.f / (float)acc->total_tokens;
     const float tol_hi = 4e-6f * prm.hi_f, tol_lo = 4e-6f * prm.lo_f;
+    RB_TSTART(5);
     const int ups = (*maxq_p + QU - 1) / QU;
     const int nu = nloc * ups;
     GrpoPartial part;
@@ -385,6 +386,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
         part.obj += (double)fsum * A;
     }
     part.inc += inc_fast;
+    RB_TEND(5);
     loss_commit(part, parts, acc, stats, 0, 0.0, dlogp, n_local, local_fix);
 }
 constexpr int LOSS_U = 4;

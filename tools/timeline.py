@@ -1,0 +1,37 @@
+"""Per-kernel GPU timeline of one C4 replay step (debug library, global timer).
+
+Runs warm-up steps eagerly, resets the timeline, runs one more step and
+prints each kernel's [start, end] relative to the step's first kernel."""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ["REPLAY_B200_LIB"] = os.path.join(ROOT, "paper_2604_08706_b200", "libreplay_b200_clocks.so")
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2604_08706_b200 import _lib  # noqa: E402
+
+_lib.lib.rb_debug_timeline.argtypes = [C.c_void_p, C.c_int]
+NAMES = ["route_fifo", "payload", "draw", "map", "gather", "loss"]
+steps = int(os.environ.get("STEPS", "4"))
+args = bench.argparse.Namespace(steps=steps, warmup=3, config=os.environ.get("CFG", "c4"),
+                                no_e2e=True, graph=os.environ.get("GRAPH", "0") == "1")
+out = (C.c_ulonglong * 64)()
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    _lib.check(_lib.lib.rb_debug_timeline(out, 1))
+    res, buf, wl, rng = bench.run_ours(args, 0, 1, None)
+torch.cuda.synchronize()
+_lib.check(_lib.lib.rb_debug_timeline(out, 0))
+t = list(out)
+print("(timeline spans all timed steps; first start .. last end per kernel)")
+t0 = min(t[2 * k] for k in range(len(NAMES)) if t[2 * k] != 2**64 - 1)
+for k, n in enumerate(NAMES):
+    a, b = t[2 * k], t[2 * k + 1]
+    if a == 2**64 - 1:
+        continue
+    print(f"{n:12s} start {(a - t0) / 1e3:9.2f} us  end {(b - t0) / 1e3:9.2f} us")
+print("phases_ms", res["phases_ms"], "ms_per_step", res["ms_per_step"])
