@@ -272,6 +272,8 @@ def run_ours(args, rank, world, dist):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    if getattr(args, "pre_timed", None):  # tools/timeline.py hook
+        args.pre_timed()
     with Clocks(torch.cuda.current_device()) as clk:
         t0 = time.perf_counter()
         if graph is not None:

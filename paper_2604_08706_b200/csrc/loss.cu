@@ -1003,3 +1003,22 @@ int rb_asymre_records(const double* logp_now, const double* reward, const double
 }
 
 }  // extern "C"
+
+// Tuning aid (debug builds): the loss kernels' part of the kernel timeline
+// (each translation unit has its own copy of the timeline array).
+extern "C" __attribute__((visibility("default"))) int rb_debug_timeline_loss(unsigned long long* out,
+                                                                             int reset) {
+    return guard([&] {
+#ifdef RB_PHASE_CLOCKS
+        RB_CUDA(cudaDeviceSynchronize());
+        RB_CUDA(cudaMemcpyFromSymbol(out, g_timeline, 64 * sizeof(unsigned long long)));
+        if (reset) {
+            unsigned long long init[64];
+            for (int i = 0; i < 64; ++i) init[i] = (i & 1) ? 0ULL : ~0ULL;
+            RB_CUDA(cudaMemcpyToSymbol(g_timeline, init, sizeof init));
+        }
+#else
+        for (int i = 0; i < 64; ++i) out[i] = 0;
+#endif
+    });
+}
