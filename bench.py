@@ -226,24 +226,22 @@ def run_ours(args, rank, world, dist):
     t_ins = []
 
     def step(i, ev=None):
+        # Timing events only at phase boundaries that are not kernel->kernel
+        # programmatic (PDL) edges: insert -> sample -> gather is one chain.
         b, n, tot = wl.steps[i]
         if ev:
             ev[0].record(stream)
         if n:
             buf.insert(**b, assume_unique=True)
-        if ev:
-            ev[1].record(stream)
         buf.sample_device(B, rng)
-        if ev:
-            ev[2].record(stream)
         buf.gather(packed_tok, None, off)
         if ev:
-            ev[3].record(stream)
+            ev[1].record(stream)
         # --- synthetic trainer stand-in (not part of the replay step)
         buf.batch_ids_device(sel_ids)
         synth.logp_now(SEED, i + 1, sel_ids, off, lpn, sh)
         if ev:
-            ev[4].record(stream)
+            ev[2].record(stream)
         buf.loss_grpo(lpn, dlogp, EPS_LOW, EPS_HIGH, stats=stats) if cfg["loss"] == "grpo" else \
             buf.loss_asymre(lpn, dlogp, DELTA_V, stats=stats)
         if world > 1:
@@ -251,14 +249,14 @@ def run_ours(args, rank, world, dist):
             dist.all_reduce(stats[2:4].view(torch.int64))  # included, excluded
             buf.loss_finalize(dlogp, stats)
         if ev:
-            ev[5].record(stream)
+            ev[3].record(stream)
 
     for i in range(Wm):
         step(i)
     buf.check()
     torch.cuda.synchronize()
     use_graph = args.graph and world == 1
-    evs = [[torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(6)]
+    evs = [[torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(4)]
            for _ in range(K)]
     graph = None
     if use_graph:
@@ -286,10 +284,10 @@ def run_ours(args, rank, world, dist):
     if world > 1:
         dist.barrier()
     buf.check()
-    ph = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(5)] for i in range(K)])
-    # phases: insert, sample, gather, stand-in, loss  (ms)
-    step_ms = ph[:, [0, 1, 2, 4]].sum(1)
-    mean = {k: float(ph[:, j].mean()) for j, k in enumerate(["insert", "sample", "gather", "standin", "loss"])}
+    ph = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(3)] for i in range(K)])
+    # phases: insert+sample+gather, stand-in, loss  (ms)
+    step_ms = ph[:, [0, 2]].sum(1)
+    mean = {k: float(ph[:, j].mean()) for j, k in enumerate(["insert_sample_gather", "standin", "loss"])}
     ms = float(step_ms.mean())
     if world > 1:
         t = torch.tensor([ms, wall], dtype=torch.float64, device=dev)
@@ -307,7 +305,6 @@ def run_ours(args, rank, world, dist):
     value = t_samp / (ms * 1e-3)
     # dominant kernel: the loss (12 B/token GRPO: logp_old, logp_now read + dlogp write)
     loss_bytes = (12 if cfg["loss"] == "grpo" else 8) * (t_samp / T)
-    gather_bytes = 8 * (t_samp / T)
     roof = {"bound": "hbm", "kernel": "k_loss_grpo_buf" if cfg["loss"] == "grpo" else "k_loss_asymre_buf",
             "achieved": loss_bytes / (mean["loss"] * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
             "peak_kind": peak_kind}
@@ -315,8 +312,8 @@ def run_ours(args, rank, world, dist):
     roof["traffic"] = load_traffic(roof["kernel"])
     roof["step"] = {"algorithmic_bytes": alg / T, "achieved_gbs": alg / T / (ms * 1e-3) / 1e9,
                     "frac": alg / T / (ms * 1e-3) / 1e9 / hbm}
-    roof["kernels_gbs"] = {"gather": gather_bytes / (mean["gather"] * 1e-3) / 1e9,
-                           "insert": 16 * T_ins / T / (mean["insert"] * 1e-3) / 1e9}
+    roof["kernels_gbs"] = {"insert_sample_gather": (16 * T_ins + 8 * t_samp) / T
+                           / (mean["insert_sample_gather"] * 1e-3) / 1e9}
     res = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
         "warmup": Wm, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -358,8 +355,7 @@ def run_e2e(args, buf, wl, rng, cfg):
     for b, n, tot in steps:
         hb = {k: v.cpu().pin_memory() for k, v in b.items()}
         host.append((hb, n, tot))
-    tot_s = B * cfg["lmax"] if not cfg["ragged"] else buf.batch_total_tokens()
-    pad = tot_s + 8
+    pad = B * cfg["lmax"] + 8  # upper bound (ragged batches differ per step)
     tok_h = torch.empty(pad, dtype=torch.int32).pin_memory()
     off_h = torch.empty(B + 1, dtype=torch.int64).pin_memory()
     dl_h = torch.empty(pad, dtype=torch.float32).pin_memory()
@@ -380,6 +376,7 @@ def run_e2e(args, buf, wl, rng, cfg):
     # re-insert the same inbound batches needs fresh ids: shift them
     shift = 10**12
     h2d = d2h = 0
+    done_tokens = 0
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for hb, n, tot in host:
@@ -391,12 +388,14 @@ def run_e2e(args, buf, wl, rng, cfg):
         buf.gather(tok_h, None, off_h)
         st = buf.loss_grpo(lpn_h, dl_h, EPS_LOW, EPS_HIGH) if cfg["loss"] == "grpo" else \
             buf.loss_asymre(lpn_h, dl_h, DELTA_V)
-        _ = st.objective
+        _ = st.objective  # device->host read of the step's result
+        tot_s = int(off_h[B])  # this step's sampled tokens (offsets already on the host)
+        done_tokens += tot_s
         h2d += sum(v.numel() * v.element_size() for v in hb.values()) + tot_s * 4
         d2h += tot_s * 4 * 2 + (B + 1) * 8 + 40
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / len(host)
-    return {"value": tot_s / dt, "unit": "tokens/s", "ms_per_step": dt * 1e3,
+    return {"value": done_tokens / len(host) / dt, "unit": "tokens/s", "ms_per_step": dt * 1e3,
             "h2d_bytes_per_step": h2d // len(host), "d2h_bytes_per_step": d2h // len(host),
             "steps": len(host), "path": "rb_insert/rb_sample/rb_gather/rb_loss_* with pinned host "
                                         "buffers (copies inside the timed region)"}

@@ -16,6 +16,8 @@
 //                     packed batch.
 #include <algorithm>
 #include <charconv>
+#include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -26,7 +28,6 @@
 #include "rng_internal.cuh"
 #include "stream_copy.cuh"
 
-#include <cooperative_groups.h>
 
 using namespace rb;
 
@@ -276,7 +277,7 @@ __device__ void posbias_push(const BufView& v, const InsertIn& in, int s, long l
 
 // ---------------------------------------------------------------- insert
 __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
-    __shared__ int s_bad, s_risk;
+    __shared__ int s_bad;
     __shared__ long long s_applied;
     const int tid = threadIdx.x, nt = blockDim.x;
     const long long n = in.n;
@@ -554,22 +555,58 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
 // Each unit copies 128*U quads of one surviving trajectory from the packed
 // inbound batch (any alignment) into its 16-byte aligned slot row, tokens and
 // logp_old interleaved so every thread keeps 2*U 16-byte loads in flight.
-template <int U>
-__global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, const Unit* desc,
-                                                                 const int* maxq_p, int n,
-                                                                 const int32_t* tokens,
-                                                                 const float* logp_old) {
+//
+// Two descriptor sources: the route kernel's table (general path), or the
+// FIFO closed form evaluated here from the pre-batch cursor and per-shard
+// push counts (host mirrors, exact on this path), so the copy does not wait
+// for the route: it is launched as a programmatic dependent of the route
+// (PDL) and only its first store waits for the route's whole-batch
+// validation flag (1 = valid, 2 = rejected; reset by the last CTA).
+struct FifoPlan {
+    int c0, T, C, ups;  // cursor % T, shards, capacity per shard, units per record
+    int pm[64];         // pushes_s % C before the batch
+};
+__device__ __forceinline__ Unit fifo_unit(const BufView& v, const FifoPlan& p,
+                                          const int64_t* toff, int n, int j) {
+    int s = p.c0 + j % p.T;
+    if (s >= p.T) s -= p.T;
+    const int rank = j / p.T, j0 = j % p.T;
+    const int ns = (n - 1 - j0) / p.T + 1;
+    Unit d;
+    d.off = toff[j];
+    const long long l = toff[j + 1] - d.off;
+    d.len = (int32_t)(l < 0 ? 0 : l);
+    d.k0 = 0;
+    d.g = j;
+    d.adv = 0.0;
+    d.row = -1;
+    if (rank + p.C >= ns && s >= v.sb && s < v.se && l > 0) {
+        int x = p.pm[s] + rank % p.C;
+        if (x >= p.C) x -= p.C;
+        d.row = (s - v.sb) * p.C + x;
+    }
+    return d;
+}
+
+template <int U, bool CLOSED>
+__device__ __forceinline__ void payload_body(const BufView& v, const Unit* desc, const FifoPlan& p,
+                                             const int64_t* toff, int ups, int n,
+                                             const int32_t* tokens, const float* logp_old,
+                                             int* sync) {
     constexpr int QU = UNIT_THREADS * U;
-    RB_TSTART(1);
+    __shared__ int s_flag;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int ups = (*maxq_p + QU - 1) / QU;  // units per record
     const int nu = n * ups;
+    auto load_desc = [&](int u) { return CLOSED ? fifo_unit(v, p, toff, n, u / ups) : ld_unit(desc + u / ups); };
+    bool ready = !CLOSED;
+    if (CLOSED) pdl_trigger();  // the sampler may launch (it waits for the route itself)
     Unit nxt;  // descriptor of the next unit, loaded one unit ahead
-    if ((int)blockIdx.x < nu) nxt = ld_unit(desc + blockIdx.x / ups);
+    if ((int)blockIdx.x < nu) nxt = load_desc(blockIdx.x);
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
         const int j = u / ups, c = u - j * ups;
+        (void)j;
         const Unit un = nxt;
-        if (u + (int)gridDim.x < nu) nxt = ld_unit(desc + (u + (int)gridDim.x) / ups);
+        if (u + (int)gridDim.x < nu) nxt = load_desc(u + (int)gridDim.x);
         const int nq = (un.len + 3) >> 2;  // destination (row) quads
         if (un.row < 0 || c * QU >= nq) continue;
         const int a = (int)(un.off & 3);
@@ -583,6 +620,16 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, cons
         if (logp_old)
             packed_to_row_quads<U>(reinterpret_cast<const uint4*>(logp_old) + (un.off >> 2), nsq,
                                    a, kw, ol);
+        if (CLOSED && !ready) {  // CTA-uniform: first store of this CTA
+            if (threadIdx.x == 0) {
+                int f;
+                while ((f = ld_acquire_i32(&sync[0])) == 0) __nanosleep(64);
+                s_flag = f;
+            }
+            __syncthreads();
+            if (s_flag != 1) break;  // batch rejected: nothing is applied
+            ready = true;
+        }
 #pragma unroll
         for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
@@ -596,9 +643,31 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, cons
             }
         }
     }
+    // completion of this copy implies completion of the route before it
+    if (CLOSED) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+template <int U>
+__global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, const Unit* desc,
+                                                                 const int* maxq_p, int n,
+                                                                 const int32_t* tokens,
+                                                                 const float* logp_old) {
+    RB_TSTART(1);
+    const int ups = (*maxq_p + UNIT_THREADS * U - 1) / (UNIT_THREADS * U);
+    payload_body<U, false>(v, desc, FifoPlan{}, nullptr, ups, n, tokens, logp_old, nullptr);
+    RB_TEND(1);
+}
+template <int U>
+__global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload_fifo(BufView v, FifoPlan p,
+                                                                      const int64_t* toff, int n,
+                                                                      const int32_t* tokens,
+                                                                      const float* logp_old,
+                                                                      int* sync) {
+    RB_TSTART(1);
+    payload_body<U, true>(v, nullptr, p, toff, p.ups, n, tokens, logp_old, sync);
     RB_TEND(1);
 }
 constexpr int PAYLOAD_U = 4;
+
 
 // ---------------------------------------------------------------- sample
 struct SampleArgs {
@@ -615,8 +684,9 @@ struct SampleArgs {
     DevLossAcc* acc;
     Unit* units;
     int* n_units;
-    int occ_known;           // occupancies below are valid (T <= 64)
-    long long occ[64];       // per-shard occupancy after the preceding inserts
+    PendingIns pend;          // a closed-form FIFO insert that may still be running
+    long long occ[64];        // per-shard occupancy after the preceding inserts (draws)
+    const long long* occ_dev;  // the same for more than 64 shards (device), else NULL
 };
 
 // x % n without a 64-bit division: q from a precomputed reciprocal
@@ -628,86 +698,574 @@ __device__ __forceinline__ uint64_t fast_mod(uint64_t x, uint64_t n, uint64_t m)
     return r;
 }
 
-__device__ void sample_map_phase(const BufView& v, const SampleArgs& a);
+#ifdef RB_PHASE_CLOCKS
+static __device__ long long g_dbg_locb[2];
+#else
+static __device__ long long g_dbg_locb[2];
+#endif
+// Per-shard heads of one sampling call, cached in shared memory for the
+// first MAP_NSH shards (more shards read them from global memory).
+constexpr int MAP_NSH = 128;
+__device__ __forceinline__ int cached_head(const BufView& v, const int* heads, int s) {
+    return s < MAP_NSH ? heads[s] : shard_head(v, s);
+}
 
-// uniform_with_replacement (replay_buffer.cpp:141-145): shard 0 takes its
-// `per` below(n_0) draws first, then shard 1, ...  One small CTA (the twist
-// needs 156 threads) generates 312 outputs per block twist; a chunk holding a
-// rejected value (v >= limit, rng.cpp:45-49; probability ~n/2^64) is replayed
-// sequentially by thread 0 so the stream advances exactly as the reference.
-// Occupancies come from the host (a.occ) so the kernel does not depend on
-// the insert and runs on the auxiliary stream, overlapping it.
-constexpr int DRAW_THREADS = 160;
-__global__ void __launch_bounds__(DRAW_THREADS) k_sample_draw(BufView v, MtState* st, SampleArgs a) {
-    __shared__ uint64_t mt[MT_N];
-    __shared__ long long s_emit;
-    RB_TSTART(2);
-    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = st->mt[i];
-    uint32_t idx = st->idx;
-    unsigned long long consumed = 0;
-    __syncthreads();
-    RB_CLOCK(0);
-    long long pos = 0;
-    for (int s = 0; s < a.nsh; ++s) {
-        const unsigned long long n =
-            a.occ_known ? (unsigned long long)a.occ[s] : (unsigned long long)occupancy(v, s);
-        const unsigned long long lim = below_limit(n);
-        const unsigned long long mag = UINT64_MAX / n;
-        long long rem = a.per;
-        while (rem > 0) {
-            if (idx >= MT_N) {
-                mt_twist_block(mt);
-                idx = 0;
+// Grid-wide bookkeeping of the multi-CTA kernels (no grid barrier): CTAs
+// take tickets in launch order, publish look-back words, and the last CTA
+// to finish (done counter) finalises and resets the control block.
+constexpr int GRID_MAX_CTAS = 4096;
+struct GridCtl {
+    unsigned int ticket, done;
+    unsigned long long gsum;
+    int first_rej;                      // fused sampler: first map CTA that saw a rejection
+    int pad;
+    long long gen_hi;                   // fused sampler: last ring block after the generator
+    unsigned long long word[GRID_MAX_CTAS];  // look-back: status (2 bits) | value (62 bits)
+    int cta_max[GRID_MAX_CTAS];
+};
+constexpr unsigned long long LB_AGG = 1ULL << 62, LB_INC = 2ULL << 62,
+                             LB_VAL = (1ULL << 62) - 1;
+// Warp 0: exclusive prefix of map CTA `t` over the aggregates / inclusive
+// values of its predecessors (decoupled look-back).  Predecessors hold
+// lower tickets, so they are running and publish without waiting.
+__device__ __forceinline__ unsigned long long lookback(GridCtl* gc, int t) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long excl = 0;
+    for (int p = t - 1; p >= 0; p -= 32) {
+        const int q = p - lane;
+        unsigned long long w = 0;
+        if (q >= 0) {
+            do {
+                w = ld_acquire_u64(&gc->word[q]);
+            } while ((w >> 62) == 0);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, q >= 0 && (w >> 62) == 2);
+        const int stop = inc ? __ffs(inc) - 1 : 32;
+        unsigned long long x = (q >= 0 && lane <= stop) ? (w & LB_VAL) : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        excl += x;
+        if (inc) break;
+    }
+    return excl;
+}
+__device__ __forceinline__ void spin_until_set(const int* flag) {
+    while (ld_acquire_i32(flag) == 0) __nanosleep(32);
+}
+
+// ---- map phase (every sampler): arrival index -> slot, use counts
+// (replay_buffer.cpp:201), lengths, advantages; packed offsets of the owned
+// selections by a decoupled look-back scan over the map CTAs; the gather /
+// loss work descriptors.  Each thread maps MAP_R consecutive selections
+// with every dependent load in flight together.
+//
+// DRAW = true (uniform_with_replacement, replay_buffer.cpp:141-145 and
+// rng.cpp:40-51): the CTA also makes its selections' draws.  Shard 0 takes
+// its `per` below(n_0) draws first, then shard 1, ...; draw k is word k of
+// the MT19937-64 stream from the current position, tempered from the ring
+// (blocks twisted ahead; blocks not resident yet are waited for from the
+// generator CTA).  A rejected value (v >= limit; probability ~n/2^64 per
+// draw) shifts every later draw: its CTA and every later one publish the
+// fact through the look-back word, apply nothing, and the last CTA replays
+// the rest exactly.
+constexpr int MAP_THREADS = 128;  // small: co-resides with the persistent payload grid
+constexpr int MAP_R = 2;
+constexpr int MAP_SPC = MAP_THREADS * MAP_R;  // selections per map CTA
+constexpr int DRAW_NSH = 64;                  // shards whose occupancy rides in the arguments
+constexpr unsigned long long LB_REJ = 1ULL << 61;
+constexpr unsigned long long LB_SUM = LB_REJ - 1;
+
+struct DrawCtx {  // ring position at the start of the call (header is constant meanwhile)
+    const MtRing* r;
+    long long q0, qhi0;
+    uint32_t idx0;
+};
+
+template <bool DRAW>
+__device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int t,
+                        const DrawCtx& dc, const int* route_done) {
+    __shared__ int s_head[MAP_NSH], s_newfrom[MAP_NSH], s_ns[MAP_NSH], s_j0[MAP_NSH];
+    __shared__ int s_occ_after[MAP_NSH];
+    __shared__ unsigned long long s_lim[DRAW_NSH], s_mag[DRAW_NSH];
+    __shared__ long long s_occ[DRAW_NSH];
+    __shared__ unsigned long long s_excl, s_w[MAP_THREADS / 32];
+    __shared__ int s_m[MAP_THREADS / 32];
+    const int tid = threadIdx.x;
+    const PendingIns& pi = a.pend;
+    // Shard heads after the preceding insert.  While a closed-form FIFO
+    // insert may still be running (pi.pending), they and the position of its
+    // records follow from its plan: the newest min(ns, C) records of shard s
+    // are its pushes to s; their lengths come from its offsets, so the map
+    // needs the route kernel only for the use counts and advantages (last).
+    for (int s = tid; s < a.nsh && s < MAP_NSH; s += MAP_THREADS) {
+        if (pi.pending) {
+            const int T = v.T, C = v.C;
+            const int j0 = ((s - pi.c0) % T + T) % T;
+            const int ns = pi.n > j0 ? (pi.n - 1 - j0) / T + 1 : 0;
+            const long long P = pi.P[s] + ns;
+            const int occ = (int)(P < C ? P : C);
+            s_head[s] = P >= C ? (int)(P % C) : 0;
+            s_newfrom[s] = occ - (ns < C ? ns : C);
+            s_ns[s] = ns;
+            s_j0[s] = j0;
+            s_occ_after[s] = occ;
+        } else {
+            s_head[s] = shard_head(v, s);
+            s_newfrom[s] = INT_MAX;
+        }
+    }
+    if (DRAW)
+        for (int s = tid; s < a.nsh && s < DRAW_NSH; s += MAP_THREADS) {
+            const unsigned long long n = (unsigned long long)a.occ[s];
+            s_occ[s] = (long long)n;
+            s_lim[s] = below_limit(n);
+            s_mag[s] = UINT64_MAX / n;
+        }
+    const long long kc = (long long)t * MAP_SPC;  // first selection of this CTA
+    RB_GCLOCK(41 + 8 * (t & 1), t < 2);
+    // Blocks past the ring's resident range (first call, or a larger batch
+    // than the generator planned for) are twisted here into shared memory
+    // (the ring itself is written only by the generator CTA).  A CTA's
+    // MAP_SPC draws span at most LOC_BLKS blocks.
+    constexpr int LOC_BLKS = MAP_SPC / MT_N + 2;
+    __shared__ uint64_t s_loc[LOC_BLKS][MT_N];
+    __shared__ uint64_t s_tw[MT_N];
+    long long locb = LLONG_MAX;  // first block held in s_loc
+    if (DRAW && kc < a.nsel) {
+        const long long kl = (kc + MAP_SPC < a.nsel ? kc + MAP_SPC : a.nsel) - 1;
+        const long long firstb = dc.q0 + (long long)((dc.idx0 + (unsigned long long)kc) / MT_N);
+        const long long lastb = dc.q0 + (long long)((dc.idx0 + (unsigned long long)kl) / MT_N);
+        if (lastb > dc.qhi0) {  // block-uniform
+            locb = firstb > dc.qhi0 + 1 ? firstb : dc.qhi0 + 1;
+            for (int i = tid; i < MT_N; i += MAP_THREADS) s_tw[i] = __ldcg(&dc.r->blk[dc.qhi0 % MT_KR][i]);
+            __syncthreads();
+            for (long long q = dc.qhi0 + 1; q <= lastb; ++q) {
+                mt_twist_block(s_tw);
+                if (q >= locb)
+                    for (int i = tid; i < MT_N; i += MAP_THREADS) s_loc[q - locb][i] = s_tw[i];
             }
-            const long long avail = (long long)(MT_N - idx);
-            const int take = (int)(avail < rem ? avail : rem);
-            bool rej = false;
-            for (int t = threadIdx.x; t < take; t += blockDim.x) rej |= mt_temper(mt[idx + t]) >= lim;
-            if (!__syncthreads_or(rej)) {
-                for (int t = threadIdx.x; t < take; t += blockDim.x) {
-                    a.sel_shard[pos + t] = s;
-                    a.sel_index[pos + t] = (int64_t)fast_mod(mt_temper(mt[idx + t]), n, mag);
-                }
-                pos += take;
-                rem -= take;
-            } else {
-                if (threadIdx.x == 0) {
-                    long long e = 0;
-                    for (int u = 0; u < take; ++u) {
-                        const uint64_t y = mt_temper(mt[idx + u]);
-                        if (y < lim) {
-                            a.sel_shard[pos + e] = s;
-                            a.sel_index[pos + e] = (int64_t)(y % n);
-                            ++e;
-                        }
-                    }
-                    s_emit = e;
-                }
-                __syncthreads();
-                pos += s_emit;
-                rem -= s_emit;
-                __syncthreads();
-            }
-            idx += take;
-            consumed += take;
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) st->mt[i] = mt[i];
-    if (threadIdx.x == 0) {
-        st->idx = idx;
-        st->draws += consumed;
+    RB_GCLOCK(42 + 8 * (t & 1), t < 2);
+    if (threadIdx.x == 0 && t < 2) g_dbg_locb[t] = locb == LLONG_MAX ? -1 : locb - dc.qhi0;
+    const long long k0 = kc + (long long)tid * MAP_R;
+    const int per = (int)a.per;
+    int sh[MAP_R], ix[MAP_R], g[MAP_R], L[MAP_R];
+    bool ok[MAP_R];
+    bool rej = false;
+    // Branch-free: every load of a stage is issued before any is consumed
+    // (out-of-range lanes read a valid dummy address), so each stage costs one
+    // memory round trip instead of MAP_R.
+    uint64_t w[MAP_R];
+#pragma unroll
+    for (int r = 0; r < MAP_R; ++r) {
+        const long long k = k0 + r;
+        ok[r] = k < a.nsel;
+        const long long kk = ok[r] ? k : 0;
+        if (DRAW) {
+            const unsigned long long o = dc.idx0 + (unsigned long long)kk;
+            const long long qb = dc.q0 + (long long)(o / MT_N);
+            const long long qr = qb < locb ? qb : dc.q0;  // resident block (or a dummy)
+            const uint64_t wr = __ldcg(&dc.r->blk[qr % MT_KR][o % MT_N]);
+            const uint64_t wl = s_loc[qb < locb ? 0 : qb - locb][o % MT_N];
+            w[r] = qb < locb ? wr : wl;
+        } else {
+            sh[r] = a.sel_shard[kk];
+            ix[r] = (int)a.sel_index[kk];
+        }
     }
-    RB_CLOCK(1);
-    RB_TEND(2);
+    if (DRAW) {
+#pragma unroll
+        for (int r = 0; r < MAP_R; ++r) {
+            const long long kk = ok[r] ? k0 + r : 0;
+            const uint64_t y = mt_temper(w[r]);
+            const int s = (int)kk / per;
+            unsigned long long n, lim, mag;
+            if (s < DRAW_NSH) {
+                n = (unsigned long long)s_occ[s];
+                lim = s_lim[s];
+                mag = s_mag[s];
+            } else {
+                n = (unsigned long long)a.occ_dev[s];
+                lim = below_limit(n);
+                mag = UINT64_MAX / n;
+            }
+            rej |= ok[r] && y >= lim;
+            sh[r] = s;
+            ix[r] = (int)fast_mod(y, n, mag);
+        }
+    }
+    RB_GCLOCK(46 + 8 * (t & 1), t < 2);
+    int lv[MAP_R];
+    long long t0[MAP_R], t1[MAP_R];
+    bool nw[MAP_R];
+#pragma unroll
+    for (int r = 0; r < MAP_R; ++r) {
+        const int s = sh[r];
+        g[r] = s * v.C + arrival_slot_h(v, s, ix[r], cached_head(v, s_head, s));
+        const int nf = s < MAP_NSH ? s_newfrom[s] : INT_MAX;
+        nw[r] = ix[r] >= nf;  // a record of the pending insert: length from its offsets
+        const int j = nw[r] ? s_j0[s] + (s_ns[s] - (s_occ_after[s] - ix[r])) * v.T : 0;
+        const int64_t* to = nw[r] ? pi.toff : reinterpret_cast<const int64_t*>(v.pushes);
+        lv[r] = v.len[g[r]];
+        t0[r] = to[j];
+        t1[r] = to[j + (nw[r] ? 1 : 0)];
+    }
+#pragma unroll
+    for (int r = 0; r < MAP_R; ++r) {
+        const long long l = t1[r] - t0[r];
+        L[r] = !ok[r] ? 0 : nw[r] ? (int)(l < 0 ? 0 : l) : lv[r];
+    }
+    unsigned long long own = 0, all = 0;
+#pragma unroll
+    for (int r = 0; r < MAP_R; ++r) {
+        all += (unsigned long long)L[r];
+        if (ok[r] && k0 + r >= a.lo && k0 + r < a.hi) own += (unsigned long long)L[r];
+    }
+    RB_GCLOCK(47 + 8 * (t & 1), t < 2);
+    const bool cta_rej = DRAW && __syncthreads_or(rej);
+    RB_GCLOCK(43 + 8 * (t & 1), t < 2);
+    long long cta_own;
+    const long long pre = block_exclusive_scan((long long)own, &cta_own);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) all += __shfl_xor_sync(0xffffffffu, all, o);
+    if ((tid & 31) == 0) s_w[tid >> 5] = all;
+    __syncthreads();
+    const unsigned long long rbit = cta_rej ? LB_REJ : 0;
+    if (tid < 32) {
+        if (tid == 0)
+            st_release_u64(&gc->word[t], (t ? LB_AGG : LB_INC) | rbit | (unsigned long long)cta_own);
+        const unsigned long long excl = t ? lookback(gc, t) : 0;  // sums and OR of reject bits
+        if (tid == 0) {
+            const unsigned long long inc = ((excl & LB_SUM) + (unsigned long long)cta_own) |
+                                           (excl & LB_REJ) | rbit;
+            if (t) st_release_u64(&gc->word[t], LB_INC | inc);
+            s_excl = excl | rbit;
+        }
+    }
+    __syncthreads();
+    RB_GCLOCK(44 + 8 * (t & 1), t < 2);
+    if (s_excl & LB_REJ) {  // a rejection at or before this CTA: the last CTA replays
+        if (tid == 0) atomicMin(&gc->first_rej, t);
+        if (tid == 0) gc->cta_max[t] = 0;
+        return;
+    }
+    if (tid == 0) {
+        unsigned long long ca = 0;
+        for (int w = 0; w < MAP_THREADS / 32; ++w) ca += s_w[w];
+        atomicAdd(&gc->gsum, ca);
+    }
+    long long pos = (long long)(s_excl & LB_SUM) + pre;
+    int maxq = 0;
+#pragma unroll
+    for (int r = 0; r < MAP_R; ++r) {
+        const long long k = k0 + r;
+        if (!ok[r]) continue;
+        if (DRAW) {
+            a.sel_shard[k] = sh[r];
+            a.sel_index[k] = ix[r];
+        }
+        a.sel_slot[k] = g[r];
+        a.sel_len[k] = L[r];
+        if (k < a.lo || k >= a.hi) continue;
+        a.off[k - a.lo] = pos;
+        Unit d;
+        d.row = (sh[r] - v.sb) * v.C + (g[r] - sh[r] * v.C);
+        d.len = L[r];
+        d.k0 = 0;
+        d.g = g[r];
+        d.off = pos;
+        d.adv = 0.0;  // below, once the route kernel has written it
+        a.units[k - a.lo] = d;
+        const int nq = ((int)(pos & 3) + L[r] + 3) >> 2;
+        if (L[r]) maxq = nq > maxq ? nq : maxq;
+        pos += L[r];
+    }
+    maxq = __reduce_max_sync(0xffffffffu, maxq);
+    if ((tid & 31) == 0) s_m[tid >> 5] = maxq;
+    // the route kernel's metadata: advantages and use counts (replay_buffer.cpp:201)
+    if (tid == 0) spin_until_set(route_done);
+    __syncthreads();
+    if (tid == 0) {
+        int m = 0;
+        for (int w = 0; w < MAP_THREADS / 32; ++w) m = s_m[w] > m ? s_m[w] : m;
+        gc->cta_max[t] = m;
+    }
+    double adv[MAP_R];
+#pragma unroll
+    for (int r = 0; r < MAP_R; ++r) adv[r] = v.adv[g[r]];
+#pragma unroll
+    for (int r = 0; r < MAP_R; ++r) {
+        if (!ok[r]) continue;
+        atomicAdd(&v.use[g[r]], 1u);
+        const long long k = k0 + r;
+        if (k >= a.lo && k < a.hi) reinterpret_cast<double*>(&a.units[k - a.lo])[3] = adv[r];
+    }
+    RB_GCLOCK(45 + 8 * (t & 1), t < 2);
+}
+// Done counter; returns (block-uniform) whether this CTA finished last.
+__device__ __forceinline__ bool last_to_finish(GridCtl* gc) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&gc->done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last;
+}
+
+// Exact sequential replay of draws [k0, k1) from a shared copy of the
+// block holding the current position (thread 0; rejections shift the stream).
+__device__ __noinline__ void draw_exact(int32_t* sel_shard, int64_t* sel_index, long long per,
+                                        const long long* occ, uint64_t* mt, long long k0,
+                                        long long k1, uint32_t* idx, long long* tw,
+                                        unsigned long long* dr) {
+    for (long long kk = k0; kk < k1; ++kk) {
+        const int ss = (int)(kk / per);
+        const unsigned long long n = (unsigned long long)occ[ss];
+        const uint64_t lim = below_limit(n);
+        uint64_t y;
+        do {
+            if (*idx >= MT_N) {
+                mt_twist_scalar(mt);
+                *idx = 0;
+                ++*tw;
+            }
+            y = mt_temper(mt[(*idx)++]);
+            ++*dr;
+        } while (y >= lim);
+        sel_shard[kk] = ss;
+        sel_index[kk] = (int64_t)(y % n);
+    }
+}
+
+// Last CTA: (replay of a rejected tail,) totals, work-unit bound,
+// loss-accumulator reset, control reset; the new ring position when drawing.
+template <bool DRAW>
+__device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc, int nmap,
+                             const DrawCtx& dc, MtRing* r) {
+    __shared__ int s_m[32];
+    __shared__ uint64_t mt[MT_N];
+    __shared__ long long s_q;
+    __shared__ uint32_t s_idx;
+    __shared__ long long s_total;
+    __shared__ unsigned long long s_g;
+    const int first = DRAW ? __ldcg(&gc->first_rej) : INT_MAX;
+    const long long D = a.nsel;
+    const long long nloc = a.hi - a.lo;
+    if (DRAW && first != INT_MAX) {
+        // the stream had no rejection before selection k0
+        const long long k0 = (long long)first * MAP_SPC;
+        long long q = dc.q0;
+        uint32_t idx = dc.idx0;
+        ring_advance(q, idx, (unsigned long long)k0);
+        for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = __ldcg(&dc.r->blk[q % MT_KR][i]);
+        __syncthreads();
+        __shared__ long long s_occ[DRAW_NSH];
+        for (int s = threadIdx.x; s < a.nsh && s < DRAW_NSH; s += blockDim.x) s_occ[s] = a.occ[s];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long tw = 0;
+            unsigned long long dr = 0;
+            draw_exact(a.sel_shard, a.sel_index, a.per, a.occ_dev ? a.occ_dev : s_occ, mt, k0, D,
+                       &idx, &tw, &dr);
+            s_q = q + tw;
+            s_idx = idx;
+            r->draws = r->draws + (unsigned long long)k0 + dr;
+        }
+        __syncthreads();
+        // map the replayed tail, then rescan every owned offset
+        __shared__ int s_head[MAP_NSH];
+        for (int s = threadIdx.x; s < a.nsh && s < MAP_NSH; s += blockDim.x) s_head[s] = shard_head(v, s);
+        __syncthreads();
+        unsigned long long tail = 0;
+        for (long long k = k0 + threadIdx.x; k < D; k += blockDim.x) {
+            const int s = a.sel_shard[k];
+            const int g = s * v.C + arrival_slot_h(v, s, a.sel_index[k], cached_head(v, s_head, s));
+            atomicAdd(&v.use[g], 1u);
+            a.sel_slot[k] = g;
+            const int L = v.len[g];
+            a.sel_len[k] = L;
+            tail += (unsigned long long)L;
+            if (k >= a.lo && k < a.hi) {
+                Unit d;
+                d.row = (s - v.sb) * v.C + (g - s * v.C);
+                d.len = L;
+                d.k0 = 0;
+                d.g = g;
+                d.off = 0;
+                d.adv = v.adv[g];
+                a.units[k - a.lo] = d;
+            }
+        }
+        tail = warp_sum_i64((long long)tail);
+        if ((threadIdx.x & 31) == 0) atomicAdd(&gc->gsum, tail);
+        __syncthreads();
+        long long carry = 0;
+        int maxq = 0;
+        for (long long cb = 0; cb < nloc; cb += blockDim.x) {
+            const long long i = cb + threadIdx.x;
+            const long long L = i < nloc ? a.sel_len[a.lo + i] : 0;
+            long long ct;
+            const long long ex = block_exclusive_scan(L, &ct);
+            if (i < nloc) {
+                const long long pos = carry + ex;
+                a.off[i] = pos;
+                reinterpret_cast<long long*>(&a.units[i])[2] = pos;  // Unit::off
+                const int nq = ((int)(pos & 3) + (int)L + 3) >> 2;
+                if (L) maxq = nq > maxq ? nq : maxq;
+            }
+            carry += ct;
+        }
+        maxq = __reduce_max_sync(0xffffffffu, maxq);
+        if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = maxq;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int mm = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = s_m[w] > mm ? s_m[w] : mm;
+            s_total = carry;
+            s_m[0] = mm;
+        }
+        __syncthreads();
+    } else {
+        int m = 0;
+        for (int c = threadIdx.x; c < nmap; c += blockDim.x) m = max(m, __ldcg(&gc->cta_max[c]));
+        m = __reduce_max_sync(0xffffffffu, m);
+        if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int mm = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = s_m[w] > mm ? s_m[w] : mm;
+            s_m[0] = mm;
+            s_total = (long long)(ld_acquire_u64(&gc->word[nmap - 1]) & LB_SUM);
+            if (DRAW) {
+                long long q = dc.q0;
+                uint32_t idx = dc.idx0;
+                ring_advance(q, idx, (unsigned long long)D);
+                s_q = q;
+                s_idx = idx;
+                r->draws = r->draws + (unsigned long long)D;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const unsigned long long global = atomicAdd(&gc->gsum, 0ULL);
+        s_g = global;
+        a.off[nloc] = s_total;
+        a.totals[0] = s_total;
+        a.totals[1] = (long long)global;
+        *a.n_units = s_m[0];  // max destination quads per selection
+        DevLossAcc* acc = a.acc;
+        acc->obj_sum = 0.0;
+        acc->included = 0;
+        acc->excluded = 0;
+        acc->done_blocks = 0;
+        acc->total_tokens = (long long)global;
+        acc->objective = 0.0;
+        acc->need_fixup = 0;
+        if (DRAW) {
+            const long long qhi = __ldcg(&gc->gen_hi);
+            const long long qn = s_q;
+            r->q_state = qn;
+            r->idx = s_idx;
+            r->q_hi = qhi > qn ? qhi : qn;
+        }
+        gc->ticket = 0;
+        gc->done = 0;
+        gc->gsum = 0;
+        gc->first_rej = INT_MAX;
+    }
+    __syncthreads();
+    if (DRAW && first != INT_MAX && s_q > __ldcg(&gc->gen_hi)) {  // replay went past the ring
+        uint64_t* dst = r->blk[s_q % MT_KR];
+        for (int i = threadIdx.x; i < MT_N; i += blockDim.x) dst[i] = mt[i];
+    }
+    for (int c = threadIdx.x; c < nmap; c += blockDim.x) gc->word[c] = 0;
+}
+
+// Map phase after k_sample_without (selections already drawn).
+__global__ void __launch_bounds__(MAP_THREADS) k_sample_map(BufView v, SampleArgs a, GridCtl* gc,
+                                                          const int* route_done) {
+    __shared__ int s_t;
+    RB_TSTART(3);
+    if (threadIdx.x == 0) s_t = (int)atomicAdd(&gc->ticket, 1u);
+    __syncthreads();
+    const DrawCtx dc{};
+    map_cta<false>(v, a, gc, s_t, dc, route_done);
+    if (last_to_finish(gc)) map_finalize<false>(v, a, gc, (int)gridDim.x, dc, nullptr);
+    RB_TEND(3);
+}
+
+// ---- fused uniform_with_replacement sampler: ticket 0 is the ring
+// generator (twists the blocks this call needs that are not resident yet,
+// publishing progress block by block, then as many again ahead for the next
+// call); tickets 1.. are map CTAs with their own draws, which wait for the
+// route kernel's completion flag (the metadata they map).  Launched as a
+// programmatic dependent of the payload copy, so it overlaps the insert;
+// griddepcontrol.wait at the end keeps "this kernel complete => the copy
+// complete" for the gather that follows.
+__device__ void gen_role(MtRing* r, const SampleArgs& a, GridCtl* gc) {
+    __shared__ uint64_t mt[MT_N];
+    const long long q0 = r->q_state, qhi0 = r->q_hi;
+    const uint32_t idx0 = r->idx;
+    const unsigned long long D = (unsigned long long)a.nsel;
+    const long long need = q0 + (long long)((idx0 + D + MT_N - 1) / MT_N);
+    long long target = need + (need - q0) + 1;
+    if (target > q0 + MT_KR - 1) target = q0 + MT_KR - 1;
+    if (target > qhi0) {
+        for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = r->blk[qhi0 % MT_KR][i];
+        __syncthreads();
+        for (long long q = qhi0 + 1; q <= target; ++q) {
+            mt_twist_block(mt);  // ends with a barrier: the stores below read a stable block
+            uint64_t* dst = r->blk[q % MT_KR];
+            for (int i = threadIdx.x; i < MT_N; i += blockDim.x) dst[i] = mt[i];
+        }
+    }
+    if (threadIdx.x == 0) gc->gen_hi = target > qhi0 ? target : qhi0;
+}
+
+__global__ void __launch_bounds__(MAP_THREADS, 4) k_sample_fused(BufView v, MtRing* r, SampleArgs a,
+                                                                 GridCtl* gc, const int* route_done) {
+    __shared__ int s_t;
+    if (threadIdx.x == 0) s_t = (int)atomicAdd(&gc->ticket, 1u);
+    const DrawCtx dc{r, r->q_state, r->q_hi, r->idx};
+    __syncthreads();
+    const int t = s_t;
+    if (t == 0) {
+        RB_TSTART(6);
+        gen_role(r, a, gc);
+        RB_TEND(6);
+    } else {
+        RB_TSTART(3);
+        RB_GCLOCK(40, t == 1);
+        map_cta<true>(v, a, gc, t - 1, dc, route_done);
+        RB_TEND(3);
+    }
+    if (last_to_finish(gc)) {
+        RB_GCLOCK(58, true);
+        map_finalize<true>(v, a, gc, (int)gridDim.x - 1, dc, r);
+        RB_GCLOCK(59, true);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 __device__ __forceinline__ uint64_t mt_below_scalar(uint64_t* mt, uint32_t* idx,
-                                                    uint64_t* draws, uint64_t bound) {
+                                                    uint64_t* draws, long long* tw,
+                                                    uint64_t bound) {
     const uint64_t lim = below_limit(bound);
     uint64_t x;
     do {
-        x = mt_next_scalar(mt, idx, draws);
+        if (*idx >= MT_N) {
+            mt_twist_scalar(mt);
+            *idx = 0;
+            ++*tw;
+        }
+        ++*draws;
+        x = mt_temper(mt[(*idx)++]);
     } while (x >= lim);
     return x % bound;
 }
@@ -715,442 +1273,300 @@ __device__ __forceinline__ uint64_t mt_below_scalar(uint64_t* mt, uint32_t* idx,
 // uniform_without_replacement / unused_first_without_replacement
 // (replay_buffer.cpp:146-179): sequential partial Fisher-Yates over the
 // arrival indices with the reference's exact draw consumption.
-__global__ void k_sample_without(BufView v, MtState* st, SampleArgs a, int strategy,
+__global__ void k_sample_without(BufView v, MtRing* r, SampleArgs a, int strategy,
                                  int64_t* scratch /* >= 2*C */) {
     __shared__ uint64_t mt[MT_N];
-    if (threadIdx.x != 0) return;
-    for (int i = 0; i < MT_N; ++i) mt[i] = st->mt[i];
-    uint32_t idx = st->idx;
-    uint64_t draws = st->draws;
-    long long pos = 0;
-    int64_t* perm = scratch;
-    int64_t* used = scratch + v.C;
-    for (int s = 0; s < a.nsh; ++s) {
-        const long long n = occupancy(v, s), k = a.per;
-        long long picked = 0;
-        if (strategy == RB_UNUSED_FIRST_WITHOUT_REPLACEMENT) {
-            for (long long i = n - 1; i >= 0 && picked < k; --i) {
-                const size_t g = (size_t)s * v.C + arrival_slot(v, s, i);
-                if (v.use[g] == 0) {
-                    a.sel_shard[pos + picked] = s;
-                    a.sel_index[pos + picked] = i;
-                    ++picked;
+    __shared__ uint32_t s_idx;
+    __shared__ uint64_t s_draws;
+    __shared__ long long s_tw;
+    const long long q0 = r->q_state;
+    ring_load_block(r, q0, mt);
+    if (threadIdx.x == 0) {
+        uint32_t idx = r->idx;
+        uint64_t draws = r->draws;
+        long long tw = 0;
+        long long pos = 0;
+        int64_t* perm = scratch;
+        int64_t* used = scratch + v.C;
+        for (int s = 0; s < a.nsh; ++s) {
+            const long long n = occupancy(v, s), k = a.per;
+            long long picked = 0;
+            if (strategy == RB_UNUSED_FIRST_WITHOUT_REPLACEMENT) {
+                for (long long i = n - 1; i >= 0 && picked < k; --i) {
+                    const size_t g = (size_t)s * v.C + arrival_slot(v, s, i);
+                    if (v.use[g] == 0) {
+                        a.sel_shard[pos + picked] = s;
+                        a.sel_index[pos + picked] = i;
+                        ++picked;
+                    }
+                }
+                if (picked == k) {
+                    pos += k;
+                    continue;
                 }
             }
-            if (picked == k) {
-                pos += k;
-                continue;
+            // population: all arrival indices, or the used ones (ascending)
+            long long m = 0;
+            if (strategy == RB_UNUSED_FIRST_WITHOUT_REPLACEMENT) {
+                for (long long i = 0; i < n; ++i) {
+                    const size_t g = (size_t)s * v.C + arrival_slot(v, s, i);
+                    if (v.use[g] != 0) used[m++] = i;
+                }
+            } else {
+                for (long long i = 0; i < n; ++i) used[m++] = i;
             }
-        }
-        // population: all arrival indices, or the used ones (ascending)
-        long long m = 0;
-        if (strategy == RB_UNUSED_FIRST_WITHOUT_REPLACEMENT) {
-            for (long long i = 0; i < n; ++i) {
-                const size_t g = (size_t)s * v.C + arrival_slot(v, s, i);
-                if (v.use[g] != 0) used[m++] = i;
+            for (long long i = 0; i < m; ++i) perm[i] = i;
+            const long long need = k - picked;
+            for (long long i = 0; i < need; ++i) {
+                const long long jj =
+                    i + (long long)mt_below_scalar(mt, &idx, &draws, &tw, (uint64_t)(m - i));
+                const int64_t t = perm[i];
+                perm[i] = perm[jj];
+                perm[jj] = t;
+                a.sel_shard[pos + picked + i] = s;
+                a.sel_index[pos + picked + i] = used[perm[i]];
             }
-        } else {
-            for (long long i = 0; i < n; ++i) used[m++] = i;
+            pos += k;
         }
-        for (long long i = 0; i < m; ++i) perm[i] = i;
-        const long long need = k - picked;
-        for (long long i = 0; i < need; ++i) {
-            const long long jj = i + (long long)mt_below_scalar(mt, &idx, &draws, (uint64_t)(m - i));
-            const int64_t t = perm[i];
-            perm[i] = perm[jj];
-            perm[jj] = t;
-            a.sel_shard[pos + picked + i] = s;
-            a.sel_index[pos + picked + i] = used[perm[i]];
-        }
-        pos += k;
-    }
-    for (int i = 0; i < MT_N; ++i) st->mt[i] = mt[i];
-    st->idx = idx;
-    st->draws = draws;
-}
-
-// Map phase of every sampler (block-wide): arrival index -> slot, use-count
-// increments (replay_buffer.cpp:201), per-selection lengths, packed offsets
-// over the selections of the shards held here, the gather/loss work units,
-// and the loss-accumulator reset.
-__device__ void sample_map_phase(const BufView& v, const SampleArgs& a) {
-    __shared__ unsigned long long s_global;
-    __shared__ int s_head[64];
-    if (threadIdx.x == 0) s_global = 0;
-    RB_CLOCK(2);
-    const int nsh_h = a.nsh < 64 ? a.nsh : 0;  // cache shard heads when few shards
-    for (int s = threadIdx.x; s < nsh_h; s += blockDim.x) s_head[s] = shard_head(v, s);
-    __syncthreads();
-    unsigned long long gsum = 0;
-    for (long long i = threadIdx.x; i < a.nsel; i += blockDim.x) {
-        const int s = a.sel_shard[i];
-        const int head = nsh_h ? s_head[s] : shard_head(v, s);
-        const int g = s * v.C + arrival_slot_h(v, s, a.sel_index[i], head);
-        a.sel_slot[i] = g;
-        const int L = v.len[g];
-        const double adv = v.adv[g];
-        atomicAdd(&v.use[g], 1u);
-        a.sel_len[i] = L;
-        gsum += (unsigned long long)L;
-        if (i >= a.lo && i < a.hi) {  // descriptor of an owned selection (offset below)
-            Unit d;
-            d.row = (s - v.sb) * v.C + (g - s * v.C);
-            d.len = L;
-            d.k0 = 0;
-            d.g = g;
-            d.off = 0;
-            d.adv = adv;
-            a.units[i - a.lo] = d;
-        }
-    }
-    {  // block sum of the lengths (warp shuffles; no shared-memory atomics)
-        __shared__ unsigned long long s_w[32];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
-        if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = gsum;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long t = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
-            s_global = t;
-        }
+        s_idx = idx;
+        s_draws = draws;
+        s_tw = tw;
     }
     __syncthreads();
-    RB_CLOCK(3);
-    // exclusive scan of the owned selections' lengths -> packed offsets, the
-    // descriptors' offsets, and the max work units per selection
-    const long long lo = a.lo, nloc = a.hi - a.lo;
-    int ups = 0;
-    {
-        const long long per = (nloc + blockDim.x - 1) / blockDim.x;
-        const long long i0 = threadIdx.x * per, i1 = i0 + per < nloc ? i0 + per : nloc;
-        constexpr int R = 8;  // register-resident run (longer runs loop)
-        int Lr[R];
-        long long local = 0;
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-            Lr[k] = (i0 + k < i1) ? a.sel_len[lo + i0 + k] : 0;
-            local += Lr[k];
-        }
-        for (long long i = i0 + R; i < i1; ++i) local += a.sel_len[lo + i];
-        long long total;
-        long long pos = block_exclusive_scan(local, &total);
-        auto put = [&](long long i, int L) {
-            a.off[i] = pos;
-            reinterpret_cast<long long*>(&a.units[i])[2] = pos;  // Unit::off
-            const int nq = ((int)(pos & 3) + L + 3) >> 2;
-            const int u = L ? nq : 0;  // destination quads
-            ups = u > ups ? u : ups;
-            pos += L;
-        };
-#pragma unroll
-        for (int k = 0; k < R; ++k)
-            if (i0 + k < i1) put(i0 + k, Lr[k]);
-        for (long long i = i0 + R; i < i1; ++i) put(i, a.sel_len[lo + i]);
-        if (threadIdx.x == 0) {
-            a.off[nloc] = total;
-            a.totals[0] = total;
-            a.totals[1] = (long long)s_global;
-        }
-    }
-    RB_CLOCK(4);
-    {
-        __shared__ int s_u[32];
-        ups = __reduce_max_sync(0xffffffffu, ups);
-        if ((threadIdx.x & 31) == 0) s_u[threadIdx.x >> 5] = ups;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int m = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = s_u[w] > m ? s_u[w] : m;
-            *a.n_units = m;  // max destination quads per selection
-            RB_CLOCK(5);
-            DevLossAcc* acc = a.acc;
-            acc->obj_sum = 0.0;
-            acc->included = 0;
-            acc->excluded = 0;
-            acc->done_blocks = 0;
-            acc->total_tokens = (long long)s_global;
-            acc->objective = 0.0;
-            acc->need_fixup = 0;
-        }
-    }
+    ring_store_state(r, mt, q0, s_tw, s_idx, s_draws);
 }
 
-__global__ void __launch_bounds__(1024) k_sample_map(BufView v, SampleArgs a) {
-    sample_map_phase(v, a);
+// ---------------------------------------------------------------- FIFO route
+// FIFO routing + eviction + group advantages + metadata scatter for ids
+// promised new and increasing (replay_buffer.cpp:83-133 in closed form;
+// bandit.cpp:276-294 per group), one record per thread, no grid barrier:
+// every CTA validates the whole batch itself (lengths, id order, group
+// offsets; ~16 B per record from L2) so it may apply its own records at
+// once, each record recomputes its group's statistics (the reference's
+// sequential fp64 order; the group's rewards are register-resident), and
+// the last CTA to finish advances the per-shard counters.  Nothing is
+// applied if the batch is invalid (the error is sticky until rb_check).
+constexpr int RT_THREADS = 128;  // small CTAs: fit beside the payload grid
+constexpr int RT_NSH = 256;
+constexpr int RT_GOFF = 2048;
+constexpr int GR = 16;  // rewards per register batch
+__device__ __forceinline__ void group_adv_one(const double* rw, long long b, long long e,
+                                              double rj, double* adv, double* mean_out) {
+    const long long m = e - b;
+    const double dn = (double)m;
+    double mean = 0.0, var = 0.0;
+    if (m <= GR) {
+        double r[GR];
+#pragma unroll
+        for (int k = 0; k < GR; ++k) r[k] = k < m ? rw[b + k] : 0.0;
+#pragma unroll
+        for (int k = 0; k < GR; ++k)
+            if (k < m) mean = __dadd_rn(mean, r[k]);
+        mean = __ddiv_rn(mean, dn);
+#pragma unroll
+        for (int k = 0; k < GR; ++k)
+            if (k < m) {
+                const double d = __dsub_rn(r[k], mean);
+                var = __dadd_rn(var, __dmul_rn(d, d));
+            }
+    } else {
+        for (long long k = b; k < e; ++k) mean = __dadd_rn(mean, rw[k]);
+        mean = __ddiv_rn(mean, dn);
+        for (long long k = b; k < e; ++k) {
+            const double d = __dsub_rn(rw[k], mean);
+            var = __dadd_rn(var, __dmul_rn(d, d));
+        }
+    }
+    var = __ddiv_rn(var, dn);
+    const double sd = __dsqrt_rn(var);
+    // bandit.cpp:289-292: zeros when the population std < 1e-8
+    *adv = sd < 1e-8 ? 0.0 : __ddiv_rn(__dsub_rn(rj, mean), sd);
+    *mean_out = mean;  // bandit.cpp:316-318 (same sequential sum)
 }
 
-// ---------------------------------------------------------------- cooperative
-// Multi-CTA versions of the two latency-bound steps for the common case
-// (FIFO retention, ids promised unique; uniform sampling).  One record /
-// selection per thread, one grid barrier between the read and write phases,
-// so the dependent-load chains run once per thread instead of serially.
-namespace cg = cooperative_groups;
-constexpr int COOP_THREADS = 256;
-
-// FIFO routing + eviction + group advantages + metadata scatter
-// (replay_buffer.cpp:83-133 closed form; bandit.cpp:276-294 per group).
-// Phase 1: per record routing/victims; per group (one thread) the reference's
-// sequential fp64 mean and population variance.  Phase 2 (after one grid
-// barrier): per record its advantage (r - mean) / sd and the metadata.  The
-// error flag alternates between two words by launch parity so no second
-// barrier is needed to reset it.
-__global__ void __launch_bounds__(COOP_THREADS) k_insert_route_fifo(BufView v, InsertIn in,
-                                                                    int parity) {
-    cg::grid_group grid = cg::this_grid();
+__global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn in, GridCtl* gc,
+                                                          int* pay_sync) {
+    __shared__ long long s_P[RT_NSH];
+    __shared__ long long s_goff[RT_GOFF + 1];
+    __shared__ int s_bad, s_last, s_m[RT_THREADS / 32];
+    const int tid = threadIdx.x;
     const int n = (int)in.n;
-    const int gt = blockIdx.x * blockDim.x + threadIdx.x, gn = gridDim.x * blockDim.x;
+    const long long ng = in.ngroups;
     DevCtl* ctl = v.ctl;
-    RB_CLOCK(20);
     RB_TSTART(0);
+    if (blockIdx.x == 0 && tid == 0) {  // this insert's verdict / completion flags
+        st_release_i32(&pay_sync[0], 0);
+        st_release_i32(&pay_sync[1], 0);
+    }
+    __syncthreads();
+    pdl_trigger();  // the closed-form payload copy may start now (it waits for pay_sync[0])
     const int sticky = ctl->err_code;
     const unsigned long long cur0 = ctl->cursor;
+    const int has_any = ctl->has_any;
+    const unsigned long long max_id = ctl->max_id;
     const int T = v.T, C = v.C;
     const int c0 = (int)(cur0 % (unsigned long long)T);
+    if (tid == 0) s_bad = sticky ? 8 : 0;
+    for (int s = tid; s < T && s < RT_NSH; s += RT_THREADS) s_P[s] = v.pushes[s];
+    const bool goff_smem = !in.adv && ng <= RT_GOFF;
+    if (goff_smem)
+        for (long long gi = tid; gi <= ng; gi += RT_THREADS) s_goff[gi] = in.goff[gi];
+    // own record (all loads issued before the validation sweep)
+    const int j = blockIdx.x * RT_THREADS + tid;
+    const bool mine = j < n;
+    uint64_t id = 0, prompt = 0, group = 0;
+    int64_t cstep = 0, pver = 0;
+    double reward = 0.0, blp = 0.0, adv = 0.0, gmean = 0.0;
+    bool correct = false;
+    long long off0 = 0, len = 0;
+    if (mine) {
+        id = in.id[j];
+        prompt = in.prompt ? in.prompt[j] : 0;
+        group = in.group ? in.group[j] : 0;
+        cstep = in.cstep ? in.cstep[j] : 0;
+        pver = in.pver ? in.pver[j] : 0;
+        reward = in.reward[j];
+        correct = in.correct ? in.correct[j] != 0 : reward == 1.0;
+        blp = in.blp ? in.blp[j] : 0.0;
+        if (in.adv) {
+            adv = in.adv[j];
+            gmean = in.gmean ? in.gmean[j] : 0.0;
+        }
+        if (in.toff) {
+            off0 = in.toff[j];
+            len = in.toff[j + 1] - off0;
+        }
+    }
+    // whole-batch validation (replay_buffer.cpp:85-88 order: nothing applied)
     int bad = 0;
-    if (gt == 0) ctl->batch_bad[parity ^ 1] = 0;  // the flag of the next launch
     if (!sticky) {
-        for (int j = gt; j < n; j += gn) {
-            long long l = in.toff ? in.toff[j + 1] - in.toff[j] : 0;
-            if (l < 0 || l > in.maxlen) {
-                bad |= 2;
-                l = 0;
+#pragma unroll 4
+        for (int jj = tid; jj < n; jj += RT_THREADS) {
+            if (in.toff) {
+                const long long l = in.toff[jj + 1] - in.toff[jj];
+                if (l < 0 || l > in.maxlen) bad |= 2;
             }
-            in.len[j] = (int32_t)l;
-            const uint64_t x = in.id[j];
-            if (j > 0 ? x <= in.id[j - 1] : (ctl->has_any && x <= ctl->max_id)) bad |= 1;
-            if (in.adv) {
-                in.adv_out[j] = in.adv[j];
-                in.gmean_out[j] = in.gmean ? in.gmean[j] : 0.0;
+            const uint64_t x = in.id[jj];
+            if (jj > 0 ? x <= in.id[jj - 1] : (has_any && x <= max_id)) bad |= 1;
+        }
+        if (!in.adv) {
+            if (tid == 0 && (in.goff[0] != 0 || in.goff[ng] != n)) bad |= 4;
+            for (long long gi = tid; gi < ng; gi += RT_THREADS) {
+                const long long b = in.goff[gi], e = in.goff[gi + 1];
+                if (e - b < 2 || b < 0 || e > n) bad |= 4;
             }
+        }
+    }
+    if (bad) atomicOr(&s_bad, bad);
+    __syncthreads();
+    const int bb = s_bad;
+    // every CTA reached the same verdict; CTA 0 alone publishes it
+    if (blockIdx.x == 0 && tid == 0) st_release_i32(&pay_sync[0], bb ? 2 : 1);
+    int maxq = 0;
+    if (mine) {
+        int32_t slot = -1;
+        uint8_t surv = 0;
+        uint64_t ev = NONE_ID;
+        Unit d;
+        d.row = -1;
+        d.len = (int32_t)(len < 0 ? 0 : len);
+        d.k0 = 0;
+        d.g = j;
+        d.off = off0;
+        d.adv = 0.0;
+        if (!bb) {
             int s = c0 + j % T;
             if (s >= T) s -= T;
             const int rank = j / T, j0 = j % T;
             const int ns = (n - 1 - j0) / T + 1;
-            const long long P = v.pushes[s];
+            const long long P = s < RT_NSH ? s_P[s] : v.pushes[s];
             int x2 = (int)(P % C) + rank % C;
             if (x2 >= C) x2 -= C;
             const size_t g = (size_t)s * C + (size_t)x2;
-            in.tslot[j] = (int32_t)g;
-            in.surv[j] = (rank + C >= ns);
-            uint64_t ev = NONE_ID;
+            slot = (int32_t)g;
+            surv = rank + C >= ns;
             if (P + rank >= C) ev = rank >= C ? in.id[j - C * T] : v.id[g];
-            in.evid[j] = ev;
-        }
-        if (!in.adv) {
-            if (gt == 0 && (in.goff[0] != 0 || in.goff[in.ngroups] != n)) bad |= 4;
-            for (long long gi = gt; gi < in.ngroups; gi += gn) {
-                const long long b = in.goff[gi], e = in.goff[gi + 1], m = e - b;
-                if (m < 2 || b < 0 || e > n) {
-                    bad |= 4;
-                    continue;
+            if (!in.adv) {
+                long long lo = 0, hi = ng;  // group gi: goff[gi] <= j < goff[gi+1]
+                while (hi - lo > 1) {
+                    const long long mid = (lo + hi) >> 1;
+                    const long long gm = goff_smem ? s_goff[mid] : in.goff[mid];
+                    if (gm <= j) lo = mid;
+                    else hi = mid;
                 }
-                const double dn = (double)m;
-                double mean = 0.0;
-#pragma unroll 8
-                for (long long k = b; k < e; ++k) mean = __dadd_rn(mean, in.reward[k]);
-                mean = __ddiv_rn(mean, dn);
-                double var = 0.0;
-#pragma unroll 8
-                for (long long k = b; k < e; ++k) {
-                    const double d = __dsub_rn(in.reward[k], mean);
-                    var = __dadd_rn(var, __dmul_rn(d, d));
-                }
-                var = __ddiv_rn(var, dn);
-                const double sd = __dsqrt_rn(var);
-                for (long long k = b; k < e; ++k) {
-                    in.adv_out[k] = sd;  // phase 2 turns it into the advantage
-                    in.gmean_out[k] = mean;
+                const long long b = goff_smem ? s_goff[lo] : in.goff[lo];
+                const long long e = goff_smem ? s_goff[lo + 1] : in.goff[lo + 1];
+                group_adv_one(in.reward, b, e, reward, &adv, &gmean);
+            }
+            if (surv) {
+                v.id[g] = id;
+                v.prompt[g] = prompt;
+                v.group[g] = group;
+                v.cstep[g] = cstep;
+                v.pver[g] = pver;
+                v.reward[g] = reward;
+                v.correct[g] = correct;
+                v.blp[g] = blp;
+                v.adv[g] = adv;
+                v.gmean[g] = gmean;
+                v.use[g] = 0;
+                v.len[g] = (int32_t)len;
+                if (s >= v.sb && s < v.se && len > 0 && v.stride > 0) {
+                    d.row = (s - v.sb) * C + x2;
+                    maxq = (int)((len + 3) >> 2);
                 }
             }
         }
+        in.len[j] = (int32_t)(len < 0 ? 0 : len);
+        in.tslot[j] = slot;
+        in.surv[j] = surv;
+        in.evid[j] = ev;
+        in.adv_out[j] = adv;
+        in.gmean_out[j] = gmean;
+        in.units[j] = d;
     }
-    RB_CLOCK(21);
-    if (bad) atomicOr(&ctl->batch_bad[parity], bad);
-    if (gt == 0) *in.n_units = 0;
-    grid.sync();
-    RB_CLOCK(22);
-    const int bb = sticky ? 8 : *(volatile int*)&ctl->batch_bad[parity];
-    if (bb) {  // nothing is applied; the error is sticky until rb_check
-        for (int j = gt; j < n; j += gn) {
-            in.surv[j] = 0;
-            in.tslot[j] = -1;
-            in.evid[j] = NONE_ID;
-            in.units[j].row = -1;
-        }
-        if (gt == 0 && !sticky) {
-            ctl->err_code = RB_EINVAL;
-            ctl->err_index = (bb & 2) ? -3 : (bb & 4) ? -2 : -4;
-        }
-    } else {
-        int maxq = 0;
-        for (int j = gt; j < n; j += gn) {
-            if (!in.adv) {  // bandit.cpp:289-292: zeros when the population std < 1e-8
-                const double sd = in.adv_out[j];
-                in.adv_out[j] =
-                    sd < 1e-8 ? 0.0 : __ddiv_rn(__dsub_rn(in.reward[j], in.gmean_out[j]), sd);
-            }
-            const int g = in.tslot[j];
-            Unit d;
-            d.row = -1;
-            d.len = in.len[j];
-            d.k0 = 0;
-            d.g = j;
-            d.off = in.toff ? in.toff[j] : 0;
-            d.adv = 0.0;
-            if (in.surv[j]) {
-                write_meta(v, (size_t)g, in, j);
-                const int s = g / C;
-                if (s >= v.sb && s < v.se && d.len > 0 && v.stride > 0) {
-                    d.row = (s - v.sb) * C + (g - s * C);
-                    const int q = (d.len + 3) >> 2;
-                    maxq = q > maxq ? q : maxq;
-                }
-            }
-            in.units[j] = d;
-        }
-        RB_CLOCK(23);
-        maxq = __reduce_max_sync(0xffffffffu, maxq);
-        if ((threadIdx.x & 31) == 0 && maxq) atomicMax(in.n_units, maxq);
-        for (int s = gt; s < T; s += gn) {
+    maxq = __reduce_max_sync(0xffffffffu, maxq);
+    if ((tid & 31) == 0) s_m[tid >> 5] = maxq;
+    __syncthreads();
+    if (tid == 0) {
+        int m = 0;
+        for (int w = 0; w < RT_THREADS / 32; ++w) m = s_m[w] > m ? s_m[w] : m;
+        gc->cta_max[blockIdx.x] = m;
+        __threadfence();
+        s_last = atomicAdd(&gc->done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // last CTA: counters (every CTA read them before its done increment)
+    __threadfence();
+    int m = 0;
+    for (int c = tid; c < (int)gridDim.x; c += RT_THREADS) m = max(m, __ldcg(&gc->cta_max[c]));
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((tid & 31) == 0) s_m[tid >> 5] = m;
+    if (!bb)
+        for (int s = tid; s < T; s += RT_THREADS) {
             const int j0 = ((s - c0) % T + T) % T;
             const int ns = n > j0 ? (n - 1 - j0) / T + 1 : 0;
             v.pushes[s] += ns;
         }
-        if (gt == 0) {
+    __syncthreads();
+    if (tid == 0) {
+        int mm = 0;
+        for (int w = 0; w < RT_THREADS / 32; ++w) mm = s_m[w] > mm ? s_m[w] : mm;
+        *in.n_units = bb ? 0 : mm;
+        if (!bb) {
             ctl->cursor = (cur0 + (unsigned long long)n) % T;
             ctl->max_id = in.id[n - 1];  // strictly increasing and above the old max
             ctl->has_any = 1;
             ctl->hash_stale = 1;
+        } else if (!sticky) {
+            ctl->err_code = RB_EINVAL;
+            ctl->err_index = (bb & 2) ? -3 : (bb & 4) ? -2 : -4;
         }
+        gc->done = 0;
+        st_release_i32(&pay_sync[1], 1);  // the sampler's map may read the metadata
     }
-    RB_CLOCK(24);
     RB_TEND(0);
-}
-
-// Sampler map phase, cooperative: slots, use counts, lengths, descriptors,
-// packed offsets (per-CTA sums + a grid barrier + per-CTA scan).
-__global__ void __launch_bounds__(COOP_THREADS) k_sample_map_coop(BufView v, SampleArgs a,
-                                                                  long long* cta_sums) {
-    cg::grid_group grid = cg::this_grid();
-    RB_CLOCK(30);
-    RB_TSTART(3);
-    __shared__ int s_head[64];
-    __shared__ long long s_red[2][32];
-    const int nsh_h = a.nsh < 64 ? a.nsh : 0;
-    for (int s = threadIdx.x; s < nsh_h; s += blockDim.x) s_head[s] = shard_head(v, s);
-    __syncthreads();
-    const long long nsel = a.nsel;
-    const long long per_cta = (nsel + gridDim.x - 1) / gridDim.x;
-    const long long i0 = blockIdx.x * per_cta;
-    const long long i1 = i0 + per_cta < nsel ? i0 + per_cta : nsel;
-    long long own_sum = 0, all_sum = 0;
-    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-        const int s = a.sel_shard[i];
-        const int head = nsh_h ? s_head[s] : shard_head(v, s);
-        const int g = s * v.C + arrival_slot_h(v, s, a.sel_index[i], head);
-        a.sel_slot[i] = g;
-        const int L = v.len[g];
-        const double adv = v.adv[g];
-        atomicAdd(&v.use[g], 1u);
-        a.sel_len[i] = L;
-        all_sum += L;
-        if (i >= a.lo && i < a.hi) {
-            own_sum += L;
-            Unit d;
-            d.row = (s - v.sb) * v.C + (g - s * v.C);
-            d.len = L;
-            d.k0 = 0;
-            d.g = g;
-            d.off = 0;
-            d.adv = adv;
-            a.units[i - a.lo] = d;
-        }
-    }
-    RB_CLOCK(31);
-    own_sum = warp_sum_i64(own_sum);
-    all_sum = warp_sum_i64(all_sum);
-    if ((threadIdx.x & 31) == 0) {
-        s_red[0][threadIdx.x >> 5] = own_sum;
-        s_red[1][threadIdx.x >> 5] = all_sum;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        long long o = 0, t = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-            o += s_red[0][w];
-            t += s_red[1][w];
-        }
-        cta_sums[2 * blockIdx.x] = o;
-        cta_sums[2 * blockIdx.x + 1] = t;
-        if (blockIdx.x == 0) *a.n_units = 0;
-    }
-    grid.sync();
-    RB_CLOCK(32);
-    // base of this CTA = owned lengths of all earlier CTAs
-    long long base = 0, total = 0, gtotal = 0;
-    for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
-        const long long o = __ldcg(&cta_sums[2 * c]);
-        if (c < (int)blockIdx.x) base += o;
-        total += o;
-        gtotal += __ldcg(&cta_sums[2 * c + 1]);
-    }
-    base = warp_sum_i64(base);
-    total = warp_sum_i64(total);
-    gtotal = warp_sum_i64(gtotal);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) {
-        s_red[0][threadIdx.x >> 5] = base;
-        s_red[1][threadIdx.x >> 5] = total;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        long long b2 = 0, t2 = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-            b2 += s_red[0][w];
-            t2 += s_red[1][w];
-        }
-        s_red[0][0] = b2;
-        s_red[1][0] = t2;
-    }
-    __syncthreads();
-    long long carry = s_red[0][0];
-    total = s_red[1][0];
-    int maxq = 0;
-    // scan this CTA's owned selections in chunks of blockDim, carrying across
-    const long long lo = a.lo;
-    const long long o0 = i0 > a.lo ? i0 : a.lo, o1 = i1 < a.hi ? i1 : a.hi;
-    for (long long cb = o0; cb < o1; cb += blockDim.x) {
-        const long long i = cb + threadIdx.x;
-        const long long L = i < o1 ? a.sel_len[i] : 0;
-        long long chunk_total;
-        const long long ex = block_exclusive_scan(L, &chunk_total);
-        if (i < o1) {
-            const long long pos = carry + ex;
-            a.off[i - lo] = pos;
-            reinterpret_cast<long long*>(&a.units[i - lo])[2] = pos;  // Unit::off
-            const int nq = ((int)(pos & 3) + (int)L + 3) >> 2;
-            if (L) maxq = nq > maxq ? nq : maxq;
-        }
-        carry += chunk_total;
-    }
-    RB_CLOCK(33);
-    maxq = __reduce_max_sync(0xffffffffu, maxq);
-    if ((threadIdx.x & 31) == 0 && maxq) atomicMax(a.n_units, maxq);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.off[a.hi - a.lo] = total;
-        a.totals[0] = total;
-        a.totals[1] = gtotal;
-        DevLossAcc* acc = a.acc;
-        acc->obj_sum = 0.0;
-        acc->included = 0;
-        acc->excluded = 0;
-        acc->done_blocks = 0;
-        acc->total_tokens = gtotal;
-        acc->objective = 0.0;
-        acc->need_fixup = 0;
-    }
-    RB_TEND(3);
 }
 
 // Record copies with the post-increment use count in draw order
@@ -1275,19 +1691,13 @@ rb_buffer::~rb_buffer() {
                     v.correct, v.use, v.len, v.order, v.head, v.pushes, v.owner, v.tok, v.lpo,
                     v.hkeys, v.hstate, v.ctl, s_tslot, s_surv, s_evid, s_evrec, s_adv, s_gmean,
                     s_len, s_toff, sel_slot, sel_shard, sel_index, sel_off, sel_total,
-                    acc, misc, n_units_ins, n_units_sel, loss_partials, coop_sums};
+                    acc, misc, n_units_ins, n_units_sel, loss_partials, route_ctl, map_ctl, pay_sync};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : stage_dev)
         if (p) cudaFree(p);
     if (stage_host) cudaFreeHost(stage_host);
     if (stage_event) cudaEventDestroy(stage_event);
-    if (aux) cudaStreamSynchronize(aux);
-    if (ev_draw) cudaEventDestroy(ev_draw);
-    if (ev_map) cudaEventDestroy(ev_map);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_pre) cudaEventDestroy(ev_pre);
-    if (aux) cudaStreamDestroy(aux);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -1366,10 +1776,7 @@ void rb_buffer::ensure_select(size_t n) {
     sel_index = dalloc<int64_t>(sel_cap);
     sel_off = dalloc<int64_t>(sel_cap + 1);
 }
-void rb_buffer::sync() {
-    RB_CUDA(cudaStreamSynchronize(stream));
-    if (aux) RB_CUDA(cudaStreamSynchronize(aux));
-}
+void rb_buffer::sync() { RB_CUDA(cudaStreamSynchronize(stream)); }
 
 namespace {
 
@@ -1463,13 +1870,6 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         b->se = se;
         RB_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
         b->own_stream = true;
-        int prio_lo = 0, prio_hi = 0;
-        RB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-        RB_CUDA(cudaStreamCreateWithPriority(&b->aux, cudaStreamNonBlocking, prio_hi));
-        RB_CUDA(cudaEventCreateWithFlags(&b->ev_draw, cudaEventDisableTiming));
-        RB_CUDA(cudaEventCreateWithFlags(&b->ev_map, cudaEventDisableTiming));
-        RB_CUDA(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
-        RB_CUDA(cudaEventCreateWithFlags(&b->ev_pre, cudaEventDisableTiming));
         BufView& v = b->v;
         v.T = (int)T;
         v.C = (int)b->C;
@@ -1512,6 +1912,20 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         b->acc = dalloc<DevLossAcc>(1);
         int sms = 148;
         RB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        // One shared-memory carveout for the kernels that run side by side: an
+        // SM configured for a smem-less streaming kernel (max L1) cannot take
+        // a CTA that needs shared memory until it drains, which would
+        // serialise the route / sampler CTAs behind the persistent copy grid.
+        // The copy bypasses L1 (ld.global.nc.L1::no_allocate).
+        {
+            const void* ks[] = {(const void*)k_route_fifo, (const void*)k_sample_fused,
+                                (const void*)k_sample_map, (const void*)k_insert_payload<PAYLOAD_U>,
+                                (const void*)k_insert_payload_fifo<PAYLOAD_U>,
+                                (const void*)k_insert_route};
+            for (const void* k : ks)
+                RB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             cudaSharedmemCarveoutMaxShared));
+        }
         b->unit_grid = sms * UNIT_CTAS_PER_SM;
         // Persistent grids: exactly the resident CTAs of each kernel.  The
         // payload copy overlaps the sampler's draw CTA, so it leaves room.
@@ -1521,15 +1935,34 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         b->grid_gather = sms * std::max(occ, 1);
         RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_insert_payload<PAYLOAD_U>,
                                                               UNIT_THREADS, 0));
-        b->payload_grid = sms * std::max(occ - 2, 1);
+        {
+            int occ2 = 0;
+            RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &occ2, k_insert_payload_fifo<PAYLOAD_U>, UNIT_THREADS, 0));
+            occ = std::min(occ, occ2);
+        }
+        // The copy overlaps the latency-bound route / sampler kernels: keep
+        // only the bytes in flight that saturate HBM (more only deepens the
+        // memory queues those kernels' dependent loads wait in), and leave
+        // room on every SM for their CTAs.
+        {
+            int per_sm = 3;
+            if (const char* e = std::getenv("RB_PAYLOAD_CTAS")) per_sm = std::atoi(e);
+            b->payload_grid = sms * std::max(1, std::min(per_sm, occ - 2));
+        }
         b->grid_loss = loss_grid(sms);
-        RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_insert_route_fifo,
-                                                              COOP_THREADS, 0));
-        b->coop_route_max = sms * std::max(occ, 1);
-        RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sample_map_coop,
-                                                              COOP_THREADS, 0));
-        b->coop_map_max = sms * std::max(occ, 1);
-        b->coop_sums = dalloc<long long>(2 * (size_t)b->coop_map_max);
+        b->route_ctl = dalloc<GridCtl>(1);
+        b->pay_sync = dalloc<int>(2);
+        {  // no insert yet: the route-completion flag starts set
+            const int one = 1;
+            RB_CUDA(cudaMemcpy(b->pay_sync + 1, &one, sizeof one, cudaMemcpyHostToDevice));
+        }
+        b->pdl = std::getenv("RB_NO_PDL") == nullptr;
+        b->map_ctl = dalloc<GridCtl>(1);
+        {
+            const int none = INT_MAX;
+            RB_CUDA(cudaMemcpy(&b->map_ctl->first_rej, &none, sizeof none, cudaMemcpyHostToDevice));
+        }
         b->n_units_ins = dalloc<int>(1);
         b->n_units_sel = dalloc<int>(1);
         b->loss_partials = dalloc<char>((size_t)b->unit_grid * 32);
@@ -1540,6 +1973,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
     }
     return b;
 }
+
 
 // Insert `bt` (pointers already resolved to device memory; lens/toff device)
 void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, bool unique) {
@@ -1570,40 +2004,51 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
     in.units = b->units_ins;
     in.n_units = b->n_units_ins;
     if (!payload) in.toff = bt.tok_offsets;  // lengths only
-    // The next sampler's MT draws may start before the route (they need only
-    // the RNG state and the occupancies); its map phase after it.
-    RB_CUDA(cudaEventRecord(b->ev_pre, b->stream));
-    if (unique && b->retention == RB_PLAIN_FIFO && !want_evrec && bt.n <= (size_t)INT32_MAX) {
-        // ids promised new and increasing: the cooperative FIFO kernel
-        const int grid = (int)std::min<size_t>((bt.n + COOP_THREADS - 1) / COOP_THREADS,
-                                               (size_t)b->coop_route_max);
-        int parity = b->route_parity;
-        b->route_parity ^= 1;
-        void* args[] = {(void*)&b->v, (void*)&in, (void*)&parity};
-        RB_CUDA(cudaLaunchCooperativeKernel((void*)k_insert_route_fifo, dim3(std::max(grid, 1)),
-                                            dim3(COOP_THREADS), args, 0, b->stream));
+    bool closed = false;
+    if (unique && b->retention == RB_PLAIN_FIFO && !want_evrec &&
+        bt.n <= (size_t)RT_THREADS * GRID_MAX_CTAS) {
+        // ids promised new and increasing: the closed-form FIFO route
+        const unsigned grid = (unsigned)((bt.n + RT_THREADS - 1) / RT_THREADS);
+        closed = payload && b->T <= 64 && b->pdl;
+        k_route_fifo<<<grid, RT_THREADS, 0, b->stream>>>(b->v, in, b->route_ctl, b->pay_sync);
     } else {
         k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
     }
     RB_CUDA(cudaGetLastError());
-    // The next sampler's map phase may start here: it needs the route's
-    // metadata, not the payload copy enqueued next.
-    RB_CUDA(cudaEventRecord(b->ev_fork, b->stream));
-    b->fork_valid = true;
-    if (payload) {
+    if (payload && closed) {
+        // closed-form copy as a programmatic dependent of the route
+        FifoPlan p{};
+        p.c0 = (int)(b->h_cursor % b->T);
+        p.T = (int)b->T;
+        p.C = (int)b->C;
+        const int maxq = (b->max_tokens + 3) / 4;
+        p.ups = std::max(1, (maxq + UNIT_THREADS * PAYLOAD_U - 1) / (UNIT_THREADS * PAYLOAD_U));
+        for (size_t s = 0; s < b->T; ++s) p.pm[s] = (int)(b->h_pushes[s] % (long long)b->C);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(b->payload_grid);
+        cfg.blockDim = dim3(UNIT_THREADS);
+        cfg.stream = b->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        RB_CUDA(cudaLaunchKernelEx(&cfg, k_insert_payload_fifo<PAYLOAD_U>, b->v, p, bt.tok_offsets,
+                                   (int)bt.n, bt.tokens, bt.logp_old, b->pay_sync));
+        b->pdl_tail = true;  // a sampler launched next may overlap this copy
+        b->pend.pending = 1;
+        b->pend.c0 = p.c0;
+        b->pend.n = (int)bt.n;
+        b->pend.toff = bt.tok_offsets;
+        for (size_t s = 0; s < b->T; ++s) b->pend.P[s] = b->h_pushes[s];
+    } else if (payload) {
         k_insert_payload<PAYLOAD_U><<<b->payload_grid, UNIT_THREADS, 0, b->stream>>>(
             b->v, b->units_ins, b->n_units_ins, (int)bt.n, bt.tokens, bt.logp_old);
         RB_CUDA(cudaGetLastError());
+        b->pdl_tail = false;
+    } else {
+        b->pdl_tail = false;
     }
-}
-
-void launch_map(rb_buffer* b, SampleArgs& a, cudaStream_t stream) {
-    const long long grid =
-        std::max<long long>(1, std::min<long long>((a.nsel + COOP_THREADS - 1) / COOP_THREADS,
-                                                   (long long)b->coop_map_max));
-    void* args[] = {(void*)&b->v, (void*)&a, (void*)&b->coop_sums};
-    RB_CUDA(cudaLaunchCooperativeKernel((void*)k_sample_map_coop, dim3((unsigned)grid),
-                                        dim3(COOP_THREADS), args, 0, stream));
 }
 
 }  // namespace
@@ -1894,46 +2339,51 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         a.acc = b->acc;
         a.units = b->units_sel;
         a.n_units = b->n_units_sel;
-        if (nsh > 0 && b->strategy == RB_UNIFORM_WITH_REPLACEMENT) {
-            // Draws on the auxiliary stream: they need only the RNG state and
-            // the occupancies (host mirror), so they overlap the insert.
-            a.occ_known = b->T <= 64;
-            for (size_t s = 0; s < b->T && s < 64; ++s)
+        const unsigned nmap = (unsigned)std::max<size_t>(1, (nsel + MAP_SPC - 1) / MAP_SPC);
+        if (nmap > (unsigned)GRID_MAX_CTAS) invalid("rb_sample: batch too large");
+        if (b->strategy == RB_UNIFORM_WITH_REPLACEMENT) {
+            // One fused launch (ring generator + draws + map), a programmatic
+            // dependent of the insert's payload copy when that is the last
+            // kernel on the stream: it overlaps the copy and waits for the
+            // route kernel's completion flag itself.
+            for (size_t s = 0; s < nsh && s < (size_t)DRAW_NSH; ++s)
                 a.occ[s] = std::min<long long>(b->h_pushes[s], (long long)b->C);
-            cudaStream_t ds = a.occ_known ? b->aux : b->stream;
-            if (a.occ_known) {
-                // Fork the auxiliary stream: the draws from just before the
-                // last insert's route kernel (if nothing else intervened), the
-                // map phase after it; both overlap the payload copy.
-                if (!b->fork_valid) RB_CUDA(cudaEventRecord(b->ev_fork, b->stream));
-                RB_CUDA(cudaStreamWaitEvent(b->aux, b->fork_valid ? b->ev_pre : b->ev_fork, 0));
+            a.occ_dev = nullptr;
+            if (nsh > (size_t)DRAW_NSH) {  // occupancies for every shard, staged on the stream
+                std::vector<long long> occ(nsh);
+                for (size_t s = 0; s < nsh; ++s) occ[s] = std::min<long long>(b->h_pushes[s], (long long)b->C);
+                long long* d = (long long*)b->dev_stage(nsh * sizeof(long long), rb_buffer::ST_OCC);
+                RB_CUDA(cudaMemcpyAsync(d, occ.data(), nsh * sizeof(long long), cudaMemcpyHostToDevice,
+                                        b->stream));
+                RB_CUDA(cudaStreamSynchronize(b->stream));  // `occ` is a host temporary
+                a.occ_dev = d;
             }
-            MtState* st = rng->to_device(ds);
-            k_sample_draw<<<1, DRAW_THREADS, 0, ds>>>(b->v, st, a);
-            RB_CUDA(cudaGetLastError());
-            rng->used_on(ds);
-            if (a.occ_known) {
-                if (b->fork_valid) RB_CUDA(cudaStreamWaitEvent(b->aux, b->ev_fork, 0));
-                launch_map(b, a, b->aux);
-                RB_CUDA(cudaEventRecord(b->ev_map, b->aux));
-                RB_CUDA(cudaStreamWaitEvent(b->stream, b->ev_map, 0));
-            } else {
-                launch_map(b, a, b->stream);
-                RB_CUDA(cudaEventRecord(b->ev_map, b->stream));
-            }
-            b->fork_valid = false;
+            MtRing* ring = rng->to_device(b->stream);
+            if (b->pdl_tail) a.pend = b->pend;  // the insert just enqueued may still run
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(nmap + 1);
+            cfg.blockDim = dim3(MAP_THREADS);
+            cfg.stream = b->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = b->pdl_tail ? 1 : 0;
+            const int* route_done = b->pay_sync + 1;
+            RB_CUDA(cudaLaunchKernelEx(&cfg, k_sample_fused, b->v, ring, a, b->map_ctl, route_done));
+            rng->used_on(b->stream);
         } else {
+            MtRing* ring = rng->to_device(b->stream);
             if (nsh > 0) {
-                MtState* st = rng->to_device(b->stream);
                 int64_t* scr = (int64_t*)b->scratch(2 * b->C * sizeof(int64_t) + 16);
-                k_sample_without<<<1, 32, 0, b->stream>>>(b->v, st, a, b->strategy, scr);
+                k_sample_without<<<1, 32, 0, b->stream>>>(b->v, ring, a, b->strategy, scr);
                 RB_CUDA(cudaGetLastError());
-                rng->used_on(b->stream);
             }
-            launch_map(b, a, b->stream);
-            RB_CUDA(cudaEventRecord(b->ev_map, b->stream));
-            b->fork_valid = false;
+            rng->used_on(b->stream);
+            k_sample_map<<<nmap, MAP_THREADS, 0, b->stream>>>(b->v, a, b->map_ctl, b->pay_sync + 1);
+            RB_CUDA(cudaGetLastError());
         }
+        b->pdl_tail = false;
         b->B = nsel;
         b->last_loss = -1;
         if (nsel > 0 && (out_records || out_events)) {
@@ -2416,7 +2866,7 @@ extern "C" __attribute__((visibility("default"))) int rb_debug_timeline(unsigned
         RB_CUDA(cudaMemcpyFromSymbol(out, g_timeline, 64 * sizeof(unsigned long long)));
         if (reset) {
             unsigned long long init[64];
-            for (int i = 0; i < 64; ++i) init[i] = (i & 1) ? 0ULL : ~0ULL;
+            for (int i = 0; i < 64; ++i) init[i] = (i < 32 && !(i & 1)) ? ~0ULL : 0ULL;
             RB_CUDA(cudaMemcpyToSymbol(g_timeline, init, sizeof init));
         }
 #else
@@ -2425,6 +2875,9 @@ extern "C" __attribute__((visibility("default"))) int rb_debug_timeline(unsigned
     });
 }
 
+extern "C" __attribute__((visibility("default"))) int rb_debug_locb(long long* out) {
+    return guard([&] { RB_CUDA(cudaMemcpyFromSymbol(out, g_dbg_locb, 2 * sizeof(long long))); });
+}
 extern "C" __attribute__((visibility("default"))) int rb_debug_phase_clocks(long long* out) {
     return guard([&] {
 #ifdef RB_PHASE_CLOCKS

@@ -29,8 +29,7 @@ struct DevCtl {
     int err_code;  // sticky asynchronous error (RB_EINVAL)
     int has_any;   // max_id valid
     int hash_stale;
-    int batch_bad[2];  // error flags of the cooperative insert, by launch parity
-    int pad;
+    int pad[3];
 };
 
 // Everything a kernel needs, passed by value.
@@ -56,7 +55,14 @@ struct BufView {
     DevCtl* ctl;
 };
 
-int loss_grid(int sms);  // loss.cu: resident CTAs of the loss kernels
+int loss_grid(int sms);
+struct GridCtl;  // buffer.cu: multi-CTA bookkeeping
+struct PendingIns {
+    int pending;          // 1: the last insert (closed-form FIFO, <= 64 shards) may be running
+    int c0, n;            // its cursor % T and record count
+    const int64_t* toff;  // its payload offsets
+    long long P[64];      // per-shard push counts before it
+};  // loss.cu: resident CTAs of the loss kernels
 
 }  // namespace rb
 
@@ -86,7 +92,7 @@ struct rb_buffer {
     int32_t* s_len = nullptr;
     int64_t* s_toff = nullptr;
     // staging of host-side insert inputs (device side) and pinned mirrors
-    enum { ST_INSERT = 0, ST_SAMPLE, ST_GATHER, ST_IDS, ST_INSPECT, ST_LOSS_IN, ST_LOSS_OUT, ST_N };
+    enum { ST_INSERT = 0, ST_SAMPLE, ST_GATHER, ST_IDS, ST_INSPECT, ST_LOSS_IN, ST_LOSS_OUT, ST_OCC, ST_N };
     void* stage_dev[ST_N] = {};
     size_t stage_dev_cap[ST_N] = {};
     void* stage_host = nullptr;
@@ -96,14 +102,14 @@ struct rb_buffer {
     // persistent-kernel work units (stream_copy.cuh)
     int unit_grid = 0;                  // SMs * UNIT_CTAS_PER_SM
     int payload_grid = 0, grid_gather = 0, grid_loss = 0;
-    int coop_route_max = 0, coop_map_max = 0;  // co-resident CTAs of the cooperative kernels
-    long long* coop_sums = nullptr;           // [2 * coop_map_max]
-    cudaStream_t aux = nullptr;         // sampler draws (overlap the insert)
-    cudaEvent_t ev_draw = nullptr, ev_map = nullptr;
-    cudaEvent_t ev_fork = nullptr;      // after the last route kernel (map may start)
-    cudaEvent_t ev_pre = nullptr;       // before the last route kernel (draws may start)
-    bool fork_valid = false;            // ev_fork recorded after the last route kernel
-    int route_parity = 0;
+    rb::GridCtl* route_ctl = nullptr;   // multi-CTA route bookkeeping
+    rb::GridCtl* map_ctl = nullptr;     // multi-CTA sampler-map bookkeeping
+    int* pay_sync = nullptr;            // [verdict, done] of the last FIFO route (0 = pending;
+                                        // verdict 1 valid / 2 rejected), read by the payload copy
+                                        // and the fused sampler
+    bool pdl = true;                    // programmatic dependent launch of the payload copy
+    bool pdl_tail = false;              // the stream's last kernel is the closed-form payload copy
+    rb::PendingIns pend{};              // its insert's plan (for a sampler that overlaps it)
     rb::Unit* units_ins = nullptr;      // payload copy units of the last insert
     int* n_units_ins = nullptr;
     size_t units_ins_cap = 0;

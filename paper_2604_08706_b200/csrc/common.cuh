@@ -27,7 +27,7 @@ void set_last_error(const std::string& msg);
                                             cudaGetErrorString(_e) + " at " #expr);    \
     } while (0)
 
-inline void invalid(const std::string& m) { throw Error(RB_EINVAL, m); }
+[[noreturn]] inline void invalid(const std::string& m) { throw Error(RB_EINVAL, m); }
 
 template <class F>
 int guard(F&& f) {
@@ -95,6 +95,39 @@ __host__ __device__ inline uint64_t mt_next_scalar(uint64_t* mt, uint32_t* idx,
     ++*draws;
     return mt_temper(mt[(*idx)++]);
 }
+// Device home of a stream: a ring of twisted MT blocks.  Block q is the
+// state after q twists of the ring's base state (block 0); the current state
+// is (block q_state, idx) and blocks (q_state, q_hi] are twisted AHEAD by a
+// generator kernel off the sampler's critical path, so a sampler only tempers
+// words it reads.  Word o (o >= 0) after the current position is word
+// (idx + o) % MT_N of block q_state + (idx + o) / MT_N.  Any consumer that
+// twists itself produces the same blocks (the stream is deterministic).
+constexpr int MT_KR = 64;  // ring capacity in blocks (19968 outputs)
+struct MtRing {
+    long long q_state;  // block of the current state
+    long long q_hi;     // last block held; [q_state, q_hi] are resident
+    uint32_t idx;       // next word of block q_state (MT_N: block exhausted)
+    uint32_t pad;
+    uint64_t draws;     // outputs consumed since seeding (parity aid)
+    long long gen_q;    // generator progress within a fused sampler (<= q_hi otherwise)
+    uint64_t blk[MT_KR][MT_N];
+};
+struct MtRingHead {  // the first bytes of MtRing (host-side header copies)
+    long long q_state, q_hi;
+    uint32_t idx, pad;
+    uint64_t draws;
+    long long gen_q;
+};
+static_assert(sizeof(MtRingHead) == 40, "MtRing header layout");
+// Advance (q, idx) past d outputs, keeping idx in [1, MT_N] once moved.
+__host__ __device__ __forceinline__ void ring_advance(long long& q, uint32_t& idx,
+                                                     unsigned long long d) {
+    if (d == 0) return;
+    const unsigned long long o = (unsigned long long)idx + d;
+    q += (long long)((o - 1) / MT_N);
+    idx = (uint32_t)((o - 1) % MT_N + 1);
+}
+
 // rng.cpp:44: values >= limit are rejected.
 __host__ __device__ __forceinline__ uint64_t below_limit(uint64_t bound) {
     return UINT64_MAX - UINT64_MAX % bound;
@@ -102,24 +135,103 @@ __host__ __device__ __forceinline__ uint64_t below_limit(uint64_t bound) {
 
 // Block-cooperative twist of a shared-memory MT state in three dependency
 // phases (i < 156 reads only old words; 156 <= i < 311 reads new words
-// i-156; i = 311 reads new word 0).  Requires blockDim.x >= 156; every
-// thread of the block must call it.
+// i-156; i = 311 reads new word 0).  Any blockDim.x >= 52 (each thread
+// computes up to three words per phase into registers); every thread of the
+// block must call it.
 __device__ __forceinline__ void mt_twist_block(uint64_t* mt) {
-    const int t = threadIdx.x;
-    uint64_t v = 0;
-    if (t < 156) v = mt[t + 156] ^ mt_mix(mt[t], mt[t + 1]);
+    const int t = threadIdx.x, nt = blockDim.x;
+    uint64_t v[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int i = t + r * nt;
+        if (i < 156) v[r] = mt[i + 156] ^ mt_mix(mt[i], mt[i + 1]);
+    }
     __syncthreads();
-    if (t < 156) mt[t] = v;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int i = t + r * nt;
+        if (i < 156) mt[i] = v[r];
+    }
     __syncthreads();
-    if (t < 155) v = mt[t] ^ mt_mix(mt[t + 156], mt[t + 157]);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int i = 156 + t + r * nt;
+        if (i < 311) v[r] = mt[i - 156] ^ mt_mix(mt[i], mt[i + 1]);
+    }
     __syncthreads();
-    if (t < 155) mt[t + 156] = v;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int i = 156 + t + r * nt;
+        if (i < 311) mt[i] = v[r];
+    }
     __syncthreads();
     if (t == 0) mt[311] = mt[155] ^ mt_mix(mt[311], mt[0]);
     __syncthreads();
 }
 
+// Block-wide: twist ring blocks (qhi, target] from block qhi (shared scratch
+// `mt`, blockDim.x >= 52; every thread calls with the same arguments).
+// The caller guarantees target - q_state < MT_KR.
+__device__ __forceinline__ void ring_extend(MtRing* r, uint64_t* mt, long long qhi,
+                                            long long target) {
+    if (qhi >= target) return;
+    const uint64_t* src = r->blk[qhi % MT_KR];
+    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = src[i];
+    __syncthreads();
+    for (long long q = qhi + 1; q <= target; ++q) {
+        mt_twist_block(mt);
+        uint64_t* dst = r->blk[q % MT_KR];
+        for (int i = threadIdx.x; i < MT_N; i += blockDim.x) dst[i] = mt[i];
+    }
+    __syncthreads();
+}
+// Block-wide: copy the current state's block into shared `mt`.
+__device__ __forceinline__ void ring_load_block(const MtRing* r, long long q, uint64_t* mt) {
+    const uint64_t* src = r->blk[q % MT_KR];
+    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = src[i];
+    __syncthreads();
+}
+// Block-wide: a consumer that advanced a shared copy `mt` of block q0 by
+// `tw` twists to index idx publishes the new state (block q0 + tw).
+__device__ __forceinline__ void ring_store_state(MtRing* r, const uint64_t* mt, long long q0,
+                                                 long long tw, uint32_t idx, uint64_t draws) {
+    const long long q = q0 + tw, qhi = r->q_hi;
+    __syncthreads();
+    if (q > qhi) {
+        uint64_t* dst = r->blk[q % MT_KR];
+        for (int i = threadIdx.x; i < MT_N; i += blockDim.x) dst[i] = mt[i];
+    }
+    if (threadIdx.x == 0) {
+        r->q_state = q;
+        r->q_hi = q > qhi ? q : qhi;
+        r->idx = idx;
+        r->draws = draws;
+    }
+    __syncthreads();
+}
+
 // ---- small device helpers ----------------------------------------------
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long x) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long x;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+    return x;
+}
+__device__ __forceinline__ void st_release_i32(int* p, int x) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+    int x;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+    return x;
+}
+// Programmatic dependent launch: let the next kernel of the stream (launched
+// with programmatic serialization) start while this one runs.
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -146,9 +258,18 @@ __device__ __forceinline__ unsigned long long rb_globaltimer() {
     do {                                                             \
         if (threadIdx.x == 0 && blockIdx.x == 0) g_phase_clock[i] = clock64(); \
     } while (0)
-#define RB_TSTART(k)                                                           \
-    do {                                                                       \
-        if (threadIdx.x == 0) atomicMin(&g_timeline[2 * (k)], rb_globaltimer()); \
+// globaltimer stamp of phase i by thread 0 when `cond` holds (one CTA)
+#define RB_GCLOCK(i, cond)                                           \
+    do {                                                             \
+        if (threadIdx.x == 0 && (cond)) g_phase_clock[i] = (long long)rb_globaltimer(); \
+    } while (0)
+#define RB_TSTART(k)                                             \
+    do {                                                         \
+        if (threadIdx.x == 0) {                                  \
+            const unsigned long long _t = rb_globaltimer();      \
+            atomicMin(&g_timeline[2 * (k)], _t);                 \
+            atomicMax(&g_timeline[32 + (k)], _t); /* latest CTA start */ \
+        }                                                        \
     } while (0)
 #define RB_TEND(k)                                                                 \
     do {                                                                           \
@@ -161,6 +282,9 @@ __device__ __forceinline__ unsigned long long rb_globaltimer() {
     } while (0)
 #define RB_TSTART(k) \
     do {             \
+    } while (0)
+#define RB_GCLOCK(i, cond) \
+    do {                   \
     } while (0)
 #define RB_TEND(k) \
     do {           \

@@ -1014,7 +1014,7 @@ extern "C" __attribute__((visibility("default"))) int rb_debug_timeline_loss(uns
         RB_CUDA(cudaMemcpyFromSymbol(out, g_timeline, 64 * sizeof(unsigned long long)));
         if (reset) {
             unsigned long long init[64];
-            for (int i = 0; i < 64; ++i) init[i] = (i & 1) ? 0ULL : ~0ULL;
+            for (int i = 0; i < 64; ++i) init[i] = (i < 32 && !(i & 1)) ? ~0ULL : 0ULL;
             RB_CUDA(cudaMemcpyToSymbol(g_timeline, init, sizeof init));
         }
 #else

@@ -6,6 +6,7 @@
 // rng.uniform01() with buffer.sample(), as the reference's own tests do).
 // Migration is a 2.5 KB copy on the owning stream.
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <string>
 
@@ -99,22 +100,37 @@ rb_rng::~rb_rng() {
 void rb_rng::to_host() {
     if (where == 0) return;
     if (done) RB_CUDA(cudaEventSynchronize(done));
-    RB_CUDA(cudaMemcpy(&host, dev, sizeof(MtState), cudaMemcpyDeviceToHost));
+    MtRingHead h;
+    static_assert(offsetof(MtRing, blk) == sizeof(MtRingHead), "MtRing header layout");
+    RB_CUDA(cudaMemcpy(&h, dev, sizeof h, cudaMemcpyDeviceToHost));
+    RB_CUDA(cudaMemcpy(host.mt, dev->blk[h.q_state % MT_KR], sizeof host.mt,
+                       cudaMemcpyDeviceToHost));
+    host.idx = h.idx;
+    host.draws = h.draws;
     where = 0;
 }
 
-MtState* rb_rng::to_device(cudaStream_t s) {
+MtRing* rb_rng::to_device(cudaStream_t s) {
     require_device();
     if (!dev) {
-        RB_CUDA(cudaMalloc(&dev, sizeof(MtState)));
+        RB_CUDA(cudaMalloc(&dev, sizeof(MtRing)));
         RB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
         RB_CUDA(cudaGetDevice(&device));
     }
     if (where == 0) {
-        // the previous device user must be finished before we overwrite
+        // the previous device user must be finished before we overwrite;
+        // the host state becomes ring block 0
         RB_CUDA(cudaEventSynchronize(done));
-        RB_CUDA(cudaMemcpyAsync(dev, &host, sizeof(MtState), cudaMemcpyHostToDevice, s));
-        // host copy must stay alive until the copy completes
+        MtRingHead h;
+        h.q_state = 0;
+        h.q_hi = 0;
+        h.idx = host.idx;
+        h.pad = 0;
+        h.draws = host.draws;
+        h.gen_q = 0;
+        RB_CUDA(cudaMemcpyAsync(dev, &h, sizeof h, cudaMemcpyHostToDevice, s));
+        RB_CUDA(cudaMemcpyAsync(dev->blk[0], host.mt, sizeof host.mt, cudaMemcpyHostToDevice, s));
+        // host copies must stay alive until the copies complete
         RB_CUDA(cudaStreamSynchronize(s));
     } else if (s != last_stream) {
         // order after the previous user of the device state on another stream
@@ -137,16 +153,19 @@ uint64_t rb_rng::next() {
 }
 
 // ---- device bulk generator (parity aid for the sampler's stream) -------
-__global__ void __launch_bounds__(320) k_mt_fill(MtState* st, uint64_t n, uint64_t* out) {
+__global__ void __launch_bounds__(320) k_mt_fill(MtRing* r, uint64_t n, uint64_t* out) {
     __shared__ uint64_t mt[MT_N];
-    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = st->mt[i];
-    uint32_t idx = st->idx;
-    __syncthreads();
+    const long long q0 = r->q_state;
+    uint32_t idx = r->idx;
+    const uint64_t draws = r->draws;
+    ring_load_block(r, q0, mt);
     uint64_t pos = 0;
+    long long tw = 0;
     while (pos < n) {
         if (idx >= MT_N) {
             mt_twist_block(mt);
             idx = 0;
+            ++tw;
         }
         const uint64_t avail = (uint64_t)(MT_N - idx);
         const uint64_t take = avail < n - pos ? avail : n - pos;
@@ -154,12 +173,7 @@ __global__ void __launch_bounds__(320) k_mt_fill(MtState* st, uint64_t n, uint64
         idx += (uint32_t)take;
         pos += take;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) st->mt[i] = mt[i];
-    if (threadIdx.x == 0) {
-        st->idx = idx;
-        st->draws += n;
-    }
+    ring_store_state(r, mt, q0, tw, idx, draws + n);
 }
 
 extern "C" {
@@ -260,7 +274,7 @@ int rb_rng_fill_u64(rb_rng* r, uint64_t n, uint64_t* out) {
     return guard([&] {
         require_device();
         cudaStream_t s = 0;  // legacy default stream
-        MtState* st = r->to_device(s);
+        MtRing* st = r->to_device(s);
         uint64_t* d = out;
         const bool dev_out = is_device_ptr(out);
         if (!dev_out) RB_CUDA(cudaMallocAsync((void**)&d, n * sizeof(uint64_t) + 8, s));

@@ -13,15 +13,15 @@ struct rb_rng {
 
     // Make the host copy authoritative (synchronises the owning stream).
     void to_host();
-    // Make the device copy authoritative for kernels on stream `s`; the
+    // Make the device ring authoritative for kernels on stream `s`; the
     // caller enqueues its kernels and then calls used_on(s).
-    rb::MtState* to_device(cudaStream_t s);
+    rb::MtRing* to_device(cudaStream_t s);
     void used_on(cudaStream_t s);  // record completion of the last device use
     uint64_t next();               // host draw (rng.cpp:38)
 
     uint64_t seed;
     rb::MtState host{};
-    rb::MtState* dev = nullptr;
+    rb::MtRing* dev = nullptr;
     int where = 0;                   // 0 = host authoritative, 1 = device authoritative
     cudaEvent_t done = nullptr;      // completes after the last kernel that used `dev`
     cudaStream_t last_stream = nullptr;  // stream of that kernel (compared, never used)
