@@ -2386,6 +2386,7 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         b->pdl_tail = false;
         b->B = nsel;
         b->last_loss = -1;
+        b->acc_norm_explicit = false;
         if (nsel > 0 && (out_records || out_events)) {
             rb_record* dr = out_records;
             rb_use_event* de = out_events;

@@ -755,13 +755,16 @@ int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double e
         p.hi = 1.0 + eps_high;
         p.lo_f = (float)p.lo;
         p.hi_f = (float)p.hi;
-        if (norm_tokens > 0 || b->last_loss != -1) {
-            // explicit normaliser, or a second loss on the same batch
+        if (norm_tokens > 0 || b->acc_norm_explicit) {
+            // explicit normaliser (or back to the batch's token count after
+            // one); the accumulator fields are rewritten by the last CTA, so a
+            // repeated loss on the same batch needs no reset
             k_acc_set_total<<<1, 1, 0, b->stream>>>(b->acc, norm_tokens > 0 ? nullptr : b->sel_total + 1,
                                                     norm_tokens);
             RB_CUDA(cudaGetLastError());
         }
         b->last_loss = 0;
+        b->acc_norm_explicit = norm_tokens > 0;
         // Device stats are written by the kernel's last CTA (no extra launch).
         const bool dev_stats = stats && is_device_ptr(stats);
         rb_loss_stats* kst = dev_stats ? stats : (stats ? (rb_loss_stats*)b->scratch(64) : nullptr);
@@ -797,11 +800,12 @@ int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double
         const long long lo = (long long)std::min(b->sb * per, b->B);
         const long long hi = (long long)std::min(b->se * per, b->B);
         const double inv_b = 1.0 / (double)(norm_batch > 0 ? norm_batch : (int64_t)b->B);
-        if (b->last_loss != -1) {
+        if (b->acc_norm_explicit) {
             k_acc_set_total<<<1, 1, 0, b->stream>>>(b->acc, b->sel_total + 1, 0);
             RB_CUDA(cudaGetLastError());
         }
         b->last_loss = 1;
+        b->acc_norm_explicit = false;
         const bool dev_stats = stats && is_device_ptr(stats);
         rb_loss_stats* kst = dev_stats ? stats : (stats ? (rb_loss_stats*)b->scratch(64) : nullptr);
         if (hi > lo) {
