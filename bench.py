@@ -430,15 +430,17 @@ def run_e2e(args, buf, wl, rng, cfg):
     synth.logp_now(SEED, 99, ids, offd, lpn_d, buf.stream())
     torch.cuda.synchronize()
     lpn_h.copy_(lpn_d.cpu())
-    # re-insert the same inbound batches needs fresh ids: shift them
+    # re-insert the same inbound batches needs fresh ids: shift them (pinned,
+    # prepared outside the timed region like every other host input)
     shift = 10**12
-    h2d = d2h = 0
-    done_tokens = 0
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for hb, n, tot in host:
-        hb2 = dict(hb)
-        hb2["rollout_id"] = hb["rollout_id"] + shift
+    plan = []
+    for r in range(2):  # r = 0: warm-up pass (staging buffers are allocated once)
+        for j, (hb, n, tot) in enumerate(host):
+            hb2 = dict(hb)
+            hb2["rollout_id"] = (hb["rollout_id"] + shift * (1 + r * len(host) + j)).pin_memory()
+            plan.append((r, hb2, n))
+
+    def e2e_step(hb2, n):
         if n:
             buf.insert(**hb2)
         buf.sample_device(B, rng)
@@ -446,16 +448,29 @@ def run_e2e(args, buf, wl, rng, cfg):
         st = buf.loss_grpo(lpn_h, dl_h, EPS_LOW, EPS_HIGH) if cfg["loss"] == "grpo" else \
             buf.loss_asymre(lpn_h, dl_h, DELTA_V)
         _ = st.objective  # device->host read of the step's result
-        tot_s = int(off_h[B])  # this step's sampled tokens (offsets already on the host)
+        return int(off_h[B])  # this step's sampled tokens (offsets already on the host)
+
+    for r, hb2, n in plan:
+        if r == 0:
+            e2e_step(hb2, n)
+    h2d = d2h = 0
+    done_tokens = 0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for r, hb2, n in plan:
+        if r == 0:
+            continue
+        tot_s = e2e_step(hb2, n)
         done_tokens += tot_s
-        h2d += sum(v.numel() * v.element_size() for v in hb.values()) + tot_s * 4
+        h2d += sum(v.numel() * v.element_size() for v in hb2.values()) + tot_s * 4
         d2h += tot_s * 4 * 2 + (B + 1) * 8 + 40
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / len(host)
     return {"value": done_tokens / len(host) / dt, "unit": "tokens/s", "ms_per_step": dt * 1e3,
             "h2d_bytes_per_step": h2d // len(host), "d2h_bytes_per_step": d2h // len(host),
             "steps": len(host), "path": "rb_insert/rb_sample/rb_gather/rb_loss_* with pinned host "
-                                        "buffers (copies inside the timed region)"}
+                                        "buffers (copies inside the timed region; the loss "
+                                        "pipelines its upload/download in chunks)"}
 
 
 # ---------------------------------------------------------------- CPU arm

@@ -1698,6 +1698,12 @@ rb_buffer::~rb_buffer() {
         if (p) cudaFree(p);
     if (stage_host) cudaFreeHost(stage_host);
     if (stage_event) cudaEventDestroy(stage_event);
+    if (cs_in) cudaStreamSynchronize(cs_in);
+    if (cs_out) cudaStreamSynchronize(cs_out);
+    for (auto e : ev_io)
+        if (e) cudaEventDestroy(e);
+    if (cs_in) cudaStreamDestroy(cs_in);
+    if (cs_out) cudaStreamDestroy(cs_out);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -1738,6 +1744,22 @@ void* rb_buffer::dev_stage(size_t bytes, int slot) {
         RB_CUDA(cudaMalloc(&stage_dev[slot], stage_dev_cap[slot]));
     }
     return stage_dev[slot];
+}
+void rb_buffer::host_stage_issued_on(cudaStream_t s) {
+    if (!stage_event) RB_CUDA(cudaEventCreateWithFlags(&stage_event, cudaEventDisableTiming));
+    RB_CUDA(cudaEventRecord(stage_event, s));
+}
+void rb_buffer::ensure_copy_streams() {
+    if (cs_in) return;
+    RB_CUDA(cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking));
+    RB_CUDA(cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking));
+    for (auto& e : ev_io) RB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+void rb_buffer::grow_loss_partials(size_t bytes) {
+    sync();
+    if (loss_partials) cudaFree(loss_partials);
+    RB_CUDA(cudaMalloc(&loss_partials, bytes));
+    loss_partials_bytes = bytes;
 }
 void rb_buffer::host_stage_issued() {
     if (!stage_event) RB_CUDA(cudaEventCreateWithFlags(&stage_event, cudaEventDisableTiming));
@@ -1966,6 +1988,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         b->n_units_ins = dalloc<int>(1);
         b->n_units_sel = dalloc<int>(1);
         b->loss_partials = dalloc<char>((size_t)b->unit_grid * 32);
+        b->loss_partials_bytes = (size_t)b->unit_grid * 32;
         b->h_pushes.assign(T, 0);
     } catch (...) {
         delete b;

@@ -117,7 +117,11 @@ struct rb_buffer {
     int* n_units_sel = nullptr;
     size_t units_sel_cap = 0;
     int32_t* sel_len = nullptr;
-    void* loss_partials = nullptr;      // [unit_grid] per-CTA loss partials
+    void* loss_partials = nullptr;      // per-CTA loss partials (32 B each)
+    size_t loss_partials_bytes = 0;
+    // host-buffer loss pipeline: upload / download streams and chunk events
+    cudaStream_t cs_in = nullptr, cs_out = nullptr;
+    cudaEvent_t ev_io[1 + 2 * 8] = {};
 
     // current batch (selection)
     size_t sel_cap = 0, B = 0;
@@ -138,6 +142,9 @@ struct rb_buffer {
     void* scratch(size_t bytes);          // device misc scratch
     void* host_stage(size_t bytes);       // pinned host scratch (waits for its last reader)
     void host_stage_issued();             // record that the stream reads stage_host
+    void host_stage_issued_on(cudaStream_t s);  // ... that stream `s` reads it
+    void ensure_copy_streams();
+    void grow_loss_partials(size_t bytes);
     void* dev_stage(size_t bytes, int slot);  // device staging areas (one per use)
     void ensure_insert(size_t n);
     void ensure_select(size_t n);

@@ -186,7 +186,7 @@ struct Partial {
 // -1/total -> -1/included correction itself when a token was excluded.
 __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
                             rb_loss_stats* stats, int asym, double inv_b, float* dlogp,
-                            const long long* n_local, int local_fix) {
+                            const long long* n_local, int local_fix, int part_base, int nparts) {
     __shared__ double s_obj[32];
     __shared__ long long s_inc[32], s_exc[32];
     __shared__ int s_last;
@@ -207,16 +207,16 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
             q.inc += s_inc[w];
             q.exc += s_exc[w];
         }
-        parts[blockIdx.x] = q;
+        parts[part_base + blockIdx.x] = q;
         __threadfence();
-        s_last = atomicAdd(&acc->done_blocks, 1ULL) == gridDim.x - 1;
+        s_last = atomicAdd(&acc->done_blocks, 1ULL) == (unsigned long long)nparts - 1;
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
     double o = 0.0;
     long long inc = 0, exc = 0;
-    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
         o += __ldcg(&parts[i].obj);
         inc += __ldcg(&parts[i].inc);
         exc += __ldcg(&parts[i].exc);
@@ -291,7 +291,7 @@ template <int U>
 __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
     BufView v, const Unit* units, const int* maxq_p, int nloc, const float* lpn_packed,
     float* dlogp, GrpoParams prm, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats,
-    const long long* n_local, int local_fix) {
+    const long long* n_local, int local_fix, int part_base, int nparts) {
     constexpr int QU = UNIT_THREADS * U;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const float scale = -1.f / (float)acc->total_tokens;
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
     }
     part.inc += inc_fast;
     RB_TEND(5);
-    loss_commit(part, parts, acc, stats, 0, 0.0, dlogp, n_local, local_fix);
+    loss_commit(part, parts, acc, stats, 0, 0.0, dlogp, n_local, local_fix, part_base, nparts);
 }
 constexpr int LOSS_U = 4;
 
@@ -395,7 +395,7 @@ template <int U>
 __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
     BufView v, const Unit* units, const int* maxq_p, int nloc, const float* lpn_packed,
     float* dlogp, double delta_v, double inv_b, DevLossAcc* acc, Partial* parts,
-    rb_loss_stats* stats);
+    rb_loss_stats* stats, int part_base, int nparts);
 
 int loss_grid(int sms) {
     int a = 0, b = 0;
@@ -450,7 +450,7 @@ template <int U>
 __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
     BufView v, const Unit* units, const int* maxq_p, int nloc, const float* lpn_packed,
     float* dlogp, double delta_v, double inv_b, DevLossAcc* acc, Partial* parts,
-    rb_loss_stats* stats) {
+    rb_loss_stats* stats, int part_base, int nparts) {
     constexpr int QU = UNIT_THREADS * U;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int ups = (*maxq_p + QU - 1) / QU;
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
         }
         part.obj += coef * (double)fs;
     }
-    loss_commit(part, parts, acc, stats, 1, inv_b, dlogp, nullptr, 0);
+    loss_commit(part, parts, acc, stats, 1, inv_b, dlogp, nullptr, 0, part_base, nparts);
 }
 
 __global__ void __launch_bounds__(256) k_loss_asymre_packed(const float* lpn, const double* reward,
@@ -692,42 +692,124 @@ void copy_stats(rb_buffer* b, rb_loss_stats* stats, int asym, double inv_b) {
 
 // Host logp_now / dlogp for the buffer losses: staged through the buffer's
 // ST_LOSS_IN / ST_LOSS_OUT device areas (H2D before, D2H after).
-struct HostIO {
-    rb_buffer* b;
-    const float* in;
-    float* out;
-    bool host_in, host_out;
-    long long total = 0;
-    HostIO(rb_buffer* b_, const float* lpn, float* dl) : b(b_), in(lpn), out(dl) {
-        host_in = lpn && !is_device_ptr(lpn);
-        host_out = dl && !is_device_ptr(dl);
-        if (!host_in && !host_out) return;
-        RB_CUDA(cudaMemcpyAsync(&total, b->sel_total, 8, cudaMemcpyDeviceToHost, b->stream));
-        b->sync();
-        const size_t bytes = (((size_t)total + 3) & ~size_t(3)) * 4 + 16;
-        if (host_in) {
-            float* d = (float*)b->dev_stage(bytes, rb_buffer::ST_LOSS_IN);
-            if (is_pinned_ptr(lpn)) {
-                RB_CUDA(cudaMemcpyAsync(d, lpn, total * 4, cudaMemcpyHostToDevice, b->stream));
-            } else {
-                void* hs = b->host_stage(total * 4 + 16);
-                std::memcpy(hs, lpn, total * 4);
-                RB_CUDA(cudaMemcpyAsync(d, hs, total * 4, cudaMemcpyHostToDevice, b->stream));
-                b->host_stage_issued();
-            }
-            in = d;
-        }
-        if (host_out) out = (float*)b->dev_stage(bytes, rb_buffer::ST_LOSS_OUT);
-    }
-    void finish(float* user_out) {
-        if (!host_out) return;
-        RB_CUDA(cudaMemcpyAsync(user_out, out, total * 4, cudaMemcpyDeviceToHost, b->stream));
-        b->sync();
-    }
-};
-
 unsigned grid_for(long long n) {
     return (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8));
+}
+
+// One loss evaluation over the current batch.
+struct LossCall {
+    int kind = 0;  // 0 GRPO, 1 AsymRE
+    GrpoParams p{};
+    double delta_v = 0.0, inv_b = 0.0;
+};
+
+// Launch the loss kernel over owned selections [s0, s1) (part slots
+// [part_base, part_base + grid) of `nparts` folded by the last CTA overall).
+void launch_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl, long long s0,
+                 long long s1, int part_base, int nparts, rb_loss_stats* kst, int local_fix) {
+    const Unit* u = b->units_sel + s0;
+    if (c.kind == 0)
+        k_loss_grpo_buf<LOSS_U><<<b->grid_loss, UNIT_THREADS, 0, b->stream>>>(
+            b->v, u, b->n_units_sel, (int)(s1 - s0), lpn, dl, c.p, b->acc,
+            (Partial*)b->loss_partials, kst, b->sel_total, local_fix, part_base, nparts);
+    else
+        k_loss_asymre_buf<LOSS_U><<<b->grid_loss, UNIT_THREADS, 0, b->stream>>>(
+            b->v, u, b->n_units_sel, (int)(s1 - s0), lpn, dl, c.delta_v, c.inv_b, b->acc,
+            (Partial*)b->loss_partials, kst, part_base, nparts);
+    RB_CUDA(cudaGetLastError());
+}
+
+constexpr int LOSS_CHUNKS = 8;  // host-buffer pipeline depth
+
+// Device buffers: one launch.  Host buffers: the batch is cut into up to
+// LOSS_CHUNKS selection ranges; per chunk the logp_now upload (copy stream
+// 1), the loss kernel (buffer stream) and the dlogp download (copy stream 2)
+// are chained by events, so upload and download overlap (PCIe is full
+// duplex).  A token excluded anywhere (non-finite ratio, rare) rescales and
+// re-downloads dlogp after the pipeline.
+void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
+              rb_loss_stats* stats) {
+    const size_t per = b->T ? b->B / b->T : 0;
+    const long long lo = (long long)std::min(b->sb * per, b->B);
+    const long long hi = (long long)std::min(b->se * per, b->B);
+    const long long nloc = hi - lo;
+    const bool dev_stats = stats && is_device_ptr(stats);
+    rb_loss_stats* kst = dev_stats ? stats : (stats ? (rb_loss_stats*)b->scratch(64) : nullptr);
+    const bool host_in = lpn && !is_device_ptr(lpn);
+    const bool host_out = dl && !is_device_ptr(dl);
+    const bool single = b->sb == 0 && b->se == b->T;
+    if (nloc <= 0) {
+        if (kst) k_stats_out<<<1, 1, 0, b->stream>>>(b->acc, kst, c.kind, c.inv_b);
+    } else if (!host_in && !host_out) {
+        launch_loss(b, c, lpn, dl, 0, nloc, 0, b->grid_loss, kst, single && c.kind == 0);
+    } else {
+        // packed offsets of the owned selections (and the total) on the host
+        std::vector<long long> off(nloc + 1);
+        RB_CUDA(cudaMemcpyAsync(off.data(), b->sel_off, (nloc + 1) * 8, cudaMemcpyDeviceToHost,
+                                b->stream));
+        b->sync();
+        const long long total = off[nloc];
+        const size_t bytes = (((size_t)total + 3) & ~size_t(3)) * 4 + 16;
+        float* din = host_in ? (float*)b->dev_stage(bytes, rb_buffer::ST_LOSS_IN) : (float*)lpn;
+        float* dout = host_out ? (float*)b->dev_stage(bytes, rb_buffer::ST_LOSS_OUT) : dl;
+        const bool pin_in = !host_in || is_pinned_ptr(lpn);
+        const bool pin_out = !host_out || is_pinned_ptr(dl);
+        b->ensure_copy_streams();
+        // chunk boundaries: ~equal token counts, at selection boundaries
+        std::vector<long long> cut{0};
+        for (int k = 1; k < LOSS_CHUNKS; ++k) {
+            const long long want = total * k / LOSS_CHUNKS;
+            const long long s = std::lower_bound(off.begin(), off.end(), want) - off.begin();
+            if (s > cut.back() && s < nloc) cut.push_back(s);
+        }
+        cut.push_back(nloc);
+        const int nch = (int)cut.size() - 1;
+        const int nparts = nch * b->grid_loss;
+        if ((size_t)nparts * 32 > b->loss_partials_bytes) b->grow_loss_partials((size_t)nparts * 32);
+        const float* hin = lpn;
+        if (host_in && !pin_in) {  // pageable: one staged copy (no overlap)
+            void* hs = b->host_stage(total * 4 + 16);
+            std::memcpy(hs, lpn, total * 4);
+            hin = (const float*)hs;
+        }
+        RB_CUDA(cudaEventRecord(b->ev_io[0], b->stream));
+        RB_CUDA(cudaStreamWaitEvent(b->cs_in, b->ev_io[0], 0));
+        RB_CUDA(cudaStreamWaitEvent(b->cs_out, b->ev_io[0], 0));
+        for (int k = 0; k < nch; ++k) {
+            const long long t0 = off[cut[k]], t1 = off[cut[k + 1]];
+            if (host_in) {
+                RB_CUDA(cudaMemcpyAsync(din + t0, hin + t0, (t1 - t0) * 4, cudaMemcpyHostToDevice,
+                                        b->cs_in));
+                RB_CUDA(cudaEventRecord(b->ev_io[1 + 2 * k], b->cs_in));
+                RB_CUDA(cudaStreamWaitEvent(b->stream, b->ev_io[1 + 2 * k], 0));
+            }
+            launch_loss(b, c, din, dout, cut[k], cut[k + 1], k * b->grid_loss, nparts, kst, 0);
+            if (host_out && pin_out) {
+                RB_CUDA(cudaEventRecord(b->ev_io[2 + 2 * k], b->stream));
+                RB_CUDA(cudaStreamWaitEvent(b->cs_out, b->ev_io[2 + 2 * k], 0));
+                RB_CUDA(cudaMemcpyAsync(dl + t0, dout + t0, (t1 - t0) * 4, cudaMemcpyDeviceToHost,
+                                        b->cs_out));
+            }
+        }
+        if (host_in && !pin_in) b->host_stage_issued_on(b->cs_in);
+        RB_CUDA(cudaStreamSynchronize(b->cs_out));
+        RB_CUDA(cudaStreamSynchronize(b->stream));
+        DevLossAcc acc;
+        RB_CUDA(cudaMemcpy(&acc, b->acc, sizeof acc, cudaMemcpyDeviceToHost));
+        const bool fix = c.kind == 0 && acc.need_fixup && single;
+        if (fix) {  // -1/total -> -1/included (rare: a non-finite ratio)
+            k_dlogp_rescale<<<grid_for(total), 256, 0, b->stream>>>(dout, total, nullptr, b->acc);
+            RB_CUDA(cudaGetLastError());
+        }
+        if (host_out && (!pin_out || fix)) {
+            RB_CUDA(cudaMemcpyAsync(dl, dout, total * 4, cudaMemcpyDeviceToHost, b->stream));
+            b->sync();
+        }
+    }
+    if (stats && !dev_stats) {
+        RB_CUDA(cudaMemcpyAsync(stats, kst, sizeof *stats, cudaMemcpyDeviceToHost, b->stream));
+        b->sync();
+    }
 }
 
 }  // namespace rb
@@ -742,19 +824,13 @@ int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double e
         if (eps_low < 0.0 || eps_high < 0.0) invalid("loss spec: clip bounds must be >= 0");
         if (!std::isfinite(eps_low) || !std::isfinite(eps_high))
             invalid("loss spec: parameters must be finite");
-        HostIO io(b, logp_now, out_dlogp);
-        logp_now = io.in;
-        float* const user_dlogp = out_dlogp;
-        out_dlogp = io.out;
-        const size_t per = b->T ? b->B / b->T : 0;
-        const long long lo = (long long)std::min(b->sb * per, b->B);
-        const long long hi = (long long)std::min(b->se * per, b->B);
         if (b->B == 0) invalid("loss gradient needs a non-empty batch");
-        GrpoParams p;
-        p.lo = 1.0 - eps_low;
-        p.hi = 1.0 + eps_high;
-        p.lo_f = (float)p.lo;
-        p.hi_f = (float)p.hi;
+        LossCall c;
+        c.kind = 0;
+        c.p.lo = 1.0 - eps_low;
+        c.p.hi = 1.0 + eps_high;
+        c.p.lo_f = (float)c.p.lo;
+        c.p.hi_f = (float)c.p.hi;
         if (norm_tokens > 0 || b->acc_norm_explicit) {
             // explicit normaliser (or back to the batch's token count after
             // one); the accumulator fields are rewritten by the last CTA, so a
@@ -765,25 +841,7 @@ int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double e
         }
         b->last_loss = 0;
         b->acc_norm_explicit = norm_tokens > 0;
-        // Device stats are written by the kernel's last CTA (no extra launch).
-        const bool dev_stats = stats && is_device_ptr(stats);
-        rb_loss_stats* kst = dev_stats ? stats : (stats ? (rb_loss_stats*)b->scratch(64) : nullptr);
-        if (hi > lo) {
-            // Single-process buffers rescale in the last CTA when a token was
-            // excluded; multi-rank buffers defer to rb_loss_finalize.
-            const int local_fix = b->sb == 0 && b->se == b->T;
-            k_loss_grpo_buf<LOSS_U><<<b->grid_loss, UNIT_THREADS, 0, b->stream>>>(
-                b->v, b->units_sel, b->n_units_sel, (int)(hi - lo), logp_now, out_dlogp, p, b->acc,
-                (Partial*)b->loss_partials, kst, b->sel_total, local_fix);
-            RB_CUDA(cudaGetLastError());
-        } else if (kst) {
-            k_stats_out<<<1, 1, 0, b->stream>>>(b->acc, kst, 0, 0.0);
-        }
-        io.finish(user_dlogp);
-        if (stats && !dev_stats) {
-            RB_CUDA(cudaMemcpyAsync(stats, kst, sizeof *stats, cudaMemcpyDeviceToHost, b->stream));
-            b->sync();
-        }
+        run_loss(b, c, logp_now, out_dlogp, stats);
     });
 }
 
@@ -792,36 +850,17 @@ int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double
     return guard([&] {
         if (!std::isfinite(delta_v)) invalid("loss spec: parameters must be finite");
         if (b->B == 0) invalid("loss gradient needs a non-empty batch");
-        HostIO io(b, logp_now, out_dlogp);
-        logp_now = io.in;
-        float* const user_dlogp = out_dlogp;
-        out_dlogp = io.out;
-        const size_t per = b->T ? b->B / b->T : 0;
-        const long long lo = (long long)std::min(b->sb * per, b->B);
-        const long long hi = (long long)std::min(b->se * per, b->B);
-        const double inv_b = 1.0 / (double)(norm_batch > 0 ? norm_batch : (int64_t)b->B);
+        LossCall c;
+        c.kind = 1;
+        c.delta_v = delta_v;
+        c.inv_b = 1.0 / (double)(norm_batch > 0 ? norm_batch : (int64_t)b->B);
         if (b->acc_norm_explicit) {
             k_acc_set_total<<<1, 1, 0, b->stream>>>(b->acc, b->sel_total + 1, 0);
             RB_CUDA(cudaGetLastError());
         }
         b->last_loss = 1;
         b->acc_norm_explicit = false;
-        const bool dev_stats = stats && is_device_ptr(stats);
-        rb_loss_stats* kst = dev_stats ? stats : (stats ? (rb_loss_stats*)b->scratch(64) : nullptr);
-        if (hi > lo) {
-            k_loss_asymre_buf<LOSS_U><<<b->grid_loss, UNIT_THREADS, 0, b->stream>>>(
-                b->v, b->units_sel, b->n_units_sel, (int)(hi - lo), logp_now, out_dlogp, delta_v,
-                inv_b, b->acc,
-                (Partial*)b->loss_partials, kst);
-            RB_CUDA(cudaGetLastError());
-        } else if (kst) {
-            k_stats_out<<<1, 1, 0, b->stream>>>(b->acc, kst, 1, inv_b);
-        }
-        io.finish(user_dlogp);
-        if (stats && !dev_stats) {
-            RB_CUDA(cudaMemcpyAsync(stats, kst, sizeof *stats, cudaMemcpyDeviceToHost, b->stream));
-            b->sync();
-        }
+        run_loss(b, c, logp_now, out_dlogp, stats);
     });
 }
 
