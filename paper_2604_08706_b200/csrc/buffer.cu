@@ -39,9 +39,10 @@ constexpr uint64_t NONE_ID = UINT64_MAX;
 __device__ __forceinline__ int fifo_head(long long P, int C) {
     return P >= C ? (int)(P % C) : 0;
 }
-// Arrival head of shard s (FIFO: implicit ring; positive bias: explicit).
+// Arrival head of shard s (FIFO: implicit ring; positive bias: v.order is
+// materialised densely after every insert, head 0).
 __device__ __forceinline__ int shard_head(const BufView& v, int s) {
-    return v.retention == RB_POSITIVE_BIAS ? v.head[s] : fifo_head(v.pushes[s], v.C);
+    return v.retention == RB_POSITIVE_BIAS ? 0 : fifo_head(v.pushes[s], v.C);
 }
 // Local slot of arrival rank i (0 = oldest) given the shard's head.
 __device__ __forceinline__ int arrival_slot_h(const BufView& v, int s, long long i, int head) {
@@ -191,88 +192,276 @@ __device__ void h_rebuild(const BufView& v) {
     __syncthreads();
 }
 
-// ---- positive-bias push (replay_buffer.cpp:98-133) on one shard --------
-// The shard is an arrival-ordered ring `order` (head, size).  Victim = the
-// first !is_correct record among arrival positions [0, size+1-fresh_slots)
-// (position C is the record being pushed), else position 0; erasing shifts
-// the older prefix one place towards the tail so arrival order is kept.
-// WARP = true: executed by a full warp; false: by one thread.
-template <bool WARP>
-__device__ void posbias_push(const BufView& v, const InsertIn& in, int s, long long j,
-                             int& size, int& head) {
-    const int lane = WARP ? (threadIdx.x & 31) : 0;
-    const int C = v.C;
-    int32_t* ord = v.order + (size_t)s * C;
-    if (size < C) {
-        const int x = size;
-        const size_t g = (size_t)s * C + x;
-        if (lane == 0) {
-            ord[(head + size) % C] = x;
-            write_meta(v, g, in, j);
-            in.tslot[j] = (int32_t)g;
-            v.owner[g] = (int32_t)j;
-            in.evid[j] = NONE_ID;
-        }
-        ++size;
-        if (WARP) __syncwarp();
-        return;
+// ---- positive-bias retention (replay_buffer.cpp:98-133) as two queues ------
+// The reference keeps a shard in arrival order and, once full, evicts the
+// first !is_correct record among the oldest cs+1 arrivals (cs =
+// correct_slots; that window is the reserve plus the record that just aged
+// out of the newest fs = fresh_slots), else the oldest record, erasing it
+// from the middle of the vector.  Equivalently: a FIFO F of the newest fs
+// records and the reserve split into two arrival-ordered queues, W (wrong)
+// and Q (correct).  A push appends x to F and moves F's oldest to W or Q;
+// the victim is W's head if W is non-empty, else Q's head.  (fs == 0: x
+// itself enters the reserve and may be the victim.)  Every push is O(1).
+// Arrival order for sampling is materialised per shard after each insert:
+// merge(W, Q) by arrival sequence number, then F (v.order, dense).
+// Queue entries: local slot | is_correct << 31.
+constexpr uint32_t PB_XMARK = 0x7fffffffu;  // "the record being pushed" (fs == 0)
+
+__device__ __forceinline__ int32_t* pb_ring(const BufView& v, int r, int s) {
+    return v.pbq + ((size_t)r * v.T + s) * (size_t)(v.C + 1);
+}
+struct GQ {  // a ring in global memory (sequential use by one thread)
+    uint32_t* ring;
+    int rc, h, n;
+    __device__ int len() const { return n; }
+    __device__ uint32_t pop() {
+        const uint32_t e = ring[h];
+        h = h + 1 == rc ? 0 : h + 1;
+        --n;
+        return e;
     }
-    const int outside = C + 1 - v.fs;  // = correct_slots + 1
-    const bool new_correct = in_correct(in, j);
-    int vpos = -1;
-    for (int base = 0; base < outside && vpos < 0; base += (WARP ? 32 : 1)) {
-        if (WARP) {
-            const int p = base + lane;
-            bool wrong = false;
-            if (p < outside) {
-                if (p < C)
-                    wrong = !v.correct[(size_t)s * C + ord[(head + p) % C]];
-                else
-                    wrong = !new_correct;
+    __device__ void push(uint32_t e) {
+        int p = h + n;
+        if (p >= rc) p -= rc;
+        ring[p] = e;
+        ++n;
+    }
+    __device__ void patch_tail(uint32_t e) {
+        int p = h + n - 1;
+        if (p >= rc) p -= rc;
+        ring[p] = e;
+    }
+};
+struct VQ {  // a ring's loaded prefix + the entries appended in this chunk (shared memory)
+    const uint32_t* pre;
+    uint32_t* app;
+    int exist, pre_h, app_n, app_h;
+    __device__ int len() const { return (exist - pre_h) + (app_n - app_h); }
+    __device__ uint32_t pop() { return pre_h < exist ? pre[pre_h++] : app[app_h++]; }
+    __device__ void push(uint32_t e) { app[app_n++] = e; }
+    __device__ void patch_tail(uint32_t e) { app[app_n - 1] = e; }
+};
+// One push; returns x's local slot, or -1 when x itself is evicted.  *vict =
+// local slot of the evicted record (-1: no eviction; -2: x itself).
+template <class Qu>
+__device__ __forceinline__ int pb_push_logic(int C, int fs, Qu& F, Qu& W, Qu& Q, int& size,
+                                             bool xc, int* vict) {
+    const uint32_t cb = xc ? 0x80000000u : 0u;
+    if (size < C) {  // filling: no eviction
+        const int gx = size++;
+        if (fs > 0) {
+            F.push((uint32_t)gx | cb);
+            if (F.len() > fs) {
+                const uint32_t y = F.pop();
+                (y >> 31 ? Q : W).push(y);
             }
-            const unsigned m = __ballot_sync(0xffffffffu, wrong);
-            if (m) vpos = base + __ffs(m) - 1;
         } else {
-            const bool wrong = base < C ? !v.correct[(size_t)s * C + ord[(head + base) % C]]
-                                        : !new_correct;
-            if (wrong) vpos = base;
+            (xc ? Q : W).push((uint32_t)gx | cb);
         }
+        *vict = -1;
+        return gx;
     }
-    if (vpos < 0) vpos = 0;
-    if (vpos == C) {  // fresh_slots == 0 and the new record is the victim
-        if (lane == 0) {
-            in.evid[j] = in.id[j];
-            if (in.evrec) in.evrec[j] = in_record(in, j);
-            in.tslot[j] = -1;
+    if (fs > 0) {
+        const uint32_t y = F.pop();
+        (y >> 31 ? Q : W).push(y);
+    } else {
+        (xc ? Q : W).push(PB_XMARK | cb);
+    }
+    const uint32_t ve = W.len() ? W.pop() : Q.pop();
+    const uint32_t vs = ve & 0x7fffffffu;
+    if (vs == PB_XMARK) {
+        *vict = -2;
+        return -1;
+    }
+    const int gx = (int)vs;
+    if (fs > 0) F.push((uint32_t)gx | cb);
+    else (xc ? Q : W).patch_tail((uint32_t)gx | cb);
+    *vict = gx;
+    return gx;
+}
+
+// Block-wide: v.order of shard s = merge(W, Q) by arrival sequence, then F.
+__device__ void pb_materialize(const BufView& v, int s) {
+    const PbState st = v.pbs[s];
+    const int C = v.C, RC = C + 1;
+    const uint32_t* F = (const uint32_t*)pb_ring(v, 0, s);
+    const uint32_t* W = (const uint32_t*)pb_ring(v, 1, s);
+    const uint32_t* Q = (const uint32_t*)pb_ring(v, 2, s);
+    const long long* seq = v.seq + (size_t)s * C;
+    int32_t* ord = v.order + (size_t)s * C;
+    auto at = [&](const uint32_t* ring, int h, int k) {
+        int p = h + k;
+        if (p >= RC) p -= RC;
+        return (int)(ring[p] & 0x7fffffffu);
+    };
+    // rank of an element of one queue in the merge = its index + the number
+    // of the other queue's elements that arrived earlier (binary search)
+    const int nw = st.n[1], nq = st.n[2], nf = st.n[0];
+    for (int k = threadIdx.x; k < nw + nq; k += blockDim.x) {
+        const bool inw = k < nw;
+        const int a = inw ? k : k - nw;
+        const int slot = inw ? at(W, st.h[1], a) : at(Q, st.h[2], a);
+        const long long sq = seq[slot];
+        const uint32_t* O = inw ? Q : W;
+        const int oh = inw ? st.h[2] : st.h[1], on = inw ? nq : nw;
+        int lo = 0, hi = on;  // first index with seq > sq
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (seq[at(O, oh, mid)] < sq) lo = mid + 1;
+            else hi = mid;
         }
-        if (WARP) __syncwarp();
-        return;
+        ord[a + lo] = slot;
     }
-    const int xv = ord[(head + vpos) % C];
-    const size_t gv = (size_t)s * C + xv;
-    if (lane == 0) {
-        in.evid[j] = v.id[gv];
-        if (in.evrec) in.evrec[j] = slot_record(v, gv);
+    for (int k = threadIdx.x; k < nf; k += blockDim.x) ord[nw + nq + k] = at(F, st.h[0], k);
+}
+
+// Positive-bias insert for ids promised new and increasing: one CTA per
+// shard runs the O(1)-per-push queue simulation on shared memory (thread
+// 0), in chunks of PB_CH pushes whose queue prefixes the whole CTA loads
+// first; then, in parallel, evicted ids, the survivors' metadata, payload
+// descriptors, the ring write-back and the materialised arrival order.
+// k_insert_route ran before it (lengths, group advantages, validation) and
+// set ctl->pb_go when this kernel is to apply the batch.
+constexpr int PB_THREADS = 256;
+constexpr int PB_CH = 512;
+__global__ void __launch_bounds__(PB_THREADS) k_posbias_batch(BufView v, InsertIn in,
+                                                              unsigned long long cur0) {
+    extern __shared__ uint32_t pb_sm[];
+    __shared__ int s_size;
+    __shared__ PbState s_st;
+    __shared__ int s_maxq, s_a0[3], s_a1[3];
+    const int s = blockIdx.x, tid = threadIdx.x;
+    const int T = v.T, C = v.C, RC = C + 1, fs = v.fs;
+    if (!v.ctl->pb_go) return;
+    const int n = (int)in.n;
+    const int j0 = (int)(((long long)s - (long long)(cur0 % (unsigned long long)T)) % T + T) % T;
+    const int ns = n > j0 ? (n - 1 - j0) / T + 1 : 0;
+    uint32_t* Fpre = pb_sm;
+    uint32_t* Wpre = Fpre + PB_CH;
+    uint32_t* Qpre = Wpre + PB_CH;
+    uint32_t* Fapp = Qpre + PB_CH;
+    uint32_t* Wapp = Fapp + PB_CH;
+    uint32_t* Qapp = Wapp + PB_CH;
+    int* gxs = (int*)(Qapp + PB_CH);  // per push of this chunk: x's slot
+    int* vic = gxs + PB_CH;           // evicted local slot / -1 / -2
+    int* vocc = vic + PB_CH;          // occupant of the victim slot: batch index or -1
+    int* occ = vocc + PB_CH;          // [C] batch index now holding each slot (-1: pre-batch)
+    const long long P0 = v.pushes[s];
+    for (int x = tid; x < C; x += PB_THREADS) occ[x] = -1;
+    if (tid == 0) {
+        s_st = v.pbs[s];
+        s_size = (int)(P0 < C ? P0 : C);
+        s_maxq = 0;
     }
-    if (WARP) __syncwarp();
-    // erase position vpos: shift [0, vpos) one place towards the tail
-    for (int hi = vpos; hi > 0; hi -= (WARP ? 32 : 1)) {
-        const int lo = WARP ? max(0, hi - 32) : hi - 1;
-        const int p = lo + lane;
-        int val = 0;
-        if (p < hi) val = ord[(head + p) % C];
-        if (WARP) __syncwarp();
-        if (p < hi) ord[(head + p + 1) % C] = val;
-        if (WARP) __syncwarp();
+    __syncthreads();
+    uint32_t* Fr = (uint32_t*)pb_ring(v, 0, s);
+    uint32_t* Wr = (uint32_t*)pb_ring(v, 1, s);
+    uint32_t* Qr = (uint32_t*)pb_ring(v, 2, s);
+    for (int c0 = 0; c0 < ns; c0 += PB_CH) {
+        const int ch = ns - c0 < PB_CH ? ns - c0 : PB_CH;
+        const PbState st = s_st;
+        // queue prefixes (a chunk pops at most `ch` entries from each)
+        for (int k = tid; k < ch; k += PB_THREADS) {
+            int p;
+            if (k < st.n[0]) { p = st.h[0] + k; if (p >= RC) p -= RC; Fpre[k] = (uint32_t)Fr[p]; }
+            if (k < st.n[1]) { p = st.h[1] + k; if (p >= RC) p -= RC; Wpre[k] = (uint32_t)Wr[p]; }
+            if (k < st.n[2]) { p = st.h[2] + k; if (p >= RC) p -= RC; Qpre[k] = (uint32_t)Qr[p]; }
+            const int j = j0 + (c0 + k) * T;
+            gxs[k] = in_correct(in, j) ? 1 : 0;  // x's correctness (overwritten below)
+        }
+        __syncthreads();
+        if (tid == 0) {
+            VQ F{Fpre, Fapp, st.n[0], 0, 0, 0}, W{Wpre, Wapp, st.n[1], 0, 0, 0},
+                Q{Qpre, Qapp, st.n[2], 0, 0, 0};
+            int size = s_size;
+            for (int k = 0; k < ch; ++k) {
+                const int j = j0 + (c0 + k) * T;
+                int vs;
+                const int gx = pb_push_logic(C, fs, F, W, Q, size, gxs[k] != 0, &vs);
+                vocc[k] = vs >= 0 ? occ[vs] : -1;
+                if (gx >= 0) occ[gx] = j;
+                gxs[k] = gx;
+                vic[k] = vs;
+            }
+            s_size = size;
+            // ring write-back bookkeeping: new heads / counts (entries below)
+            VQ* qs[3] = {&F, &W, &Q};
+            for (int r = 0; r < 3; ++r) {
+                const int pops = qs[r]->pre_h + qs[r]->app_h;
+                s_st.h[r] = (st.h[r] + pops) % RC;
+                s_st.n[r] = st.n[r] + qs[r]->app_n - pops;
+                // appended entries still queued: app[app_h..app_n) at old tail + index
+                s_a0[r] = qs[r]->app_h;
+                s_a1[r] = qs[r]->app_n;
+            }
+        }
+        __syncthreads();
+        // write back the live appended entries at the rings' tails
+        {
+            const uint32_t* apps[3] = {Fapp, Wapp, Qapp};
+            uint32_t* rings[3] = {Fr, Wr, Qr};
+            for (int r = 0; r < 3; ++r) {
+                const int a0 = s_a0[r], a1 = s_a1[r];
+                for (int k = a0 + tid; k < a1; k += PB_THREADS) {
+                    int p = st.h[r] + st.n[r] + k;
+                    p %= RC;
+                    rings[r][p] = apps[r][k];
+                }
+            }
+        }
+        // per push: evicted id (the victim's occupant before this push), seq
+        for (int k = tid; k < ch; k += PB_THREADS) {
+            const int j = j0 + (c0 + k) * T;
+            const int vs = vic[k], gx = gxs[k];
+            uint64_t ev = NONE_ID;
+            if (vs == -2) {
+                ev = in.id[j];
+                if (in.evrec) in.evrec[j] = in_record(in, j);
+            } else if (vs >= 0) {
+                const int o = vocc[k];
+                ev = o >= 0 ? in.id[o] : v.id[(size_t)s * C + vs];
+                if (in.evrec) in.evrec[j] = o >= 0 ? in_record(in, o) : slot_record(v, (size_t)s * C + vs);
+            }
+            in.evid[j] = ev;
+            in.tslot[j] = gx >= 0 ? (int32_t)((size_t)s * C + gx) : -1;
+            if (gx >= 0) v.seq[(size_t)s * C + gx] = P0 + c0 + k;
+        }
+        __syncthreads();
     }
-    head = (head + 1) % C;
-    if (lane == 0) {
-        ord[(head + C - 1) % C] = xv;  // the new record takes the victim's slot, at the tail
-        write_meta(v, gv, in, j);
-        in.tslot[j] = (int32_t)gv;
-        v.owner[gv] = (int32_t)j;
+    // survivors (final occupant of their slot): metadata + payload descriptors
+    int maxq = 0;
+    for (int r = tid; r < ns; r += PB_THREADS) {
+        const int j = j0 + r * T;
+        const int32_t g = in.tslot[j];
+        const bool surv = g >= 0 && occ[g - s * C] == j;
+        in.surv[j] = surv;
+        Unit d;
+        d.row = -1;
+        d.len = in.len[j];
+        d.k0 = 0;
+        d.g = j;
+        d.off = in.toff ? in.toff[j] : 0;
+        d.adv = 0.0;
+        if (surv) {
+            write_meta(v, (size_t)g, in, j);
+            if (s >= v.sb && s < v.se && d.len > 0 && v.stride > 0) {
+                d.row = (s - v.sb) * C + (g - s * C);
+                const int q = (d.len + 3) >> 2;
+                maxq = q > maxq ? q : maxq;
+            }
+        }
+        in.units[j] = d;
     }
-    if (WARP) __syncwarp();
+    maxq = __reduce_max_sync(0xffffffffu, maxq);
+    if ((tid & 31) == 0 && maxq) atomicMax(&s_maxq, maxq);
+    if (tid == 0) {
+        PbState st = s_st;
+        v.pbs[s] = st;
+        v.pushes[s] = P0 + ns;
+    }
+    __syncthreads();
+    if (tid == 0 && s_maxq) atomicMax(in.n_units, s_maxq);
+    pb_materialize(v, s);
 }
 
 // ---------------------------------------------------------------- insert
@@ -282,6 +471,7 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const long long n = in.n;
     DevCtl* ctl = v.ctl;
+    if (tid == 0) ctl->pb_go = 0;  // set again below when k_posbias_batch is to apply
     if (ctl->err_code != 0) {  // sticky error: buffer frozen until rb_check
         if (tid == 0) *in.n_units = 0;
         for (long long j = tid; j < n; j += nt) {
@@ -418,21 +608,13 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
         }
         if (tid == 0) ctl->cursor = (cur0 + n) % T;
     } else if (!risk) {
-        // 3b. positive bias: one warp per shard, pushes in arrival order.
-        const int w = tid >> 5, nw = nt >> 5;
-        for (int s = w; s < T; s += nw) {
-            long long P = v.pushes[s];
-            int size = (int)(P < C ? P : C), head = v.head[s];
-            const long long j0 = (((long long)s - (long long)(cur0 % T)) % T + T) % T;
-            long long ns = 0;
-            for (long long j = j0; j < n; j += T, ++ns) posbias_push<true>(v, in, s, j, size, head);
-            if ((tid & 31) == 0) {
-                v.pushes[s] = P + ns;
-                v.head[s] = head;
-            }
+        // 3b. positive bias, ids promised new: k_posbias_batch (launched next)
+        //     applies the batch, writes the descriptors and the unit bound.
+        if (tid == 0) {
+            ctl->pb_go = 1;
+            ctl->cursor = (cur0 + n) % T;
+            *in.n_units = 0;
         }
-        __syncthreads();
-        if (tid == 0) ctl->cursor = (cur0 + n) % T;
     } else {
         // 3c. exact sequential path (possible duplicates): replay_buffer.cpp:83-96
         //     push by push against the present-id set.
@@ -467,10 +649,39 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
                     v.pushes[s] = P + 1;
                 } else {
                     const long long P = v.pushes[s];
-                    int size = (int)(P < C ? P : C), head = v.head[s];
-                    posbias_push<false>(v, in, s, j, size, head);
+                    PbState st = v.pbs[s];
+                    const int RC = C + 1;
+                    GQ F{(uint32_t*)pb_ring(v, 0, s), RC, st.h[0], st.n[0]};
+                    GQ W{(uint32_t*)pb_ring(v, 1, s), RC, st.h[1], st.n[1]};
+                    GQ Q{(uint32_t*)pb_ring(v, 2, s), RC, st.h[2], st.n[2]};
+                    int size = (int)(P < C ? P : C), vs;
+                    const int gx = pb_push_logic(C, v.fs, F, W, Q, size, in_correct(in, j), &vs);
+                    uint64_t ev = NONE_ID;
+                    if (vs == -2) {
+                        ev = in.id[j];
+                        if (in.evrec) in.evrec[j] = in_record(in, j);
+                    } else if (vs >= 0) {
+                        const size_t gv = (size_t)s * C + vs;
+                        ev = v.id[gv];
+                        if (in.evrec) in.evrec[j] = slot_record(v, gv);
+                    }
+                    in.tslot[j] = -1;
+                    if (gx >= 0) {
+                        const size_t g = (size_t)s * C + gx;
+                        write_meta(v, g, in, j);
+                        in.tslot[j] = (int32_t)g;
+                        v.owner[g] = (int32_t)j;
+                        v.seq[g] = P;
+                    }
+                    in.evid[j] = ev;
+                    st.h[0] = F.h;
+                    st.n[0] = F.n;
+                    st.h[1] = W.h;
+                    st.n[1] = W.n;
+                    st.h[2] = Q.h;
+                    st.n[2] = Q.n;
+                    v.pbs[s] = st;
                     v.pushes[s] = P + 1;
-                    v.head[s] = head;
                 }
                 if (in.evid[j] != NONE_ID) h_erase(v, in.evid[j]);
             }
@@ -482,8 +693,11 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
             }
         }
         __syncthreads();
+        if (v.retention == RB_POSITIVE_BIAS)
+            for (int s = 0; s < T; ++s) pb_materialize(v, s);
     }
-    if (risk || v.retention != RB_PLAIN_FIFO) {
+    const bool pb_fast = !risk && v.retention == RB_POSITIVE_BIAS;  // k_posbias_batch applies
+    if (risk || (v.retention != RB_PLAIN_FIFO && !pb_fast)) {
         for (long long j = tid; j < n; j += nt) {
             const int32_t g = in.tslot[j];
             in.surv[j] = g >= 0 && v.owner[g] == (int32_t)j;
@@ -494,7 +708,7 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
     // 4. payload descriptors: one per record (row = -1 unless it survived the
     //    batch in a shard held here) and the max units per record; the
     //    payload kernel strides over n * ups virtual units.
-    {
+    if (!pb_fast) {
         int ups = 0;
         if (in.toff && v.stride > 0) {
             for (long long j = tid; j < n; j += nt) {
@@ -1677,8 +1891,30 @@ __global__ void k_load_shard(BufView v, int s, long long n, const rb_record* rec
         v.gmean[g] = 0.0;
         v.use[g] = r.use_count;
         v.len[g] = 0;
-        if (v.retention == RB_POSITIVE_BIAS) v.order[g] = (int32_t)i;
+        if (v.retention == RB_POSITIVE_BIAS) {
+            v.order[g] = (int32_t)i;
+            v.seq[g] = i;
+        }
     }
+}
+// Positive-bias queues of a loaded shard (records at slots 0..n-1 in arrival
+// order): F = the newest min(n, fs), the rest split into W / Q.
+__global__ void k_load_posbias(BufView v, int s, int n, const rb_record* recs) {
+    if (threadIdx.x != 0) return;
+    const int C = v.C, RC = C + 1;
+    const int nf = n < v.fs ? n : v.fs;
+    uint32_t* F = (uint32_t*)pb_ring(v, 0, s);
+    uint32_t* W = (uint32_t*)pb_ring(v, 1, s);
+    uint32_t* Q = (uint32_t*)pb_ring(v, 2, s);
+    PbState st{};
+    for (int i = 0; i < n; ++i) {
+        const uint32_t e = (uint32_t)i | (recs[i].is_correct ? 0x80000000u : 0u);
+        if (i >= n - nf) F[st.n[0]++] = e;
+        else if (recs[i].is_correct) Q[st.n[2]++] = e;
+        else W[st.n[1]++] = e;
+    }
+    (void)RC;
+    v.pbs[s] = st;
 }
 
 }  // namespace rb
@@ -1688,7 +1924,7 @@ rb_buffer::~rb_buffer() {
     if (device >= 0) cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     void* ptrs[] = {v.id, v.prompt, v.group, v.cstep, v.pver, v.reward, v.blp, v.adv, v.gmean,
-                    v.correct, v.use, v.len, v.order, v.head, v.pushes, v.owner, v.tok, v.lpo,
+                    v.correct, v.use, v.len, v.order, v.head, v.pushes, v.owner, v.tok, v.lpo, v.pbq, v.pbs, v.seq,
                     v.hkeys, v.hstate, v.ctl, s_tslot, s_surv, s_evid, s_evrec, s_adv, s_gmean,
                     s_len, s_toff, sel_slot, sel_shard, sel_index, sel_off, sel_total,
                     acc, misc, n_units_ins, n_units_sel, loss_partials, route_ctl, map_ctl, pay_sync};
@@ -1919,6 +2155,17 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         v.len = dalloc<int32_t>(N);
         v.order = dalloc<int32_t>(N);
         v.head = dalloc<int32_t>(T);
+        if (retention == RB_POSITIVE_BIAS) {
+            v.pbq = dalloc<int32_t>(3 * T * (b->C + 1));
+            v.pbs = dalloc<PbState>(T);
+            v.seq = dalloc<long long>(N);
+            const size_t smem = (9 * (size_t)PB_CH + b->C) * sizeof(uint32_t);
+            if (smem > 48 * 1024) {
+                if (smem > 200 * 1024) invalid("rb_create: positive-bias shard capacity too large");
+                RB_CUDA(cudaFuncSetAttribute(k_posbias_batch,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            }
+        }
         v.pushes = dalloc<long long>(T);
         v.owner = dalloc<int32_t>(N);
         const size_t rows = (se - sb) * b->C * (size_t)b->stride;
@@ -2036,6 +2283,12 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         k_route_fifo<<<grid, RT_THREADS, 0, b->stream>>>(b->v, in, b->route_ctl, b->pay_sync);
     } else {
         k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
+        if (b->retention == RB_POSITIVE_BIAS) {
+            RB_CUDA(cudaGetLastError());
+            const size_t smem = (9 * (size_t)PB_CH + b->C) * sizeof(uint32_t);
+            k_posbias_batch<<<(unsigned)b->T, PB_THREADS, smem, b->stream>>>(
+                b->v, in, (unsigned long long)b->h_cursor);
+        }
     }
     RB_CUDA(cudaGetLastError());
     if (payload && closed) {
@@ -2812,6 +3065,10 @@ extern "C" int rb_load(const char* text, int32_t max_tokens, int device, rb_buff
                 k_load_shard<<<(unsigned)((n + 255) / 256), 256, 0, b->stream>>>(b->v, (int)s,
                                                                                 (long long)n, d);
                 RB_CUDA(cudaGetLastError());
+                if (b->retention == RB_POSITIVE_BIAS) {
+                    k_load_posbias<<<1, 32, 0, b->stream>>>(b->v, (int)s, (int)n, d);
+                    RB_CUDA(cudaGetLastError());
+                }
                 b->sync();
             }
             RB_CUDA(cudaMemcpy(b->v.pushes, b->h_pushes.data(), T * sizeof(long long),

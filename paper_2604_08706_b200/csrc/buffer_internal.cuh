@@ -29,7 +29,13 @@ struct DevCtl {
     int err_code;  // sticky asynchronous error (RB_EINVAL)
     int has_any;   // max_id valid
     int hash_stale;
-    int pad[3];
+    int pb_go;  // k_posbias_batch applies the current insert
+    int pad[2];
+};
+
+// Positive-bias queue state of one shard: head and count of F, W, Q.
+struct PbState {
+    int h[3], n[3];
 };
 
 // Everything a kernel needs, passed by value.
@@ -47,6 +53,9 @@ struct BufView {
     int32_t* head;       // [T]
     long long* pushes;   // [T]
     int32_t* owner;      // [N] last writer in the current insert
+    int32_t* pbq;        // positive bias: rings F, W, Q per shard [3][T][C+1] (slot | correct<<31)
+    struct PbState* pbs; // positive bias: ring heads / counts per shard [T]
+    long long* seq;      // positive bias: arrival sequence number per slot [N]
     int32_t* tok;        // owned payload
     float* lpo;
     uint64_t* hkeys;     // present-id set (exact path)
