@@ -1138,7 +1138,8 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
         if (ok[r] && k0 + r >= a.lo && k0 + r < a.hi) own += (unsigned long long)L[r];
     }
     RB_GCLOCK(47 + 8 * (t & 1), t < 2);
-    const bool cta_rej = DRAW && __syncthreads_or(rej);
+    // v.dbg_replay (tests): every CTA takes the exact-replay path
+    const bool cta_rej = DRAW && __syncthreads_or(rej || v.dbg_replay);
     RB_GCLOCK(43 + 8 * (t & 1), t < 2);
     long long cta_own;
     const long long pre = block_exclusive_scan((long long)own, &cta_own);
@@ -2227,6 +2228,8 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
             RB_CUDA(cudaMemcpy(b->pay_sync + 1, &one, sizeof one, cudaMemcpyHostToDevice));
         }
         b->pdl = std::getenv("RB_NO_PDL") == nullptr;
+        // test hook: force the sampler's exact draw replay (must not change results)
+        v.dbg_replay = std::getenv("RB_DEBUG_FORCE_DRAW_REPLAY") != nullptr;
         b->map_ctl = dalloc<GridCtl>(1);
         {
             const int none = INT_MAX;
@@ -2502,6 +2505,7 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
         if (out_evicted_ids) {
             RB_CUDA(cudaMemcpyAsync(out_evicted_ids, b->s_evid, n * 8, cudaMemcpyDefault,
                                     b->stream));
+            b->pdl_tail = false;  // the copy, not the payload kernel, is the stream's tail
         }
         // host mirrors: assume fully applied, corrected below when synchronous
         for (size_t j = 0; j < n; ++j) b->h_pushes[(b->h_cursor + j) % b->T]++;

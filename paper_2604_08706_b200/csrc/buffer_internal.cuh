@@ -43,6 +43,7 @@ struct BufView {
     int T, C, stride, retention;
     int sb, se;  // owned shards [sb, se)
     int cs, fs;  // positive bias: correct_slots, fresh_slots (replay_buffer.cpp:110-112)
+    int dbg_replay;  // test hook: the sampler replays its draws exactly
     uint64_t *id, *prompt, *group;
     int64_t *cstep, *pver;
     double *reward, *blp, *adv, *gmean;

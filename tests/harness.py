@@ -39,7 +39,8 @@ class StepConfig:
     delta_v: float = -0.1
     prompts: int = 16
     device_inputs: bool = True   # torch CUDA tensors (hot path) vs numpy host arrays
-    assume_unique: bool = False  # RB_INSERT_ASSUME_UNIQUE (cooperative FIFO insert kernel)
+    assume_unique: bool = False  # RB_INSERT_ASSUME_UNIQUE (closed-form FIFO insert kernels)
+    overlap: bool = False        # no host sync between insert and sample (evicted ids to the device)
 
     @property
     def per_step(self):
@@ -94,10 +95,13 @@ def _to(x, dev):
     return torch.from_numpy(np.ascontiguousarray(x)).to(dev) if dev else x
 
 
-def insert_groups(buf, rec, toff, tok, lpo, group, dev, assume_unique=False):
+def insert_groups(buf, rec, toff, tok, lpo, group, dev, assume_unique=False, overlap=False):
     n = rec.shape[0]
     goff = np.arange(0, n + 1, group, dtype=np.int64)
-    ev = np.zeros(n, np.uint64)
+    # overlap: no evicted-id output (its copy would serialise the stream) and
+    # nothing waits for the insert; evictions are checked through the samples
+    # and the final shard contents instead
+    ev = None if overlap else np.zeros(n, np.uint64)
     buf.insert(rollout_id=_to(rec["rollout_id"].copy(), dev), prompt_id=_to(rec["prompt_id"].copy(), dev),
                group_id=_to(rec["group_id"].copy(), dev),
                creation_step=_to(rec["creation_step"].copy(), dev),
@@ -106,7 +110,7 @@ def insert_groups(buf, rec, toff, tok, lpo, group, dev, assume_unique=False):
                behavior_logprob=_to(rec["behavior_logprob"].copy(), dev),
                group_offsets=_to(goff, dev), tok_offsets=_to(toff, dev), tokens=_to(tok, dev),
                logp_old=_to(lpo, dev), evicted=ev, assume_unique=assume_unique)
-    if assume_unique:
+    if assume_unique and not overlap:
         buf.synchronize()  # the evicted-id copy is asynchronous
         buf.check()
     return ev
@@ -134,7 +138,14 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
         for i, r in enumerate(rec):
             lengths[int(r["rollout_id"])] = int(length[i])
             gmeans[int(r["rollout_id"])] = gmean[i]
-        ev = insert_groups(gbuf, rec, toff, tok, lpo, cfg.group, dev, cfg.assume_unique)
+        ev = insert_groups(gbuf, rec, toff, tok, lpo, cfg.group, dev, cfg.assume_unique,
+                           cfg.overlap)
+        if cfg.overlap:
+            for r in rec:
+                e = obuf.push(r)
+                counts["pushes"] += 1
+                counts["evictions"] += e is not None
+            return
         for i, r in enumerate(rec):
             e = obuf.push(r)
             want = np.uint64(np.iinfo(np.uint64).max) if e is None else e["rollout_id"]
@@ -154,6 +165,8 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
         if ng:
             push_groups(ng, step)
         grec, gsh, gix = gbuf.sample(cfg.batch, grng, with_index=True)
+        if cfg.overlap:
+            gbuf.check()
         orec, osh, oix = obuf.sample(cfg.batch, orng)
         assert np.array_equal(gsh, osh) and np.array_equal(gix, oix), f"sample index mismatch step {step}"
         assert same_records(grec, orec), f"sampled records mismatch step {step}"
@@ -201,4 +214,6 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
         np.testing.assert_allclose(got, d_want, rtol=1e-5, atol=1e-12,
                                    err_msg=f"dlogp mismatch step {step}")
         assert abs(st.objective - obj) <= 1e-5 * max(1.0, abs(obj)), (st.objective, obj)
+    for s in range(cfg.shards):  # final state, arrival order per shard
+        assert same_records(gbuf.shard_contents(s), obuf.shard_contents(s)), f"shard {s} contents"
     return counts

@@ -354,6 +354,21 @@ STEP_CASES = {
     "posbias_in_batch": dict(capacity=32, shards=2, batch=16, group=8, lmax=12, ragged=True,
                              seed=9, workers=16, trainers=1, mu=1.0, retention="positive_bias",
                              delta=0.75),
+    # insert -> sample with no host sync: the sampler overlaps the running
+    # route / payload kernels and maps the new records from the insert's plan
+    "c4_unique_overlap": dict(capacity=256, shards=4, batch=64, group=16, lmax=96, ragged=True,
+                              seed=21, assume_unique=True, overlap=True),
+    "c3_unique_overlap_big": dict(capacity=512, shards=1, batch=2048, group=16, lmax=33,
+                                  ragged=True, seed=22, assume_unique=True, overlap=True),
+    # more shards than the samplers cache per-shard state for (64 / 128)
+    "many_shards_unique": dict(capacity=130 * 3, shards=130, batch=260, group=10, lmax=9,
+                               ragged=True, seed=23, assume_unique=True, overlap=True),
+    "many_shards": dict(capacity=70 * 2, shards=70, batch=140, group=10, lmax=9, ragged=True,
+                        seed=24),
+    "posbias_delta_one": dict(capacity=48, shards=3, batch=24, group=8, lmax=10, ragged=True,
+                              seed=25, retention="positive_bias", delta=1.0, assume_unique=True),
+    "posbias_delta_zero": dict(capacity=48, shards=3, batch=24, group=8, lmax=10, ragged=True,
+                               seed=26, retention="positive_bias", delta=0.0),
 }
 
 
@@ -363,3 +378,15 @@ def test_replay_step_parity(rb, oracle, case):
 
     counts = run_step_parity(StepConfig(**STEP_CASES[case]), steps=12, ora=oracle)
     assert counts["samples"] > 0 and counts["tokens"] > 0
+
+
+@pytest.mark.parametrize("case", ["c4_unique_overlap", "c3_unique_overlap_big", "many_shards"])
+def test_forced_draw_replay_matches(rb, oracle, case, monkeypatch):
+    """The sampler's exact-replay path (taken for real only after a below()
+    rejection, probability ~n/2^64) forced on every CTA gives the same
+    stream, selections and losses (env read at buffer creation)."""
+    from tests.harness import StepConfig, run_step_parity
+
+    monkeypatch.setenv("RB_DEBUG_FORCE_DRAW_REPLAY", "1")
+    counts = run_step_parity(StepConfig(**STEP_CASES[case]), steps=6, ora=oracle)
+    assert counts["samples"] > 0
