@@ -883,6 +883,193 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload_fifo(BufView v,
 constexpr int PAYLOAD_U = 4;
 
 
+// ---- payload insert over the bulk-copy engine (TMA) ------------------------
+// The closed-form FIFO copy as a cp.async.bulk pipeline: one CTA per SM, a
+// ring of TP_S shared-memory stages, loads TP_LAG items ahead of the stores.
+// An item is up to TP_CH tokens of one surviving trajectory (tokens and
+// logp_old).  A 16-byte aligned source goes global -> smem -> slot row
+// untouched; otherwise the aligned-down source quads are loaded and the
+// CTA's threads shift them in place in shared memory before the bulk store (rows are
+// 16-byte aligned and padded to a multiple of 4 tokens, so a store may round
+// its length up to whole quads).  Descriptors come from the closed form
+// (fifo_unit); stores start once the route kernel has published a valid
+// verdict.  Little register and thread use, so the route / sampler CTAs that
+// overlap the copy find room on every SM.
+constexpr int TP_THREADS = 128;
+constexpr int TP_CH = 1024;           // tokens per item
+constexpr int TP_S = 16;              // stages
+constexpr int TP_LAG = 12;            // loads issued ahead of stores
+constexpr int TP_RAW = TP_CH + 4;     // raw words per array (aligned-down source + spill)
+constexpr int TP_STAGE = 2 * TP_RAW;  // words per stage
+constexpr int TP_LIST = 128;          // items listed per round
+constexpr size_t TP_SMEM = (size_t)TP_S * TP_STAGE * 4 + TP_S * 8 + TP_LIST * 16;
+static_assert((TP_RAW * 4) % 16 == 0 && (TP_CH * 4) % 16 == 0, "bulk-copy alignment");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct TpItem {
+    int32_t row, n;  // slot row; tokens in this item
+    int64_t src;     // packed element index of the item's first token
+};
+
+__global__ void __launch_bounds__(TP_THREADS) k_insert_payload_tma(BufView v, FifoPlan p,
+                                                                  const int64_t* toff, int n,
+                                                                  const int32_t* tokens,
+                                                                  const float* logp_old,
+                                                                  int* sync) {
+    extern __shared__ __align__(128) uint32_t tp_sm[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tp_sm + TP_S * TP_STAGE);
+    TpItem* list = reinterpret_cast<TpItem*>(bar + TP_S);
+    __shared__ int s_flag;
+    RB_TSTART(1);
+    pdl_trigger();  // the sampler may launch (it waits for the route itself)
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < TP_S; ++s) mbar_init(&bar[s]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_flag = 0;
+    }
+    __syncthreads();
+    const int ipr = (int)((v.stride + TP_CH - 1) / TP_CH);  // items per record (bound)
+    const long long nitems = (long long)n * ipr;
+    long long issued = 0, stored = 0;  // this CTA's pipeline counters (all threads track)
+    // Rounds of up to TP_LIST items of this CTA (item u = blockIdx.x + k * gridDim.x).
+    for (long long u0 = blockIdx.x; u0 < nitems; u0 += (long long)TP_LIST * gridDim.x) {
+        // list this round's valid items
+        const long long u = u0 + (long long)tid * gridDim.x;
+        TpItem it{-1, 0, 0};
+        if (tid < TP_LIST && u < nitems) {
+            const int j = (int)(u / ipr), c = (int)(u - (long long)j * ipr);
+            const Unit d = fifo_unit(v, p, toff, n, j);
+            const int rest = d.len - c * TP_CH;
+            if (d.row >= 0 && rest > 0) {
+                it.row = d.row;
+                it.n = rest < TP_CH ? rest : TP_CH;
+                it.src = d.off + (long long)c * TP_CH;
+                it.n |= c << 20;             // chunk index rides in the high bits
+            }
+        }
+        const bool ok = it.row >= 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        __shared__ int s_wc[TP_THREADS / 32];
+        if ((tid & 31) == 0) s_wc[tid >> 5] = __popc(bal);
+        __syncthreads();
+        int base = 0, m = 0;
+        for (int w = 0; w < TP_THREADS / 32; ++w) {
+            if (w < (tid >> 5)) base += s_wc[w];
+            m += s_wc[w];
+        }
+        if (ok) list[base + __popc(bal & ((1u << (tid & 31)) - 1))] = it;
+        __syncthreads();
+        // pipeline over the listed items (global item counter keeps stages / parities)
+        for (int i = 0; i < m + TP_LAG; ++i) {
+            if (i < m && tid == 0) {  // load
+                const long long g = issued++;
+                const int st = (int)(g % TP_S);
+                if (g >= TP_S) bulk_wait_read<TP_S - 1 - TP_LAG>();  // store of item g-S has read its stage
+                const TpItem x = list[i];
+                const int cnt = x.n & 0xfffff;
+                const int a = (int)(x.src & 3);
+                const int words = (a + cnt + 3) & ~3;
+                uint32_t* stg = tp_sm + (size_t)st * TP_STAGE;
+                const uint32_t bytes = (uint32_t)words * 4;
+                mbar_expect_tx(&bar[st], bytes * ((tokens ? 1 : 0) + (logp_old ? 1 : 0)));
+                if (tokens) bulk_g2s(stg, tokens + (x.src - a), bytes, &bar[st]);
+                if (logp_old) bulk_g2s(stg + TP_RAW, logp_old + (x.src - a), bytes, &bar[st]);
+            }
+            if (i >= TP_LAG && i - TP_LAG < m) {  // store item k
+                const int k = i - TP_LAG;
+                const long long g = stored++;
+                const int st = (int)(g % TP_S);
+                mbar_wait(&bar[st], (uint32_t)((g / TP_S) & 1));
+                if (s_flag == 0) {  // first store of this CTA: the route's verdict
+                    if (tid == 0) {
+                        int f;
+                        while ((f = ld_acquire_i32(&sync[0])) == 0) __nanosleep(64);
+                        s_flag = f;
+                    }
+                    __syncthreads();
+                }
+                const TpItem x = list[k];
+                const int cnt = x.n & 0xfffff, c = x.n >> 20;
+                const int a = (int)(x.src & 3);
+                const int words = (cnt + 3) & ~3;
+                uint32_t* stg = tp_sm + (size_t)st * TP_STAGE;
+                const uint32_t* out_t = stg;
+                const uint32_t* out_l = stg + TP_RAW;
+                if (a != 0) {  // shift the aligned-down source quads down by `a`, in place
+                    constexpr int PER = TP_CH / TP_THREADS;
+                    uint32_t rt[PER], rl[PER];
+#pragma unroll
+                    for (int q = 0; q < PER; ++q) {
+                        const int e = tid + q * TP_THREADS;
+                        rt[q] = stg[a + e];
+                        rl[q] = stg[TP_RAW + a + e];
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (int q = 0; q < PER; ++q) {
+                        const int e = tid + q * TP_THREADS;
+                        stg[e] = rt[q];
+                        stg[TP_RAW + e] = rl[q];
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncthreads();
+                }
+                if (tid == 0 && s_flag == 1) {
+                    const size_t row = (size_t)x.row * v.stride + (size_t)c * TP_CH;
+                    if (tokens) bulk_s2g(v.tok + row, out_t, (uint32_t)words * 4);
+                    if (logp_old) bulk_s2g(v.lpo + row, out_l, (uint32_t)words * 4);
+                    bulk_commit();
+                } else if (tid == 0) {
+                    bulk_commit();  // keeps the group count in step (empty group)
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) bulk_wait_all();
+    RB_TEND(1);
+    // completion of this copy implies completion of the route before it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- sample
 struct SampleArgs {
     int nsh;            // shards to draw from (error semantics: [0, nsh))
@@ -2191,6 +2378,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
             const void* ks[] = {(const void*)k_route_fifo, (const void*)k_sample_fused,
                                 (const void*)k_sample_map, (const void*)k_insert_payload<PAYLOAD_U>,
                                 (const void*)k_insert_payload_fifo<PAYLOAD_U>,
+                                (const void*)k_insert_payload_tma,
                                 (const void*)k_insert_route};
             for (const void* k : ks)
                 RB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -2228,6 +2416,10 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
             RB_CUDA(cudaMemcpy(b->pay_sync + 1, &one, sizeof one, cudaMemcpyHostToDevice));
         }
         b->pdl = std::getenv("RB_NO_PDL") == nullptr;
+        b->tma_payload = std::getenv("RB_PAYLOAD_LSU") == nullptr;
+        b->sms = sms;
+        RB_CUDA(cudaFuncSetAttribute(k_insert_payload_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)TP_SMEM));
         // test hook: force the sampler's exact draw replay (must not change results)
         v.dbg_replay = std::getenv("RB_DEBUG_FORCE_DRAW_REPLAY") != nullptr;
         b->map_ctl = dalloc<GridCtl>(1);
@@ -2312,8 +2504,17 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        RB_CUDA(cudaLaunchKernelEx(&cfg, k_insert_payload_fifo<PAYLOAD_U>, b->v, p, bt.tok_offsets,
-                                   (int)bt.n, bt.tokens, bt.logp_old, b->pay_sync));
+        if (b->tma_payload) {
+            cfg.gridDim = dim3(b->sms);
+            cfg.blockDim = dim3(TP_THREADS);
+            cfg.dynamicSmemBytes = TP_SMEM;
+            RB_CUDA(cudaLaunchKernelEx(&cfg, k_insert_payload_tma, b->v, p, bt.tok_offsets,
+                                       (int)bt.n, bt.tokens, bt.logp_old, b->pay_sync));
+        } else {
+            RB_CUDA(cudaLaunchKernelEx(&cfg, k_insert_payload_fifo<PAYLOAD_U>, b->v, p,
+                                       bt.tok_offsets, (int)bt.n, bt.tokens, bt.logp_old,
+                                       b->pay_sync));
+        }
         b->pdl_tail = true;  // a sampler launched next may overlap this copy
         b->pend.pending = 1;
         b->pend.c0 = p.c0;

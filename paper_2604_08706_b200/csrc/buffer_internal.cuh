@@ -118,6 +118,8 @@ struct rb_buffer {
                                         // verdict 1 valid / 2 rejected), read by the payload copy
                                         // and the fused sampler
     bool pdl = true;                    // programmatic dependent launch of the payload copy
+    bool tma_payload = true;            // bulk-copy (TMA) payload kernel (else 128-bit LSU)
+    int sms = 148;
     bool pdl_tail = false;              // the stream's last kernel is the closed-form payload copy
     rb::PendingIns pend{};              // its insert's plan (for a sampler that overlaps it)
     rb::Unit* units_ins = nullptr;      // payload copy units of the last insert
