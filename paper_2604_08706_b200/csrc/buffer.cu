@@ -1,19 +1,21 @@
 // buffer.cu — ShardedReplayBuffer on the GPU (replay_buffer.hpp:57-108).
 //
-// Kernels (one step of the replay path):
-//   k_insert_route    1 CTA: group advantages (bandit.cpp:276-294), duplicate
-//                     screening, round-robin routing (replay_buffer.cpp:89-90),
-//                     eviction (FIFO closed form / positive-bias warp per shard /
-//                     exact sequential path), metadata scatter.
-//   k_insert_payload  one CTA per inserted trajectory: 128-bit funnel-shifted
-//                     copy of the surviving trajectories' {token, logp_old}.
-//   k_sample_with     1 CTA: MT19937-64 block twist + below() rejection
-//                     (rng.cpp:40-51) for uniform_with_replacement.
-//   k_sample_without  1 thread: partial Fisher-Yates / unused-first
-//                     (replay_buffer.cpp:146-179, rng.cpp:108-121).
-//   k_sample_map      1 CTA: arrival index -> slot, use counts, packed offsets.
-//   k_gather          one CTA per selection: ragged 128-bit gather into the
-//                     packed batch.
+// Kernels of one replay step, all on the buffer's stream:
+//   k_route_fifo          FIFO insert, ids promised unique: one record per
+//                         thread, whole-batch validation per CTA, group
+//                         advantages (bandit.cpp:276-294), routing and
+//                         victims in closed form (replay_buffer.cpp:83-133).
+//   k_insert_payload_tma  closed-form payload copy over cp.async.bulk, a
+//                         programmatic dependent of the route (gated on its
+//                         verdict); k_insert_payload: the table-driven copy.
+//   k_sample_fused        uniform_with_replacement: MT19937-64 ring twisted
+//                         ahead, draws, arrival index -> slot, look-back scan
+//                         of the packed offsets (replay_buffer.cpp:135-217).
+//   k_gather              ragged 128-bit gather of the sampled rows.
+// General paths: k_insert_route (exact sequential semantics: duplicate ids,
+// positive bias validation) + k_posbias_batch (positive bias as O(1) queues),
+// k_sample_without + k_sample_map (without-replacement strategies),
+// k_sample_records (record copies with post-increment use counts, ledger).
 #include <algorithm>
 #include <charconv>
 #include <climits>
