@@ -45,6 +45,10 @@ CONFIGS = {
     "c1": dict(name="C1: buffer 84, (W,T)=(5,3), G=8, 64 prompts, 1024 tokens, GRPO",
                capacity=84, batch=512, group=8, lmax=1024, ragged=False,
                retention="plain_fifo", delta=0.0, loss="grpo"),
+    "c5": dict(name="C5: staleness/reuse sweep W in {1,2,4,8}, T in {1,2,4} shards, buffer "
+                    "84..4092, B=504 (63 prompts x G=8), record level (insert+evict+sample)",
+               capacity=0, batch=504, group=8, lmax=0, ragged=False, retention="plain_fifo",
+               delta=0.0, loss="none"),
     "c2": dict(name="C2: C1 + positive-bias retention (delta=0.5) + AsymRE",
                capacity=84, batch=512, group=8, lmax=1024, ragged=False,
                retention="positive_bias", delta=0.5, loss="asymre"),
@@ -473,6 +477,109 @@ def run_e2e(args, buf, wl, rng, cfg):
                                         "pipelines its upload/download in chunks)"}
 
 
+# ---------------------------------------------------------------- C5 sweep
+C5_W = (1, 2, 4, 8)
+C5_T = (1, 2, 4)
+C5_N = (84, 756, 4092)
+
+
+def c5_cpu(T, N, W, steps):
+    import ctypes as C
+
+    from oracle.pyoracle import REF_SO
+
+    L = C.CDLL(REF_SO)
+    L.ref_c5_run.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_double, C.c_uint64,
+                             C.c_uint64, C.c_int, C.c_double, C.c_uint64, C.c_int,
+                             C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+    sec, rec = C.c_double(), C.c_uint64()
+    if L.ref_c5_run(T, N, W, T_TRAINERS, MU, 504, 8, 0, 0.0, SEED, steps, C.byref(sec), C.byref(rec)):
+        raise RuntimeError("ref_c5_run failed")
+    return rec.value / sec.value
+
+
+def run_c5(args):
+    """Record-level (W,T) sweep: insert (route + eviction + advantages) and
+    sample through the library, T shards on one GPU (simulate() semantics,
+    async_sim.cpp:138-139), timed as one CUDA graph of K steps; the
+    unmodified reference buffer on 1 host core beside it."""
+    import torch
+
+    import paper_2604_08706_b200 as rb
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    B, G = 504, 8
+    K = max(args.steps, 20)
+    rows = []
+    for N in C5_N:
+        for T in C5_T:
+            for W in C5_W:
+                print(f"c5: N={N} T={T} W={W}", file=sys.stderr, flush=True)
+                buf = rb.ShardedReplayBuffer(T, N, "uniform_with_replacement", "plain_fifo", 0.0,
+                                             max_tokens=0)
+                buf.set_stream(stream.cuda_stream)
+                rng = rb.Rng(SEED).stream("buffer_sampling")
+                per = W * B / (MU * T_TRAINERS)
+                nid = [0]
+
+                def batch(ng, step):
+                    n = ng * G
+                    ids = torch.arange(nid[0], nid[0] + n, dtype=torch.int64, device=dev)
+                    nid[0] += n
+                    rew = (torch.rand(n, device=dev) < 0.5).to(torch.float64)
+                    return dict(rollout_id=ids, reward=rew, group_id=ids // G,
+                                creation_step=torch.full((n,), step, dtype=torch.int64, device=dev),
+                                group_offsets=torch.arange(0, n + 1, G, dtype=torch.int64, device=dev))
+
+                buf.insert(**batch(-(-N // G), 0), assume_unique=True)
+                debt, plan = 0.0, []
+                for i in range(K + 3):
+                    debt += per
+                    ng = int(debt // G)
+                    debt -= ng * G
+                    plan.append(batch(ng, i + 1) if ng else None)
+                ins = sum(int(p["rollout_id"].numel()) for p in plan[3:] if p is not None)
+
+                def step(p):
+                    if p is not None:
+                        buf.insert(**p, assume_unique=True)
+                    buf.sample_device(B, rng)
+
+                for p in plan[:3]:
+                    step(p)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+                    for p in plan[3:]:
+                        step(p)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                buf.check()
+                ms = e0.elapsed_time(e1) / K
+                gpu = (ins + K * B) / (ms * K * 1e-3)
+                cpu = None if args.no_cpu_baseline else c5_cpu(T, N, W, 20)
+                rows.append({"W": W, "T": T, "N": N, "us_per_step": ms * 1e3,
+                             "gpu_records_per_s": gpu, "cpu_records_per_s": cpu,
+                             "gpu_over_cpu": gpu / cpu if cpu else None})
+                del g, buf
+    gm = float(np.exp(np.mean([np.log(r["gpu_records_per_s"]) for r in rows])))
+    return {"metric": "C5 eviction+sampling throughput: (inserted+sampled) records/s, geometric "
+                      "mean over the sweep", "value": gm, "unit": "records/s", "n_gpus": 1,
+            "steps": K, "warmup": 3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": CONFIGS["c5"]["name"], "W": C5_W, "T": C5_T, "N": C5_N,
+                       "B": B, "G": G, "mu": MU},
+            "cpu_baseline": {"kind": "reference", "cores": 1,
+                             "sample": "20 steps of the same schedule through the unmodified "
+                                       "replab ShardedReplayBuffer per configuration"},
+            "sweep": rows}
+
+
 # ---------------------------------------------------------------- CPU arm
 def cpu_reference(cfg, steps, warmup, threads=0):
     """The reference's CPU path (oracle/_ref: unmodified replab buffer/sampler/
@@ -616,6 +723,12 @@ def main():
     import torch
 
     torch.cuda.set_device(local)
+    if args.config == "c5":  # record-level sweep (one GPU; not the headline metric)
+        if rank == 0:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                print(json.dumps(run_c5(args)), flush=True)
+        return
     dist = None
     if world > 1:
         import torch.distributed as dist

@@ -10,6 +10,7 @@
 //   replab::ShardedReplayBuffer replay_buffer.hpp:57-108
 //   replab::group_advantages    bandit.hpp:106
 //   replab::grpo_loss_grad / asymre_loss_grad  bandit.hpp:133-139
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -377,3 +378,54 @@ int ref_bench_phase_b(void* hv, const float* logp_now, double eps_low, double ep
 }
 
 }  // extern "C"
+
+// =========================================================================
+// CPU reference arm of the C5 sweep (record level): the
+// (W,T) schedule of train()/simulate() through the unmodified reference
+// buffer — warm-up fill (bandit.cpp:609-615), then per step the production
+// debt W*B/(mu*T) in whole groups (617-640, records pushed one by one,
+// replay_buffer.cpp:83-133) and sample(B) with the "buffer_sampling" stream
+// (replay_buffer.cpp:184-217).  Returns the seconds spent in the timed
+// steps and the records processed (inserted + sampled).
+extern "C" int ref_c5_run(uint64_t T, uint64_t N, int W, int Ttr, double mu, uint64_t B,
+                          uint64_t G, int retention, double delta, uint64_t seed, int steps,
+                          double* seconds, uint64_t* records) {
+    return guard([&] {
+        ShardedReplayBuffer buf(T, N, SamplingStrategy::uniform_with_replacement,
+                                retention_of(retention, delta));
+        Rng sampling = Rng(seed).stream("buffer_sampling");
+        Rng gen = Rng(seed).stream("generation");
+        uint64_t next_id = 0;
+        auto push_group = [&](int64_t step) {
+            for (uint64_t i = 0; i < G; ++i) {
+                RolloutRecord r{};
+                r.rollout_id = next_id++;
+                r.group_id = r.rollout_id / G;
+                r.creation_step = step;
+                r.policy_version = step;
+                r.reward = gen.uniform01() < 0.5 ? 1.0 : 0.0;
+                r.is_correct = r.reward == 1.0;
+                buf.push(r);
+            }
+        };
+        while (buf.size() < N) push_group(0);
+        const double per = (double)W * (double)B / (mu * (double)Ttr);
+        double debt = 0.0;
+        uint64_t recs = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int step = 0; step < steps; ++step) {
+            debt += per;
+            while (debt >= (double)G) {
+                push_group(step);
+                debt -= (double)G;
+                recs += G;
+            }
+            auto batch = buf.sample(B, sampling);
+            recs += batch.size();
+        }
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+        *records = recs;
+    });
+}
+

@@ -1309,11 +1309,12 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
         g[r] = s * v.C + arrival_slot_h(v, s, ix[r], cached_head(v, s_head, s));
         const int nf = s < MAP_NSH ? s_newfrom[s] : INT_MAX;
         nw[r] = ix[r] >= nf;  // a record of the pending insert: length from its offsets
-        const int j = nw[r] ? s_j0[s] + (s_ns[s] - (s_occ_after[s] - ix[r])) * v.T : 0;
-        const int64_t* to = nw[r] ? pi.toff : reinterpret_cast<const int64_t*>(v.pushes);
+        const bool has_off = nw[r] && pi.toff != nullptr;  // no offsets: length 0
+        const int j = has_off ? s_j0[s] + (s_ns[s] - (s_occ_after[s] - ix[r])) * v.T : 0;
+        const int64_t* to = has_off ? pi.toff : reinterpret_cast<const int64_t*>(v.pushes);
         lv[r] = v.len[g[r]];
         t0[r] = to[j];
-        t1[r] = to[j + (nw[r] ? 1 : 0)];
+        t1[r] = to[j + (has_off ? 1 : 0)];
     }
 #pragma unroll
     for (int r = 0; r < MAP_R; ++r) {
@@ -2130,6 +2131,7 @@ rb_buffer::~rb_buffer() {
         if (e) cudaEventDestroy(e);
     if (cs_in) cudaStreamDestroy(cs_in);
     if (cs_out) cudaStreamDestroy(cs_out);
+    cudaGetLastError();  // destructors report nothing: leave no error behind
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -2472,8 +2474,9 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
     in.n_units = b->n_units_ins;
     if (!payload) in.toff = bt.tok_offsets;  // lengths only
     bool closed = false;
-    if (unique && b->retention == RB_PLAIN_FIFO && !want_evrec &&
-        bt.n <= (size_t)RT_THREADS * GRID_MAX_CTAS) {
+    const bool fifo_route = unique && b->retention == RB_PLAIN_FIFO && !want_evrec &&
+                            bt.n <= (size_t)RT_THREADS * GRID_MAX_CTAS;
+    if (fifo_route) {
         // ids promised new and increasing: the closed-form FIFO route
         const unsigned grid = (unsigned)((bt.n + RT_THREADS - 1) / RT_THREADS);
         closed = payload && b->T <= 64 && b->pdl;
@@ -2528,6 +2531,15 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
             b->v, b->units_ins, b->n_units_ins, (int)bt.n, bt.tokens, bt.logp_old);
         RB_CUDA(cudaGetLastError());
         b->pdl_tail = false;
+    } else if (fifo_route && b->T <= 64 && b->pdl) {
+        // no payload: the route kernel (which triggers its dependents at its
+        // start) is the tail; a sampler may overlap it with the insert's plan
+        b->pdl_tail = true;
+        b->pend.pending = 1;
+        b->pend.c0 = (int)(b->h_cursor % b->T);
+        b->pend.n = (int)bt.n;
+        b->pend.toff = bt.tok_offsets;  // lengths only (or NULL: length 0)
+        for (size_t s = 0; s < b->T; ++s) b->pend.P[s] = b->h_pushes[s];
     } else {
         b->pdl_tail = false;
     }
@@ -2584,6 +2596,12 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
               size_t* out_applied, int flags) {
     return guard([&] {
         DeviceScope ds(b->device);
+        {  // an error left by an unrelated earlier call must not be blamed on this one
+            const cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess)
+                throw Error(RB_ECUDA, std::string("CUDA error pending before rb_insert: ") +
+                                          cudaGetErrorString(e));
+        }
         rb_insert_batch bt = *bt_in;
         if (out_applied) *out_applied = 0;
         if (bt.n == 0) return;

@@ -91,15 +91,21 @@ rb_rng::rb_rng(uint64_t seed_) : seed(seed_) {
 }
 rb_rng::~rb_rng() {
     if (done) {
-        cudaEventSynchronize(done);
+        // an event last recorded inside a stream capture cannot be waited on
+        if (cudaEventSynchronize(done) != cudaSuccess) cudaDeviceSynchronize();
         cudaEventDestroy(done);
     }
     if (dev) cudaFree(dev);
+    cudaGetLastError();  // destructors report nothing: leave no error behind
 }
 
 void rb_rng::to_host() {
     if (where == 0) return;
-    if (done) RB_CUDA(cudaEventSynchronize(done));
+    if (done && cudaEventSynchronize(done) != cudaSuccess) {
+        // last recorded inside a stream capture: wait for the device instead
+        cudaGetLastError();
+        RB_CUDA(cudaDeviceSynchronize());
+    }
     MtRingHead h;
     static_assert(offsetof(MtRing, blk) == sizeof(MtRingHead), "MtRing header layout");
     RB_CUDA(cudaMemcpy(&h, dev, sizeof h, cudaMemcpyDeviceToHost));
@@ -120,7 +126,10 @@ MtRing* rb_rng::to_device(cudaStream_t s) {
     if (where == 0) {
         // the previous device user must be finished before we overwrite;
         // the host state becomes ring block 0
-        RB_CUDA(cudaEventSynchronize(done));
+        if (cudaEventSynchronize(done) != cudaSuccess) {
+            cudaGetLastError();
+            RB_CUDA(cudaDeviceSynchronize());
+        }
         MtRingHead h;
         h.q_state = 0;
         h.q_hi = 0;
