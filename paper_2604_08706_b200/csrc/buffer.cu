@@ -2980,10 +2980,11 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
         if (ht) dt = (int32_t*)stage;
         if (hl) dl = (float*)(stage + pb);
         if (nloc > 0 && (dt || dl)) {
-            k_gather<GATHER_U><<<b->grid_gather, UNIT_THREADS, 0, b->stream>>>(b->v, b->units_sel, b->n_units_sel, (int)nloc, dt, dl);
+            k_gather<GATHER_U><<<b->grid_gather, UNIT_THREADS, 0, b->stream>>>(
+                b->v, b->units_sel, b->n_units_sel, (int)nloc, dt, dl);
             RB_CUDA(cudaGetLastError());
         }
-        if (ht) RB_CUDA(cudaMemcpyAsync(out_tokens, dt, total * 4, cudaMemcpyDeviceToHost, b->stream));
+            if (ht) RB_CUDA(cudaMemcpyAsync(out_tokens, dt, total * 4, cudaMemcpyDeviceToHost, b->stream));
         if (hl) RB_CUDA(cudaMemcpyAsync(out_logp_old, dl, total * 4, cudaMemcpyDeviceToHost, b->stream));
         if (out_offsets)
             RB_CUDA(cudaMemcpyAsync(out_offsets, b->sel_off, (nloc + 1) * 8, cudaMemcpyDefault,
@@ -2995,6 +2996,7 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
 int rb_batch_ids(rb_buffer* b, uint64_t* out_ids, int32_t* out_lengths, int64_t* out_offsets) {
     return guard([&] {
         DeviceScope ds(b->device);
+        b->other_work();
         const size_t per = b->T ? (b->B / b->T) : 0;
         const long long lo = (long long)std::min(b->sb * per, b->B);
         const long long hi = (long long)std::min(b->se * per, b->B);
@@ -3041,6 +3043,7 @@ int rb_shard_contents(rb_buffer* b, size_t shard, rb_record* out, size_t capacit
                       size_t* count) {
     return guard([&] {
         DeviceScope ds(b->device);
+        b->other_work();
         if (shard >= b->T) throw Error(RB_ELOGIC, "vector::_M_range_check: shard out of range");
         const size_t n = (size_t)std::min<long long>(b->h_pushes[shard], (long long)b->C);
         *count = n;
@@ -3059,6 +3062,7 @@ int rb_record_tokens(rb_buffer* b, size_t shard, size_t index, int32_t* tokens,
                      float* logp_old, int32_t capacity, int32_t* n_tokens) {
     return guard([&] {
         DeviceScope ds(b->device);
+        b->other_work();
         if (shard >= b->T) invalid("rb_record_tokens: shard out of range");
         const size_t n = (size_t)std::min<long long>(b->h_pushes[shard], (long long)b->C);
         if (index >= n) invalid("rb_record_tokens: index out of range");
@@ -3278,6 +3282,7 @@ extern "C" int rb_load(const char* text, int32_t max_tokens, int device, rb_buff
                             std::to_string(shards[shard].back().rollout_id));
             }
             DeviceScope ds(b->device);
+        b->other_work();
             unsigned long long mx = 0;
             for (size_t s = 0; s < T; ++s) {
                 const size_t n = shards[s].size();

@@ -122,6 +122,7 @@ struct rb_buffer {
     int sms = 148;
     bool pdl_tail = false;              // the stream's last kernel is the closed-form payload copy
     rb::PendingIns pend{};              // its insert's plan (for a sampler that overlaps it)
+    void other_work() { pdl_tail = false; }  // anything else enqueued on the stream
     rb::Unit* units_ins = nullptr;      // payload copy units of the last insert
     int* n_units_ins = nullptr;
     size_t units_ins_cap = 0;

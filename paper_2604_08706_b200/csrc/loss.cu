@@ -729,6 +729,7 @@ constexpr int LOSS_CHUNKS = 8;  // host-buffer pipeline depth
 // re-downloads dlogp after the pipeline.
 void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
               rb_loss_stats* stats) {
+    b->other_work();
     const size_t per = b->T ? b->B / b->T : 0;
     const long long lo = (long long)std::min(b->sb * per, b->B);
     const long long hi = (long long)std::min(b->se * per, b->B);
@@ -866,6 +867,7 @@ int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double
 
 int rb_loss_finalize(rb_buffer* b, float* dlogp, rb_loss_stats* stats) {
     return guard([&] {
+        b->other_work();
         // Asynchronous when stats is a device pointer (the multi-GPU hot path:
         // allreduce the device stats, then finalize without a host round trip).
         if (!stats) invalid("rb_loss_finalize: stats required");
