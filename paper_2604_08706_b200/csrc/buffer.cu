@@ -1113,6 +1113,18 @@ __device__ __forceinline__ int cached_head(const BufView& v, const int* heads, i
     return s < MAP_NSH ? heads[s] : shard_head(v, s);
 }
 
+// Arrival head of shard s once the preceding insert is applied: from the
+// insert's plan while it may still be running (closed-form FIFO, <= 64
+// shards), else from the device counters.
+__device__ __forceinline__ int head_after(const BufView& v, const PendingIns& pi, int s) {
+    if (!pi.pending) return shard_head(v, s);
+    const int T = v.T, C = v.C;
+    const int j0 = ((s - pi.c0) % T + T) % T;
+    const int ns = pi.n > j0 ? (pi.n - 1 - j0) / T + 1 : 0;
+    const long long P = pi.P[s] + ns;
+    return P >= C ? (int)(P % C) : 0;
+}
+
 // Grid-wide bookkeeping of the multi-CTA kernels (no grid barrier): CTAs
 // take tickets in launch order, publish look-back words, and the last CTA
 // to finish (done counter) finalises and resets the control block.
@@ -1301,6 +1313,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
     }
     RB_GCLOCK(46 + 8 * (t & 1), t < 2);
     int lv[MAP_R];
+    double av[MAP_R];
     long long t0[MAP_R], t1[MAP_R];
     bool nw[MAP_R];
 #pragma unroll
@@ -1313,6 +1326,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
         const int j = has_off ? s_j0[s] + (s_ns[s] - (s_occ_after[s] - ix[r])) * v.T : 0;
         const int64_t* to = has_off ? pi.toff : reinterpret_cast<const int64_t*>(v.pushes);
         lv[r] = v.len[g[r]];
+        av[r] = v.adv[g[r]];  // old records' advantages (new ones: after the route)
         t0[r] = to[j];
         t1[r] = to[j + (has_off ? 1 : 0)];
     }
@@ -1381,7 +1395,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
         d.k0 = 0;
         d.g = g[r];
         d.off = pos;
-        d.adv = 0.0;  // below, once the route kernel has written it
+        d.adv = av[r];  // new records: patched below once the route kernel wrote it
         a.units[k - a.lo] = d;
         const int nq = ((int)(pos & 3) + L[r] + 3) >> 2;
         if (L[r]) maxq = nq > maxq ? nq : maxq;
@@ -1389,23 +1403,34 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
     }
     maxq = __reduce_max_sync(0xffffffffu, maxq);
     if ((tid & 31) == 0) s_m[tid >> 5] = maxq;
-    // the route kernel's metadata: advantages and use counts (replay_buffer.cpp:201)
-    if (tid == 0) spin_until_set(route_done);
-    __syncthreads();
+    // use counts (replay_buffer.cpp:201): records older than the pending
+    // insert now (its route kernel leaves their slots alone) ...
+    bool any_new = false;
+#pragma unroll
+    for (int r = 0; r < MAP_R; ++r) {
+        if (!ok[r]) continue;
+        if (nw[r]) any_new = true;
+        else atomicAdd(&v.use[g[r]], 1u);
+    }
+    // ... and its own records once the route kernel has written them
+    if (__syncthreads_or(any_new)) {
+        if (tid == 0) spin_until_set(route_done);
+        __syncthreads();
+        double adv[MAP_R];
+#pragma unroll
+        for (int r = 0; r < MAP_R; ++r) adv[r] = v.adv[g[r]];
+#pragma unroll
+        for (int r = 0; r < MAP_R; ++r) {
+            if (!ok[r] || !nw[r]) continue;
+            atomicAdd(&v.use[g[r]], 1u);
+            const long long k = k0 + r;
+            if (k >= a.lo && k < a.hi) reinterpret_cast<double*>(&a.units[k - a.lo])[3] = adv[r];
+        }
+    }
     if (tid == 0) {
         int m = 0;
         for (int w = 0; w < MAP_THREADS / 32; ++w) m = s_m[w] > m ? s_m[w] : m;
         gc->cta_max[t] = m;
-    }
-    double adv[MAP_R];
-#pragma unroll
-    for (int r = 0; r < MAP_R; ++r) adv[r] = v.adv[g[r]];
-#pragma unroll
-    for (int r = 0; r < MAP_R; ++r) {
-        if (!ok[r]) continue;
-        atomicAdd(&v.use[g[r]], 1u);
-        const long long k = k0 + r;
-        if (k >= a.lo && k < a.hi) reinterpret_cast<double*>(&a.units[k - a.lo])[3] = adv[r];
     }
     RB_GCLOCK(45 + 8 * (t & 1), t < 2);
 }
@@ -1482,9 +1507,12 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
             r->draws = r->draws + (unsigned long long)k0 + dr;
         }
         __syncthreads();
-        // map the replayed tail, then rescan every owned offset
+        // map the replayed tail, then rescan every owned offset (shard heads
+        // from the insert's plan: the route kernel may still be advancing
+        // the device counters)
         __shared__ int s_head[MAP_NSH];
-        for (int s = threadIdx.x; s < a.nsh && s < MAP_NSH; s += blockDim.x) s_head[s] = shard_head(v, s);
+        for (int s = threadIdx.x; s < a.nsh && s < MAP_NSH; s += blockDim.x)
+            s_head[s] = head_after(v, a.pend, s);
         __syncthreads();
         unsigned long long tail = 0;
         for (long long k = k0 + threadIdx.x; k < D; k += blockDim.x) {
@@ -1862,8 +1890,10 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
             }
         }
     }
+    RB_GCLOCK(60, blockIdx.x == 0);
     if (bad) atomicOr(&s_bad, bad);
     __syncthreads();
+    RB_GCLOCK(61, blockIdx.x == 0);
     const int bb = s_bad;
     // every CTA reached the same verdict; CTA 0 alone publishes it
     if (blockIdx.x == 0 && tid == 0) st_release_i32(&pay_sync[0], bb ? 2 : 1);
@@ -1930,6 +1960,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
         in.gmean_out[j] = gmean;
         in.units[j] = d;
     }
+    RB_GCLOCK(62, blockIdx.x == 0);
     maxq = __reduce_max_sync(0xffffffffu, maxq);
     if ((tid & 31) == 0) s_m[tid >> 5] = maxq;
     __syncthreads();
@@ -1941,9 +1972,14 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
         s_last = atomicAdd(&gc->done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
+    RB_GCLOCK(63, blockIdx.x == 0);
     if (!s_last) return;
-    // last CTA: counters (every CTA read them before its done increment)
+    RB_GCLOCK(56, true);
+    // last CTA: every CTA's records are written (each fenced before its done
+    // increment): the sampler's map may read the metadata now; the counters
+    // below are not read by it (it uses the insert's plan)
     __threadfence();
+    if (tid == 0) st_release_i32(&pay_sync[1], 1);
     int m = 0;
     for (int c = tid; c < (int)gridDim.x; c += RT_THREADS) m = max(m, __ldcg(&gc->cta_max[c]));
     m = __reduce_max_sync(0xffffffffu, m);
@@ -1969,7 +2005,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
             ctl->err_index = (bb & 2) ? -3 : (bb & 4) ? -2 : -4;
         }
         gc->done = 0;
-        st_release_i32(&pay_sync[1], 1);  // the sampler's map may read the metadata
+        RB_GCLOCK(57, true);
     }
     RB_TEND(0);
 }

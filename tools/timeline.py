@@ -59,7 +59,9 @@ names = {40: "map t0 start", 41: "map0 enter", 42: "map0 after local twist", 46:
          44: "map0 after lookback", 45: "map0 end", 49: "map1 enter", 50: "map1 after local twist",
          54: "map1 after draws", 55: "map1 after L loads",
          51: "map1 after loads", 52: "map1 after lookback", 53: "map1 end", 58: "finalize start",
-         59: "finalize end"}
+         59: "finalize end", 60: "route0 loads+validation", 61: "route0 verdict",
+         62: "route0 records written", 63: "route0 done-count", 56: "route last CTA start",
+         57: "route done flag"}
 for i, nm in names.items():
     if ck[i] > 0:
         print(f"  {nm:22s} {(ck[i] - t0) / 1e3:9.2f} us")
