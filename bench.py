@@ -403,13 +403,14 @@ def load_traffic(kernel):
         return None
 
 
-def run_e2e(args, buf, wl, rng, cfg):
+def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None):
     """Same metric through the C-ABI with HOST (pinned) buffers, copies timed."""
     import torch
 
     import paper_2604_08706_b200 as rb  # noqa: F401
 
     B = cfg["batch"]
+    nloc = B // world  # selections held by this rank
     K = min(args.steps, 8)
     steps = wl.steps[-K:] if len(wl.steps) >= K else wl.steps
     host = []
@@ -425,8 +426,8 @@ def run_e2e(args, buf, wl, rng, cfg):
     lpn_h = torch.empty(pad, dtype=torch.float32).pin_memory()
     buf.sample_device(B, rng)
     buf.gather(tok_h, None, off_h)
-    ids = torch.empty(B, dtype=torch.int64, device="cuda")
-    offd = off_h.cuda()
+    ids = torch.empty(nloc, dtype=torch.int64, device="cuda")
+    offd = off_h[:nloc + 1].cuda()
     lpn_d = torch.empty(pad, dtype=torch.float32, device="cuda")
     from tools import synth
 
@@ -452,7 +453,7 @@ def run_e2e(args, buf, wl, rng, cfg):
         st = buf.loss_grpo(lpn_h, dl_h, EPS_LOW, EPS_HIGH) if cfg["loss"] == "grpo" else \
             buf.loss_asymre(lpn_h, dl_h, DELTA_V)
         _ = st.objective  # device->host read of the step's result
-        return int(off_h[B])  # this step's sampled tokens (offsets already on the host)
+        return int(off_h[nloc])  # this rank's sampled tokens (offsets already on the host)
 
     for r, hb2, n in plan:
         if r == 0:
@@ -470,6 +471,12 @@ def run_e2e(args, buf, wl, rng, cfg):
         d2h += tot_s * 4 * 2 + (B + 1) * 8 + 40
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / len(host)
+    if world > 1:  # whole job: tokens of every rank over the slowest rank's time
+        t = torch.tensor([float(done_tokens), dt], dtype=torch.float64)
+        dist.all_reduce(t[0:1])
+        dist.all_reduce(t[1:2], op=dist.ReduceOp.MAX)
+        done_tokens, dt = float(t[0]), float(t[1])
+        h2d, d2h = h2d * world, d2h * world
     return {"value": done_tokens / len(host) / dt, "unit": "tokens/s", "ms_per_step": dt * 1e3,
             "h2d_bytes_per_step": h2d // len(host), "d2h_bytes_per_step": d2h // len(host),
             "steps": len(host), "path": "rb_insert/rb_sample/rb_gather/rb_loss_* with pinned host "
@@ -722,6 +729,11 @@ def main():
 
     import torch
 
+    # RB_BENCH_SAME_GPU=1 (test aid): every rank on cuda:0 with gloo, to
+    # exercise the sharded path on a one-GPU box (not a performance number)
+    same_gpu = os.environ.get("RB_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if args.config == "c5":  # record-level sweep (one GPU; not the headline metric)
         if rank == 0:
@@ -733,12 +745,15 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()  # a real stream handle (not the legacy default)
     with torch.cuda.stream(stream):
         res, buf, wl, rng = run_ours(args, rank, world, dist)
         if not args.no_e2e:
-            res["e2e"] = run_e2e(args, buf, wl, rng, cfg)
+            res["e2e"] = run_e2e(args, buf, wl, rng, cfg, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             r = cpu_reference(cfg, args.cpu_steps, 1)

@@ -2457,6 +2457,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         }
         b->pdl = std::getenv("RB_NO_PDL") == nullptr;
         b->tma_payload = std::getenv("RB_PAYLOAD_LSU") == nullptr;
+        if (const char* e = std::getenv("RB_TMA_CTAS")) b->tma_ctas = std::max(1, std::atoi(e));
         b->sms = sms;
         RB_CUDA(cudaFuncSetAttribute(k_insert_payload_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)TP_SMEM));
@@ -2546,7 +2547,7 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         cfg.attrs = at;
         cfg.numAttrs = 1;
         if (b->tma_payload) {
-            cfg.gridDim = dim3(b->sms);
+            cfg.gridDim = dim3(b->sms * b->tma_ctas);
             cfg.blockDim = dim3(TP_THREADS);
             cfg.dynamicSmemBytes = TP_SMEM;
             RB_CUDA(cudaLaunchKernelEx(&cfg, k_insert_payload_tma, b->v, p, bt.tok_offsets,

@@ -120,6 +120,7 @@ struct rb_buffer {
     bool pdl = true;                    // programmatic dependent launch of the payload copy
     bool tma_payload = true;            // bulk-copy (TMA) payload kernel (else 128-bit LSU)
     int sms = 148;
+    int tma_ctas = 1;                   // bulk-copy payload CTAs per SM
     bool pdl_tail = false;              // the stream's last kernel is the closed-form payload copy
     rb::PendingIns pend{};              // its insert's plan (for a sampler that overlaps it)
     void other_work() { pdl_tail = false; }  // anything else enqueued on the stream

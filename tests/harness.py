@@ -126,6 +126,8 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
     dev = "cuda:0" if cfg.device_inputs else None
     gbuf = ShardedReplayBuffer(cfg.shards, cfg.capacity, cfg.strategy, cfg.retention, cfg.delta,
                                max_tokens=cfg.lmax)
+    if dev:  # inputs are copied to the device on torch's stream: run the library on it too
+        gbuf.set_stream(torch.cuda.current_stream().cuda_stream)
     obuf = ora.buffer(cfg.shards, cfg.capacity, cfg.strategy, cfg.retention, cfg.delta)
     grng = Rng(cfg.seed).stream("buffer_sampling")
     orng = ora.rng(cfg.seed).stream("buffer_sampling")

@@ -1,0 +1,171 @@
+"""World-size-2 run of the CUDA replay step with one buffer shard per rank
+(DESIGN.md §6), both ranks on cuda:0 and gloo for the 24-byte loss
+all-reduce (the only collective of the path): every rank replicates the
+metadata of all shards and regenerates the same MT19937-64 stream, owns the
+payload of its shard, gathers and evaluates its own selections, all-reduces
+{objective_sum, included, excluded} and finalises dlogp.  Checked against
+the single-process CPU oracle: sampled records, the owned packed tokens, the
+globally normalised dlogp and the objective.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from tests.harness import Producer, StepConfig
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "fifo_unique": dict(capacity=128, shards=2, batch=32, group=8, lmax=40, ragged=True, seed=31,
+                        assume_unique=True),
+    "posbias": dict(capacity=96, shards=2, batch=32, group=8, lmax=24, ragged=True, seed=32,
+                    retention="positive_bias", delta=0.5),
+}
+STEPS = 6
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _run(rank, world, port, case, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from oracle.pyoracle import Oracle, same_records
+        from paper_2604_08706_b200 import Rng, ShardedReplayBuffer
+
+        cfg = StepConfig(**CASES[case])
+        ora = Oracle()
+        obuf = ora.buffer(cfg.shards, cfg.capacity, cfg.strategy, cfg.retention, cfg.delta)
+        orng = ora.rng(cfg.seed).stream("buffer_sampling")
+        gbuf = ShardedReplayBuffer(cfg.shards, cfg.capacity, cfg.strategy, cfg.retention,
+                                   cfg.delta, max_tokens=cfg.lmax, shard_range=(rank, rank + 1))
+        # the library on torch's stream: the inputs torch copies to the device
+        # are ordered before the kernels that read them
+        gbuf.set_stream(torch.cuda.current_stream().cuda_stream)
+        grng = Rng(cfg.seed).stream("buffer_sampling")
+        prod = Producer(cfg, ora)
+        lengths = {}
+        dev = "cuda:0"
+
+        def push(ng, step):
+            rec, length, tok, lpo, toff, _ = prod.groups(ng, step)
+            for r, L in zip(rec, length):
+                lengths[int(r["rollout_id"])] = int(L)
+                obuf.push(r)
+            n = rec.shape[0]
+            t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+            gbuf.insert(rollout_id=t(rec["rollout_id"].copy()), prompt_id=t(rec["prompt_id"].copy()),
+                        group_id=t(rec["group_id"].copy()),
+                        creation_step=t(rec["creation_step"].copy()),
+                        policy_version=t(rec["policy_version"].copy()),
+                        reward=t(rec["reward"].copy()),
+                        behavior_logprob=t(rec["behavior_logprob"].copy()),
+                        group_offsets=t(np.arange(0, n + 1, cfg.group, dtype=np.int64)),
+                        tok_offsets=t(toff), tokens=t(tok), logp_old=t(lpo),
+                        assume_unique=cfg.assume_unique)
+
+        while obuf.size() < cfg.capacity:
+            push(1, 0)
+        per = cfg.batch // cfg.shards
+        lo, hi = rank * per, (rank + 1) * per
+        debt = 0.0
+        for step in range(STEPS):
+            debt += cfg.per_step
+            ng = int(debt // cfg.group)
+            debt -= ng * cfg.group
+            if ng:
+                push(ng, step)
+            grec = gbuf.sample(cfg.batch, grng)
+            orec, _, _ = obuf.sample(cfg.batch, orng)
+            if not same_records(grec, orec):
+                diffs = [f for f in orec.dtype.names if not np.array_equal(grec[f], orec[f])]
+                i = int(np.argmax(grec[diffs[0]] != orec[diffs[0]])) if diffs else -1
+                raise AssertionError(f"rank {rank}: sampled records, step {step}: fields {diffs}, "
+                                     f"first at {i}: got {grec[i]} want {orec[i]}")
+            # owned selections: packed tokens
+            ids = orec["rollout_id"][lo:hi]
+            lens = np.array([lengths[int(i)] for i in ids], np.int64)
+            off = np.zeros(per + 1, np.int64)
+            np.cumsum(lens, out=off[1:])
+            tot = int(off[-1])
+            tok_want, lpo_want, _ = ora.synth_payload(cfg.seed, ids, lens)
+            pad = (tot + 3) // 4 * 4 + 4
+            gt = torch.zeros(pad, dtype=torch.int32, device=dev)
+            go = torch.zeros(per + 1, dtype=torch.int64, device=dev)
+            torch.cuda.synchronize()
+            gbuf.gather(gt, None, go)
+            gbuf.synchronize()
+            assert np.array_equal(go.cpu().numpy(), off), f"rank {rank}: offsets, step {step}"
+            assert np.array_equal(gt[:tot].cpu().numpy(), tok_want), f"rank {rank}: tokens, step {step}"
+            # loss: the whole batch's token loss (oracle), this rank's slice of it
+            all_ids = orec["rollout_id"]
+            all_lens = np.array([lengths[int(i)] for i in all_ids], np.int64)
+            aoff = np.zeros(cfg.batch + 1, np.int64)
+            np.cumsum(all_lens, out=aoff[1:])
+            lpn_all = ora.synth_logp_now(cfg.seed, step + 1, all_ids, aoff)
+            if step % 2 == 1:  # the same excluded tokens on every rank (one per shard)
+                for r0 in range(cfg.shards):
+                    if aoff[(r0 + 1) * per] > aoff[r0 * per] + 1:
+                        lpn_all[aoff[r0 * per] + 1] = np.float32(np.inf)
+            _, lpo_all, _ = ora.synth_payload(cfg.seed, all_ids, all_lens)
+            d_want, obj, inc, exc = ora.loss_grpo_tokens(lpn_all, lpo_all, orec["advantage"], aoff,
+                                                         cfg.eps_low, cfg.eps_high)
+            lpn = torch.zeros(pad, dtype=torch.float32, device=dev)
+            lpn[:tot] = torch.from_numpy(lpn_all[aoff[lo]:aoff[hi]])
+            dl = torch.zeros(pad, dtype=torch.float32, device=dev)
+            stats = torch.zeros(5, dtype=torch.float64, device=dev)
+            torch.cuda.synchronize()
+            gbuf.loss_grpo(lpn, dl, cfg.eps_low, cfg.eps_high, stats=stats)
+            gbuf.synchronize()
+            host = stats.cpu()
+            s_obj = host[0:1].clone()
+            s_cnt = host[2:4].clone().view(torch.int64)
+            dist.all_reduce(s_obj)
+            dist.all_reduce(s_cnt)
+            host[0:1] = s_obj
+            host[2:4] = s_cnt.view(torch.float64)
+            stats.copy_(host.to(dev))
+            torch.cuda.synchronize()  # torch's stream wrote the reduced stats
+            gbuf.loss_finalize(dl, stats)
+            gbuf.synchronize()
+            got = dl[:tot].cpu().numpy()
+            np.testing.assert_allclose(got, d_want[aoff[lo]:aoff[hi]], rtol=1e-5, atol=1e-12,
+                                       err_msg=f"rank {rank}: dlogp, step {step}")
+            inc_got, exc_got = (int(x) for x in s_cnt)
+            assert (inc_got, exc_got) == (inc, exc), (rank, step, inc_got, exc_got, inc, exc)
+            assert abs(float(s_obj[0]) / max(inc_got, 1) - obj) <= 1e-5 * max(1.0, abs(obj))
+        q.put((rank, "ok"))
+    except Exception as e:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_two_ranks_one_shard_each(case):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    bad = {r: m for r, m in res.items() if m != "ok"}
+    assert not bad, "\n".join(f"rank {r}:\n{m}" for r, m in sorted(bad.items()))
