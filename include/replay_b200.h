@@ -97,6 +97,10 @@ int rb_rng_uniform01(rb_rng* r, double* out);                           /* rng.h
 int rb_rng_normal(rb_rng* r, double* out);                              /* rng.hpp:46 */
 int rb_rng_sample_without_replacement(rb_rng* r, uint64_t n, uint64_t k,
                                       uint64_t* out);                   /* rng.hpp:56 */
+/* Engine position for checkpoints (the reference's Rng has none, rng.hpp:26-31):
+ * the 312 state words, the index of the next word and the outputs consumed. */
+int rb_rng_get_state(rb_rng* r, uint64_t* mt312, uint32_t* idx, uint64_t* draws);
+int rb_rng_set_state(rb_rng* r, const uint64_t* mt312, uint32_t idx, uint64_t draws);
 /* Device bulk generation: n raw engine outputs into out (device or host),
  * produced by the GPU generator (parity aid for the sampler's stream). */
 int rb_rng_fill_u64(rb_rng* r, uint64_t n, uint64_t* out);
@@ -241,6 +245,16 @@ int rb_route_cursor(rb_buffer* b, size_t* out);
  * full length; call with out=NULL to size. */
 int rb_dump(rb_buffer* b, char* out, size_t cap, size_t* len);
 int rb_load(const char* text, int32_t max_tokens, int device, rb_buffer** out);
+
+/* Binary checkpoint of the whole device state — metadata columns, arrival
+ * structures (positive-bias queues), owned token payload rows, route cursor,
+ * per-shard push counts — for run resumption (the
+ * reference persists only the text dump above, replay_buffer.cpp:238-324,
+ * SPEC.md:113-114).  dst / src may be host or device memory.  rb_snapshot
+ * with dst = NULL only sets *len.  rb_restore requires a buffer of the same
+ * shape (shards, capacity, strategy, retention, max_tokens, owned shards). */
+int rb_snapshot(rb_buffer* b, void* dst, size_t cap, size_t* len);
+int rb_restore(rb_buffer* b, const void* src, size_t len);
 
 /* Sticky asynchronous error check (synchronises the stream). */
 int rb_check(rb_buffer* b);

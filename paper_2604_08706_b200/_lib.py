@@ -102,6 +102,10 @@ def _load():
         "rb_route_cursor": (ip, [vp, vp]),
         "rb_dump": (ip, [vp, C.c_char_p, sz, vp]),
         "rb_load": (ip, [C.c_char_p, i32, ip, vp]),
+        "rb_snapshot": (ip, [vp, vp, sz, vp]),
+        "rb_restore": (ip, [vp, vp, sz]),
+        "rb_rng_get_state": (ip, [vp, vp, vp, vp]),
+        "rb_rng_set_state": (ip, [vp, vp, C.c_uint32, u64]),
         "rb_check": (ip, [vp]),
         "rb_synchronize": (ip, [vp]),
         "rb_group_advantages": (ip, [vp, vp, sz, vp, vp]),

@@ -3132,6 +3132,116 @@ int rb_route_cursor(rb_buffer* b, size_t* out) {
     return RB_OK;
 }
 
+namespace {
+// ---- binary snapshot (rb_snapshot / rb_restore) ---------------------------
+struct SnapHeader {
+    char magic[8];  // "RBSNAP01"
+    uint64_t T, N, C;
+    int32_t max_tokens, strategy, retention, pad;
+    double delta;
+    uint64_t sb, se, sections;
+};
+struct Section {
+    void* ptr;
+    size_t bytes;
+};
+std::vector<Section> snap_sections(rb_buffer* b) {
+    const BufView& v = b->v;
+    const size_t N = b->N, T = b->T, C = b->C;
+    std::vector<Section> s = {
+        {v.ctl, sizeof(DevCtl)}, {v.pushes, T * 8}, {v.id, N * 8}, {v.prompt, N * 8},
+        {v.group, N * 8}, {v.cstep, N * 8}, {v.pver, N * 8}, {v.reward, N * 8}, {v.blp, N * 8},
+        {v.adv, N * 8}, {v.gmean, N * 8}, {v.correct, N}, {v.use, N * 4}, {v.len, N * 4},
+        {v.order, N * 4}};
+    if (b->retention == RB_POSITIVE_BIAS) {
+        s.push_back({v.pbq, 3 * T * (C + 1) * 4});
+        s.push_back({v.pbs, T * sizeof(PbState)});
+        s.push_back({v.seq, N * 8});
+    }
+    const size_t rows = (b->se - b->sb) * C * (size_t)b->stride;
+    if (rows) {
+        s.push_back({v.tok, rows * 4});
+        s.push_back({v.lpo, rows * 4});
+    }
+    return s;
+}
+SnapHeader snap_header(rb_buffer* b, size_t nsec) {
+    SnapHeader h{};
+    std::memcpy(h.magic, "RBSNAP01", 8);
+    h.T = b->T;
+    h.N = b->N;
+    h.C = b->C;
+    h.max_tokens = b->max_tokens;
+    h.strategy = b->strategy;
+    h.retention = b->retention;
+    h.delta = b->delta;
+    h.sb = b->sb;
+    h.se = b->se;
+    h.sections = nsec;
+    return h;
+}
+}  // namespace
+
+int rb_snapshot(rb_buffer* b, void* dst, size_t cap, size_t* len) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        b->other_work();
+        const auto secs = snap_sections(b);
+        size_t total = sizeof(SnapHeader);
+        for (auto& x : secs) total += 8 + x.bytes;
+        if (len) *len = total;
+        if (!dst) return;
+        if (cap < total) invalid("rb_snapshot: destination too small");
+        check_sticky(b);  // synchronises; the state is consistent
+        const SnapHeader h = snap_header(b, secs.size());
+        char* o = (char*)dst;
+        RB_CUDA(cudaMemcpy(o, &h, sizeof h, cudaMemcpyDefault));
+        o += sizeof h;
+        for (auto& x : secs) {
+            const uint64_t n = x.bytes;
+            RB_CUDA(cudaMemcpy(o, &n, 8, cudaMemcpyDefault));
+            RB_CUDA(cudaMemcpy(o + 8, x.ptr, x.bytes, cudaMemcpyDefault));
+            o += 8 + x.bytes;
+        }
+    });
+}
+
+int rb_restore(rb_buffer* b, const void* src, size_t len) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        b->other_work();
+        const auto secs = snap_sections(b);
+        SnapHeader h;
+        if (!src || len < sizeof h) invalid("rb_restore: snapshot truncated");
+        RB_CUDA(cudaMemcpy(&h, src, sizeof h, cudaMemcpyDefault));
+        const SnapHeader want = snap_header(b, secs.size());
+        if (std::memcmp(h.magic, want.magic, 8) != 0) invalid("rb_restore: not a buffer snapshot");
+        if (h.T != want.T || h.N != want.N || h.C != want.C || h.max_tokens != want.max_tokens ||
+            h.strategy != want.strategy || h.retention != want.retention ||
+            h.delta != want.delta || h.sb != want.sb || h.se != want.se ||
+            h.sections != want.sections)
+            invalid("rb_restore: snapshot of a buffer with a different shape");
+        size_t total = sizeof h;
+        for (auto& x : secs) total += 8 + x.bytes;
+        if (len < total) invalid("rb_restore: snapshot truncated");
+        b->sync();
+        const char* o = (const char*)src + sizeof h;
+        for (auto& x : secs) {
+            uint64_t n = 0;
+            RB_CUDA(cudaMemcpy(&n, o, 8, cudaMemcpyDefault));
+            if (n != x.bytes) invalid("rb_restore: section size mismatch");
+            RB_CUDA(cudaMemcpy(x.ptr, o + 8, x.bytes, cudaMemcpyDefault));
+            o += 8 + x.bytes;
+        }
+        // host mirrors from the restored device state
+        DevCtl c;
+        RB_CUDA(cudaMemcpy(&c, b->v.ctl, sizeof c, cudaMemcpyDeviceToHost));
+        RB_CUDA(cudaMemcpy(b->h_pushes.data(), b->v.pushes, b->T * 8, cudaMemcpyDeviceToHost));
+        b->h_cursor = (size_t)c.cursor;
+        b->B = 0;  // no current batch after a restore
+    });
+}
+
 int rb_check(rb_buffer* b) {
     return guard([&] {
         DeviceScope ds(b->device);

@@ -279,6 +279,25 @@ int rb_rng_sample_without_replacement(rb_rng* r, uint64_t n, uint64_t k, uint64_
     });
 }
 
+int rb_rng_get_state(rb_rng* r, uint64_t* mt312, uint32_t* idx, uint64_t* draws) {
+    return guard([&] {
+        r->to_host();
+        if (mt312) std::memcpy(mt312, r->host.mt, sizeof r->host.mt);
+        if (idx) *idx = r->host.idx;
+        if (draws) *draws = r->host.draws;
+    });
+}
+
+int rb_rng_set_state(rb_rng* r, const uint64_t* mt312, uint32_t idx, uint64_t draws) {
+    return guard([&] {
+        if (!mt312 || idx > (uint32_t)MT_N) invalid("rb_rng_set_state: bad state");
+        r->to_host();  // the device ring (if any) is superseded
+        std::memcpy(r->host.mt, mt312, sizeof r->host.mt);
+        r->host.idx = idx;
+        r->host.draws = draws;
+    });
+}
+
 int rb_rng_fill_u64(rb_rng* r, uint64_t n, uint64_t* out) {
     return guard([&] {
         require_device();

@@ -101,6 +101,18 @@ class Rng:
     def draws(self) -> int:
         return lib.rb_rng_draws(self._h)
 
+    def get_state(self):
+        """(312 uint64 words, next index, outputs consumed) — a checkpoint."""
+        mt = np.zeros(312, np.uint64)
+        idx, dr = C.c_uint32(), C.c_uint64()
+        check(lib.rb_rng_get_state(self._h, mt.ctypes.data, C.byref(idx), C.byref(dr)))
+        return mt, idx.value, dr.value
+
+    def set_state(self, state) -> None:
+        mt, idx, dr = state
+        mt = np.ascontiguousarray(mt, np.uint64)
+        check(lib.rb_rng_set_state(self._h, mt.ctypes.data, int(idx), int(dr)))
+
     def next_u64(self) -> int:
         v = C.c_uint64()
         check(lib.rb_rng_next_u64(self._h, C.byref(v)))
@@ -374,6 +386,22 @@ class ShardedReplayBuffer:
         h = C.c_void_p()
         check(lib.rb_load(text.encode(), int(max_tokens), int(device), C.byref(h)))
         return ShardedReplayBuffer(0, 0, _handle=h, max_tokens=max_tokens)
+
+    def snapshot(self, out=None):
+        """Binary checkpoint of the device state (rb_snapshot) into a new
+        numpy uint8 array, or into `out` (numpy or torch, host or device)."""
+        n = C.c_size_t()
+        check(lib.rb_snapshot(self._h, None, 0, C.byref(n)))
+        if out is None:
+            out = np.empty(n.value, np.uint8)
+        cap = out.nbytes if hasattr(out, "nbytes") else out.numel() * out.element_size()
+        check(lib.rb_snapshot(self._h, _ptr(out), cap, C.byref(n)))
+        return out
+
+    def restore(self, snap) -> None:
+        """Restore a buffer of the same shape from rb_snapshot bytes."""
+        cap = snap.nbytes if hasattr(snap, "nbytes") else snap.numel() * snap.element_size()
+        check(lib.rb_restore(self._h, _ptr(snap), cap))
 
     def check(self) -> None:
         check(lib.rb_check(self._h))
