@@ -388,11 +388,22 @@ def run_ours(args, rank, world, dist):
         "phases_ms": mean, "step_excludes": "synthetic trainer stand-in (logp_now), phases_ms.standin",
         "wall_ms_per_step_incl_standin": wall * 1e3 / K,
         "roofline": roof,
-        "gpu_launches": 8 * K,
+        "gpu_launches": launches_per_step(cfg, world) * K,
+        "gpu_launches_per_step": launches_per_step(cfg, world),
         "launch_mode": "cuda_graph (K steps captured once, launched once)" if use_graph else "eager",
         "clocks": clk.summary(),
     }
     return res, buf, wl, rng
+
+
+def launches_per_step(cfg, world):
+    """Library kernels of one timed step (the stand-in's kernels are not counted):
+    FIFO (ids promised unique): k_route_fifo, k_insert_payload_tma, k_sample_fused,
+    k_gather, loss; positive bias: k_insert_route, k_posbias_batch, k_insert_payload,
+    k_sample_fused, k_gather, loss; + k_stats_in/k_dlogp_rescale/k_stats_out
+    (rb_loss_finalize) per step on more than one rank."""
+    n = 5 if cfg["retention"] == "plain_fifo" else 6
+    return n + (3 if world > 1 else 0)
 
 
 def load_traffic(kernel):
