@@ -1438,12 +1438,8 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
 __device__ __forceinline__ bool last_to_finish(GridCtl* gc) {
     __shared__ int s_last;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&gc->done, 1u) == gridDim.x - 1;
-    }
+    if (threadIdx.x == 0) s_last = done_add_u32(&gc->done) == gridDim.x - 1;
     __syncthreads();
-    if (s_last) __threadfence();
     return s_last;
 }
 
@@ -1968,17 +1964,15 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
         int m = 0;
         for (int w = 0; w < RT_THREADS / 32; ++w) m = s_m[w] > m ? s_m[w] : m;
         gc->cta_max[blockIdx.x] = m;
-        __threadfence();
-        s_last = atomicAdd(&gc->done, 1u) == gridDim.x - 1;
+        s_last = done_add_u32(&gc->done) == gridDim.x - 1;
     }
     __syncthreads();
     RB_GCLOCK(63, blockIdx.x == 0);
     if (!s_last) return;
     RB_GCLOCK(56, true);
-    // last CTA: every CTA's records are written (each fenced before its done
-    // increment): the sampler's map may read the metadata now; the counters
-    // below are not read by it (it uses the insert's plan)
-    __threadfence();
+    // last CTA: every CTA's records are written (each released by its done
+    // increment, acquired by ours): the sampler's map may read the metadata
+    // now; the counters below are not read by it (it uses the insert's plan)
     if (tid == 0) st_release_i32(&pay_sync[1], 1);
     int m = 0;
     for (int c = tid; c < (int)gridDim.x; c += RT_THREADS) m = max(m, __ldcg(&gc->cta_max[c]));

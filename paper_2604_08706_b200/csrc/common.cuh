@@ -227,6 +227,21 @@ __device__ __forceinline__ int ld_acquire_i32(const int* p) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
     return x;
 }
+// Done counters of the multi-CTA kernels: one acq_rel atomic by thread 0
+// after a CTA barrier publishes the CTA's writes (release, cumulative over
+// the barrier) and, for the last CTA, acquires everyone else's — instead of
+// a sequentially consistent __threadfence() plus a relaxed atomic.
+__device__ __forceinline__ unsigned done_add_u32(unsigned* p) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned long long done_add_u64(unsigned long long* p) {
+    unsigned long long old;
+    asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], 1;" : "=l"(old) : "l"(p) : "memory");
+    return old;
+}
+
 // Programmatic dependent launch: let the next kernel of the stream (launched
 // with programmatic serialization) start while this one runs.
 __device__ __forceinline__ void pdl_trigger() {

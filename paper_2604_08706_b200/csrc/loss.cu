@@ -208,12 +208,10 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
             q.exc += s_exc[w];
         }
         parts[part_base + blockIdx.x] = q;
-        __threadfence();
-        s_last = atomicAdd(&acc->done_blocks, 1ULL) == (unsigned long long)nparts - 1;
+        s_last = done_add_u64(&acc->done_blocks) == (unsigned long long)nparts - 1;
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     double o = 0.0;
     long long inc = 0, exc = 0;
     for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
