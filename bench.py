@@ -42,6 +42,9 @@ CONFIGS = {
     "c3": dict(name="C3: buffer 1024, G=16, 64 prompts, ragged U{1..8192} tokens, 1 GPU, GRPO",
                capacity=1024, batch=1024, group=16, lmax=8192, ragged=True,
                retention="plain_fifo", delta=0.0, loss="grpo"),
+    "c3fixed": dict(name="C3 shape with fixed 4096-token responses (diagnostic)",
+                    capacity=1024, batch=1024, group=16, lmax=4096, ragged=False,
+                    retention="plain_fifo", delta=0.0, loss="grpo"),
     "c1": dict(name="C1: buffer 84, (W,T)=(5,3), G=8, 64 prompts, 1024 tokens, GRPO",
                capacity=84, batch=512, group=8, lmax=1024, ragged=False,
                retention="plain_fifo", delta=0.0, loss="grpo"),

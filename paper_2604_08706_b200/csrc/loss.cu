@@ -212,12 +212,29 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
     }
     __syncthreads();
     if (!s_last) return;
+    RB_GCLOCK(3, true);
     double o = 0.0;
     long long inc = 0, exc = 0;
-    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
-        o += __ldcg(&parts[i].obj);
-        inc += __ldcg(&parts[i].inc);
-        exc += __ldcg(&parts[i].exc);
+    // FB partials per thread per round, all loads in flight together; the
+    // order of the additions is fixed (bitwise-reproducible objective)
+    constexpr int FB = 8;
+    for (int base = threadIdx.x; base < nparts; base += FB * blockDim.x) {
+        double ob[FB];
+        long long ib[FB], eb[FB];
+#pragma unroll
+        for (int k = 0; k < FB; ++k) {
+            const int i = base + k * blockDim.x;
+            const bool ok = i < nparts;
+            ob[k] = ok ? __ldcg(&parts[i].obj) : 0.0;
+            ib[k] = ok ? __ldcg(&parts[i].inc) : 0;
+            eb[k] = ok ? __ldcg(&parts[i].exc) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < FB; ++k) {
+            o += ob[k];
+            inc += ib[k];
+            exc += eb[k];
+        }
     }
     o = warp_sum_f64(o);
     inc = warp_sum_i64(inc);
@@ -251,6 +268,7 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
             stats->total_tokens = acc->total_tokens;
         }
         s_last = acc->need_fixup && local_fix;
+        RB_GCLOCK(4, true);
     }
     __syncthreads();
     if (s_last) {  // rare: some ratio was non-finite
@@ -295,6 +313,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
     const float scale = -1.f / (float)acc->total_tokens;
     const float tol_hi = 4e-6f * prm.hi_f, tol_lo = 4e-6f * prm.lo_f;
     RB_TSTART(5);
+    RB_GCLOCK(0, blockIdx.x == 0);
     const int ups = (*maxq_p + QU - 1) / QU;
     const int nu = nloc * ups;
     GrpoPartial part;
@@ -384,8 +403,10 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
         part.obj += (double)fsum * A;
     }
     part.inc += inc_fast;
+    RB_GCLOCK(1, blockIdx.x == 0);
     RB_TEND(5);
     loss_commit(part, parts, acc, stats, 0, 0.0, dlogp, n_local, local_fix, part_base, nparts);
+    RB_GCLOCK(2, blockIdx.x == 0);
 }
 constexpr int LOSS_U = 4;
 
@@ -1049,6 +1070,16 @@ int rb_asymre_records(const double* logp_now, const double* reward, const double
 
 // Tuning aid (debug builds): the loss kernels' part of the kernel timeline
 // (each translation unit has its own copy of the timeline array).
+extern "C" __attribute__((visibility("default"))) int rb_debug_phase_clocks_loss(long long* out) {
+    return guard([&] {
+#ifdef RB_PHASE_CLOCKS
+        RB_CUDA(cudaDeviceSynchronize());
+        RB_CUDA(cudaMemcpyFromSymbol(out, g_phase_clock, 64 * sizeof(long long)));
+#else
+        for (int i = 0; i < 64; ++i) out[i] = 0;
+#endif
+    });
+}
 extern "C" __attribute__((visibility("default"))) int rb_debug_timeline_loss(unsigned long long* out,
                                                                              int reset) {
     return guard([&] {
