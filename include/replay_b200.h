@@ -256,6 +256,26 @@ int rb_load(const char* text, int32_t max_tokens, int device, rb_buffer** out);
 int rb_snapshot(rb_buffer* b, void* dst, size_t cap, size_t* len);
 int rb_restore(rb_buffer* b, const void* src, size_t len);
 
+/* ======================================================================
+ * TransferQueue — replaces replab::TransferQueue (transfer_queue.hpp:12-35,
+ * transfer_queue.cpp:1-50), the consume-once LIFO of the no-buffer
+ * baseline, with the token payload kept in HBM next to the records.
+ * ==================================================================== */
+typedef struct rb_queue rb_queue;
+/* capacity 0 = unbounded (the reference's nullopt; device storage grows). */
+int rb_queue_create(size_t capacity, int32_t max_tokens, int device, rb_queue** out);
+void rb_queue_destroy(rb_queue* q);
+/* push_group (transfer_queue.cpp:22-29): all or nothing; *accepted = 0 when
+ * the group does not fit (back-pressure, nothing enqueued).  A single push is
+ * a group of one (13-20).  Advantages: given, or per group on the device. */
+int rb_queue_push_group(rb_queue* q, const rb_insert_batch* batch, int* accepted);
+/* k pops (31-39): up to k most recent records, most recent first; optional
+ * packed payload + offsets (host or device).  *n_popped = 0: empty queue. */
+int rb_queue_pop(rb_queue* q, size_t k, rb_record* out_records, size_t* n_popped,
+                 int32_t* out_tokens, float* out_logp_old, int64_t* out_offsets);
+int rb_queue_size(const rb_queue* q, size_t* out);                       /* 41-44 */
+int rb_queue_capacity(const rb_queue* q, size_t* capacity, int* bounded); /* hpp:31 */
+
 /* Sticky asynchronous error check (synchronises the stream). */
 int rb_check(rb_buffer* b);
 int rb_synchronize(rb_buffer* b);

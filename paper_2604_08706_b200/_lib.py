@@ -106,6 +106,12 @@ def _load():
         "rb_restore": (ip, [vp, vp, sz]),
         "rb_rng_get_state": (ip, [vp, vp, vp, vp]),
         "rb_rng_set_state": (ip, [vp, vp, C.c_uint32, u64]),
+        "rb_queue_create": (ip, [sz, i32, ip, vp]),
+        "rb_queue_destroy": (None, [vp]),
+        "rb_queue_push_group": (ip, [vp, vp, vp]),
+        "rb_queue_pop": (ip, [vp, sz, vp, vp, vp, vp, vp]),
+        "rb_queue_size": (ip, [vp, vp]),
+        "rb_queue_capacity": (ip, [vp, vp, vp]),
         "rb_check": (ip, [vp]),
         "rb_synchronize": (ip, [vp]),
         "rb_group_advantages": (ip, [vp, vp, sz, vp, vp]),

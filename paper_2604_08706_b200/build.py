@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libreplay_b200.so")
-SOURCES = ["rng.cu", "buffer.cu", "loss.cu"]
-HEADERS = ["common.cuh", "rng_internal.cuh", "buffer_internal.cuh"]
+SOURCES = ["rng.cu", "buffer.cu", "loss.cu", "queue.cu"]
+HEADERS = ["common.cuh", "rng_internal.cuh", "buffer_internal.cuh", "stream_copy.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -464,3 +464,92 @@ def asymre_records(logp_now, reward, group_mean, delta_v=-0.1, out=None):
     check(lib.rb_asymre_records(_ptr(lpn), _ptr(r), _ptr(g), int(lpn.shape[0]), delta_v,
                                 _ptr(out), C.byref(st)))
     return out, st
+
+
+# ---------------------------------------------------------------------------
+class TransferQueue:
+    """replab::TransferQueue (transfer_queue.hpp:12-35) on the GPU: a
+    consume-once LIFO hand-off whose records and token payload stay in HBM.
+    capacity=None is the reference's unbounded queue."""
+
+    def __init__(self, capacity: Optional[int] = None, max_tokens: int = 0, device: int = -1):
+        if capacity is not None and capacity <= 0:
+            raise ValueError("TransferQueue: capacity must be positive")  # transfer_queue.cpp:8-10
+        h = C.c_void_p()
+        check(lib.rb_queue_create(int(capacity or 0), int(max_tokens), int(device), C.byref(h)))
+        self._h = h
+        self._cap = capacity
+        self.max_tokens = max_tokens
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.rb_queue_destroy(self._h)
+            self._h = None
+
+    def capacity(self) -> Optional[int]:
+        return self._cap
+
+    def size(self) -> int:
+        v = C.c_size_t()
+        check(lib.rb_queue_size(self._h, C.byref(v)))
+        return v.value
+
+    def push_group(self, records, tok_offsets=None, tokens=None, logp_old=None,
+                   group_offsets=None) -> bool:
+        """All or nothing (transfer_queue.cpp:22-29).  `records`: RECORD_DTYPE
+        array (advantages as given), or None with the SoA keyword form of
+        ShardedReplayBuffer.insert passed through `group_offsets`."""
+        recs = np.ascontiguousarray(np.atleast_1d(_records_from(records)))
+        keep = []
+
+        def col(name, dt):
+            a = np.ascontiguousarray(recs[name].astype(dt))
+            keep.append(a)
+            return a.ctypes.data
+
+        bt = InsertBatch()
+        bt.n = recs.shape[0]
+        bt.rollout_id = col("rollout_id", np.uint64)
+        bt.prompt_id = col("prompt_id", np.uint64)
+        bt.group_id = col("group_id", np.uint64)
+        bt.creation_step = col("creation_step", np.int64)
+        bt.policy_version = col("policy_version", np.int64)
+        bt.reward = col("reward", np.float64)
+        bt.is_correct = col("is_correct", np.uint8)
+        bt.behavior_logprob = col("behavior_logprob", np.float64)
+        if group_offsets is None:
+            bt.advantage = col("advantage", np.float64)
+        else:
+            go = _arr(group_offsets, np.int64)
+            keep.append(go)
+            bt.group_offsets = _ptr(go)
+            bt.n_groups = int(go.shape[0]) - 1
+        for name, x, dt in (("tok_offsets", tok_offsets, np.int64), ("tokens", tokens, np.int32),
+                            ("logp_old", logp_old, np.float32)):
+            y = _arr(x, dt)
+            keep.append(y)
+            setattr(bt, name, _ptr(y))
+        ok = C.c_int()
+        check(lib.rb_queue_push_group(self._h, C.byref(bt), C.byref(ok)))
+        return bool(ok.value)
+
+    def push(self, record, tokens=None, logp_old=None) -> bool:
+        """transfer_queue.cpp:13-20 (a group of one)."""
+        toff = None
+        if tokens is not None or logp_old is not None:
+            n = len(tokens if tokens is not None else logp_old)
+            toff = np.array([0, n], np.int64)
+        return self.push_group(record, toff, tokens, logp_old)
+
+    def pop(self):
+        """transfer_queue.cpp:31-39: the most recent record, or None."""
+        r = self.pop_batch(1)[0]
+        return r[0] if len(r) else None
+
+    def pop_batch(self, k: int, out_tokens=None, out_logp_old=None, out_offsets=None):
+        """k pops, most recent first; optional packed payload (+ offsets)."""
+        out = np.zeros(k, RECORD_DTYPE)
+        n = C.c_size_t()
+        check(lib.rb_queue_pop(self._h, k, out.ctypes.data, C.byref(n), _ptr(out_tokens),
+                               _ptr(out_logp_old), _ptr(out_offsets)))
+        return out[: n.value], n.value

@@ -1,4 +1,4 @@
-"""The reference's OWN test suites (test_buffer_core.cpp, test_rng.cpp),
+"""The reference's OWN test suites (test_buffer_core.cpp, test_rng.cpp, test_queue.cpp),
 compiled unchanged from /root/reference/proj/tests by oracle/Makefile with
 the doctest shim (tests/doctest_shim) against
   * the unmodified reference library  (*_ref: pins the shim), and
@@ -24,7 +24,7 @@ def run(name):
     return summary[-1]
 
 
-@pytest.mark.parametrize("suite", ["test_buffer_core", "test_rng"])
+@pytest.mark.parametrize("suite", ["test_buffer_core", "test_rng", "test_queue"])
 def test_reference_suite_against_reference(suite):
     run(f"{suite}_ref")
 
@@ -38,3 +38,9 @@ def test_reference_rng_suite_against_facade_host_draws():
 def test_reference_buffer_suite_against_b200_facade():
     """All 20 cases of test_buffer_core.cpp pass against the GPU buffer."""
     run("test_buffer_core_b200")
+
+
+@pytest.mark.gpu
+def test_reference_queue_suite_against_b200_facade():
+    """All 6 cases of test_queue.cpp (transfer_queue.hpp) pass against the GPU queue."""
+    run("test_queue_b200")
