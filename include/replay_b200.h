@@ -246,6 +246,20 @@ int rb_route_cursor(rb_buffer* b, size_t* out);
 int rb_dump(rb_buffer* b, char* out, size_t cap, size_t* len);
 int rb_load(const char* text, int32_t max_tokens, int device, rb_buffer** out);
 
+/* Replay diagnostics on the device (the reference derives
+ * them from the UseEvent ledger on the host, metrics.cpp:37-44, 123-131,
+ * 185-202).  Integer-valued metrics as histograms of bins 0..max_bin (the last
+ * bin counts every value >= max_bin), from which the reference's summarize()
+ * (mean, nearest-rank quartiles) follows exactly while no value reaches
+ * max_bin:
+ *   rb_batch_staleness_hist — staleness(e) = use_step - creation_step of
+ *     every selection of the current batch (metrics.cpp:37-39);
+ *   rb_use_count_hist       — use counts of the resident records (replay
+ *     counts so far, replay_buffer.cpp:201). */
+int rb_batch_staleness_hist(rb_buffer* b, int64_t use_step, int32_t max_bin, uint64_t* hist,
+                            int64_t* sum);
+int rb_use_count_hist(rb_buffer* b, int32_t max_bin, uint64_t* hist, uint64_t* sum);
+
 /* Binary checkpoint of the whole device state — metadata columns, arrival
  * structures (positive-bias queues), owned token payload rows, route cursor,
  * per-shard push counts — for run resumption (the

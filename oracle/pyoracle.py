@@ -337,6 +337,7 @@ class Reference:
         L.ref_rng_swor.argtypes = [vp, u64, u64, vp]
         L.ref_hash_name.restype = u64
         L.ref_hash_name.argtypes = [C.c_char_p]
+        L.ref_summarize.argtypes = [vp, u64, vp, vp, vp, u64, vp]
         L.ref_buf_new.restype = vp
         L.ref_buf_new.argtypes = [u64, u64, C.c_int, C.c_int, dbl]
         L.ref_buf_free.argtypes = [vp]
@@ -371,6 +372,20 @@ class Reference:
         if self.lib.ref_group_advantages(_p(r), r.size, _p(out)):
             raise self.err()
         return out
+
+    def summarize(self, values):
+        """The reference's summarize() (metrics.cpp:185-202) as a dict."""
+        v = np.ascontiguousarray(values, np.float64)
+        out = np.zeros(5)
+        cap = 4096
+        keys = np.zeros(cap, np.int64)
+        cnt = np.zeros(cap, np.uint64)
+        hn = C.c_uint64()
+        if self.lib.ref_summarize(_p(v), v.size, _p(out), _p(keys), _p(cnt), cap, C.byref(hn)):
+            raise self.err()
+        n = min(hn.value, cap)
+        return {"count": int(out[0]), "mean": out[1], "q25": out[2], "median": out[3],
+                "q75": out[4], "histogram": {int(k): int(c) for k, c in zip(keys[:n], cnt[:n])}}
 
     def loss_records(self, kind, logp_want, recs, group_mean=None, eps_low=0.2, eps_high=0.2,
                      delta_v=-0.1):

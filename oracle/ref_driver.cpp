@@ -154,6 +154,29 @@ void* ref_buf_load(const char* text) {
     return st == 0 ? out : nullptr;
 }
 
+// ---- metrics ------------------------------------------------------------
+// The reference's summarize() (metrics.cpp:185-202): out = {count, mean,
+// q25, median, q75}; the histogram goes to (hist_keys, hist_counts), up to
+// hist_cap entries, *hist_n = its size.
+int ref_summarize(const double* v, uint64_t n, double* out, int64_t* hist_keys,
+                  uint64_t* hist_counts, uint64_t hist_cap, uint64_t* hist_n) {
+    return guard([&] {
+        const MetricSummary s = summarize(std::vector<double>(v, v + n));
+        out[0] = (double)s.count;
+        out[1] = s.mean;
+        out[2] = s.q25;
+        out[3] = s.median;
+        out[4] = s.q75;
+        *hist_n = s.histogram.size();
+        uint64_t i = 0;
+        for (const auto& kv : s.histogram) {
+            if (i == hist_cap) break;
+            hist_keys[i] = kv.first;
+            hist_counts[i++] = kv.second;
+        }
+    });
+}
+
 // ---- advantages and losses ---------------------------------------------
 int ref_group_advantages(const double* r, uint64_t n, double* out) {
     return guard([&] {

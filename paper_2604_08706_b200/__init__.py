@@ -8,8 +8,9 @@ over that ABI; there is no CPU fallback.
 """
 from .replay import (EVENT_DTYPE, NONE_ID, RECORD_DTYPE, Rng, ShardedReplayBuffer, TransferQueue,
                      asymre_records,
-                     asymre_tokens, group_advantages, grpo_records, grpo_tokens, hash_name)
+                     asymre_tokens, group_advantages, grpo_records, grpo_tokens, hash_name,
+                     summarize_hist)
 
 __all__ = ["Rng", "ShardedReplayBuffer", "TransferQueue", "group_advantages", "grpo_tokens", "grpo_records",
            "asymre_tokens", "asymre_records", "hash_name", "RECORD_DTYPE", "EVENT_DTYPE",
-           "NONE_ID"]
+           "NONE_ID", "summarize_hist"]

@@ -102,6 +102,8 @@ def _load():
         "rb_route_cursor": (ip, [vp, vp]),
         "rb_dump": (ip, [vp, C.c_char_p, sz, vp]),
         "rb_load": (ip, [C.c_char_p, i32, ip, vp]),
+        "rb_batch_staleness_hist": (ip, [vp, i64, i32, vp, vp]),
+        "rb_use_count_hist": (ip, [vp, i32, vp, vp]),
         "rb_snapshot": (ip, [vp, vp, sz, vp]),
         "rb_restore": (ip, [vp, vp, sz]),
         "rb_rng_get_state": (ip, [vp, vp, vp, vp]),

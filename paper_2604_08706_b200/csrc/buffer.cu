@@ -3127,6 +3127,69 @@ int rb_route_cursor(rb_buffer* b, size_t* out) {
 }
 
 namespace {
+// ---- replay diagnostics ------------------------------------------------------
+// Histogram of integer values (shared-memory bins, one global atomic per bin
+// per CTA) and their sum.
+__global__ void k_hist_staleness(const BufView v, const int32_t* sel_slot, long long n,
+                                 long long use_step, int max_bin, unsigned long long* hist,
+                                 long long* sum) {
+    extern __shared__ unsigned long long sh[];
+    for (int i = threadIdx.x; i <= max_bin; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    long long s = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long st = use_step - v.cstep[sel_slot[i]];  // metrics.cpp:37-39
+        s += st;
+        const long long b = st < 0 ? 0 : (st > max_bin ? max_bin : st);
+        atomicAdd(&sh[b], 1ULL);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i <= max_bin; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+    s = warp_sum_i64(s);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd((unsigned long long*)sum, (unsigned long long)s);
+}
+__global__ void k_hist_use(const BufView v, int max_bin, unsigned long long* hist,
+                           unsigned long long* sum) {
+    extern __shared__ unsigned long long sh[];
+    for (int i = threadIdx.x; i <= max_bin; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    unsigned long long s = 0;
+    const long long N = (long long)v.T * v.C;
+    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+         g += (long long)gridDim.x * blockDim.x) {
+        const int sh_ = (int)(g / v.C), x = (int)(g % v.C);
+        if (x >= occupancy(v, sh_)) continue;  // resident slots only
+        const unsigned u = v.use[g];
+        s += u;
+        atomicAdd(&sh[u > (unsigned)max_bin ? max_bin : u], 1ULL);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i <= max_bin; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+    s = (unsigned long long)warp_sum_i64((long long)s);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(sum, s);
+}
+}  // namespace
+}  // extern "C"
+namespace {
+template <class T, class F>
+void run_hist(rb_buffer* b, int32_t max_bin, uint64_t* hist, T* sum, F launch) {
+    if (max_bin < 0 || max_bin > 4095) invalid("histogram: max_bin must be in [0, 4095]");
+    const size_t hb = ((size_t)max_bin + 1) * 8;
+    char* d = (char*)b->scratch(hb + 16);
+    RB_CUDA(cudaMemsetAsync(d, 0, hb + 16, b->stream));
+    launch((unsigned long long*)d, (T*)(d + hb), (size_t)hb);
+    RB_CUDA(cudaGetLastError());
+    RB_CUDA(cudaMemcpyAsync(hist, d, hb, cudaMemcpyDefault, b->stream));
+    if (sum) RB_CUDA(cudaMemcpyAsync(sum, d + hb, sizeof(T), cudaMemcpyDefault, b->stream));
+    b->sync();
+}
+}  // namespace
+extern "C" {
+namespace {
+
 // ---- binary snapshot (rb_snapshot / rb_restore) ---------------------------
 struct SnapHeader {
     char magic[8];  // "RBSNAP01"
@@ -3175,6 +3238,32 @@ SnapHeader snap_header(rb_buffer* b, size_t nsec) {
     return h;
 }
 }  // namespace
+
+int rb_batch_staleness_hist(rb_buffer* b, int64_t use_step, int32_t max_bin, uint64_t* hist,
+                            int64_t* sum) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        b->other_work();
+        run_hist(b, max_bin, hist, sum, [&](unsigned long long* h, int64_t* sm, size_t hb) {
+            if (b->B)
+                k_hist_staleness<<<std::max<unsigned>(1, std::min<unsigned>((unsigned)((b->B + 255) / 256), 148)),
+                                   256, hb, b->stream>>>(b->v, b->sel_slot, (long long)b->B,
+                                                         (long long)use_step, max_bin, h,
+                                                         (long long*)sm);
+        });
+    });
+}
+
+int rb_use_count_hist(rb_buffer* b, int32_t max_bin, uint64_t* hist, uint64_t* sum) {
+    return guard([&] {
+        DeviceScope ds(b->device);
+        b->other_work();
+        run_hist(b, max_bin, hist, sum, [&](unsigned long long* h, uint64_t* sm, size_t hb) {
+            k_hist_use<<<std::max<unsigned>(1, std::min<unsigned>((unsigned)((b->N + 255) / 256), 148)),
+                         256, hb, b->stream>>>(b->v, max_bin, h, (unsigned long long*)sm);
+        });
+    });
+}
 
 int rb_snapshot(rb_buffer* b, void* dst, size_t cap, size_t* len) {
     return guard([&] {

@@ -387,6 +387,22 @@ class ShardedReplayBuffer:
         check(lib.rb_load(text.encode(), int(max_tokens), int(device), C.byref(h)))
         return ShardedReplayBuffer(0, 0, _handle=h, max_tokens=max_tokens)
 
+    def staleness_hist(self, use_step: int, max_bin: int = 255):
+        """Histogram (bins 0..max_bin, last = overflow) and sum of the current
+        batch's staleness use_step - creation_step (metrics.cpp:37-39)."""
+        h = np.zeros(max_bin + 1, np.uint64)
+        sm = C.c_int64()
+        check(lib.rb_batch_staleness_hist(self._h, int(use_step), int(max_bin), h.ctypes.data,
+                                          C.byref(sm)))
+        return h, sm.value
+
+    def use_count_hist(self, max_bin: int = 255):
+        """Histogram and sum of the resident records' use counts."""
+        h = np.zeros(max_bin + 1, np.uint64)
+        sm = C.c_uint64()
+        check(lib.rb_use_count_hist(self._h, int(max_bin), h.ctypes.data, C.byref(sm)))
+        return h, sm.value
+
     def snapshot(self, out=None):
         """Binary checkpoint of the device state (rb_snapshot) into a new
         numpy uint8 array, or into `out` (numpy or torch, host or device)."""
@@ -553,3 +569,23 @@ class TransferQueue:
         check(lib.rb_queue_pop(self._h, k, out.ctypes.data, C.byref(n), _ptr(out_tokens),
                                _ptr(out_logp_old), _ptr(out_offsets)))
         return out[: n.value], n.value
+
+
+def summarize_hist(hist, total_sum=None):
+    """The reference's summarize() (metrics.cpp:185-202: mean, nearest-rank
+    quartiles, histogram) from an integer-valued histogram — exact while the
+    last (overflow) bin is empty."""
+    hist = np.asarray(hist, np.uint64)
+    n = int(hist.sum())
+    if n == 0:
+        raise ValueError("summarize requires at least one value")
+    cdf = np.cumsum(hist)
+
+    def rank(q):  # value at rank ceil(q * n), 1-indexed (metrics.cpp:174-181)
+        r = min(max(int(np.ceil(q * n)), 1), n)
+        return float(np.searchsorted(cdf, r))
+
+    mean = (float(total_sum) if total_sum is not None
+            else float((np.arange(hist.size) * hist).sum())) / n
+    return {"count": n, "mean": mean, "q25": rank(0.25), "median": rank(0.5), "q75": rank(0.75),
+            "histogram": {int(i): int(c) for i, c in enumerate(hist) if c}}
