@@ -88,6 +88,9 @@ struct InsertIn {
     const int64_t* goff;
     long long ngroups;
     const int64_t* toff;  // n+1 payload offsets (may be NULL: length 0)
+    int64_t* toff_keep;   // closed-form route: copy of toff for a sampler that overlaps it
+    int pay_follows;      // closed-form route: the payload copy is launched next
+    unsigned long long* keep_cnt;  // route CTAs that finished their toff_keep slice (monotonic)
     int32_t maxlen;
     int32_t* len;         // scratch: per-record length
     double *adv_out, *gmean_out;
@@ -804,6 +807,17 @@ __device__ __forceinline__ Unit fifo_unit(const BufView& v, const FifoPlan& p,
     return d;
 }
 
+// Completion flag of the closed-form payload copy for the early gather:
+// sync[2] = 1 while the copy runs (set by the route kernel before any
+// dependent can launch), cleared by the last CTA to finish (sync[3] counts
+// them).
+__device__ __forceinline__ void payload_pending_end(int* sync) {  // thread 0, CTA's stores done
+    if (done_add_u32(reinterpret_cast<unsigned*>(&sync[3])) == gridDim.x - 1) {
+        sync[3] = 0;
+        st_release_i32(&sync[2], 0);
+    }
+}
+
 template <int U, bool CLOSED>
 __device__ __forceinline__ void payload_body(const BufView& v, const Unit* desc, const FifoPlan& p,
                                              const int64_t* toff, int ups, int n,
@@ -859,8 +873,12 @@ __device__ __forceinline__ void payload_body(const BufView& v, const Unit* desc,
             }
         }
     }
-    // completion of this copy implies completion of the route before it
-    if (CLOSED) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (CLOSED) {
+        __syncthreads();
+        if (threadIdx.x == 0) payload_pending_end(sync);
+        // completion of this copy implies completion of the route before it
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
 }
 template <int U>
 __global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload(BufView v, const Unit* desc,
@@ -1066,7 +1084,11 @@ __global__ void __launch_bounds__(TP_THREADS) k_insert_payload_tma(BufView v, Fi
         }
         __syncthreads();
     }
-    if (tid == 0) bulk_wait_all();
+    if (tid == 0) {
+        bulk_wait_all();  // this CTA's row writes are complete
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        payload_pending_end(sync);
+    }
     RB_TEND(1);
     // completion of this copy implies completion of the route before it
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1088,6 +1110,7 @@ struct SampleArgs {
     Unit* units;
     int* n_units;
     PendingIns pend;          // a closed-form FIFO insert that may still be running
+    int early;                // publish the early-gather flags (seg, fin)
     long long occ[64];        // per-shard occupancy after the preceding inserts (draws)
     const long long* occ_dev;  // the same for more than 64 shards (device), else NULL
 };
@@ -1137,6 +1160,13 @@ struct GridCtl {
     long long gen_hi;                   // fused sampler: last ring block after the generator
     unsigned long long word[GRID_MAX_CTAS];  // look-back: status (2 bits) | value (62 bits)
     int cta_max[GRID_MAX_CTAS];
+    // fused sampler -> early gather (k_gather_early): per map CTA, 0 = not
+    // mapped yet, 1 = its units are final, 2 = a rejected draw at or before
+    // it (final only once `fin` is set); fin = the last CTA has finalised
+    int seg[GRID_MAX_CTAS];
+    int fin;
+    unsigned gwork, gdone;  // early gather: unit claim counter, done counter
+    unsigned long long keep_cnt;  // route: CTAs that copied their offsets slice (monotonic)
 };
 constexpr unsigned long long LB_AGG = 1ULL << 62, LB_INC = 2ULL << 62,
                              LB_VAL = (1ULL << 62) - 1;
@@ -1312,6 +1342,11 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
         }
     }
     RB_GCLOCK(46 + 8 * (t & 1), t < 2);
+    if (pi.pending && pi.toff) {  // the route kernel's copy of the insert's offsets
+        if (tid == 0)
+            while (ld_acquire_u64(pi.keep_cnt) < pi.keep_target) __nanosleep(32);
+        __syncthreads();
+    }
     int lv[MAP_R];
     double av[MAP_R];
     long long t0[MAP_R], t1[MAP_R];
@@ -1368,6 +1403,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
     if (s_excl & LB_REJ) {  // a rejection at or before this CTA: the last CTA replays
         if (tid == 0) atomicMin(&gc->first_rej, t);
         if (tid == 0) gc->cta_max[t] = 0;
+        if (a.early && tid == 0) st_release_i32(&gc->seg[t], 2);
         return;
     }
     if (tid == 0) {
@@ -1392,7 +1428,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
         Unit d;
         d.row = (sh[r] - v.sb) * v.C + (g[r] - sh[r] * v.C);
         d.len = L[r];
-        d.k0 = 0;
+        d.k0 = nw[r] ? 1 : 0;  // a record of the pending insert (its row may still be copied)
         d.g = g[r];
         d.off = pos;
         d.adv = av[r];  // new records: patched below once the route kernel wrote it
@@ -1413,7 +1449,9 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
         else atomicAdd(&v.use[g[r]], 1u);
     }
     // ... and its own records once the route kernel has written them
-    if (__syncthreads_or(any_new)) {
+    const bool cta_new = __syncthreads_or(any_new);
+    if (DRAW && a.early && tid == 0) st_release_i32(&gc->seg[t], 1);  // this CTA's units are final
+    if (cta_new) {
         if (tid == 0) spin_until_set(route_done);
         __syncthreads();
         double adv[MAP_R];
@@ -1472,7 +1510,7 @@ __device__ __noinline__ void draw_exact(int32_t* sel_shard, int64_t* sel_index, 
 // loss-accumulator reset, control reset; the new ring position when drawing.
 template <bool DRAW>
 __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc, int nmap,
-                             const DrawCtx& dc, MtRing* r) {
+                             const DrawCtx& dc, MtRing* r, const int* route_done) {
     __shared__ int s_m[32];
     __shared__ uint64_t mt[MT_N];
     __shared__ long long s_q;
@@ -1505,7 +1543,8 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
         __syncthreads();
         // map the replayed tail, then rescan every owned offset (shard heads
         // from the insert's plan: the route kernel may still be advancing
-        // the device counters)
+        // the device counters; the metadata it writes is read below)
+        if (threadIdx.x == 0 && a.pend.pending) spin_while_eq(route_done, 0);
         __shared__ int s_head[MAP_NSH];
         for (int s = threadIdx.x; s < a.nsh && s < MAP_NSH; s += blockDim.x)
             s_head[s] = head_after(v, a.pend, s);
@@ -1614,6 +1653,10 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
         for (int i = threadIdx.x; i < MT_N; i += blockDim.x) dst[i] = mt[i];
     }
     for (int c = threadIdx.x; c < nmap; c += blockDim.x) gc->word[c] = 0;
+    if (DRAW && a.early) {
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_i32(&gc->fin, 1);  // every unit is final
+    }
 }
 
 // Map phase after k_sample_without (selections already drawn).
@@ -1625,7 +1668,7 @@ __global__ void __launch_bounds__(MAP_THREADS) k_sample_map(BufView v, SampleArg
     __syncthreads();
     const DrawCtx dc{};
     map_cta<false>(v, a, gc, s_t, dc, route_done);
-    if (last_to_finish(gc)) map_finalize<false>(v, a, gc, (int)gridDim.x, dc, nullptr);
+    if (last_to_finish(gc)) map_finalize<false>(v, a, gc, (int)gridDim.x, dc, nullptr, route_done);
     RB_TEND(3);
 }
 
@@ -1660,6 +1703,9 @@ __device__ void gen_role(MtRing* r, const SampleArgs& a, GridCtl* gc) {
 __global__ void __launch_bounds__(MAP_THREADS, 4) k_sample_fused(BufView v, MtRing* r, SampleArgs a,
                                                                  GridCtl* gc, const int* route_done) {
     __shared__ int s_t;
+    // the early-gather flags (seg, fin) start clear: reset by the early
+    // gather that consumed them, or by the host before this launch
+    pdl_trigger();  // the early gather may launch (it waits for the flags)
     if (threadIdx.x == 0) s_t = (int)atomicAdd(&gc->ticket, 1u);
     const DrawCtx dc{r, r->q_state, r->q_hi, r->idx};
     __syncthreads();
@@ -1676,7 +1722,7 @@ __global__ void __launch_bounds__(MAP_THREADS, 4) k_sample_fused(BufView v, MtRi
     }
     if (last_to_finish(gc)) {
         RB_GCLOCK(58, true);
-        map_finalize<true>(v, a, gc, (int)gridDim.x - 1, dc, r);
+        map_finalize<true>(v, a, gc, (int)gridDim.x - 1, dc, r, route_done);
         RB_GCLOCK(59, true);
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1826,9 +1872,24 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     if (blockIdx.x == 0 && tid == 0) {  // this insert's verdict / completion flags
         st_release_i32(&pay_sync[0], 0);
         st_release_i32(&pay_sync[1], 0);
+        if (in.pay_follows) st_release_i32(&pay_sync[2], 1);  // the copy's completion flag
+        fence_gpu();  // performed before any dependent can launch
     }
     __syncthreads();
     pdl_trigger();  // the closed-form payload copy may start now (it waits for pay_sync[0])
+    // the route proper runs on the first nrt CTAs
+    const unsigned nrt = gridDim.x - (in.toff_keep ? 1u : 0u);
+    if (blockIdx.x == nrt) {
+        // Extra CTA: the caller may reuse its offsets as soon as later stream
+        // work runs, but an overlapping sampler reads the new records'
+        // lengths after this call: keep a copy, published by a monotonic
+        // counter (the sampler waits for its target).
+        for (int i = tid; i <= n; i += RT_THREADS) in.toff_keep[i] = in.toff[i];
+        __syncthreads();
+        if (tid == 0)
+            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(in.keep_cnt) : "memory");
+        return;
+    }
     const int sticky = ctl->err_code;
     const unsigned long long cur0 = ctl->cursor;
     const int has_any = ctl->has_any;
@@ -1898,6 +1959,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
         int32_t slot = -1;
         uint8_t surv = 0;
         uint64_t ev = NONE_ID;
+        bool ev_by_survivor = false;
         Unit d;
         d.row = -1;
         d.len = (int32_t)(len < 0 ? 0 : len);
@@ -1916,7 +1978,17 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
             const size_t g = (size_t)s * C + (size_t)x2;
             slot = (int32_t)g;
             surv = rank + C >= ns;
+            // The id a push evicts: an earlier record of this batch, or the
+            // slot's resident one.  A slot pushed again later in this batch
+            // is overwritten by its survivor (another CTA): that survivor
+            // reports the resident id for the slot's first push instead
+            // (read before its own write, same thread).
             if (P + rank >= C) ev = rank >= C ? in.id[j - C * T] : v.id[g];
+            if (rank < C && !surv) ev_by_survivor = true;
+            if (surv && rank >= C) {
+                const int r0 = rank % C;
+                in.evid[r0 * T + j0] = P + r0 >= C ? v.id[g] : NONE_ID;
+            }
             if (!in.adv) {
                 long long lo = 0, hi = ng;  // group gi: goff[gi] <= j < goff[gi+1]
                 while (hi - lo > 1) {
@@ -1951,7 +2023,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
         in.len[j] = (int32_t)(len < 0 ? 0 : len);
         in.tslot[j] = slot;
         in.surv[j] = surv;
-        in.evid[j] = ev;
+        if (!ev_by_survivor) in.evid[j] = ev;
         in.adv_out[j] = adv;
         in.gmean_out[j] = gmean;
         in.units[j] = d;
@@ -1964,7 +2036,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
         int m = 0;
         for (int w = 0; w < RT_THREADS / 32; ++w) m = s_m[w] > m ? s_m[w] : m;
         gc->cta_max[blockIdx.x] = m;
-        s_last = done_add_u32(&gc->done) == gridDim.x - 1;
+        s_last = done_add_u32(&gc->done) == nrt - 1;
     }
     __syncthreads();
     RB_GCLOCK(63, blockIdx.x == 0);
@@ -1975,7 +2047,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     // now; the counters below are not read by it (it uses the insert's plan)
     if (tid == 0) st_release_i32(&pay_sync[1], 1);
     int m = 0;
-    for (int c = tid; c < (int)gridDim.x; c += RT_THREADS) m = max(m, __ldcg(&gc->cta_max[c]));
+    for (int c = tid; c < (int)nrt; c += RT_THREADS) m = max(m, __ldcg(&gc->cta_max[c]));
     m = __reduce_max_sync(0xffffffffu, m);
     if ((tid & 31) == 0) s_m[tid >> 5] = m;
     if (!bb)
@@ -2083,6 +2155,190 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* 
     RB_TEND(4);
 }
 constexpr int GATHER_U = 4;
+
+// ---- early gather: a programmatic dependent of the fused sampler, which is
+// itself a dependent of the insert's payload copy.  It starts while the copy
+// and the sampler run: a unit (QU quads of one selection) is claimed from a
+// counter and copied as soon as its map CTA has published its descriptors
+// (gc->seg), so the gather of the records that were already resident overlaps
+// the insert.  Units of the pending insert's records wait for the copy's
+// completion flag (pay_sync[2]); units behind a rejected draw wait for the
+// sampler's exact replay (gc->fin).  Deferred units are kept in shared memory
+// and copied as soon as their condition holds.  Rows written by the
+// concurrent copy are read through L2 (ld.cg), never the non-coherent path.
+__device__ __forceinline__ Unit ld_unit_cg(const Unit* u) {
+    const uint4 a = __ldcg(reinterpret_cast<const uint4*>(u));
+    const uint4 b = __ldcg(reinterpret_cast<const uint4*>(u) + 1);
+    Unit r;
+    r.row = (int32_t)a.x;
+    r.len = (int32_t)a.y;
+    r.k0 = (int32_t)a.z;
+    r.g = (int32_t)a.w;
+    r.off = (int64_t)(((uint64_t)b.y << 32) | b.x);
+    r.adv = __hiloint2double((int)b.w, (int)b.z);
+    return r;
+}
+template <int U, bool CG>
+__device__ __forceinline__ void row_to_packed_quads_l2(const uint4* rowq, int nsq, int a, int kw,
+                                                       uint4 (&o)[U]) {
+    if (!CG) {
+        row_to_packed_quads<U>(rowq, nsq, a, kw, o);
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    uint4 cur[U];
+#pragma unroll
+    for (int s = 0; s < U; ++s) {
+        const int k = kw + 32 * s + lane;
+        cur[s] = (k >= 0 && k < nsq) ? __ldcg(rowq + k) : make_uint4(0, 0, 0, 0);
+    }
+    if (a == 0) {
+#pragma unroll
+        for (int s = 0; s < U; ++s) o[s] = cur[s];
+        return;
+    }
+    uint4 first_prev = make_uint4(0, 0, 0, 0);
+    if (lane == 0 && kw >= 1 && kw - 1 < nsq) first_prev = __ldcg(rowq + kw - 1);
+#pragma unroll
+    for (int s = 0; s < U; ++s) {
+        uint4 prev = shfl_up4(cur[s]);
+        const uint4 carry = s ? shfl4(cur[s > 0 ? s - 1 : 0], 31) : first_prev;
+        if (lane == 0) prev = carry;
+        o[s] = funnel(prev, cur[s], 4 - a);
+    }
+}
+// Chunk c of a selection's destination quads: [c*QU, (c+1)*QU), the last
+// chunk (c == ups-1) running to the end.
+template <int U, bool CG>
+__device__ __forceinline__ void gather_chunk(const uint4* tok_row, const uint4* lpo_row, int len,
+                                          long long off, int c, int ups, int32_t* out_tok,
+                                          float* out_lpo) {
+    constexpr int QU = UNIT_THREADS * U;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int a = (int)(off & 3);
+    const int nq = (a + len + 3) >> 2;
+    const int nsq = (len + 3) >> 2;
+    const long long P0 = off >> 2;
+    const int end = c == ups - 1 ? nq : min(nq, (c + 1) * QU);
+    for (int cq = c * QU; cq < end; cq += QU) {
+        const int kw = cq + wid * 32 * U;
+        uint4 q[U];
+        if (out_tok) {
+            row_to_packed_quads_l2<U, CG>(tok_row, nsq, a, kw, q);
+#pragma unroll
+            for (int s = 0; s < U; ++s) {
+                const int k = kw + 32 * s + lane;
+                if (k < end)
+                    store_quad_masked(reinterpret_cast<uint32_t*>(out_tok), P0 + k, q[s], 4 * k - a, len);
+            }
+        }
+        if (out_lpo) {
+            row_to_packed_quads_l2<U, CG>(lpo_row, nsq, a, kw, q);
+#pragma unroll
+            for (int s = 0; s < U; ++s) {
+                const int k = kw + 32 * s + lane;
+                if (k < end)
+                    store_quad_masked(reinterpret_cast<uint32_t*>(out_lpo), P0 + k, q[s], 4 * k - a, len);
+            }
+        }
+    }
+}
+template <int U, bool CG>
+__device__ __forceinline__ void gather_unit(const BufView& v, const Unit& un, int c, int ups,
+                                            int32_t* out_tok, float* out_lpo) {
+    const size_t row = (size_t)un.row * v.stride;
+    gather_chunk<U, CG>(reinterpret_cast<const uint4*>(v.tok + row),
+                        reinterpret_cast<const uint4*>(v.lpo + row), un.len, un.off, c, ups,
+                        out_tok, out_lpo);
+}
+constexpr int GE_DEFER = 64;  // deferred units held per CTA
+template <int U>
+__global__ void __launch_bounds__(UNIT_THREADS, 8) k_gather_early(BufView v, const Unit* desc, int nloc,
+                                                              long long lo, int ups, GridCtl* gc,
+                                                              int nseg, const int* pay_pending,
+                                                              int32_t* out_tok, float* out_lpo) {
+    __shared__ int s_claim[2], s_state, s_pay, s_fin, s_ndef;
+    __shared__ int s_def[GE_DEFER];
+    RB_TSTART(4);
+    const int tid = threadIdx.x;
+    const int nu = nloc * ups;
+    if (tid == 0) {
+        s_claim[0] = (int)atomicAdd(&gc->gwork, 1u);
+        s_pay = 0;
+        s_fin = 0;
+        s_ndef = 0;
+    }
+    __syncthreads();
+    // Copies the deferred units whose condition now holds (block-uniform).
+    auto drain = [&](bool wait) {
+        if (tid == 0) {
+            if (!s_pay) s_pay = wait ? (spin_while_eq(pay_pending, 1), 1) : ld_acquire_i32(pay_pending) == 0;
+            if (!s_fin) s_fin = wait ? (spin_while_eq(&gc->fin, 0), 1) : ld_acquire_i32(&gc->fin) != 0;
+        }
+        __syncthreads();
+        if (!s_pay) return;  // every deferred unit needs the copy (replayed ones too)
+        int keep = 0;
+        const int n = s_ndef;
+        for (int i = 0; i < n; ++i) {
+            const int u = s_def[i];
+            const bool replayed = u < 0;  // encoded as -(u+1)
+            const int uu = replayed ? -(u + 1) : u;
+            const int bb = uu / ups, c = uu - bb * ups;
+            if (replayed && !s_fin) {
+                __syncthreads();
+                if (tid == 0) s_def[keep] = u;
+                ++keep;
+                continue;
+            }
+            const Unit un = ld_unit_cg(desc + bb);
+            if (un.len > 0) gather_unit<U, true>(v, un, c, ups, out_tok, out_lpo);
+        }
+        __syncthreads();
+        if (tid == 0) s_ndef = keep;
+        __syncthreads();
+    };
+    int p = 0;
+    for (;;) {
+        const int u = s_claim[p];
+        if (u >= nu) break;
+        if (tid == 0) {
+            s_claim[p ^ 1] = (int)atomicAdd(&gc->gwork, 1u);  // next claim, in flight meanwhile
+            s_state = spin_while_eq(&gc->seg[(int)((lo + u / ups) / MAP_SPC)], 0);
+            if (!s_pay) s_pay = ld_acquire_i32(pay_pending) == 0;
+        }
+        __syncthreads();
+        const int b = u / ups, c = u - b * ups;
+        const Unit un = ld_unit_cg(desc + b);
+        if (s_state == 2) {  // behind a rejected draw: after the replay
+            if (tid == 0) s_def[s_ndef++] = -(u + 1);
+        } else if (un.k0 && !s_pay) {  // a record of the pending insert
+            if (tid == 0) s_def[s_ndef++] = u;
+        } else if (un.len > 0) {
+            if (un.k0) gather_unit<U, true>(v, un, c, ups, out_tok, out_lpo);
+            else gather_unit<U, false>(v, un, c, ups, out_tok, out_lpo);
+        }
+        __syncthreads();
+        if (s_ndef == GE_DEFER) drain(true);
+        else if (s_ndef && s_pay) drain(false);
+        p ^= 1;
+    }
+    while (s_ndef) drain(true);
+    __syncthreads();
+    __shared__ int s_lastg;
+    if (tid == 0) s_lastg = done_add_u32(&gc->gdone) == gridDim.x - 1;
+    __syncthreads();
+    if (s_lastg) {  // every CTA is past its waits: reset the flags for the next call
+        for (int t = tid; t < nseg; t += UNIT_THREADS) gc->seg[t] = 0;
+        if (tid == 0) {
+            gc->fin = 0;
+            gc->gwork = 0;
+            gc->gdone = 0;
+        }
+    }
+    RB_TEND(4);
+    // completion of this gather implies completion of the sampler and the copy
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 // ---------------------------------------------------------------- inspect
 __global__ void k_shard_contents(BufView v, int s, long long n, rb_record* out) {
@@ -2444,12 +2700,16 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         }
         b->grid_loss = loss_grid(sms);
         b->route_ctl = dalloc<GridCtl>(1);
-        b->pay_sync = dalloc<int>(2);
+        b->pay_sync = dalloc<int>(4);
         {  // no insert yet: the route-completion flag starts set
             const int one = 1;
             RB_CUDA(cudaMemcpy(b->pay_sync + 1, &one, sizeof one, cudaMemcpyHostToDevice));
         }
         b->pdl = std::getenv("RB_NO_PDL") == nullptr;
+        // early gather (k_gather_early): opt-in, see DESIGN.md §4 — overlapping
+        // the gather with the payload copy did not raise their combined HBM
+        // throughput on C4 (both are bandwidth-bound)
+        b->early_gather_ok = b->pdl && std::getenv("RB_EARLY_GATHER") != nullptr;
         b->tma_payload = std::getenv("RB_PAYLOAD_LSU") == nullptr;
         if (const char* e = std::getenv("RB_TMA_CTAS")) b->tma_ctas = std::max(1, std::atoi(e));
         b->sms = sms;
@@ -2511,7 +2771,14 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         // ids promised new and increasing: the closed-form FIFO route
         const unsigned grid = (unsigned)((bt.n + RT_THREADS - 1) / RT_THREADS);
         closed = payload && b->T <= 64 && b->pdl;
-        k_route_fifo<<<grid, RT_THREADS, 0, b->stream>>>(b->v, in, b->route_ctl, b->pay_sync);
+        // a sampler enqueued next reads the new records' lengths from the
+        // offsets after this call returns: the route kernel keeps a copy
+        in.toff_keep = bt.tok_offsets && b->T <= 64 && b->pdl ? b->s_toff : nullptr;
+        in.pay_follows = closed ? 1 : 0;
+        in.keep_cnt = &b->route_ctl->keep_cnt;
+        if (in.toff_keep) b->keep_total += 1;  // one extra CTA copies them
+        k_route_fifo<<<grid + (in.toff_keep ? 1 : 0), RT_THREADS, 0, b->stream>>>(
+            b->v, in, b->route_ctl, b->pay_sync);
     } else {
         k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
         if (b->retention == RB_POSITIVE_BIAS) {
@@ -2555,7 +2822,9 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         b->pend.pending = 1;
         b->pend.c0 = p.c0;
         b->pend.n = (int)bt.n;
-        b->pend.toff = bt.tok_offsets;
+        b->pend.toff = b->s_toff;  // the route kernel's copy
+        b->pend.keep_cnt = &b->route_ctl->keep_cnt;
+        b->pend.keep_target = b->keep_total;
         for (size_t s = 0; s < b->T; ++s) b->pend.P[s] = b->h_pushes[s];
     } else if (payload) {
         k_insert_payload<PAYLOAD_U><<<b->payload_grid, UNIT_THREADS, 0, b->stream>>>(
@@ -2569,7 +2838,9 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         b->pend.pending = 1;
         b->pend.c0 = (int)(b->h_cursor % b->T);
         b->pend.n = (int)bt.n;
-        b->pend.toff = bt.tok_offsets;  // lengths only (or NULL: length 0)
+        b->pend.toff = bt.tok_offsets ? b->s_toff : nullptr;  // lengths only (or NULL: length 0)
+        b->pend.keep_cnt = &b->route_ctl->keep_cnt;
+        b->pend.keep_target = b->keep_total;
         for (size_t s = 0; s < b->T; ++s) b->pend.P[s] = b->h_pushes[s];
     } else {
         b->pdl_tail = false;
@@ -2614,6 +2885,7 @@ void rb_destroy(rb_buffer* b) { delete b; }
 int rb_set_stream(rb_buffer* b, void* stream) {
     return guard([&] {
         DeviceScope ds(b->device);
+        b->gather_early = false;
         b->sync();
         if (b->own_stream && b->stream) cudaStreamDestroy(b->stream);
         // Any handle is taken as given; NULL is the legacy default stream.
@@ -2627,6 +2899,7 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
               size_t* out_applied, int flags) {
     return guard([&] {
         DeviceScope ds(b->device);
+        b->gather_early = false;
         {  // an error left by an unrelated earlier call must not be blamed on this one
             const cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess)
@@ -2788,6 +3061,7 @@ int rb_push(rb_buffer* b, const rb_record* rec, const int32_t* tokens, const flo
             int32_t n_tokens, rb_record* evicted, int* has_evicted) {
     return guard([&] {
         DeviceScope ds(b->device);
+        b->gather_early = false;
         if (has_evicted) *has_evicted = 0;
         if (n_tokens < 0 || n_tokens > b->max_tokens)
             invalid("rb_push: n_tokens exceeds max_tokens");
@@ -2873,6 +3147,7 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         a.n_units = b->n_units_sel;
         const unsigned nmap = (unsigned)std::max<size_t>(1, (nsel + MAP_SPC - 1) / MAP_SPC);
         if (nmap > (unsigned)GRID_MAX_CTAS) invalid("rb_sample: batch too large");
+        bool fused = false;
         if (b->strategy == RB_UNIFORM_WITH_REPLACEMENT) {
             // One fused launch (ring generator + draws + map), a programmatic
             // dependent of the insert's payload copy when that is the last
@@ -2890,6 +3165,15 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 RB_CUDA(cudaStreamSynchronize(b->stream));  // `occ` is a host temporary
                 a.occ_dev = d;
             }
+            // early-gather flags only when an early gather can follow
+            a.early = b->early_gather_ok && !(nsel > 0 && (out_records || out_events));
+            if (b->seg_used) {  // flags of a sampling call no early gather consumed
+                RB_CUDA(cudaMemsetAsync(b->map_ctl->seg, 0, (size_t)b->seg_used * sizeof(int),
+                                        b->stream));
+                RB_CUDA(cudaMemsetAsync(&b->map_ctl->fin, 0, sizeof(int), b->stream));
+                b->pdl_tail = false;  // the memsets are now the stream's tail
+                b->seg_used = 0;
+            }
             MtRing* ring = rng->to_device(b->stream);
             if (b->pdl_tail) a.pend = b->pend;  // the insert just enqueued may still run
             cudaLaunchConfig_t cfg = {};
@@ -2904,6 +3188,8 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
             const int* route_done = b->pay_sync + 1;
             RB_CUDA(cudaLaunchKernelEx(&cfg, k_sample_fused, b->v, ring, a, b->map_ctl, route_done));
             rng->used_on(b->stream);
+            fused = true;
+            b->seg_used = a.early ? (int)nmap : 0;
         } else {
             MtRing* ring = rng->to_device(b->stream);
             if (nsh > 0) {
@@ -2916,6 +3202,9 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
             RB_CUDA(cudaGetLastError());
         }
         b->pdl_tail = false;
+        // the next rb_gather may overlap the sampler (and the insert before it)
+        // when nothing else is enqueued after the sampler
+        b->gather_early = fused && b->seg_used > 0;
         b->B = nsel;
         b->last_loss = -1;
         b->acc_norm_explicit = false;
@@ -3010,7 +3299,26 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
         if (ht || hl) stage = (char*)b->dev_stage(2 * pb + 16, rb_buffer::ST_GATHER);
         if (ht) dt = (int32_t*)stage;
         if (hl) dl = (float*)(stage + pb);
-        if (nloc > 0 && (dt || dl)) {
+        const bool early = b->gather_early;
+        b->gather_early = false;  // one early gather per sampling call (it consumes the claims)
+        if (nloc > 0 && (dt || dl) && early) {
+            // programmatic dependent of the fused sampler: overlaps the insert
+            constexpr int QU = UNIT_THREADS * GATHER_U;
+            const int ups = std::max(1, (int)(((b->stride + 3) / 4 + QU - 1) / QU));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(b->grid_gather);
+            cfg.blockDim = dim3(UNIT_THREADS);
+            cfg.stream = b->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            RB_CUDA(cudaLaunchKernelEx(&cfg, k_gather_early<GATHER_U>, b->v,
+                                       (const Unit*)b->units_sel, (int)nloc, lo, ups, b->map_ctl,
+                                       b->seg_used, (const int*)(b->pay_sync + 2), dt, dl));
+            b->seg_used = 0;  // the early gather resets the flags it consumed
+        } else if (nloc > 0 && (dt || dl)) {
             k_gather<GATHER_U><<<b->grid_gather, UNIT_THREADS, 0, b->stream>>>(
                 b->v, b->units_sel, b->n_units_sel, (int)nloc, dt, dl);
             RB_CUDA(cudaGetLastError());

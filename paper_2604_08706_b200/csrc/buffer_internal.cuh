@@ -70,7 +70,9 @@ struct GridCtl;  // buffer.cu: multi-CTA bookkeeping
 struct PendingIns {
     int pending;          // 1: the last insert (closed-form FIFO, <= 64 shards) may be running
     int c0, n;            // its cursor % T and record count
-    const int64_t* toff;  // its payload offsets
+    const int64_t* toff;  // its payload offsets (the route kernel's copy)
+    const unsigned long long* keep_cnt;  // the copy is complete once *keep_cnt >= keep_target
+    unsigned long long keep_target;
     long long P[64];      // per-shard push counts before it
 };  // loss.cu: resident CTAs of the loss kernels
 
@@ -123,7 +125,11 @@ struct rb_buffer {
     int tma_ctas = 1;                   // bulk-copy payload CTAs per SM
     bool pdl_tail = false;              // the stream's last kernel is the closed-form payload copy
     rb::PendingIns pend{};              // its insert's plan (for a sampler that overlaps it)
-    void other_work() { pdl_tail = false; }  // anything else enqueued on the stream
+    unsigned long long keep_total = 0;  // route CTAs launched with an offsets copy (host count)
+    int seg_used = 0;                   // map CTAs whose early-gather flags are set (to reset)
+    bool gather_early = false;          // the last kernel on the stream is the fused sampler
+    bool early_gather_ok = true;        // RB_NO_EARLY_GATHER unset
+    void other_work() { pdl_tail = false; gather_early = false; }  // anything else enqueued
     rb::Unit* units_ins = nullptr;      // payload copy units of the last insert
     int* n_units_ins = nullptr;
     size_t units_ins_cap = 0;

@@ -242,6 +242,29 @@ __device__ __forceinline__ unsigned long long done_add_u64(unsigned long long* p
     return old;
 }
 
+// Bounded spins on a flag published by a kernel that runs concurrently
+// (programmatic dependent launch): a producer that never publishes is a bug,
+// so after ~4 s the waiting kernel traps (a sticky launch error) instead of
+// hanging the device.
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+static __device__ __noinline__ int spin_while_eq(const int* f, int v) {
+    int x = ld_acquire_i32(f);
+    if (x != v) return x;
+    const unsigned long long t0 = gtimer_ns();
+    while ((x = ld_acquire_i32(f)) == v) {
+        __nanosleep(64);
+        if (gtimer_ns() - t0 > 4000000000ULL) __trap();
+    }
+    return x;
+}
+
+// Writes made before a programmatic trigger, performed before it executes.
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // Programmatic dependent launch: let the next kernel of the stream (launched
 // with programmatic serialization) start while this one runs.
 __device__ __forceinline__ void pdl_trigger() {

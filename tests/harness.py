@@ -41,6 +41,7 @@ class StepConfig:
     device_inputs: bool = True   # torch CUDA tensors (hot path) vs numpy host arrays
     assume_unique: bool = False  # RB_INSERT_ASSUME_UNIQUE (closed-form FIFO insert kernels)
     overlap: bool = False        # no host sync between insert and sample (evicted ids to the device)
+    early_gather: bool = False   # sample with no host outputs, gather right away (overlapped gather)
 
     @property
     def per_step(self):
@@ -166,14 +167,28 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
             debt -= float(cfg.group)
         if ng:
             push_groups(ng, step)
-        grec, gsh, gix = gbuf.sample(cfg.batch, grng, with_index=True)
-        if cfg.overlap:
+        if cfg.early_gather:
+            # insert -> sample -> gather enqueued back to back (outputs allocated
+            # first): the gather runs as a dependent of the sampler and overlaps it
+            cap = cfg.batch * cfg.lmax + 8
+            eg = [torch.full((cap,), -7, dtype=torch.int32, device="cuda:0"),
+                  torch.full((cap,), -7.0, dtype=torch.float32, device="cuda:0"),
+                  torch.zeros(cfg.batch + 1, dtype=torch.int64, device="cuda:0")]
+            gbuf.sample_device(cfg.batch, grng)
+            gbuf.gather(*eg)
             gbuf.check()
-        orec, osh, oix = obuf.sample(cfg.batch, orng)
-        assert np.array_equal(gsh, osh) and np.array_equal(gix, oix), f"sample index mismatch step {step}"
-        assert same_records(grec, orec), f"sampled records mismatch step {step}"
+            orec, osh, oix = obuf.sample(cfg.batch, orng)
+            gids, glens, _ = gbuf.batch_ids()
+            assert np.array_equal(gids, orec["rollout_id"]), f"sampled ids mismatch step {step}"
+        else:
+            grec, gsh, gix = gbuf.sample(cfg.batch, grng, with_index=True)
+            if cfg.overlap:
+                gbuf.check()
+            orec, osh, oix = obuf.sample(cfg.batch, orng)
+            assert np.array_equal(gsh, osh) and np.array_equal(gix, oix), f"sample index mismatch step {step}"
+            assert same_records(grec, orec), f"sampled records mismatch step {step}"
         counts["samples"] += cfg.batch
-        if step % check_every:
+        if step % check_every and not cfg.early_gather:
             continue
         # ---- gather
         ids = orec["rollout_id"]
@@ -186,10 +201,18 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
         gt = torch.zeros(pad, dtype=torch.int32, device="cuda:0")
         gl = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
         go = torch.zeros(len(ids) + 1, dtype=torch.int64, device="cuda:0")
-        torch.cuda.synchronize()  # inputs written on torch's stream
-        gbuf.gather(gt, gl, go)
-        gbuf.synchronize()  # the library runs on its own stream
-        assert np.array_equal(go.cpu().numpy(), off), "packed offsets mismatch"
+        if cfg.early_gather:
+            gt, gl, go = eg
+            assert int(gt[tot].item()) == -7 and float(gl[tot].item()) == -7.0, "gather overran"
+        else:
+            torch.cuda.synchronize()  # inputs written on torch's stream
+            gbuf.gather(gt, gl, go)
+            gbuf.synchronize()  # the library runs on its own stream
+        go_h = go.cpu().numpy()[: len(off)]
+        if not np.array_equal(go_h, off):
+            bad = np.nonzero(go_h != off)[0]
+            raise AssertionError(f"packed offsets mismatch step {step}: {bad.size} entries from "
+                                 f"{bad[0]}: got {go_h[bad[:4]]} want {off[bad[:4]]}")
         assert np.array_equal(gt[:tot].cpu().numpy(), tok_want), f"gathered tokens mismatch step {step}"
         assert np.array_equal(gl[:tot].cpu().numpy(), lpo_want), f"gathered logp_old mismatch step {step}"
         counts["tokens"] += tot

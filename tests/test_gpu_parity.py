@@ -369,18 +369,36 @@ STEP_CASES = {
                               seed=25, retention="positive_bias", delta=1.0, assume_unique=True),
     "posbias_delta_zero": dict(capacity=48, shards=3, batch=24, group=8, lmax=10, ragged=True,
                                seed=26, retention="positive_bias", delta=0.0),
+    # insert -> sample -> gather with no host sync: the gather is a dependent
+    # of the sampler (k_gather_early) and overlaps it and the payload copy
+    "early_gather_c4": dict(capacity=256, shards=4, batch=64, group=16, lmax=96, ragged=True,
+                            seed=31, assume_unique=True, overlap=True, early_gather=True),
+    "early_gather_long": dict(capacity=48, shards=2, batch=32, group=8, lmax=4200, ragged=True,
+                              seed=32, assume_unique=True, overlap=True, early_gather=True),
+    "early_gather_fixed_len": dict(capacity=64, shards=1, batch=48, group=8, lmax=2052,
+                                   ragged=False, seed=33, assume_unique=True, overlap=True,
+                                   early_gather=True),
+    "early_gather_many_shards": dict(capacity=130 * 3, shards=130, batch=260, group=10, lmax=9,
+                                     ragged=True, seed=34, assume_unique=True, overlap=True,
+                                     early_gather=True),
+    "early_gather_not_unique": dict(capacity=96, shards=3, batch=48, group=8, lmax=40,
+                                    ragged=True, seed=35, early_gather=True),
 }
 
 
 @pytest.mark.parametrize("case", sorted(STEP_CASES))
-def test_replay_step_parity(rb, oracle, case):
+def test_replay_step_parity(rb, oracle, case, monkeypatch):
     from tests.harness import StepConfig, run_step_parity
+
+    if STEP_CASES[case].get("early_gather"):
+        monkeypatch.setenv("RB_EARLY_GATHER", "1")  # read at buffer creation
 
     counts = run_step_parity(StepConfig(**STEP_CASES[case]), steps=12, ora=oracle)
     assert counts["samples"] > 0 and counts["tokens"] > 0
 
 
-@pytest.mark.parametrize("case", ["c4_unique_overlap", "c3_unique_overlap_big", "many_shards"])
+@pytest.mark.parametrize("case", ["c4_unique_overlap", "c3_unique_overlap_big", "many_shards",
+                                  "early_gather_c4", "early_gather_long"])
 def test_forced_draw_replay_matches(rb, oracle, case, monkeypatch):
     """The sampler's exact-replay path (taken for real only after a below()
     rejection, probability ~n/2^64) forced on every CTA gives the same
@@ -388,5 +406,7 @@ def test_forced_draw_replay_matches(rb, oracle, case, monkeypatch):
     from tests.harness import StepConfig, run_step_parity
 
     monkeypatch.setenv("RB_DEBUG_FORCE_DRAW_REPLAY", "1")
+    if STEP_CASES[case].get("early_gather"):
+        monkeypatch.setenv("RB_EARLY_GATHER", "1")
     counts = run_step_parity(StepConfig(**STEP_CASES[case]), steps=6, ora=oracle)
     assert counts["samples"] > 0

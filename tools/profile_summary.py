@@ -18,6 +18,8 @@ from launches import load  # noqa: E402
 from ncu_summary import metrics  # noqa: E402
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+if tag.startswith("-"):
+    sys.exit(__doc__)
 src = os.path.join(ROOT, "gpurun_out")
 dst = os.path.join(ROOT, "profiles")
 os.makedirs(dst, exist_ok=True)

@@ -7,7 +7,8 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-os.environ["REPLAY_B200_LIB"] = os.path.join(ROOT, "paper_2604_08706_b200", "libreplay_b200_clocks.so")
+os.environ["REPLAY_B200_LIB"] = os.environ.get("TIMELINE_LIB") or os.path.join(
+    ROOT, "paper_2604_08706_b200", "libreplay_b200_clocks.so")
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
