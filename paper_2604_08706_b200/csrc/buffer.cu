@@ -1214,7 +1214,10 @@ __device__ __forceinline__ void spin_until_set(const int* flag) {
 // fact through the look-back word, apply nothing, and the last CTA replays
 // the rest exactly.
 constexpr int MAP_THREADS = 128;  // small: co-resides with the persistent payload grid
-constexpr int MAP_R = 2;
+#ifndef RB_MAP_R
+#define RB_MAP_R 2
+#endif
+constexpr int MAP_R = RB_MAP_R;
 constexpr int MAP_SPC = MAP_THREADS * MAP_R;  // selections per map CTA
 constexpr int DRAW_NSH = 64;                  // shards whose occupancy rides in the arguments
 constexpr unsigned long long LB_REJ = 1ULL << 61;
@@ -1515,8 +1518,20 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
     __shared__ uint64_t mt[MT_N];
     __shared__ long long s_q;
     __shared__ uint32_t s_idx;
-    __shared__ long long s_total;
+    __shared__ long long s_total, s_genhi;
     __shared__ unsigned long long s_g;
+    // every map CTA's writes were acquired by the done counter: the loads
+    // of the common path are independent and issued together with `first`
+    unsigned long long wl = 0, dr = 0, gs = 0;
+    long long gh = 0;
+    if (threadIdx.x == 0) {
+        wl = __ldcg(&gc->word[nmap - 1]);
+        gs = __ldcg(&gc->gsum);
+        if (DRAW) {
+            dr = r->draws;
+            gh = __ldcg(&gc->gen_hi);
+        }
+    }
     const int first = DRAW ? __ldcg(&gc->first_rej) : INT_MAX;
     const long long D = a.nsel;
     const long long nloc = a.hi - a.lo;
@@ -1608,20 +1623,22 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
             int mm = 0;
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = s_m[w] > mm ? s_m[w] : mm;
             s_m[0] = mm;
-            s_total = (long long)(ld_acquire_u64(&gc->word[nmap - 1]) & LB_SUM);
+            s_total = (long long)(wl & LB_SUM);
+            s_g = gs;
+            s_genhi = gh;
             if (DRAW) {
                 long long q = dc.q0;
                 uint32_t idx = dc.idx0;
                 ring_advance(q, idx, (unsigned long long)D);
                 s_q = q;
                 s_idx = idx;
-                r->draws = r->draws + (unsigned long long)D;
+                r->draws = dr + (unsigned long long)D;
             }
         }
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        const unsigned long long global = atomicAdd(&gc->gsum, 0ULL);
+        const unsigned long long global = (DRAW && first != INT_MAX) ? atomicAdd(&gc->gsum, 0ULL) : s_g;
         s_g = global;
         a.off[nloc] = s_total;
         a.totals[0] = s_total;
@@ -1636,7 +1653,7 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
         acc->objective = 0.0;
         acc->need_fixup = 0;
         if (DRAW) {
-            const long long qhi = __ldcg(&gc->gen_hi);
+            const long long qhi = first != INT_MAX ? __ldcg(&gc->gen_hi) : s_genhi;
             const long long qn = s_q;
             r->q_state = qn;
             r->idx = s_idx;
