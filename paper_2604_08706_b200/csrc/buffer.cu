@@ -917,8 +917,12 @@ constexpr int PAYLOAD_U = 4;
 // overlap the copy find room on every SM.
 constexpr int TP_THREADS = 128;
 constexpr int TP_CH = 1024;           // tokens per item
-constexpr int TP_S = 16;              // stages
-constexpr int TP_LAG = 12;            // loads issued ahead of stores
+#ifndef RB_TP_S
+#define RB_TP_S 16
+#define RB_TP_LAG 12
+#endif
+constexpr int TP_S = RB_TP_S;         // stages
+constexpr int TP_LAG = RB_TP_LAG;     // loads issued ahead of stores
 constexpr int TP_RAW = TP_CH + 4;     // raw words per array (aligned-down source + spill)
 constexpr int TP_STAGE = 2 * TP_RAW;  // words per stage
 constexpr int TP_LIST = 128;          // items listed per round
@@ -3009,19 +3013,24 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
             }
         }
         if (!items.empty()) {
-            // Pinned host arrays are copied straight to the device; pageable
-            // ones go through the pinned staging area (one H2D for all).
+            // Large pinned host arrays (the token payload) are copied straight
+            // to the device, issued first; pageable ones and the small
+            // per-record columns are packed into the pinned staging area
+            // while those copies run, then sent in one H2D (a copy per
+            // column would cost a PCIe round trip each).
+            constexpr size_t DIRECT_MIN = 1 << 20;
+            auto direct = [&](const Item& it) { return it.bytes >= DIRECT_MIN && is_pinned_ptr(*it.ptr); };
             size_t total = 0, paged = 0;
             for (auto& it : items) {
                 total += (it.bytes + 255) & ~size_t(255);
-                if (!is_pinned_ptr(*it.ptr)) paged += (it.bytes + 255) & ~size_t(255);
+                if (!direct(it)) paged += (it.bytes + 255) & ~size_t(255);
             }
             char* dsg = (char*)b->dev_stage(total, rb_buffer::ST_INSERT);
             char* hs = paged ? (char*)b->host_stage(paged) : nullptr;
             size_t o = 0, ho = 0;
             for (auto& it : items) {
                 const size_t sz = (it.bytes + 255) & ~size_t(255);
-                if (is_pinned_ptr(*it.ptr)) {
+                if (direct(it)) {
                     RB_CUDA(cudaMemcpyAsync(dsg + o, *it.ptr, it.bytes, cudaMemcpyHostToDevice,
                                             b->stream));
                     *it.ptr = dsg + o;

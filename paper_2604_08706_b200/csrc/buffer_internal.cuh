@@ -141,7 +141,7 @@ struct rb_buffer {
     size_t loss_partials_bytes = 0;
     // host-buffer loss pipeline: upload / download streams and chunk events
     cudaStream_t cs_in = nullptr, cs_out = nullptr;
-    cudaEvent_t ev_io[1 + 2 * 8] = {};
+    cudaEvent_t ev_io[1 + 2 * 8] = {};  // LOSS_CHUNKS = 8
 
     // current batch (selection)
     size_t sel_cap = 0, B = 0;

@@ -747,7 +747,7 @@ void launch_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl, l
     RB_CUDA(cudaGetLastError());
 }
 
-constexpr int LOSS_CHUNKS = 8;  // host-buffer pipeline depth
+constexpr int LOSS_CHUNKS = 8;  // host-buffer pipeline depth (16 measured slower: per-copy setup)
 
 // Device buffers: one launch.  Host buffers: the batch is cut into up to
 // LOSS_CHUNKS selection ranges; per chunk the logp_now upload (copy stream
