@@ -190,13 +190,31 @@ class Workload:
         self.steps = self.batches[1:]
 
 
+def scaled_cfg(cfg, world):
+    """Weak scaling (BASELINE north_star: the buffer partitions
+    by shard across the GPUs): every GPU holds one shard of the single-GPU
+    size and serves the single-GPU batch, so per-GPU work is fixed and the job
+    is N shards of one sharded buffer (one MT19937-64 stream, round-robin
+    routing, metadata replicated, payload sharded)."""
+    if world == 1:
+        return cfg
+    c = dict(cfg)
+    c["capacity"] = cfg["capacity"] * world
+    c["batch"] = cfg["batch"] * world
+    c["name"] = (f"{cfg['name'].split(':')[0]} per GPU x {world}: buffer {c['capacity']} "
+                 f"trajectories in {world} shards of {cfg['capacity']} (one per GPU), "
+                 f"{c['batch'] // cfg['group']} prompts x G={cfg['group']} per step, "
+                 f"{cfg['lmax']}-token responses, {cfg['retention']}, {cfg['loss']}")
+    return c
+
+
 def run_ours(args, rank, world, dist):
     import torch
 
     import paper_2604_08706_b200 as rb
     from tools import synth
 
-    cfg = CONFIGS[args.config]
+    cfg = scaled_cfg(CONFIGS[args.config], world)
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -252,8 +270,9 @@ def run_ours(args, rank, world, dist):
         buf.loss_grpo(lpn, dlogp, EPS_LOW, EPS_HIGH, stats=stats) if cfg["loss"] == "grpo" else \
             buf.loss_asymre(lpn, dlogp, DELTA_V, stats=stats)
         if world > 1:
-            dist.all_reduce(stats[0:1])            # objective_sum (fp64)
-            dist.all_reduce(stats[2:4].view(torch.int64))  # included, excluded
+            if dist is not None:
+                dist.all_reduce(stats[0:1])            # objective_sum (fp64)
+                dist.all_reduce(stats[2:4].view(torch.int64))  # included, excluded
             buf.loss_finalize(dlogp, stats)
         if ev:
             ev[3].record(stream)
@@ -262,7 +281,7 @@ def run_ours(args, rank, world, dist):
         step(i)
     buf.check()
     torch.cuda.synchronize()
-    use_graph = args.graph and world == 1
+    use_graph = args.graph and dist is None  # one process (N = 1, or an emulated rank)
     phase_events = not use_graph or getattr(args, "phases", False)
     evs = [[torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(4)]
            for _ in range(K)] if phase_events else [None] * K
@@ -283,7 +302,7 @@ def run_ours(args, rank, world, dist):
                 buf.batch_ids_device(sel_ids)
                 synth.logp_now(SEED, Wm + i + 1, sel_ids, off, lpn, sh)
         torch.cuda.synchronize()
-    if world > 1:
+    if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     if getattr(args, "pre_timed", None):  # tools/timeline.py hook
@@ -337,7 +356,7 @@ def run_ours(args, rank, world, dist):
     torch.cuda.synchronize()
     loss_kernel_ms = float(np.mean([a.elapsed_time(b) for a, b in e_k]))
     del flush
-    if world > 1:
+    if dist is not None:
         dist.barrier()
     buf.check()
     total_ms = e_all[0].elapsed_time(e_all[1])
@@ -353,7 +372,7 @@ def run_ours(args, rank, world, dist):
                 "method": "graph(K steps) - graph(K stand-ins), CUDA events on the stream"}
     else:
         ms = float(ph[:, [0, 2]].sum(1).mean())
-    if world > 1:
+    if dist is not None:
         t = torch.tensor([ms, wall], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, wall = float(t[0]), float(t[1])
@@ -380,7 +399,7 @@ def run_ours(args, rank, world, dist):
                     "frac": alg / T / (ms * 1e-3) / 1e9 / hbm}
     res = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
-        "warmup": Wm, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "warmup": Wm, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic (include/replay_synth.h)",
         "config": {"workload": cfg["name"], "buffer": N, "shards": T, "batch": B,
                    "group": cfg["group"], "tokens_per_traj": cfg["lmax"], "ragged": cfg["ragged"],
@@ -602,7 +621,7 @@ def run_c5(args):
 
 
 # ---------------------------------------------------------------- CPU arm
-def cpu_reference(cfg, steps, warmup, threads=0):
+def cpu_reference(cfg, steps, warmup, threads=0, budget_s=90.0):
     """The reference's CPU path (oracle/_ref: unmodified replab buffer/sampler/
     group_advantages + restated token loss) on the host cores."""
     import ctypes as C
@@ -669,9 +688,14 @@ def cpu_reference(cfg, steps, warmup, threads=0):
 
     rec, toff, tok, lpo = make(warm, 0)
     phase_a(rec, toff, tok, lpo)
-    inputs = [make(n, s) for s, n in enumerate(per_step)]
     times = []
-    for i, (rec, toff, tok, lpo) in enumerate(inputs):
+    spent = 0.0
+    for i, n_i in enumerate(per_step):
+        # inputs made untimed, one step at a time; the timed steps stop once
+        # `budget_s` of timed work is done (a bounded sample of the run)
+        if i >= warmup and times and spent >= budget_s:
+            break
+        rec, toff, tok, lpo = make(n_i, i)
         t0 = time.perf_counter()
         phase_a(rec, toff, tok, lpo)
         ta = time.perf_counter() - t0
@@ -684,6 +708,7 @@ def cpu_reference(cfg, steps, warmup, threads=0):
             raise RuntimeError(L.ref_last_error().decode())
         if i >= warmup:
             times.append(ta + tb)
+            spent += ta + tb
     L.ref_bench_free(h)
     tok_per_step = int(out_off[-1])
     mean = float(np.mean(times))
@@ -715,27 +740,38 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--eager", dest="graph", action="store_false",
                     help="launch the timed steps eagerly instead of from a CUDA graph")
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="diagnostic: run rank 0 of an N-GPU job alone on one GPU (no "
+                         "collective); the line predicts the N-GPU step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = CONFIGS[args.config]
+    emulated = args.emulate_world > 1 and world == 1
+    if emulated:
+        world = args.emulate_world
+    cfg = scaled_cfg(CONFIGS[args.config], world)
 
     if args.impl == "reference":
         if rank != 0:
             return
-        r = cpu_reference(cfg, args.steps, args.warmup)
+        # bounded sample: the per-GPU workload of each step (the N-GPU job's
+        # step is N of them), at most ~90 s of timed steps
+        r = cpu_reference(CONFIGS[args.config], args.steps, args.warmup)
+        per_gpu = (f", each 1/{world} of the {world}-GPU job's step (weak scaling)"
+                   if world > 1 else "")
         line = {"metric": METRIC, "value": r["value"], "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
                 "data": "synthetic (include/replay_synth.h)", "impl": "reference",
                 "config": {"workload": cfg["name"], "parallelism": "host threads"},
                 "cpu_baseline": {"value": r["value"], "unit": "tokens/s", "cores": r["cores"],
                                  "kind": "reference",
-                                 "sample": f"{args.steps} full {args.config.upper()} replay steps "
-                                           f"({r['cpu']}); record ops through the unmodified "
-                                           "replab library, token payload/gather/loss restated"},
+                                 "sample": f"{r['steps']} single-GPU-size {args.config.upper()} "
+                                           f"replay steps ({r['cpu']}){per_gpu}; record ops "
+                                           "through the unmodified replab library, token "
+                                           "payload/gather/loss restated"},
                 "e2e": {"value": r["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -756,7 +792,7 @@ def main():
                 print(json.dumps(run_c5(args)), flush=True)
         return
     dist = None
-    if world > 1:
+    if world > 1 and not emulated:
         import torch.distributed as dist
 
         if same_gpu:
@@ -768,6 +804,9 @@ def main():
         res, buf, wl, rng = run_ours(args, rank, world, dist)
         if not args.no_e2e:
             res["e2e"] = run_e2e(args, buf, wl, rng, cfg, world, dist)
+    if emulated:
+        res["emulated"] = (f"rank 0 of a {world}-GPU job alone on one GPU, no collective: "
+                           "a prediction of the N-GPU step, not a measurement")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             r = cpu_reference(cfg, args.cpu_steps, 1)

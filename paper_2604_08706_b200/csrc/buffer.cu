@@ -90,6 +90,8 @@ struct InsertIn {
     const int64_t* toff;  // n+1 payload offsets (may be NULL: length 0)
     int64_t* toff_keep;   // closed-form route: copy of toff for a sampler that overlaps it
     int pay_follows;      // closed-form route: the payload copy is launched next
+    int split_validate;   // closed-form route: validation split over the CTAs (large batches)
+    int keep_ctas;        // closed-form route: extra CTAs copying toff into toff_keep
     unsigned long long* keep_cnt;  // route CTAs that finished their toff_keep slice (monotonic)
     int32_t maxlen;
     int32_t* len;         // scratch: per-record length
@@ -1115,6 +1117,7 @@ struct SampleArgs {
     int* n_units;
     PendingIns pend;          // a closed-form FIFO insert that may still be running
     int early;                // publish the early-gather flags (seg, fin)
+    int gen_ahead;            // the generator CTA also twists the next call's blocks
     long long occ[64];        // per-shard occupancy after the preceding inserts (draws)
     const long long* occ_dev;  // the same for more than 64 shards (device), else NULL
 };
@@ -1171,6 +1174,7 @@ struct GridCtl {
     int fin;
     unsigned gwork, gdone;  // early gather: unit claim counter, done counter
     unsigned long long keep_cnt;  // route: CTAs that copied their offsets slice (monotonic)
+    unsigned vdone, vbad;         // route (split validation): CTAs past it, OR of their bits
 };
 constexpr unsigned long long LB_AGG = 1ULL << 62, LB_INC = 2ULL << 62,
                              LB_VAL = (1ULL << 62) - 1;
@@ -1702,20 +1706,27 @@ __global__ void __launch_bounds__(MAP_THREADS) k_sample_map(BufView v, SampleArg
 // griddepcontrol.wait at the end keeps "this kernel complete => the copy
 // complete" for the gather that follows.
 __device__ void gen_role(MtRing* r, const SampleArgs& a, GridCtl* gc) {
-    __shared__ uint64_t mt[MT_N];
     const long long q0 = r->q_state, qhi0 = r->q_hi;
     const uint32_t idx0 = r->idx;
     const unsigned long long D = (unsigned long long)a.nsel;
     const long long need = q0 + (long long)((idx0 + D + MT_N - 1) / MT_N);
-    long long target = need + (need - q0) + 1;
+    // this call's blocks only (a first call, or a larger batch than the
+    // lookahead planned for); the next call's come from the Rng's lookahead
+    // (or, with RB_NO_LOOKAHEAD, from here: as many again ahead)
+    long long target = a.gen_ahead ? need + (need - q0) + 1 : need;
     if (target > q0 + MT_KR - 1) target = q0 + MT_KR - 1;
-    if (target > qhi0) {
-        for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[i] = r->blk[qhi0 % MT_KR][i];
-        __syncthreads();
+    if (target > qhi0 && threadIdx.x < 32) {  // one warp, the block in registers
+        const int l = threadIdx.x;
+        uint64_t w[10];
+        const uint64_t* src = r->blk[qhi0 % MT_KR];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) w[k] = (l + 32 * k < MT_N) ? src[l + 32 * k] : 0;
         for (long long q = qhi0 + 1; q <= target; ++q) {
-            mt_twist_block(mt);  // ends with a barrier: the stores below read a stable block
+            mt_twist_warp(w);
             uint64_t* dst = r->blk[q % MT_KR];
-            for (int i = threadIdx.x; i < MT_N; i += blockDim.x) dst[i] = mt[i];
+#pragma unroll
+            for (int k = 0; k < 10; ++k)
+                if (l + 32 * k < MT_N) dst[l + 32 * k] = w[k];
         }
     }
     if (threadIdx.x == 0) gc->gen_hi = target > qhi0 ? target : qhi0;
@@ -1880,6 +1891,12 @@ __device__ __forceinline__ void group_adv_one(const double* rw, long long b, lon
     *mean_out = mean;  // bandit.cpp:316-318 (same sequential sum)
 }
 
+// Batches above this size split the route's validation over its CTAs (at
+// 1293 records the whole-batch sweep per CTA publishes the verdict ~2 µs
+// sooner than the counter; at 8 GPUs' 10344 records it is ~7 µs later).
+constexpr int RT_SPLIT_MIN = 4096;
+constexpr int RT_KEEP = 1024;  // token offsets copied per extra route CTA
+
 __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn in, GridCtl* gc,
                                                           int* pay_sync) {
     __shared__ long long s_P[RT_NSH];
@@ -1899,13 +1916,25 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     __syncthreads();
     pdl_trigger();  // the closed-form payload copy may start now (it waits for pay_sync[0])
     // the route proper runs on the first nrt CTAs
-    const unsigned nrt = gridDim.x - (in.toff_keep ? 1u : 0u);
-    if (blockIdx.x == nrt) {
-        // Extra CTA: the caller may reuse its offsets as soon as later stream
-        // work runs, but an overlapping sampler reads the new records'
-        // lengths after this call: keep a copy, published by a monotonic
-        // counter (the sampler waits for its target).
-        for (int i = tid; i <= n; i += RT_THREADS) in.toff_keep[i] = in.toff[i];
+    const unsigned nrt = gridDim.x - (in.toff_keep ? (unsigned)in.keep_ctas : 0u);
+    if (blockIdx.x >= nrt) {
+        // Extra CTAs (RT_KEEP offsets each, all loads in flight): the caller
+        // may reuse its offsets as soon as later stream work runs, but an
+        // overlapping sampler reads the new records' lengths after this
+        // call: keep a copy, published by a monotonic counter (the sampler
+        // waits for its target).
+        const int base = (int)(blockIdx.x - nrt) * RT_KEEP + tid;
+        int64_t t[RT_KEEP / RT_THREADS];
+#pragma unroll
+        for (int k = 0; k < RT_KEEP / RT_THREADS; ++k) {
+            const int i = base + k * RT_THREADS;
+            t[k] = i <= n ? in.toff[i] : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < RT_KEEP / RT_THREADS; ++k) {
+            const int i = base + k * RT_THREADS;
+            if (i <= n) in.toff_keep[i] = t[k];
+        }
         __syncthreads();
         if (tid == 0)
             asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(in.keep_cnt) : "memory");
@@ -1948,9 +1977,28 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
             len = in.toff[j + 1] - off0;
         }
     }
-    // whole-batch validation (replay_buffer.cpp:85-88 order: nothing applied)
+    // whole-batch validation (replay_buffer.cpp:85-88 order: nothing applied).
+    // Up to RT_SPLIT_MIN records every CTA sweeps the whole batch and reaches
+    // the verdict alone; larger batches (many GPUs: the metadata of every
+    // shard's records) split it: each CTA checks its own records and a stride
+    // of the groups, the last CTA to finish ORs the bits and publishes the
+    // verdict, the others wait for it.
+    const bool split = in.split_validate != 0;
     int bad = 0;
-    if (!sticky) {
+    if (!sticky && split) {
+        if (mine) {
+            if (in.toff && (len < 0 || len > in.maxlen)) bad |= 2;
+            if (j > 0 ? id <= in.id[j - 1] : (has_any && id <= max_id)) bad |= 1;
+        }
+        if (!in.adv) {
+            if (blockIdx.x == 0 && tid == 0 && (in.goff[0] != 0 || in.goff[ng] != n)) bad |= 4;
+            for (long long gi = (long long)blockIdx.x * RT_THREADS + tid; gi < ng;
+                 gi += (long long)nrt * RT_THREADS) {
+                const long long b = in.goff[gi], e = in.goff[gi + 1];
+                if (e - b < 2 || b < 0 || e > n) bad |= 4;
+            }
+        }
+    } else if (!sticky) {
 #pragma unroll 4
         for (int jj = tid; jj < n; jj += RT_THREADS) {
             if (in.toff) {
@@ -1971,10 +2019,24 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     RB_GCLOCK(60, blockIdx.x == 0);
     if (bad) atomicOr(&s_bad, bad);
     __syncthreads();
+    if (split) {
+        if (tid == 0) {
+            if (s_bad) atomicOr(&gc->vbad, (unsigned)s_bad);
+            if (done_add_u32(&gc->vdone) == nrt - 1) {  // acquires every CTA's bits
+                const int vb = (int)atomicOr(&gc->vbad, 0u);
+                s_bad = vb;
+                st_release_i32(&pay_sync[0], vb ? 2 : 1);
+            } else {
+                const int f = spin_while_eq(&pay_sync[0], 0);
+                s_bad = f == 2 ? (int)__ldcg(&gc->vbad) : 0;
+            }
+        }
+        __syncthreads();
+    }
     RB_GCLOCK(61, blockIdx.x == 0);
     const int bb = s_bad;
-    // every CTA reached the same verdict; CTA 0 alone publishes it
-    if (blockIdx.x == 0 && tid == 0) st_release_i32(&pay_sync[0], bb ? 2 : 1);
+    // unsplit: every CTA reached the same verdict; CTA 0 alone publishes it
+    if (!split && blockIdx.x == 0 && tid == 0) st_release_i32(&pay_sync[0], bb ? 2 : 1);
     int maxq = 0;
     if (mine) {
         int32_t slot = -1;
@@ -2092,6 +2154,8 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
             ctl->err_index = (bb & 2) ? -3 : (bb & 4) ? -2 : -4;
         }
         gc->done = 0;
+        gc->vdone = 0;
+        gc->vbad = 0;
         RB_GCLOCK(57, true);
     }
     RB_TEND(0);
@@ -2134,7 +2198,10 @@ __global__ void k_sample_records(BufView v, long long nsel, long long per,
 // 128-bit stores; boundary quads shared with the neighbouring trajectory use
 // masked stores).
 template <int U>
-__global__ void __launch_bounds__(UNIT_THREADS) k_gather(BufView v, const Unit* desc,
+// Registers capped so 8 CTAs per SM leave room for one more warp: the Rng's
+// ring lookahead (one warp, launched when the sampler completes) runs beside
+// the gather without displacing a CTA of this static-stride grid.
+__global__ void __launch_bounds__(UNIT_THREADS, 9) k_gather(BufView v, const Unit* desc,
                                                         const int* maxq_p, int nloc,
                                                         int32_t* out_tok, float* out_lpo) {
     constexpr int QU = UNIT_THREADS * U;
@@ -2421,6 +2488,10 @@ __global__ void k_load_posbias(BufView v, int s, int n, const rb_record* recs) {
 rb_buffer::~rb_buffer() {
     if (device >= 0) cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
+    if (look_ev) {
+        if (cudaEventSynchronize(look_ev) != cudaSuccess) cudaDeviceSynchronize();  // captured
+        cudaEventDestroy(look_ev);
+    }
     void* ptrs[] = {v.id, v.prompt, v.group, v.cstep, v.pver, v.reward, v.blp, v.adv, v.gmean,
                     v.correct, v.use, v.len, v.order, v.head, v.pushes, v.owner, v.tok, v.lpo, v.pbq, v.pbs, v.seq,
                     v.hkeys, v.hstate, v.ctl, s_tslot, s_surv, s_evid, s_evrec, s_adv, s_gmean,
@@ -2499,6 +2570,13 @@ void rb_buffer::grow_loss_partials(size_t bytes) {
 void rb_buffer::host_stage_issued() {
     if (!stage_event) RB_CUDA(cudaEventCreateWithFlags(&stage_event, cudaEventDisableTiming));
     RB_CUDA(cudaEventRecord(stage_event, stream));
+}
+void rb_buffer::join_lookahead() {
+    if (!look_pending) return;
+    RB_CUDA(cudaStreamWaitEvent(stream, look_ev, 0));
+    look_pending = false;
+    joined_uid = look_uid;
+    joined_seq = look_seq;
 }
 void rb_buffer::ensure_insert(size_t n) {
     if (n <= ins_cap) return;
@@ -2701,7 +2779,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         int occ = 0;
         RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<GATHER_U>,
                                                               UNIT_THREADS, 0));
-        b->grid_gather = sms * std::max(occ, 1);
+        b->grid_gather = sms * std::max(std::min(occ, 8), 1);
         RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_insert_payload<PAYLOAD_U>,
                                                               UNIT_THREADS, 0));
         {
@@ -2727,6 +2805,8 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
             RB_CUDA(cudaMemcpy(b->pay_sync + 1, &one, sizeof one, cudaMemcpyHostToDevice));
         }
         b->pdl = std::getenv("RB_NO_PDL") == nullptr;
+        b->lookahead = std::getenv("RB_NO_LOOKAHEAD") == nullptr;
+        if (const char* e = std::getenv("RB_LOOKAHEAD_MIN_DRAWS")) b->lookahead_min_draws = std::atoll(e);
         // early gather (k_gather_early): opt-in, see DESIGN.md §4 — overlapping
         // the gather with the payload copy did not raise their combined HBM
         // throughput on C4 (both are bandwidth-bound)
@@ -2796,9 +2876,11 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         // offsets after this call returns: the route kernel keeps a copy
         in.toff_keep = bt.tok_offsets && b->T <= 64 && b->pdl ? b->s_toff : nullptr;
         in.pay_follows = closed ? 1 : 0;
+        in.split_validate = bt.n > (size_t)RT_SPLIT_MIN ? 1 : 0;
         in.keep_cnt = &b->route_ctl->keep_cnt;
-        if (in.toff_keep) b->keep_total += 1;  // one extra CTA copies them
-        k_route_fifo<<<grid + (in.toff_keep ? 1 : 0), RT_THREADS, 0, b->stream>>>(
+        in.keep_ctas = in.toff_keep ? (int)((bt.n + 1 + RT_KEEP - 1) / RT_KEEP) : 0;
+        b->keep_total += (unsigned long long)in.keep_ctas;  // extra CTAs copy them
+        k_route_fifo<<<grid + (unsigned)in.keep_ctas, RT_THREADS, 0, b->stream>>>(
             b->v, in, b->route_ctl, b->pay_sync);
     } else {
         k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
@@ -2921,6 +3003,7 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
     return guard([&] {
         DeviceScope ds(b->device);
         b->gather_early = false;
+        b->join_lookahead();  // before the route: the sampler that follows stays a PDL dependent
         {  // an error left by an unrelated earlier call must not be blamed on this one
             const cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess)
@@ -3193,6 +3276,12 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
             }
             // early-gather flags only when an early gather can follow
             a.early = b->early_gather_ok && !(nsel > 0 && (out_records || out_events));
+            // The next call's blocks: twisted by the sampler's generator CTA
+            // while the batch is small (it finishes inside the payload copy),
+            // by the Rng's side-stream lookahead once that serial chain would
+            // outlast it (measured: 8192 draws faster inside, 16384 beside).
+            const bool side = b->lookahead && nsel > (size_t)b->lookahead_min_draws;
+            a.gen_ahead = side ? 0 : 1;
             if (b->seg_used) {  // flags of a sampling call no early gather consumed
                 RB_CUDA(cudaMemsetAsync(b->map_ctl->seg, 0, (size_t)b->seg_used * sizeof(int),
                                         b->stream));
@@ -3200,6 +3289,10 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 b->pdl_tail = false;  // the memsets are now the stream's tail
                 b->seg_used = 0;
             }
+            // a lookahead this buffer already joined on its stream needs no
+            // second wait (which would sit between the payload and the sampler)
+            if (rng->gen_pending && rng->uid == b->joined_uid && rng->gen_seq == b->joined_seq)
+                rng->gen_pending = false;
             MtRing* ring = rng->to_device(b->stream);
             if (b->pdl_tail) a.pend = b->pend;  // the insert just enqueued may still run
             cudaLaunchConfig_t cfg = {};
@@ -3215,6 +3308,15 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
             RB_CUDA(cudaLaunchKernelEx(&cfg, k_sample_fused, b->v, ring, a, b->map_ctl, route_done));
             rng->used_on(b->stream);
             fused = true;
+            // the next call's MT blocks, twisted beside the rest of the step
+            if (side) rng->launch_lookahead(b->stream, (unsigned long long)nsel);
+            if (rng->gen_pending) {
+                if (!b->look_ev) RB_CUDA(cudaEventCreateWithFlags(&b->look_ev, cudaEventDisableTiming));
+                RB_CUDA(cudaEventRecord(b->look_ev, rng->gen_stream));
+                b->look_pending = true;
+                b->look_uid = rng->uid;
+                b->look_seq = rng->gen_seq;
+            }
             b->seg_used = a.early ? (int)nmap : 0;
         } else {
             MtRing* ring = rng->to_device(b->stream);
@@ -3668,6 +3770,7 @@ int rb_check(rb_buffer* b) {
 int rb_synchronize(rb_buffer* b) {
     return guard([&] {
         DeviceScope ds(b->device);
+        b->join_lookahead();
         b->sync();
     });
 }

@@ -127,6 +127,16 @@ struct rb_buffer {
     rb::PendingIns pend{};              // its insert's plan (for a sampler that overlaps it)
     unsigned long long keep_total = 0;  // route CTAs launched with an offsets copy (host count)
     int seg_used = 0;                   // map CTAs whose early-gather flags are set (to reset)
+    // the ring lookahead launched after the last fused sampler (on the Rng's
+    // side stream): joined by the next insert / loss / synchronize, or by the
+    // next sampler itself
+    cudaEvent_t look_ev = nullptr;
+    bool look_pending = false;
+    bool lookahead = true;              // RB_NO_LOOKAHEAD unset
+    long long lookahead_min_draws = 8192;  // side-stream lookahead above this batch
+    unsigned long long look_uid = 0, look_seq = 0;  // the lookahead recorded in look_ev
+    unsigned long long joined_uid = 0, joined_seq = 0;  // the last one joined on `stream`
+    void join_lookahead();
     bool gather_early = false;          // the last kernel on the stream is the fused sampler
     bool early_gather_ok = true;        // RB_NO_EARLY_GATHER unset
     void other_work() { pdl_tail = false; gather_early = false; }  // anything else enqueued

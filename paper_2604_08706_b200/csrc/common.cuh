@@ -102,7 +102,7 @@ __host__ __device__ inline uint64_t mt_next_scalar(uint64_t* mt, uint32_t* idx,
 // words it reads.  Word o (o >= 0) after the current position is word
 // (idx + o) % MT_N of block q_state + (idx + o) / MT_N.  Any consumer that
 // twists itself produces the same blocks (the stream is deterministic).
-constexpr int MT_KR = 64;  // ring capacity in blocks (19968 outputs)
+constexpr int MT_KR = 256;  // ring capacity in blocks (79872 outputs: a call of up to ~38k draws is twisted ahead by the previous one)
 struct MtRing {
     long long q_state;  // block of the current state
     long long q_hi;     // last block held; [q_state, q_hi] are resident
@@ -139,34 +139,78 @@ __host__ __device__ __forceinline__ uint64_t below_limit(uint64_t bound) {
 // computes up to three words per phase into registers); every thread of the
 // block must call it.
 __device__ __forceinline__ void mt_twist_block(uint64_t* mt) {
+    // new[i] = old[i+156] ^ mix(old[i], old[i+1])            i in [0, 156)
+    // new[j] = new[j-156] ^ mix(old[j], old[j+1])            j in [156, 311)
+    // new[311] = new[155] ^ mix(old[311], new[0])
+    // Thread t owns i = t + r*nt and j = i + 156, so new[j-156] is its own
+    // register: every old word is read before any write (one barrier), the
+    // words are written, and thread 0 finishes word 311 (one more barrier).
     const int t = threadIdx.x, nt = blockDim.x;
-    uint64_t v[3];
+    uint64_t a[3], b[3], old311 = 0;
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
         const int i = t + r * nt;
-        if (i < 156) v[r] = mt[i + 156] ^ mt_mix(mt[i], mt[i + 1]);
+        if (i < 156) {
+            a[r] = mt[i + 156] ^ mt_mix(mt[i], mt[i + 1]);
+            if (i + 156 < 311) b[r] = a[r] ^ mt_mix(mt[i + 156], mt[i + 157]);
+        }
     }
+    if (t == 0) old311 = mt[311];
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
         const int i = t + r * nt;
-        if (i < 156) mt[i] = v[r];
+        if (i < 156) {
+            mt[i] = a[r];
+            if (i + 156 < 311) mt[i + 156] = b[r];
+        }
     }
     __syncthreads();
+    if (t == 0) mt[311] = mt[155] ^ mt_mix(old311, mt[0]);
+    __syncthreads();
+}
+
+// One warp, block held in registers: lane l holds word l + 32k in w[k]
+// (k < 10; slot 9 exists for lanes < 24).  Twists w in place with shuffles
+// only (no shared memory, no barriers): the ring generator's serial chain.
+//   new[i] = old[i+156] ^ mix(old[i], old[i+1])     i < 156
+//   new[j] = new[j-156] ^ mix(old[j], old[j+1])     156 <= j < 311
+//   new[311] = new[155] ^ mix(old[311], new[0])
+__device__ __forceinline__ void mt_twist_warp(uint64_t (&w)[10]) {
+    const int l = threadIdx.x & 31;
+    const unsigned F = 0xffffffffu;
+    uint64_t nw[10];
+    // old[i+1] for every slot (lane 31 takes lane 0 of the next slot)
+    uint64_t o1[10];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        const int i = 156 + t + r * nt;
-        if (i < 311) v[r] = mt[i - 156] ^ mt_mix(mt[i], mt[i + 1]);
+    for (int k = 0; k < 10; ++k) {
+        const uint64_t dn = __shfl_down_sync(F, w[k], 1);
+        const uint64_t nx = __shfl_sync(F, w[k < 9 ? k + 1 : 9], 0);
+        o1[k] = l == 31 ? nx : dn;
     }
-    __syncthreads();
+    // phase 1: slots 0..4 (index < 156: every lane of slots 0..3, lanes < 28 of slot 4);
+    // old[i+156] = lane (l+28)&31, slot k+4 (source lane >= 28) or k+5
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        const int i = 156 + t + r * nt;
-        if (i < 311) mt[i] = v[r];
+    for (int k = 0; k < 5; ++k) {
+        const uint64_t src = l >= 28 ? w[k + 4] : w[k + 5 < 10 ? k + 5 : 9];
+        const uint64_t o156 = __shfl_sync(F, src, (l + 28) & 31);
+        nw[k] = o156 ^ mt_mix(w[k], o1[k]);
     }
-    __syncthreads();
-    if (t == 0) mt[311] = mt[155] ^ mt_mix(mt[311], mt[0]);
-    __syncthreads();
+    // phase 2: slots 4..9 (156 <= j < 311); new[j-156] = lane (l+4)&31,
+    // slot k-5 (source lane >= 4) or k-4 (source lane < 4)
+#pragma unroll
+    for (int k = 4; k < 10; ++k) {
+        const uint64_t src = l < 4 ? nw[k - 4] : nw[k - 5 >= 0 ? k - 5 : 0];
+        const uint64_t n156 = __shfl_sync(F, src, (l + 4) & 31);
+        const int j = l + 32 * k;
+        if (j >= 156 && j < 311) nw[k] = n156 ^ mt_mix(w[k], o1[k]);
+    }
+    // word 311 (lane 23, slot 9): new[155] (lane 27, slot 4), new[0] (lane 0, slot 0)
+    const uint64_t n155 = __shfl_sync(F, nw[4], 27);
+    const uint64_t n0 = __shfl_sync(F, nw[0], 0);
+    if (l == 23) nw[9] = n155 ^ mt_mix(w[9], n0);
+#pragma unroll
+    for (int k = 0; k < 10; ++k) w[k] = nw[k];
 }
 
 // Block-wide: twist ring blocks (qhi, target] from block qhi (shared scratch

@@ -758,6 +758,7 @@ constexpr int LOSS_CHUNKS = 8;  // host-buffer pipeline depth (16 measured slowe
 void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
               rb_loss_stats* stats) {
     b->other_work();
+    b->join_lookahead();  // the step's ring lookahead rejoins the stream here (graph capture)
     const size_t per = b->T ? b->B / b->T : 0;
     const long long lo = (long long)std::min(b->sb * per, b->B);
     const long long hi = (long long)std::min(b->se * per, b->B);

@@ -5,6 +5,7 @@
 // a caller asks for a host-side draw (test code that interleaves
 // rng.uniform01() with buffer.sample(), as the reference's own tests do).
 // Migration is a 2.5 KB copy on the owning stream.
+#include <atomic>
 #include <cmath>
 #include <cstddef>
 #include <cstring>
@@ -85,11 +86,17 @@ static void mt_seed(MtState& s, uint64_t seed) {  // [rand.predef] seeding
     s.draws = 0;
 }
 
+static std::atomic<unsigned long long> g_rng_uid{1};
 rb_rng::rb_rng(uint64_t seed_) : seed(seed_) {
     mt_seed(host, seed_);
     where = 0;
+    uid = g_rng_uid.fetch_add(1);
 }
 rb_rng::~rb_rng() {
+    wait_lookahead();
+    if (gen_fork) cudaEventDestroy(gen_fork);
+    if (gen_done) cudaEventDestroy(gen_done);
+    if (gen_stream) cudaStreamDestroy(gen_stream);
     if (done) {
         // an event last recorded inside a stream capture cannot be waited on
         if (cudaEventSynchronize(done) != cudaSuccess) cudaDeviceSynchronize();
@@ -99,7 +106,22 @@ rb_rng::~rb_rng() {
     cudaGetLastError();  // destructors report nothing: leave no error behind
 }
 
+void rb_rng::wait_lookahead() {
+    if (!gen_pending) return;
+    if (cudaEventSynchronize(gen_done) != cudaSuccess) {  // recorded inside a capture
+        cudaGetLastError();
+        cudaDeviceSynchronize();
+    }
+    gen_pending = false;
+}
+void rb_rng::join(cudaStream_t s) {
+    if (!gen_pending) return;
+    RB_CUDA(cudaStreamWaitEvent(s, gen_done, 0));
+    gen_pending = false;
+}
+
 void rb_rng::to_host() {
+    wait_lookahead();
     if (where == 0) return;
     if (done && cudaEventSynchronize(done) != cudaSuccess) {
         // last recorded inside a stream capture: wait for the device instead
@@ -124,8 +146,9 @@ MtRing* rb_rng::to_device(cudaStream_t s) {
         RB_CUDA(cudaGetDevice(&device));
     }
     if (where == 0) {
-        // the previous device user must be finished before we overwrite;
-        // the host state becomes ring block 0
+        // the previous device user (and any lookahead) must be finished
+        // before we overwrite; the host state becomes ring block 0
+        wait_lookahead();
         if (cudaEventSynchronize(done) != cudaSuccess) {
             cudaGetLastError();
             RB_CUDA(cudaDeviceSynchronize());
@@ -141,6 +164,10 @@ MtRing* rb_rng::to_device(cudaStream_t s) {
         RB_CUDA(cudaMemcpyAsync(dev->blk[0], host.mt, sizeof host.mt, cudaMemcpyHostToDevice, s));
         // host copies must stay alive until the copies complete
         RB_CUDA(cudaStreamSynchronize(s));
+    } else if (gen_pending) {
+        // a lookahead still extends the ring: order after it (and so after
+        // the previous user, which it follows)
+        join(s);
     } else if (s != last_stream) {
         // order after the previous user of the device state on another stream
         // (same-stream users are ordered already; skipping the wait keeps the
@@ -162,6 +189,48 @@ uint64_t rb_rng::next() {
 }
 
 // ---- device bulk generator (parity aid for the sampler's stream) -------
+// Ring lookahead (one warp, blocks in registers): extend the ring so the next
+// call of `draws` draws finds its blocks twisted: (q_hi, need + 1], capped by
+// the ring's capacity from the current block.
+__global__ void __launch_bounds__(32) k_ring_lookahead(MtRing* r, unsigned long long draws) {
+    const int l = threadIdx.x;
+    const long long q0 = r->q_state, qhi = r->q_hi;
+    const long long need = q0 + (long long)((r->idx + draws + MT_N - 1) / MT_N);
+    long long target = need + 1;
+    if (target > q0 + MT_KR - 1) target = q0 + MT_KR - 1;
+    if (target <= qhi) return;
+    uint64_t w[10];
+    const uint64_t* src = r->blk[qhi % MT_KR];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) w[k] = (l + 32 * k < MT_N) ? src[l + 32 * k] : 0;
+    for (long long q = qhi + 1; q <= target; ++q) {
+        mt_twist_warp(w);
+        uint64_t* dst = r->blk[q % MT_KR];
+#pragma unroll
+        for (int k = 0; k < 10; ++k)
+            if (l + 32 * k < MT_N) dst[l + 32 * k] = w[k];
+    }
+    __syncwarp();
+    if (l == 0) r->q_hi = target;  // the joiners see it after this kernel completes
+}
+
+void rb_rng::launch_lookahead(cudaStream_t s, unsigned long long draws) {
+    if (!dev) return;
+    if (!gen_stream) {
+        RB_CUDA(cudaStreamCreateWithFlags(&gen_stream, cudaStreamNonBlocking));
+        RB_CUDA(cudaEventCreateWithFlags(&gen_fork, cudaEventDisableTiming));
+        RB_CUDA(cudaEventCreateWithFlags(&gen_done, cudaEventDisableTiming));
+    }
+    join(s);  // at most one lookahead in flight
+    RB_CUDA(cudaEventRecord(gen_fork, s));
+    RB_CUDA(cudaStreamWaitEvent(gen_stream, gen_fork, 0));
+    k_ring_lookahead<<<1, 32, 0, gen_stream>>>(dev, draws);
+    RB_CUDA(cudaGetLastError());
+    RB_CUDA(cudaEventRecord(gen_done, gen_stream));
+    gen_pending = true;
+    ++gen_seq;
+}
+
 __global__ void __launch_bounds__(320) k_mt_fill(MtRing* r, uint64_t n, uint64_t* out) {
     __shared__ uint64_t mt[MT_N];
     const long long q0 = r->q_state;

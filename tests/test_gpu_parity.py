@@ -167,6 +167,34 @@ def test_assume_unique_violation_is_sticky(rb):
     assert sorted(ids(b.shard_contents(0)) + ids(b.shard_contents(1))) == [1, 2, 3]
 
 
+@pytest.mark.parametrize("where", [1, 4500, -1])
+def test_assume_unique_violation_split_validation(rb, where):
+    """Batches above 4096 records split the route's validation over its CTAs:
+    a broken promise in any CTA's slice still applies nothing, and the next
+    valid batch goes through (the verdict counters are reset)."""
+    b = rb.ShardedReplayBuffer(2, 64)
+    n = 5000
+    ids_ = np.arange(1, n + 1, dtype=np.uint64)
+    if where >= 0:
+        ids_[where] = ids_[where - 1]  # not strictly increasing
+    goff = np.arange(0, n + 1, 8, dtype=np.int64)
+    goff[-1] = n
+    if where < 0:
+        goff[300] = goff[299] + 1  # a group of one
+    rew = (np.arange(n) % 3 == 0).astype(np.float64)
+    b.insert(rollout_id=ids_, reward=rew, group_offsets=goff, assume_unique=True)
+    with pytest.raises(ValueError, match="ASSUME_UNIQUE|group"):
+        b.check()
+    b.check()
+    assert b.size() == 0
+    good = np.arange(1, n + 1, dtype=np.uint64)
+    goff = np.arange(0, n + 1, 8, dtype=np.int64)
+    goff[-1] = n
+    b.insert(rollout_id=good, reward=rew, group_offsets=goff, assume_unique=True)
+    b.check()
+    assert sorted(ids(b.shard_contents(0)) + ids(b.shard_contents(1))) == list(range(n - 63, n + 1))
+
+
 def test_sample_validation(rb):
     """test_buffer_core.cpp:347-359"""
     b = rb.ShardedReplayBuffer(2, 8, strategy="uniform_without_replacement")
@@ -381,6 +409,10 @@ STEP_CASES = {
     "early_gather_many_shards": dict(capacity=130 * 3, shards=130, batch=260, group=10, lmax=9,
                                      ragged=True, seed=34, assume_unique=True, overlap=True,
                                      early_gather=True),
+    # more than 4096 records per insert: the route splits its validation
+    "split_validation_unique": dict(capacity=1024, shards=2, batch=64, group=8, lmax=6,
+                                    ragged=True, seed=36, workers=80, trainers=1, mu=1.0,
+                                    assume_unique=True, overlap=True),
     "early_gather_not_unique": dict(capacity=96, shards=3, batch=48, group=8, lmax=40,
                                     ragged=True, seed=35, early_gather=True),
 }
@@ -395,6 +427,39 @@ def test_replay_step_parity(rb, oracle, case, monkeypatch):
 
     counts = run_step_parity(StepConfig(**STEP_CASES[case]), steps=12, ora=oracle)
     assert counts["samples"] > 0 and counts["tokens"] > 0
+
+
+@pytest.mark.parametrize("case", ["c4_unique_overlap", "c3_unique_overlap_big", "many_shards",
+                                  "early_gather_c4", "host_inputs"])
+def test_side_lookahead_matches(rb, oracle, case, monkeypatch):
+    """The Rng's side-stream ring lookahead (taken above 8192 draws per call)
+    forced on every call: same stream, selections, payload and losses; host
+    draws after device sampling continue the stream (it is joined first)."""
+    from tests.harness import StepConfig, run_step_parity
+
+    monkeypatch.setenv("RB_LOOKAHEAD_MIN_DRAWS", "0")
+    if STEP_CASES[case].get("early_gather"):
+        monkeypatch.setenv("RB_EARLY_GATHER", "1")
+    counts = run_step_parity(StepConfig(**STEP_CASES[case]), steps=10, ora=oracle)
+    assert counts["samples"] > 0
+
+
+def test_side_lookahead_rng_continues_on_host(rb, oracle, monkeypatch):
+    monkeypatch.setenv("RB_LOOKAHEAD_MIN_DRAWS", "0")
+    buf = rb.ShardedReplayBuffer(2, 64)
+    obuf = oracle.buffer(2, 64)
+    for i in range(1, 65):
+        r = make_record(i)
+        buf.push(r)
+        obuf.push(r)
+    g = rb.Rng(7).stream("buffer_sampling")
+    o = oracle.rng(7).stream("buffer_sampling")
+    for _ in range(5):
+        buf.sample_device(2000, g)
+        obuf.sample(2000, o)
+    buf.synchronize()
+    assert [g.next_u64() for _ in range(3)] == [o.next_u64() for _ in range(3)]
+    assert g.draws == 5 * 2000 + 3
 
 
 @pytest.mark.parametrize("case", ["c4_unique_overlap", "c3_unique_overlap_big", "many_shards",

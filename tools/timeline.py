@@ -33,7 +33,7 @@ def reset():
 args.pre_timed = reset
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
-    res, buf, wl, rng = bench.run_ours(args, 0, 1, None)
+    res, buf, wl, rng = bench.run_ours(args, 0, int(os.environ.get("EMU_WORLD", "1")), None)
 torch.cuda.synchronize()
 _lib.check(_lib.lib.rb_debug_timeline(out, 0))
 _lib.check(_lib.lib.rb_debug_timeline_loss(out2, 0))
