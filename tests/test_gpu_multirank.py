@@ -154,10 +154,13 @@ def _run(rank, world, port, case, q):
             dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("side_lookahead", [False, True])
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_two_ranks_one_shard_each(case):
+def test_two_ranks_one_shard_each(case, side_lookahead, monkeypatch):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
+    if side_lookahead:  # every sampling call forks its ring lookahead (inherited by the ranks)
+        monkeypatch.setenv("RB_LOOKAHEAD_MIN_DRAWS", "0")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
