@@ -1895,6 +1895,10 @@ __device__ __forceinline__ void group_adv_one(const double* rw, long long b, lon
 // 1293 records the whole-batch sweep per CTA publishes the verdict ~2 µs
 // sooner than the counter; at 8 GPUs' 10344 records it is ~7 µs later).
 constexpr int RT_SPLIT_MIN = 4096;
+#ifndef RB_RT_UNROLL
+#define RB_RT_UNROLL 8
+#endif
+constexpr int RT_UNROLL = RB_RT_UNROLL;  // whole-batch validation sweep: records in flight per thread
 constexpr int RT_KEEP = 1024;  // token offsets copied per extra route CTA
 
 __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn in, GridCtl* gc,
@@ -1999,7 +2003,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
             }
         }
     } else if (!sticky) {
-#pragma unroll 4
+#pragma unroll (RT_UNROLL)
         for (int jj = tid; jj < n; jj += RT_THREADS) {
             if (in.toff) {
                 const long long l = in.toff[jj + 1] - in.toff[jj];
