@@ -248,6 +248,9 @@ def run_ours(args, rank, world, dist):
     off = torch.empty(per_rank + 1, dtype=torch.int64, device=dev)
     sel_ids = torch.empty(per_rank, dtype=torch.int64, device=dev)
     stats = torch.zeros(5, dtype=torch.float64, device=dev)  # rb_loss_stats (40 B)
+    red3 = torch.zeros(3, dtype=torch.float64, device=dev)   # multi-GPU reduce vector (24 B)
+    if world > 1:
+        buf.loss_set_reduce_vector(red3)
     t_ins = []
 
     def step(i, ev=None):
@@ -269,11 +272,10 @@ def run_ours(args, rank, world, dist):
             ev[2].record(stream)
         buf.loss_grpo(lpn, dlogp, EPS_LOW, EPS_HIGH, stats=stats) if cfg["loss"] == "grpo" else \
             buf.loss_asymre(lpn, dlogp, DELTA_V, stats=stats)
-        if world > 1:
+        if world > 1:  # one collective: the registered {objective_sum, included, excluded}
             if dist is not None:
-                dist.all_reduce(stats[0:1])            # objective_sum (fp64)
-                dist.all_reduce(stats[2:4].view(torch.int64))  # included, excluded
-            buf.loss_finalize(dlogp, stats)
+                dist.all_reduce(red3)
+            buf.loss_finalize_vec(dlogp, red3, stats)
         if ev:
             ev[3].record(stream)
 
@@ -422,10 +424,10 @@ def launches_per_step(cfg, world):
     """Library kernels of one timed step (the stand-in's kernels are not counted):
     FIFO (ids promised unique): k_route_fifo, k_insert_payload_tma, k_sample_fused,
     k_gather, loss; positive bias: k_insert_route, k_posbias_batch, k_insert_payload,
-    k_sample_fused, k_gather, loss; + k_stats_in/k_dlogp_rescale/k_stats_out
-    (rb_loss_finalize) per step on more than one rank."""
+    k_sample_fused, k_gather, loss; + k_finalize_vec (rb_loss_finalize_vec) per
+    step on more than one rank; + k_ring_lookahead above 8192 draws per call."""
     n = 5 if cfg["retention"] == "plain_fifo" else 6
-    return n + (3 if world > 1 else 0)
+    return n + (1 if world > 1 else 0) + (1 if cfg["batch"] > 8192 else 0)
 
 
 def load_traffic(kernel):

@@ -223,6 +223,14 @@ int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double
 /* Re-normalise out_dlogp after a cross-rank reduction of stats (only does
  * work when excluded > 0; objective recomputed).  Device or host stats. */
 int rb_loss_finalize(rb_buffer* b, float* dlogp, rb_loss_stats* stats);
+/* The same reduction with ONE collective: once a device vector of three
+ * doubles is registered, every loss call also writes {objective_sum,
+ * included, excluded} into it (counts exact below 2^53); the caller
+ * all-reduces it (sum) across ranks and calls rb_loss_finalize_vec, which
+ * applies the global normalisation in one kernel and fills `stats` (host,
+ * device or NULL).  vec3 = NULL unregisters. */
+int rb_loss_set_reduce_vector(rb_buffer* b, double* vec3);
+int rb_loss_finalize_vec(rb_buffer* b, float* dlogp, const double* vec3, rb_loss_stats* stats);
 
 /* Inspection (replay_buffer.hpp:74-84). */
 int rb_num_shards(const rb_buffer* b, size_t* out);

@@ -383,6 +383,7 @@ struct DevLossAcc {
     double objective;
     int need_fixup;
     int pad;
+    double* red3;  // registered reduce vector {objective_sum, included, excluded} (or NULL)
 };
 
 }  // namespace rb

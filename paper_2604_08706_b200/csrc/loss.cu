@@ -266,6 +266,11 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
         acc->obj_sum = o;
         acc->included = (unsigned long long)inc;
         acc->excluded = (unsigned long long)exc;
+        if (double* r3 = acc->red3) {  // one-collective multi-GPU reduction
+            r3[0] = o;
+            r3[1] = (double)inc;
+            r3[2] = (double)exc;
+        }
         acc->objective = asym ? o * inv_b : (inc ? o / (double)inc : 0.0);
         acc->need_fixup = !asym && exc > 0 && inc > 0;
         acc->done_blocks = 0;
@@ -664,6 +669,7 @@ struct Ctx {
         require_device();
         RB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
         RB_CUDA(cudaMalloc(&acc, sizeof(DevLossAcc)));
+        RB_CUDA(cudaMemset(acc, 0, sizeof(DevLossAcc)));  // no reduce vector (red3 = NULL)
         RB_CUDA(cudaMalloc(&dstats, sizeof(rb_loss_stats)));
         RB_CUDA(cudaMalloc(&dflag, sizeof(int)));
     }
@@ -893,6 +899,65 @@ int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double
         b->last_loss = 1;
         b->acc_norm_explicit = false;
         run_loss(b, c, logp_now, out_dlogp, stats);
+    });
+}
+
+// After the all-reduce of the reduce vector: every CTA derives the global
+// normalisation from it and rescales its slice of dlogp if a token was
+// excluded anywhere (GRPO); CTA 0 updates the accumulator and the stats.
+__global__ void k_finalize_vec(DevLossAcc* acc, const double* v3, float* dlogp,
+                               const long long* n_dev, rb_loss_stats* st, int grpo) {
+    const double obj = v3[0];
+    const unsigned long long inc = (unsigned long long)v3[1], exc = (unsigned long long)v3[2];
+    const bool fix = grpo && exc > 0 && inc > 0;
+    if (fix && dlogp) {
+        const float f = (float)((double)acc->total_tokens / (double)inc);
+        const long long n = *n_dev;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x)
+            dlogp[i] *= f;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        acc->obj_sum = obj;
+        acc->included = inc;
+        acc->excluded = exc;
+        acc->objective = inc ? obj / (double)inc : 0.0;
+        acc->need_fixup = 0;  // applied
+        if (st) {
+            st->objective_sum = obj;
+            st->objective = acc->objective;
+            st->included = (int64_t)inc;
+            st->excluded = (int64_t)exc;
+            st->total_tokens = acc->total_tokens;
+        }
+    }
+}
+__global__ void k_set_red3(DevLossAcc* acc, double* v) { acc->red3 = v; }
+
+int rb_loss_set_reduce_vector(rb_buffer* b, double* vec3) {
+    return guard([&] {
+        if (vec3 && !is_device_ptr(vec3)) invalid("rb_loss_set_reduce_vector: device memory required");
+        b->other_work();
+        k_set_red3<<<1, 1, 0, b->stream>>>(b->acc, vec3);
+        RB_CUDA(cudaGetLastError());
+    });
+}
+
+int rb_loss_finalize_vec(rb_buffer* b, float* dlogp, const double* vec3, rb_loss_stats* stats) {
+    return guard([&] {
+        if (!vec3 || !is_device_ptr(vec3)) invalid("rb_loss_finalize_vec: device vector required");
+        b->other_work();
+        const bool host = stats && !is_device_ptr(stats);
+        rb_loss_stats* dst = host ? (rb_loss_stats*)b->scratch(sizeof(rb_loss_stats)) : stats;
+        // the normalisation needs the tokens of this rank's batch: sel_total[0]
+        k_finalize_vec<<<148, 256, 0, b->stream>>>(b->acc, vec3, dlogp, b->sel_total, dst,
+                                                   b->last_loss == 0 ? 1 : 0);
+        RB_CUDA(cudaGetLastError());
+        if (host) {
+            RB_CUDA(cudaMemcpyAsync(stats, dst, sizeof(rb_loss_stats), cudaMemcpyDeviceToHost,
+                                    b->stream));
+            b->sync();
+        }
     });
 }
 

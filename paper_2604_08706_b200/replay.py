@@ -353,6 +353,18 @@ class ShardedReplayBuffer:
         check(lib.rb_loss_finalize(self._h, _ptr(dlogp), p))
         return stats
 
+    def loss_set_reduce_vector(self, vec3) -> None:
+        """Register a device float64[3] that every loss call fills with
+        {objective_sum, included, excluded} (one-collective multi-GPU path)."""
+        check(lib.rb_loss_set_reduce_vector(self._h, _ptr(vec3)))
+
+    def loss_finalize_vec(self, dlogp, vec3, stats=None):
+        """After all-reducing the registered vector: global normalisation
+        (one kernel); `stats` a LossStats, a device tensor or None."""
+        p = C.byref(stats) if isinstance(stats, LossStats) else _ptr(stats)
+        check(lib.rb_loss_finalize_vec(self._h, _ptr(dlogp), _ptr(vec3), p))
+        return stats
+
     def batch_ids_device(self, out_ids, out_lengths=None, out_offsets=None) -> None:
         """Per-selection ids / lengths / packed offsets into device arrays (no sync)."""
         check(lib.rb_batch_ids(self._h, _ptr(out_ids), _ptr(out_lengths), _ptr(out_offsets)))

@@ -35,11 +35,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _run(rank, world, port, case, q):
+def _run(rank, world, port, case, q, one_collective=False):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
+        vec3 = torch.zeros(3, dtype=torch.float64, device="cuda:0")
         from oracle.pyoracle import Oracle, same_records
         from paper_2604_08706_b200 import Rng, ShardedReplayBuffer
 
@@ -125,19 +126,33 @@ def _run(rank, world, port, case, q):
             dl = torch.zeros(pad, dtype=torch.float32, device=dev)
             stats = torch.zeros(5, dtype=torch.float64, device=dev)
             torch.cuda.synchronize()
-            gbuf.loss_grpo(lpn, dl, cfg.eps_low, cfg.eps_high, stats=stats)
-            gbuf.synchronize()
-            host = stats.cpu()
-            s_obj = host[0:1].clone()
-            s_cnt = host[2:4].clone().view(torch.int64)
-            dist.all_reduce(s_obj)
-            dist.all_reduce(s_cnt)
-            host[0:1] = s_obj
-            host[2:4] = s_cnt.view(torch.float64)
-            stats.copy_(host.to(dev))
-            torch.cuda.synchronize()  # torch's stream wrote the reduced stats
-            gbuf.loss_finalize(dl, stats)
-            gbuf.synchronize()
+            if one_collective:  # the registered reduce vector, one all-reduce
+                gbuf.loss_set_reduce_vector(vec3)
+                gbuf.loss_grpo(lpn, dl, cfg.eps_low, cfg.eps_high, stats=stats)
+                gbuf.synchronize()
+                red = vec3.cpu()
+                dist.all_reduce(red)
+                vec3.copy_(red.to(dev))
+                torch.cuda.synchronize()
+                gbuf.loss_finalize_vec(dl, vec3, stats)
+                gbuf.synchronize()
+                host = stats.cpu()
+                s_obj = host[0:1].clone()
+                s_cnt = host[2:4].clone().view(torch.int64)
+            else:
+                gbuf.loss_grpo(lpn, dl, cfg.eps_low, cfg.eps_high, stats=stats)
+                gbuf.synchronize()
+                host = stats.cpu()
+                s_obj = host[0:1].clone()
+                s_cnt = host[2:4].clone().view(torch.int64)
+                dist.all_reduce(s_obj)
+                dist.all_reduce(s_cnt)
+                host[0:1] = s_obj
+                host[2:4] = s_cnt.view(torch.float64)
+                stats.copy_(host.to(dev))
+                torch.cuda.synchronize()  # torch's stream wrote the reduced stats
+                gbuf.loss_finalize(dl, stats)
+                gbuf.synchronize()
             got = dl[:tot].cpu().numpy()
             np.testing.assert_allclose(got, d_want[aoff[lo]:aoff[hi]], rtol=1e-5, atol=1e-12,
                                        err_msg=f"rank {rank}: dlogp, step {step}")
@@ -154,9 +169,10 @@ def _run(rank, world, port, case, q):
             dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("one_collective", [False, True])
 @pytest.mark.parametrize("side_lookahead", [False, True])
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_two_ranks_one_shard_each(case, side_lookahead, monkeypatch):
+def test_two_ranks_one_shard_each(case, side_lookahead, one_collective, monkeypatch):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     if side_lookahead:  # every sampling call forks its ring lookahead (inherited by the ranks)
@@ -164,7 +180,8 @@ def test_two_ranks_one_shard_each(case, side_lookahead, monkeypatch):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, 2, port, case, q)) for r in range(2)]
+    procs = [ctx.Process(target=_run, args=(r, 2, port, case, q, one_collective))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in procs)
