@@ -438,7 +438,7 @@ def load_traffic(kernel):
         return None
 
 
-def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None):
+def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None, rank=0):
     """Same metric through the C-ABI with HOST (pinned) buffers, copies timed."""
     import torch
 
@@ -493,6 +493,19 @@ def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None):
     for r, hb2, n in plan:
         if r == 0:
             e2e_step(hb2, n)
+    # bytes that cross PCIe per insert: every column, and of the token
+    # payload only this rank's records' ranges (round-robin from the cursor)
+    cursor = buf.route_cursor()
+    T = buf.num_shards()
+
+    def h2d_insert(hb2, n, c0):
+        meta = sum(v.numel() * v.element_size() for k, v in hb2.items()
+                   if k not in ("tokens", "logp_old"))
+        toff = hb2["tok_offsets"].numpy()
+        lens = np.diff(toff)
+        own = ((c0 + np.arange(n)) % T) == rank if T > 1 else np.ones(n, bool)
+        return meta + int(lens[own].sum()) * 8
+
     h2d = d2h = 0
     done_tokens = 0
     torch.cuda.synchronize()
@@ -502,15 +515,19 @@ def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None):
             continue
         tot_s = e2e_step(hb2, n)
         done_tokens += tot_s
-        h2d += sum(v.numel() * v.element_size() for v in hb2.values()) + tot_s * 4
+        h2d += (h2d_insert(hb2, n, cursor) if n else 0) + tot_s * 4
+        cursor = (cursor + n) % T
         d2h += tot_s * 4 * 2 + (B + 1) * 8 + 40
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / len(host)
     if world > 1:  # whole job: tokens of every rank over the slowest rank's time
-        t = torch.tensor([float(done_tokens), dt], dtype=torch.float64)
-        dist.all_reduce(t[0:1])
-        dist.all_reduce(t[1:2], op=dist.ReduceOp.MAX)
-        done_tokens, dt = float(t[0]), float(t[1])
+        if dist is not None:
+            t = torch.tensor([float(done_tokens), dt], dtype=torch.float64)
+            dist.all_reduce(t[0:1])
+            dist.all_reduce(t[1:2], op=dist.ReduceOp.MAX)
+            done_tokens, dt = float(t[0]), float(t[1])
+        else:  # emulated rank 0: every rank alike
+            done_tokens *= world
         h2d, d2h = h2d * world, d2h * world
     return {"value": done_tokens / len(host) / dt, "unit": "tokens/s", "ms_per_step": dt * 1e3,
             "h2d_bytes_per_step": h2d // len(host), "d2h_bytes_per_step": d2h // len(host),
@@ -805,7 +822,7 @@ def main():
     with torch.cuda.stream(stream):
         res, buf, wl, rng = run_ours(args, rank, world, dist)
         if not args.no_e2e:
-            res["e2e"] = run_e2e(args, buf, wl, rng, cfg, world, dist)
+            res["e2e"] = run_e2e(args, buf, wl, rng, cfg, world, dist, rank)
     if emulated:
         res["emulated"] = (f"rank 0 of a {world}-GPU job alone on one GPU, no collective: "
                            "a prediction of the N-GPU step, not a measurement")

@@ -3115,15 +3115,40 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
             char* dsg = (char*)b->dev_stage(total, rb_buffer::ST_INSERT);
             char* hs = paged ? (char*)b->host_stage(paged) : nullptr;
             size_t o = 0, ho = 0;
+            // A rank holding one of the shards reads only its own records'
+            // payload (every T-th record from the cursor).  With the offsets
+            // on the host and equal lengths, only those rows cross PCIe, as
+            // one strided 2-D copy per array (a batch of per-record copies
+            // measured slower than the whole array: ~2.4 µs per range).
+            bool partial = b->se == b->sb + 1 && b->T > 1 && toff_host && n > 0;
+            const int64_t L0 = partial ? toff_user[1] - toff_user[0] : 0;
+            for (size_t j = 1; partial && j < n; ++j)
+                if (toff_user[j + 1] - toff_user[j] != L0) partial = false;
+            partial = partial && L0 > 0;
+            const size_t j0 = partial ? (b->sb + b->T - b->h_cursor % b->T) % b->T : 0;
+            const size_t rows = partial && j0 < n ? (n - 1 - j0) / b->T + 1 : 0;
             for (auto& it : items) {
                 const size_t sz = (it.bytes + 255) & ~size_t(255);
                 if (direct(it)) {
-                    RB_CUDA(cudaMemcpyAsync(dsg + o, *it.ptr, it.bytes, cudaMemcpyHostToDevice,
-                                            b->stream));
+                    const bool payload_arr = it.ptr == (const void**)&bt.tokens ||
+                                             it.ptr == (const void**)&bt.logp_old;
+                    if (partial && payload_arr) {
+                        if (rows) {
+                            const size_t t0 = (size_t)toff_user[j0] * 4, w = (size_t)L0 * 4;
+                            const size_t pitch = w * b->T;
+                            RB_CUDA(cudaMemcpy2DAsync(dsg + o + t0, pitch, (const char*)*it.ptr + t0,
+                                                      pitch, w, rows, cudaMemcpyHostToDevice,
+                                                      b->stream));
+                        }
+                    } else {
+                        RB_CUDA(cudaMemcpyAsync(dsg + o, *it.ptr, it.bytes,
+                                                cudaMemcpyHostToDevice, b->stream));
+                    }
                     *it.ptr = dsg + o;
                     o += sz;
                 }
             }
+
             const size_t paged_base = o;
             for (auto& it : items) {
                 const size_t sz = (it.bytes + 255) & ~size_t(255);
