@@ -521,8 +521,8 @@ def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None, rank=0):
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / len(host)
     if world > 1:  # whole job: tokens of every rank over the slowest rank's time
-        if dist is not None:
-            t = torch.tensor([float(done_tokens), dt], dtype=torch.float64)
+        if dist is not None:  # device tensors: NCCL reduces CUDA memory only
+            t = torch.tensor([float(done_tokens), dt], dtype=torch.float64, device="cuda")
             dist.all_reduce(t[0:1])
             dist.all_reduce(t[1:2], op=dist.ReduceOp.MAX)
             done_tokens, dt = float(t[0]), float(t[1])
