@@ -2,16 +2,21 @@
 //
 // Kernels of one replay step, all on the buffer's stream:
 //   k_route_fifo          FIFO insert, ids promised unique: one record per
-//                         thread, whole-batch validation per CTA, group
-//                         advantages (bandit.cpp:276-294), routing and
-//                         victims in closed form (replay_buffer.cpp:83-133).
+//                         thread, whole-batch validation per CTA (split over
+//                         the CTAs above 4096 records), group advantages
+//                         (bandit.cpp:276-294), routing and victims in closed
+//                         form (replay_buffer.cpp:83-133); extra CTAs keep a
+//                         copy of the token offsets for the sampler.
 //   k_insert_payload_tma  closed-form payload copy over cp.async.bulk, a
 //                         programmatic dependent of the route (gated on its
 //                         verdict); k_insert_payload: the table-driven copy.
 //   k_sample_fused        uniform_with_replacement: MT19937-64 ring twisted
 //                         ahead, draws, arrival index -> slot, look-back scan
 //                         of the packed offsets (replay_buffer.cpp:135-217).
-//   k_gather              ragged 128-bit gather of the sampled rows.
+//                         Above 8192 draws the next call's blocks come from
+//                         the Rng's side-stream lookahead (rng.cu).
+//   k_gather              ragged 128-bit gather of the sampled rows;
+//                         k_gather_early (opt-in) overlaps it with the copy.
 // General paths: k_insert_route (exact sequential semantics: duplicate ids,
 // positive bias validation) + k_posbias_batch (positive bias as O(1) queues),
 // k_sample_without + k_sample_map (without-replacement strategies),
