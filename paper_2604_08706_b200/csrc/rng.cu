@@ -4,7 +4,11 @@
 // the sampler consumes it (the hot path never copies it back), the host when
 // a caller asks for a host-side draw (test code that interleaves
 // rng.uniform01() with buffer.sample(), as the reference's own tests do).
-// Migration is a 2.5 KB copy on the owning stream.
+// Migration is a 2.5 KB copy on the owning stream.  On the device the state
+// lives in a ring of twisted blocks (MtRing); a sampler that consumed a
+// large batch forks the next call's block twisting onto a side stream
+// (k_ring_lookahead, one warp with the block in registers), and every later
+// user of the ring joins it first (join / to_device / to_host).
 #include <atomic>
 #include <cmath>
 #include <cstddef>
