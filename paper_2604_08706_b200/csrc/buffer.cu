@@ -3481,7 +3481,13 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
                                        b->seg_used, (const int*)(b->pay_sync + 2), dt, dl));
             b->seg_used = 0;  // the early gather resets the flags it consumed
         } else if (nloc > 0 && (dt || dl)) {
-            k_gather<GATHER_U><<<b->grid_gather, UNIT_THREADS, 0, b->stream>>>(
+            // the resident grid, or one CTA per work unit for small batches
+            constexpr int QU = UNIT_THREADS * GATHER_U;
+            const long long ups = (((long long)b->stride + 3) / 4 + 1 + QU - 1) / QU;
+            const long long units = std::max<long long>(1, nloc * ups);
+            const unsigned grid = (unsigned)std::min<long long>(b->grid_gather,
+                                                                std::max<long long>(units, b->sms));
+            k_gather<GATHER_U><<<grid, UNIT_THREADS, 0, b->stream>>>(
                 b->v, b->units_sel, b->n_units_sel, (int)nloc, dt, dl);
             RB_CUDA(cudaGetLastError());
         }

@@ -741,15 +741,26 @@ struct LossCall {
 
 // Launch the loss kernel over owned selections [s0, s1) (part slots
 // [part_base, part_base + grid) of `nparts` folded by the last CTA overall).
+// CTAs for a launch over `nsel` selections: the resident grid, or fewer
+// when the batch has fewer work units (small batches: fewer idle CTAs and
+// fewer partials for the last CTA to fold).
+int loss_grid_for(const rb_buffer* b, long long nsel) {
+    const long long qmax = ((long long)b->max_tokens + 3) / 4 + 1;  // quads per selection (bound)
+    const long long ups = (qmax + UNIT_THREADS * LOSS_U - 1) / (UNIT_THREADS * LOSS_U);
+    const long long units = std::max(1LL, nsel * ups);
+    return (int)std::min<long long>(b->grid_loss, std::max<long long>(units, b->sms));
+}
+
 void launch_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl, long long s0,
                  long long s1, int part_base, int nparts, rb_loss_stats* kst, int local_fix) {
     const Unit* u = b->units_sel + s0;
+    const int grid = loss_grid_for(b, s1 - s0);
     if (c.kind == 0)
-        k_loss_grpo_buf<LOSS_U><<<b->grid_loss, UNIT_THREADS, 0, b->stream>>>(
+        k_loss_grpo_buf<LOSS_U><<<grid, UNIT_THREADS, 0, b->stream>>>(
             b->v, u, b->n_units_sel, (int)(s1 - s0), lpn, dl, c.p, b->acc,
             (Partial*)b->loss_partials, kst, b->sel_total, local_fix, part_base, nparts);
     else
-        k_loss_asymre_buf<LOSS_U><<<b->grid_loss, UNIT_THREADS, 0, b->stream>>>(
+        k_loss_asymre_buf<LOSS_U><<<grid, UNIT_THREADS, 0, b->stream>>>(
             b->v, u, b->n_units_sel, (int)(s1 - s0), lpn, dl, c.delta_v, c.inv_b, b->acc,
             (Partial*)b->loss_partials, kst, part_base, nparts);
     RB_CUDA(cudaGetLastError());
@@ -779,7 +790,7 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
     if (nloc <= 0) {
         if (kst) k_stats_out<<<1, 1, 0, b->stream>>>(b->acc, kst, c.kind, c.inv_b);
     } else if (!host_in && !host_out) {
-        launch_loss(b, c, lpn, dl, 0, nloc, 0, b->grid_loss, kst, single && c.kind == 0);
+        launch_loss(b, c, lpn, dl, 0, nloc, 0, loss_grid_for(b, nloc), kst, single && c.kind == 0);
     } else {
         // packed offsets of the owned selections (and the total) on the host
         std::vector<long long> off(nloc + 1);
@@ -802,7 +813,9 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
         }
         cut.push_back(nloc);
         const int nch = (int)cut.size() - 1;
-        const int nparts = nch * b->grid_loss;
+        std::vector<int> pbase(nch + 1, 0);  // partial slots of each chunk's launch
+        for (int k = 0; k < nch; ++k) pbase[k + 1] = pbase[k] + loss_grid_for(b, cut[k + 1] - cut[k]);
+        const int nparts = pbase[nch];
         if ((size_t)nparts * 32 > b->loss_partials_bytes) b->grow_loss_partials((size_t)nparts * 32);
         const float* hin = lpn;
         if (host_in && !pin_in) {  // pageable: one staged copy (no overlap)
@@ -821,7 +834,7 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
                 RB_CUDA(cudaEventRecord(b->ev_io[1 + 2 * k], b->cs_in));
                 RB_CUDA(cudaStreamWaitEvent(b->stream, b->ev_io[1 + 2 * k], 0));
             }
-            launch_loss(b, c, din, dout, cut[k], cut[k + 1], k * b->grid_loss, nparts, kst, 0);
+            launch_loss(b, c, din, dout, cut[k], cut[k + 1], pbase[k], nparts, kst, 0);
             if (host_out && pin_out) {
                 RB_CUDA(cudaEventRecord(b->ev_io[2 + 2 * k], b->stream));
                 RB_CUDA(cudaStreamWaitEvent(b->cs_out, b->ev_io[2 + 2 * k], 0));
