@@ -444,6 +444,18 @@ def test_side_lookahead_matches(rb, oracle, case, monkeypatch):
     assert counts["samples"] > 0
 
 
+@pytest.mark.parametrize("switch", ["RB_NO_PDL", "RB_PAYLOAD_LSU", "RB_NO_LOOKAHEAD",
+                                    "RB_TMA_CTAS"])
+@pytest.mark.parametrize("case", ["c4_unique_overlap", "c3_unique_overlap_big"])
+def test_env_switches_do_not_change_results(rb, oracle, case, switch, monkeypatch):
+    """Every performance switch leaves the results bit-identical."""
+    from tests.harness import StepConfig, run_step_parity
+
+    monkeypatch.setenv(switch, "1")
+    counts = run_step_parity(StepConfig(**STEP_CASES[case]), steps=8, ora=oracle)
+    assert counts["samples"] > 0
+
+
 def test_side_lookahead_rng_continues_on_host(rb, oracle, monkeypatch):
     monkeypatch.setenv("RB_LOOKAHEAD_MIN_DRAWS", "0")
     buf = rb.ShardedReplayBuffer(2, 64)
