@@ -384,6 +384,7 @@ struct DevLossAcc {
     int need_fixup;
     int pad;
     double* red3;  // registered reduce vector {objective_sum, included, excluded} (or NULL)
+    unsigned claim, pad2;  // claimed work units of a dynamic loss launch (reset by its last CTA)
 };
 
 }  // namespace rb

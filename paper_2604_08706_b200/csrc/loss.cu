@@ -274,6 +274,7 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
         acc->objective = asym ? o * inv_b : (inc ? o / (double)inc : 0.0);
         acc->need_fixup = !asym && exc > 0 && inc > 0;
         acc->done_blocks = 0;
+        acc->claim = 0;  // every CTA has made its last claim
         if (stats) {
             stats->objective_sum = o;
             stats->objective = acc->objective;
@@ -317,7 +318,12 @@ __device__ __noinline__ float grpo_token_exact(float lpn, float lpo, double A,
 // Fast path per token: one ex2, the branch as two threshold compares chosen
 // per unit from sign(A), and an fp32 per-unit objective sum; tokens near a
 // clip edge or with |d| >= 80 / non-finite take grpo_token_exact.
-template <int U>
+//
+// DYN (long trajectories, one launch): units are claimed from a counter
+// (the next claim in flight while the current unit runs) instead of a static
+// stride, so ragged batches — whose later chunks are mostly empty — do not
+// leave a few CTAs with all the full units.
+template <int U, bool DYN>
 // (More CTAs per SM via a register cap spill and run slower: 44 µs at 10
 // CTAs per SM vs 37 µs at 8.)
 __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
@@ -334,15 +340,24 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
     const int nu = nloc * ups;
     GrpoPartial part;
     long long inc_fast = 0;
-    Unit nxt;  // descriptor of the next unit, loaded one unit ahead
-    if ((int)blockIdx.x < nu) nxt = ld_unit(units + blockIdx.x / ups);
-    for (int u = blockIdx.x; u < nu; u += gridDim.x) {
+    __shared__ int s_claim[2];
+    int u = blockIdx.x, p = 0;
+    if (DYN) {
+        if (threadIdx.x == 0) s_claim[0] = (int)atomicAdd(&acc->claim, 1u);
+        __syncthreads();
+        u = s_claim[0];
+    }
+    Unit nxt;  // static stride: descriptor of the next unit, loaded one unit ahead
+    if (!DYN && u < nu) nxt = ld_unit(units + u / ups);
+    for (; u < nu;) {
+        if (DYN && threadIdx.x == 0) s_claim[p ^ 1] = (int)atomicAdd(&acc->claim, 1u);
         const int b = u / ups, c = u - b * ups;
-        const Unit un = nxt;
-        if (u + (int)gridDim.x < nu) nxt = ld_unit(units + (u + (int)gridDim.x) / ups);
+        const Unit un = DYN ? ld_unit(units + b) : nxt;
+        const int un_next = DYN ? 0 : u + (int)gridDim.x;
+        if (!DYN && un_next < nu) nxt = ld_unit(units + un_next / ups);
         const int a = (int)(un.off & 3);
         const int nq = (a + un.len + 3) >> 2;
-        if (c * QU >= nq) continue;
+        if (c * QU < nq) {
         const int nsq = (un.len + 3) >> 2;
         const long long P0 = un.off >> 2;
         const int kw = c * QU + wid * 32 * U;
@@ -417,6 +432,14 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
             }
         }
         part.obj += (double)fsum * A;
+        }
+        if (DYN) {
+            __syncthreads();
+            u = s_claim[p ^ 1];
+            p ^= 1;
+        } else {
+            u = un_next;
+        }
     }
     part.inc += inc_fast;
     RB_GCLOCK(1, blockIdx.x == 0);
@@ -434,7 +457,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
 
 int loss_grid(int sms) {
     int a = 0, b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_loss_grpo_buf<LOSS_U>, UNIT_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_loss_grpo_buf<LOSS_U, false>, UNIT_THREADS, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_loss_asymre_buf<LOSS_U>, UNIT_THREADS, 0);
     return sms * std::max(1, std::min(a, b));
 }
@@ -755,8 +778,15 @@ void launch_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl, l
                  long long s1, int part_base, int nparts, rb_loss_stats* kst, int local_fix) {
     const Unit* u = b->units_sel + s0;
     const int grid = loss_grid_for(b, s1 - s0);
-    if (c.kind == 0)
-        k_loss_grpo_buf<LOSS_U><<<grid, UNIT_THREADS, 0, b->stream>>>(
+    // claimed units for long (ragged-prone) trajectories in a one-launch loss
+    const bool dyn = b->max_tokens > 2 * UNIT_THREADS * LOSS_U * 4 && part_base == 0 &&
+                     nparts == grid;
+    if (c.kind == 0 && dyn)
+        k_loss_grpo_buf<LOSS_U, true><<<grid, UNIT_THREADS, 0, b->stream>>>(
+            b->v, u, b->n_units_sel, (int)(s1 - s0), lpn, dl, c.p, b->acc,
+            (Partial*)b->loss_partials, kst, b->sel_total, local_fix, part_base, nparts);
+    else if (c.kind == 0)
+        k_loss_grpo_buf<LOSS_U, false><<<grid, UNIT_THREADS, 0, b->stream>>>(
             b->v, u, b->n_units_sel, (int)(s1 - s0), lpn, dl, c.p, b->acc,
             (Partial*)b->loss_partials, kst, b->sel_total, local_fix, part_base, nparts);
     else
