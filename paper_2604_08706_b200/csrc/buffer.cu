@@ -1226,7 +1226,10 @@ __device__ __forceinline__ void spin_until_set(const int* flag) {
 // draw) shifts every later draw: its CTA and every later one publish the
 // fact through the look-back word, apply nothing, and the last CTA replays
 // the rest exactly.
-constexpr int MAP_THREADS = 128;  // small: co-resides with the persistent payload grid
+#ifndef RB_MAP_THREADS
+#define RB_MAP_THREADS 128
+#endif
+constexpr int MAP_THREADS = RB_MAP_THREADS;  // small: co-resides with the persistent payload grid
 #ifndef RB_MAP_R
 #define RB_MAP_R 2
 #endif
