@@ -977,6 +977,33 @@ __global__ void k_finalize_vec(DevLossAcc* acc, const double* v3, float* dlogp,
 }
 __global__ void k_set_red3(DevLossAcc* acc, double* v) { acc->red3 = v; }
 
+// rb_loss_finalize in one kernel (reduced rb_loss_stats in, stats out).
+__global__ void k_finalize_stats(DevLossAcc* acc, rb_loss_stats* st, float* dlogp,
+                                 const long long* n_dev) {
+    const double obj = st->objective_sum;
+    const long long inc = st->included, exc = st->excluded;
+    if (dlogp && exc > 0 && inc > 0) {
+        const float f = (float)((double)acc->total_tokens / (double)inc);
+        const long long n = *n_dev;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x)
+            dlogp[i] *= f;
+    }
+    __syncthreads();  // every thread of CTA 0 has read st before it is rewritten
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        acc->obj_sum = obj;
+        acc->included = (unsigned long long)inc;
+        acc->excluded = (unsigned long long)exc;
+        acc->objective = inc ? obj / (double)inc : 0.0;
+        acc->need_fixup = 0;  // applied
+        st->objective_sum = obj;
+        st->objective = acc->objective;
+        st->included = inc;
+        st->excluded = exc;
+        st->total_tokens = acc->total_tokens;
+    }
+}
+
 int rb_loss_set_reduce_vector(rb_buffer* b, double* vec3) {
     return guard([&] {
         if (vec3 && !is_device_ptr(vec3)) invalid("rb_loss_set_reduce_vector: device memory required");
@@ -1017,13 +1044,11 @@ int rb_loss_finalize(rb_buffer* b, float* dlogp, rb_loss_stats* stats) {
             RB_CUDA(cudaMemcpyAsync(dst, stats, sizeof(rb_loss_stats), cudaMemcpyHostToDevice,
                                     b->stream));
         }
-        k_stats_in<<<1, 1, 0, b->stream>>>(b->acc, dst);
-        RB_CUDA(cudaGetLastError());
-        if (b->last_loss == 0 && dlogp) {
-            k_dlogp_rescale<<<148, 256, 0, b->stream>>>(dlogp, 0, b->sel_total, b->acc);
-            RB_CUDA(cudaGetLastError());
-        }
-        k_stats_out<<<1, 1, 0, b->stream>>>(b->acc, dst, 0, 0.0);
+        // one kernel: every CTA reads the reduced stats and rescales its slice
+        // of dlogp if a token was excluded anywhere; CTA 0 updates the
+        // accumulator and writes the stats back
+        k_finalize_stats<<<148, 256, 0, b->stream>>>(b->acc, dst, b->last_loss == 0 ? dlogp : nullptr,
+                                                     b->sel_total);
         RB_CUDA(cudaGetLastError());
         if (host) {
             RB_CUDA(cudaMemcpyAsync(stats, dst, sizeof(rb_loss_stats), cudaMemcpyDeviceToHost,
