@@ -859,9 +859,7 @@ __device__ __forceinline__ void payload_body(const BufView& v, const Unit* desc,
                                    a, kw, ol);
         if (CLOSED && !ready) {  // CTA-uniform: first store of this CTA
             if (threadIdx.x == 0) {
-                int f;
-                while ((f = ld_acquire_i32(&sync[0])) == 0) __nanosleep(64);
-                s_flag = f;
+                s_flag = spin_while_eq(&sync[0], 0);
             }
             __syncthreads();
             if (s_flag != 1) break;  // batch rejected: nothing is applied
@@ -1051,9 +1049,7 @@ __global__ void __launch_bounds__(TP_THREADS) k_insert_payload_tma(BufView v, Fi
                 mbar_wait(&bar[st], (uint32_t)((g / TP_S) & 1));
                 if (s_flag == 0) {  // first store of this CTA: the route's verdict
                     if (tid == 0) {
-                        int f;
-                        while ((f = ld_acquire_i32(&sync[0])) == 0) __nanosleep(64);
-                        s_flag = f;
+                        s_flag = spin_while_eq(&sync[0], 0);
                     }
                     __syncthreads();
                 }
@@ -1208,7 +1204,7 @@ __device__ __forceinline__ unsigned long long lookback(GridCtl* gc, int t) {
     return excl;
 }
 __device__ __forceinline__ void spin_until_set(const int* flag) {
-    while (ld_acquire_i32(flag) == 0) __nanosleep(32);
+    spin_while_eq(flag, 0);  // bounded: traps instead of hanging if never set
 }
 
 // ---- map phase (every sampler): arrival index -> slot, use counts
@@ -1362,8 +1358,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
     }
     RB_GCLOCK(46 + 8 * (t & 1), t < 2);
     if (pi.pending && pi.toff) {  // the route kernel's copy of the insert's offsets
-        if (tid == 0)
-            while (ld_acquire_u64(pi.keep_cnt) < pi.keep_target) __nanosleep(32);
+        if (tid == 0) spin_until_ge_u64(pi.keep_cnt, pi.keep_target);  // bounded: traps, never hangs
         __syncthreads();
     }
     int lv[MAP_R];

@@ -309,6 +309,16 @@ static __device__ __noinline__ int spin_while_eq(const int* f, int v) {
 // Writes made before a programmatic trigger, performed before it executes.
 __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
+static __device__ __noinline__ void spin_until_ge_u64(const unsigned long long* f,
+                                                      unsigned long long v) {
+    if (ld_acquire_u64(f) >= v) return;
+    const unsigned long long t0 = gtimer_ns();
+    while (ld_acquire_u64(f) < v) {
+        __nanosleep(32);
+        if (gtimer_ns() - t0 > 4000000000ULL) __trap();
+    }
+}
+
 // Programmatic dependent launch: let the next kernel of the stream (launched
 // with programmatic serialization) start while this one runs.
 __device__ __forceinline__ void pdl_trigger() {
