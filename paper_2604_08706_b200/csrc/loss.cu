@@ -226,6 +226,7 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
     long long inc = 0, exc = 0;
     // FB partials per thread per round, all loads in flight together; the
     // order of the additions is fixed (bitwise-reproducible objective)
+    // (16 in flight raised the whole kernel to 128 registers: 41 µs vs 37)
     constexpr int FB = 8;
     for (int base = threadIdx.x; base < nparts; base += FB * blockDim.x) {
         double ob[FB];
