@@ -49,3 +49,17 @@ def test_launch_accounting(bench):
     assert bench.launches_per_step(bench.scaled_cfg(c4, 2), 2) == 6      # + finalize
     assert bench.launches_per_step(bench.scaled_cfg(c4, 4), 4) == 7      # + ring lookahead
     assert bench.launches_per_step(bench.CONFIGS["c2"], 1) == 6          # positive bias route
+
+
+def test_documented_switches_exist():
+    """Every environment switch INTEGRATION.md §5 documents is read by the library."""
+    import re
+
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    sec = doc[doc.index("## 5. Environment switches"):]
+    names = set(re.findall(r"`(RB_[A-Z_]+)`", sec))
+    src = "".join(open(os.path.join(ROOT, "paper_2604_08706_b200", "csrc", f)).read()
+                  for f in ("buffer.cu", "loss.cu", "rng.cu"))
+    assert names, "no switches documented"
+    for n in names:
+        assert f'"{n}"' in src, f"{n} documented but not read"
