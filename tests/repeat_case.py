@@ -1,5 +1,5 @@
 """Run one replay-step parity case repeatedly (flake hunting):
-    python tools/repeat_case.py <case> [reps]"""
+    python tests/repeat_case.py <case> [reps]   (test infrastructure: uses the oracle)"""
 import os
 import sys
 import traceback
