@@ -326,6 +326,16 @@ def run_ours(args, rank, world, dist):
         g_standin.replay()
         e_all[3].record(stream)
         torch.cuda.synchronize()
+    # Parity of the timed run against the CPU oracle (outside the timed region)
+    check = None
+    if getattr(args, "check", True):
+        torch.cuda.synchronize()
+        check = parity_check(cfg, wl, Wm + K, buf, rank, world, packed_tok, lpn, dlogp, stats)
+        if dist is not None:
+            ok = torch.tensor([1 if check["parity"] == "ok" else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok) == 0 and check["parity"] == "ok":
+                check["parity"] = "MISMATCH on another rank"
     # Dominant kernel timed alone (roofline.achieved): loss launches on the
     # last batch, each bracketed by CUDA events on the launching stream, with
     # a 256 MB read between launches so no launch starts with the previous
@@ -417,7 +427,109 @@ def run_ours(args, rank, world, dist):
         "launch_mode": "cuda_graph (K steps captured once, launched once)" if use_graph else "eager",
         "clocks": clk.summary(),
     }
+    if check is not None:
+        res["parity"] = check.pop("parity")
+        res["parity_check"] = dict(check, method="last timed step vs the CPU oracle replaying the "
+                                                  "whole schedule (oracle/replay_oracle.c)")
     return res, buf, wl, rng
+
+
+def parity_check(cfg, wl, nsteps, buf, rank, world, packed_tok, lpn, dlogp, stats):
+    """Outside the timed region: replay the whole schedule (warm-up fill + every
+    warm-up and timed step) through the CPU oracle (oracle/, the checker) and
+    compare the LAST step's sampled trajectories, packed offsets and tokens,
+    dL/dlogp (rtol 1e-5, the north star's tolerance) and objective, plus the
+    final shard contents (ids, use counts, frozen advantages) of every shard
+    (replay_buffer.cpp:83-217, bandit.cpp:276-294, 363-438)."""
+    import torch
+
+    from oracle.pyoracle import RECORD_DTYPE, Oracle, same_records
+
+    t0 = time.perf_counter()
+    ora = Oracle()
+    T, N, B, G = world, cfg["capacity"], cfg["batch"], cfg["group"]
+    ob = ora.buffer(T, N, "uniform_with_replacement", cfg["retention"], cfg["delta"])
+    orng = ora.rng(SEED).stream("buffer_sampling")
+    gmean_of = {}
+
+    def push_batch(b, n):
+        if not n:
+            return
+        h = {k: v.cpu().numpy() for k, v in b.items() if k not in ("tokens", "logp_old")}
+        rec = np.zeros(n, RECORD_DTYPE)
+        for k in ("rollout_id", "prompt_id", "group_id", "creation_step", "policy_version",
+                  "reward", "behavior_logprob"):
+            rec[k] = h[k]
+        rec["is_correct"] = h["reward"] == 1.0
+        rw = h["reward"].reshape(-1, G)
+        m = np.zeros(rw.shape[0])
+        for k in range(G):  # bandit.cpp:316-318, the sequential sum
+            m += rw[:, k]
+        m /= G
+        for gi in range(n // G):
+            rec["advantage"][gi * G:(gi + 1) * G] = ora.group_advantages(rw[gi])
+        for i, r in enumerate(rec):
+            gmean_of[int(r["rollout_id"])] = m[i // G]
+            ob.push(r)
+
+    push_batch(wl.warm[0], wl.warm[1])
+    orec = None
+    for i in range(nsteps):
+        b, n, _ = wl.steps[i]
+        push_batch(b, n)
+        orec, _, _ = ob.sample(B, orng)
+    per = B // T
+    own = orec[rank * per:(rank + 1) * per]
+    ids, lens, off = buf.batch_ids()
+    res = {"checked_step": nsteps - 1, "shards_checked": T}
+    bad = []
+    if not np.array_equal(ids, own["rollout_id"]):
+        bad.append("sampled ids")
+    _, want_len, _ = ora.synth_meta(SEED, own["rollout_id"], cfg["lmax"], cfg["ragged"])
+    want_off = np.zeros(per + 1, np.int64)
+    np.cumsum(want_len.astype(np.int64), out=want_off[1:])
+    if not np.array_equal(off, want_off):
+        bad.append("packed offsets")
+    tot = int(want_off[-1])
+    tok_want, lpo_want, _ = ora.synth_payload(SEED, own["rollout_id"], want_len)
+    if not np.array_equal(packed_tok[:tot].cpu().numpy(), tok_want):
+        bad.append("packed tokens")
+    lpn_h = lpn[:tot].cpu().numpy()
+    if not np.array_equal(lpn_h, ora.synth_logp_now(SEED, nsteps, own["rollout_id"], want_off)):
+        bad.append("trainer stand-in logp_now")
+    got = dlogp[:tot].cpu().numpy()
+    st = stats.cpu()
+    obj = float(st[1])
+    if cfg["loss"] == "grpo":
+        d_want, obj_want, inc, exc = ora.loss_grpo_tokens(lpn_h, lpo_want, own["advantage"],
+                                                          want_off, EPS_LOW, EPS_HIGH)
+        sti = st.view(torch.int64)
+        if world > 1:  # the per-rank oracle call normalises by this rank's included tokens
+            d_want = (d_want.astype(np.float64) * (inc / float(sti[2]))).astype(np.float32)
+        res["included"], res["excluded"] = int(sti[2]), int(sti[3])
+        if world == 1 and (res["included"], res["excluded"]) != (inc, exc):
+            bad.append("included/excluded counts")
+    else:
+        gm = np.array([gmean_of[int(i)] for i in own["rollout_id"]])
+        d_want, obj_want = ora.loss_asymre_tokens(lpn_h, own["reward"], gm, want_off, DELTA_V)
+        if world > 1:
+            d_want = d_want / np.float32(world)
+    denom = np.maximum(np.abs(d_want), 1e-30)
+    rel = float(np.max(np.abs(got - d_want) / denom)) if tot else 0.0
+    res["dlogp_max_rel_err"] = rel
+    if not np.allclose(got, d_want, rtol=1e-5, atol=1e-12):
+        bad.append("dlogp")
+    if world == 1:
+        res["objective_rel_err"] = abs(obj - obj_want) / max(1.0, abs(obj_want))
+        if res["objective_rel_err"] > 1e-5:
+            bad.append("objective")
+    for s in range(T):
+        if not same_records(buf.shard_contents(s), ob.shard_contents(s)):
+            bad.append(f"shard {s} contents")
+    res["parity"] = "ok" if not bad else "MISMATCH: " + ", ".join(bad)
+    res["tokens_checked"] = tot
+    res["oracle_s"] = round(time.perf_counter() - t0, 1)
+    return res
 
 
 def launches_per_step(cfg, world):
@@ -757,6 +869,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-check", dest="check", action="store_false",
+                    help="skip the parity check of the last timed step against the CPU oracle")
     ap.add_argument("--eager", dest="graph", action="store_false",
                     help="launch the timed steps eagerly instead of from a CUDA graph")
     ap.add_argument("--emulate-world", type=int, default=0,

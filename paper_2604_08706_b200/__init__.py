@@ -6,6 +6,7 @@ sm_100a CUDA kernels behind the C-ABI of include/replay_b200.h
 (libreplay_b200.so).  This package is a thin mirror of the reference's API
 over that ABI; there is no CPU fallback.
 """
+from ._lib import LossStats
 from .replay import (EVENT_DTYPE, NONE_ID, RECORD_DTYPE, Rng, ShardedReplayBuffer, TransferQueue,
                      asymre_records,
                      asymre_tokens, group_advantages, grpo_records, grpo_tokens, hash_name,
@@ -13,4 +14,4 @@ from .replay import (EVENT_DTYPE, NONE_ID, RECORD_DTYPE, Rng, ShardedReplayBuffe
 
 __all__ = ["Rng", "ShardedReplayBuffer", "TransferQueue", "group_advantages", "grpo_tokens", "grpo_records",
            "asymre_tokens", "asymre_records", "hash_name", "RECORD_DTYPE", "EVENT_DTYPE",
-           "NONE_ID", "summarize_hist"]
+           "NONE_ID", "summarize_hist", "LossStats"]

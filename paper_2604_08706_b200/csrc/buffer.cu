@@ -1121,7 +1121,18 @@ struct SampleArgs {
     int gen_ahead;            // the generator CTA also twists the next call's blocks
     long long occ[64];        // per-shard occupancy after the preceding inserts (draws)
     const long long* occ_dev;  // the same for more than 64 shards (device), else NULL
+    const int* verdict;       // the pending insert's whole-batch verdict (1 valid, 2 rejected)
 };
+
+// A rejected insert leaves a sticky error and freezes the buffer until
+// rb_check: a fused sampler enqueued behind it applies nothing (no use
+// counts, no RNG consumption, an empty batch).  Thread 0; block-uniform via
+// the caller's shared copy.  While the insert may still run, its verdict
+// flag decides (published before any of its records is applied).
+__device__ __forceinline__ int sampler_frozen(const BufView& v, const SampleArgs& a) {
+    if (a.pend.pending) return spin_while_eq(a.verdict, 0) == 2;
+    return *(volatile const int*)&v.ctl->err_code != 0;
+}
 
 // x % n without a 64-bit division: q from a precomputed reciprocal
 // m = floor((2^64-1)/n) underestimates floor(x/n) by at most 2.
@@ -1414,6 +1425,24 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
     }
     __syncthreads();
     RB_GCLOCK(44 + 8 * (t & 1), t < 2);
+    if (DRAW) {
+        __shared__ int s_frozen;
+        if (tid == 0) s_frozen = sampler_frozen(v, a);
+        __syncthreads();
+        if (s_frozen) {  // empty batch: zero-length work units, nothing mutated
+#pragma unroll
+            for (int r = 0; r < MAP_R; ++r) {
+                const long long k = k0 + r;
+                if (!ok[r] || k < a.lo || k >= a.hi) continue;
+                Unit d{};
+                a.units[k - a.lo] = d;
+                a.off[k - a.lo] = 0;
+            }
+            if (tid == 0) gc->cta_max[t] = 0;
+            if (a.early && tid == 0) st_release_i32(&gc->seg[t], 1);
+            return;
+        }
+    }
     if (s_excl & LB_REJ) {  // a rejection at or before this CTA: the last CTA replays
         if (tid == 0) atomicMin(&gc->first_rej, t);
         if (tid == 0) gc->cta_max[t] = 0;
@@ -1546,7 +1575,21 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
     const int first = DRAW ? __ldcg(&gc->first_rej) : INT_MAX;
     const long long D = a.nsel;
     const long long nloc = a.hi - a.lo;
-    if (DRAW && first != INT_MAX) {
+    __shared__ int s_frozen;
+    if (threadIdx.x == 0) s_frozen = DRAW ? sampler_frozen(v, a) : 0;  // final: a map CTA waited for it
+    __syncthreads();
+    const bool frozen = s_frozen != 0;
+    if (frozen) {  // a rejected insert before this sampler: empty batch, ring position unchanged
+        if (threadIdx.x == 0) {
+            s_total = 0;
+            s_g = 0;
+            s_m[0] = 0;
+            s_q = dc.q0;
+            s_idx = dc.idx0;
+            s_genhi = gh;
+        }
+        __syncthreads();
+    } else if (DRAW && first != INT_MAX) {
         // the stream had no rejection before selection k0
         const long long k0 = (long long)first * MAP_SPC;
         long long q = dc.q0;
@@ -1649,7 +1692,8 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        const unsigned long long global = (DRAW && first != INT_MAX) ? atomicAdd(&gc->gsum, 0ULL) : s_g;
+        const unsigned long long global =
+            (DRAW && first != INT_MAX && !frozen) ? atomicAdd(&gc->gsum, 0ULL) : s_g;
         s_g = global;
         a.off[nloc] = s_total;
         a.totals[0] = s_total;
@@ -1664,7 +1708,7 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
         acc->objective = 0.0;
         acc->need_fixup = 0;
         if (DRAW) {
-            const long long qhi = first != INT_MAX ? __ldcg(&gc->gen_hi) : s_genhi;
+            const long long qhi = (first != INT_MAX && !frozen) ? __ldcg(&gc->gen_hi) : s_genhi;
             const long long qn = s_q;
             r->q_state = qn;
             r->idx = s_idx;
@@ -1676,7 +1720,7 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
         gc->first_rej = INT_MAX;
     }
     __syncthreads();
-    if (DRAW && first != INT_MAX && s_q > __ldcg(&gc->gen_hi)) {  // replay went past the ring
+    if (DRAW && first != INT_MAX && !frozen && s_q > __ldcg(&gc->gen_hi)) {  // replay went past the ring
         uint64_t* dst = r->blk[s_q % MT_KR];
         for (int i = threadIdx.x; i < MT_N; i += blockDim.x) dst[i] = mt[i];
     }
@@ -2649,6 +2693,7 @@ void check_sticky(rb_buffer* b) {
     DevCtl c;
     RB_CUDA(cudaMemcpyAsync(&c, b->v.ctl, sizeof c, cudaMemcpyDeviceToHost, b->stream));
     RB_CUDA(cudaStreamSynchronize(b->stream));
+    b->async_unchecked = false;
     if (c.err_code) {
         DevCtl z = c;
         z.err_code = 0;
@@ -2668,6 +2713,13 @@ void check_sticky(rb_buffer* b) {
                 " is already stored");
     }
 }
+
+}  // namespace
+void rb_buffer::sync_checked() {
+    sync();
+    if (async_unchecked) check_sticky(this);
+}
+namespace {
 
 std::string fmt_double(double x) {  // text_io.cpp:10-14 (shortest round trip)
     char buf[64];
@@ -3062,13 +3114,17 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
         // Resolve every input array to device memory (host arrays staged).
         struct Item {
             const void** ptr;
-            size_t bytes;
+            size_t bytes;  // device staging size
+            size_t copy;   // bytes read from the caller's array (<= bytes; the rest is zeroed)
         };
         std::vector<Item> items;
         const int64_t* toff_user = bt.tok_offsets;
-        auto add = [&](const void** p, size_t bytes) {
-            if (*p && !is_device_ptr(*p)) items.push_back({p, bytes});
+        auto add = [&](const void** p, size_t bytes, size_t copy = SIZE_MAX) {
+            if (*p && !is_device_ptr(*p)) items.push_back({p, bytes, std::min(bytes, copy)});
         };
+        // packed device arrays are read with 16-byte vector loads / bulk copies
+        require_aligned16(bt.tokens, "rb_insert: tokens");
+        require_aligned16(bt.logp_old, "rb_insert: logp_old");
         add((const void**)&bt.rollout_id, n * 8);
         add((const void**)&bt.prompt_id, n * 8);
         add((const void**)&bt.group_id, n * 8);
@@ -3094,8 +3150,8 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
                 payload_elems = (size_t)last;
             }
             const size_t pbytes = ((payload_elems + 3) & ~size_t(3)) * 4;
-            add((const void**)&bt.tokens, pbytes);
-            add((const void**)&bt.logp_old, pbytes);
+            add((const void**)&bt.tokens, pbytes, payload_elems * 4);
+            add((const void**)&bt.logp_old, pbytes, payload_elems * 4);
         }
         if (toff_host) {
             for (size_t j = 0; j < n; ++j) {
@@ -3147,8 +3203,10 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
                                                       b->stream));
                         }
                     } else {
-                        RB_CUDA(cudaMemcpyAsync(dsg + o, *it.ptr, it.bytes,
+                        RB_CUDA(cudaMemcpyAsync(dsg + o, *it.ptr, it.copy,
                                                 cudaMemcpyHostToDevice, b->stream));
+                        if (it.copy < it.bytes)
+                            RB_CUDA(cudaMemsetAsync(dsg + o + it.copy, 0, it.bytes - it.copy, b->stream));
                     }
                     *it.ptr = dsg + o;
                     o += sz;
@@ -3159,7 +3217,8 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
             for (auto& it : items) {
                 const size_t sz = (it.bytes + 255) & ~size_t(255);
                 if (*it.ptr >= (const void*)dsg && *it.ptr < (const void*)(dsg + total)) continue;
-                std::memcpy(hs + ho, *it.ptr, it.bytes);
+                std::memcpy(hs + ho, *it.ptr, it.copy);
+                if (it.copy < it.bytes) std::memset(hs + ho + it.copy, 0, it.bytes - it.copy);
                 *it.ptr = dsg + paged_base + ho;
                 ho += sz;
             }
@@ -3169,6 +3228,7 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
                 b->host_stage_issued();
             }
         }
+        if (flags & RB_INSERT_ASSUME_UNIQUE) b->async_unchecked = true;
         const bool want_evrec = (flags & 0x100) != 0;  // internal: rb_push
         launch_insert(b, bt, want_evrec, (flags & RB_INSERT_ASSUME_UNIQUE) != 0);
         if (out_evicted_ids) {
@@ -3252,6 +3312,11 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         if (batch_size == 0 || batch_size % T != 0)  // replay_buffer.cpp:189-192
             invalid("ShardedReplayBuffer: batch size must be a positive multiple of the shard count");
         const size_t per = batch_size / T;
+        // An asynchronous insert may have been rejected on the device (sticky
+        // error): the fused sampler checks that itself (it freezes, applying
+        // nothing); the serial without-replacement path, which sizes its
+        // draws from the host mirrors, checks first.
+        if (b->strategy != RB_UNIFORM_WITH_REPLACEMENT && b->async_unchecked) check_sticky(b);
         // The reference fails at the first empty (197-199) or too-small
         // (148-150, without replacement) shard after mutating earlier shards.
         size_t nsh = T;
@@ -3289,6 +3354,7 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         a.acc = b->acc;
         a.units = b->units_sel;
         a.n_units = b->n_units_sel;
+        a.verdict = b->pay_sync;
         const unsigned nmap = (unsigned)std::max<size_t>(1, (nsel + MAP_SPC - 1) / MAP_SPC);
         if (nmap > (unsigned)GRID_MAX_CTAS) invalid("rb_sample: batch too large");
         bool fused = false;
@@ -3414,7 +3480,12 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         const bool host_out = (out_records && !is_device_ptr(out_records)) ||
                               (out_events && !is_device_ptr(out_events)) ||
                               (out_index && !is_device_ptr(out_index));
-        if (host_out) b->sync();
+        if (host_out) {
+            b->sync();
+            // results handed back while an asynchronous insert was rejected
+            // would be those of an empty (frozen) batch: report the error
+            if (b->async_unchecked) check_sticky(b);
+        }
         if (!err.empty()) {
             b->sync();
             invalid(err);
@@ -3432,7 +3503,7 @@ int rb_batch_total_tokens(rb_buffer* b, int64_t* total) {
         DeviceScope ds(b->device);
         long long t[2];
         RB_CUDA(cudaMemcpyAsync(t, b->sel_total, sizeof t, cudaMemcpyDeviceToHost, b->stream));
-        b->sync();
+        b->sync_checked();
         *total = t[0];
     });
 }
@@ -3442,6 +3513,8 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
         DeviceScope ds(b->device);
         if (b->stride == 0 && (out_tokens || out_logp_old))
             invalid("rb_gather: buffer holds no token payload (max_tokens = 0)");
+        require_aligned16(out_tokens, "rb_gather: out_tokens");
+        require_aligned16(out_logp_old, "rb_gather: out_logp_old");
         const size_t per = b->T ? (b->B / b->T) : 0;
         const long long lo = (long long)std::min(b->sb * per, b->B);
         const long long hi = (long long)std::min(b->se * per, b->B);
@@ -3497,7 +3570,7 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
         if (out_offsets)
             RB_CUDA(cudaMemcpyAsync(out_offsets, b->sel_off, (nloc + 1) * 8, cudaMemcpyDefault,
                                     b->stream));
-        if (ht || hl || (out_offsets && !is_device_ptr(out_offsets))) b->sync();
+        if (ht || hl || (out_offsets && !is_device_ptr(out_offsets))) b->sync_checked();
     });
 }
 
@@ -3519,7 +3592,7 @@ int rb_batch_ids(rb_buffer* b, uint64_t* out_ids, int32_t* out_lengths, int64_t*
         if (hlen) RB_CUDA(cudaMemcpyAsync(out_lengths, dlen, n * 4, cudaMemcpyDeviceToHost, b->stream));
         if (out_offsets)
             RB_CUDA(cudaMemcpyAsync(out_offsets, b->sel_off, (n + 1) * 8, cudaMemcpyDefault, b->stream));
-        if (hid || hlen || (out_offsets && !is_device_ptr(out_offsets))) b->sync();
+        if (hid || hlen || (out_offsets && !is_device_ptr(out_offsets))) b->sync_checked();
     });
 }
 

@@ -92,6 +92,7 @@ struct rb_buffer {
     // host mirrors (exact; updated when an insert is applied)
     std::vector<long long> h_pushes;
     size_t h_cursor = 0;
+    bool async_unchecked = false;  // an RB_INSERT_ASSUME_UNIQUE insert ran since the last sticky check
 
     // scratch (device), grown on demand
     size_t ins_cap = 0;
@@ -179,4 +180,5 @@ struct rb_buffer {
     void ensure_insert(size_t n);
     void ensure_select(size_t n);
     void sync();
+    void sync_checked();  // sync(), then report a sticky error left by an asynchronous insert
 };

@@ -52,6 +52,13 @@ void require_device();
 // Pointer classification: true if `p` is device memory / page-locked host memory.
 bool is_device_ptr(const void* p);
 bool is_pinned_ptr(const void* p);
+// Packed device arrays are accessed with 16-byte vector loads / stores and
+// bulk copies: a misaligned device pointer (e.g. a torch slice x[1:]) is an
+// RB_EINVAL, not a misaligned-address fault that poisons the context.
+inline void require_aligned16(const void* p, const char* what) {
+    if (p && ((uintptr_t)p & 15) != 0 && is_device_ptr(p))
+        throw Error(RB_EINVAL, std::string(what) + ": device array must be 16-byte aligned");
+}
 
 // ---- MT19937-64 (rng.hpp:68, std::mt19937_64 per [rand.predef]) --------
 constexpr int MT_N = 312;
@@ -392,9 +399,12 @@ struct DevLossAcc {
     long long total_tokens;  // normaliser used for the optimistic scale
     double objective;
     int need_fixup;
-    int pad;
+    int kind;      // loss that filled the accumulator: 0 GRPO, 1 AsymRE
     double* red3;  // registered reduce vector {objective_sum, included, excluded} (or NULL)
-    unsigned claim, pad2;  // claimed work units of a dynamic loss launch (reset by its last CTA)
+    unsigned claim;   // claimed work units of a dynamic loss launch (reset by its last CTA)
+    unsigned fin_cnt; // CTAs of a finalize kernel past their reads of the accumulator
+    double inv_b;    // AsymRE: 1 / B (objective = obj_sum * inv_b)
+    double cur_div;  // GRPO: the divisor D baked into dlogp (dlogp = -g / D); 0 = total_tokens
 };
 
 }  // namespace rb

@@ -8,13 +8,18 @@
 //   rb_group_advantages, rb_grpo_tokens, rb_grpo_records, rb_asymre_*:
 //                     the same arithmetic over explicit arrays.
 //
-// Precision: the ratio is evaluated in fp32 (expf) and the branch decided in
-// fp32 unless the token sits within 4e-6 (relative) of a clip edge, has
-// |logp_now - logp_old| >= 80 or is non-finite; those tokens are recomputed
-// exactly as the reference does, in fp64 (exp, clamp, r*A <= c*A with ties to
-// the unclipped branch, non-finite => excluded).  Objective terms accumulate
-// in fp64.  dlogp is written with the optimistic scale -1/total_tokens; if any
-// token was excluded, the last CTA flags a rescale to -1/included.
+// Precision: the ratio is evaluated in fp32 (one ex2.approx) and the branch
+// decided in fp32 unless the token sits within 4e-6 (relative) of a clip
+// edge, has |logp_now - logp_old| >= RB_FAST_D (16) or is non-finite; those
+// tokens are recomputed exactly as the reference does, in fp64 (exp, clamp,
+// r*A <= c*A with ties to the unclipped branch, non-finite => excluded).  On
+// the fast path the fp32 difference d (<= 0.5 ulp(16)), the product
+// d*log2(e) (<= 0.5 ulp(23)) and ex2.approx (~2 ulp) bound the ratio's
+// relative error by ~2e-6, inside the north star's 1e-5
+// (tests/test_gpu_bench_shapes.py sweeps |d| up to 79 at 1e-5).  Objective
+// terms accumulate in fp64 (per-thread unit sums included).  dlogp is
+// written with the optimistic scale -1/total_tokens; if any token was
+// excluded, the last CTA flags a rescale to -1/included.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -27,6 +32,9 @@ using namespace rb;
 
 namespace rb {
 
+// |logp_now - logp_old| below which the fp32 fast path evaluates a token
+#define RB_FAST_D 16.f
+
 struct GrpoParams {
     float lo_f, hi_f;    // 1-eps_low, 1+eps_high (fp32)
     double lo, hi;       // same in fp64
@@ -37,48 +45,12 @@ struct GrpoPartial {
     long long inc = 0, exc = 0;
 };
 
-// One token of the hot kernel: like grpo_token below, but the fast path adds
-// the (ratio | clip bound) of the objective term to a per-unit fp32 sum that
-// is scaled by A once per unit (no per-token fp64 conversion on the XU pipe).
-__device__ __forceinline__ float grpo_token_unit(float lpn, float lpo, double A, float Af,
-                                                 int sgn, const GrpoParams& p, GrpoPartial& acc,
-                                                 float& fsum) {
-    const float d = lpn - lpo;
-    const float r = __expf(d);
-    const bool edge = !(fabsf(d) < 80.f) || fabsf(r - p.hi_f) <= 4e-6f * p.hi_f ||
-                      fabsf(r - p.lo_f) <= 4e-6f * p.lo_f;
-    if (!edge) {
-        ++acc.inc;
-        const bool unclipped = sgn > 0 ? r <= p.hi_f : (sgn < 0 ? r >= p.lo_f : true);
-        if (unclipped) {
-            fsum += r;
-            return Af * r;
-        }
-        fsum += sgn > 0 ? p.hi_f : p.lo_f;
-        return 0.f;
-    }
-    const double rd = exp((double)lpn - (double)lpo);
-    if (!isfinite(rd)) {  // bandit.cpp:381-386
-        ++acc.exc;
-        return 0.f;
-    }
-    ++acc.inc;
-    const double c = rd < p.lo ? p.lo : (p.hi < rd ? p.hi : rd);  // std::clamp
-    const double uv = __dmul_rn(rd, A), cv = __dmul_rn(c, A);
-    if (uv <= cv) {  // ties -> unclipped (bandit.cpp:392)
-        acc.obj += uv;
-        return (float)(A * rd);
-    }
-    acc.obj += cv;
-    return 0.f;
-}
-
 // One token (bandit.cpp:380-400).  Returns the un-normalised coefficient.
 __device__ __forceinline__ float grpo_token(float lpn, float lpo, double A, float Af,
                                             const GrpoParams& p, GrpoPartial& acc) {
     const float d = lpn - lpo;
     const float r = __expf(d);
-    const bool edge = !(fabsf(d) < 80.f) || fabsf(r - p.hi_f) <= 4e-6f * p.hi_f ||
+    const bool edge = !(fabsf(d) < RB_FAST_D) || fabsf(r - p.hi_f) <= 4e-6f * p.hi_f ||
                       fabsf(r - p.lo_f) <= 4e-6f * p.lo_f;
     if (!edge) {
         ++acc.inc;
@@ -274,6 +246,10 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
         }
         acc->objective = asym ? o * inv_b : (inc ? o / (double)inc : 0.0);
         acc->need_fixup = !asym && exc > 0 && inc > 0;
+        acc->kind = asym;
+        acc->inv_b = inv_b;
+        // dlogp was written as -g / total_tokens; the local fix below makes it -g / included
+        acc->cur_div = (acc->need_fixup && local_fix) ? (double)inc : (double)acc->total_tokens;
         acc->done_blocks = 0;
         acc->claim = 0;  // every CTA has made its last claim
         if (stats) {
@@ -380,7 +356,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
         const int sgn = A > 0.0 ? 1 : (A < 0.0 ? -1 : 0);
         const float thr = sgn > 0 ? prm.hi_f : prm.lo_f;
         const float tol = sgn > 0 ? tol_hi : tol_lo;
-        float fsum = 0.f;
+        double fsum = 0.0;  // fp64: the objective matches the reference's fp64 sum
 #pragma unroll
         for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
@@ -396,7 +372,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
                     for (int i = 0; i < 4; ++i) {
                         const float d = qf(now[s], i) - qf(old[s], i);
                         r[i] = exp_ftz(d);
-                        edge |= !(d < 80.f) || (sgn != 0 && fabsf(r[i] - thr) <= tol);
+                        edge |= !(fabsf(d) < RB_FAST_D) || (sgn != 0 && fabsf(r[i] - thr) <= tol);
                     }
                     if (!edge) {
                         if (sgn > 0) {
@@ -404,14 +380,14 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
                             for (int i = 0; i < 4; ++i) {
                                 const bool unc = r[i] <= thr;
                                 o[i] = unc ? Afs * r[i] : 0.f;
-                                fsum += unc ? r[i] : thr;
+                                fsum += (double)(unc ? r[i] : thr);
                             }
                         } else if (sgn < 0) {
 #pragma unroll
                             for (int i = 0; i < 4; ++i) {
                                 const bool unc = r[i] >= thr;
                                 o[i] = unc ? Afs * r[i] : 0.f;
-                                fsum += unc ? r[i] : thr;
+                                fsum += (double)(unc ? r[i] : thr);
                             }
                         }
                         inc_fast += 4;
@@ -432,7 +408,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
                                   e0, un.len);
             }
         }
-        part.obj += (double)fsum * A;
+        part.obj += fsum * A;
         }
         if (DYN) {
             __syncthreads();
@@ -492,6 +468,9 @@ __global__ void __launch_bounds__(256) k_loss_grpo_packed(const float* lpn, cons
     grpo_block_commit(part, acc);
 }
 
+__global__ void k_set_cur_div_included(DevLossAcc* acc) {
+    if (acc->need_fixup) acc->cur_div = (double)acc->included;
+}
 __global__ void k_dlogp_rescale(float* d, long long n, const long long* n_dev,
                                 const DevLossAcc* acc) {
     if (!acc->need_fixup) return;
@@ -536,7 +515,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
             const int k = kw + 32 * s + lane;
             now[s] = k < nq ? ld_stream(lpn_packed + 4 * (P0 + k)) : make_uint4(0, 0, 0, 0);
         }
-        float fs = 0.f;
+        double fs = 0.0;  // fp64 sum of logp_now (the reference's objective is fp64)
 #pragma unroll
         for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
@@ -544,11 +523,11 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
                 const int e0 = 4 * k - a;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    if (e0 + i >= 0 && e0 + i < un.len) fs += qf(now[s], i);
+                    if (e0 + i >= 0 && e0 + i < un.len) fs += (double)qf(now[s], i);
                 store_quad_masked(reinterpret_cast<uint32_t*>(dlogp), P0 + k, gq, e0, un.len);
             }
         }
-        part.obj += coef * (double)fs;
+        part.obj += coef * fs;
     }
     loss_commit(part, parts, acc, stats, 1, inv_b, dlogp, nullptr, 0, part_base, nparts);
 }
@@ -670,13 +649,6 @@ __global__ void k_stats_out(const DevLossAcc* acc, rb_loss_stats* out, int asym,
     out->included = (long long)acc->included;
     out->excluded = (long long)acc->excluded;
     out->total_tokens = acc->total_tokens;
-}
-__global__ void k_stats_in(DevLossAcc* acc, const rb_loss_stats* in) {
-    acc->obj_sum = in->objective_sum;
-    acc->included = (unsigned long long)in->included;
-    acc->excluded = (unsigned long long)in->excluded;
-    acc->objective = in->included ? in->objective_sum / (double)in->included : 0.0;
-    acc->need_fixup = in->excluded > 0 && in->included > 0;
 }
 
 // ---- stateless context: stream + staging per process ---------------------
@@ -807,6 +779,8 @@ constexpr int LOSS_CHUNKS = 8;  // host-buffer pipeline depth (16 measured slowe
 // re-downloads dlogp after the pipeline.
 void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
               rb_loss_stats* stats) {
+    require_aligned16(lpn, "loss: logp_now");
+    require_aligned16(dl, "loss: out_dlogp");
     b->other_work();
     b->join_lookahead();  // the step's ring lookahead rejoins the stream here (graph capture)
     const size_t per = b->T ? b->B / b->T : 0;
@@ -881,6 +855,7 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
         const bool fix = c.kind == 0 && acc.need_fixup && single;
         if (fix) {  // -1/total -> -1/included (rare: a non-finite ratio)
             k_dlogp_rescale<<<grid_for(total), 256, 0, b->stream>>>(dout, total, nullptr, b->acc);
+            k_set_cur_div_included<<<1, 1, 0, b->stream>>>(b->acc);  // after every rescale CTA read it
             RB_CUDA(cudaGetLastError());
         }
         if (host_out && (!pin_out || fix)) {
@@ -890,7 +865,7 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
     }
     if (stats && !dev_stats) {
         RB_CUDA(cudaMemcpyAsync(stats, kst, sizeof *stats, cudaMemcpyDeviceToHost, b->stream));
-        b->sync();
+        b->sync_checked();
     }
 }
 
@@ -949,23 +924,55 @@ int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double
 // After the all-reduce of the reduce vector: every CTA derives the global
 // normalisation from it and rescales its slice of dlogp if a token was
 // excluded anywhere (GRPO); CTA 0 updates the accumulator and the stats.
+// The global GRPO normalisation: dlogp holds -g / acc->cur_div (the loss
+// kernel's total_tokens, or the single-process fix's included count); the
+// target is -g / inc (bandit.cpp:402-406).  Idempotent: a second finalize
+// (or one after the local fix) finds cur_div == inc and leaves dlogp alone.
+__device__ __forceinline__ bool finalize_scale(const DevLossAcc* acc, unsigned long long inc,
+                                               float* f) {
+    if (inc == 0) return false;  // every token excluded: dlogp is already all zeros
+    const double cur = acc->cur_div > 0.0 ? acc->cur_div : (double)acc->total_tokens;
+    if (cur == (double)inc) return false;
+    *f = (float)(cur / (double)inc);
+    return true;
+}
+// Barrier over the finalize grid's reads of acc (before CTA 0 rewrites it):
+// every CTA reads cur_div first, then CTA 0 waits for the others.
+__device__ __forceinline__ void finalize_publish_wait(unsigned* cnt) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned t = done_add_u32(cnt);
+        if (blockIdx.x == 0) {
+            const unsigned long long t0 = gtimer_ns();
+            while (ld_acquire_i32((const int*)cnt) < (int)gridDim.x) {
+                __nanosleep(32);
+                if (gtimer_ns() - t0 > 4000000000ULL) __trap();
+            }
+        }
+        (void)t;
+    }
+    __syncthreads();
+}
 __global__ void k_finalize_vec(DevLossAcc* acc, const double* v3, float* dlogp,
                                const long long* n_dev, rb_loss_stats* st, int grpo) {
     const double obj = v3[0];
     const unsigned long long inc = (unsigned long long)v3[1], exc = (unsigned long long)v3[2];
-    const bool fix = grpo && exc > 0 && inc > 0;
+    float f = 1.f;
+    const bool fix = grpo && finalize_scale(acc, inc, &f);
     if (fix && dlogp) {
-        const float f = (float)((double)acc->total_tokens / (double)inc);
         const long long n = *n_dev;
         for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
              i += (long long)gridDim.x * blockDim.x)
             dlogp[i] *= f;
     }
+    finalize_publish_wait(&acc->fin_cnt);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        acc->fin_cnt = 0;
         acc->obj_sum = obj;
         acc->included = inc;
         acc->excluded = exc;
-        acc->objective = inc ? obj / (double)inc : 0.0;
+        acc->objective = grpo ? (inc ? obj / (double)inc : 0.0) : obj * acc->inv_b;
+        if (grpo && inc) acc->cur_div = (double)inc;
         acc->need_fixup = 0;  // applied
         if (st) {
             st->objective_sum = obj;
@@ -980,22 +987,24 @@ __global__ void k_set_red3(DevLossAcc* acc, double* v) { acc->red3 = v; }
 
 // rb_loss_finalize in one kernel (reduced rb_loss_stats in, stats out).
 __global__ void k_finalize_stats(DevLossAcc* acc, rb_loss_stats* st, float* dlogp,
-                                 const long long* n_dev) {
+                                 const long long* n_dev, int grpo) {
     const double obj = st->objective_sum;
     const long long inc = st->included, exc = st->excluded;
-    if (dlogp && exc > 0 && inc > 0) {
-        const float f = (float)((double)acc->total_tokens / (double)inc);
+    float f = 1.f;
+    if (grpo && dlogp && finalize_scale(acc, (unsigned long long)(inc > 0 ? inc : 0), &f)) {
         const long long n = *n_dev;
         for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
              i += (long long)gridDim.x * blockDim.x)
             dlogp[i] *= f;
     }
-    __syncthreads();  // every thread of CTA 0 has read st before it is rewritten
+    finalize_publish_wait(&acc->fin_cnt);  // every CTA has read st and acc before they are rewritten
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        acc->fin_cnt = 0;
         acc->obj_sum = obj;
         acc->included = (unsigned long long)inc;
         acc->excluded = (unsigned long long)exc;
-        acc->objective = inc ? obj / (double)inc : 0.0;
+        acc->objective = grpo ? (inc ? obj / (double)inc : 0.0) : obj * acc->inv_b;
+        if (grpo && inc > 0) acc->cur_div = (double)inc;
         acc->need_fixup = 0;  // applied
         st->objective_sum = obj;
         st->objective = acc->objective;
@@ -1049,7 +1058,7 @@ int rb_loss_finalize(rb_buffer* b, float* dlogp, rb_loss_stats* stats) {
         // of dlogp if a token was excluded anywhere; CTA 0 updates the
         // accumulator and writes the stats back
         k_finalize_stats<<<148, 256, 0, b->stream>>>(b->acc, dst, b->last_loss == 0 ? dlogp : nullptr,
-                                                     b->sel_total);
+                                                     b->sel_total, b->last_loss == 0 ? 1 : 0);
         RB_CUDA(cudaGetLastError());
         if (host) {
             RB_CUDA(cudaMemcpyAsync(stats, dst, sizeof(rb_loss_stats), cudaMemcpyDeviceToHost,
@@ -1110,6 +1119,9 @@ int rb_grpo_tokens(const float* logp_now, const float* logp_old, const double* a
             last = offsets[n_traj];
         }
         if (first != 0) invalid("rb_grpo_tokens: offsets must start at 0");
+        require_aligned16(logp_now, "rb_grpo_tokens: logp_now");
+        require_aligned16(logp_old, "rb_grpo_tokens: logp_old");
+        require_aligned16(out_dlogp, "rb_grpo_tokens: out_dlogp");
         const size_t nt = ((size_t)last + 3) & ~size_t(3);
         std::vector<std::pair<void*, std::pair<void*, size_t>>> back;
         const float* lpn = c.in(logp_now, (size_t)last);

@@ -26,12 +26,12 @@ if [[ $what == ncu || $what == all ]]; then
   # launch list of one short bench run (cold-cache, serialised: compare shares)
   timeout 600 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
       --clock-control none -k regex:'^k_' -c 400 --csv --log-file $out/launches.csv \
-      python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --eager > $out/ncu_bench.log 2>&1
+      python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-check --eager > $out/ncu_bench.log 2>&1
   echo "launches: $(grep -c k_ $out/launches.csv)"
   # full captures of the heavy kernels in steady state
   for k in ${NCU_KERNELS:-k_loss_grpo_buf k_gather k_insert_payload_tma k_route_fifo k_sample_fused}; do
     timeout 600 $NCU --set full --clock-control none --import-source on -k regex:"^$k\$" -s 4 -c 1 \
-        -o $out/prof_$k -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --eager \
+        -o $out/prof_$k -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-check --eager \
         > $out/ncu_$k.log 2>&1
     echo "$k: $(ls -la $out/prof_$k.ncu-rep 2>/dev/null | awk '{print $5}')"
   done
