@@ -110,6 +110,8 @@ class Oracle:
         L.or_group_advantages.argtypes = [vp, sz, vp]
         L.or_loss_grpo_tokens.argtypes = [vp, vp, vp, vp, sz, dbl, dbl, vp, vp, vp, vp]
         L.or_loss_grpo_records.argtypes = [vp, vp, vp, sz, dbl, dbl, vp, vp, vp, vp]
+        L.or_loss_grpo_tokens_mode.argtypes = [vp, vp, vp, vp, vp, sz, dbl, dbl, C.c_int, vp, vp,
+                                               vp, vp]
         L.or_loss_asymre_tokens.argtypes = [vp, vp, vp, vp, sz, dbl, vp, vp]
         L.or_loss_asymre_records.argtypes = [vp, vp, vp, sz, dbl, vp, vp]
         L.or_production_groups.restype = i64
@@ -179,6 +181,23 @@ class Oracle:
         exc = np.zeros(1, np.int64)
         self.lib.or_loss_grpo_tokens(_p(lpn), _p(lpo), _p(a), _p(off), a.size, eps_low,
                                      eps_high, _p(d), _p(obj), _p(inc), _p(exc))
+        return d, float(obj[0]), int(inc[0]), int(exc[0])
+
+    def loss_grpo_tokens_mode(self, logp_now, logp_old, adv, offsets, mode, blp=None,
+                              eps_low=0.2, eps_high=0.2):
+        """mode 0 token mean, 1 per-sequence mean, 2 sequence ratio (replay_oracle.c)."""
+        lpn = np.ascontiguousarray(logp_now, np.float32)
+        lpo = np.ascontiguousarray(logp_old, np.float32)
+        a = np.ascontiguousarray(adv, np.float64)
+        b = None if blp is None else np.ascontiguousarray(blp, np.float64)
+        off = np.ascontiguousarray(offsets, np.int64)
+        d = np.zeros(lpn.size, np.float32)
+        obj = np.zeros(1, np.float64)
+        inc = np.zeros(1, np.int64)
+        exc = np.zeros(1, np.int64)
+        self.lib.or_loss_grpo_tokens_mode(_p(lpn), _p(lpo), _p(a), _p(b), _p(off), a.size,
+                                          eps_low, eps_high, int(mode), _p(d), _p(obj), _p(inc),
+                                          _p(exc))
         return d, float(obj[0]), int(inc[0]), int(exc[0])
 
     def loss_grpo_records(self, logp_now, blp, adv, eps_low=0.2, eps_high=0.2):

@@ -448,6 +448,87 @@ void or_loss_grpo_tokens(const float* logp_now, const float* logp_old, const dou
     free(coef);
 }
 
+/* GRPO normalisation modes at the token level (SURVEY.md §8c "token
+ * generalisation"; the reference has no tokens):
+ *   mode 0  per-token ratio, mean over the batch's included tokens
+ *           (or_loss_grpo_tokens above);
+ *   mode 1  per-token ratio, mean over each sequence's included tokens, then
+ *           mean over the sequences with at least one included token:
+ *           objective = (1/S) sum_i (1/n_i) sum_t term_t,
+ *           dL/dlogp_t = -coef_t / (n_i * S); included = S;
+ *   mode 2  sequence-level ratio pi(z|q)/pi_old(z|q):
+ *           the reference's record-level grpo_loss_grad (bandit.cpp:363-408)
+ *           with logp_now(record) = sum_t logp_now_t (fp64, token order) and
+ *           behavior_logprob = blp[i] (the record field, bandit.cpp:380; NULL:
+ *           sum_t logp_old_t); every token of sequence i gets the record's
+ *           dL/dlogp = -coef_i / included; included/excluded count sequences.
+ * dlogp is rounded to fp32 once from the fp64 value. */
+void or_loss_grpo_tokens_mode(const float* logp_now, const float* logp_old, const double* adv,
+                              const double* blp, const int64_t* offsets, size_t n_traj,
+                              double eps_low, double eps_high, int mode, float* dlogp,
+                              double* objective, int64_t* included, int64_t* excluded) {
+    if (mode == 0) {
+        or_loss_grpo_tokens(logp_now, logp_old, adv, offsets, n_traj, eps_low, eps_high, dlogp,
+                            objective, included, excluded);
+        return;
+    }
+    double obj = 0.0;
+    int64_t inc = 0, exc = 0;
+    const int64_t total = offsets[n_traj];
+    double* coef = (double*)malloc((size_t)(total ? total : 1) * sizeof(double));
+    double* seqn = (double*)malloc((n_traj ? n_traj : 1) * sizeof(double)); /* mode 1: n_i */
+    for (size_t i = 0; i < n_traj; ++i) {
+        const int64_t o0 = offsets[i], o1 = offsets[i + 1];
+        if (mode == 2) {
+            double lp = 0.0, lo = 0.0;
+            for (int64_t t = o0; t < o1; ++t) {
+                lp += (double)logp_now[t];
+                lo += (double)logp_old[t];
+            }
+            double term, c;
+            if (grpo_unit(lp, blp ? blp[i] : lo, adv[i], eps_low, eps_high, &term, &c)) {
+                ++inc;
+                obj += term;
+            } else {
+                ++exc;
+                c = 0.0;
+            }
+            for (int64_t t = o0; t < o1; ++t) coef[t] = c;
+        } else {
+            double sum = 0.0;
+            int64_t n = 0;
+            for (int64_t t = o0; t < o1; ++t) {
+                double term, c;
+                if (grpo_unit((double)logp_now[t], (double)logp_old[t], adv[i], eps_low, eps_high,
+                              &term, &c)) {
+                    ++n;
+                    sum += term;
+                    coef[t] = c;
+                } else {
+                    ++exc;
+                    coef[t] = 0.0;
+                }
+            }
+            seqn[i] = (double)n;
+            if (n > 0) {
+                ++inc;
+                obj += sum / (double)n;
+            }
+        }
+    }
+    const double scale = inc > 0 ? 1.0 / (double)inc : 0.0;
+    for (size_t i = 0; i < n_traj; ++i) {
+        const double ni = mode == 1 ? seqn[i] : 1.0;
+        for (int64_t t = offsets[i]; t < offsets[i + 1]; ++t)
+            dlogp[t] = (inc > 0 && ni > 0) ? (float)(-coef[t] / (ni * (double)inc)) : 0.0f;
+    }
+    *objective = inc > 0 ? obj * scale : 0.0;
+    *included = inc;
+    *excluded = exc;
+    free(coef);
+    free(seqn);
+}
+
 void or_loss_grpo_records(const double* logp_now, const double* behavior_logprob,
                           const double* adv, size_t n, double eps_low, double eps_high,
                           double* dlogp, double* objective, int64_t* included,

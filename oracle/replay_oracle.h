@@ -95,6 +95,12 @@ void or_loss_grpo_tokens(const float* logp_now, const float* logp_old, const dou
                          const int64_t* offsets, size_t n_traj, double eps_low,
                          double eps_high, float* dlogp, double* objective, int64_t* included,
                          int64_t* excluded);
+/* GRPO normalisation modes (0 token mean, 1 per-sequence mean, 2 sequence
+ * ratio); see replay_oracle.c.  blp may be NULL (sum of logp_old). */
+void or_loss_grpo_tokens_mode(const float* logp_now, const float* logp_old, const double* adv,
+                              const double* blp, const int64_t* offsets, size_t n_traj,
+                              double eps_low, double eps_high, int mode, float* dlogp,
+                              double* objective, int64_t* included, int64_t* excluded);
 /* Same over fp64 per-record inputs with fp64 output (the L=1 record form). */
 void or_loss_grpo_records(const double* logp_now, const double* behavior_logprob,
                           const double* adv, size_t n, double eps_low, double eps_high,

@@ -44,8 +44,45 @@ SCHEDULES = {
 STEPS = 40
 
 
+def seq_ratio_golden(ref: Reference) -> dict:
+    """Sequence-level GRPO: ragged token trajectories whose
+    record-level inputs are logp_now = sum_t logp_now_t and behavior_logprob =
+    sum_t logp_old_t (fp64, token order), run through the reference's own
+    grpo_loss_grad (bandit.cpp:363-408) by the 2-arm embedding.  Every token of
+    trajectory i must get the record's dL/dlogp."""
+    rs = np.random.default_rng(2604)
+    n = 48
+    lens = rs.integers(1, 41, n)
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    tot = int(off[-1])
+    lpo = (-rs.uniform(0.005, 0.2, tot)).astype(np.float32)
+    lpn = (lpo.astype(np.float64) + rs.normal(0.0, 0.02, tot)).astype(np.float32)
+    lpn = np.minimum(lpn, np.float32(-1e-4))
+    recs = np.zeros(n, RECORD_DTYPE)
+    blp = np.array([float(np.sum(lpo[off[i]:off[i + 1]].astype(np.float64))) for i in range(n)])
+    want = np.zeros(n)
+    for i in range(n):  # sequential fp64 sums, token order
+        a = b = 0.0
+        for t in range(off[i], off[i + 1]):
+            a += float(lpn[t])
+            b += float(lpo[t])
+        want[i], blp[i] = a, b
+    recs["behavior_logprob"] = blp
+    recs["advantage"] = rs.normal(size=n)
+    recs["advantage"][::11] = 0.0
+    used, d, obj, exc = ref.loss_records("grpo", want, recs, eps_low=0.2, eps_high=0.28)
+    return {"seq_offsets": off, "seq_logp_old": lpo, "seq_logp_now": lpn, "seq_blp": blp,
+            "seq_adv": recs["advantage"].copy(), "seq_logp_used": used, "seq_dlogp_record": d,
+            "seq_obj": np.float64(obj), "seq_excluded": np.int64(exc)}
+
+
 def main():
     build_oracle(with_ref=True)
+    if "--seq-only" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "golden_seq.npz"), **seq_ratio_golden(Reference()))
+        print("wrote", os.path.join(HERE, "golden_seq.npz"))
+        return
     ref = Reference()
     ora = Oracle()
     out = {}
@@ -115,6 +152,7 @@ def main():
         out[f"sched_{name}_dump"] = np.frombuffer(buf.dump().encode(), np.uint8)
         meta[name] = cfg.__dict__
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
+    np.savez_compressed(os.path.join(HERE, "golden_seq.npz"), **seq_ratio_golden(ref))
     with open(os.path.join(HERE, "schedules.json"), "w") as f:
         json.dump({"steps": STEPS, "schedules": meta}, f, indent=1, sort_keys=True)
     print("wrote", os.path.join(HERE, "golden.npz"))
