@@ -215,6 +215,23 @@ typedef struct rb_loss_stats {
  * ranks, then call rb_loss_finalize with the reduced stats. */
 int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double eps_low,
                  double eps_high, int64_t norm_tokens, rb_loss_stats* stats);
+/* GRPO normalisation modes (SURVEY.md §8c token generalisation; the
+ * reference has no tokens):
+ *   RB_GRPO_TOKEN_MEAN  per-token ratio, mean over the batch's included
+ *                       tokens (rb_loss_grpo);
+ *   RB_GRPO_SEQ_MEAN    per-token ratio, mean over each sequence's included
+ *                       tokens, then over the sequences with one or more;
+ *   RB_GRPO_SEQ_RATIO   sequence-level ratio pi(z|q)/pi_old(z|q) =
+ *                       exp(sum_t logp_now_t - behavior_logprob) (PAPER.md
+ *                       :1022-1025): the reference's record-level
+ *                       grpo_loss_grad (bandit.cpp:363-408) per trajectory,
+ *                       its dL/dlogp on every token.
+ * In the sequence modes stats.included / excluded count sequences (mode 2)
+ * or included sequences / excluded tokens (mode 1) and `norm` (0 = the batch
+ * size) is the global sequence count used as the normaliser. */
+enum { RB_GRPO_TOKEN_MEAN = 0, RB_GRPO_SEQ_MEAN = 1, RB_GRPO_SEQ_RATIO = 2 };
+int rb_loss_grpo_ex(rb_buffer* b, const float* logp_now, float* out_dlogp, double eps_low,
+                    double eps_high, int mode, int64_t norm, rb_loss_stats* stats);
 /* AsymRE (asymre_loss_grad, bandit.cpp:410-438): coef = reward - (group
  * mean + delta_v); dlogp = -coef / norm_batch on every token; objective =
  * sum coef * sum_t logp_now / norm_batch.  norm_batch 0 = this batch size. */
@@ -314,6 +331,12 @@ int rb_group_advantages(const double* rewards, const int64_t* offsets, size_t n_
 int rb_grpo_tokens(const float* logp_now, const float* logp_old, const double* adv,
                    const int64_t* offsets, size_t n_traj, double eps_low, double eps_high,
                    float* out_dlogp, rb_loss_stats* stats);
+/* The same with a normalisation mode; behavior_logprob (n_traj, may be NULL
+ * = sum_t logp_old) is the record's sequence log-prob for RB_GRPO_SEQ_RATIO. */
+int rb_grpo_tokens_ex(const float* logp_now, const float* logp_old, const double* adv,
+                      const double* behavior_logprob, const int64_t* offsets, size_t n_traj,
+                      double eps_low, double eps_high, int mode, float* out_dlogp,
+                      rb_loss_stats* stats);
 /* Record-level fp64 form (L = 1): the reference's grpo_loss_grad per record. */
 int rb_grpo_records(const double* logp_now, const double* behavior_logprob,
                     const double* adv, size_t n, double eps_low, double eps_high,

@@ -19,6 +19,8 @@ STRATEGIES = {"uniform_with_replacement": 0, "uniform_without_replacement": 1,
               "unused_first_without_replacement": 2}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 RETENTIONS = {"plain_fifo": 0, "positive_bias": 1}
+# GRPO normalisation modes (include/replay_b200.h RB_GRPO_*)
+GRPO_MODES = {"token_mean": 0, "seq_mean": 1, "seq_ratio": 2}
 
 
 class Record(C.Structure):  # rb_record, rollout.hpp:13-31
@@ -88,6 +90,7 @@ def _load():
         "rb_batch_ids": (ip, [vp, vp, vp, vp]),
         "rb_gather": (ip, [vp, vp, vp, vp]),
         "rb_loss_grpo": (ip, [vp, vp, vp, dbl, dbl, i64, vp]),
+        "rb_loss_grpo_ex": (ip, [vp, vp, vp, dbl, dbl, ip, i64, vp]),
         "rb_loss_asymre": (ip, [vp, vp, vp, dbl, i64, vp]),
         "rb_loss_finalize": (ip, [vp, vp, vp]),
         "rb_loss_set_reduce_vector": (ip, [vp, vp]),
@@ -120,6 +123,7 @@ def _load():
         "rb_synchronize": (ip, [vp]),
         "rb_group_advantages": (ip, [vp, vp, sz, vp, vp]),
         "rb_grpo_tokens": (ip, [vp, vp, vp, vp, sz, dbl, dbl, vp, vp]),
+        "rb_grpo_tokens_ex": (ip, [vp, vp, vp, vp, vp, sz, dbl, dbl, ip, vp, vp]),
         "rb_grpo_records": (ip, [vp, vp, vp, sz, dbl, dbl, vp, vp]),
         "rb_asymre_tokens": (ip, [vp, vp, vp, vp, sz, dbl, vp, vp]),
         "rb_asymre_records": (ip, [vp, vp, vp, sz, dbl, vp, vp]),

@@ -167,7 +167,8 @@ struct Partial {
 // -1/total -> -1/included correction itself when a token was excluded.
 __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
                             rb_loss_stats* stats, int asym, double inv_b, float* dlogp,
-                            const long long* n_local, int local_fix, int part_base, int nparts) {
+                            const long long* n_local, int local_fix, int part_base, int nparts,
+                            double opt_div = 0.0) {
     __shared__ double s_obj[32];
     __shared__ long long s_inc[32], s_exc[32];
     __shared__ int s_last;
@@ -248,8 +249,10 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
         acc->need_fixup = !asym && exc > 0 && inc > 0;
         acc->kind = asym;
         acc->inv_b = inv_b;
-        // dlogp was written as -g / total_tokens; the local fix below makes it -g / included
-        acc->cur_div = (acc->need_fixup && local_fix) ? (double)inc : (double)acc->total_tokens;
+        // dlogp was written as -g / opt_div (the token mode: total_tokens; the
+        // sequence modes: the selection count); the local fix below makes it -g / included
+        const double od = opt_div > 0.0 ? opt_div : (double)acc->total_tokens;
+        acc->cur_div = (acc->need_fixup && local_fix) ? (double)inc : od;
         acc->done_blocks = 0;
         acc->claim = 0;  // every CTA has made its last claim
         if (stats) {
@@ -264,7 +267,8 @@ __device__ void loss_commit(GrpoPartial p, Partial* parts, DevLossAcc* acc,
     }
     __syncthreads();
     if (s_last) {  // rare: some ratio was non-finite
-        const float f = (float)((double)acc->total_tokens / (double)acc->included);
+        const double od = opt_div > 0.0 ? opt_div : (double)acc->total_tokens;
+        const float f = (float)(od / (double)acc->included);
         const long long n = *n_local;
         for (long long i = threadIdx.x; i < n; i += blockDim.x) dlogp[i] *= f;
     }
@@ -432,6 +436,145 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
     float* dlogp, double delta_v, double inv_b, DevLossAcc* acc, Partial* parts,
     rb_loss_stats* stats, int part_base, int nparts);
 
+// ---- GRPO normalisation modes 1 and 2 (oracle: or_loss_grpo_tokens_mode) ---
+// One CTA per sequence (persistent over the batch's selections).
+//   mode 1  per-sequence mean: n_i included tokens counted first (a token is
+//           excluded iff exp(logp_now - logp_old) is not finite in fp64), then
+//           every token's coefficient (same arithmetic as the token mode) is
+//           written as -g_t / (n_i * S0) and the sequence contributes
+//           mean_t(term_t) to the objective; included = sequences with n_i > 0.
+//   mode 2  sequence ratio exp(sum_t logp_now_t - behavior_logprob) (PAPER.md
+//           :1022-1025; bandit.cpp:375-406 with the record's logp = the sum):
+//           one fp64 ratio / clip / tie decision per sequence; every token gets
+//           -c_i / S0; included / excluded count sequences.
+// S0 = the number of sequences of the (global) batch, the optimistic divisor;
+// an exclusion that empties a sequence (mode 1) or excludes one (mode 2)
+// rescales to -1/included afterwards like the token mode.
+constexpr int SEQ_THREADS = 256;
+__device__ __forceinline__ double block_sum_f64(double x) {
+    __shared__ double s_r[32];
+    __shared__ double s_tot;
+    x = warp_sum_f64(x);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s_r[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_r[w];
+        s_tot = t;
+    }
+    __syncthreads();
+    return s_tot;
+}
+__device__ __forceinline__ long long block_sum_i64(long long x) {
+    __shared__ long long s_r[32];
+    __shared__ long long s_tot;
+    x = warp_sum_i64(x);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s_r[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_r[w];
+        s_tot = t;
+    }
+    __syncthreads();
+    return s_tot;
+}
+// bandit.cpp:381: a ratio is excluded iff exp(logp_now - logp_old) is not
+// finite in fp64 (NaN, or d above ln(DBL_MAX) ~ 709.78).
+__device__ __forceinline__ bool ratio_finite(float lpn, float lpo) {
+    const double d = (double)lpn - (double)lpo;
+    return d <= 709.0 || (d < 710.0 && isfinite(exp(d)));
+}
+// One sequence (block-wide).  lpn / lpo / dl are the sequence's first token;
+// blp: the record's behavior_logprob, or NaN to use sum_t logp_old (mode 2).
+template <int MODE>
+__device__ __forceinline__ void seq_loss_cta(const float* lpn, const float* lpo, float* dl,
+                                             int len, double A, double blp, double s0,
+                                             const GrpoParams& prm, GrpoPartial& part) {
+    const int tid = threadIdx.x;
+    if (MODE == 2) {
+        const bool own_blp = isnan(blp);
+        double sn = 0.0, so = 0.0;
+        for (int t = tid; t < len; t += blockDim.x) {
+            sn += (double)lpn[t];
+            if (own_blp) so += (double)lpo[t];
+        }
+        sn = block_sum_f64(sn);
+        if (own_blp) so = block_sum_f64(so);
+        __shared__ double s_c;
+        if (tid == 0) {
+            const double rd = exp(sn - (own_blp ? so : blp));  // bandit.cpp:380
+            double c = 0.0;
+            if (!isfinite(rd)) {  // 381-386
+                ++part.exc;
+            } else {
+                ++part.inc;
+                const double cl = rd < prm.lo ? prm.lo : (prm.hi < rd ? prm.hi : rd);
+                const double uv = __dmul_rn(rd, A), cv = __dmul_rn(cl, A);
+                if (uv <= cv) {  // ties -> unclipped (392)
+                    part.obj += uv;
+                    c = __dmul_rn(A, rd);
+                } else {
+                    part.obj += cv;
+                }
+            }
+            s_c = c;
+        }
+        __syncthreads();
+        const float g = (float)(-s_c / s0);
+        for (int t = tid; t < len; t += blockDim.x) dl[t] = g;
+        __syncthreads();  // s_c is reused by the next sequence
+    } else {
+        long long bad = 0;
+        for (int t = tid; t < len; t += blockDim.x) bad += ratio_finite(lpn[t], lpo[t]) ? 0 : 1;
+        bad = block_sum_i64(bad);
+        const long long ni = (long long)len - bad;
+        const float scale = ni > 0 ? (float)(-1.0 / ((double)ni * s0)) : 0.f;
+        const float Af = (float)A;
+        GrpoPartial tmp;  // this thread's terms of the sequence
+        for (int t = tid; t < len; t += blockDim.x)
+            dl[t] = ni > 0 ? grpo_token(lpn[t], lpo[t], A, Af, prm, tmp) * scale : 0.f;
+        const double ssum = block_sum_f64(tmp.obj);
+        if (tid == 0) {
+            part.exc += bad;
+            if (ni > 0) {
+                ++part.inc;
+                part.obj += ssum / (double)ni;
+            }
+        }
+    }
+}
+// The buffer path: selection u's logp_old from its slot row, logp_now /
+// dlogp packed at its offset, behavior_logprob from the record column.
+template <int MODE>
+__global__ void __launch_bounds__(SEQ_THREADS) k_loss_grpo_seq_buf(
+    BufView v, const Unit* units, int nloc, const float* lpn, float* dlogp, GrpoParams prm,
+    double s0, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats, const long long* n_local,
+    int local_fix, int part_base, int nparts) {
+    GrpoPartial part;
+    for (int u = blockIdx.x; u < nloc; u += gridDim.x) {
+        const Unit un = ld_unit(units + u);
+        if (un.len <= 0) continue;
+        seq_loss_cta<MODE>(lpn + un.off, v.lpo + (size_t)un.row * v.stride, dlogp + un.off,
+                           un.len, un.adv, MODE == 2 ? v.blp[un.g] : 0.0, s0, prm, part);
+    }
+    loss_commit(part, parts, acc, stats, 0, 0.0, dlogp, n_local, local_fix, part_base, nparts, s0);
+}
+// The stateless path over explicit packed arrays (one CTA per trajectory).
+template <int MODE>
+__global__ void __launch_bounds__(SEQ_THREADS) k_loss_grpo_seq_packed(
+    const float* lpn, const float* lpo, const double* adv, const double* blp,
+    const int64_t* offsets, float* dlogp, GrpoParams prm, double s0, DevLossAcc* acc) {
+    const long long i = blockIdx.x;
+    const long long o0 = offsets[i], o1 = offsets[i + 1];
+    GrpoPartial part;
+    seq_loss_cta<MODE>(lpn + o0, lpo + o0, dlogp + o0, (int)(o1 - o0), adv[i],
+                       blp ? blp[i] : __longlong_as_double(0x7ff8000000000000LL), s0, prm, part);
+    grpo_block_commit(part, acc);
+}
+
 int loss_grid(int sms) {
     int a = 0, b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_loss_grpo_buf<LOSS_U, false>, UNIT_THREADS, 0);
@@ -475,7 +618,8 @@ __global__ void k_dlogp_rescale(float* d, long long n, const long long* n_dev,
                                 const DevLossAcc* acc) {
     if (!acc->need_fixup) return;
     if (n_dev) n = *n_dev;
-    const float f = (float)((double)acc->total_tokens / (double)acc->included);
+    const double cur = acc->cur_div > 0.0 ? acc->cur_div : (double)acc->total_tokens;
+    const float f = (float)(cur / (double)acc->included);
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         d[i] *= f;
@@ -626,6 +770,7 @@ __global__ void k_group_adv(const double* r, const int64_t* off, long long ng, d
 }
 
 __global__ void k_acc_reset(DevLossAcc* acc, long long total) {
+    acc->cur_div = 0.0;
     acc->obj_sum = 0.0;
     acc->included = 0;
     acc->excluded = 0;
@@ -731,8 +876,10 @@ unsigned grid_for(long long n) {
 // One loss evaluation over the current batch.
 struct LossCall {
     int kind = 0;  // 0 GRPO, 1 AsymRE
+    int mode = 0;  // GRPO normalisation: RB_GRPO_TOKEN_MEAN / SEQ_MEAN / SEQ_RATIO
     GrpoParams p{};
     double delta_v = 0.0, inv_b = 0.0;
+    double s0 = 0.0;  // sequence modes: the optimistic divisor (sequences in the batch)
 };
 
 // Launch the loss kernel over owned selections [s0, s1) (part slots
@@ -740,6 +887,14 @@ struct LossCall {
 // CTAs for a launch over `nsel` selections: the resident grid, or fewer
 // when the batch has fewer work units (small batches: fewer idle CTAs and
 // fewer partials for the last CTA to fold).
+int loss_grid_for(const rb_buffer* b, long long nsel);
+// CTAs of the call's kernel over nsel selections (the sequence modes: one
+// 256-thread CTA per selection, at most 8 resident per SM).
+int call_grid(const rb_buffer* b, const LossCall& c, long long nsel) {
+    if (c.kind == 0 && c.mode != RB_GRPO_TOKEN_MEAN)
+        return (int)std::max<long long>(1, std::min<long long>(nsel, (long long)b->sms * 8));
+    return loss_grid_for(b, nsel);
+}
 int loss_grid_for(const rb_buffer* b, long long nsel) {
     const long long qmax = ((long long)b->max_tokens + 3) / 4 + 1;  // quads per selection (bound)
     const long long ups = (qmax + UNIT_THREADS * LOSS_U - 1) / (UNIT_THREADS * LOSS_U);
@@ -750,7 +905,19 @@ int loss_grid_for(const rb_buffer* b, long long nsel) {
 void launch_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl, long long s0,
                  long long s1, int part_base, int nparts, rb_loss_stats* kst, int local_fix) {
     const Unit* u = b->units_sel + s0;
-    const int grid = loss_grid_for(b, s1 - s0);
+    const int grid = call_grid(b, c, s1 - s0);
+    if (c.kind == 0 && c.mode != RB_GRPO_TOKEN_MEAN) {
+        if (c.mode == RB_GRPO_SEQ_MEAN)
+            k_loss_grpo_seq_buf<1><<<grid, SEQ_THREADS, 0, b->stream>>>(
+                b->v, u, (int)(s1 - s0), lpn, dl, c.p, c.s0, b->acc, (Partial*)b->loss_partials,
+                kst, b->sel_total, local_fix, part_base, nparts);
+        else
+            k_loss_grpo_seq_buf<2><<<grid, SEQ_THREADS, 0, b->stream>>>(
+                b->v, u, (int)(s1 - s0), lpn, dl, c.p, c.s0, b->acc, (Partial*)b->loss_partials,
+                kst, b->sel_total, local_fix, part_base, nparts);
+        RB_CUDA(cudaGetLastError());
+        return;
+    }
     // claimed units for long (ragged-prone) trajectories in a one-launch loss
     const bool dyn = b->max_tokens > 2 * UNIT_THREADS * LOSS_U * 4 && part_base == 0 &&
                      nparts == grid;
@@ -795,7 +962,7 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
     if (nloc <= 0) {
         if (kst) k_stats_out<<<1, 1, 0, b->stream>>>(b->acc, kst, c.kind, c.inv_b);
     } else if (!host_in && !host_out) {
-        launch_loss(b, c, lpn, dl, 0, nloc, 0, loss_grid_for(b, nloc), kst, single && c.kind == 0);
+        launch_loss(b, c, lpn, dl, 0, nloc, 0, call_grid(b, c, nloc), kst, single && c.kind == 0);
     } else {
         // packed offsets of the owned selections (and the total) on the host
         std::vector<long long> off(nloc + 1);
@@ -819,7 +986,7 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
         cut.push_back(nloc);
         const int nch = (int)cut.size() - 1;
         std::vector<int> pbase(nch + 1, 0);  // partial slots of each chunk's launch
-        for (int k = 0; k < nch; ++k) pbase[k + 1] = pbase[k] + loss_grid_for(b, cut[k + 1] - cut[k]);
+        for (int k = 0; k < nch; ++k) pbase[k + 1] = pbase[k] + call_grid(b, c, cut[k + 1] - cut[k]);
         const int nparts = pbase[nch];
         if ((size_t)nparts * 32 > b->loss_partials_bytes) b->grow_loss_partials((size_t)nparts * 32);
         const float* hin = lpn;
@@ -876,7 +1043,39 @@ extern "C" {
 
 int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double eps_low,
                  double eps_high, int64_t norm_tokens, rb_loss_stats* stats) {
+    return rb_loss_grpo_ex(b, logp_now, out_dlogp, eps_low, eps_high, RB_GRPO_TOKEN_MEAN,
+                           norm_tokens, stats);
+}
+
+int rb_loss_grpo_ex(rb_buffer* b, const float* logp_now, float* out_dlogp, double eps_low,
+                    double eps_high, int mode, int64_t norm, rb_loss_stats* stats) {
     return guard([&] {
+        if (mode < RB_GRPO_TOKEN_MEAN || mode > RB_GRPO_SEQ_RATIO)
+            invalid("rb_loss_grpo_ex: unknown normalisation mode");
+        if (mode != RB_GRPO_TOKEN_MEAN) {
+            if (b->stride == 0) invalid("rb_loss_grpo: buffer holds no token payload");
+            if (eps_low < 0.0 || eps_high < 0.0) invalid("loss spec: clip bounds must be >= 0");
+            if (!std::isfinite(eps_low) || !std::isfinite(eps_high))
+                invalid("loss spec: parameters must be finite");
+            if (b->B == 0) invalid("loss gradient needs a non-empty batch");
+            LossCall c;
+            c.kind = 0;
+            c.mode = mode;
+            c.p.lo = 1.0 - eps_low;
+            c.p.hi = 1.0 + eps_high;
+            c.p.lo_f = (float)c.p.lo;
+            c.p.hi_f = (float)c.p.hi;
+            c.s0 = (double)(norm > 0 ? norm : (int64_t)b->B);
+            if (b->acc_norm_explicit) {  // back to the batch's token count (stats)
+                k_acc_set_total<<<1, 1, 0, b->stream>>>(b->acc, b->sel_total + 1, 0);
+                RB_CUDA(cudaGetLastError());
+            }
+            b->last_loss = 0;
+            b->acc_norm_explicit = false;
+            run_loss(b, c, logp_now, out_dlogp, stats);
+            return;
+        }
+        const int64_t norm_tokens = norm;
         if (b->stride == 0) invalid("rb_loss_grpo: buffer holds no token payload");
         if (eps_low < 0.0 || eps_high < 0.0) invalid("loss spec: clip bounds must be >= 0");
         if (!std::isfinite(eps_low) || !std::isfinite(eps_high))
@@ -1138,6 +1337,59 @@ int rb_grpo_tokens(const float* logp_now, const float* logp_old, const double* a
         k_acc_reset<<<1, 1, 0, c.stream>>>(c.acc, last);
         k_loss_grpo_packed<<<(unsigned)n_traj, 256, 0, c.stream>>>(lpn, lpo, a, o, d, p, c.acc,
                                                                   (long long)n_traj);
+        k_dlogp_rescale<<<148, 256, 0, c.stream>>>(d, last, nullptr, c.acc);
+        RB_CUDA(cudaGetLastError());
+        c.stats(stats, 0, 0.0, back);
+        c.finish(back);
+    });
+}
+
+int rb_grpo_tokens_ex(const float* logp_now, const float* logp_old, const double* adv,
+                      const double* behavior_logprob, const int64_t* offsets, size_t n_traj,
+                      double eps_low, double eps_high, int mode, float* out_dlogp,
+                      rb_loss_stats* stats) {
+    if (mode == RB_GRPO_TOKEN_MEAN)
+        return rb_grpo_tokens(logp_now, logp_old, adv, offsets, n_traj, eps_low, eps_high,
+                              out_dlogp, stats);
+    return guard([&] {
+        if (mode < RB_GRPO_TOKEN_MEAN || mode > RB_GRPO_SEQ_RATIO)
+            invalid("rb_grpo_tokens_ex: unknown normalisation mode");
+        if (eps_low < 0.0 || eps_high < 0.0) invalid("loss spec: clip bounds must be >= 0");
+        if (!std::isfinite(eps_low) || !std::isfinite(eps_high))
+            invalid("loss spec: parameters must be finite");
+        if (n_traj == 0) invalid("loss gradient needs a non-empty batch");
+        Ctx& c = ctx();
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.init();
+        int64_t first = 0, last = 0;
+        if (is_device_ptr(offsets)) {
+            RB_CUDA(cudaMemcpy(&first, offsets, 8, cudaMemcpyDeviceToHost));
+            RB_CUDA(cudaMemcpy(&last, offsets + n_traj, 8, cudaMemcpyDeviceToHost));
+        } else {
+            first = offsets[0];
+            last = offsets[n_traj];
+        }
+        if (first != 0) invalid("rb_grpo_tokens: offsets must start at 0");
+        std::vector<std::pair<void*, std::pair<void*, size_t>>> back;
+        const float* lpn = c.in(logp_now, (size_t)last);
+        const float* lpo = c.in(logp_old, (size_t)last);
+        const double* a = c.in(adv, n_traj);
+        const double* bl = c.in(behavior_logprob, n_traj);
+        const int64_t* o = c.in(offsets, n_traj + 1);
+        float* d = c.out(out_dlogp, (size_t)last, back);
+        GrpoParams p;
+        p.lo = 1.0 - eps_low;
+        p.hi = 1.0 + eps_high;
+        p.lo_f = (float)p.lo;
+        p.hi_f = (float)p.hi;
+        const double s0 = (double)n_traj;
+        k_acc_reset<<<1, 1, 0, c.stream>>>(c.acc, (long long)n_traj);  // divisor: sequences
+        if (mode == RB_GRPO_SEQ_MEAN)
+            k_loss_grpo_seq_packed<1><<<(unsigned)n_traj, SEQ_THREADS, 0, c.stream>>>(
+                lpn, lpo, a, bl, o, d, p, s0, c.acc);
+        else
+            k_loss_grpo_seq_packed<2><<<(unsigned)n_traj, SEQ_THREADS, 0, c.stream>>>(
+                lpn, lpo, a, bl, o, d, p, s0, c.acc);
         k_dlogp_rescale<<<148, 256, 0, c.stream>>>(d, last, nullptr, c.acc);
         RB_CUDA(cudaGetLastError());
         c.stats(stats, 0, 0.0, back);

@@ -16,8 +16,8 @@ from typing import Optional
 
 import numpy as np
 
-from ._lib import (RB_INSERT_ASSUME_UNIQUE, RETENTIONS, STRATEGIES, STRATEGY_NAMES, InsertBatch,
-                   LossStats, Record, check, lib)
+from ._lib import (GRPO_MODES, RB_INSERT_ASSUME_UNIQUE, RETENTIONS, STRATEGIES, STRATEGY_NAMES,
+                   InsertBatch, LossStats, Record, check, lib)
 
 RECORD_DTYPE = np.dtype(
     {
@@ -335,10 +335,15 @@ class ShardedReplayBuffer:
         return stats, _ptr(stats)
 
     def loss_grpo(self, logp_now, out_dlogp, eps_low=0.2, eps_high=0.2, norm_tokens=0,
-                  stats=True):
+                  stats=True, mode="token_mean"):
+        """GRPO clipped surrogate (bandit.cpp:363-408) per token of the batch.
+        mode: "token_mean" (default), "seq_mean" or "seq_ratio" (sequence-level
+        ratio; norm_tokens is then the global sequence count, 0 = this batch)."""
         st, p = self._stats_arg(stats)
-        check(lib.rb_loss_grpo(self._h, _ptr(logp_now), _ptr(out_dlogp), eps_low, eps_high,
-                               int(norm_tokens), p))
+        if mode not in GRPO_MODES:
+            raise ValueError(f"unknown GRPO normalisation mode: '{mode}'")
+        check(lib.rb_loss_grpo_ex(self._h, _ptr(logp_now), _ptr(out_dlogp), eps_low, eps_high,
+                                  GRPO_MODES[mode], int(norm_tokens), p))
         return st
 
     def loss_asymre(self, logp_now, out_dlogp, delta_v=-0.1, norm_batch=0, stats=True):
@@ -452,14 +457,22 @@ def group_advantages(rewards, offsets=None, out=None, out_mean=None):
     return out
 
 
-def grpo_tokens(logp_now, logp_old, adv, offsets, eps_low=0.2, eps_high=0.2, out=None):
+def grpo_tokens(logp_now, logp_old, adv, offsets, eps_low=0.2, eps_high=0.2, out=None,
+                mode="token_mean", behavior_logprob=None):
+    """grpo_loss_grad at the token level; mode as in ShardedReplayBuffer.loss_grpo
+    (behavior_logprob: per-trajectory sequence log-prob for "seq_ratio",
+    default sum_t logp_old)."""
+    if mode not in GRPO_MODES:
+        raise ValueError(f"unknown GRPO normalisation mode: '{mode}'")
     lpn, lpo = _arr(logp_now, np.float32), _arr(logp_old, np.float32)
     a, off = _arr(adv, np.float64), _arr(offsets, np.int64)
+    blp = _arr(behavior_logprob, np.float64)
     if out is None:
         out = np.zeros(lpn.shape[0], np.float32)
     st = LossStats()
-    check(lib.rb_grpo_tokens(_ptr(lpn), _ptr(lpo), _ptr(a), _ptr(off), int(off.shape[0]) - 1,
-                             eps_low, eps_high, _ptr(out), C.byref(st)))
+    check(lib.rb_grpo_tokens_ex(_ptr(lpn), _ptr(lpo), _ptr(a), _ptr(blp), _ptr(off),
+                                int(off.shape[0]) - 1, eps_low, eps_high, GRPO_MODES[mode],
+                                _ptr(out), C.byref(st)))
     return out, st
 
 
