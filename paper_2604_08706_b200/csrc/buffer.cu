@@ -909,30 +909,33 @@ constexpr int PAYLOAD_U = 4;
 
 
 // ---- payload insert over the bulk-copy engine (TMA) ------------------------
-// The closed-form FIFO copy as a cp.async.bulk pipeline: one CTA per SM, a
-// ring of TP_S shared-memory stages, loads TP_LAG items ahead of the stores.
-// An item is up to TP_CH tokens of one surviving trajectory (tokens and
-// logp_old).  A 16-byte aligned source goes global -> smem -> slot row
-// untouched; otherwise the aligned-down source quads are loaded and the
-// CTA's threads shift them in place in shared memory before the bulk store (rows are
+// The closed-form FIFO copy as independent cp.async.bulk pipelines, one per
+// single-warp CTA (PB_CTAS per SM), each a ring of PB_S shared-memory stages
+// of up to PB_CH tokens.  An item is one array (tokens or logp_old) of one
+// chunk of one surviving trajectory: a 16-byte aligned source goes global ->
+// smem -> slot row untouched; otherwise the aligned-down source quads are
+// loaded and the warp shifts them in place before the bulk store (rows are
 // 16-byte aligned and padded to a multiple of 4 tokens, so a store may round
-// its length up to whole quads).  Descriptors come from the closed form
-// (fifo_unit); stores start once the route kernel has published a valid
-// verdict.  Little register and thread use, so the route / sampler CTAs that
-// overlap the copy find room on every SM.
-constexpr int TP_THREADS = 128;
-constexpr int TP_CH = 1024;           // tokens per item
-#ifndef RB_TP_S
-#define RB_TP_S 16
-#define RB_TP_LAG 12
+// its length up to whole quads).  Lane 0 issues; the warp builds the list of
+// its next 32 candidate items' descriptors in parallel (fifo_unit, one per
+// lane) so descriptor loads never serialise the pipeline.  Descriptors come
+// from the closed form; stores start once the route kernel has published a
+// valid verdict.  tools/probes/payload_tma.cu: many small independent
+// pipelines of 16 KB items reach the HBM copy rate (6.6-6.9 TB/s on 339 MB),
+// a single thread issuing 4 KB items per SM does not (1.6 TB/s).
+#ifndef RB_PB_S
+#define RB_PB_S 2
+#define RB_PB_L 1
+#define RB_PB_CTAS 3
 #endif
-constexpr int TP_S = RB_TP_S;         // stages
-constexpr int TP_LAG = RB_TP_LAG;     // loads issued ahead of stores
-constexpr int TP_RAW = TP_CH + 4;     // raw words per array (aligned-down source + spill)
-constexpr int TP_STAGE = 2 * TP_RAW;  // words per stage
-constexpr int TP_LIST = 128;          // items listed per round
-constexpr size_t TP_SMEM = (size_t)TP_S * TP_STAGE * 4 + TP_S * 8 + TP_LIST * 16;
-static_assert((TP_RAW * 4) % 16 == 0 && (TP_CH * 4) % 16 == 0, "bulk-copy alignment");
+constexpr int PB_S = RB_PB_S;                  // stages per pipeline
+constexpr int PB_L = RB_PB_L;                  // loads issued ahead of the stores
+constexpr int PB_CTAS = RB_PB_CTAS;            // pipelines (single-warp CTAs) per SM
+constexpr int PB_CHT = 4096;                   // tokens per item (16 KB)
+constexpr int PB_RAW = PB_CHT + 4;             // words per stage (aligned-down source + spill)
+constexpr size_t PB_SMEM = (size_t)PB_S * PB_RAW * 4 + PB_S * 8 + 32 * 16 + PB_S * 16;
+static_assert(PB_S - PB_L - 1 >= 0, "bulk pipeline lag");
+static_assert((PB_RAW * 4) % 16 == 0, "bulk-copy alignment");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -972,126 +975,116 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-struct TpItem {
-    int32_t row, n;  // slot row; tokens in this item
-    int64_t src;     // packed element index of the item's first token
+struct PbItem {
+    int64_t src;  // packed element index of the item's first token
+    int32_t row;  // slot row (local), -1 = none
+    int32_t n;    // tokens | array << 30 | chunk << 20
 };
 
-__global__ void __launch_bounds__(TP_THREADS) k_insert_payload_tma(BufView v, FifoPlan p,
-                                                                  const int64_t* toff, int n,
-                                                                  const int32_t* tokens,
-                                                                  const float* logp_old,
-                                                                  int* sync) {
-    extern __shared__ __align__(128) uint32_t tp_sm[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(tp_sm + TP_S * TP_STAGE);
-    TpItem* list = reinterpret_cast<TpItem*>(bar + TP_S);
-    __shared__ int s_flag;
+__global__ void __launch_bounds__(32) k_insert_payload_tma(BufView v, FifoPlan p, const int64_t* toff,
+                                                           int n, const int32_t* tokens,
+                                                           const float* logp_old, int* sync) {
+    extern __shared__ __align__(128) uint32_t pb_smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(pb_smem + PB_S * PB_RAW);
+    PbItem* list = reinterpret_cast<PbItem*>(bar + PB_S);
+    PbItem* meta = list + 32;  // the item held by each stage
     RB_TSTART(1);
     pdl_trigger();  // the sampler may launch (it waits for the route itself)
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        for (int s = 0; s < TP_S; ++s) mbar_init(&bar[s]);
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+        for (int s = 0; s < PB_S; ++s) mbar_init(&bar[s]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s_flag = 0;
     }
-    __syncthreads();
-    const int ipr = (int)((v.stride + TP_CH - 1) / TP_CH);  // items per record (bound)
-    const long long nitems = (long long)n * ipr;
-    long long issued = 0, stored = 0;  // this CTA's pipeline counters (all threads track)
-    // Rounds of up to TP_LIST items of this CTA (item u = blockIdx.x + k * gridDim.x).
-    for (long long u0 = blockIdx.x; u0 < nitems; u0 += (long long)TP_LIST * gridDim.x) {
-        // list this round's valid items
-        const long long u = u0 + (long long)tid * gridDim.x;
-        TpItem it{-1, 0, 0};
-        if (tid < TP_LIST && u < nitems) {
-            const int j = (int)(u / ipr), c = (int)(u - (long long)j * ipr);
+    __syncwarp();
+    const int cpr = (v.stride + PB_CHT - 1) / PB_CHT;  // chunks per record (bound)
+    const int arrays = 2;                              // tokens, logp_old
+    const long long nitems = (long long)n * arrays * cpr;
+    const long long P = gridDim.x;
+    long long issued = 0, stored = 0;
+    int flag = 0;  // route verdict (1 valid, 2 rejected), read before the first store
+    // store step of item g (whole warp): wait for its load, shift, bulk store
+    auto store_one = [&](long long g) {
+        const int st = (int)(g % PB_S);
+        if (lane == 0) mbar_wait(&bar[st], (uint32_t)((g / PB_S) & 1));
+        __syncwarp();
+        const PbItem x = meta[st];
+        const int cnt = x.n & 0xfffff, c = (x.n >> 20) & 0x3ff, arr = x.n >> 30;
+        const int a = (int)(x.src & 3);
+        const int words = (cnt + 3) & ~3;
+        uint32_t* stg = pb_smem + (size_t)st * PB_RAW;
+        if (a != 0) {  // shift the aligned-down source quads down by `a`, in place
+            for (int e0 = 0; e0 < words; e0 += 128) {
+                uint32_t r[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int e = e0 + lane + 32 * q;
+                    r[q] = e < words ? stg[a + e] : 0u;
+                }
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int e = e0 + lane + 32 * q;
+                    if (e < words) stg[e] = r[q];
+                }
+                __syncwarp();
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+        }
+        if (lane == 0) {
+            if (flag == 0) flag = spin_while_eq(&sync[0], 0);
+            if (flag == 1) {
+                const size_t row = (size_t)x.row * v.stride + (size_t)c * PB_CHT;
+                uint32_t* dst = arr ? reinterpret_cast<uint32_t*>(v.lpo) + row
+                                    : reinterpret_cast<uint32_t*>(v.tok) + row;
+                bulk_s2g(dst, stg, (uint32_t)words * 4);
+            }
+            bulk_commit();  // (an empty group when rejected keeps the count in step)
+        }
+    };
+    for (long long base = blockIdx.x; base < nitems; base += 32 * P) {
+        // this warp's next 32 candidate items: descriptors in parallel, compacted
+        const long long u = base + (long long)lane * P;
+        PbItem it{0, -1, 0};
+        if (u < nitems) {
+            const int j = (int)(u / (arrays * cpr));
+            const int r = (int)(u - (long long)j * arrays * cpr);
+            const int arr = r / cpr, c = r - arr * cpr;
             const Unit d = fifo_unit(v, p, toff, n, j);
-            const int rest = d.len - c * TP_CH;
-            if (d.row >= 0 && rest > 0) {
+            const int rest = d.len - c * PB_CHT;
+            const bool have = arr ? logp_old != nullptr : tokens != nullptr;
+            if (d.row >= 0 && rest > 0 && have) {
                 it.row = d.row;
-                it.n = rest < TP_CH ? rest : TP_CH;
-                it.src = d.off + (long long)c * TP_CH;
-                it.n |= c << 20;             // chunk index rides in the high bits
+                it.src = d.off + (long long)c * PB_CHT;
+                it.n = (rest < PB_CHT ? rest : PB_CHT) | (c << 20) | (arr << 30);
             }
         }
-        const bool ok = it.row >= 0;
-        const unsigned bal = __ballot_sync(0xffffffffu, ok);
-        __shared__ int s_wc[TP_THREADS / 32];
-        if ((tid & 31) == 0) s_wc[tid >> 5] = __popc(bal);
-        __syncthreads();
-        int base = 0, m = 0;
-        for (int w = 0; w < TP_THREADS / 32; ++w) {
-            if (w < (tid >> 5)) base += s_wc[w];
-            m += s_wc[w];
-        }
-        if (ok) list[base + __popc(bal & ((1u << (tid & 31)) - 1))] = it;
-        __syncthreads();
-        // pipeline over the listed items (global item counter keeps stages / parities)
-        for (int i = 0; i < m + TP_LAG; ++i) {
-            if (i < m && tid == 0) {  // load
-                const long long g = issued++;
-                const int st = (int)(g % TP_S);
-                if (g >= TP_S) bulk_wait_read<TP_S - 1 - TP_LAG>();  // store of item g-S has read its stage
-                const TpItem x = list[i];
-                const int cnt = x.n & 0xfffff;
+        const unsigned ok = __ballot_sync(0xffffffffu, it.row >= 0);
+        if (it.row >= 0) list[__popc(ok & ((1u << lane) - 1))] = it;
+        __syncwarp();
+        const int m = __popc(ok);
+        for (int i = 0; i < m; ++i) {
+            if (lane == 0) {  // load item `issued` into its stage
+                const long long g = issued;
+                const int st = (int)(g % PB_S);
+                if (g >= PB_S) bulk_wait_read<PB_S - PB_L - 1>();  // its stage's last store has read it
+                const PbItem x = list[i];
+                meta[st] = x;
+                const int cnt = x.n & 0xfffff, arr = x.n >> 30;
                 const int a = (int)(x.src & 3);
-                const int words = (a + cnt + 3) & ~3;
-                uint32_t* stg = tp_sm + (size_t)st * TP_STAGE;
-                const uint32_t bytes = (uint32_t)words * 4;
-                mbar_expect_tx(&bar[st], bytes * ((tokens ? 1 : 0) + (logp_old ? 1 : 0)));
-                if (tokens) bulk_g2s(stg, tokens + (x.src - a), bytes, &bar[st]);
-                if (logp_old) bulk_g2s(stg + TP_RAW, logp_old + (x.src - a), bytes, &bar[st]);
+                const uint32_t bytes = (uint32_t)((a + cnt + 3) & ~3) * 4;
+                const uint32_t* srcb = arr ? reinterpret_cast<const uint32_t*>(logp_old)
+                                           : reinterpret_cast<const uint32_t*>(tokens);
+                mbar_expect_tx(&bar[st], bytes);
+                bulk_g2s(pb_smem + (size_t)st * PB_RAW, srcb + (x.src - a), bytes, &bar[st]);
             }
-            if (i >= TP_LAG && i - TP_LAG < m) {  // store item k
-                const int k = i - TP_LAG;
-                const long long g = stored++;
-                const int st = (int)(g % TP_S);
-                mbar_wait(&bar[st], (uint32_t)((g / TP_S) & 1));
-                if (s_flag == 0) {  // first store of this CTA: the route's verdict
-                    if (tid == 0) {
-                        s_flag = spin_while_eq(&sync[0], 0);
-                    }
-                    __syncthreads();
-                }
-                const TpItem x = list[k];
-                const int cnt = x.n & 0xfffff, c = x.n >> 20;
-                const int a = (int)(x.src & 3);
-                const int words = (cnt + 3) & ~3;
-                uint32_t* stg = tp_sm + (size_t)st * TP_STAGE;
-                const uint32_t* out_t = stg;
-                const uint32_t* out_l = stg + TP_RAW;
-                if (a != 0) {  // shift the aligned-down source quads down by `a`, in place
-                    constexpr int PER = TP_CH / TP_THREADS;
-                    uint32_t rt[PER], rl[PER];
-#pragma unroll
-                    for (int q = 0; q < PER; ++q) {
-                        const int e = tid + q * TP_THREADS;
-                        rt[q] = stg[a + e];
-                        rl[q] = stg[TP_RAW + a + e];
-                    }
-                    __syncthreads();
-#pragma unroll
-                    for (int q = 0; q < PER; ++q) {
-                        const int e = tid + q * TP_THREADS;
-                        stg[e] = rt[q];
-                        stg[TP_RAW + e] = rl[q];
-                    }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    __syncthreads();
-                }
-                if (tid == 0 && s_flag == 1) {
-                    const size_t row = (size_t)x.row * v.stride + (size_t)c * TP_CH;
-                    if (tokens) bulk_s2g(v.tok + row, out_t, (uint32_t)words * 4);
-                    if (logp_old) bulk_s2g(v.lpo + row, out_l, (uint32_t)words * 4);
-                    bulk_commit();
-                } else if (tid == 0) {
-                    bulk_commit();  // keeps the group count in step (empty group)
-                }
-            }
+            ++issued;
+            __syncwarp();
+            if (issued - stored > PB_L) store_one(stored++);
         }
-        __syncthreads();
     }
-    if (tid == 0) {
+    while (stored < issued) store_one(stored++);
+    if (lane == 0) {
         bulk_wait_all();  // this CTA's row writes are complete
         asm volatile("fence.proxy.async.global;" ::: "memory");
         payload_pending_end(sync);
@@ -2877,7 +2870,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         if (const char* e = std::getenv("RB_TMA_CTAS")) b->tma_ctas = std::max(1, std::atoi(e));
         b->sms = sms;
         RB_CUDA(cudaFuncSetAttribute(k_insert_payload_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)TP_SMEM));
+                                     (int)PB_SMEM));
         // test hook: force the sampler's exact draw replay (must not change results)
         v.dbg_replay = std::getenv("RB_DEBUG_FORCE_DRAW_REPLAY") != nullptr;
         b->map_ctl = dalloc<GridCtl>(1);
@@ -2972,10 +2965,10 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        if (b->tma_payload) {
+        if (b->tma_payload && b->stride <= 1023 * PB_CHT) {  // chunk index: 10 bits
             cfg.gridDim = dim3(b->sms * b->tma_ctas);
-            cfg.blockDim = dim3(TP_THREADS);
-            cfg.dynamicSmemBytes = TP_SMEM;
+            cfg.blockDim = dim3(32);
+            cfg.dynamicSmemBytes = PB_SMEM;
             RB_CUDA(cudaLaunchKernelEx(&cfg, k_insert_payload_tma, b->v, p, bt.tok_offsets,
                                        (int)bt.n, bt.tokens, bt.logp_old, b->pay_sync));
         } else {

@@ -123,7 +123,7 @@ struct rb_buffer {
     bool pdl = true;                    // programmatic dependent launch of the payload copy
     bool tma_payload = true;            // bulk-copy (TMA) payload kernel (else 128-bit LSU)
     int sms = 148;
-    int tma_ctas = 1;                   // bulk-copy payload CTAs per SM
+    int tma_ctas = 3;                   // bulk-copy payload pipelines (single-warp CTAs) per SM
     bool pdl_tail = false;              // the stream's last kernel is the closed-form payload copy
     rb::PendingIns pend{};              // its insert's plan (for a sampler that overlaps it)
     unsigned long long keep_total = 0;  // route CTAs launched with an offsets copy (host count)
