@@ -190,22 +190,49 @@ class Workload:
         self.steps = self.batches[1:]
 
 
-def scaled_cfg(cfg, world):
-    """Weak scaling (BASELINE north_star: the buffer partitions
-    by shard across the GPUs): every GPU holds one shard of the single-GPU
-    size and serves the single-GPU batch, so per-GPU work is fixed and the job
-    is N shards of one sharded buffer (one MT19937-64 stream, round-robin
-    routing, metadata replicated, payload sharded)."""
+def scaled_cfg(cfg, world, weak=False):
+    """The N-GPU job (BASELINE.json configs[3]).
+
+    Strong scaling (default): the single-GPU workload itself — the buffer of
+    `capacity` trajectories and the batch of `batch` draws — split into N
+    shards, one per GPU (round-robin routing, replay_buffer.cpp:89-90; B/N
+    draws per shard, replay_buffer.cpp:193-204).  Per-GPU payload, gather and
+    loss work shrink as 1/N.
+
+    Weak scaling (--weak): every GPU holds one shard of the single-GPU size
+    and serves the single-GPU batch, so the job is N x the single-GPU
+    workload."""
     if world == 1:
-        return cfg
+        return dict(cfg, scaling="weak")
     c = dict(cfg)
-    c["capacity"] = cfg["capacity"] * world
-    c["batch"] = cfg["batch"] * world
-    c["name"] = (f"{cfg['name'].split(':')[0]} per GPU x {world}: buffer {c['capacity']} "
-                 f"trajectories in {world} shards of {cfg['capacity']} (one per GPU), "
-                 f"{c['batch'] // cfg['group']} prompts x G={cfg['group']} per step, "
-                 f"{cfg['lmax']}-token responses, {cfg['retention']}, {cfg['loss']}")
+    tag = cfg["name"].split(":")[0]
+    if weak:
+        c["capacity"] = cfg["capacity"] * world
+        c["batch"] = cfg["batch"] * world
+        c["scaling"] = "weak"
+        c["name"] = (f"{tag} per GPU x {world}: buffer {c['capacity']} "
+                     f"trajectories in {world} shards of {cfg['capacity']} (one per GPU), "
+                     f"{c['batch'] // cfg['group']} prompts x G={cfg['group']} per step, "
+                     f"{cfg['lmax']}-token responses, {cfg['retention']}, {cfg['loss']}")
+    else:
+        c["scaling"] = "strong"
+        c["name"] = (f"{tag} over {world} GPUs: buffer {cfg['capacity']} trajectories in "
+                     f"{world} shards of {cfg['capacity'] // world} (one per GPU), "
+                     f"{cfg['batch'] // cfg['group']} prompts x G={cfg['group']} per step "
+                     f"({cfg['batch'] // world} draws per shard), {cfg['lmax']}-token responses, "
+                     f"{cfg['retention']}, {cfg['loss']}")
     return c
+
+
+def config_dict(cfg, world):
+    """The `config` object of the JSON line — identical for both arms."""
+    return {"workload": cfg["name"], "buffer": cfg["capacity"], "shards": world,
+            "batch": cfg["batch"], "group": cfg["group"], "tokens_per_traj": cfg["lmax"],
+            "ragged": cfg["ragged"], "retention": cfg["retention"], "delta": cfg["delta"],
+            "W": W_WORKERS, "T": T_TRAINERS, "mu": MU, "loss": cfg["loss"],
+            "l2": "inputs larger than L2 (buffer + per-step traffic >> 126 MB); the trainer "
+                  "stand-in ends with a 256 MB read, so the loss reads logp_now from HBM",
+            "parallelism": f"shard{world}"}
 
 
 def run_ours(args, rank, world, dist):
@@ -214,7 +241,7 @@ def run_ours(args, rank, world, dist):
     import paper_2604_08706_b200 as rb
     from tools import synth
 
-    cfg = scaled_cfg(CONFIGS[args.config], world)
+    cfg = scaled_cfg(CONFIGS[args.config], world, getattr(args, "weak", False))
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -418,16 +445,11 @@ def run_ours(args, rank, world, dist):
                     "frac": alg / T / (ms * 1e-3) / 1e9 / hbm}
     res = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
-        "warmup": Wm, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": Wm, "ms_per_step": ms, "higher_is_better": True, "scaling": cfg["scaling"],
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic (include/replay_synth.h)",
-        "config": {"workload": cfg["name"], "buffer": N, "shards": T, "batch": B,
-                   "group": cfg["group"], "tokens_per_traj": cfg["lmax"], "ragged": cfg["ragged"],
-                   "W": W_WORKERS, "T": T_TRAINERS, "mu": MU, "inserted_per_step": R,
-                   "sampled_tokens_per_step": t_samp, "loss": cfg["loss"],
-                   "l2": "inputs larger than L2 (buffer + per-step traffic >> 126 MB); the "
-                         "trainer stand-in ends with a 256 MB read, so the loss reads logp_now "
-                         "from HBM",
-                   "parallelism": f"shard{T}"},
+        "config": config_dict(cfg, world),
+        "accounting": {"inserted_per_step": R, "sampled_tokens_per_step": t_samp,
+                       "algorithmic_bytes_per_step": alg},
         "phases_ms": mean, "step_excludes": "synthetic trainer stand-in (logp_now), phases_ms.standin",
         "wall_ms_per_step_incl_standin": wall * 1e3 / K,
         "roofline": roof,
@@ -761,7 +783,7 @@ def run_c5(args):
 
 
 # ---------------------------------------------------------------- CPU arm
-def cpu_reference(cfg, steps, warmup, threads=0, budget_s=90.0):
+def cpu_reference(cfg, steps, warmup, threads=0, budget_s=90.0, shards=1):
     """The reference's CPU path (oracle/_ref: unmodified replab buffer/sampler/
     group_advantages + restated token loss) on the host cores."""
     import ctypes as C
@@ -783,7 +805,7 @@ def cpu_reference(cfg, steps, warmup, threads=0, budget_s=90.0):
     L.ref_bench_phase_b.argtypes = [vp, vp, C.c_double, C.c_double, vp, vp, vp, vp]
     L.ref_last_error.restype = C.c_char_p
     ora = Oracle()
-    h = L.ref_bench_new(1, cfg["capacity"], 0, 1 if cfg["retention"] == "positive_bias" else 0,
+    h = L.ref_bench_new(shards, cfg["capacity"], 0, 1 if cfg["retention"] == "positive_bias" else 0,
                         cfg["delta"], cfg["lmax"], SEED, threads)
     if not h:
         raise RuntimeError(L.ref_last_error().decode())
@@ -882,6 +904,12 @@ def main():
                     help="skip the parity check of the last timed step against the CPU oracle")
     ap.add_argument("--eager", dest="graph", action="store_false",
                     help="launch the timed steps eagerly instead of from a CUDA graph")
+    ap.add_argument("--phases", action="store_true",
+                    help="record CUDA events at the phase boundaries (front end | stand-in | "
+                         "loss) inside the graph; the step is the sum of the front end and loss")
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: weak scaling (N x the single-GPU buffer and batch) instead of "
+                         "splitting the single-GPU workload over the N GPUs")
     ap.add_argument("--emulate-world", type=int, default=0,
                     help="diagnostic: run rank 0 of an N-GPU job alone on one GPU (no "
                          "collective); the line predicts the N-GPU step")
@@ -893,26 +921,24 @@ def main():
     emulated = args.emulate_world > 1 and world == 1
     if emulated:
         world = args.emulate_world
-    cfg = scaled_cfg(CONFIGS[args.config], world)
+    cfg = scaled_cfg(CONFIGS[args.config], world, args.weak)
 
     if args.impl == "reference":
         if rank != 0:
             return
-        # bounded sample: the per-GPU workload of each step (the N-GPU job's
-        # step is N of them), at most ~90 s of timed steps
-        r = cpu_reference(CONFIGS[args.config], args.steps, args.warmup)
-        per_gpu = (f", each 1/{world} of the {world}-GPU job's step (weak scaling)"
-                   if world > 1 else "")
+        # bounded sample of the same job's steps (at most ~90 s of timed
+        # steps); N shards for an N-GPU job, like our arm
+        r = cpu_reference(cfg, args.steps, args.warmup, shards=world)
         line = {"metric": METRIC, "value": r["value"], "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-                "data": "synthetic (include/replay_synth.h)", "impl": "reference",
-                "config": {"workload": cfg["name"], "parallelism": "host threads"},
+                "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None,
+                "dtype": "fp32", "data": "synthetic (include/replay_synth.h)", "impl": "reference",
+                "config": config_dict(cfg, world),
                 "cpu_baseline": {"value": r["value"], "unit": "tokens/s", "cores": r["cores"],
                                  "kind": "reference",
-                                 "sample": f"{r['steps']} single-GPU-size {args.config.upper()} "
-                                           f"replay steps ({r['cpu']}){per_gpu}; record ops "
-                                           "through the unmodified replab library, token "
+                                 "sample": f"{r['steps']} {args.config.upper()} replay steps of "
+                                           f"the same job ({r['cpu']}), {world} shard(s); record "
+                                           "ops through the unmodified replab library, token "
                                            "payload/gather/loss restated"},
                 "e2e": {"value": r["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
@@ -940,6 +966,8 @@ def main():
         if same_gpu:
             dist.init_process_group("gloo")
         else:
+            # NCCL's own log (stderr) shows nranks / the NVLink(S) transport
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()  # a real stream handle (not the legacy default)
     with torch.cuda.stream(stream):

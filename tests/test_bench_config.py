@@ -1,4 +1,4 @@
-"""Host logic of bench.py (no GPU): the weak-scaling workload, the production
+"""Host logic of bench.py (no GPU): the strong/weak-scaling workloads, the production
 schedule (bandit.cpp:609-640) and the launch accounting."""
 import importlib.util
 import os
@@ -16,16 +16,24 @@ def bench():
     return m
 
 
-def test_weak_scaling_config(bench):
+def test_scaling_configs(bench):
     c4 = bench.CONFIGS["c4"]
-    assert bench.scaled_cfg(c4, 1) is c4
+    assert bench.scaled_cfg(c4, 1)["capacity"] == c4["capacity"]
     for n in (2, 4, 8):
+        # default: strong scaling — BASELINE configs[3], the 16384 buffer and
+        # B = 4096 split into n shards (one per GPU)
         c = bench.scaled_cfg(c4, n)
-        # per-GPU work fixed: one C4 shard and one C4 batch per GPU
-        assert c["capacity"] == n * c4["capacity"] and c["batch"] == n * c4["batch"]
-        assert c["capacity"] // n == 16384 and c["batch"] // n == 4096
-        assert (c["lmax"], c["group"], c["loss"]) == (c4["lmax"], c4["group"], c4["loss"])
-        assert c["name"].startswith(f"C4 per GPU x {n}")
+        assert (c["capacity"], c["batch"], c["scaling"]) == (16384, 4096, "strong")
+        assert c["capacity"] % n == 0 and c["batch"] % n == 0
+        assert c["name"].startswith(f"C4 over {n} GPUs")
+        # --weak: one C4 shard and one C4 batch per GPU
+        w = bench.scaled_cfg(c4, n, weak=True)
+        assert w["capacity"] == n * c4["capacity"] and w["batch"] == n * c4["batch"]
+        assert w["scaling"] == "weak" and w["name"].startswith(f"C4 per GPU x {n}")
+        assert (w["lmax"], w["group"], w["loss"]) == (c4["lmax"], c4["group"], c4["loss"])
+        # both arms print the same config object
+        assert bench.config_dict(c, n) == bench.config_dict(dict(c), n)
+        assert bench.config_dict(c, n)["shards"] == n
 
 
 def test_schedule_matches_reference_debt(bench):
@@ -39,7 +47,7 @@ def test_schedule_matches_reference_debt(bench):
         total += n * 16
         assert abs(total - per * (i + 1)) < 16
     # weak scaling multiplies the production N-fold
-    _, per8 = bench.schedule(bench.scaled_cfg(c4, 8), 50)
+    _, per8 = bench.schedule(bench.scaled_cfg(c4, 8, weak=True), 50)
     assert abs(sum(per8) - 8 * sum(per_step)) <= 8  # each carries < 1 group of debt
 
 
@@ -47,7 +55,8 @@ def test_launch_accounting(bench):
     c4 = bench.CONFIGS["c4"]
     assert bench.launches_per_step(c4, 1) == 5
     assert bench.launches_per_step(bench.scaled_cfg(c4, 2), 2) == 6      # + finalize
-    assert bench.launches_per_step(bench.scaled_cfg(c4, 4), 4) == 7      # + ring lookahead
+    assert bench.launches_per_step(bench.scaled_cfg(c4, 4), 4) == 6      # strong: B stays 4096
+    assert bench.launches_per_step(bench.scaled_cfg(c4, 4, weak=True), 4) == 7  # + ring lookahead
     assert bench.launches_per_step(bench.CONFIGS["c2"], 1) == 6          # positive bias route
 
 

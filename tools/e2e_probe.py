@@ -9,12 +9,12 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 
-args = bench.argparse.Namespace(steps=8, warmup=3, config="c4", no_e2e=True, graph=False)
+args = bench.argparse.Namespace(steps=8, warmup=3, config="c4", no_e2e=True, graph=False, weak=False)
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
     world = int(os.environ.get("EMU_WORLD", "1"))  # rank 0 of an emulated N-GPU job
     res, buf, wl, rng = bench.run_ours(args, 0, world, None)
-    cfg = bench.scaled_cfg(bench.CONFIGS["c4"], world)
+    cfg = bench.scaled_cfg(bench.CONFIGS["c4"], world, getattr(args, "weak", False))
     B = cfg["batch"]
     hb = {k: v.cpu().pin_memory() for k, v in wl.steps[-1][0].items()}
     pad = B * cfg["lmax"] + 8
