@@ -310,6 +310,8 @@ def run_ours(args, rank, world, dist):
         if world > 1:  # one collective: the registered {objective_sum, included, excluded}
             if dist is not None:
                 dist.all_reduce(red3)
+            else:  # emulated rank 0: the sum over N ranks alike (the collective's result)
+                red3.mul_(world)
             buf.loss_finalize_vec(dlogp, red3, stats)
         if ev:
             ev[3].record(stream)

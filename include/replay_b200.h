@@ -4,7 +4,7 @@
  * reference (/root/reference/proj, C++20, CPU only) has no FFI: its operator
  * API is the C++ headers.  Each entry point below names the reference
  * interface it replaces (file:line relative to /root/reference/proj); the
- * C++ facade in paper_2604_08706_b200/facade/replab/*.hpp re-exposes the
+ * C++ facade in paper_2604_08706_b200/facade/replab/ (one .hpp per header) re-exposes the
  * reference's own class/function signatures on top of this ABI (see
  * INTEGRATION.md for the bindings a maintainer would add).
  *

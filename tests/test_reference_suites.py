@@ -1,4 +1,5 @@
-"""The reference's OWN test suites (test_buffer_core.cpp, test_rng.cpp, test_queue.cpp),
+"""The reference's OWN test suites (test_buffer_core.cpp, test_rng.cpp, test_queue.cpp,
+test_bandit.cpp),
 compiled unchanged from /root/reference/proj/tests by oracle/Makefile with
 the doctest shim (tests/doctest_shim) against
   * the unmodified reference library  (*_ref: pins the shim), and
@@ -13,18 +14,19 @@ import pytest
 REF_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
 
 
-def run(name):
+def run(name, env=None):
     path = os.path.join(REF_DIR, name)
     if not os.path.exists(path):
         pytest.skip(f"{name} not built (reference sources absent where the repo was built)")
-    r = subprocess.run([path], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([path], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, **(env or {})))
     summary = [line for line in r.stdout.splitlines() if line.startswith("[doctest-shim]")]
     assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-4000:])
     assert summary and " 0 failed" in summary[-1], summary
-    return summary[-1]
+    return r.stdout
 
 
-@pytest.mark.parametrize("suite", ["test_buffer_core", "test_rng", "test_queue"])
+@pytest.mark.parametrize("suite", ["test_buffer_core", "test_rng", "test_queue", "test_bandit"])
 def test_reference_suite_against_reference(suite):
     run(f"{suite}_ref")
 
@@ -44,3 +46,21 @@ def test_reference_buffer_suite_against_b200_facade():
 def test_reference_queue_suite_against_b200_facade():
     """All 6 cases of test_queue.cpp (transfer_queue.hpp) pass against the GPU queue."""
     run("test_queue_b200")
+
+
+@pytest.mark.gpu
+def test_reference_bandit_suite_against_b200_facade():
+    """All 19 cases of test_bandit.cpp (advantages, clipped surrogate, exclusion,
+    AsymRE, finite-difference gradients, train() identities) with
+    group_advantages / grpo_loss_grad / asymre_loss_grad / loss_grad replaced by
+    facade/bandit_b200.cpp over the GPU kernels (interposed on the unmodified
+    library, so train() calls them too)."""
+    out = run("test_bandit_b200", env={"RB_FACADE_TRACE": "1"})
+    calls = [line for line in out.splitlines() if line.startswith("[b200-bandit]")]
+    assert calls and int(calls[-1].split()[1]) > 100, calls  # the GPU definitions ran
+
+
+@pytest.mark.gpu
+def test_bandit_facade_header_suite():
+    """Our suite for the standalone facade header replab/bandit.hpp."""
+    run("test_bandit_facade")
