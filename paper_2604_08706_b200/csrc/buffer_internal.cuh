@@ -140,6 +140,9 @@ struct rb_buffer {
     void join_lookahead();
     bool gather_early = false;          // the last kernel on the stream is the fused sampler
     bool early_gather_ok = true;        // RB_NO_EARLY_GATHER unset
+    bool loss_dyn = true;               // long rows: claimed loss units (RB_LOSS_CHUNK_MAJOR: static)
+    bool tma_long = false;              // RB_PAYLOAD_TMA_LONG: bulk copy for rows > PB_CHT too
+    bool chunk_major = true;            // RB_NO_CHUNK_MAJOR unset: long rows, chunk-major units
     void other_work() { pdl_tail = false; gather_early = false; }  // anything else enqueued
     rb::Unit* units_ins = nullptr;      // payload copy units of the last insert
     int* n_units_ins = nullptr;

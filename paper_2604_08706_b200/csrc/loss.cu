@@ -333,11 +333,15 @@ __device__ __noinline__ float grpo_token_exact(float lpn, float lpo, double A,
 // per unit from sign(A), and an fp32 per-unit objective sum; tokens near a
 // clip edge or with |d| >= 80 / non-finite take grpo_token_exact.
 //
-// DYN (long trajectories, one launch): units are claimed from a counter
-// (the next claim in flight while the current unit runs) instead of a static
-// stride, so ragged batches — whose later chunks are mostly empty — do not
-// leave a few CTAs with all the full units.
-template <int U, bool DYN>
+// Unit order.  Selection-major (chunk c of selection b is unit b*ups + c)
+// keeps a selection's chunks together (DRAM page locality: C4).  CM
+// (chunk-major, unit c*nloc + b; long trajectories) deals every CTA of the
+// static stride one chunk of each rank, so ragged batches — whose later
+// chunks are mostly empty — leave no CTA with all the full units (it
+// is the gather's order for long rows; for the loss it measured level with
+// DYN, C3 24.6 vs 24.0 µs).  DYN (long rows, default): units claimed from a
+// counter, the next claim in flight while the current unit runs.
+template <int U, bool DYN, bool CM = false>
 // (More CTAs per SM via a register cap spill and run slower: 44 µs at 10
 // CTAs per SM vs 37 µs at 8.)
 __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
@@ -362,13 +366,14 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
         u = s_claim[0];
     }
     Unit nxt;  // static stride: descriptor of the next unit, loaded one unit ahead
-    if (!DYN && u < nu) nxt = ld_unit(units + u / ups);
+    if (!DYN && u < nu) nxt = ld_unit(units + (CM ? u % nloc : u / ups));
     for (; u < nu;) {
         if (DYN && threadIdx.x == 0) s_claim[p ^ 1] = (int)atomicAdd(&acc->claim, 1u);
-        const int b = u / ups, c = u - b * ups;
+        const int b = CM ? u % nloc : u / ups;
+        const int c = CM ? u / nloc : u - b * ups;
         const Unit un = DYN ? ld_unit(units + b) : nxt;
         const int un_next = DYN ? 0 : u + (int)gridDim.x;
-        if (!DYN && un_next < nu) nxt = ld_unit(units + un_next / ups);
+        if (!DYN && un_next < nu) nxt = ld_unit(units + (CM ? un_next % nloc : un_next / ups));
         const int a = (int)(un.off & 3);
         const int nq = (a + un.len + 3) >> 2;
         if (c * QU < nq) {
@@ -953,8 +958,12 @@ void launch_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl, l
     // claimed units for long (ragged-prone) trajectories in a one-launch loss
     const bool dyn = b->max_tokens > 2 * UNIT_THREADS * LOSS_U * 4 && part_base == 0 &&
                      nparts == grid;
-    if (c.kind == 0 && dyn)
+    if (c.kind == 0 && dyn && b->loss_dyn)
         k_loss_grpo_buf<LOSS_U, true><<<grid, UNIT_THREADS, 0, b->stream>>>(
+            b->v, u, b->n_units_sel, (int)(s1 - s0), lpn, dl, c.p, b->acc,
+            (Partial*)b->loss_partials, kst, b->sel_total, local_fix, part_base, nparts);
+    else if (c.kind == 0 && b->chunk_major && b->max_tokens > 2 * UNIT_THREADS * LOSS_U * 4)
+        k_loss_grpo_buf<LOSS_U, false, true><<<grid, UNIT_THREADS, 0, b->stream>>>(
             b->v, u, b->n_units_sel, (int)(s1 - s0), lpn, dl, c.p, b->acc,
             (Partial*)b->loss_partials, kst, b->sel_total, local_fix, part_base, nparts);
     else if (c.kind == 0)

@@ -415,6 +415,26 @@ STEP_CASES = {
                                     assume_unique=True, overlap=True),
     "early_gather_not_unique": dict(capacity=96, shards=3, batch=48, group=8, lmax=40,
                                     ragged=True, seed=35, early_gather=True),
+    # packed-range gather / loss (packed_range.cuh): trajectories of 1-2
+    # tokens put > PK_SL selections in one CTA's run (the unstaged search), of
+    # 1-5 tokens make almost every warp unit straddle selections
+    "tiny_traj_unstaged": dict(capacity=512, shards=1, batch=4096, group=8, lmax=2, ragged=True,
+                               seed=41, assume_unique=True),
+    "tiny_traj_sharded": dict(capacity=512, shards=2, batch=2048, group=8, lmax=5, ragged=True,
+                              seed=42),
+    "tiny_traj_asymre": dict(capacity=256, shards=1, batch=2048, group=8, lmax=3, ragged=True,
+                             seed=43, loss="asymre", assume_unique=True),
+    "one_token_fixed": dict(capacity=64, shards=1, batch=1024, group=8, lmax=1, ragged=False,
+                            seed=44),
+    # rows longer than 4096 tokens: LSU payload, chunk-major gather, claimed
+    # loss units by default; the alternatives through their switches
+    "long_rows": dict(capacity=64, shards=2, batch=64, group=8, lmax=9000, ragged=True, seed=45,
+                      assume_unique=True),
+    "long_rows_switches": dict(capacity=64, shards=1, batch=48, group=8, lmax=8500, ragged=True,
+                               seed=46, env={"RB_LOSS_CHUNK_MAJOR": "1", "RB_NO_CHUNK_MAJOR": "1",
+                                             "RB_PAYLOAD_TMA_LONG": "1"}),
+    "long_rows_cm_loss": dict(capacity=64, shards=1, batch=48, group=8, lmax=8500, ragged=True,
+                              seed=47, assume_unique=True, env={"RB_LOSS_CHUNK_MAJOR": "1"}),
 }
 
 
@@ -422,10 +442,13 @@ STEP_CASES = {
 def test_replay_step_parity(rb, oracle, case, monkeypatch):
     from tests.harness import StepConfig, run_step_parity
 
-    if STEP_CASES[case].get("early_gather"):
+    cfg = dict(STEP_CASES[case])
+    if cfg.get("early_gather"):
         monkeypatch.setenv("RB_EARLY_GATHER", "1")  # read at buffer creation
+    for k, v in cfg.pop("env", {}).items():
+        monkeypatch.setenv(k, v)
 
-    counts = run_step_parity(StepConfig(**STEP_CASES[case]), steps=12, ora=oracle)
+    counts = run_step_parity(StepConfig(**cfg), steps=12, ora=oracle)
     assert counts["samples"] > 0 and counts["tokens"] > 0
 
 
