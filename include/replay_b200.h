@@ -195,6 +195,16 @@ int rb_batch_ids(rb_buffer* b, uint64_t* out_ids, int32_t* out_lengths, int64_t*
  * out_offsets (n+1, may be NULL) = exclusive scan of lengths.  No reference
  * counterpart (the reference has no tokens). */
 int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* out_offsets);
+/* Zero-copy hand-off of the packed batch (SURVEY.md §8f producer/consumer
+ * edge): gathers this buffer's selections into library-owned device arrays
+ * and returns them as DLPack tensors (DLManagedTensor*, DLPack ABI v0.8:
+ * int32 tokens [total], float32 logp_old [total], int64 offsets [n+1]) that
+ * any DLPack consumer (torch.from_dlpack, cupy, jax) takes over without a
+ * copy; the consumer calls each tensor's deleter.  Synchronises the buffer's
+ * stream (the shapes are device values).  Any output pointer may be NULL. */
+int rb_gather_dlpack(rb_buffer* b, void** out_tokens, void** out_logp_old, void** out_offsets);
+/* Releases an exported tensor nobody consumed (calls its deleter). */
+void rb_dlpack_free(void* managed_tensor);
 
 /* Loss statistics of one step (bandit.hpp:127-131 LossResult, token form). */
 typedef struct rb_loss_stats {

@@ -89,6 +89,8 @@ def _load():
         "rb_batch_total_tokens": (ip, [vp, vp]),
         "rb_batch_ids": (ip, [vp, vp, vp, vp]),
         "rb_gather": (ip, [vp, vp, vp, vp]),
+        "rb_gather_dlpack": (ip, [vp, vp, vp, vp]),
+        "rb_dlpack_free": (None, [vp]),
         "rb_loss_grpo": (ip, [vp, vp, vp, dbl, dbl, i64, vp]),
         "rb_loss_grpo_ex": (ip, [vp, vp, vp, dbl, dbl, ip, i64, vp]),
         "rb_loss_asymre": (ip, [vp, vp, vp, dbl, i64, vp]),

@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <unordered_set>
 #include <vector>
@@ -3050,6 +3051,7 @@ void rb_destroy(rb_buffer* b) { delete b; }
 
 int rb_set_stream(rb_buffer* b, void* stream) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->gather_early = false;
         b->sync();
@@ -3064,6 +3066,7 @@ void* rb_get_stream(rb_buffer* b) { return (void*)b->stream; }
 int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_ids,
               size_t* out_applied, int flags) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->gather_early = false;
         b->join_lookahead();  // before the route: the sampler that follows stays a PDL dependent
@@ -3265,6 +3268,7 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
 int rb_push(rb_buffer* b, const rb_record* rec, const int32_t* tokens, const float* logp_old,
             int32_t n_tokens, rb_record* evicted, int* has_evicted) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->gather_early = false;
         if (has_evicted) *has_evicted = 0;
@@ -3308,6 +3312,7 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
               int64_t* out_shard, int64_t* out_index, rb_use_event* out_events,
               int64_t batch_id, int64_t use_step) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         const size_t T = b->T;
         if (batch_size == 0 || batch_size % T != 0)  // replay_buffer.cpp:189-192
@@ -3495,12 +3500,14 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
 }
 
 int rb_batch_size(const rb_buffer* b, size_t* n) {
+    std::lock_guard<std::recursive_mutex> lk(const_cast<rb_buffer*>(b)->mu);
     *n = b->B;
     return RB_OK;
 }
 
 int rb_batch_total_tokens(rb_buffer* b, int64_t* total) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         long long t[2];
         RB_CUDA(cudaMemcpyAsync(t, b->sel_total, sizeof t, cudaMemcpyDeviceToHost, b->stream));
@@ -3511,6 +3518,7 @@ int rb_batch_total_tokens(rb_buffer* b, int64_t* total) {
 
 int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* out_offsets) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         if (b->stride == 0 && (out_tokens || out_logp_old))
             invalid("rb_gather: buffer holds no token payload (max_tokens = 0)");
@@ -3579,8 +3587,98 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
     });
 }
 
+// ---- DLPack export (ABI v0.8 structs, declared here: no header dependency)
+namespace {
+struct DLDevice_ { int32_t device_type, device_id; };  // kDLCUDA = 2
+struct DLDataType_ { uint8_t code, bits; uint16_t lanes; };  // kDLInt 0, kDLFloat 2
+struct DLTensor_ {
+    void* data;
+    DLDevice_ device;
+    int32_t ndim;
+    DLDataType_ dtype;
+    int64_t* shape;
+    int64_t* strides;
+    uint64_t byte_offset;
+};
+struct DLManagedTensor_ {
+    DLTensor_ dl_tensor;
+    void* manager_ctx;
+    void (*deleter)(DLManagedTensor_*);
+};
+struct DlHolder {
+    DLManagedTensor_ mt;
+    int64_t shape[1];
+    void* mem;
+    int device;
+};
+void dl_delete(DLManagedTensor_* m) {
+    DlHolder* h = static_cast<DlHolder*>(m->manager_ctx);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(h->device);
+    cudaFree(h->mem);
+    cudaSetDevice(prev);
+    delete h;
+}
+DlHolder* dl_alloc(int device, int64_t n, uint8_t code, uint8_t bits) {
+    DlHolder* h = new DlHolder();
+    h->device = device;
+    h->shape[0] = n;
+    if (cudaMalloc(&h->mem, (size_t)std::max<int64_t>(n, 1) * (bits / 8) + 16) != cudaSuccess) {
+        delete h;
+        throw Error(RB_ECUDA, "rb_gather_dlpack: device allocation failed");
+    }
+    DLTensor_& t = h->mt.dl_tensor;
+    t.data = h->mem;
+    t.device = DLDevice_{2, device};
+    t.ndim = 1;
+    t.dtype = DLDataType_{code, bits, 1};
+    t.shape = h->shape;
+    t.strides = nullptr;  // compact
+    t.byte_offset = 0;
+    h->mt.manager_ctx = h;
+    h->mt.deleter = dl_delete;
+    return h;
+}
+}  // namespace
+
+void rb_dlpack_free(void* managed_tensor) {
+    if (auto* m = static_cast<DLManagedTensor_*>(managed_tensor))
+        if (m->deleter) m->deleter(m);
+}
+
+int rb_gather_dlpack(rb_buffer* b, void** out_tokens, void** out_logp_old, void** out_offsets) {
+    return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
+        DeviceScope ds(b->device);
+        if (b->stride == 0 && (out_tokens || out_logp_old))
+            invalid("rb_gather_dlpack: buffer holds no token payload (max_tokens = 0)");
+        const size_t per = b->T ? (b->B / b->T) : 0;
+        const long long lo = (long long)std::min(b->sb * per, b->B);
+        const long long hi = (long long)std::min(b->se * per, b->B);
+        const long long nloc = hi - lo;
+        long long t[2] = {0, 0};
+        RB_CUDA(cudaMemcpyAsync(t, b->sel_total, sizeof t, cudaMemcpyDeviceToHost, b->stream));
+        b->sync_checked();
+        std::unique_ptr<DlHolder, void (*)(DlHolder*)> ht(nullptr, [](DlHolder* h) { if (h) dl_delete(&h->mt); }),
+            hl(nullptr, [](DlHolder* h) { if (h) dl_delete(&h->mt); }),
+            ho(nullptr, [](DlHolder* h) { if (h) dl_delete(&h->mt); });
+        if (out_tokens) ht.reset(dl_alloc(b->device, t[0], 0, 32));
+        if (out_logp_old) hl.reset(dl_alloc(b->device, t[0], 2, 32));
+        if (out_offsets) ho.reset(dl_alloc(b->device, nloc + 1, 0, 64));
+        const int rc = rb_gather(b, ht ? (int32_t*)ht->mem : nullptr, hl ? (float*)hl->mem : nullptr,
+                                 ho ? (int64_t*)ho->mem : nullptr);
+        if (rc != RB_OK) throw Error(rc, rb_last_error());
+        b->sync_checked();  // the arrays are complete for a consumer on any stream
+        if (out_tokens) *out_tokens = &ht.release()->mt;
+        if (out_logp_old) *out_logp_old = &hl.release()->mt;
+        if (out_offsets) *out_offsets = &ho.release()->mt;
+    });
+}
+
 int rb_batch_ids(rb_buffer* b, uint64_t* out_ids, int32_t* out_lengths, int64_t* out_offsets) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->other_work();
         const size_t per = b->T ? (b->B / b->T) : 0;
@@ -3614,6 +3712,7 @@ int rb_shard_capacity(const rb_buffer* b, size_t* out) {
     return RB_OK;
 }
 int rb_size(rb_buffer* b, size_t* out) {
+    std::lock_guard<std::recursive_mutex> lk(b->mu);
     size_t t = 0;
     for (size_t s = 0; s < b->T; ++s) t += (size_t)std::min<long long>(b->h_pushes[s], (long long)b->C);
     *out = t;
@@ -3621,6 +3720,7 @@ int rb_size(rb_buffer* b, size_t* out) {
 }
 int rb_shard_size(rb_buffer* b, size_t shard, size_t* out) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         if (shard >= b->T) throw Error(RB_ELOGIC, "vector::_M_range_check: shard out of range");
         *out = (size_t)std::min<long long>(b->h_pushes[shard], (long long)b->C);
     });
@@ -3628,6 +3728,7 @@ int rb_shard_size(rb_buffer* b, size_t shard, size_t* out) {
 int rb_shard_contents(rb_buffer* b, size_t shard, rb_record* out, size_t capacity,
                       size_t* count) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->other_work();
         if (shard >= b->T) throw Error(RB_ELOGIC, "vector::_M_range_check: shard out of range");
@@ -3647,6 +3748,7 @@ int rb_shard_contents(rb_buffer* b, size_t shard, rb_record* out, size_t capacit
 int rb_record_tokens(rb_buffer* b, size_t shard, size_t index, int32_t* tokens,
                      float* logp_old, int32_t capacity, int32_t* n_tokens) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->other_work();
         if (shard >= b->T) invalid("rb_record_tokens: shard out of range");
@@ -3677,6 +3779,7 @@ int rb_retention(const rb_buffer* b, int* kind, double* delta) {
     return RB_OK;
 }
 int rb_route_cursor(rb_buffer* b, size_t* out) {
+    std::lock_guard<std::recursive_mutex> lk(b->mu);
     *out = b->h_cursor;
     return RB_OK;
 }
@@ -3797,6 +3900,7 @@ SnapHeader snap_header(rb_buffer* b, size_t nsec) {
 int rb_batch_staleness_hist(rb_buffer* b, int64_t use_step, int32_t max_bin, uint64_t* hist,
                             int64_t* sum) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->other_work();
         run_hist(b, max_bin, hist, sum, [&](unsigned long long* h, int64_t* sm, size_t hb) {
@@ -3811,6 +3915,7 @@ int rb_batch_staleness_hist(rb_buffer* b, int64_t use_step, int32_t max_bin, uin
 
 int rb_use_count_hist(rb_buffer* b, int32_t max_bin, uint64_t* hist, uint64_t* sum) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->other_work();
         run_hist(b, max_bin, hist, sum, [&](unsigned long long* h, uint64_t* sm, size_t hb) {
@@ -3822,6 +3927,7 @@ int rb_use_count_hist(rb_buffer* b, int32_t max_bin, uint64_t* hist, uint64_t* s
 
 int rb_snapshot(rb_buffer* b, void* dst, size_t cap, size_t* len) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->other_work();
         const auto secs = snap_sections(b);
@@ -3846,6 +3952,7 @@ int rb_snapshot(rb_buffer* b, void* dst, size_t cap, size_t* len) {
 
 int rb_restore(rb_buffer* b, const void* src, size_t len) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->other_work();
         const auto secs = snap_sections(b);
@@ -3882,12 +3989,14 @@ int rb_restore(rb_buffer* b, const void* src, size_t len) {
 
 int rb_check(rb_buffer* b) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         check_sticky(b);
     });
 }
 int rb_synchronize(rb_buffer* b) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         DeviceScope ds(b->device);
         b->join_lookahead();
         b->sync();
@@ -3897,6 +4006,7 @@ int rb_synchronize(rb_buffer* b) {
 // replay_buffer.cpp:238-255
 int rb_dump(rb_buffer* b, char* out, size_t cap, size_t* len) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         std::string s;
         s += "# sharded_replay_buffer v1\n";
         s += "# shards = " + std::to_string(b->T) + "\n";

@@ -13,6 +13,7 @@
 //             fp32[C][stride], stride = max_tokens rounded up to 4 (16 B rows).
 #pragma once
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -79,6 +80,12 @@ struct PendingIns {
 }  // namespace rb
 
 struct rb_buffer {
+    // Every C-ABI call on a buffer holds this lock, as every method of the
+    // reference's ShardedReplayBuffer holds its mutex (replay_buffer.cpp:84,
+    // 188, 220, 229, 234, 239; replay_buffer.hpp:106-107): concurrent callers
+    // see one total order of pushes and samples.  Recursive: entry points
+    // call one another (rb_push -> rb_insert).
+    std::recursive_mutex mu;
     size_t T = 0, N = 0, C = 0;
     int strategy = 0, retention = 0;
     double delta = 0.0;

@@ -1091,6 +1091,7 @@ int rb_loss_grpo(rb_buffer* b, const float* logp_now, float* out_dlogp, double e
 int rb_loss_grpo_ex(rb_buffer* b, const float* logp_now, float* out_dlogp, double eps_low,
                     double eps_high, int mode, int64_t norm, rb_loss_stats* stats) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         if (mode < RB_GRPO_TOKEN_MEAN || mode > RB_GRPO_SEQ_RATIO)
             invalid("rb_loss_grpo_ex: unknown normalisation mode");
         if (mode != RB_GRPO_TOKEN_MEAN) {
@@ -1145,6 +1146,7 @@ int rb_loss_grpo_ex(rb_buffer* b, const float* logp_now, float* out_dlogp, doubl
 int rb_loss_asymre(rb_buffer* b, const float* logp_now, float* out_dlogp, double delta_v,
                    int64_t norm_batch, rb_loss_stats* stats) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         if (!std::isfinite(delta_v)) invalid("loss spec: parameters must be finite");
         if (b->B == 0) invalid("loss gradient needs a non-empty batch");
         LossCall c;
@@ -1252,6 +1254,7 @@ __global__ void k_finalize_stats(DevLossAcc* acc, rb_loss_stats* st, float* dlog
 
 int rb_loss_set_reduce_vector(rb_buffer* b, double* vec3) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         if (vec3 && !is_device_ptr(vec3)) invalid("rb_loss_set_reduce_vector: device memory required");
         b->other_work();
         k_set_red3<<<1, 1, 0, b->stream>>>(b->acc, vec3);
@@ -1261,6 +1264,7 @@ int rb_loss_set_reduce_vector(rb_buffer* b, double* vec3) {
 
 int rb_loss_finalize_vec(rb_buffer* b, float* dlogp, const double* vec3, rb_loss_stats* stats) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         if (!vec3 || !is_device_ptr(vec3)) invalid("rb_loss_finalize_vec: device vector required");
         b->other_work();
         const bool host = stats && !is_device_ptr(stats);
@@ -1279,6 +1283,7 @@ int rb_loss_finalize_vec(rb_buffer* b, float* dlogp, const double* vec3, rb_loss
 
 int rb_loss_finalize(rb_buffer* b, float* dlogp, rb_loss_stats* stats) {
     return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
         b->other_work();
         // Asynchronous when stats is a device pointer (the multi-GPU hot path:
         // allreduce the device stats, then finalize without a host round trip).

@@ -323,6 +323,15 @@ class ShardedReplayBuffer:
     def gather(self, out_tokens=None, out_logp_old=None, out_offsets=None) -> None:
         check(lib.rb_gather(self._h, _ptr(out_tokens), _ptr(out_logp_old), _ptr(out_offsets)))
 
+    def gather_dlpack(self):
+        """The packed batch as library-owned device arrays handed over through
+        DLPack (rb_gather_dlpack): returns (tokens int32, logp_old float32,
+        offsets int64) as PyCapsules any DLPack consumer takes without a copy,
+        e.g. torch.from_dlpack(capsule)."""
+        ptrs = [C.c_void_p() for _ in range(3)]
+        check(lib.rb_gather_dlpack(self._h, *[C.byref(p) for p in ptrs]))
+        return tuple(_dl_capsule(p.value) for p in ptrs)
+
     @staticmethod
     def _stats_arg(stats):
         """True -> host LossStats (synchronous); None/False -> no stats;
@@ -614,3 +623,28 @@ def summarize_hist(hist, total_sum=None):
             else float((np.arange(hist.size) * hist).sum())) / n
     return {"count": n, "mean": mean, "q25": rank(0.25), "median": rank(0.5), "q75": rank(0.75),
             "histogram": {int(i): int(c) for i, c in enumerate(hist) if c}}
+
+
+# DLPack capsules (the legacy "dltensor" protocol): a consumer renames the
+# capsule "used_dltensor" and owns the tensor; an unconsumed capsule releases
+# it through rb_dlpack_free when collected.
+_capsule_new = C.pythonapi.PyCapsule_New
+_capsule_new.restype = C.py_object
+_capsule_new.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+# (the destructor sees the dying capsule as a raw pointer: no refcounting)
+_capsule_valid = C.pythonapi.PyCapsule_IsValid
+_capsule_valid.restype = C.c_int
+_capsule_valid.argtypes = [C.c_void_p, C.c_char_p]
+_capsule_ptr = C.pythonapi.PyCapsule_GetPointer
+_capsule_ptr.restype = C.c_void_p
+_capsule_ptr.argtypes = [C.c_void_p, C.c_char_p]
+
+
+@C.CFUNCTYPE(None, C.c_void_p)
+def _dl_capsule_destructor(cap):
+    if _capsule_valid(cap, b"dltensor"):
+        lib.rb_dlpack_free(_capsule_ptr(cap, b"dltensor"))
+
+
+def _dl_capsule(ptr):
+    return _capsule_new(ptr, b"dltensor", C.cast(_dl_capsule_destructor, C.c_void_p))
