@@ -295,6 +295,39 @@ int rb_batch_staleness_hist(rb_buffer* b, int64_t use_step, int32_t max_bin, uin
                             int64_t* sum);
 int rb_use_count_hist(rb_buffer* b, int32_t max_bin, uint64_t* hist, uint64_t* sum);
 
+/* ---- the UseEvent ledger on the device (metrics.hpp:36-93) -------------
+ * Replaces MetricsLedger + replay_counts / global_use_order /
+ * steps_since_last_use (metrics.cpp:44-69, 123-170).  Events are SoA device
+ * arrays; record_batch appends the buffer's current batch from a kernel on
+ * the buffer's stream (call it after rb_sample*, before the next insert).
+ * Generated twice / duplicate (batch, rank) fail at the call with the
+ * reference's messages; a use before creation is detected on the device and
+ * reported (RB_EINVAL) by the next rb_ledger_* call that synchronises, which
+ * then holds the events recorded before the offending one — the reference's
+ * state after its throw.  Output arrays may be host or device memory. */
+typedef struct rb_ledger rb_ledger;
+int rb_ledger_create(int device, rb_ledger** out);
+void rb_ledger_destroy(rb_ledger* l);
+int rb_ledger_note_generated(rb_ledger* l, const uint64_t* ids, size_t n);        /* metrics.cpp:44-53 */
+int rb_ledger_record_batch(rb_ledger* l, rb_buffer* b, int64_t batch_id, int64_t use_step);
+                                                             /* replay_buffer.cpp:205-215 */
+int rb_ledger_record_uses(rb_ledger* l, const rb_use_event* events, size_t n);   /* metrics.cpp:56-69 */
+int rb_ledger_check(rb_ledger* l);
+int rb_ledger_sizes(rb_ledger* l, size_t* n_events, size_t* n_generated);
+int rb_ledger_events(rb_ledger* l, rb_use_event* out, size_t cap, size_t* n);
+/* metrics.cpp:123-131: ascending ids and their use counts (generated ids
+ * never used at 0 when include_zero_use); call with NULL outputs to size. */
+int rb_ledger_replay_counts(rb_ledger* l, int include_zero_use, uint64_t* out_ids,
+                            uint64_t* out_counts, size_t cap, size_t* n);
+/* metrics.cpp:133-151: event indices in global use order; consumes rng
+ * exactly like Rng::shuffle of every batch (rng.hpp:59-64). */
+int rb_ledger_global_use_order(rb_ledger* l, rb_rng* rng, uint64_t* out_order, size_t cap,
+                               size_t* n);
+/* metrics.cpp:153-170: per position of the global use order, the event
+ * index and the gap to the rollout's previous use (has_gap 0 = first use). */
+int rb_ledger_steps_since_last_use(rb_ledger* l, rb_rng* rng, uint64_t* out_event_index,
+                                   int64_t* out_gap, uint8_t* out_has_gap, size_t cap, size_t* n);
+
 /* Binary checkpoint of the whole device state — metadata columns, arrival
  * structures (positive-bias queues), owned token payload rows, route cursor,
  * per-shard push counts — for run resumption (the

@@ -373,6 +373,18 @@ class Reference:
         L.ref_buf_load.restype = vp
         L.ref_buf_load.argtypes = [C.c_char_p]
         L.ref_group_advantages.argtypes = [vp, u64, vp]
+        L.ref_ledger_new.restype = vp
+        L.ref_ledger_free.argtypes = [vp]
+        L.ref_ledger_note_generated.argtypes = [vp, u64]
+        L.ref_ledger_record_use.argtypes = [vp, vp]
+        L.ref_ledger_events.restype = u64
+        L.ref_ledger_events.argtypes = [vp, vp]
+        L.ref_ledger_replay_counts.restype = u64
+        L.ref_ledger_replay_counts.argtypes = [vp, C.c_int, vp, vp]
+        L.ref_ledger_global_use_order.restype = u64
+        L.ref_ledger_global_use_order.argtypes = [vp, vp, vp]
+        L.ref_ledger_steps_since_last_use.restype = u64
+        L.ref_ledger_steps_since_last_use.argtypes = [vp, vp, vp, vp, vp]
         L.ref_loss_records.argtypes = [C.c_int, vp, vp, vp, u64, dbl, dbl, dbl, vp, vp, vp, vp]
 
     def err(self):
@@ -391,6 +403,9 @@ class Reference:
         if self.lib.ref_group_advantages(_p(r), r.size, _p(out)):
             raise self.err()
         return out
+
+    def ledger(self):
+        return RefLedger(self)
 
     def summarize(self, values):
         """The reference's summarize() (metrics.cpp:185-202) as a dict."""
@@ -513,3 +528,49 @@ class RefBuffer:
         if not h:
             raise ref.err()
         return RefBuffer(ref, 0, 0, None, None, 0.0, _h=h)
+
+
+class RefLedger:
+    """replab::MetricsLedger and its diagnostics (metrics.cpp:44-170)."""
+
+    def __init__(self, ref: Reference):
+        self.r, self.h = ref, ref.lib.ref_ledger_new()
+
+    def __del__(self):
+        try:
+            self.r.lib.ref_ledger_free(self.h)
+        except Exception:  # noqa: BLE001
+            pass
+
+    def note_generated(self, rid):
+        if self.r.lib.ref_ledger_note_generated(self.h, int(rid)):
+            raise self.r.err()
+
+    def record_use(self, rid, creation_step, use_step, batch_id, rank):
+        e = np.array([rid, creation_step, use_step, batch_id, rank], np.int64)
+        if self.r.lib.ref_ledger_record_use(self.h, _p(e)):
+            raise self.r.err()
+
+    def events(self):
+        n = self.r.lib.ref_ledger_events(self.h, None)
+        out = np.zeros((n, 5), np.int64)
+        self.r.lib.ref_ledger_events(self.h, _p(out))
+        return out
+
+    def replay_counts(self, include_zero_use=True):
+        n = self.r.lib.ref_ledger_replay_counts(self.h, int(include_zero_use), None, None)
+        ids, cnt = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
+        self.r.lib.ref_ledger_replay_counts(self.h, int(include_zero_use), _p(ids), _p(cnt))
+        return ids, cnt
+
+    def global_use_order(self, rng: "RefRng"):
+        n = self.r.lib.ref_ledger_events(self.h, None)
+        out = np.zeros(n, np.uint64)
+        self.r.lib.ref_ledger_global_use_order(self.h, rng.h, _p(out))
+        return out
+
+    def steps_since_last_use(self, rng: "RefRng"):
+        n = self.r.lib.ref_ledger_events(self.h, None)
+        idx, gap, has = np.zeros(n, np.uint64), np.zeros(n, np.int64), np.zeros(n, np.uint8)
+        self.r.lib.ref_ledger_steps_since_last_use(self.h, rng.h, _p(idx), _p(gap), _p(has))
+        return idx, gap, has

@@ -178,6 +178,62 @@ int ref_summarize(const double* v, uint64_t n, double* out, int64_t* hist_keys,
 }
 
 // ---- advantages and losses ---------------------------------------------
+// MetricsLedger + its diagnostics (metrics.hpp:36-93, metrics.cpp:44-170).
+// Events as 5 int64 words: rollout_id, creation_step, use_step, batch_id, rank.
+void* ref_ledger_new() { return new MetricsLedger(); }
+void ref_ledger_free(void* l) { delete static_cast<MetricsLedger*>(l); }
+int ref_ledger_note_generated(void* l, uint64_t id) {
+    return guard([&] { static_cast<MetricsLedger*>(l)->note_generated(id); });
+}
+int ref_ledger_record_use(void* l, const int64_t* e) {
+    return guard([&] {
+        UseEvent u;
+        u.rollout_id = (uint64_t)e[0];
+        u.creation_step = e[1];
+        u.use_step = e[2];
+        u.batch_id = e[3];
+        u.within_batch_rank = e[4];
+        static_cast<MetricsLedger*>(l)->record_use(u);
+    });
+}
+uint64_t ref_ledger_events(void* l, int64_t* out) {
+    const auto& ev = static_cast<MetricsLedger*>(l)->events();
+    if (out)
+        for (size_t i = 0; i < ev.size(); ++i) {
+            out[5 * i] = (int64_t)ev[i].rollout_id;
+            out[5 * i + 1] = ev[i].creation_step;
+            out[5 * i + 2] = ev[i].use_step;
+            out[5 * i + 3] = ev[i].batch_id;
+            out[5 * i + 4] = ev[i].within_batch_rank;
+        }
+    return ev.size();
+}
+uint64_t ref_ledger_replay_counts(void* l, int include_zero, uint64_t* ids, uint64_t* counts) {
+    const auto m = replay_counts(*static_cast<MetricsLedger*>(l), include_zero != 0);
+    size_t i = 0;
+    for (const auto& [k, v] : m) {
+        if (ids) ids[i] = k;
+        if (counts) counts[i] = v;
+        ++i;
+    }
+    return m.size();
+}
+uint64_t ref_ledger_global_use_order(void* l, void* rng, uint64_t* order) {
+    const auto o = global_use_order(static_cast<MetricsLedger*>(l)->events(), *static_cast<Rng*>(rng));
+    for (size_t i = 0; i < o.size(); ++i) order[i] = o[i];
+    return o.size();
+}
+uint64_t ref_ledger_steps_since_last_use(void* l, void* rng, uint64_t* idx, int64_t* gap,
+                                         uint8_t* has) {
+    const auto lab = steps_since_last_use(*static_cast<MetricsLedger*>(l), *static_cast<Rng*>(rng));
+    for (size_t i = 0; i < lab.size(); ++i) {
+        idx[i] = lab[i].event_index;
+        has[i] = lab[i].gap.has_value();
+        gap[i] = lab[i].gap.value_or(0);
+    }
+    return lab.size();
+}
+
 int ref_group_advantages(const double* r, uint64_t n, double* out) {
     return guard([&] {
         auto v = group_advantages(std::vector<double>(r, r + n));

@@ -7,11 +7,12 @@ sm_100a CUDA kernels behind the C-ABI of include/replay_b200.h
 over that ABI; there is no CPU fallback.
 """
 from ._lib import LossStats
-from .replay import (EVENT_DTYPE, NONE_ID, RECORD_DTYPE, Rng, ShardedReplayBuffer, TransferQueue,
+from .replay import (EVENT_DTYPE, NONE_ID, RECORD_DTYPE, MetricsLedger, Rng, ShardedReplayBuffer,
+                     TransferQueue,
                      asymre_records,
                      asymre_tokens, group_advantages, grpo_records, grpo_tokens, hash_name,
                      summarize_hist)
 
-__all__ = ["Rng", "ShardedReplayBuffer", "TransferQueue", "group_advantages", "grpo_tokens", "grpo_records",
+__all__ = ["Rng", "ShardedReplayBuffer", "TransferQueue", "MetricsLedger", "group_advantages", "grpo_tokens", "grpo_records",
            "asymre_tokens", "asymre_records", "hash_name", "RECORD_DTYPE", "EVENT_DTYPE",
            "NONE_ID", "summarize_hist", "LossStats"]

@@ -91,6 +91,17 @@ def _load():
         "rb_gather": (ip, [vp, vp, vp, vp]),
         "rb_gather_dlpack": (ip, [vp, vp, vp, vp]),
         "rb_dlpack_free": (None, [vp]),
+        "rb_ledger_create": (ip, [ip, vp]),
+        "rb_ledger_destroy": (None, [vp]),
+        "rb_ledger_note_generated": (ip, [vp, vp, sz]),
+        "rb_ledger_record_batch": (ip, [vp, vp, i64, i64]),
+        "rb_ledger_record_uses": (ip, [vp, vp, sz]),
+        "rb_ledger_check": (ip, [vp]),
+        "rb_ledger_sizes": (ip, [vp, vp, vp]),
+        "rb_ledger_events": (ip, [vp, vp, sz, vp]),
+        "rb_ledger_replay_counts": (ip, [vp, ip, vp, vp, sz, vp]),
+        "rb_ledger_global_use_order": (ip, [vp, vp, vp, sz, vp]),
+        "rb_ledger_steps_since_last_use": (ip, [vp, vp, vp, vp, vp, sz, vp]),
         "rb_loss_grpo": (ip, [vp, vp, vp, dbl, dbl, i64, vp]),
         "rb_loss_grpo_ex": (ip, [vp, vp, vp, dbl, dbl, ip, i64, vp]),
         "rb_loss_asymre": (ip, [vp, vp, vp, dbl, i64, vp]),

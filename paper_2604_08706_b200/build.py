@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libreplay_b200.so")
-SOURCES = ["rng.cu", "buffer.cu", "loss.cu", "queue.cu"]
+SOURCES = ["rng.cu", "buffer.cu", "loss.cu", "queue.cu", "ledger.cu"]
 HEADERS = ["common.cuh", "rng_internal.cuh", "buffer_internal.cuh", "stream_copy.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -517,6 +517,76 @@ def asymre_records(logp_now, reward, group_mean, delta_v=-0.1, out=None):
 
 
 # ---------------------------------------------------------------------------
+class MetricsLedger:
+    """replab::MetricsLedger (metrics.hpp:36-93) on the device, with
+    replay_counts / global_use_order / steps_since_last_use
+    (metrics.cpp:123-170) computed by kernels (rb_ledger_*)."""
+
+    def __init__(self, device: int = -1):
+        h = C.c_void_p()
+        check(lib.rb_ledger_create(device, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.rb_ledger_destroy(h)
+            self._h = None
+
+    def note_generated(self, ids) -> None:
+        a = _arr(ids, np.uint64)
+        check(lib.rb_ledger_note_generated(self._h, _ptr(a), int(a.shape[0])))
+
+    def record_batch(self, buffer: "ShardedReplayBuffer", batch_id: int, use_step: int) -> None:
+        """The events of buffer's current batch (sample(..., &ledger, batch_id,
+        use_step)), appended on the device."""
+        check(lib.rb_ledger_record_batch(self._h, buffer._h, int(batch_id), int(use_step)))
+
+    def record_use(self, events) -> None:
+        ev = np.ascontiguousarray(events, EVENT_DTYPE).reshape(-1)
+        check(lib.rb_ledger_record_uses(self._h, ev.ctypes.data, ev.shape[0]))
+
+    def check(self) -> None:
+        check(lib.rb_ledger_check(self._h))
+
+    def __len__(self) -> int:
+        n = C.c_size_t()
+        check(lib.rb_ledger_sizes(self._h, C.byref(n), None))
+        return n.value
+
+    def events(self) -> np.ndarray:
+        n = C.c_size_t()
+        check(lib.rb_ledger_events(self._h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, EVENT_DTYPE)
+        check(lib.rb_ledger_events(self._h, out.ctypes.data, n.value, C.byref(n)))
+        return out
+
+    def replay_counts(self, include_zero_use: bool = True):
+        """(ids ascending, use counts) — replay_counts() as two arrays."""
+        n = C.c_size_t()
+        check(lib.rb_ledger_replay_counts(self._h, int(include_zero_use), None, None, 0, C.byref(n)))
+        ids, cnt = np.zeros(n.value, np.uint64), np.zeros(n.value, np.uint64)
+        check(lib.rb_ledger_replay_counts(self._h, int(include_zero_use), ids.ctypes.data,
+                                          cnt.ctypes.data, n.value, C.byref(n)))
+        return ids, cnt
+
+    def global_use_order(self, rng: Rng) -> np.ndarray:
+        m = len(self)
+        out = np.zeros(m, np.uint64)
+        n = C.c_size_t()
+        check(lib.rb_ledger_global_use_order(self._h, rng.handle, out.ctypes.data, m, C.byref(n)))
+        return out
+
+    def steps_since_last_use(self, rng: Rng):
+        """(event_index, gap, has_gap) in global use order; has_gap 0 = first use."""
+        m = len(self)
+        idx, gap, has = np.zeros(m, np.uint64), np.zeros(m, np.int64), np.zeros(m, np.uint8)
+        n = C.c_size_t()
+        check(lib.rb_ledger_steps_since_last_use(self._h, rng.handle, idx.ctypes.data,
+                                                 gap.ctypes.data, has.ctypes.data, m, C.byref(n)))
+        return idx, gap, has
+
+
 class TransferQueue:
     """replab::TransferQueue (transfer_queue.hpp:12-35) on the GPU: a
     consume-once LIFO hand-off whose records and token payload stay in HBM.
