@@ -598,6 +598,10 @@ def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None, rank=0):
         hb = {k: v.cpu().pin_memory() for k, v in b.items()}
         host.append((hb, n, tot))
     pad = B * cfg["lmax"] + 8  # upper bound (ragged batches differ per step)
+    # the dlogp download of step i drains while step i+1's insert uploads
+    # (the other PCIe direction); every step's copies complete inside the
+    # timed region (device-wide synchronise at its end)
+    buf.set_async_outputs(True)
     tok_h = torch.empty(pad, dtype=torch.int32).pin_memory()
     off_h = torch.empty(B + 1, dtype=torch.int64).pin_memory()
     dl_h = torch.empty(pad, dtype=torch.float32).pin_memory()
@@ -665,6 +669,7 @@ def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None, rank=0):
         d2h += tot_s * 4 * 2 + (B + 1) * 8 + 40
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / len(host)
+    buf.set_async_outputs(False)
     if world > 1:  # whole job: tokens of every rank over the slowest rank's time
         if dist is not None:  # device tensors: NCCL reduces CUDA memory only
             t = torch.tensor([float(done_tokens), dt], dtype=torch.float64, device="cuda")
@@ -678,7 +683,9 @@ def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None, rank=0):
             "h2d_bytes_per_step": h2d // len(host), "d2h_bytes_per_step": d2h // len(host),
             "steps": len(host), "path": "rb_insert/rb_sample/rb_gather/rb_loss_* with pinned host "
                                         "buffers (copies inside the timed region; the loss "
-                                        "pipelines its upload/download in chunks)"}
+                                        "pipelines its upload/download in chunks; its dlogp "
+                                        "download overlaps the next step's insert upload, "
+                                        "rb_set_async_outputs)"}
 
 
 # ---------------------------------------------------------------- C5 sweep

@@ -127,6 +127,12 @@ void rb_destroy(rb_buffer* b);
 /* Enqueue on the given CUDA stream (cudaStream_t as void*; NULL = the legacy
  * default stream).  Buffers start on a library-owned non-blocking stream. */
 int rb_set_stream(rb_buffer* b, void* stream);
+/* Asynchronous host outputs (off by default): a loss whose out_dlogp is
+ * pinned host memory returns once its stats are final while the dlogp
+ * download drains on a copy stream beside the caller's next call (e.g. the
+ * next insert's upload, the other PCIe direction).  out_dlogp is complete
+ * after rb_synchronize (or cudaDeviceSynchronize). */
+int rb_set_async_outputs(rb_buffer* b, int on);
 void* rb_get_stream(rb_buffer* b);
 
 /* push (replay_buffer.cpp:83-96): one record, synchronous.  Rejects an id

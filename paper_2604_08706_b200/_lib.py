@@ -91,6 +91,7 @@ def _load():
         "rb_gather": (ip, [vp, vp, vp, vp]),
         "rb_gather_dlpack": (ip, [vp, vp, vp, vp]),
         "rb_dlpack_free": (None, [vp]),
+        "rb_set_async_outputs": (ip, [vp, ip]),
         "rb_ledger_create": (ip, [ip, vp]),
         "rb_ledger_destroy": (None, [vp]),
         "rb_ledger_note_generated": (ip, [vp, vp, sz]),

@@ -2538,6 +2538,8 @@ __global__ void k_load_posbias(BufView v, int s, int n, const rb_record* recs) {
 rb_buffer::~rb_buffer() {
     if (device >= 0) cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
+    if (out_pending) cudaEventSynchronize(out_done);
+    if (out_done) cudaEventDestroy(out_done);
     if (look_ev) {
         if (cudaEventSynchronize(look_ev) != cudaSuccess) cudaDeviceSynchronize();  // captured
         cudaEventDestroy(look_ev);
@@ -2595,6 +2597,7 @@ void* rb_buffer::host_stage(size_t bytes) {
 void* rb_buffer::dev_stage(size_t bytes, int slot) {
     if (bytes > stage_dev_cap[slot]) {
         sync();
+        drain_outputs();  // an asynchronous download may still read the old area
         if (stage_dev[slot]) cudaFree(stage_dev[slot]);
         stage_dev_cap[slot] = std::max(bytes, stage_dev_cap[slot] * 2);
         RB_CUDA(cudaMalloc(&stage_dev[slot], stage_dev_cap[slot]));
@@ -2662,6 +2665,14 @@ void rb_buffer::ensure_select(size_t n) {
     sel_off = dalloc<int64_t>(sel_cap + 1);
 }
 void rb_buffer::sync() { RB_CUDA(cudaStreamSynchronize(stream)); }
+void rb_buffer::wait_outputs_on(cudaStream_t s) {
+    if (out_pending) RB_CUDA(cudaStreamWaitEvent(s, out_done, 0));
+}
+void rb_buffer::drain_outputs() {
+    if (!out_pending) return;
+    RB_CUDA(cudaEventSynchronize(out_done));
+    out_pending = false;
+}
 
 namespace {
 
@@ -4000,6 +4011,16 @@ int rb_synchronize(rb_buffer* b) {
         DeviceScope ds(b->device);
         b->join_lookahead();
         b->sync();
+        b->drain_outputs();
+    });
+}
+
+int rb_set_async_outputs(rb_buffer* b, int on) {
+    return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
+        DeviceScope ds(b->device);
+        if (!on) b->drain_outputs();
+        b->async_out = on != 0;
     });
 }
 

@@ -163,6 +163,14 @@ struct rb_buffer {
     // host-buffer loss pipeline: upload / download streams and chunk events
     cudaStream_t cs_in = nullptr, cs_out = nullptr;
     cudaEvent_t ev_io[1 + 2 * 8] = {};  // LOSS_CHUNKS = 8
+    // rb_set_async_outputs: a loss with pinned host dlogp returns once its
+    // stats are final; the download drains on cs_out beside the next call
+    // (an insert's upload runs the other way over PCIe).  out_done marks it.
+    bool async_out = false;
+    bool out_pending = false;
+    cudaEvent_t out_done = nullptr;
+    void wait_outputs_on(cudaStream_t s);  // order s after a pending download
+    void drain_outputs();                  // host wait for it
 
     // current batch (selection)
     size_t sel_cap = 0, B = 0;

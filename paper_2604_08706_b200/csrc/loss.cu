@@ -1012,6 +1012,7 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
         b->sync();
         const long long total = off[nloc];
         const size_t bytes = (((size_t)total + 3) & ~size_t(3)) * 4 + 16;
+        b->wait_outputs_on(b->stream);  // the last async download still reads the staging output
         float* din = host_in ? (float*)b->dev_stage(bytes, rb_buffer::ST_LOSS_IN) : (float*)lpn;
         float* dout = host_out ? (float*)b->dev_stage(bytes, rb_buffer::ST_LOSS_OUT) : dl;
         const bool pin_in = !host_in || is_pinned_ptr(lpn);
@@ -1056,11 +1057,19 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
             }
         }
         if (host_in && !pin_in) b->host_stage_issued_on(b->cs_in);
-        RB_CUDA(cudaStreamSynchronize(b->cs_out));
+        const bool async_dl = b->async_out && host_out && pin_out;
+        if (async_dl) {  // the download drains beside the caller's next call
+            if (!b->out_done) RB_CUDA(cudaEventCreateWithFlags(&b->out_done, cudaEventDisableTiming));
+            RB_CUDA(cudaEventRecord(b->out_done, b->cs_out));
+            b->out_pending = true;
+        } else {
+            RB_CUDA(cudaStreamSynchronize(b->cs_out));
+        }
         RB_CUDA(cudaStreamSynchronize(b->stream));
         DevLossAcc acc;
         RB_CUDA(cudaMemcpy(&acc, b->acc, sizeof acc, cudaMemcpyDeviceToHost));
         const bool fix = c.kind == 0 && acc.need_fixup && single;
+        if (fix) b->drain_outputs();  // the rescaled array is downloaded again below
         if (fix) {  // -1/total -> -1/included (rare: a non-finite ratio)
             k_dlogp_rescale<<<grid_for(total), 256, 0, b->stream>>>(dout, total, nullptr, b->acc);
             k_set_cur_div_included<<<1, 1, 0, b->stream>>>(b->acc);  // after every rescale CTA read it

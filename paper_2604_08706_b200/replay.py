@@ -323,6 +323,11 @@ class ShardedReplayBuffer:
     def gather(self, out_tokens=None, out_logp_old=None, out_offsets=None) -> None:
         check(lib.rb_gather(self._h, _ptr(out_tokens), _ptr(out_logp_old), _ptr(out_offsets)))
 
+    def set_async_outputs(self, on: bool = True) -> None:
+        """rb_set_async_outputs: pinned host dlogp of a loss completes after
+        synchronize() instead of before the call returns."""
+        check(lib.rb_set_async_outputs(self._h, int(bool(on))))
+
     def gather_dlpack(self):
         """The packed batch as library-owned device arrays handed over through
         DLPack (rb_gather_dlpack): returns (tokens int32, logp_old float32,

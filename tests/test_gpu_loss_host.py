@@ -77,3 +77,34 @@ def test_host_buffer_loss_matches_device(batch, kind, memory, excluded):
         assert abs(st_h.objective - st_d.objective) <= 1e-12 * max(1.0, abs(st_d.objective))
     else:  # AsymRE has no exclusion: a non-finite logp_now reaches the objective
         assert st_h.objective == st_d.objective
+
+
+@pytest.mark.parametrize("excluded", [False, True])
+def test_async_host_outputs(batch, excluded):
+    """rb_set_async_outputs: the pinned dlogp download completes after
+    synchronize(); back-to-back calls reuse the staging area safely."""
+    buf, lpn0, total = batch
+    lpn = lpn0.copy()
+    if excluded:
+        lpn[total // 5] = np.float32(np.inf)
+    pad = total + 8
+    lpn_d = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
+    lpn_d[:total] = torch.from_numpy(lpn)
+    dl_d = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
+    torch.cuda.synchronize()
+    st_d = _run(buf, "grpo", lpn_d, dl_d)
+    buf.synchronize()
+    want = dl_d[:total].cpu().numpy()
+    lpn_h = torch.zeros(pad, dtype=torch.float32).pin_memory()
+    lpn_h[:total] = torch.from_numpy(lpn)
+    outs = [torch.full((pad,), -5.0, dtype=torch.float32).pin_memory() for _ in range(3)]
+    buf.set_async_outputs(True)
+    try:
+        for o in outs:  # three calls in a row, no synchronisation between them
+            st = _run(buf, "grpo", lpn_h, o)
+            assert (st.included, st.excluded) == (st_d.included, st_d.excluded)
+        buf.synchronize()
+    finally:
+        buf.set_async_outputs(False)
+    for o in outs:
+        np.testing.assert_array_equal(o[:total].numpy(), want)
