@@ -2209,6 +2209,453 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     RB_TEND(0);
 }
 
+// ---- positive bias, ids promised new: one launch, one CTA per shard -------
+// Replaces k_insert_route + k_posbias_batch for RB_INSERT_ASSUME_UNIQUE
+// batches whose shard state fits shared memory (C <= PBP_CMAX, <= PBP_NSMAX
+// pushes per shard).  Every CTA validates the whole batch itself (the
+// reference's all-or-nothing order, replay_buffer.cpp:85-88) and computes
+// its own records' group advantages (bandit.cpp:276-294, fp64, sequential
+// order).  The queue update (replay_buffer.cpp:98-133 as F/W/Q queues, see
+// pb_push_logic) runs in parallel once the shard is full:
+//   * push k moves e_k — the k-th element of (F ++ batch) — from F into the
+//     reserve (W if wrong, Q if correct) and then evicts W's head if W is
+//     non-empty, else Q's head;
+//   * |W| follows the Lindley recursion w_k = max(w_{k-1} + wrong_k - 1, 0),
+//     whose prefix is a block scan of the max-plus maps w -> max(w + A, B)
+//     ((A1,B1) then (A2,B2) = (A1+A2, max(B1+A2, B2)));
+//   * the m-th W pop takes the m-th element of (W ++ wrong entries), the
+//     m-th Q pop likewise (prefix counts), so every victim is known at once;
+//   * a pushed record takes its victim's slot: chains through earlier pushes
+//     of the batch are resolved by pointer jumping.
+// While a shard is still filling (or fresh_slots == 0) thread 0 runs the
+// O(1)-per-push simulation on the shared-memory rings instead.  Then, per
+// shard in parallel: evicted ids, survivors' metadata, payload descriptors,
+// rings rewritten from head 0, and the materialised arrival order
+// (merge(W, Q) by arrival sequence, then F).
+constexpr int PBP_THREADS = 1024;
+constexpr int PBP_CMAX = 4096;
+constexpr int PBP_NSMAX = 4096;
+constexpr int PBP_NMAX = 65536;
+
+struct MaxPlus {
+    int a, b;  // w -> max(w + a, b)
+};
+__device__ __forceinline__ MaxPlus mp_then(MaxPlus x, MaxPlus y) {  // x first, then y
+    return MaxPlus{x.a + y.a, max(x.b + y.a, y.b)};
+}
+// Block-wide exclusive scan of max-plus maps (identity {0, INT_MIN/2}).
+__device__ MaxPlus block_scan_mp(MaxPlus x) {
+    __shared__ int s_a[32], s_b[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    MaxPlus inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const MaxPlus y{__shfl_up_sync(0xffffffffu, inc.a, o), __shfl_up_sync(0xffffffffu, inc.b, o)};
+        if (lane >= o) inc = mp_then(y, inc);
+    }
+    if (lane == 31) {
+        s_a[wid] = inc.a;
+        s_b[wid] = inc.b;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        MaxPlus w = lane < nw ? MaxPlus{s_a[lane], s_b[lane]} : MaxPlus{0, INT_MIN / 2};
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const MaxPlus y{__shfl_up_sync(0xffffffffu, w.a, o), __shfl_up_sync(0xffffffffu, w.b, o)};
+            if (lane >= o) w = mp_then(y, w);
+        }
+        s_a[lane] = w.a;
+        s_b[lane] = w.b;
+    }
+    __syncthreads();
+    const MaxPlus base = wid ? MaxPlus{s_a[wid - 1], s_b[wid - 1]} : MaxPlus{0, INT_MIN / 2};
+    // exclusive within the warp: the inclusive value of the lane before
+    MaxPlus ex{__shfl_up_sync(0xffffffffu, inc.a, 1), __shfl_up_sync(0xffffffffu, inc.b, 1)};
+    if (lane == 0) ex = MaxPlus{0, INT_MIN / 2};
+    __syncthreads();
+    return mp_then(base, ex);
+}
+
+__global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn in,
+                                                             unsigned long long cur0,
+                                                             GridCtl* gc, int nsp) {
+    extern __shared__ __align__(16) unsigned char pbp_sm[];
+    __shared__ long long s_goff[RT_GOFF + 1];
+    __shared__ int s_maxq;
+    __shared__ PbState s_st;
+    const int s = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    const int T = v.T, C = v.C, RC = C + 1, fs = v.fs;
+    DevCtl* ctl = v.ctl;
+    const int n = (int)in.n;
+    const long long ng = in.ngroups;
+    const int j0 = (int)(((long long)s - (long long)(cur0 % (unsigned long long)T)) % T + T) % T;
+    const int ns = n > j0 ? (n - 1 - j0) / T + 1 : 0;
+    RB_GCLOCK(20, s == 0);
+    // shared memory: preseq / preid [C] (i64), rings [3][RC], occb [C], per
+    // push: vk, slotk, WE, QE (i32), cx, evw (u8)
+    long long* preseq = reinterpret_cast<long long*>(pbp_sm);
+    uint64_t* preid = reinterpret_cast<uint64_t*>(preseq + C);
+    uint32_t* ring = reinterpret_cast<uint32_t*>(preid + C);
+    int* occb = reinterpret_cast<int*>(ring + 3 * RC);
+    int* vk = occb + C;       // victim of push k: -1 none, -2 itself, < C pre slot, C + k'' push k''
+    int* slotk = vk + nsp;  // local slot of push k's record (-1: evicted on arrival)
+    int* WE = slotk + nsp;  // wrong entries in order (element ids)
+    int* QE = WE + nsp;     // correct entries in order
+    uint8_t* cx = reinterpret_cast<uint8_t*>(QE + nsp);  // correctness of push k
+    uint8_t* evw = cx + nsp;                             // push k pops W
+    // Every load below is independent (one memory round trip): control
+    // block, queue state, group offsets, the shard's pre-batch ids and
+    // sequence numbers, the whole batch's validation inputs.
+    const int sticky = ctl->err_code;
+    const int has_any = ctl->has_any;
+    const unsigned long long max_id = ctl->max_id;
+    const long long P0 = v.pushes[s];
+    if (tid == 0) {
+        s_st = v.pbs[s];
+        s_maxq = 0;
+    }
+    const bool goff_smem = !in.adv && ng <= RT_GOFF;
+    if (goff_smem)
+        for (long long gi = tid; gi <= ng; gi += nt) s_goff[gi] = in.goff[gi];
+    for (int x = tid; x < C; x += nt) {
+        preseq[x] = v.seq[(size_t)s * C + x];
+        preid[x] = v.id[(size_t)s * C + x];
+        occb[x] = -1;
+    }
+    // whole-batch validation (nothing applied if any check fails)
+    int bad = 0;
+    for (int jj = tid; jj < n; jj += nt) {
+        if (in.toff) {
+            const long long l = in.toff[jj + 1] - in.toff[jj];
+            if (l < 0 || l > in.maxlen) bad |= 2;
+        }
+        const uint64_t x = in.id[jj];
+        if (jj > 0 ? x <= in.id[jj - 1] : (has_any && x <= max_id)) bad |= 1;
+    }
+    if (!in.adv) {
+        if (tid == 0 && (in.goff[0] != 0 || in.goff[ng] != n)) bad |= 4;
+        for (long long gi = tid; gi < ng; gi += nt) {
+            const long long b = in.goff[gi], e = in.goff[gi + 1];
+            if (e - b < 2 || b < 0 || e > n) bad |= 4;
+        }
+    }
+    const int bb = (sticky ? 8 : 0) | (__syncthreads_or(bad & 1) ? 1 : 0) |
+                   (__syncthreads_or(bad & 2) ? 2 : 0) | (__syncthreads_or(bad & 4) ? 4 : 0);
+    RB_GCLOCK(21, s == 0);
+    if (bb) {  // frozen or rejected: nothing applied
+        for (int k = tid; k < ns; k += nt) {
+            const int j = j0 + k * T;
+            in.surv[j] = 0;
+            in.tslot[j] = -1;
+            in.evid[j] = NONE_ID;
+            Unit d{};
+            d.row = -1;
+            d.g = j;
+            in.units[j] = d;
+        }
+        if (tid == 0 && done_add_u32(&gc->done) == (unsigned)T - 1) {
+            *in.n_units = 0;
+            if (!sticky) {
+                ctl->err_code = RB_EINVAL;
+                ctl->err_index = (bb & 2) ? -3 : (bb & 4) ? -2 : -4;
+            }
+            gc->done = 0;
+        }
+        return;
+    }
+    // Second round trip: the shard's rings (pre-batch heads, rebased to 0)
+    // and the group rewards of the own records (advantages frozen at
+    // insertion, bandit.cpp:276-294, the reference's fp64 order).
+    const PbState st = s_st;
+    uint32_t* gring[3] = {(uint32_t*)pb_ring(v, 0, s), (uint32_t*)pb_ring(v, 1, s),
+                          (uint32_t*)pb_ring(v, 2, s)};
+    for (int r = 0; r < 3; ++r)
+        for (int i = tid; i < st.n[r]; i += nt) {
+            int p = st.h[r] + i;
+            if (p >= RC) p -= RC;
+            ring[r * RC + i] = gring[r][p];
+        }
+    for (int k = tid; k < ns; k += nt) {
+        const int j = j0 + k * T;
+        const long long l = in.toff ? in.toff[j + 1] - in.toff[j] : 0;
+        in.len[j] = (int32_t)l;
+        double adv, gmean;
+        if (in.adv) {
+            adv = in.adv[j];
+            gmean = in.gmean ? in.gmean[j] : 0.0;
+        } else {
+            long long lo = 0, hi = ng;
+            while (hi - lo > 1) {
+                const long long mid = (lo + hi) >> 1;
+                const long long gm = goff_smem ? s_goff[mid] : in.goff[mid];
+                if (gm <= j) lo = mid;
+                else hi = mid;
+            }
+            const long long b = goff_smem ? s_goff[lo] : in.goff[lo];
+            const long long e = goff_smem ? s_goff[lo + 1] : in.goff[lo + 1];
+            group_adv_one(in.reward, b, e, in.reward[j], &adv, &gmean);
+        }
+        in.adv_out[j] = adv;
+        in.gmean_out[j] = gmean;
+        cx[k] = in_correct(in, j) ? 1 : 0;
+    }
+    __syncthreads();
+    RB_GCLOCK(22, s == 0);
+    const int size0 = (int)(P0 < C ? P0 : C);
+    const bool par = size0 == C && fs > 0 && st.n[0] == fs && ns > 0;
+    const uint32_t* Fp = ring;
+    const uint32_t* Wp = ring + RC;
+    const uint32_t* Qp = ring + 2 * RC;
+    const int w0 = st.n[1], q0 = st.n[2];
+    // element e: < C a pre-batch record (its local slot), else push e - C
+    PbState nst;
+    if (par) {
+        // 1. e_k = (F ++ batch)[k]; |W| by the max-plus scan; pops from W
+        const int per = (ns + nt - 1) / nt;
+        const int k0 = tid * per, k1 = min(ns, k0 + per);
+        auto ent = [&](int k, bool* wrong) {
+            if (k < fs) {
+                const uint32_t x = Fp[k];
+                *wrong = (x >> 31) == 0;
+                return (int)(x & 0x7fffffffu);
+            }
+            *wrong = cx[k - fs] == 0;
+            return C + (k - fs);
+        };
+        MaxPlus loc{0, INT_MIN / 2};
+        int nwr = 0, npw = 0;
+        for (int k = k0; k < k1; ++k) {
+            bool wr;
+            ent(k, &wr);
+            loc = mp_then(loc, MaxPlus{wr ? 0 : -1, 0});
+            nwr += wr;
+        }
+        const MaxPlus pre = block_scan_mp(loc);
+        int w = max(w0 + pre.a, pre.b);
+        for (int k = k0; k < k1; ++k) {
+            bool wr;
+            ent(k, &wr);
+            const bool pw = w + (wr ? 1 : 0) >= 1;
+            evw[k] = pw;
+            npw += pw;
+            w = max(w + (wr ? 0 : -1), 0);
+        }
+        long long tot_wr, tot_pw;
+        int ew = (int)block_exclusive_scan(nwr, &tot_wr);  // wrong entries before k0
+        int cw = (int)block_exclusive_scan(npw, &tot_pw);  // W pops before k0
+        // 2. entries in order
+        {
+            int e_w = ew;
+            for (int k = k0; k < k1; ++k) {
+                bool wr;
+                const int e = ent(k, &wr);
+                if (wr) WE[e_w++] = e;
+                else QE[k - e_w] = e;  // correct entries before k = k - wrong entries before k
+            }
+        }
+        __syncthreads();
+        // 3. victims
+        {
+            int c_w = cw;
+            for (int k = k0; k < k1; ++k) {
+                int e;
+                if (evw[k]) {
+                    const int m = c_w++;
+                    e = m < w0 ? (int)(Wp[m] & 0x7fffffffu) : WE[m - w0];
+                } else {
+                    const int m = k - c_w;  // Q pops before k
+                    e = m < q0 ? (int)(Qp[m] & 0x7fffffffu) : QE[m - q0];
+                }
+                vk[k] = e;
+                slotk[k] = e;
+            }
+        }
+        __syncthreads();
+        // 4. slots: push k takes its victim's slot (pointer jumping)
+        RB_GCLOCK(23, s == 0);
+        for (;;) {
+            int ch = 0;
+            for (int k = tid; k < ns; k += nt) {
+                const int e = ((volatile int*)slotk)[k];
+                if (e >= C) {
+                    ((volatile int*)slotk)[k] = ((volatile int*)slotk)[e - C];
+                    ch = 1;
+                }
+            }
+            if (!__syncthreads_or(ch)) break;
+        }
+        // 5. survivors: the pushes no later push evicted
+        RB_GCLOCK(24, s == 0);
+        // mark batch victims
+        for (int k = tid; k < ns; k += nt)
+            if (vk[k] >= C) cx[vk[k] - C] |= 2;  // bit 1: evicted within the batch
+        __syncthreads();
+        for (int k = tid; k < ns; k += nt)
+            if (!(cx[k] & 2)) occb[slotk[k]] = k;
+        // 6. new queues (head 0): F = (F ++ batch)[ns, ns + fs), W / Q = unpopped entries
+        const int nw_new = w0 + (int)tot_wr - (int)tot_pw;
+        const int nq_new = q0 + (ns - (int)tot_wr) - (ns - (int)tot_pw);
+        nst.h[0] = nst.h[1] = nst.h[2] = 0;
+        nst.n[0] = fs;
+        nst.n[1] = nw_new;
+        nst.n[2] = nq_new;
+        // Every new entry is computed (reads of the old rings), then stored:
+        // F_new[i] = (F ++ batch)[ns + i], W_new[i] = (W ++ WE)[pops_W + i],
+        // Q_new[i] = (Q ++ QE)[pops_Q + i]; entry = slot | correct << 31
+        auto entry_of = [&](int e, bool pre_bit) -> uint32_t {
+            const int sl = e < C ? e : slotk[e - C];
+            const bool c = e < C ? pre_bit : (cx[e - C] & 1) != 0;
+            return (uint32_t)sl | (c ? 0x80000000u : 0u);
+        };
+        const int tot = fs + nw_new + nq_new;  // == C
+        uint32_t val[4];  // C <= PBP_CMAX = 4 * blockDim.x at most (see the launch)
+        int cnt = 0;
+        for (int i = tid; i < tot; i += nt, ++cnt) {
+            uint32_t x;
+            if (i < fs) {
+                const int t = ns + i;
+                x = t < fs ? Fp[t] : entry_of(C + (t - fs), false);
+            } else if (i < fs + nw_new) {
+                const int m = (int)tot_pw + (i - fs);
+                x = m < w0 ? Wp[m] : entry_of(WE[m - w0], false);
+            } else {
+                const int m = (ns - (int)tot_pw) + (i - fs - nw_new);
+                x = m < q0 ? Qp[m] : entry_of(QE[m - q0], true);
+            }
+            val[cnt] = x;
+        }
+        __syncthreads();
+        cnt = 0;
+        for (int i = tid; i < tot; i += nt, ++cnt) {
+            const uint32_t x = val[cnt];
+            if (i < fs) ring[i] = x;
+            else if (i < fs + nw_new) ring[RC + (i - fs)] = x;
+            else ring[2 * RC + (i - fs - nw_new)] = x;
+        }
+    } else if (tid == 0) {
+        // filling (or fresh_slots == 0): the sequential queue simulation
+        GQ F{ring, RC, 0, st.n[0]}, W{ring + RC, RC, 0, st.n[1]}, Q{ring + 2 * RC, RC, 0, st.n[2]};
+        int size = size0;
+        for (int k = 0; k < ns; ++k) {
+            int vs;
+            const int gx = pb_push_logic(C, fs, F, W, Q, size, (cx[k] & 1) != 0, &vs);
+            int e = -1;  // victim element
+            if (vs == -2) e = -2;
+            else if (vs >= 0) e = occb[vs] >= 0 ? C + occb[vs] : vs;
+            if (e >= C) cx[e - C] |= 2;
+            vk[k] = e;
+            slotk[k] = gx;
+            if (gx >= 0) occb[gx] = k;
+        }
+        nst.h[0] = F.h;
+        nst.n[0] = F.n;
+        nst.h[1] = W.h;
+        nst.n[1] = W.n;
+        nst.h[2] = Q.h;
+        nst.n[2] = Q.n;
+        s_st = nst;
+    }
+    __syncthreads();
+    if (!par) nst = s_st;
+    RB_GCLOCK(25, s == 0);
+    // per push: evicted id (pre-batch occupants from the shared copy, so no
+    // write below races with it), slot, survivor, metadata, payload descriptor
+    int maxq = 0;
+    for (int k = tid; k < ns; k += nt) {
+        const int j = j0 + k * T;
+        const int e = vk[k];
+        uint64_t ev = NONE_ID;
+        if (e == -2) ev = in.id[j];
+        else if (e >= C) ev = in.id[j0 + (e - C) * T];
+        else if (e >= 0) ev = preid[e];
+        const int sl = slotk[k];
+        const bool surv = sl >= 0 && !(cx[k] & 2);
+        in.evid[j] = ev;
+        in.tslot[j] = sl >= 0 ? (int32_t)((size_t)s * C + sl) : -1;
+        in.surv[j] = surv;
+        Unit d;
+        d.row = -1;
+        d.len = in.len[j];
+        d.k0 = 0;
+        d.g = j;
+        d.off = in.toff ? in.toff[j] : 0;
+        d.adv = 0.0;
+        if (surv) {
+            const size_t g = (size_t)s * C + sl;
+            write_meta(v, g, in, j);
+            v.seq[g] = P0 + k;
+            if (s >= v.sb && s < v.se && d.len > 0 && v.stride > 0) {
+                d.row = (s - v.sb) * C + sl;
+                const int q = (d.len + 3) >> 2;
+                maxq = q > maxq ? q : maxq;
+            }
+        }
+        in.units[j] = d;
+    }
+    maxq = __reduce_max_sync(0xffffffffu, maxq);
+    if ((tid & 31) == 0 && maxq) atomicMax(&s_maxq, maxq);
+    RB_GCLOCK(26, s == 0);
+    // rings back to global memory (rebased), state, push count
+    for (int r = 0; r < 3; ++r)
+        for (int i = tid; i < nst.n[r]; i += nt) {
+            int p = nst.h[r] + i;
+            if (p >= RC) p -= RC;
+            gring[r][i] = ring[r * RC + p];
+        }
+    // arrival order: merge(W, Q) by sequence number, then F
+    auto seqof = [&](uint32_t x) -> long long {
+        const int sl = (int)(x & 0x7fffffffu);
+        const int k = occb[sl];
+        return k >= 0 ? P0 + k : preseq[sl];
+    };
+    auto at = [&](int r, int i) -> uint32_t {
+        int p = nst.h[r] + i;
+        if (p >= RC) p -= RC;
+        return ring[r * RC + p];
+    };
+    int32_t* ord = v.order + (size_t)s * C;
+    const int nw = nst.n[1], nq = nst.n[2], nf = nst.n[0];
+    for (int k = tid; k < nw + nq; k += nt) {
+        const bool inw = k < nw;
+        const int a = inw ? k : k - nw;
+        const uint32_t x = at(inw ? 1 : 2, a);
+        const long long sq = seqof(x);
+        const int orr = inw ? 2 : 1, on = inw ? nq : nw;
+        int lo = 0, hi = on;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (seqof(at(orr, mid)) < sq) lo = mid + 1;
+            else hi = mid;
+        }
+        ord[a + lo] = (int32_t)(x & 0x7fffffffu);
+    }
+    for (int k = tid; k < nf; k += nt) ord[nw + nq + k] = (int32_t)(at(0, k) & 0x7fffffffu);
+    __syncthreads();
+    RB_GCLOCK(27, s == 0);
+    if (tid == 0) {
+        PbState o;
+        for (int r = 0; r < 3; ++r) {
+            o.h[r] = 0;
+            o.n[r] = nst.n[r];
+        }
+        v.pbs[s] = o;
+        v.pushes[s] = P0 + ns;
+        if (s_maxq) atomicMax(&gc->cta_max[0], s_maxq);
+        if (done_add_u32(&gc->done) == (unsigned)T - 1) {
+            *in.n_units = atomicExch(&gc->cta_max[0], 0);
+            ctl->cursor = (cur0 + (unsigned long long)n) % T;
+            if (n > 0) {
+                ctl->max_id = in.id[n - 1];
+                ctl->has_any = 1;
+            }
+            ctl->hash_stale = 1;
+            gc->done = 0;
+            RB_GCLOCK(28, true);
+        }
+    }
+}
+
 // Record copies with the post-increment use count in draw order
 // (replay_buffer.cpp:201-202) and optional UseEvents (205-215).
 __global__ void k_sample_records(BufView v, long long nsel, long long per,
@@ -2881,6 +3328,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         // throughput on C4 (both are bandwidth-bound)
         b->early_gather_ok = b->pdl && std::getenv("RB_EARLY_GATHER") != nullptr;
         b->tma_payload = std::getenv("RB_PAYLOAD_LSU") == nullptr;
+        b->pb_par = std::getenv("RB_NO_PB_PAR") == nullptr;
         b->loss_dyn = std::getenv("RB_LOSS_CHUNK_MAJOR") == nullptr;
         b->tma_long = std::getenv("RB_PAYLOAD_TMA_LONG") != nullptr;
         b->chunk_major = std::getenv("RB_NO_CHUNK_MAJOR") == nullptr;
@@ -2954,6 +3402,26 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         b->keep_total += (unsigned long long)in.keep_ctas;  // extra CTAs copy them
         k_route_fifo<<<grid + (unsigned)in.keep_ctas, RT_THREADS, 0, b->stream>>>(
             b->v, in, b->route_ctl, b->pay_sync);
+    } else if (unique && b->retention == RB_POSITIVE_BIAS && !want_evrec && b->pb_par &&
+               b->C <= (size_t)PBP_CMAX && bt.n <= (size_t)PBP_NMAX &&
+               (bt.n + b->T - 1) / b->T <= (size_t)PBP_NSMAX) {
+        // ids promised new: validation, advantages and the queue update in one
+        // launch, one CTA per shard (k_posbias_par)
+        const int nsp = (int)((bt.n + b->T - 1) / b->T + 3) & ~3;
+        const size_t smem = b->C * 16 + 3 * (b->C + 1) * 4 + b->C * 4 + (size_t)nsp * 18;
+        static bool attr_set = false;  // per process: the kernel's opt-in limit
+        if (!attr_set) {
+            RB_CUDA(cudaFuncSetAttribute(k_posbias_par, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         208 * 1024));
+            attr_set = true;
+        }
+        // CTA size from the work: every phase ends in a CTA barrier, whose cost
+        // grows with the warp count (C2: 162 pushes -> 192 threads); at least
+        // C/4 threads (the ring rewrite keeps 4 entries per thread in registers)
+        const int need = std::max({nsp, (int)(b->C + 3) / 4, 128});
+        const int nthr = std::min(PBP_THREADS, (need + 31) & ~31);
+        k_posbias_par<<<(unsigned)b->T, nthr, smem, b->stream>>>(
+            b->v, in, (unsigned long long)b->h_cursor, b->route_ctl, nsp);
     } else {
         k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
         if (b->retention == RB_POSITIVE_BIAS) {

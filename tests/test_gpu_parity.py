@@ -395,6 +395,16 @@ STEP_CASES = {
                         seed=24),
     "posbias_delta_one": dict(capacity=48, shards=3, batch=24, group=8, lmax=10, ragged=True,
                               seed=25, retention="positive_bias", delta=1.0, assume_unique=True),
+    # positive bias with ids promised new: one-launch parallel queue update (k_posbias_par)
+    "posbias_unique_c2": dict(capacity=84, shards=1, batch=64, group=8, lmax=40, ragged=True,
+                              retention="positive_bias", delta=0.5, loss="asymre", seed=51,
+                              assume_unique=True),
+    "posbias_unique_in_batch": dict(capacity=32, shards=2, batch=16, group=8, lmax=12,
+                                    ragged=True, seed=52, workers=16, trainers=1, mu=1.0,
+                                    retention="positive_bias", delta=0.75, assume_unique=True),
+    "posbias_unique_overlap": dict(capacity=600, shards=3, batch=96, group=8, lmax=33,
+                                   ragged=True, seed=53, retention="positive_bias", delta=0.5,
+                                   assume_unique=True, overlap=True),
     "posbias_delta_zero": dict(capacity=48, shards=3, batch=24, group=8, lmax=10, ragged=True,
                                seed=26, retention="positive_bias", delta=0.0),
     # insert -> sample -> gather with no host sync: the gather is a dependent

@@ -63,6 +63,7 @@ names = {40: "map t0 start", 41: "map0 enter", 42: "map0 after local twist", 46:
          59: "finalize end", 60: "route0 loads+validation", 61: "route0 verdict",
          62: "route0 records written", 63: "route0 done-count", 56: "route last CTA start",
          57: "route done flag"}
-for i, nm in names.items():
+names.update({i: f"clock {i}" for i in range(64) if i not in names})
+for i, nm in sorted(names.items()):
     if ck[i] > 0:
         print(f"  {nm:22s} {(ck[i] - t0) / 1e3:9.2f} us")
