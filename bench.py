@@ -278,6 +278,13 @@ def run_ours(args, rank, world, dist):
     red3 = torch.zeros(3, dtype=torch.float64, device=dev)   # multi-GPU reduce vector (24 B)
     if world > 1:
         buf.loss_set_reduce_vector(red3)
+    # N > 1 over NCCL: the library issues the step's one collective itself
+    # (rb_allreduce_loss_stats on the buffer's stream, torch's communicator)
+    comm = None
+    if dist is not None and dist.get_backend() == "nccl":
+        dist.all_reduce(red3)  # the communicator exists once a collective ran
+        torch.cuda.synchronize()
+        comm = dist.group.WORLD._get_backend(dev)._comm_ptr()
     # The trainer stand-in ends with a 256 MB read: the 126 MB L2 holds none of
     # logp_now when the loss starts (a real trainer's forward would have moved
     # far more data through L2 in between).
@@ -308,11 +315,14 @@ def run_ours(args, rank, world, dist):
         buf.loss_grpo(lpn, dlogp, EPS_LOW, EPS_HIGH, stats=stats) if cfg["loss"] == "grpo" else \
             buf.loss_asymre(lpn, dlogp, DELTA_V, stats=stats)
         if world > 1:  # one collective: the registered {objective_sum, included, excluded}
-            if dist is not None:
-                dist.all_reduce(red3)
-            else:  # emulated rank 0: the sum over N ranks alike (the collective's result)
-                red3.mul_(world)
-            buf.loss_finalize_vec(dlogp, red3, stats)
+            if comm:
+                buf.allreduce_loss_stats(comm, dlogp, stats)
+            else:
+                if dist is not None:  # gloo (CPU tests)
+                    dist.all_reduce(red3)
+                else:  # emulated rank 0: the sum over N ranks alike (the collective's result)
+                    red3.mul_(world)
+                buf.loss_finalize_vec(dlogp, red3, stats)
         if ev:
             ev[3].record(stream)
 
@@ -568,10 +578,12 @@ def parity_check(cfg, wl, nsteps, buf, rank, world, packed_tok, lpn, dlogp, stat
 def launches_per_step(cfg, world):
     """Library kernels of one timed step (the stand-in's kernels are not counted):
     FIFO (ids promised unique): k_route_fifo, k_insert_payload_tma, k_sample_fused,
-    k_gather, loss; positive bias: k_insert_route, k_posbias_batch, k_insert_payload,
-    k_sample_fused, k_gather, loss; + k_finalize_vec (rb_loss_finalize_vec) per
-    step on more than one rank; + k_ring_lookahead above 8192 draws per call."""
-    n = 5 if cfg["retention"] == "plain_fifo" else 6
+    k_gather, loss; positive bias (ids promised unique): k_posbias_par,
+    k_insert_payload, k_sample_fused, k_gather, loss; + k_finalize_vec
+    (rb_loss_finalize_vec / rb_allreduce_loss_stats, whose NCCL kernel is not
+    ours) per step on more than one rank; + k_ring_lookahead above 8192 draws
+    per call."""
+    n = 5
     return n + (1 if world > 1 else 0) + (1 if cfg["batch"] > 8192 else 0)
 
 

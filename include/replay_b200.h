@@ -264,6 +264,15 @@ int rb_loss_finalize(rb_buffer* b, float* dlogp, rb_loss_stats* stats);
  * device or NULL).  vec3 = NULL unregisters. */
 int rb_loss_set_reduce_vector(rb_buffer* b, double* vec3);
 int rb_loss_finalize_vec(rb_buffer* b, float* dlogp, const double* vec3, rb_loss_stats* stats);
+/* The collective itself (SURVEY.md §8b `rb_allreduce_loss_stats(comm, ...)`):
+ * ncclAllReduce (sum, in place, on the buffer's stream) of the registered
+ * vector across the communicator's ranks, then rb_loss_finalize_vec.
+ * nccl_comm is an ncclComm_t of the NCCL library loaded in the process
+ * (e.g. torch's ProcessGroupNCCL `_comm_ptr()`); libnccl.so.2 is resolved at
+ * run time, never linked.  RB_ELOGIC without a registered vector.  The
+ * reference runs its shards in one process and needs no collective
+ * (async_sim.cpp:138-139, bandit.cpp:363-408 over the whole batch). */
+int rb_allreduce_loss_stats(rb_buffer* b, void* nccl_comm, float* dlogp, rb_loss_stats* stats);
 
 /* Inspection (replay_buffer.hpp:74-84). */
 int rb_num_shards(const rb_buffer* b, size_t* out);

@@ -109,6 +109,7 @@ def _load():
         "rb_loss_finalize": (ip, [vp, vp, vp]),
         "rb_loss_set_reduce_vector": (ip, [vp, vp]),
         "rb_loss_finalize_vec": (ip, [vp, vp, vp, vp]),
+        "rb_allreduce_loss_stats": (ip, [vp, vp, vp, vp]),
         "rb_num_shards": (ip, [vp, vp]),
         "rb_total_capacity": (ip, [vp, vp]),
         "rb_shard_capacity": (ip, [vp, vp]),

@@ -182,6 +182,7 @@ struct rb_buffer {
     long long* sel_total = nullptr;  // [0] local tokens, [1] global tokens
     rb::DevLossAcc* acc = nullptr;
     int last_loss = -1;              // 0 grpo, 1 asymre
+    double* red3 = nullptr;          // registered reduce vector (rb_loss_set_reduce_vector)
     bool acc_norm_explicit = false;  // the accumulator holds an explicit GRPO normaliser
 
     // misc scratch

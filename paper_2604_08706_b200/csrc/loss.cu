@@ -20,6 +20,9 @@
 // terms accumulate in fp64 (per-thread unit sums included).  dlogp is
 // written with the optimistic scale -1/total_tokens; if any token was
 // excluded, the last CTA flags a rescale to -1/included.
+#include <dlfcn.h>
+#include <nccl.h>  // types and enums; the symbols are resolved at run time
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -1268,6 +1271,54 @@ int rb_loss_set_reduce_vector(rb_buffer* b, double* vec3) {
         b->other_work();
         k_set_red3<<<1, 1, 0, b->stream>>>(b->acc, vec3);
         RB_CUDA(cudaGetLastError());
+        b->red3 = vec3;
+    });
+}
+
+namespace {
+// ncclAllReduce of the NCCL library already in the process (e.g. torch's
+// bundled one, found by soname without loading a second copy), else of the
+// system's libnccl.so.2.  Resolved at run time: a communicator is only valid
+// with the library instance that created it, so the product never links one.
+using NcclAllReduceFn = ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                         ncclComm_t, cudaStream_t);
+using NcclErrFn = const char* (*)(ncclResult_t);
+struct NcclSyms {
+    NcclAllReduceFn allreduce = nullptr;
+    NcclErrFn errstr = nullptr;
+};
+const NcclSyms& nccl_syms() {
+    static NcclSyms s;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        s.allreduce = (NcclAllReduceFn)dlsym(h, "ncclAllReduce");
+        s.errstr = (NcclErrFn)dlsym(h, "ncclGetErrorString");
+    });
+    return s;
+}
+}  // namespace
+
+int rb_allreduce_loss_stats(rb_buffer* b, void* nccl_comm, float* dlogp, rb_loss_stats* stats) {
+    return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
+        if (!nccl_comm) invalid("rb_allreduce_loss_stats: NULL communicator");
+        if (!b->red3)
+            throw Error(RB_ELOGIC, "rb_allreduce_loss_stats: register a reduce vector first "
+                                   "(rb_loss_set_reduce_vector)");
+        const NcclSyms& nc = nccl_syms();
+        if (!nc.allreduce) throw Error(RB_ECUDA, "rb_allreduce_loss_stats: libnccl.so.2 not found");
+        b->other_work();
+        // the 24-B {objective_sum, included, excluded} the loss fold wrote, in place
+        const ncclResult_t r = nc.allreduce(b->red3, b->red3, 3, ncclFloat64, ncclSum,
+                                            (ncclComm_t)nccl_comm, b->stream);
+        if (r != ncclSuccess)
+            throw Error(RB_ECUDA, std::string("ncclAllReduce: ") +
+                                      (nc.errstr ? nc.errstr(r) : std::to_string((int)r)));
+        const int st = rb_loss_finalize_vec(b, dlogp, b->red3, stats);
+        if (st != RB_OK) throw Error(st, rb_last_error());
     });
 }
 

@@ -384,6 +384,16 @@ class ShardedReplayBuffer:
         check(lib.rb_loss_finalize_vec(self._h, _ptr(dlogp), _ptr(vec3), p))
         return stats
 
+    def allreduce_loss_stats(self, nccl_comm: int, dlogp, stats=None):
+        """The one collective of a multi-GPU step inside the library: NCCL
+        all-reduce (sum) of the registered vector on the buffer's stream, then
+        the global normalisation.  `nccl_comm`: an ncclComm_t address of the
+        NCCL loaded in this process, e.g. torch's
+        ``dist.group.WORLD._get_backend(torch.device("cuda"))._comm_ptr()``."""
+        p = C.byref(stats) if isinstance(stats, LossStats) else _ptr(stats)
+        check(lib.rb_allreduce_loss_stats(self._h, C.c_void_p(int(nccl_comm)), _ptr(dlogp), p))
+        return stats
+
     def batch_ids_device(self, out_ids, out_lengths=None, out_offsets=None) -> None:
         """Per-selection ids / lengths / packed offsets into device arrays (no sync)."""
         check(lib.rb_batch_ids(self._h, _ptr(out_ids), _ptr(out_lengths), _ptr(out_offsets)))

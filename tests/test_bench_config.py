@@ -57,7 +57,7 @@ def test_launch_accounting(bench):
     assert bench.launches_per_step(bench.scaled_cfg(c4, 2), 2) == 6      # + finalize
     assert bench.launches_per_step(bench.scaled_cfg(c4, 4), 4) == 6      # strong: B stays 4096
     assert bench.launches_per_step(bench.scaled_cfg(c4, 4, weak=True), 4) == 7  # + ring lookahead
-    assert bench.launches_per_step(bench.CONFIGS["c2"], 1) == 6          # positive bias route
+    assert bench.launches_per_step(bench.CONFIGS["c2"], 1) == 5          # positive bias: one route launch
 
 
 def test_documented_switches_exist():
