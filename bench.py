@@ -643,7 +643,7 @@ def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None, rank=0):
 
     def e2e_step(hb2, n):
         if n:
-            buf.insert(**hb2)
+            buf.insert(**hb2, assume_unique=True)  # ids new and increasing, as on the device path
         buf.sample_device(B, rng)
         buf.gather(tok_h, None, off_h)
         st = buf.loss_grpo(lpn_h, dl_h, EPS_LOW, EPS_HIGH) if cfg["loss"] == "grpo" else \

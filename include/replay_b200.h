@@ -130,8 +130,10 @@ int rb_set_stream(rb_buffer* b, void* stream);
 /* Asynchronous host outputs (off by default): a loss whose out_dlogp is
  * pinned host memory returns once its stats are final while the dlogp
  * download drains on a copy stream beside the caller's next call (e.g. the
- * next insert's upload, the other PCIe direction).  out_dlogp is complete
- * after rb_synchronize (or cudaDeviceSynchronize). */
+ * next insert's upload, the other PCIe direction); a gather into pinned host
+ * arrays returns once its offsets are on the host while the packed tokens /
+ * logp_old drain the same way (beside the loss's logp_now upload).  The host
+ * arrays are complete after rb_synchronize (or cudaDeviceSynchronize). */
 int rb_set_async_outputs(rb_buffer* b, int on);
 void* rb_get_stream(rb_buffer* b);
 

@@ -2987,6 +2987,10 @@ rb_buffer::~rb_buffer() {
     if (stream) cudaStreamSynchronize(stream);
     if (out_pending) cudaEventSynchronize(out_done);
     if (out_done) cudaEventDestroy(out_done);
+    if (hmap_h) cudaFreeHost(hmap_h);
+    if (gout_pending) cudaEventSynchronize(gather_done);
+    if (gather_done) cudaEventDestroy(gather_done);
+    if (gather_ready) cudaEventDestroy(gather_ready);
     if (look_ev) {
         if (cudaEventSynchronize(look_ev) != cudaSuccess) cudaDeviceSynchronize();  // captured
         cudaEventDestroy(look_ev);
@@ -3112,10 +3116,47 @@ void rb_buffer::ensure_select(size_t n) {
     sel_off = dalloc<int64_t>(sel_cap + 1);
 }
 void rb_buffer::sync() { RB_CUDA(cudaStreamSynchronize(stream)); }
+namespace rb {
+// dst (mapped host or device) <- src (device), 8-byte words (bytes % 8 == 0)
+// or bytes; one CTA.
+__global__ void k_copy_small(void* dst, const void* src, size_t bytes) {
+    if (((uintptr_t)dst | (uintptr_t)src | bytes) % 8 == 0) {
+        uint64_t* d = (uint64_t*)dst;
+        const uint64_t* s = (const uint64_t*)src;
+        for (size_t i = threadIdx.x; i < bytes / 8; i += blockDim.x) d[i] = s[i];
+    } else {
+        for (size_t i = threadIdx.x; i < bytes; i += blockDim.x)
+            ((char*)dst)[i] = ((const char*)src)[i];
+    }
+}
+}  // namespace rb
+void rb_buffer::fetch(void* host_dst, const void* dev_src, size_t bytes) {
+    if (bytes > hmap_cap) {
+        sync();
+        if (hmap_h) cudaFreeHost(hmap_h);
+        hmap_cap = std::max<size_t>(bytes, std::max<size_t>(4096, hmap_cap * 2));
+        RB_CUDA(cudaHostAlloc(&hmap_h, hmap_cap, cudaHostAllocMapped));
+        RB_CUDA(cudaHostGetDevicePointer(&hmap_d, hmap_h, 0));
+    }
+    k_copy_small<<<1, 256, 0, stream>>>(hmap_d, dev_src, bytes);
+    RB_CUDA(cudaGetLastError());
+    sync();
+    std::memcpy(host_dst, hmap_h, bytes);
+}
+void rb_buffer::to_host_async(void* host_dst, const void* dev_src, size_t bytes) {
+    void* d = nullptr;
+    RB_CUDA(cudaHostGetDevicePointer(&d, host_dst, 0));  // pinned: mapped under UVA
+    k_copy_small<<<1, 256, 0, stream>>>(d, dev_src, bytes);
+    RB_CUDA(cudaGetLastError());
+}
 void rb_buffer::wait_outputs_on(cudaStream_t s) {
     if (out_pending) RB_CUDA(cudaStreamWaitEvent(s, out_done, 0));
 }
 void rb_buffer::drain_outputs() {
+    if (gout_pending) {
+        RB_CUDA(cudaEventSynchronize(gather_done));
+        gout_pending = false;
+    }
     if (!out_pending) return;
     RB_CUDA(cudaEventSynchronize(out_done));
     out_pending = false;
@@ -3145,8 +3186,7 @@ struct Stager {
 
 void check_sticky(rb_buffer* b) {
     DevCtl c;
-    RB_CUDA(cudaMemcpyAsync(&c, b->v.ctl, sizeof c, cudaMemcpyDeviceToHost, b->stream));
-    RB_CUDA(cudaStreamSynchronize(b->stream));
+    b->fetch(&c, b->v.ctl, sizeof c);
     b->async_unchecked = false;
     if (c.err_code) {
         DevCtl z = c;
@@ -4012,8 +4052,7 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
         long long total = 0;
         if (ht || hl) {
             long long t[2];
-            RB_CUDA(cudaMemcpyAsync(t, b->sel_total, sizeof t, cudaMemcpyDeviceToHost, b->stream));
-            b->sync();
+            b->fetch(t, b->sel_total, sizeof t);
             total = t[0];
         }
         int32_t* dt = out_tokens;
@@ -4023,6 +4062,8 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
         if (ht || hl) stage = (char*)b->dev_stage(2 * pb + 16, rb_buffer::ST_GATHER);
         if (ht) dt = (int32_t*)stage;
         if (hl) dl = (float*)(stage + pb);
+        // the previous gather's asynchronous download still reads the staging area
+        if (b->gout_pending && stage) RB_CUDA(cudaStreamWaitEvent(b->stream, b->gather_done, 0));
         const bool early = b->gather_early;
         b->gather_early = false;  // one early gather per sampling call (it consumes the claims)
         if (nloc > 0 && (dt || dl) && early) {
@@ -4057,12 +4098,35 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
                     b->v, b->units_sel, b->n_units_sel, (int)nloc, dt, dl);
             RB_CUDA(cudaGetLastError());
         }
-            if (ht) RB_CUDA(cudaMemcpyAsync(out_tokens, dt, total * 4, cudaMemcpyDeviceToHost, b->stream));
-        if (hl) RB_CUDA(cudaMemcpyAsync(out_logp_old, dl, total * 4, cudaMemcpyDeviceToHost, b->stream));
-        if (out_offsets)
+        // Pinned host outputs with rb_set_async_outputs: the download drains on
+        // the copy stream (complete after rb_synchronize) while the caller's
+        // next call runs, e.g. the loss's logp_now upload (full-duplex PCIe).
+        const bool async_g = b->async_out && (ht || hl) && (!ht || is_pinned_ptr(out_tokens)) &&
+                             (!hl || is_pinned_ptr(out_logp_old));
+        cudaStream_t cs = b->stream;
+        if (async_g) {
+            b->ensure_copy_streams();
+            if (!b->gather_ready) {
+                RB_CUDA(cudaEventCreateWithFlags(&b->gather_ready, cudaEventDisableTiming));
+                RB_CUDA(cudaEventCreateWithFlags(&b->gather_done, cudaEventDisableTiming));
+            }
+            RB_CUDA(cudaEventRecord(b->gather_ready, b->stream));
+            RB_CUDA(cudaStreamWaitEvent(b->cs_out, b->gather_ready, 0));
+            cs = b->cs_out;
+        }
+        if (ht) RB_CUDA(cudaMemcpyAsync(out_tokens, dt, total * 4, cudaMemcpyDeviceToHost, cs));
+        if (hl) RB_CUDA(cudaMemcpyAsync(out_logp_old, dl, total * 4, cudaMemcpyDeviceToHost, cs));
+        if (async_g) {
+            RB_CUDA(cudaEventRecord(b->gather_done, b->cs_out));
+            b->gout_pending = true;
+        }
+        const bool host_off = out_offsets && !is_device_ptr(out_offsets);
+        if (host_off && is_pinned_ptr(out_offsets))  // kernel store into the mapped array
+            b->to_host_async(out_offsets, b->sel_off, (nloc + 1) * 8);
+        else if (out_offsets)
             RB_CUDA(cudaMemcpyAsync(out_offsets, b->sel_off, (nloc + 1) * 8, cudaMemcpyDefault,
                                     b->stream));
-        if (ht || hl || (out_offsets && !is_device_ptr(out_offsets))) b->sync_checked();
+        if (((ht || hl) && !async_g) || host_off) b->sync_checked();
     });
 }
 

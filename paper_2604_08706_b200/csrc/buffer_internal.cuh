@@ -170,8 +170,13 @@ struct rb_buffer {
     bool async_out = false;
     bool out_pending = false;
     cudaEvent_t out_done = nullptr;
-    void wait_outputs_on(cudaStream_t s);  // order s after a pending download
-    void drain_outputs();                  // host wait for it
+    // the same for a gather into pinned host arrays: its download (from the
+    // ST_GATHER staging area) drains on cs_out beside the loss's logp_now
+    // upload on cs_in; gather_done marks it
+    bool gout_pending = false;
+    cudaEvent_t gather_ready = nullptr, gather_done = nullptr;
+    void wait_outputs_on(cudaStream_t s);  // order s after a pending loss download
+    void drain_outputs();                  // host wait for every pending download
 
     // current batch (selection)
     size_t sel_cap = 0, B = 0;
@@ -192,6 +197,16 @@ struct rb_buffer {
     ~rb_buffer();
     void* scratch(size_t bytes);          // device misc scratch
     void* host_stage(size_t bytes);       // pinned host scratch (waits for its last reader)
+    // Small device->host results (totals, offsets, stats, the loss
+    // accumulator, the control block) are written by a one-CTA kernel
+    // straight into mapped pinned memory: a cudaMemcpy of a few bytes would
+    // queue behind a pending multi-MB download on the D2H copy engine
+    // (rb_set_async_outputs) and stall the call for a millisecond.
+    void* hmap_h = nullptr;
+    void* hmap_d = nullptr;
+    size_t hmap_cap = 0;
+    void fetch(void* host_dst, const void* dev_src, size_t bytes);  // stream-ordered, synchronous
+    void to_host_async(void* host_dst, const void* dev_src, size_t bytes);  // pinned dst, no sync
     void host_stage_issued();             // record that the stream reads stage_host
     void host_stage_issued_on(cudaStream_t s);  // ... that stream `s` reads it
     void ensure_copy_streams();

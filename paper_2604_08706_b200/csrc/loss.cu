@@ -1010,9 +1010,7 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
     } else {
         // packed offsets of the owned selections (and the total) on the host
         std::vector<long long> off(nloc + 1);
-        RB_CUDA(cudaMemcpyAsync(off.data(), b->sel_off, (nloc + 1) * 8, cudaMemcpyDeviceToHost,
-                                b->stream));
-        b->sync();
+        b->fetch(off.data(), b->sel_off, (nloc + 1) * 8);
         const long long total = off[nloc];
         const size_t bytes = (((size_t)total + 3) & ~size_t(3)) * 4 + 16;
         b->wait_outputs_on(b->stream);  // the last async download still reads the staging output
@@ -1070,7 +1068,7 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
         }
         RB_CUDA(cudaStreamSynchronize(b->stream));
         DevLossAcc acc;
-        RB_CUDA(cudaMemcpy(&acc, b->acc, sizeof acc, cudaMemcpyDeviceToHost));
+        b->fetch(&acc, b->acc, sizeof acc);
         const bool fix = c.kind == 0 && acc.need_fixup && single;
         if (fix) b->drain_outputs();  // the rescaled array is downloaded again below
         if (fix) {  // -1/total -> -1/included (rare: a non-finite ratio)
@@ -1084,8 +1082,8 @@ void run_loss(rb_buffer* b, const LossCall& c, const float* lpn, float* dl,
         }
     }
     if (stats && !dev_stats) {
-        RB_CUDA(cudaMemcpyAsync(stats, kst, sizeof *stats, cudaMemcpyDeviceToHost, b->stream));
-        b->sync_checked();
+        b->fetch(stats, kst, sizeof *stats);
+        if (b->async_unchecked) b->sync_checked();
     }
 }
 

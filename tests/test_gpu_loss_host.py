@@ -108,3 +108,36 @@ def test_async_host_outputs(batch, excluded):
         buf.set_async_outputs(False)
     for o in outs:
         np.testing.assert_array_equal(o[:total].numpy(), want)
+
+
+def test_async_host_gather(batch):
+    """rb_set_async_outputs with a pinned host gather: the packed tokens /
+    logp_old drain on the copy stream (complete after synchronize()) while
+    the next calls run; gather -> loss -> gather with no synchronisation
+    between them reuses the staging area safely."""
+    buf, lpn0, total = batch
+    pad = total + 8
+    tok_d = torch.zeros(pad, dtype=torch.int32, device="cuda:0")
+    lpo_d = torch.zeros(pad, dtype=torch.float32, device="cuda:0")
+    off_d = torch.zeros(buf.batch_size() + 1, dtype=torch.int64, device="cuda:0")
+    buf.gather(tok_d, lpo_d, off_d)
+    buf.synchronize()
+    lpn_h = torch.zeros(pad, dtype=torch.float32).pin_memory()
+    lpn_h[:total] = torch.from_numpy(lpn0)
+    dl_h = torch.zeros(pad, dtype=torch.float32).pin_memory()
+    toks = [torch.full((pad,), -7, dtype=torch.int32).pin_memory() for _ in range(2)]
+    lpos = [torch.full((pad,), -7.0, dtype=torch.float32).pin_memory() for _ in range(2)]
+    offs = [torch.zeros(buf.batch_size() + 1, dtype=torch.int64).pin_memory() for _ in range(2)]
+    buf.set_async_outputs(True)
+    try:
+        for i in range(2):
+            buf.gather(toks[i], lpos[i], offs[i])
+            assert int(offs[i][-1]) == total  # the offsets are synchronous
+            _run(buf, "grpo", lpn_h, dl_h)
+        buf.synchronize()
+    finally:
+        buf.set_async_outputs(False)
+    for i in range(2):
+        assert np.array_equal(toks[i][:total].numpy(), tok_d[:total].cpu().numpy())
+        assert np.array_equal(lpos[i][:total].numpy(), lpo_d[:total].cpu().numpy())
+        assert (toks[i][total:].numpy() == -7).all()

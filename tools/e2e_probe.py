@@ -23,15 +23,18 @@ with torch.cuda.stream(s):
     dl_h = torch.empty(pad, dtype=torch.float32).pin_memory()
     lpn_h = torch.randn(pad, dtype=torch.float32).mul_(0.01).sub_(1.0).pin_memory()
     shift = 10**12
-    for it in range(4):
+    asy = os.environ.get("ASYNC") == "1"  # rb_set_async_outputs, no syncs between calls
+    buf.set_async_outputs(asy)
+    sync = (lambda: None) if asy else torch.cuda.synchronize
+    for it in range(6):
         hb2 = dict(hb)
         hb2["rollout_id"] = (hb["rollout_id"] + shift * (it + 1)).pin_memory()
         t = [time.perf_counter()]
-        buf.insert(**hb2)
-        torch.cuda.synchronize()
+        buf.insert(**hb2, assume_unique=True)
+        sync()
         t.append(time.perf_counter())
         buf.sample_device(B, rng)
-        torch.cuda.synchronize()
+        sync()
         t.append(time.perf_counter())
         buf.gather(tok_h, None, off_h)
         t.append(time.perf_counter())
