@@ -189,6 +189,52 @@ class Workload:
         self.warm = self.batches[0]
         self.steps = self.batches[1:]
 
+    def make_owned(self, rank, T):
+        """Owned-metadata job (rb_insert_owned): every batch reduced to the records
+        the round robin routes to shard `rank` (arrival positions = rank mod T
+        from the cursor, replay_buffer.cpp:89-90), with their group advantages
+        (computed by the producer from the whole group, bandit.cpp:276-294);
+        `n_global` is the global batch size.  Prepared outside the timed region."""
+        import torch
+
+        import paper_2604_08706_b200 as rb
+
+        cursor = 0
+        out = []
+        for b, n, _ in self.batches:
+            dev = b["rollout_id"].device
+            adv = torch.empty(n, dtype=torch.float64, device=dev)
+            rb.group_advantages(b["reward"], b["group_offsets"], out=adv)
+            j0 = (rank - cursor) % T
+            idx = torch.arange(j0, n, T, device=dev)
+            toff = b["tok_offsets"]
+            lens = (toff[1:] - toff[:-1])[idx]
+            ooff = torch.zeros(idx.numel() + 1, dtype=torch.int64, device=dev)
+            ooff[1:] = torch.cumsum(lens, 0)
+            tot = int(ooff[-1])
+            # token gather indices: start of each own row + position within it
+            starts = torch.repeat_interleave(toff[:-1][idx], lens)
+            pos = torch.arange(tot, device=dev) - torch.repeat_interleave(ooff[:-1], lens)
+            src = starts + pos
+            pad = (tot + 3) // 4 * 4 + 4
+            tok = torch.zeros(pad, dtype=torch.int32, device=dev)
+            lpo = torch.zeros(pad, dtype=torch.float32, device=dev)
+            tok[:tot] = b["tokens"][src]
+            lpo[:tot] = b["logp_old"][src]
+            o = {k: b[k][idx].contiguous() for k in ("rollout_id", "reward", "behavior_logprob",
+                                                     "group_id", "prompt_id", "creation_step",
+                                                     "policy_version")}
+            o.update(advantage=adv[idx].contiguous(), tok_offsets=ooff, tokens=tok, logp_old=lpo,
+                     n_global=n)
+            out.append((o, int(idx.numel()), tot))
+            cursor = (cursor + n) % T
+        torch.cuda.synchronize()
+        self.owned = True
+        self.full = self.batches
+        self.batches = out
+        self.warm = out[0]
+        self.steps = out[1:]
+
 
 def scaled_cfg(cfg, world, weak=False):
     """The N-GPU job (BASELINE.json configs[3]).
@@ -253,8 +299,15 @@ def run_ours(args, rank, world, dist):
     rng = rb.Rng(SEED).stream("buffer_sampling")
     K, Wm = args.steps, args.warmup
     wl = Workload(cfg, K + Wm, dev, sh)
+    owned = getattr(args, "owned", False) and T > 1
+    if owned:  # each rank holds and routes only its own shard's records
+        wl.make_owned(rank, T)
+        buf.set_owned_metadata()
     # warm-up fill (bandit.cpp:609-615)
     b, n, _ = wl.warm
+    if owned:
+        buf.insert(**b, assume_unique=True)
+        n = 0  # inserted whole
     for lo in range(0, n, 4096):
         hi = min(n, lo + 4096)
         part = {k: v for k, v in b.items() if k not in ("group_offsets", "tok_offsets", "tokens", "logp_old")}
@@ -376,7 +429,8 @@ def run_ours(args, rank, world, dist):
     check = None
     if getattr(args, "check", True):
         torch.cuda.synchronize()
-        check = parity_check(cfg, wl, Wm + K, buf, rank, world, packed_tok, lpn, dlogp, stats)
+        check = parity_check(cfg, wl, Wm + K, buf, rank, world, packed_tok, lpn, dlogp, stats,
+                             owned=owned)
         if dist is not None:
             ok = torch.tensor([1 if check["parity"] == "ok" else 0], dtype=torch.int32, device=dev)
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
@@ -477,7 +531,7 @@ def run_ours(args, rank, world, dist):
     return res, buf, wl, rng
 
 
-def parity_check(cfg, wl, nsteps, buf, rank, world, packed_tok, lpn, dlogp, stats):
+def parity_check(cfg, wl, nsteps, buf, rank, world, packed_tok, lpn, dlogp, stats, owned=False):
     """Outside the timed region: replay the whole schedule (warm-up fill + every
     warm-up and timed step) through the CPU oracle (oracle/, the checker) and
     compare the LAST step's sampled trajectories, packed offsets and tokens,
@@ -515,10 +569,11 @@ def parity_check(cfg, wl, nsteps, buf, rank, world, packed_tok, lpn, dlogp, stat
             gmean_of[int(r["rollout_id"])] = m[i // G]
             ob.push(r)
 
-    push_batch(wl.warm[0], wl.warm[1])
+    full = wl.full if owned else wl.batches  # the oracle replays the global batches
+    push_batch(full[0][0], full[0][1])
     orec = None
     for i in range(nsteps):
-        b, n, _ = wl.steps[i]
+        b, n, _ = full[1 + i]
         push_batch(b, n)
         orec, _, _ = ob.sample(B, orng)
     per = B // T
@@ -566,7 +621,7 @@ def parity_check(cfg, wl, nsteps, buf, rank, world, packed_tok, lpn, dlogp, stat
         res["objective_rel_err"] = abs(obj - obj_want) / max(1.0, abs(obj_want))
         if res["objective_rel_err"] > 1e-5:
             bad.append("objective")
-    for s in range(T):
+    for s in ([rank] if owned else range(T)):  # an owned-metadata rank holds its shard only
         if not same_records(buf.shard_contents(s), ob.shard_contents(s)):
             bad.append(f"shard {s} contents")
     res["parity"] = "ok" if not bad else "MISMATCH: " + ", ".join(bad)
@@ -607,7 +662,7 @@ def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None, rank=0):
     steps = wl.steps[-K:] if len(wl.steps) >= K else wl.steps
     host = []
     for b, n, tot in steps:
-        hb = {k: v.cpu().pin_memory() for k, v in b.items()}
+        hb = {k: (v.cpu().pin_memory() if hasattr(v, "cpu") else v) for k, v in b.items()}
         host.append((hb, n, tot))
     pad = B * cfg["lmax"] + 8  # upper bound (ragged batches differ per step)
     # the dlogp download of step i drains while step i+1's insert uploads
@@ -661,9 +716,11 @@ def run_e2e(args, buf, wl, rng, cfg, world=1, dist=None, rank=0):
 
     def h2d_insert(hb2, n, c0):
         meta = sum(v.numel() * v.element_size() for k, v in hb2.items()
-                   if k not in ("tokens", "logp_old"))
+                   if hasattr(v, "numel") and k not in ("tokens", "logp_old"))
         toff = hb2["tok_offsets"].numpy()
         lens = np.diff(toff)
+        if "n_global" in hb2:  # an owned batch holds this rank's records only
+            return meta + int(lens.sum()) * 8
         own = ((c0 + np.arange(n)) % T) == rank if T > 1 else np.ones(n, bool)
         return meta + int(lens[own].sum()) * 8
 
@@ -928,6 +985,9 @@ def main():
     ap.add_argument("--phases", action="store_true",
                     help="record CUDA events at the phase boundaries (front end | stand-in | "
                          "loss) inside the graph; the step is the sum of the front end and loss")
+    ap.add_argument("--owned", action="store_true",
+                    help="N > 1: each rank receives and routes only its own shard's records "
+                         "(rb_set_owned_metadata / rb_insert_owned) instead of the whole batch")
     ap.add_argument("--weak", action="store_true",
                     help="N > 1: weak scaling (N x the single-GPU buffer and batch) instead of "
                          "splitting the single-GPU workload over the N GPUs")
@@ -993,7 +1053,10 @@ def main():
     stream = torch.cuda.Stream()  # a real stream handle (not the legacy default)
     with torch.cuda.stream(stream):
         res, buf, wl, rng = run_ours(args, rank, world, dist)
-        if not args.no_e2e:
+        if not args.no_e2e and getattr(wl, "owned", False):
+            res["e2e"] = {"skipped": "--owned: the replayed batches' shard positions change with "
+                                     "the cursor; run without --owned for the e2e figure"}
+        elif not args.no_e2e:
             res["e2e"] = run_e2e(args, buf, wl, rng, cfg, world, dist, rank)
     if emulated:
         res["emulated"] = (f"rank 0 of a {world}-GPU job alone on one GPU, no collective: "

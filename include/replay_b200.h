@@ -180,6 +180,24 @@ typedef struct rb_insert_batch {
 int rb_insert(rb_buffer* b, const rb_insert_batch* batch, uint64_t* out_evicted_ids,
               size_t* out_applied, int flags);
 
+/* Owned metadata (multi-GPU): a buffer holding ONE shard of
+ * 2..64 (shard_begin + 1 == shard_end; FIFO, uniform draws with
+ * replacement) keeps the metadata of its own records only.  After
+ * rb_set_owned_metadata(b, 1), rb_insert_owned(b, batch, n_global, flags)
+ * takes only the records the reference's round robin (replay_buffer.cpp:
+ * 89-90) routes to the owned shard out of a global batch of n_global — in
+ * arrival order, with their advantages (a group spans every rank's shard),
+ * ids promised unique — and advances every shard's push count; the sampler
+ * still draws the whole MT19937-64 stream (an earlier shard's below()
+ * rejection shifts this shard's draws; occupancies are closed-form) but maps
+ * only the owned slice [s*B/T, (s+1)*B/T): use counts, lengths, packed
+ * offsets.  The loss normalises by the rank's own tokens until the
+ * all-reduced {objective_sum, included, excluded} arrives
+ * (rb_allreduce_loss_stats / rb_loss_finalize_vec rescale dlogp to the
+ * global count).  Inspection of other shards returns stale metadata. */
+int rb_set_owned_metadata(rb_buffer* b, int on);
+int rb_insert_owned(rb_buffer* b, const rb_insert_batch* batch, size_t n_global, int flags);
+
 /* sample (replay_buffer.cpp:184-217): batch_size/num_shards draws per shard
  * in shard order 0..T-1 from rng (replay_buffer.cpp:135-182), use counts
  * incremented.  The selection is kept inside the buffer as the "current

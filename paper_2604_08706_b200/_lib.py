@@ -84,6 +84,8 @@ def _load():
         "rb_get_stream": (vp, [vp]),
         "rb_push": (ip, [vp, vp, vp, vp, i32, vp, vp]),
         "rb_insert": (ip, [vp, vp, vp, vp, ip]),
+        "rb_insert_owned": (ip, [vp, vp, sz, ip]),
+        "rb_set_owned_metadata": (ip, [vp, ip]),
         "rb_sample": (ip, [vp, sz, vp, vp, vp, vp, vp, i64, i64]),
         "rb_batch_size": (ip, [vp, vp]),
         "rb_batch_total_tokens": (ip, [vp, vp]),

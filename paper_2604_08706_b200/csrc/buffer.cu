@@ -108,6 +108,11 @@ struct InsertIn {
     rb_record* evrec;     // may be NULL
     Unit* units;          // payload copy work units (owned survivors)
     int* n_units;
+    // owned-metadata buffers (rb_insert_owned): the batch holds only the
+    // records of the global batch of n_global routed to the one owned shard
+    // v.sb, in arrival order (global arrival j0 + k*T for record k)
+    int own_only;
+    long long n_global;
 };
 
 __device__ __forceinline__ bool in_correct(const InsertIn& in, long long j) {
@@ -791,14 +796,21 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
 // validation flag (1 = valid, 2 = rejected; reset by the last CTA).
 struct FifoPlan {
     int c0, T, C, ups;  // cursor % T, shards, capacity per shard, units per record
+    int own;            // owned-metadata batch: the owned shard (its records only), else -1
     int pm[64];         // pushes_s % C before the batch
 };
 __device__ __forceinline__ Unit fifo_unit(const BufView& v, const FifoPlan& p,
                                           const int64_t* toff, int n, int j) {
     int s = p.c0 + j % p.T;
     if (s >= p.T) s -= p.T;
-    const int rank = j / p.T, j0 = j % p.T;
-    const int ns = (n - 1 - j0) / p.T + 1;
+    int rank = j / p.T;
+    const int j0 = j % p.T;
+    int ns = (n - 1 - j0) / p.T + 1;
+    if (p.own >= 0) {  // record j is the owned shard's j-th push of the batch
+        s = p.own;
+        rank = j;
+        ns = n;
+    }
     Unit d;
     d.off = toff[j];
     const long long l = toff[j + 1] - d.off;
@@ -1116,6 +1128,7 @@ struct SampleArgs {
     long long occ[64];        // per-shard occupancy after the preceding inserts (draws)
     const long long* occ_dev;  // the same for more than 64 shards (device), else NULL
     const int* verdict;       // the pending insert's whole-batch verdict (1 valid, 2 rejected)
+    int own_only;             // owned-metadata buffer: map (use counts, lengths, totals) only [lo, hi)
 };
 
 // A rejected insert leaves a sticky error and freezes the buffer until
@@ -1377,17 +1390,24 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
         const int nf = s < MAP_NSH ? s_newfrom[s] : INT_MAX;
         nw[r] = ix[r] >= nf;  // a record of the pending insert: length from its offsets
         const bool has_off = nw[r] && pi.toff != nullptr;  // no offsets: length 0
-        const int j = has_off ? s_j0[s] + (s_ns[s] - (s_occ_after[s] - ix[r])) * v.T : 0;
+        const int jr = s_ns[s] - (s_occ_after[s] - ix[r]);  // its push index within shard s
+        const int j = has_off ? (pi.own ? jr : s_j0[s] + jr * v.T) : 0;
         const int64_t* to = has_off ? pi.toff : reinterpret_cast<const int64_t*>(v.pushes);
         lv[r] = v.len[g[r]];
         av[r] = v.adv[g[r]];  // old records' advantages (new ones: after the route)
         t0[r] = to[j];
         t1[r] = to[j + (has_off ? 1 : 0)];
     }
+    // live: mapped selections (an owned-metadata buffer maps its own slice only;
+    // the other draws still count for the rejection check above)
+    bool live[MAP_R];
+#pragma unroll
+    for (int r = 0; r < MAP_R; ++r)
+        live[r] = ok[r] && (!a.own_only || (k0 + r >= a.lo && k0 + r < a.hi));
 #pragma unroll
     for (int r = 0; r < MAP_R; ++r) {
         const long long l = t1[r] - t0[r];
-        L[r] = !ok[r] ? 0 : nw[r] ? (int)(l < 0 ? 0 : l) : lv[r];
+        L[r] = !live[r] ? 0 : nw[r] ? (int)(l < 0 ? 0 : l) : lv[r];
     }
     unsigned long long own = 0, all = 0;
 #pragma unroll
@@ -1458,6 +1478,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
             a.sel_shard[k] = sh[r];
             a.sel_index[k] = ix[r];
         }
+        if (!live[r]) continue;
         a.sel_slot[k] = g[r];
         a.sel_len[k] = L[r];
         if (k < a.lo || k >= a.hi) continue;
@@ -1481,7 +1502,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
     bool any_new = false;
 #pragma unroll
     for (int r = 0; r < MAP_R; ++r) {
-        if (!ok[r]) continue;
+        if (!live[r]) continue;
         if (nw[r]) any_new = true;
         else atomicAdd(&v.use[g[r]], 1u);
     }
@@ -1496,7 +1517,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
         for (int r = 0; r < MAP_R; ++r) adv[r] = v.adv[g[r]];
 #pragma unroll
         for (int r = 0; r < MAP_R; ++r) {
-            if (!ok[r] || !nw[r]) continue;
+            if (!live[r] || !nw[r]) continue;
             atomicAdd(&v.use[g[r]], 1u);
             const long long k = k0 + r;
             if (k >= a.lo && k < a.hi) reinterpret_cast<double*>(&a.units[k - a.lo])[3] = adv[r];
@@ -1613,7 +1634,9 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
             s_head[s] = head_after(v, a.pend, s);
         __syncthreads();
         unsigned long long tail = 0;
-        for (long long k = k0 + threadIdx.x; k < D; k += blockDim.x) {
+        const long long kb = a.own_only ? (k0 > a.lo ? k0 : a.lo) : k0;
+        const long long ke = a.own_only ? (D < a.hi ? D : a.hi) : D;
+        for (long long k = kb + threadIdx.x; k < ke; k += blockDim.x) {
             const int s = a.sel_shard[k];
             const int g = s * v.C + arrival_slot_h(v, s, a.sel_index[k], cached_head(v, s_head, s));
             atomicAdd(&v.use[g], 1u);
@@ -2101,8 +2124,17 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
         if (!bb) {
             int s = c0 + j % T;
             if (s >= T) s -= T;
-            const int rank = j / T, j0 = j % T;
-            const int ns = (n - 1 - j0) / T + 1;
+            int rank = j / T, j0 = j % T;
+            int ns = (n - 1 - j0) / T + 1;
+            // owned-metadata batch: record j is the owned shard's j-th push
+            // (its records only; an evictee of this batch is record j - C)
+            const int jst = in.own_only ? 1 : T;
+            if (in.own_only) {
+                s = v.sb;
+                rank = j;
+                j0 = 0;
+                ns = n;
+            }
             const long long P = s < RT_NSH ? s_P[s] : v.pushes[s];
             int x2 = (int)(P % C) + rank % C;
             if (x2 >= C) x2 -= C;
@@ -2114,11 +2146,11 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
             // is overwritten by its survivor (another CTA): that survivor
             // reports the resident id for the slot's first push instead
             // (read before its own write, same thread).
-            if (P + rank >= C) ev = rank >= C ? in.id[j - C * T] : v.id[g];
+            if (P + rank >= C) ev = rank >= C ? in.id[j - C * jst] : v.id[g];
             if (rank < C && !surv) ev_by_survivor = true;
             if (surv && rank >= C) {
                 const int r0 = rank % C;
-                in.evid[r0 * T + j0] = P + r0 >= C ? v.id[g] : NONE_ID;
+                in.evid[r0 * jst + j0] = P + r0 >= C ? v.id[g] : NONE_ID;
             }
             if (!in.adv) {
                 long long lo = 0, hi = ng;  // group gi: goff[gi] <= j < goff[gi+1]
@@ -2181,10 +2213,11 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     for (int c = tid; c < (int)nrt; c += RT_THREADS) m = max(m, __ldcg(&gc->cta_max[c]));
     m = __reduce_max_sync(0xffffffffu, m);
     if ((tid & 31) == 0) s_m[tid >> 5] = m;
+    const int nG = in.own_only ? (int)in.n_global : n;  // the global batch
     if (!bb)
         for (int s = tid; s < T; s += RT_THREADS) {
             const int j0 = ((s - c0) % T + T) % T;
-            const int ns = n > j0 ? (n - 1 - j0) / T + 1 : 0;
+            const int ns = nG > j0 ? (nG - 1 - j0) / T + 1 : 0;
             v.pushes[s] += ns;
         }
     __syncthreads();
@@ -2193,7 +2226,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
         for (int w = 0; w < RT_THREADS / 32; ++w) mm = s_m[w] > mm ? s_m[w] : mm;
         *in.n_units = bb ? 0 : mm;
         if (!bb) {
-            ctl->cursor = (cur0 + (unsigned long long)n) % T;
+            ctl->cursor = (cur0 + (unsigned long long)nG) % T;
             ctl->max_id = in.id[n - 1];  // strictly increasing and above the old max
             ctl->has_any = 1;
             ctl->hash_stale = 1;
@@ -3428,6 +3461,10 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
     bool closed = false;
     const bool fifo_route = unique && b->retention == RB_PLAIN_FIFO && !want_evrec &&
                             bt.n <= (size_t)RT_THREADS * GRID_MAX_CTAS;
+    in.own_only = b->own_n_global ? 1 : 0;
+    in.n_global = b->own_n_global ? (long long)b->own_n_global : in.n;
+    if (in.own_only && !fifo_route)
+        throw Error(RB_ELOGIC, "rb_insert_owned: FIFO retention and ids promised unique required");
     if (fifo_route) {
         // ids promised new and increasing: the closed-form FIFO route
         const unsigned grid = (unsigned)((bt.n + RT_THREADS - 1) / RT_THREADS);
@@ -3478,6 +3515,7 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         p.c0 = (int)(b->h_cursor % b->T);
         p.T = (int)b->T;
         p.C = (int)b->C;
+        p.own = b->own_n_global ? (int)b->sb : -1;
         const int maxq = (b->max_tokens + 3) / 4;
         p.ups = std::max(1, (maxq + UNIT_THREADS * PAYLOAD_U - 1) / (UNIT_THREADS * PAYLOAD_U));
         for (size_t s = 0; s < b->T; ++s) p.pm[s] = (int)(b->h_pushes[s] % (long long)b->C);
@@ -3507,7 +3545,8 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         b->pdl_tail = true;  // a sampler launched next may overlap this copy
         b->pend.pending = 1;
         b->pend.c0 = p.c0;
-        b->pend.n = (int)bt.n;
+        b->pend.n = b->own_n_global ? (int)b->own_n_global : (int)bt.n;
+        b->pend.own = b->own_n_global ? 1 : 0;
         b->pend.toff = b->s_toff;  // the route kernel's copy
         b->pend.keep_cnt = &b->route_ctl->keep_cnt;
         b->pend.keep_target = b->keep_total;
@@ -3523,7 +3562,8 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         b->pdl_tail = true;
         b->pend.pending = 1;
         b->pend.c0 = (int)(b->h_cursor % b->T);
-        b->pend.n = (int)bt.n;
+        b->pend.n = b->own_n_global ? (int)b->own_n_global : (int)bt.n;
+        b->pend.own = b->own_n_global ? 1 : 0;
         b->pend.toff = bt.tok_offsets ? b->s_toff : nullptr;  // lengths only (or NULL: length 0)
         b->pend.keep_cnt = &b->route_ctl->keep_cnt;
         b->pend.keep_target = b->keep_total;
@@ -3603,7 +3643,7 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
             invalid("rb_insert: need advantage or group_offsets");
         // Split very large batches so the exact path's hash set stays sparse.
         const size_t chunk_max = (size_t)(b->v.hcap / 4);
-        if (bt.n > chunk_max) {
+        if (bt.n > chunk_max && !b->own_n_global) {  // (an owned batch takes the closed form)
             if (!bt.advantage) invalid("rb_insert: batch too large for device advantages");
             size_t done = 0;
             while (done < bt.n) {
@@ -3705,7 +3745,7 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
             // on the host and equal lengths, only those rows cross PCIe, as
             // one strided 2-D copy per array (a batch of per-record copies
             // measured slower than the whole array: ~2.4 µs per range).
-            bool partial = b->se == b->sb + 1 && b->T > 1 && toff_host && n > 0;
+            bool partial = b->se == b->sb + 1 && b->T > 1 && toff_host && n > 0 && !b->own_n_global;
             const int64_t L0 = partial ? toff_user[1] - toff_user[0] : 0;
             for (size_t j = 1; partial && j < n; ++j)
                 if (toff_user[j + 1] - toff_user[j] != L0) partial = false;
@@ -3760,10 +3800,11 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
             b->pdl_tail = false;  // the copy, not the payload kernel, is the stream's tail
         }
         // host mirrors: assume fully applied, corrected below when synchronous
-        for (size_t j = 0; j < n; ++j) b->h_pushes[(b->h_cursor + j) % b->T]++;
+        const size_t nG = b->own_n_global ? b->own_n_global : n;  // the global batch
+        for (size_t j = 0; j < nG; ++j) b->h_pushes[(b->h_cursor + j) % b->T]++;
         const size_t cursor_before = b->h_cursor;
         std::vector<long long> pushes_before;
-        b->h_cursor = (b->h_cursor + n) % b->T;
+        b->h_cursor = (b->h_cursor + nG) % b->T;
         if (!(flags & RB_INSERT_ASSUME_UNIQUE)) {
             DevCtl c;
             RB_CUDA(cudaMemcpyAsync(&c, b->v.ctl, sizeof c, cudaMemcpyDeviceToHost, b->stream));
@@ -3781,6 +3822,57 @@ int rb_insert(rb_buffer* b, const rb_insert_batch* bt_in, uint64_t* out_evicted_
         } else if (out_applied) {
             *out_applied = n;
         }
+    });
+}
+
+int rb_set_owned_metadata(rb_buffer* b, int on) {
+    return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
+        if (on && !(b->T > 1 && b->se == b->sb + 1 && b->T <= 64))
+            throw Error(RB_ELOGIC, "rb_set_owned_metadata: one owned shard of 2..64 required");
+        if (on && (b->retention != RB_PLAIN_FIFO || b->strategy != RB_UNIFORM_WITH_REPLACEMENT))
+            throw Error(RB_ELOGIC,
+                        "rb_set_owned_metadata: FIFO retention and uniform draws with replacement required");
+        b->owned_meta = on != 0;
+    });
+}
+
+int rb_insert_owned(rb_buffer* b, const rb_insert_batch* batch, size_t n_global, int flags) {
+    return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)
+        if (!b->owned_meta) throw Error(RB_ELOGIC, "rb_insert_owned: rb_set_owned_metadata first");
+        if (!(flags & RB_INSERT_ASSUME_UNIQUE))
+            throw Error(RB_ELOGIC, "rb_insert_owned: ids must be promised unique (RB_INSERT_ASSUME_UNIQUE)");
+        if (!batch->advantage && batch->n > 0)
+            invalid("rb_insert_owned: advantages required (groups span the shards of other ranks)");
+        // the owned shard's arrival positions among the global batch (round robin
+        // from the cursor, replay_buffer.cpp:89-90)
+        const size_t T = b->T, j0 = (b->sb + T - b->h_cursor % T) % T;
+        const size_t mine = n_global > j0 ? (n_global - 1 - j0) / T + 1 : 0;
+        if (batch->n != mine)
+            invalid("rb_insert_owned: the batch must hold exactly the owned shard's " +
+                    std::to_string(mine) + " records of the global batch of " +
+                    std::to_string(n_global));
+        if (n_global == 0) return;
+        if (batch->n == 0) {  // only the other shards' counters and the cursor advance
+            b->sync_checked();
+            for (size_t j = 0; j < n_global; ++j) b->h_pushes[(b->h_cursor + j) % T]++;
+            b->h_cursor = (b->h_cursor + n_global) % T;
+            DevCtl c;
+            b->fetch(&c, b->v.ctl, sizeof c);
+            c.cursor = b->h_cursor;
+            RB_CUDA(cudaMemcpy(b->v.pushes, b->h_pushes.data(), T * sizeof(long long),
+                               cudaMemcpyHostToDevice));
+            RB_CUDA(cudaMemcpy(b->v.ctl, &c, sizeof c, cudaMemcpyHostToDevice));
+            return;
+        }
+        b->own_n_global = n_global;
+        struct Reset {
+            rb_buffer* b;
+            ~Reset() { b->own_n_global = 0; }
+        } reset{b};
+        const int st = rb_insert(b, batch, nullptr, nullptr, flags);
+        if (st != RB_OK) throw Error(st, rb_last_error());
     });
 }
 
@@ -3880,6 +3972,9 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         a.units = b->units_sel;
         a.n_units = b->n_units_sel;
         a.verdict = b->pay_sync;
+        a.own_only = b->owned_meta ? 1 : 0;
+        if (b->owned_meta && b->strategy != RB_UNIFORM_WITH_REPLACEMENT)
+            throw Error(RB_ELOGIC, "owned-metadata buffers sample uniformly with replacement");
         const unsigned nmap = (unsigned)std::max<size_t>(1, (nsel + MAP_SPC - 1) / MAP_SPC);
         if (nmap > (unsigned)GRID_MAX_CTAS) invalid("rb_sample: batch too large");
         bool fused = false;

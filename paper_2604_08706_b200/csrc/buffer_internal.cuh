@@ -70,7 +70,8 @@ int loss_grid(int sms);
 struct GridCtl;  // buffer.cu: multi-CTA bookkeeping
 struct PendingIns {
     int pending;          // 1: the last insert (closed-form FIFO, <= 64 shards) may be running
-    int c0, n;            // its cursor % T and record count
+    int c0, n;            // its cursor % T and (global) record count
+    int own;              // owned-metadata insert: its offsets index the owned shard's records only
     const int64_t* toff;  // its payload offsets (the route kernel's copy)
     const unsigned long long* keep_cnt;  // the copy is complete once *keep_cnt >= keep_target
     unsigned long long keep_target;
@@ -100,6 +101,11 @@ struct rb_buffer {
     std::vector<long long> h_pushes;
     size_t h_cursor = 0;
     bool async_unchecked = false;  // an RB_INSERT_ASSUME_UNIQUE insert ran since the last sticky check
+    // owned metadata (rb_set_owned_metadata): one owned shard keeps the
+    // metadata of its own records only; inserts carry only those records
+    // (rb_insert_owned, own_n_global = the global batch size during the call)
+    bool owned_meta = false;
+    size_t own_n_global = 0;
 
     // scratch (device), grown on demand
     size_t ins_cap = 0;

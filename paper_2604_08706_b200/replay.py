@@ -179,6 +179,8 @@ class ShardedReplayBuffer:
             _handle = h
         self._h = _handle
         self.max_tokens = int(max_tokens)
+        # shards whose slice of the draws this buffer maps (None: every shard)
+        self._owned_shards = (shard_range[1] - shard_range[0]) if shard_range else None
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -246,8 +248,11 @@ class ShardedReplayBuffer:
     def insert(self, *, rollout_id, reward, prompt_id=None, group_id=None, creation_step=None,
                policy_version=None, is_correct=None, behavior_logprob=None, advantage=None,
                group_mean=None, group_offsets=None, tok_offsets=None, tokens=None,
-               logp_old=None, evicted=None, assume_unique: bool = False) -> int:
-        """Batched push of n trajectories (rb_insert).  Returns the number applied."""
+               logp_old=None, evicted=None, assume_unique: bool = False,
+               n_global: Optional[int] = None) -> int:
+        """Batched push of n trajectories (rb_insert).  Returns the number applied.
+        n_global (owned-metadata buffers, rb_insert_owned): the batch holds only
+        this buffer's shard's records out of a global batch of n_global."""
         keep = []
 
         def a(x, dt):
@@ -280,8 +285,15 @@ class ShardedReplayBuffer:
         applied = C.c_size_t(0)
         ev = _arr(evicted, np.uint64)
         flags = RB_INSERT_ASSUME_UNIQUE if assume_unique else 0
+        if n_global is not None:
+            check(lib.rb_insert_owned(self._h, C.byref(bt), int(n_global), flags))
+            return n
         check(lib.rb_insert(self._h, C.byref(bt), _ptr(ev), C.byref(applied), flags))
         return applied.value
+
+    def set_owned_metadata(self, on: bool = True) -> None:
+        """Keep the metadata of the one owned shard only (rb_set_owned_metadata)."""
+        check(lib.rb_set_owned_metadata(self._h, 1 if on else 0))
 
     # -- sample / gather / loss
     def sample(self, batch_size: int, rng: Rng, ledger: bool = False, batch_id: int = 0,
@@ -313,7 +325,10 @@ class ShardedReplayBuffer:
         return v.value
 
     def batch_ids(self):
-        n = self.batch_size() // max(1, self.num_shards()) * self.num_shards()
+        """(ids, lengths, packed offsets) of the current batch's selections held here
+        (a shard-range buffer: its own shards' slice of the draws)."""
+        T = self.num_shards()
+        n = self.batch_size() // max(1, T) * (self._owned_shards or T)
         ids = np.zeros(max(n, 1), np.uint64)
         lens = np.zeros(max(n, 1), np.int32)
         off = np.zeros(n + 1, np.int64)
