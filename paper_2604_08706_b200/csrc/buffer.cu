@@ -3178,7 +3178,11 @@ void rb_buffer::fetch(void* host_dst, const void* dev_src, size_t bytes) {
 }
 void rb_buffer::to_host_async(void* host_dst, const void* dev_src, size_t bytes) {
     void* d = nullptr;
-    RB_CUDA(cudaHostGetDevicePointer(&d, host_dst, 0));  // pinned: mapped under UVA
+    if (cudaHostGetDevicePointer(&d, host_dst, 0) != cudaSuccess) {  // pinned but not mapped
+        cudaGetLastError();
+        RB_CUDA(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, stream));
+        return;
+    }
     k_copy_small<<<1, 256, 0, stream>>>(d, dev_src, bytes);
     RB_CUDA(cudaGetLastError());
 }
