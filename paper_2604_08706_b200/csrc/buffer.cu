@@ -918,7 +918,10 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_insert_payload_fifo(BufView v,
     payload_body<U, true>(v, nullptr, p, toff, p.ups, n, tokens, logp_old, sync);
     RB_TEND(1);
 }
-constexpr int PAYLOAD_U = 4;
+#ifndef RB_PAYLOAD_U
+#define RB_PAYLOAD_U 4
+#endif
+constexpr int PAYLOAD_U = RB_PAYLOAD_U;
 
 
 // ---- payload insert over the bulk-copy engine (TMA) ------------------------
@@ -2772,7 +2775,10 @@ __global__ void __launch_bounds__(UNIT_THREADS, 9) k_gather(BufView v, const Uni
     }
     RB_TEND(4);
 }
-constexpr int GATHER_U = 4;
+#ifndef RB_GATHER_U
+#define RB_GATHER_U 4
+#endif
+constexpr int GATHER_U = RB_GATHER_U;
 
 // ---- early gather: a programmatic dependent of the fused sampler, which is
 // itself a dependent of the insert's payload copy.  It starts while the copy

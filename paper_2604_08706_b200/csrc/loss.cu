@@ -469,7 +469,10 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
     loss_commit(part, parts, acc, stats, 0, 0.0, dlogp, n_local, local_fix, part_base, nparts);
     RB_GCLOCK(2, blockIdx.x == 0);
 }
-constexpr int LOSS_U = 4;
+#ifndef RB_LOSS_U
+#define RB_LOSS_U 4
+#endif
+constexpr int LOSS_U = RB_LOSS_U;
 
 template <int U>
 __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
