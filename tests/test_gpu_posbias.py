@@ -99,3 +99,38 @@ def test_posbias_unique_rejects_non_increasing_ids(rb):
         buf.check()
     for s in range(2):  # nothing applied
         assert np.array_equal(buf.shard_contents(s)["rollout_id"], before[s])
+
+
+def test_posbias_unique_with_given_advantages(rb, oracle):
+    """Advantages / group means supplied by the caller (no group offsets): the
+    one-launch path stores them as given (frozen at insertion)."""
+    from oracle.pyoracle import RECORD_DTYPE
+
+    g = np.random.default_rng(5)
+    buf = rb.ShardedReplayBuffer(2, 64, "uniform_with_replacement", "positive_bias", 0.5)
+    obuf = oracle.buffer(2, 64, "uniform_with_replacement", "positive_bias", 0.5)
+    nid = 1
+    for bsz in (64, 50, 130):
+        ids = np.arange(nid, nid + bsz, dtype=np.uint64)
+        nid += bsz
+        corr = g.random(bsz) < 0.4
+        adv = g.normal(size=bsz)
+        gm = g.random(bsz)
+        ev = np.zeros(bsz, np.uint64)
+        buf.insert(rollout_id=ids, reward=corr.astype(np.float64), advantage=adv, group_mean=gm,
+                   evicted=ev, assume_unique=True)
+        buf.synchronize()
+        buf.check()
+        recs = np.zeros(bsz, RECORD_DTYPE)
+        recs["rollout_id"] = ids
+        recs["reward"] = corr
+        recs["is_correct"] = corr
+        recs["advantage"] = adv
+        for i in range(bsz):
+            e = obuf.push(recs[i])
+            want = np.iinfo(np.uint64).max if e is None else int(e["rollout_id"])
+            assert int(ev[i]) == want
+    for s in range(2):
+        got, want = buf.shard_contents(s), obuf.shard_contents(s)
+        assert np.array_equal(got["rollout_id"], want["rollout_id"])
+        assert np.array_equal(got["advantage"], want["advantage"])
