@@ -866,10 +866,10 @@ __device__ __forceinline__ void payload_body(const BufView& v, const Unit* desc,
         uint4 ot[U], ol[U];
         if (tokens)
             packed_to_row_quads<U>(reinterpret_cast<const uint4*>(tokens) + (un.off >> 2), nsq, a,
-                                   kw, ot);
+                                   kw, ot, a + un.len);
         if (logp_old)
             packed_to_row_quads<U>(reinterpret_cast<const uint4*>(logp_old) + (un.off >> 2), nsq,
-                                   a, kw, ol);
+                                   a, kw, ol, a + un.len);
         if (CLOSED && !ready) {  // CTA-uniform: first store of this CTA
             if (threadIdx.x == 0) {
                 s_flag = spin_while_eq(&sync[0], 0);
@@ -1028,6 +1028,15 @@ __global__ void __launch_bounds__(32) k_insert_payload_tma(BufView v, FifoPlan p
         const int a = (int)(x.src & 3);
         const int words = (cnt + 3) & ~3;
         uint32_t* stg = pb_smem + (size_t)st * PB_RAW;
+        {  // the source's last partial quad: word loads (the bulk copy stops at a quad boundary)
+            const int full = (a + cnt) & ~3, tw = (a + cnt) & 3;
+            const uint32_t* srcb = arr ? reinterpret_cast<const uint32_t*>(logp_old)
+                                       : reinterpret_cast<const uint32_t*>(tokens);
+            if (lane < tw) stg[full + lane] = __ldg(srcb + (x.src - a) + full + lane);
+            if (tw && a == 0)  // generic-proxy writes read by the bulk store below
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+        }
         if (a != 0) {  // shift the aligned-down source quads down by `a`, in place
             for (int e0 = 0; e0 < words; e0 += 128) {
                 uint32_t r[4];
@@ -1088,11 +1097,11 @@ __global__ void __launch_bounds__(32) k_insert_payload_tma(BufView v, FifoPlan p
                 meta[st] = x;
                 const int cnt = x.n & 0xfffff, arr = x.n >> 30;
                 const int a = (int)(x.src & 3);
-                const uint32_t bytes = (uint32_t)((a + cnt + 3) & ~3) * 4;
+                const uint32_t bytes = (uint32_t)((a + cnt) & ~3) * 4;  // whole quads only
                 const uint32_t* srcb = arr ? reinterpret_cast<const uint32_t*>(logp_old)
                                            : reinterpret_cast<const uint32_t*>(tokens);
                 mbar_expect_tx(&bar[st], bytes);
-                bulk_g2s(pb_smem + (size_t)st * PB_RAW, srcb + (x.src - a), bytes, &bar[st]);
+                if (bytes) bulk_g2s(pb_smem + (size_t)st * PB_RAW, srcb + (x.src - a), bytes, &bar[st]);
             }
             ++issued;
             __syncwarp();
@@ -2510,14 +2519,26 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
         __syncthreads();
         // 4. slots: push k takes its victim's slot (pointer jumping)
         RB_GCLOCK(23, s == 0);
+        // (reads and writes of a round separated by a barrier: at most 4 pushes
+        // per thread, the CTA has >= min(1024, pushes) threads)
         for (;;) {
+            int nv[4];
             int ch = 0;
-            for (int k = tid; k < ns; k += nt) {
-                const int e = ((volatile int*)slotk)[k];
-                if (e >= C) {
-                    ((volatile int*)slotk)[k] = ((volatile int*)slotk)[e - C];
-                    ch = 1;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int k = tid + i * nt;
+                nv[i] = 0;
+                if (k < ns) {
+                    const int e = slotk[k];
+                    nv[i] = e >= C ? slotk[e - C] : e;
+                    ch |= e >= C;
                 }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int k = tid + i * nt;
+                if (k < ns) slotk[k] = nv[i];
             }
             if (!__syncthreads_or(ch)) break;
         }

@@ -387,7 +387,8 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
 #pragma unroll
         for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
-            now[s] = k < nq ? ld_stream(lpn_packed + 4 * (P0 + k)) : make_uint4(0, 0, 0, 0);
+            now[s] = k < nq ? ld_stream_lim(lpn_packed, P0 + k, un.off + un.len)
+                            : make_uint4(0, 0, 0, 0);
         }
         row_to_packed_quads<U>(
             reinterpret_cast<const uint4*>(v.lpo + (size_t)un.row * v.stride), nsq, a, kw, old);
@@ -642,8 +643,8 @@ __global__ void __launch_bounds__(256) k_loss_grpo_packed(const float* lpn, cons
     const long long q0 = o0 >> 2, q1 = (o1 + 3) >> 2;
     GrpoPartial part;
     for (long long q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
-        const uint4 now = ldg4(lpn + 4 * q);
-        const uint4 old = ldg4(lpo + 4 * q);
+        const uint4 now = ld_stream_lim(lpn, q, o1);
+        const uint4 old = ld_stream_lim(lpo, q, o1);
         float* dq = dlogp + 4 * q;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -700,7 +701,8 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
 #pragma unroll
         for (int s = 0; s < U; ++s) {
             const int k = kw + 32 * s + lane;
-            now[s] = k < nq ? ld_stream(lpn_packed + 4 * (P0 + k)) : make_uint4(0, 0, 0, 0);
+            now[s] = k < nq ? ld_stream_lim(lpn_packed, P0 + k, un.off + un.len)
+                            : make_uint4(0, 0, 0, 0);
         }
         double fs = 0.0;  // fp64 sum of logp_now (the reference's objective is fp64)
 #pragma unroll

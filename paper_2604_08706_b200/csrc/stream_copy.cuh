@@ -45,6 +45,16 @@ __device__ __forceinline__ void st_stream(void* p, const uint4& q) {
                  "r"(q.z), "r"(q.w)
                  : "memory");
 }
+// Quad q of a packed 4-byte array whose valid elements end at element `lim`
+// (exclusive): one 128-bit load when the quad lies before `lim`, else the
+// valid words one by one (zeros past `lim`) — a batch's last quad never
+// reads past the caller's array.
+__device__ __forceinline__ uint4 ld_stream_lim(const void* base, long long q, long long lim) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(base) + 4 * q;
+    if (4 * q + 4 <= lim) return ld_stream(w);
+    const long long e = lim - 4 * q;
+    return make_uint4(e > 0 ? __ldg(w) : 0u, e > 1 ? __ldg(w + 1) : 0u, e > 2 ? __ldg(w + 2) : 0u, 0u);
+}
 __device__ __forceinline__ Unit ld_unit(const Unit* u) {
     const uint4 a = *reinterpret_cast<const uint4*>(u);
     const uint4 b = *(reinterpret_cast<const uint4*>(u) + 1);
@@ -116,15 +126,17 @@ __device__ __forceinline__ void row_to_packed_quads(const uint4* rowq, int nsq, 
 
 // Packed (element offset `soff`, any alignment) -> aligned row quads: row
 // quad k = funnel(src quad Q0+k, src quad Q0+k+1, a), a = soff & 3.
+// (lim = a + len: the valid elements counted from quad Q0's first element;
+// the last quad is read word by word, never past the caller's array)
 template <int U>
 __device__ __forceinline__ void packed_to_row_quads(const uint4* srcq0 /* quad Q0 */, int nsq,
-                                                    int a, int kw, uint4 (&o)[U]) {
+                                                    int a, int kw, uint4 (&o)[U], int lim) {
     const int lane = threadIdx.x & 31;
     uint4 cur[U];
 #pragma unroll
     for (int s = 0; s < U; ++s) {
         const int k = kw + 32 * s + lane;
-        cur[s] = (k < nsq) ? ld_stream(srcq0 + k) : make_uint4(0, 0, 0, 0);
+        cur[s] = (k < nsq) ? ld_stream_lim(srcq0, k, lim) : make_uint4(0, 0, 0, 0);
     }
     if (a == 0) {
 #pragma unroll
@@ -133,7 +145,7 @@ __device__ __forceinline__ void packed_to_row_quads(const uint4* srcq0 /* quad Q
     }
     const int klast = kw + 32 * U;  // first quad after the warp's span
     uint4 last_next = make_uint4(0, 0, 0, 0);
-    if (lane == 31 && klast < nsq) last_next = ld_stream(srcq0 + klast);
+    if (lane == 31 && klast < nsq) last_next = ld_stream_lim(srcq0, klast, lim);
 #pragma unroll
     for (int s = 0; s < U; ++s) {
         uint4 next = shfl_down4(cur[s]);
