@@ -849,7 +849,10 @@ __device__ __forceinline__ void payload_body(const BufView& v, const Unit* desc,
     const int nu = n * ups;
     auto load_desc = [&](int u) { return CLOSED ? fifo_unit(v, p, toff, n, u / ups) : ld_unit(desc + u / ups); };
     bool ready = !CLOSED;
-    if (CLOSED) pdl_trigger();  // the sampler may launch (it waits for the route itself)
+    // the sampler may launch: it waits for the route itself (closed form), or
+    // the insert kernels before this copy are complete (table form); it never
+    // reads the rows this copy writes, and waits for the copy before it exits
+    pdl_trigger();
     Unit nxt;  // descriptor of the next unit, loaded one unit ahead
     if ((int)blockIdx.x < nu) nxt = load_desc(blockIdx.x);
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
@@ -3586,7 +3589,10 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         k_insert_payload<PAYLOAD_U><<<b->payload_grid, UNIT_THREADS, 0, b->stream>>>(
             b->v, b->units_ins, b->n_units_ins, (int)bt.n, bt.tokens, bt.logp_old);
         RB_CUDA(cudaGetLastError());
-        b->pdl_tail = false;
+        // the insert's metadata is final once this copy starts: a fused sampler
+        // launched next may run beside the copy (no pending plan)
+        b->pdl_tail = b->pdl;
+        b->pend.pending = 0;
     } else if (fifo_route && b->T <= 64 && b->pdl) {
         // no payload: the route kernel (which triggers its dependents at its
         // start) is the tail; a sampler may overlap it with the insert's plan
