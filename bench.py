@@ -579,7 +579,7 @@ def parity_check(cfg, wl, nsteps, buf, rank, world, packed_tok, lpn, dlogp, stat
     per = B // T
     own = orec[rank * per:(rank + 1) * per]
     ids, lens, off = buf.batch_ids()
-    res = {"checked_step": nsteps - 1, "shards_checked": T}
+    res = {"checked_step": nsteps - 1, "shards_checked": 1 if owned else T}
     bad = []
     if not np.array_equal(ids, own["rollout_id"]):
         bad.append("sampled ids")

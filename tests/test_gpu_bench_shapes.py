@@ -95,3 +95,30 @@ def test_grpo_fast_path_large_log_ratio(oracle, ratio_sign):
     assert float(rel[live].max()) <= 1e-5, float(rel[live].max())
     assert float(np.abs(got[~live] - d_want[~live]).max(initial=0.0)) <= 1e-37
     assert abs(st.objective - obj) <= 1e-5 * max(1.0, abs(obj)), (st.objective, obj)
+
+
+@pytest.mark.parametrize("owned", [False, True])
+def test_bench_two_ranks_strong_scaled(owned):
+    """bench.py's N-GPU path end to end with 2 processes (torchrun, gloo, both on
+    cuda:0 — the test box has one GPU): C4 split over 2 shards, one per rank,
+    the loss statistics all-reduced, and each rank's --check leg against the
+    oracle's replay of the whole job (owned: each rank received only its
+    shard's records)."""
+    import socket
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test requested but CUDA is not available")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"]
+    if owned:
+        cmd.append("--owned")
+    env = dict(os.environ, RB_BENCH_SAME_GPU="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["parity"] == "ok", line["parity_check"]
