@@ -1993,6 +1993,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     const long long ng = in.ngroups;
     DevCtl* ctl = v.ctl;
     RB_TSTART(0);
+    RB_GCLOCK(30, blockIdx.x == 0);
     if (blockIdx.x == 0 && tid == 0) {  // this insert's verdict / completion flags
         st_release_i32(&pay_sync[0], 0);
         st_release_i32(&pay_sync[1], 0);
@@ -2000,6 +2001,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
         fence_gpu();  // performed before any dependent can launch
     }
     __syncthreads();
+    RB_GCLOCK(31, blockIdx.x == 0);
     pdl_trigger();  // the closed-form payload copy may start now (it waits for pay_sync[0])
     // the route proper runs on the first nrt CTAs
     const unsigned nrt = gridDim.x - (in.toff_keep ? (unsigned)in.keep_ctas : 0u);
@@ -2028,6 +2030,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     }
     const int sticky = ctl->err_code;
     const unsigned long long cur0 = ctl->cursor;
+    RB_GCLOCK(32, blockIdx.x == 0);  // (debug builds: after the control-block loads are issued)
     const int has_any = ctl->has_any;
     const unsigned long long max_id = ctl->max_id;
     const int T = v.T, C = v.C;
