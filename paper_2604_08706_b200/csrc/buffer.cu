@@ -113,6 +113,7 @@ struct InsertIn {
     // v.sb, in arrival order (global arrival j0 + k*T for record k)
     int own_only;
     long long n_global;
+    int epoch;            // closed-form route: the flag epoch of this insert (pay_sync tags)
 };
 
 __device__ __forceinline__ bool in_correct(const InsertIn& in, long long j) {
@@ -797,6 +798,7 @@ __global__ void __launch_bounds__(1024) k_insert_route(BufView v, InsertIn in) {
 struct FifoPlan {
     int c0, T, C, ups;  // cursor % T, shards, capacity per shard, units per record
     int own;            // owned-metadata batch: the owned shard (its records only), else -1
+    int epoch;          // the insert's flag epoch (verdict wait, copy-done publish)
     int pm[64];         // pushes_s % C before the batch
 };
 __device__ __forceinline__ Unit fifo_unit(const BufView& v, const FifoPlan& p,
@@ -831,10 +833,10 @@ __device__ __forceinline__ Unit fifo_unit(const BufView& v, const FifoPlan& p,
 // sync[2] = 1 while the copy runs (set by the route kernel before any
 // dependent can launch), cleared by the last CTA to finish (sync[3] counts
 // them).
-__device__ __forceinline__ void payload_pending_end(int* sync) {  // thread 0, CTA's stores done
+__device__ __forceinline__ void payload_pending_end(int* sync, int epoch) {  // thread 0, CTA's stores done
     if (done_add_u32(reinterpret_cast<unsigned*>(&sync[3])) == gridDim.x - 1) {
         sync[3] = 0;
-        st_release_i32(&sync[2], 0);
+        st_release_i32(&sync[2], epoch << 2 | 2);  // the copy of this insert is complete
     }
 }
 
@@ -875,7 +877,7 @@ __device__ __forceinline__ void payload_body(const BufView& v, const Unit* desc,
                                    a, kw, ol, a + un.len);
         if (CLOSED && !ready) {  // CTA-uniform: first store of this CTA
             if (threadIdx.x == 0) {
-                s_flag = spin_while_eq(&sync[0], 0);
+                s_flag = spin_epoch(&sync[0], p.epoch);
             }
             __syncthreads();
             if (s_flag != 1) break;  // batch rejected: nothing is applied
@@ -896,7 +898,7 @@ __device__ __forceinline__ void payload_body(const BufView& v, const Unit* desc,
     }
     if (CLOSED) {
         __syncthreads();
-        if (threadIdx.x == 0) payload_pending_end(sync);
+        if (threadIdx.x == 0) payload_pending_end(sync, p.epoch);
         // completion of this copy implies completion of the route before it
         asm volatile("griddepcontrol.wait;" ::: "memory");
     }
@@ -1060,7 +1062,7 @@ __global__ void __launch_bounds__(32) k_insert_payload_tma(BufView v, FifoPlan p
             __syncwarp();
         }
         if (lane == 0) {
-            if (flag == 0) flag = spin_while_eq(&sync[0], 0);
+            if (flag == 0) flag = spin_epoch(&sync[0], p.epoch);
             if (flag == 1) {
                 const size_t row = (size_t)x.row * v.stride + (size_t)c * PB_CHT;
                 uint32_t* dst = arr ? reinterpret_cast<uint32_t*>(v.lpo) + row
@@ -1115,7 +1117,7 @@ __global__ void __launch_bounds__(32) k_insert_payload_tma(BufView v, FifoPlan p
     if (lane == 0) {
         bulk_wait_all();  // this CTA's row writes are complete
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        payload_pending_end(sync);
+        payload_pending_end(sync, p.epoch);
     }
     RB_TEND(1);
     // completion of this copy implies completion of the route before it
@@ -1152,7 +1154,7 @@ struct SampleArgs {
 // the caller's shared copy.  While the insert may still run, its verdict
 // flag decides (published before any of its records is applied).
 __device__ __forceinline__ int sampler_frozen(const BufView& v, const SampleArgs& a) {
-    if (a.pend.pending) return spin_while_eq(a.verdict, 0) == 2;
+    if (a.pend.pending) return spin_epoch(a.verdict, a.pend.epoch) == 2;
     return *(volatile const int*)&v.ctl->err_code != 0;
 }
 
@@ -1525,7 +1527,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
     const bool cta_new = __syncthreads_or(any_new);
     if (DRAW && a.early && tid == 0) st_release_i32(&gc->seg[t], 1);  // this CTA's units are final
     if (cta_new) {
-        if (tid == 0) spin_until_set(route_done);
+        if (tid == 0) spin_epoch(route_done, pi.epoch);
         __syncthreads();
         double adv[MAP_R];
 #pragma unroll
@@ -1643,7 +1645,7 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
         // map the replayed tail, then rescan every owned offset (shard heads
         // from the insert's plan: the route kernel may still be advancing
         // the device counters; the metadata it writes is read below)
-        if (threadIdx.x == 0 && a.pend.pending) spin_while_eq(route_done, 0);
+        if (threadIdx.x == 0 && a.pend.pending) spin_epoch(route_done, a.pend.epoch);
         __shared__ int s_head[MAP_NSH];
         for (int s = threadIdx.x; s < a.nsh && s < MAP_NSH; s += blockDim.x)
             s_head[s] = head_after(v, a.pend, s);
@@ -1994,15 +1996,11 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     DevCtl* ctl = v.ctl;
     RB_TSTART(0);
     RB_GCLOCK(30, blockIdx.x == 0);
-    if (blockIdx.x == 0 && tid == 0) {  // this insert's verdict / completion flags
-        st_release_i32(&pay_sync[0], 0);
-        st_release_i32(&pay_sync[1], 0);
-        if (in.pay_follows) st_release_i32(&pay_sync[2], 1);  // the copy's completion flag
-        fence_gpu();  // performed before any dependent can launch
-    }
-    __syncthreads();
+    // This insert's flags (verdict, done; the copy's completion) carry its
+    // epoch: the dependents wait for the epoch, so nothing is reset here.
+    const int E = in.epoch;
     RB_GCLOCK(31, blockIdx.x == 0);
-    pdl_trigger();  // the closed-form payload copy may start now (it waits for pay_sync[0])
+    pdl_trigger();  // the closed-form payload copy may start now (it waits for the verdict)
     // the route proper runs on the first nrt CTAs
     const unsigned nrt = gridDim.x - (in.toff_keep ? (unsigned)in.keep_ctas : 0u);
     if (blockIdx.x >= nrt) {
@@ -2114,9 +2112,9 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
             if (done_add_u32(&gc->vdone) == nrt - 1) {  // acquires every CTA's bits
                 const int vb = (int)atomicOr(&gc->vbad, 0u);
                 s_bad = vb;
-                st_release_i32(&pay_sync[0], vb ? 2 : 1);
+                st_release_i32(&pay_sync[0], E << 2 | (vb ? 2 : 1));
             } else {
-                const int f = spin_while_eq(&pay_sync[0], 0);
+                const int f = spin_epoch(&pay_sync[0], E);
                 s_bad = f == 2 ? (int)__ldcg(&gc->vbad) : 0;
             }
         }
@@ -2125,7 +2123,9 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     RB_GCLOCK(61, blockIdx.x == 0);
     const int bb = s_bad;
     // unsplit: every CTA reached the same verdict; CTA 0 alone publishes it
-    if (!split && blockIdx.x == 0 && tid == 0) st_release_i32(&pay_sync[0], bb ? 2 : 1);
+    if (!split && blockIdx.x == 0 && tid == 0) st_release_i32(&pay_sync[0], E << 2 | (bb ? 2 : 1));
+    // no payload copy follows: its completion flag is trivially this insert's
+    if (!in.pay_follows && blockIdx.x == 0 && tid == 0) st_release_i32(&pay_sync[2], E << 2 | 2);
     int maxq = 0;
     if (mine) {
         int32_t slot = -1;
@@ -2226,7 +2226,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     // last CTA: every CTA's records are written (each released by its done
     // increment, acquired by ours): the sampler's map may read the metadata
     // now; the counters below are not read by it (it uses the insert's plan)
-    if (tid == 0) st_release_i32(&pay_sync[1], 1);
+    if (tid == 0) st_release_i32(&pay_sync[1], E << 2 | 1);
     int m = 0;
     for (int c = tid; c < (int)nrt; c += RT_THREADS) m = max(m, __ldcg(&gc->cta_max[c]));
     m = __reduce_max_sync(0xffffffffu, m);
@@ -2907,6 +2907,7 @@ template <int U>
 __global__ void __launch_bounds__(UNIT_THREADS, 8) k_gather_early(BufView v, const Unit* desc, int nloc,
                                                               long long lo, int ups, GridCtl* gc,
                                                               int nseg, const int* pay_pending,
+                                                              int pay_epoch,
                                                               int32_t* out_tok, float* out_lpo) {
     __shared__ int s_claim[2], s_state, s_pay, s_fin, s_ndef;
     __shared__ int s_def[GE_DEFER];
@@ -2923,7 +2924,9 @@ __global__ void __launch_bounds__(UNIT_THREADS, 8) k_gather_early(BufView v, con
     // Copies the deferred units whose condition now holds (block-uniform).
     auto drain = [&](bool wait) {
         if (tid == 0) {
-            if (!s_pay) s_pay = wait ? (spin_while_eq(pay_pending, 1), 1) : ld_acquire_i32(pay_pending) == 0;
+            if (!s_pay)  // the copy of the pending insert has completed
+                s_pay = wait ? (spin_epoch(pay_pending, pay_epoch), 1)
+                             : ld_acquire_i32(pay_pending) == (pay_epoch << 2 | 2);
             if (!s_fin) s_fin = wait ? (spin_while_eq(&gc->fin, 0), 1) : ld_acquire_i32(&gc->fin) != 0;
         }
         __syncthreads();
@@ -2955,7 +2958,7 @@ __global__ void __launch_bounds__(UNIT_THREADS, 8) k_gather_early(BufView v, con
         if (tid == 0) {
             s_claim[p ^ 1] = (int)atomicAdd(&gc->gwork, 1u);  // next claim, in flight meanwhile
             s_state = spin_while_eq(&gc->seg[(int)((lo + u / ups) / MAP_SPC)], 0);
-            if (!s_pay) s_pay = ld_acquire_i32(pay_pending) == 0;
+            if (!s_pay) s_pay = ld_acquire_i32(pay_pending) == (pay_epoch << 2 | 2);
         }
         __syncthreads();
         const int b = u / ups, c = u - b * ups;
@@ -3504,6 +3507,8 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         throw Error(RB_ELOGIC, "rb_insert_owned: FIFO retention and ids promised unique required");
     if (fifo_route) {
         // ids promised new and increasing: the closed-form FIFO route
+        b->ins_epoch = (b->ins_epoch + 1) & RB_EPOCH_MASK;
+        in.epoch = b->ins_epoch;
         const unsigned grid = (unsigned)((bt.n + RT_THREADS - 1) / RT_THREADS);
         closed = payload && b->T <= 64 && b->pdl;
         // a sampler enqueued next reads the new records' lengths from the
@@ -3553,6 +3558,7 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         p.T = (int)b->T;
         p.C = (int)b->C;
         p.own = b->own_n_global ? (int)b->sb : -1;
+        p.epoch = in.epoch;
         const int maxq = (b->max_tokens + 3) / 4;
         p.ups = std::max(1, (maxq + UNIT_THREADS * PAYLOAD_U - 1) / (UNIT_THREADS * PAYLOAD_U));
         for (size_t s = 0; s < b->T; ++s) p.pm[s] = (int)(b->h_pushes[s] % (long long)b->C);
@@ -3584,6 +3590,7 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         b->pend.c0 = p.c0;
         b->pend.n = b->own_n_global ? (int)b->own_n_global : (int)bt.n;
         b->pend.own = b->own_n_global ? 1 : 0;
+        b->pend.epoch = in.epoch;
         b->pend.toff = b->s_toff;  // the route kernel's copy
         b->pend.keep_cnt = &b->route_ctl->keep_cnt;
         b->pend.keep_target = b->keep_total;
@@ -3604,6 +3611,7 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         b->pend.c0 = (int)(b->h_cursor % b->T);
         b->pend.n = b->own_n_global ? (int)b->own_n_global : (int)bt.n;
         b->pend.own = b->own_n_global ? 1 : 0;
+        b->pend.epoch = in.epoch;
         b->pend.toff = bt.tok_offsets ? b->s_toff : nullptr;  // lengths only (or NULL: length 0)
         b->pend.keep_cnt = &b->route_ctl->keep_cnt;
         b->pend.keep_target = b->keep_total;
@@ -3895,6 +3903,7 @@ int rb_insert_owned(rb_buffer* b, const rb_insert_batch* batch, size_t n_global,
                     std::to_string(n_global));
         if (n_global == 0) return;
         if (batch->n == 0) {  // only the other shards' counters and the cursor advance
+            b->other_work();  // no insert plan is pending for a sampler
             b->sync_checked();
             for (size_t j = 0; j < n_global; ++j) b->h_pushes[(b->h_cursor + j) % T]++;
             b->h_cursor = (b->h_cursor + n_global) % T;
@@ -4056,6 +4065,7 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 rng->gen_pending = false;
             MtRing* ring = rng->to_device(b->stream);
             if (b->pdl_tail) a.pend = b->pend;  // the insert just enqueued may still run
+            b->gather_epoch = a.pend.pending ? a.pend.epoch : b->gather_epoch;
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(nmap + 1);
             cfg.blockDim = dim3(MAP_THREADS);
@@ -4216,7 +4226,8 @@ int rb_gather(rb_buffer* b, int32_t* out_tokens, float* out_logp_old, int64_t* o
             cfg.numAttrs = 1;
             RB_CUDA(cudaLaunchKernelEx(&cfg, k_gather_early<GATHER_U>, b->v,
                                        (const Unit*)b->units_sel, (int)nloc, lo, ups, b->map_ctl,
-                                       b->seg_used, (const int*)(b->pay_sync + 2), dt, dl));
+                                       b->seg_used, (const int*)(b->pay_sync + 2),
+                                       b->gather_epoch, dt, dl));
             b->seg_used = 0;  // the early gather resets the flags it consumed
         } else if (nloc > 0 && (dt || dl)) {
             // the resident grid, or one CTA per work unit for small batches

@@ -72,6 +72,7 @@ struct PendingIns {
     int pending;          // 1: the last insert (closed-form FIFO, <= 64 shards) may be running
     int c0, n;            // its cursor % T and (global) record count
     int own;              // owned-metadata insert: its offsets index the owned shard's records only
+    int epoch;            // its flag epoch (verdict / done / copy-done carry it)
     const int64_t* toff;  // its payload offsets (the route kernel's copy)
     const unsigned long long* keep_cnt;  // the copy is complete once *keep_cnt >= keep_target
     unsigned long long keep_target;
@@ -139,6 +140,8 @@ struct rb_buffer {
     int sms = 148;
     int tma_ctas = 3;                   // bulk-copy payload pipelines (single-warp CTAs) per SM
     bool pdl_tail = false;              // the stream's last kernel is the closed-form payload copy
+    int ins_epoch = 0;                  // epoch of the last closed-form FIFO insert (pay_sync tags)
+    int gather_epoch = 0;               // epoch of the insert pending at the last fused sampler
     rb::PendingIns pend{};              // its insert's plan (for a sampler that overlaps it)
     unsigned long long keep_total = 0;  // route CTAs launched with an offsets copy (host count)
     int seg_used = 0;                   // map CTAs whose early-gather flags are set (to reset)

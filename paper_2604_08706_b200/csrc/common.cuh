@@ -313,6 +313,23 @@ static __device__ __noinline__ int spin_while_eq(const int* f, int v) {
     return x;
 }
 
+// Epoch-tagged flags of an insert (verdict, route done, copy done):
+// value = epoch << 2 | state.  A waiter knows the epoch it waits for, so a
+// flag left by an earlier insert is simply "not yet": nothing is reset (no
+// reset store has to become visible before a dependent launches).
+// Returns the state once the flag carries `epoch`; bounded like spin_while_eq.
+constexpr int RB_EPOCH_MASK = (1 << 29) - 1;
+static __device__ __noinline__ int spin_epoch(const int* f, int epoch) {
+    int x = ld_acquire_i32(f);
+    if ((x >> 2) == epoch) return x & 3;
+    const unsigned long long t0 = gtimer_ns();
+    while (((x = ld_acquire_i32(f)) >> 2) != epoch) {
+        __nanosleep(64);
+        if (gtimer_ns() - t0 > 4000000000ULL) __trap();
+    }
+    return x & 3;
+}
+
 // Writes made before a programmatic trigger, performed before it executes.
 __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
