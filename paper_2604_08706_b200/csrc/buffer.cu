@@ -2008,7 +2008,9 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
         // may reuse its offsets as soon as later stream work runs, but an
         // overlapping sampler reads the new records' lengths after this
         // call: keep a copy, published by a monotonic counter (the sampler
-        // waits for its target).
+        // waits for its target).  The previous insert's sampler may still
+        // read the copy area: written after the wait.
+        pdl_wait();
         const int base = (int)(blockIdx.x - nrt) * RT_KEEP + tid;
         int64_t t[RT_KEEP / RT_THREADS];
 #pragma unroll
@@ -2026,15 +2028,10 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
             asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(in.keep_cnt) : "memory");
         return;
     }
-    const int sticky = ctl->err_code;
-    const unsigned long long cur0 = ctl->cursor;
-    RB_GCLOCK(32, blockIdx.x == 0);  // (debug builds: after the control-block loads are issued)
-    const int has_any = ctl->has_any;
-    const unsigned long long max_id = ctl->max_id;
-    const int T = v.T, C = v.C;
-    const int c0 = (int)(cur0 % (unsigned long long)T);
-    if (tid == 0) s_bad = sticky ? 8 : 0;
-    for (int s = tid; s < T && s < RT_NSH; s += RT_THREADS) s_P[s] = v.pushes[s];
+    // ---- before the wait: the caller's batch only (when launched as a
+    // programmatic dependent of the previous step's sampler or loss, this
+    // overlaps its tail; nothing of the buffer is read or written yet)
+    if (tid == 0) s_bad = 0;
     const bool goff_smem = !in.adv && ng <= RT_GOFF;
     if (goff_smem)
         for (long long gi = tid; gi <= ng; gi += RT_THREADS) s_goff[gi] = in.goff[gi];
@@ -2069,13 +2066,14 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
     // the verdict alone; larger batches (many GPUs: the metadata of every
     // shard's records) split it: each CTA checks its own records and a stride
     // of the groups, the last CTA to finish ORs the bits and publishes the
-    // verdict, the others wait for it.
+    // verdict, the others wait for it.  The first id's check against the
+    // buffer's largest id comes after the wait.
     const bool split = in.split_validate != 0;
     int bad = 0;
-    if (!sticky && split) {
+    if (split) {
         if (mine) {
             if (in.toff && (len < 0 || len > in.maxlen)) bad |= 2;
-            if (j > 0 ? id <= in.id[j - 1] : (has_any && id <= max_id)) bad |= 1;
+            if (j > 0 && id <= in.id[j - 1]) bad |= 1;
         }
         if (!in.adv) {
             if (blockIdx.x == 0 && tid == 0 && (in.goff[0] != 0 || in.goff[ng] != n)) bad |= 4;
@@ -2085,15 +2083,14 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
                 if (e - b < 2 || b < 0 || e > n) bad |= 4;
             }
         }
-    } else if (!sticky) {
+    } else {
 #pragma unroll (RT_UNROLL)
         for (int jj = tid; jj < n; jj += RT_THREADS) {
             if (in.toff) {
                 const long long l = in.toff[jj + 1] - in.toff[jj];
                 if (l < 0 || l > in.maxlen) bad |= 2;
             }
-            const uint64_t x = in.id[jj];
-            if (jj > 0 ? x <= in.id[jj - 1] : (has_any && x <= max_id)) bad |= 1;
+            if (jj > 0 && in.id[jj] <= in.id[jj - 1]) bad |= 1;
         }
         if (!in.adv) {
             if (tid == 0 && (in.goff[0] != 0 || in.goff[ng] != n)) bad |= 4;
@@ -2103,6 +2100,34 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
             }
         }
     }
+    const uint64_t id0 = n > 0 ? in.id[0] : 0;
+    __syncthreads();  // s_bad and s_goff written
+    // group advantages of the own record (bandit.cpp:276-294), from the batch
+    if (mine && !in.adv && !bad) {
+        long long lo = 0, hi = ng;  // group gi: goff[gi] <= j < goff[gi+1]
+        while (hi - lo > 1) {
+            const long long mid = (lo + hi) >> 1;
+            const long long gm = goff_smem ? s_goff[mid] : in.goff[mid];
+            if (gm <= j) lo = mid;
+            else hi = mid;
+        }
+        const long long b = goff_smem ? s_goff[lo] : in.goff[lo];
+        const long long e = goff_smem ? s_goff[lo + 1] : in.goff[lo + 1];
+        if (e - b >= 2 && b >= 0 && e <= n) group_adv_one(in.reward, b, e, reward, &adv, &gmean);
+    }
+    // ---- the buffer's state: after the previous kernel (if a programmatic
+    // dependency) has completed
+    pdl_wait();
+    const int sticky = ctl->err_code;
+    const unsigned long long cur0 = ctl->cursor;
+    RB_GCLOCK(32, blockIdx.x == 0);  // (debug builds: after the control-block loads are issued)
+    const int has_any = ctl->has_any;
+    const unsigned long long max_id = ctl->max_id;
+    const int T = v.T, C = v.C;
+    const int c0 = (int)(cur0 % (unsigned long long)T);
+    for (int s = tid; s < T && s < RT_NSH; s += RT_THREADS) s_P[s] = v.pushes[s];
+    if (sticky) bad |= 8;
+    if (tid == 0 && (split ? blockIdx.x == 0 : true) && n > 0 && has_any && id0 <= max_id) bad |= 1;
     RB_GCLOCK(60, blockIdx.x == 0);
     if (bad) atomicOr(&s_bad, bad);
     __syncthreads();
@@ -2170,18 +2195,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_route_fifo(BufView v, InsertIn i
                 const int r0 = rank % C;
                 in.evid[r0 * jst + j0] = P + r0 >= C ? v.id[g] : NONE_ID;
             }
-            if (!in.adv) {
-                long long lo = 0, hi = ng;  // group gi: goff[gi] <= j < goff[gi+1]
-                while (hi - lo > 1) {
-                    const long long mid = (lo + hi) >> 1;
-                    const long long gm = goff_smem ? s_goff[mid] : in.goff[mid];
-                    if (gm <= j) lo = mid;
-                    else hi = mid;
-                }
-                const long long b = goff_smem ? s_goff[lo] : in.goff[lo];
-                const long long e = goff_smem ? s_goff[lo + 1] : in.goff[lo + 1];
-                group_adv_one(in.reward, b, e, reward, &adv, &gmean);
-            }
+            // (advantages: computed from the batch before the wait)
             if (surv) {
                 v.id[g] = id;
                 v.prompt[g] = prompt;
@@ -3442,6 +3456,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         b->early_gather_ok = b->pdl && std::getenv("RB_EARLY_GATHER") != nullptr;
         b->tma_payload = std::getenv("RB_PAYLOAD_LSU") == nullptr;
         b->pb_par = std::getenv("RB_NO_PB_PAR") == nullptr;
+        b->route_pdl = b->pdl && std::getenv("RB_NO_ROUTE_PDL") == nullptr;
         b->loss_dyn = std::getenv("RB_LOSS_CHUNK_MAJOR") == nullptr;
         b->tma_long = std::getenv("RB_PAYLOAD_TMA_LONG") != nullptr;
         b->chunk_major = std::getenv("RB_NO_CHUNK_MAJOR") == nullptr;
@@ -3519,8 +3534,20 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         in.keep_cnt = &b->route_ctl->keep_cnt;
         in.keep_ctas = in.toff_keep ? (int)((bt.n + 1 + RT_KEEP - 1) / RT_KEEP) : 0;
         b->keep_total += (unsigned long long)in.keep_ctas;  // extra CTAs copy them
-        k_route_fifo<<<grid + (unsigned)in.keep_ctas, RT_THREADS, 0, b->stream>>>(
-            b->v, in, b->route_ctl, b->pay_sync);
+        // a programmatic dependent of the previous kernel (the last step's
+        // sampler or loss trigger at their start): the batch's loads,
+        // validation and group advantages overlap that kernel's tail; the
+        // buffer is touched only after griddepcontrol.wait
+        cudaLaunchConfig_t rcfg = {};
+        rcfg.gridDim = dim3(grid + (unsigned)in.keep_ctas);
+        rcfg.blockDim = dim3(RT_THREADS);
+        rcfg.stream = b->stream;
+        cudaLaunchAttribute rat[1];
+        rat[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        rat[0].val.programmaticStreamSerializationAllowed = 1;
+        rcfg.attrs = rat;
+        rcfg.numAttrs = b->route_pdl ? 1 : 0;
+        RB_CUDA(cudaLaunchKernelEx(&rcfg, k_route_fifo, b->v, in, b->route_ctl, b->pay_sync));
     } else if (unique && b->retention == RB_POSITIVE_BIAS && !want_evrec && b->pb_par &&
                b->C <= (size_t)PBP_CMAX && bt.n <= (size_t)PBP_NMAX &&
                (bt.n + b->T - 1) / b->T <= (size_t)PBP_NSMAX) {

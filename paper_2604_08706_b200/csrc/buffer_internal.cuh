@@ -137,6 +137,7 @@ struct rb_buffer {
     bool pdl = true;                    // programmatic dependent launch of the payload copy
     bool tma_payload = true;            // bulk-copy (TMA) payload kernel (else 128-bit LSU)
     bool pb_par = true;                 // positive bias, unique ids: k_posbias_par (one launch)
+    bool route_pdl = true;              // FIFO route as a programmatic dependent of the previous kernel
     int sms = 148;
     int tma_ctas = 3;                   // bulk-copy payload pipelines (single-warp CTAs) per SM
     bool pdl_tail = false;              // the stream's last kernel is the closed-form payload copy

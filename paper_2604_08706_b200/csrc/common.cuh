@@ -348,6 +348,9 @@ static __device__ __noinline__ void spin_until_ge_u64(const unsigned long long* 
 __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Waits until the grid this one programmatically depends on has completed and
+// its writes are visible (returns at once without such a dependency).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
     const float tol_hi = 4e-6f * prm.hi_f, tol_lo = 4e-6f * prm.lo_f;
     RB_TSTART(5);
     RB_GCLOCK(0, blockIdx.x == 0);
+    pdl_trigger();  // the next step's route may start on its batch (it waits before the buffer)
     const int ups = (*maxq_p + QU - 1) / QU;
     const int nu = nloc * ups;
     GrpoPartial part;
@@ -679,6 +680,7 @@ __global__ void __launch_bounds__(UNIT_THREADS) k_loss_asymre_buf(
     rb_loss_stats* stats, int part_base, int nparts) {
     constexpr int QU = UNIT_THREADS * U;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    pdl_trigger();  // the next step's route may start on its batch (it waits before the buffer)
     const int ups = (*maxq_p + QU - 1) / QU;
     const int nu = nloc * ups;
     GrpoPartial part;

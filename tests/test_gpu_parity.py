@@ -478,7 +478,7 @@ def test_side_lookahead_matches(rb, oracle, case, monkeypatch):
 
 
 @pytest.mark.parametrize("switch", ["RB_NO_PDL", "RB_PAYLOAD_LSU", "RB_NO_LOOKAHEAD",
-                                    "RB_TMA_CTAS"])
+                                    "RB_TMA_CTAS", "RB_NO_ROUTE_PDL"])
 @pytest.mark.parametrize("case", ["c4_unique_overlap", "c3_unique_overlap_big"])
 def test_env_switches_do_not_change_results(rb, oracle, case, switch, monkeypatch):
     """Every performance switch leaves the results bit-identical."""
