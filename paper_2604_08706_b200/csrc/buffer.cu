@@ -2369,34 +2369,21 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
     int* QE = WE + nsp;     // correct entries in order
     uint8_t* cx = reinterpret_cast<uint8_t*>(QE + nsp);  // correctness of push k
     uint8_t* evw = cx + nsp;                             // push k pops W
-    // Every load below is independent (one memory round trip): control
-    // block, queue state, group offsets, the shard's pre-batch ids and
-    // sequence numbers, the whole batch's validation inputs.
-    const int sticky = ctl->err_code;
-    const int has_any = ctl->has_any;
-    const unsigned long long max_id = ctl->max_id;
-    const long long P0 = v.pushes[s];
-    if (tid == 0) {
-        s_st = v.pbs[s];
-        s_maxq = 0;
-    }
+    // ---- before the wait: the caller's batch only (a programmatic dependent
+    // of the previous kernel: this overlaps its tail; the buffer is read and
+    // written only after griddepcontrol.wait)
     const bool goff_smem = !in.adv && ng <= RT_GOFF;
     if (goff_smem)
         for (long long gi = tid; gi <= ng; gi += nt) s_goff[gi] = in.goff[gi];
-    for (int x = tid; x < C; x += nt) {
-        preseq[x] = v.seq[(size_t)s * C + x];
-        preid[x] = v.id[(size_t)s * C + x];
-        occb[x] = -1;
-    }
-    // whole-batch validation (nothing applied if any check fails)
+    // whole-batch validation (nothing applied if any check fails); the first
+    // id against the buffer's largest id after the wait
     int bad = 0;
     for (int jj = tid; jj < n; jj += nt) {
         if (in.toff) {
             const long long l = in.toff[jj + 1] - in.toff[jj];
             if (l < 0 || l > in.maxlen) bad |= 2;
         }
-        const uint64_t x = in.id[jj];
-        if (jj > 0 ? x <= in.id[jj - 1] : (has_any && x <= max_id)) bad |= 1;
+        if (jj > 0 && in.id[jj] <= in.id[jj - 1]) bad |= 1;
     }
     if (!in.adv) {
         if (tid == 0 && (in.goff[0] != 0 || in.goff[ng] != n)) bad |= 4;
@@ -2404,6 +2391,51 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
             const long long b = in.goff[gi], e = in.goff[gi + 1];
             if (e - b < 2 || b < 0 || e > n) bad |= 4;
         }
+    }
+    const uint64_t id0 = n > 0 ? in.id[0] : 0;
+    __syncthreads();  // s_goff written
+    // own records: lengths, advantages (frozen at insertion, bandit.cpp:276-294,
+    // the reference's fp64 order), correctness — into the insert's own scratch
+    // columns (no kernel before this one reads them)
+    for (int k = tid; k < ns; k += nt) {
+        const int j = j0 + k * T;
+        const long long l = in.toff ? in.toff[j + 1] - in.toff[j] : 0;
+        in.len[j] = (int32_t)l;
+        double adv = 0.0, gmean = 0.0;
+        if (in.adv) {
+            adv = in.adv[j];
+            gmean = in.gmean ? in.gmean[j] : 0.0;
+        } else if (!bad) {
+            long long lo = 0, hi = ng;
+            while (hi - lo > 1) {
+                const long long mid = (lo + hi) >> 1;
+                const long long gm = goff_smem ? s_goff[mid] : in.goff[mid];
+                if (gm <= j) lo = mid;
+                else hi = mid;
+            }
+            const long long b = goff_smem ? s_goff[lo] : in.goff[lo];
+            const long long e = goff_smem ? s_goff[lo + 1] : in.goff[lo + 1];
+            if (e - b >= 2 && b >= 0 && e <= n) group_adv_one(in.reward, b, e, in.reward[j], &adv, &gmean);
+        }
+        in.adv_out[j] = adv;
+        in.gmean_out[j] = gmean;
+        cx[k] = in_correct(in, j) ? 1 : 0;
+    }
+    // ---- the buffer's state
+    pdl_wait();
+    const int sticky = ctl->err_code;
+    const int has_any = ctl->has_any;
+    const unsigned long long max_id = ctl->max_id;
+    const long long P0 = v.pushes[s];
+    if (tid == 0) {
+        s_st = v.pbs[s];
+        s_maxq = 0;
+        if (n > 0 && has_any && id0 <= max_id) bad |= 1;
+    }
+    for (int x = tid; x < C; x += nt) {
+        preseq[x] = v.seq[(size_t)s * C + x];
+        preid[x] = v.id[(size_t)s * C + x];
+        occb[x] = -1;
     }
     const int bb = (sticky ? 8 : 0) | (__syncthreads_or(bad & 1) ? 1 : 0) |
                    (__syncthreads_or(bad & 2) ? 2 : 0) | (__syncthreads_or(bad & 4) ? 4 : 0);
@@ -2429,9 +2461,7 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
         }
         return;
     }
-    // Second round trip: the shard's rings (pre-batch heads, rebased to 0)
-    // and the group rewards of the own records (advantages frozen at
-    // insertion, bandit.cpp:276-294, the reference's fp64 order).
+    // the shard's rings (pre-batch heads, rebased to 0)
     const PbState st = s_st;
     uint32_t* gring[3] = {(uint32_t*)pb_ring(v, 0, s), (uint32_t*)pb_ring(v, 1, s),
                           (uint32_t*)pb_ring(v, 2, s)};
@@ -2441,30 +2471,6 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
             if (p >= RC) p -= RC;
             ring[r * RC + i] = gring[r][p];
         }
-    for (int k = tid; k < ns; k += nt) {
-        const int j = j0 + k * T;
-        const long long l = in.toff ? in.toff[j + 1] - in.toff[j] : 0;
-        in.len[j] = (int32_t)l;
-        double adv, gmean;
-        if (in.adv) {
-            adv = in.adv[j];
-            gmean = in.gmean ? in.gmean[j] : 0.0;
-        } else {
-            long long lo = 0, hi = ng;
-            while (hi - lo > 1) {
-                const long long mid = (lo + hi) >> 1;
-                const long long gm = goff_smem ? s_goff[mid] : in.goff[mid];
-                if (gm <= j) lo = mid;
-                else hi = mid;
-            }
-            const long long b = goff_smem ? s_goff[lo] : in.goff[lo];
-            const long long e = goff_smem ? s_goff[lo + 1] : in.goff[lo + 1];
-            group_adv_one(in.reward, b, e, in.reward[j], &adv, &gmean);
-        }
-        in.adv_out[j] = adv;
-        in.gmean_out[j] = gmean;
-        cx[k] = in_correct(in, j) ? 1 : 0;
-    }
     __syncthreads();
     RB_GCLOCK(22, s == 0);
     const int size0 = (int)(P0 < C ? P0 : C);
@@ -3566,8 +3572,19 @@ void launch_insert(rb_buffer* b, const rb_insert_batch& bt, bool want_evrec, boo
         // C/4 threads (the ring rewrite keeps 4 entries per thread in registers)
         const int need = std::max({nsp, (int)(b->C + 3) / 4, 128});
         const int nthr = std::min(PBP_THREADS, (need + 31) & ~31);
-        k_posbias_par<<<(unsigned)b->T, nthr, smem, b->stream>>>(
-            b->v, in, (unsigned long long)b->h_cursor, b->route_ctl, nsp);
+        // a programmatic dependent of the previous kernel, like the FIFO route
+        cudaLaunchConfig_t pcfg = {};
+        pcfg.gridDim = dim3((unsigned)b->T);
+        pcfg.blockDim = dim3((unsigned)nthr);
+        pcfg.dynamicSmemBytes = smem;
+        pcfg.stream = b->stream;
+        cudaLaunchAttribute pat[1];
+        pat[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        pat[0].val.programmaticStreamSerializationAllowed = 1;
+        pcfg.attrs = pat;
+        pcfg.numAttrs = b->route_pdl ? 1 : 0;
+        RB_CUDA(cudaLaunchKernelEx(&pcfg, k_posbias_par, b->v, in, (unsigned long long)b->h_cursor,
+                                   b->route_ctl, nsp));
     } else {
         k_insert_route<<<1, 1024, 0, b->stream>>>(b->v, in);
         if (b->retention == RB_POSITIVE_BIAS) {
