@@ -1214,6 +1214,7 @@ __device__ __forceinline__ void finalize_publish_wait(unsigned* cnt) {
 }
 __global__ void k_finalize_vec(DevLossAcc* acc, const double* v3, float* dlogp,
                                const long long* n_dev, rb_loss_stats* st, int grpo) {
+    pdl_trigger();  // the next step's route may start on its batch (it waits before the buffer)
     const double obj = v3[0];
     const unsigned long long inc = (unsigned long long)v3[1], exc = (unsigned long long)v3[2];
     float f = 1.f;
@@ -1245,6 +1246,7 @@ __global__ void k_set_red3(DevLossAcc* acc, double* v) { acc->red3 = v; }
 // rb_loss_finalize in one kernel (reduced rb_loss_stats in, stats out).
 __global__ void k_finalize_stats(DevLossAcc* acc, rb_loss_stats* st, float* dlogp,
                                  const long long* n_dev, int grpo) {
+    pdl_trigger();  // the next step's route may start on its batch (it waits before the buffer)
     const double obj = st->objective_sum;
     const long long inc = st->included, exc = st->excluded;
     float f = 1.f;
