@@ -1238,9 +1238,6 @@ __device__ __forceinline__ unsigned long long lookback(GridCtl* gc, int t) {
     }
     return excl;
 }
-__device__ __forceinline__ void spin_until_set(const int* flag) {
-    spin_while_eq(flag, 0);  // bounded: traps instead of hanging if never set
-}
 
 // ---- map phase (every sampler): arrival index -> slot, use counts
 // (replay_buffer.cpp:201), lengths, advantages; packed offsets of the owned

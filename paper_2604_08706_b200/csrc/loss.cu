@@ -96,13 +96,6 @@ __device__ __forceinline__ float exp_ftz(float d) {
     return r;
 }
 
-__device__ __forceinline__ uint4 ldg4(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
 __device__ __forceinline__ uint4 funnel4(const uint4& lo, const uint4& hi, int a) {
     switch (a & 3) {
         case 0: return lo;
