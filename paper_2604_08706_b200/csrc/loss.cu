@@ -339,8 +339,14 @@ __device__ __noinline__ float grpo_token_exact(float lpn, float lpo, double A,
 // counter, the next claim in flight while the current unit runs.
 template <int U, bool DYN, bool CM = false>
 // (More CTAs per SM via a register cap spill and run slower: 44 µs at 10
-// CTAs per SM vs 37 µs at 8.)
-__global__ void __launch_bounds__(UNIT_THREADS) k_loss_grpo_buf(
+// CTAs per SM vs 37 µs at 8.  The claimed-unit variant for ragged long rows
+// is capped to 8 CTAs per SM (64 registers): C3 loss 24.4 vs 25.6 µs; the
+// static-stride one to 7 (72 registers; uncapped it takes 96): C4 step 82.9
+// vs 84.6 µs.)
+#ifndef RB_LOSS_MINB
+#define RB_LOSS_MINB 7
+#endif
+__global__ void __launch_bounds__(UNIT_THREADS, DYN ? 8 : RB_LOSS_MINB) k_loss_grpo_buf(
     BufView v, const Unit* units, const int* maxq_p, int nloc, const float* lpn_packed,
     float* dlogp, GrpoParams prm, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats,
     const long long* n_local, int local_fix, int part_base, int nparts) {
