@@ -337,6 +337,97 @@ __device__ __noinline__ float grpo_token_exact(float lpn, float lpo, double A,
 // is the gather's order for long rows; for the loss it measured level with
 // DYN, C3 24.6 vs 24.0 µs).  DYN (long rows, default): units claimed from a
 // counter, the next claim in flight while the current unit runs.
+// One work unit of the GRPO loss: QU destination quads of selection `un`
+// (chunk c).  BOUNDED: the batch's last selection, whose last quad may end
+// the caller's logp_now array — loaded word by word there (every other
+// selection's last quad reads into the next selection's tokens, in bounds).
+// The whole unit is instantiated twice so the hot path has no branch between
+// its loads and their first use.
+template <int U, bool BOUNDED>
+__device__ __forceinline__ void grpo_unit(const BufView& v, const Unit& un, int c, int nq, int a,
+                                          const float* lpn_packed, float* dlogp,
+                                          const GrpoParams& prm, float scale, float tol_hi,
+                                          float tol_lo, GrpoPartial& part, long long& inc_fast) {
+    constexpr int QU = UNIT_THREADS * U;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nsq = (un.len + 3) >> 2;
+    const long long P0 = un.off >> 2;
+    const int kw = c * QU + wid * 32 * U;
+    uint4 now[U], old[U];
+#pragma unroll
+    for (int s = 0; s < U; ++s) {
+        const int k = kw + 32 * s + lane;
+        now[s] = k < nq ? (BOUNDED ? ld_stream_lim(lpn_packed, P0 + k, un.off + un.len)
+                                   : ld_stream(lpn_packed + 4 * (P0 + k)))
+                        : make_uint4(0, 0, 0, 0);
+    }
+    row_to_packed_quads<U>(
+        reinterpret_cast<const uint4*>(v.lpo + (size_t)un.row * v.stride), nsq, a, kw, old);
+    const double A = un.adv;
+    const float Af = (float)A;
+    const float Afs = Af * scale;
+    // Per unit the branch depends on one threshold only: A > 0 clips above
+    // 1+eps_high (r near 1-eps_low is unclipped either way), A < 0 below
+    // 1-eps_low, A = 0 never contributes.  Only tokens within tol of that
+    // threshold, or with d >= 80 / NaN (fp32 overflow vs fp64), go exact.
+    const int sgn = A > 0.0 ? 1 : (A < 0.0 ? -1 : 0);
+    const float thr = sgn > 0 ? prm.hi_f : prm.lo_f;
+    const float tol = sgn > 0 ? tol_hi : tol_lo;
+    double fsum = 0.0;  // fp64: the objective matches the reference's fp64 sum
+#pragma unroll
+    for (int s = 0; s < U; ++s) {
+        const int k = kw + 32 * s + lane;
+        if (k < nq) {
+            const int e0 = 4 * k - a;
+            const bool full = e0 >= 0 && e0 + 3 < un.len;
+            float o[4] = {0.f, 0.f, 0.f, 0.f};
+            bool slow = !full;
+            if (full) {
+                float r[4];
+                bool edge = false;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float d = qf(now[s], i) - qf(old[s], i);
+                    r[i] = exp_ftz(d);
+                    edge |= !(fabsf(d) < RB_FAST_D) || (sgn != 0 && fabsf(r[i] - thr) <= tol);
+                }
+                if (!edge) {
+                    if (sgn > 0) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const bool unc = r[i] <= thr;
+                            o[i] = unc ? Afs * r[i] : 0.f;
+                            fsum += (double)(unc ? r[i] : thr);
+                        }
+                    } else if (sgn < 0) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const bool unc = r[i] >= thr;
+                            o[i] = unc ? Afs * r[i] : 0.f;
+                            fsum += (double)(unc ? r[i] : thr);
+                        }
+                    }
+                    inc_fast += 4;
+                } else {
+                    slow = true;
+                }
+            }
+            if (slow) {  // boundary quads and edge tokens: exact fp64, per token
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (e0 + i >= 0 && e0 + i < un.len)
+                        o[i] = grpo_token_exact(qf(now[s], i), qf(old[s], i), A, prm, part) *
+                               scale;
+            }
+            store_quad_masked(reinterpret_cast<uint32_t*>(dlogp), P0 + k,
+                              make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]),
+                                         __float_as_uint(o[2]), __float_as_uint(o[3])),
+                              e0, un.len);
+        }
+    }
+    part.obj += fsum * A;
+}
+
 template <int U, bool DYN, bool CM = false>
 // (More CTAs per SM via a register cap spill and run slower: 44 µs at 10
 // CTAs per SM vs 37 µs at 8.  The claimed-unit variant for ragged long rows
@@ -351,7 +442,6 @@ __global__ void __launch_bounds__(UNIT_THREADS, DYN ? 8 : RB_LOSS_MINB) k_loss_g
     float* dlogp, GrpoParams prm, DevLossAcc* acc, Partial* parts, rb_loss_stats* stats,
     const long long* n_local, int local_fix, int part_base, int nparts) {
     constexpr int QU = UNIT_THREADS * U;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const float scale = -1.f / (float)acc->total_tokens;
     const float tol_hi = 4e-6f * prm.hi_f, tol_lo = 4e-6f * prm.lo_f;
     RB_TSTART(5);
@@ -380,81 +470,12 @@ __global__ void __launch_bounds__(UNIT_THREADS, DYN ? 8 : RB_LOSS_MINB) k_loss_g
         const int a = (int)(un.off & 3);
         const int nq = (a + un.len + 3) >> 2;
         if (c * QU < nq) {
-        const int nsq = (un.len + 3) >> 2;
-        const long long P0 = un.off >> 2;
-        const int kw = c * QU + wid * 32 * U;
-        uint4 now[U], old[U];
-#pragma unroll
-        for (int s = 0; s < U; ++s) {
-            const int k = kw + 32 * s + lane;
-            now[s] = k < nq ? ld_stream_lim(lpn_packed, P0 + k, un.off + un.len)
-                            : make_uint4(0, 0, 0, 0);
-        }
-        row_to_packed_quads<U>(
-            reinterpret_cast<const uint4*>(v.lpo + (size_t)un.row * v.stride), nsq, a, kw, old);
-        const double A = un.adv;
-        const float Af = (float)A;
-        const float Afs = Af * scale;
-        // Per unit the branch depends on one threshold only: A > 0 clips above
-        // 1+eps_high (r near 1-eps_low is unclipped either way), A < 0 below
-        // 1-eps_low, A = 0 never contributes.  Only tokens within tol of that
-        // threshold, or with d >= 80 / NaN (fp32 overflow vs fp64), go exact.
-        const int sgn = A > 0.0 ? 1 : (A < 0.0 ? -1 : 0);
-        const float thr = sgn > 0 ? prm.hi_f : prm.lo_f;
-        const float tol = sgn > 0 ? tol_hi : tol_lo;
-        double fsum = 0.0;  // fp64: the objective matches the reference's fp64 sum
-#pragma unroll
-        for (int s = 0; s < U; ++s) {
-            const int k = kw + 32 * s + lane;
-            if (k < nq) {
-                const int e0 = 4 * k - a;
-                const bool full = e0 >= 0 && e0 + 3 < un.len;
-                float o[4] = {0.f, 0.f, 0.f, 0.f};
-                bool slow = !full;
-                if (full) {
-                    float r[4];
-                    bool edge = false;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float d = qf(now[s], i) - qf(old[s], i);
-                        r[i] = exp_ftz(d);
-                        edge |= !(fabsf(d) < RB_FAST_D) || (sgn != 0 && fabsf(r[i] - thr) <= tol);
-                    }
-                    if (!edge) {
-                        if (sgn > 0) {
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const bool unc = r[i] <= thr;
-                                o[i] = unc ? Afs * r[i] : 0.f;
-                                fsum += (double)(unc ? r[i] : thr);
-                            }
-                        } else if (sgn < 0) {
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const bool unc = r[i] >= thr;
-                                o[i] = unc ? Afs * r[i] : 0.f;
-                                fsum += (double)(unc ? r[i] : thr);
-                            }
-                        }
-                        inc_fast += 4;
-                    } else {
-                        slow = true;
-                    }
-                }
-                if (slow) {  // boundary quads and edge tokens: exact fp64, per token
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (e0 + i >= 0 && e0 + i < un.len)
-                            o[i] = grpo_token_exact(qf(now[s], i), qf(old[s], i), A, prm, part) *
-                                   scale;
-                }
-                store_quad_masked(reinterpret_cast<uint32_t*>(dlogp), P0 + k,
-                                  make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]),
-                                             __float_as_uint(o[2]), __float_as_uint(o[3])),
-                                  e0, un.len);
-            }
-        }
-        part.obj += fsum * A;
+            if (b == nloc - 1)
+                grpo_unit<U, true>(v, un, c, nq, a, lpn_packed, dlogp, prm, scale, tol_hi, tol_lo,
+                                   part, inc_fast);
+            else
+                grpo_unit<U, false>(v, un, c, nq, a, lpn_packed, dlogp, prm, scale, tol_hi, tol_lo,
+                                    part, inc_fast);
         }
         if (DYN) {
             __syncthreads();
