@@ -857,9 +857,9 @@ __device__ __forceinline__ void payload_body(const BufView& v, const Unit* desc,
     pdl_trigger();
     Unit nxt;  // descriptor of the next unit, loaded one unit ahead
     if ((int)blockIdx.x < nu) nxt = load_desc(blockIdx.x);
+    const long long tend = CLOSED ? toff[n] : 0;
     for (int u = blockIdx.x; u < nu; u += gridDim.x) {
-        const int j = u / ups, c = u - j * ups;
-        (void)j;
+        const int c = u % ups;
         const Unit un = nxt;
         if (u + (int)gridDim.x < nu) nxt = load_desc(u + (int)gridDim.x);
         const int nq = (un.len + 3) >> 2;  // destination (row) quads
@@ -869,12 +869,18 @@ __device__ __forceinline__ void payload_body(const BufView& v, const Unit* desc,
         const int kw = c * QU + wid * 32 * U;
         const size_t row = (size_t)un.row * v.stride;
         uint4 ot[U], ol[U];
-        if (tokens)
-            packed_to_row_quads<U>(reinterpret_cast<const uint4*>(tokens) + (un.off >> 2), nsq, a,
-                                   kw, ot, a + un.len);
-        if (logp_old)
-            packed_to_row_quads<U>(reinterpret_cast<const uint4*>(logp_old) + (un.off >> 2), nsq,
-                                   a, kw, ol, a + un.len);
+        const uint4* tq = reinterpret_cast<const uint4*>(tokens) + (un.off >> 2);
+        const uint4* lq = reinterpret_cast<const uint4*>(logp_old) + (un.off >> 2);
+        // closed form: only a record whose last quad crosses the batch's end
+        // (toff[n]) reads word by word; any other record's last quad reads
+        // into the next record's tokens, inside the caller's arrays
+        if (!CLOSED || ((un.off + un.len + 3) & ~3LL) > tend) {
+            if (tokens) packed_to_row_quads<U, true>(tq, nsq, a, kw, ot, a + un.len);
+            if (logp_old) packed_to_row_quads<U, true>(lq, nsq, a, kw, ol, a + un.len);
+        } else {
+            if (tokens) packed_to_row_quads<U, false>(tq, nsq, a, kw, ot, a + un.len);
+            if (logp_old) packed_to_row_quads<U, false>(lq, nsq, a, kw, ol, a + un.len);
+        }
         if (CLOSED && !ready) {  // CTA-uniform: first store of this CTA
             if (threadIdx.x == 0) {
                 s_flag = spin_epoch(&sync[0], p.epoch);

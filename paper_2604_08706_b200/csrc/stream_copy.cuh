@@ -128,7 +128,8 @@ __device__ __forceinline__ void row_to_packed_quads(const uint4* rowq, int nsq, 
 // quad k = funnel(src quad Q0+k, src quad Q0+k+1, a), a = soff & 3.
 // (lim = a + len: the valid elements counted from quad Q0's first element;
 // the last quad is read word by word, never past the caller's array)
-template <int U>
+// (BOUNDED = false: the caller knows quad nsq-1 ends inside its array)
+template <int U, bool BOUNDED = true>
 __device__ __forceinline__ void packed_to_row_quads(const uint4* srcq0 /* quad Q0 */, int nsq,
                                                     int a, int kw, uint4 (&o)[U], int lim) {
     const int lane = threadIdx.x & 31;
@@ -136,7 +137,8 @@ __device__ __forceinline__ void packed_to_row_quads(const uint4* srcq0 /* quad Q
 #pragma unroll
     for (int s = 0; s < U; ++s) {
         const int k = kw + 32 * s + lane;
-        cur[s] = (k < nsq) ? ld_stream_lim(srcq0, k, lim) : make_uint4(0, 0, 0, 0);
+        cur[s] = (k < nsq) ? (BOUNDED ? ld_stream_lim(srcq0, k, lim) : ld_stream(srcq0 + k))
+                           : make_uint4(0, 0, 0, 0);
     }
     if (a == 0) {
 #pragma unroll
@@ -145,7 +147,8 @@ __device__ __forceinline__ void packed_to_row_quads(const uint4* srcq0 /* quad Q
     }
     const int klast = kw + 32 * U;  // first quad after the warp's span
     uint4 last_next = make_uint4(0, 0, 0, 0);
-    if (lane == 31 && klast < nsq) last_next = ld_stream_lim(srcq0, klast, lim);
+    if (lane == 31 && klast < nsq)
+        last_next = BOUNDED ? ld_stream_lim(srcq0, klast, lim) : ld_stream(srcq0 + klast);
 #pragma unroll
     for (int s = 0; s < U; ++s) {
         uint4 next = shfl_down4(cur[s]);
