@@ -2311,33 +2311,48 @@ struct MaxPlus {
 __device__ __forceinline__ MaxPlus mp_then(MaxPlus x, MaxPlus y) {  // x first, then y
     return MaxPlus{x.a + y.a, max(x.b + y.a, y.b)};
 }
-// Block-wide exclusive scan of max-plus maps (identity {0, INT_MIN/2}).
-__device__ MaxPlus block_scan_mp(MaxPlus x) {
-    __shared__ int s_a[32], s_b[32];
+// Block-wide exclusive scan of max-plus maps (identity {0, INT_MIN/2}),
+// together with an exclusive sum of one int per thread (*cex; *ctot the total).
+__device__ MaxPlus block_scan_mp(MaxPlus x, int c, int* cex, int* ctot) {
+    __shared__ int s_a[32], s_b[32], s_c[32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     MaxPlus inc = x;
+    int ci = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const MaxPlus y{__shfl_up_sync(0xffffffffu, inc.a, o), __shfl_up_sync(0xffffffffu, inc.b, o)};
-        if (lane >= o) inc = mp_then(y, inc);
+        const int yc = __shfl_up_sync(0xffffffffu, ci, o);
+        if (lane >= o) {
+            inc = mp_then(y, inc);
+            ci += yc;
+        }
     }
     if (lane == 31) {
         s_a[wid] = inc.a;
         s_b[wid] = inc.b;
+        s_c[wid] = ci;
     }
     __syncthreads();
     if (wid == 0) {
         MaxPlus w = lane < nw ? MaxPlus{s_a[lane], s_b[lane]} : MaxPlus{0, INT_MIN / 2};
+        int wc = lane < nw ? s_c[lane] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const MaxPlus y{__shfl_up_sync(0xffffffffu, w.a, o), __shfl_up_sync(0xffffffffu, w.b, o)};
-            if (lane >= o) w = mp_then(y, w);
+            const int yc = __shfl_up_sync(0xffffffffu, wc, o);
+            if (lane >= o) {
+                w = mp_then(y, w);
+                wc += yc;
+            }
         }
         s_a[lane] = w.a;
         s_b[lane] = w.b;
+        s_c[lane] = wc;
     }
     __syncthreads();
     const MaxPlus base = wid ? MaxPlus{s_a[wid - 1], s_b[wid - 1]} : MaxPlus{0, INT_MIN / 2};
+    *cex = (wid ? s_c[wid - 1] : 0) + ci - c;
+    *ctot = s_c[nw - 1];
     // exclusive within the warp: the inclusive value of the lane before
     MaxPlus ex{__shfl_up_sync(0xffffffffu, inc.a, 1), __shfl_up_sync(0xffffffffu, inc.b, 1)};
     if (lane == 0) ex = MaxPlus{0, INT_MIN / 2};
@@ -2359,6 +2374,7 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
     const long long ng = in.ngroups;
     const int j0 = (int)(((long long)s - (long long)(cur0 % (unsigned long long)T)) % T + T) % T;
     const int ns = n > j0 ? (n - 1 - j0) / T + 1 : 0;
+    RB_TSTART(0);
     RB_GCLOCK(20, s == 0);
     // shared memory: preseq / preid [C] (i64), rings [3][RC], occb [C], per
     // push: vk, slotk, WE, QE (i32), cx, evw (u8)
@@ -2396,6 +2412,7 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
         }
     }
     const uint64_t id0 = n > 0 ? in.id[0] : 0;
+    const uint64_t idl = n > 0 ? in.id[n - 1] : 0;  // the buffer's new largest id
     __syncthreads();  // s_goff written
     // own records: lengths, advantages (frozen at insertion, bandit.cpp:276-294,
     // the reference's fp64 order), correctness — into the insert's own scratch
@@ -2426,6 +2443,7 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
     }
     // ---- the buffer's state
     pdl_wait();
+    RB_GCLOCK(29, s == 0);
     const int sticky = ctl->err_code;
     const int has_any = ctl->has_any;
     const unsigned long long max_id = ctl->max_id;
@@ -2505,7 +2523,8 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
             loc = mp_then(loc, MaxPlus{wr ? 0 : -1, 0});
             nwr += wr;
         }
-        const MaxPlus pre = block_scan_mp(loc);
+        int ew, tot_wr;  // wrong entries before k0, in all
+        const MaxPlus pre = block_scan_mp(loc, nwr, &ew, &tot_wr);
         int w = max(w0 + pre.a, pre.b);
         for (int k = k0; k < k1; ++k) {
             bool wr;
@@ -2515,8 +2534,7 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
             npw += pw;
             w = max(w + (wr ? 0 : -1), 0);
         }
-        long long tot_wr, tot_pw;
-        int ew = (int)block_exclusive_scan(nwr, &tot_wr);  // wrong entries before k0
+        long long tot_pw;
         int cw = (int)block_exclusive_scan(npw, &tot_pw);  // W pops before k0
         // 2. entries in order
         {
@@ -2727,8 +2745,19 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
         }
         v.pbs[s] = o;
         v.pushes[s] = P0 + ns;
-        if (s_maxq) atomicMax(&gc->cta_max[0], s_maxq);
-        if (done_add_u32(&gc->done) == (unsigned)T - 1) {
+        if (T == 1) {  // one CTA: no grid-wide counters
+            *in.n_units = s_maxq;
+            ctl->cursor = 0;
+            if (n > 0) {
+                ctl->max_id = idl;
+                ctl->has_any = 1;
+            }
+            ctl->hash_stale = 1;
+            RB_GCLOCK(28, true);
+        } else if (s_maxq) {
+            atomicMax(&gc->cta_max[0], s_maxq);
+        }
+        if (T > 1 && done_add_u32(&gc->done) == (unsigned)T - 1) {
             *in.n_units = atomicExch(&gc->cta_max[0], 0);
             ctl->cursor = (cur0 + (unsigned long long)n) % T;
             if (n > 0) {
@@ -2740,6 +2769,7 @@ __global__ void __launch_bounds__(PBP_THREADS) k_posbias_par(BufView v, InsertIn
             RB_GCLOCK(28, true);
         }
     }
+    RB_TEND(0);
 }
 
 // Record copies with the post-increment use count in draw order
