@@ -50,7 +50,10 @@ int rb_device_info(int* device, int* sm_count, int* cc_major, int* cc_minor);
 
 /* ---- enums (replay_buffer.hpp:17-46) ------------------------------------ */
 enum { RB_UNIFORM_WITH_REPLACEMENT = 0, RB_UNIFORM_WITHOUT_REPLACEMENT = 1,
-       RB_UNUSED_FIRST_WITHOUT_REPLACEMENT = 2 };
+       RB_UNUSED_FIRST_WITHOUT_REPLACEMENT = 2,
+       /* builder extension (no reference counterpart): per
+        * shard B/T draws with probability w_i / W, see rb_set_priority */
+       RB_PRIORITY_WITH_REPLACEMENT = 3 };
 enum { RB_PLAIN_FIFO = 0, RB_POSITIVE_BIAS = 1 };
 
 /* ---- record (rollout.hpp:13-31; same 80-byte layout) -------------------- */
@@ -308,6 +311,16 @@ int rb_record_tokens(rb_buffer* b, size_t shard, size_t index, int32_t* tokens,
                      float* logp_old, int32_t capacity, int32_t* n_tokens);
 int rb_strategy(const rb_buffer* b, int* out);
 int rb_retention(const rb_buffer* b, int* kind, double* delta);
+/* priority_with_replacement (builder extension; the reference's sampler is
+ * uniform, replay_buffer.cpp:135-182, and its "positive bias" is a retention
+ * rule).  Record weight w = base + floor(min(|advantage|, 2^15) * adv_scale)
+ * + pos_bonus * [reward > 0] (integers: the per-shard CDF is exact); each
+ * draw is index = upper_bound(cdf, rng.below(W)) over the shard's arrival
+ * order, shards in order, B/T draws each as rb_sample.  Defaults (1, 0, 0)
+ * reproduce uniform_with_replacement draw for draw.  base >= 1 (every
+ * record stays reachable), adv_scale <= 65536. */
+int rb_set_priority(rb_buffer* b, uint32_t base, uint32_t adv_scale, uint32_t pos_bonus);
+int rb_get_priority(const rb_buffer* b, uint32_t* base, uint32_t* adv_scale, uint32_t* pos_bonus);
 int rb_route_cursor(rb_buffer* b, size_t* out);
 
 /* dump/load (replay_buffer.cpp:238-324): byte-identical text format.

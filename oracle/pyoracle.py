@@ -31,7 +31,8 @@ RECORD_DTYPE = np.dtype(
 )
 
 STRATEGIES = {"uniform_with_replacement": 0, "uniform_without_replacement": 1,
-              "unused_first_without_replacement": 2}
+              "unused_first_without_replacement": 2,
+              "priority_with_replacement": 3}  # builder extension: oracle only
 
 
 def _p(a):
@@ -99,6 +100,7 @@ class Oracle:
         L.or_buf_free.argtypes = [vp]
         L.or_buf_push.argtypes = [vp, vp, vp, vp]
         L.or_buf_sample.argtypes = [vp, sz, vp, vp, vp, vp]
+        L.or_buf_set_priority.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint32]
         L.or_buf_size.restype = sz
         L.or_buf_size.argtypes = [vp]
         L.or_buf_shard_size.restype = sz
@@ -305,6 +307,10 @@ class OracleBuffer:
         if self.o.lib.or_buf_push(self.h, _p(r), _p(ev), C.byref(has)):
             raise self.o.err()
         return ev[0] if has.value else None
+
+    def set_priority(self, base=1, adv_scale=0, pos_bonus=0):
+        if self.o.lib.or_buf_set_priority(self.h, int(base), int(adv_scale), int(pos_bonus)):
+            raise self.o.err()
 
     def sample(self, batch, rng: OracleRng):
         out = records(batch)

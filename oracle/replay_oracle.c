@@ -157,6 +157,7 @@ struct or_buffer {
     size_t total_capacity, shard_capacity, num_shards, route_cursor;
     int strategy, retention;
     double delta;
+    uint32_t prio_base, prio_adv_scale, prio_pos_bonus; /* priority_with_replacement */
     or_shard* shards;
     or_idset ids;
 };
@@ -210,6 +211,7 @@ or_buffer* or_buf_new(size_t num_shards, size_t total_capacity, int strategy, in
     b->total_capacity = total_capacity;
     b->shard_capacity = total_capacity / num_shards;
     b->strategy = strategy;
+    b->prio_base = 1;
     b->retention = retention;
     b->delta = retention == OR_POSITIVE_BIAS ? delta : 0.0;
     b->shards = (or_shard*)calloc(num_shards, sizeof(or_shard));
@@ -288,6 +290,25 @@ int or_buf_push(or_buffer* b, const or_record* rec, or_record* evicted, int* has
     return OR_OK;
 }
 
+/* priority_with_replacement (builder extension, no reference counterpart;
+ * include/replay_b200.h rb_set_priority): integer weight of one record. */
+static uint64_t prio_weight(const or_buffer* b, const or_record* r) {
+    double a = fabs(r->advantage);
+    if (!(a <= 32768.0)) a = a > 32768.0 ? 32768.0 : 0.0; /* clamp; NaN -> 0 */
+    uint64_t w = (uint64_t)b->prio_base + (uint64_t)(a * (double)b->prio_adv_scale);
+    if (b->prio_pos_bonus != 0 && r->reward > 0.0) w += b->prio_pos_bonus;
+    return w;
+}
+
+int or_buf_set_priority(or_buffer* b, uint32_t base, uint32_t adv_scale, uint32_t pos_bonus) {
+    if (base == 0) return fail("rb_set_priority: base weight must be >= 1");
+    if (adv_scale > 65536u) return fail("rb_set_priority: adv_scale must be <= 65536");
+    b->prio_base = base;
+    b->prio_adv_scale = adv_scale;
+    b->prio_pos_bonus = pos_bonus;
+    return OR_OK;
+}
+
 /* replay_buffer.cpp:135-182 pick_indices; returns count written */
 static int pick_indices(const or_buffer* b, const or_shard* sh, size_t k, or_rng* rng,
                         uint64_t* picks) {
@@ -297,6 +318,28 @@ static int pick_indices(const or_buffer* b, const or_shard* sh, size_t k, or_rng
             int st = or_rng_below(rng, n, &picks[i]);
             if (st) return st;
         }
+        return OR_OK;
+    }
+    if (b->strategy == OR_PRIORITY_WITH) { /* the 141-145 loop over a weighted CDF */
+        uint64_t* cdf = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+        uint64_t W = 0;
+        for (size_t i = 0; i < n; ++i) cdf[i] = (W += prio_weight(b, &sh->rec[i]));
+        for (size_t i = 0; i < k; ++i) {
+            uint64_t x;
+            int st = or_rng_below(rng, W, &x);
+            if (st) {
+                free(cdf);
+                return st;
+            }
+            size_t lo = 0, hi = n; /* upper_bound: first i with cdf[i] > x */
+            while (lo < hi) {
+                const size_t mid = (lo + hi) / 2;
+                if (cdf[mid] > x) hi = mid;
+                else lo = mid + 1;
+            }
+            picks[i] = lo;
+        }
+        free(cdf);
         return OR_OK;
     }
     if (k > n) {

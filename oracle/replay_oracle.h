@@ -59,7 +59,7 @@ typedef struct or_record {
 } or_record;
 
 /* ---- replay_buffer.hpp / replay_buffer.cpp ------------------------------ */
-enum { OR_UNIFORM_WITH = 0, OR_UNIFORM_WITHOUT = 1, OR_UNUSED_FIRST = 2 };
+enum { OR_UNIFORM_WITH = 0, OR_UNIFORM_WITHOUT = 1, OR_UNUSED_FIRST = 2, OR_PRIORITY_WITH = 3 };
 enum { OR_FIFO = 0, OR_POSITIVE_BIAS = 1 };
 enum { OR_OK = 0, OR_INVALID = 1 };
 
@@ -73,6 +73,8 @@ void or_buf_free(or_buffer* b);
 int or_buf_push(or_buffer* b, const or_record* rec, or_record* evicted, int* has_evicted);
 /* replay_buffer.cpp:135-217.  out_shard/out_index may be NULL.  On error the
  * shards before the failing one are already mutated (as in the reference).  */
+/* priority_with_replacement weights (builder extension; rb_set_priority) */
+int or_buf_set_priority(or_buffer* b, uint32_t base, uint32_t adv_scale, uint32_t pos_bonus);
 int or_buf_sample(or_buffer* b, size_t batch, or_rng* rng, or_record* out, int64_t* out_shard,
                   int64_t* out_index);
 size_t or_buf_size(const or_buffer* b);

@@ -16,7 +16,9 @@ RB_OK, RB_EINVAL, RB_ELOGIC, RB_ECUDA, RB_ENOMEM = range(5)
 RB_INSERT_ASSUME_UNIQUE = 1
 
 STRATEGIES = {"uniform_with_replacement": 0, "uniform_without_replacement": 1,
-              "unused_first_without_replacement": 2}
+              "unused_first_without_replacement": 2,
+              # builder extension (include/replay_b200.h RB_PRIORITY_WITH_REPLACEMENT)
+              "priority_with_replacement": 3}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 RETENTIONS = {"plain_fifo": 0, "positive_bias": 1}
 # GRPO normalisation modes (include/replay_b200.h RB_GRPO_*)
@@ -121,6 +123,8 @@ def _load():
         "rb_record_tokens": (ip, [vp, sz, sz, vp, vp, i32, vp]),
         "rb_strategy": (ip, [vp, vp]),
         "rb_retention": (ip, [vp, vp, vp]),
+        "rb_set_priority": (ip, [vp, C.c_uint32, C.c_uint32, C.c_uint32]),
+        "rb_get_priority": (ip, [vp, vp, vp, vp]),
         "rb_route_cursor": (ip, [vp, vp]),
         "rb_dump": (ip, [vp, C.c_char_p, sz, vp]),
         "rb_load": (ip, [C.c_char_p, i32, ip, vp]),

@@ -1927,6 +1927,104 @@ __global__ void k_sample_without(BufView v, MtRing* r, SampleArgs a, int strateg
     ring_store_state(r, mt, q0, s_tw, s_idx, s_draws);
 }
 
+// priority_with_replacement (builder extension, no reference counterpart;
+// SURVEY.md §8e): per shard, in shard order, `per` draws with probability
+// w_i / W over the arrival indices, w_i = prio_weight (integer, so the CDF is
+// exact and order-independent), each draw x = below(W) with the reference's
+// rejection rule (rng.cpp:40-51) and index = upper_bound(cdf, x).  With every
+// weight 1 it is pick_indices' uniform_with_replacement (replay_buffer.cpp:
+// 141-145) draw for draw.  One CTA: the CDF is a block scan in chunks, the
+// draws take one MT word per thread (a block scan of the accept flags ranks
+// them, so a rejected word shifts the later draws exactly as the serial
+// loop does), then one binary search per draw over the CDF (L2-resident).
+constexpr int PR_THREADS = 512;
+__device__ __forceinline__ unsigned long long prio_weight(const BufView& v, size_t g,
+                                                          const PrioParams& p) {
+    double a = fabs(v.adv[g]);
+    if (!(a <= 32768.0)) a = a > 32768.0 ? 32768.0 : 0.0;  // clamp; NaN -> 0
+    unsigned long long w = (unsigned long long)p.base +
+                           (unsigned long long)__dmul_rn(a, (double)p.adv_scale);
+    if (p.pos_bonus != 0 && v.reward[g] > 0.0) w += p.pos_bonus;
+    return w;
+}
+// CDF of up to PR_SMEM_CDF records in dynamic shared memory (the searches
+// are then shared-memory round trips), else in global scratch.
+constexpr int PR_SMEM_CDF = 24576;  // 192 KB
+__global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r, SampleArgs a,
+                                                            PrioParams p,
+                                                            unsigned long long* g_cdf /* >= C */,
+                                                            int cdf_in_smem) {
+    extern __shared__ unsigned long long s_cdf[];
+    __shared__ uint64_t mt[MT_N];
+    __shared__ int s_consumed;
+    unsigned long long* cdf = cdf_in_smem ? s_cdf : g_cdf;
+    const long long q0 = r->q_state;
+    ring_load_block(r, q0, mt);
+    uint32_t idx = r->idx;  // block-uniform copies
+    uint64_t draws = r->draws;
+    long long tw = 0, pos = 0;
+    for (int s = 0; s < a.nsh; ++s) {
+        const long long n = occupancy(v, s), k = a.per;
+        const int head = shard_head(v, s);
+        // weights in arrival order (oldest first), coalesced, 8 loads in flight
+#pragma unroll 8
+        for (long long i = threadIdx.x; i < n; i += PR_THREADS)
+            cdf[i] = prio_weight(v, (size_t)s * v.C + arrival_slot_h(v, s, i, head), p);
+        __syncthreads();
+        // inclusive scan: a contiguous run per thread, one block scan of the run sums
+        const long long per = (n + PR_THREADS - 1) / PR_THREADS;
+        const long long i0 = threadIdx.x * per, i1 = i0 + per < n ? i0 + per : n;
+        long long run = 0;
+        for (long long i = i0; i < i1; ++i) run += (long long)cdf[i];
+        long long W;
+        long long acc = block_exclusive_scan(run, &W);
+        for (long long i = i0; i < i1; ++i) {
+            acc += (long long)cdf[i];
+            cdf[i] = (unsigned long long)acc;
+        }
+        __syncthreads();
+        const uint64_t lim = below_limit((uint64_t)W);
+        long long got = 0;
+        while (got < k) {
+            if (idx >= MT_N) {
+                mt_twist_block(mt);
+                __syncthreads();
+                idx = 0;
+                ++tw;
+            }
+            const int avail = MT_N - (int)idx;
+            const int t = threadIdx.x;
+            uint64_t x = 0;
+            const bool ok = t < avail && (x = mt_temper(mt[idx + t])) < lim;
+            long long nacc;
+            const long long rank = block_exclusive_scan(ok ? 1 : 0, &nacc);
+            const long long need = k - got;
+            if (threadIdx.x == 0) s_consumed = avail;
+            __syncthreads();
+            if (ok && rank == need - 1) s_consumed = t + 1;  // the last word this shard needs
+            if (ok && rank < need) {
+                const uint64_t xr = x % (uint64_t)W;
+                long long lo = 0, hi = n;
+                while (lo < hi) {  // upper_bound: first i with cdf[i] > xr
+                    const long long mid = (lo + hi) >> 1;
+                    if (cdf[mid] > xr) hi = mid;
+                    else lo = mid + 1;
+                }
+                a.sel_shard[pos + got + rank] = s;
+                a.sel_index[pos + got + rank] = lo;
+            }
+            __syncthreads();
+            const int used = s_consumed;
+            idx += (uint32_t)used;
+            draws += (uint64_t)used;
+            got += nacc < need ? nacc : need;
+            __syncthreads();
+        }
+        pos += k;
+    }
+    ring_store_state(r, mt, q0, tw, idx, draws);
+}
+
 // ---------------------------------------------------------------- FIFO route
 // FIFO routing + eviction + group advantages + metadata scatter for ids
 // promised new and increasing (replay_buffer.cpp:83-133 in closed form;
@@ -3352,6 +3450,7 @@ std::string strategy_name(int s) {
         case RB_UNIFORM_WITH_REPLACEMENT: return "uniform_with_replacement";
         case RB_UNIFORM_WITHOUT_REPLACEMENT: return "uniform_without_replacement";
         case RB_UNUSED_FIRST_WITHOUT_REPLACEMENT: return "unused_first_without_replacement";
+        case RB_PRIORITY_WITH_REPLACEMENT: return "priority_with_replacement";
     }
     throw Error(RB_ELOGIC, "bad SamplingStrategy");
 }
@@ -3364,7 +3463,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         invalid("ShardedReplayBuffer: capacity must be a positive multiple of the shard count");
     if (retention == RB_POSITIVE_BIAS && !(delta >= 0.0 && delta <= 1.0))
         invalid("RetentionPolicy: delta must be in [0, 1]");
-    if (strategy < 0 || strategy > 2) throw Error(RB_ELOGIC, "bad SamplingStrategy");
+    if (strategy < 0 || strategy > 3) throw Error(RB_ELOGIC, "bad SamplingStrategy");
     if (max_tokens < 0) invalid("rb_create: max_tokens must be >= 0");
     if (sb == 0 && se == 0) se = T;
     if (sb >= se || se > T) invalid("rb_create: bad owned shard range");
@@ -4071,7 +4170,9 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 err = "ShardedReplayBuffer: cannot sample from an empty shard";
                 break;
             }
-            if (b->strategy != RB_UNIFORM_WITH_REPLACEMENT && (long long)per > occ) {
+            const bool without = b->strategy == RB_UNIFORM_WITHOUT_REPLACEMENT ||
+                                 b->strategy == RB_UNUSED_FIRST_WITHOUT_REPLACEMENT;
+            if (without && (long long)per > occ) {
                 nsh = s;
                 err = "ShardedReplayBuffer: batch exceeds shard occupancy for sampling without "
                       "replacement";
@@ -4168,7 +4269,20 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
             b->seg_used = a.early ? (int)nmap : 0;
         } else {
             MtRing* ring = rng->to_device(b->stream);
-            if (nsh > 0) {
+            if (nsh > 0 && b->strategy == RB_PRIORITY_WITH_REPLACEMENT) {
+                const bool sm = b->C <= (size_t)PR_SMEM_CDF;
+                const size_t smem = sm ? b->C * sizeof(unsigned long long) : 0;
+                auto* cdf = sm ? nullptr
+                               : (unsigned long long*)b->scratch(b->C * sizeof(unsigned long long) + 16);
+                static bool attr_set = false;  // per process; the attribute is per function
+                if (!attr_set) {
+                    RB_CUDA(cudaFuncSetAttribute(k_sample_prio, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)(PR_SMEM_CDF * sizeof(unsigned long long))));
+                    attr_set = true;
+                }
+                k_sample_prio<<<1, PR_THREADS, smem, b->stream>>>(b->v, ring, a, b->prio, cdf, sm ? 1 : 0);
+                RB_CUDA(cudaGetLastError());
+            } else if (nsh > 0) {
                 int64_t* scr = (int64_t*)b->scratch(2 * b->C * sizeof(int64_t) + 16);
                 k_sample_without<<<1, 32, 0, b->stream>>>(b->v, ring, a, b->strategy, scr);
                 RB_CUDA(cudaGetLastError());
@@ -4537,6 +4651,21 @@ int rb_record_tokens(rb_buffer* b, size_t shard, size_t index, int32_t* tokens,
 
 int rb_strategy(const rb_buffer* b, int* out) {
     *out = b->strategy;
+    return RB_OK;
+}
+// priority_with_replacement weights (builder extension; k_sample_prio).
+int rb_set_priority(rb_buffer* b, uint32_t base, uint32_t adv_scale, uint32_t pos_bonus) {
+    return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);
+        if (base == 0) invalid("rb_set_priority: base weight must be >= 1");
+        if (adv_scale > 65536u) invalid("rb_set_priority: adv_scale must be <= 65536");
+        b->prio = rb::PrioParams{base, adv_scale, pos_bonus};
+    });
+}
+int rb_get_priority(const rb_buffer* b, uint32_t* base, uint32_t* adv_scale, uint32_t* pos_bonus) {
+    *base = b->prio.base;
+    *adv_scale = b->prio.adv_scale;
+    *pos_bonus = b->prio.pos_bonus;
     return RB_OK;
 }
 int rb_retention(const rb_buffer* b, int* kind, double* delta) {
@@ -4917,6 +5046,7 @@ extern "C" int rb_load(const char* text, int32_t max_tokens, int device, rb_buff
         if (sname == "uniform_with_replacement") strategy = 0;
         else if (sname == "uniform_without_replacement") strategy = 1;
         else if (sname == "unused_first_without_replacement") strategy = 2;
+        else if (sname == "priority_with_replacement") strategy = 3;
         else invalid("unknown sampling strategy: '" + std::string(sname) + "'");
         const std::string_view rname = header_value(lines[4], "retention");
         int retention = RB_PLAIN_FIFO;

@@ -66,6 +66,12 @@ struct BufView {
     DevCtl* ctl;
 };
 
+// priority_with_replacement weights (rb_set_priority): w = base +
+// floor(min(|advantage|, 2^15) * adv_scale) + pos_bonus * [reward > 0].
+struct PrioParams {
+    uint32_t base, adv_scale, pos_bonus;
+};
+
 int loss_grid(int sms);
 struct GridCtl;  // buffer.cu: multi-CTA bookkeeping
 struct PendingIns {
@@ -90,6 +96,7 @@ struct rb_buffer {
     std::recursive_mutex mu;
     size_t T = 0, N = 0, C = 0;
     int strategy = 0, retention = 0;
+    rb::PrioParams prio{1, 0, 0};  // priority_with_replacement weights
     double delta = 0.0;
     int32_t max_tokens = 0, stride = 0;
     int device = 0;

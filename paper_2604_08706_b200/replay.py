@@ -225,6 +225,18 @@ class ShardedReplayBuffer:
         check(lib.rb_retention(self._h, C.byref(k), C.byref(d)))
         return ("plain_fifo" if k.value == 0 else "positive_bias", d.value)
 
+    def set_priority(self, base: int = 1, adv_scale: int = 0, pos_bonus: int = 0) -> None:
+        """Weights of the priority_with_replacement strategy (builder extension,
+        include/replay_b200.h rb_set_priority): w = base + floor(min(|A|, 2^15) *
+        adv_scale) + pos_bonus * [reward > 0]; (1, 0, 0) draws exactly as
+        uniform_with_replacement (replay_buffer.cpp:141-145)."""
+        check(lib.rb_set_priority(self._h, int(base), int(adv_scale), int(pos_bonus)))
+
+    def priority(self):
+        b, a, p = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        check(lib.rb_get_priority(self._h, C.byref(b), C.byref(a), C.byref(p)))
+        return b.value, a.value, p.value
+
     def set_stream(self, stream) -> None:
         """Enqueue on an external stream (int handle, e.g. torch.cuda.current_stream().cuda_stream)."""
         check(lib.rb_set_stream(self._h, C.c_void_p(stream)))

@@ -42,6 +42,7 @@ class StepConfig:
     assume_unique: bool = False  # RB_INSERT_ASSUME_UNIQUE (closed-form FIFO insert kernels)
     overlap: bool = False        # no host sync between insert and sample (evicted ids to the device)
     early_gather: bool = False   # sample with no host outputs, gather right away (overlapped gather)
+    priority: tuple | None = None  # (base, adv_scale, pos_bonus) of priority_with_replacement
 
     @property
     def per_step(self):
@@ -130,6 +131,9 @@ def run_step_parity(cfg: StepConfig, steps: int, ora: Oracle | None = None, chec
     if dev:  # inputs are copied to the device on torch's stream: run the library on it too
         gbuf.set_stream(torch.cuda.current_stream().cuda_stream)
     obuf = ora.buffer(cfg.shards, cfg.capacity, cfg.strategy, cfg.retention, cfg.delta)
+    if cfg.priority is not None:
+        gbuf.set_priority(*cfg.priority)
+        obuf.set_priority(*cfg.priority)
     grng = Rng(cfg.seed).stream("buffer_sampling")
     orng = ora.rng(cfg.seed).stream("buffer_sampling")
     prod = Producer(cfg, ora)
