@@ -56,6 +56,11 @@ CONFIGS = {
                capacity=84, batch=512, group=8, lmax=1024, ragged=False,
                retention="positive_bias", delta=0.5, loss="asymre"),
 }
+# C4 with the prioritised-sampling CDF (builder extension, include/replay_b200.h
+# rb_set_priority): w = 1 + floor(4096 |A|) + 4096 [reward > 0]
+CONFIGS["c4prio"] = dict(CONFIGS["c4"], name=CONFIGS["c4"]["name"].replace(
+    "uniform with replacement", "priority_with_replacement (w = 1 + 4096|A| + 4096[r > 0])"),
+    strategy="priority_with_replacement", priority=(1, 4096, 4096))
 W_WORKERS, T_TRAINERS, MU, SEED = 5, 3, 5.28, 1
 EPS_LOW, EPS_HIGH, DELTA_V = 0.2, 0.2, -0.1
 
@@ -275,6 +280,7 @@ def config_dict(cfg, world):
     return {"workload": cfg["name"], "buffer": cfg["capacity"], "shards": world,
             "batch": cfg["batch"], "group": cfg["group"], "tokens_per_traj": cfg["lmax"],
             "ragged": cfg["ragged"], "retention": cfg["retention"], "delta": cfg["delta"],
+            "sampling": cfg.get("strategy", "uniform_with_replacement"),
             "W": W_WORKERS, "T": T_TRAINERS, "mu": MU, "loss": cfg["loss"],
             "l2": "inputs larger than L2 (buffer + per-step traffic >> 126 MB); the trainer "
                   "stand-in ends with a 256 MB read, so the loss reads logp_now from HBM",
@@ -293,8 +299,11 @@ def run_ours(args, rank, world, dist):
     sh = stream.cuda_stream
     T, N, B = world, cfg["capacity"], cfg["batch"]
     assert N % T == 0 and B % T == 0, "config not divisible by the GPU count"
-    buf = rb.ShardedReplayBuffer(T, N, "uniform_with_replacement", cfg["retention"], cfg["delta"],
+    buf = rb.ShardedReplayBuffer(T, N, cfg.get("strategy", "uniform_with_replacement"),
+                                 cfg["retention"], cfg["delta"],
                                  max_tokens=cfg["lmax"], shard_range=(rank, rank + 1))
+    if cfg.get("priority"):
+        buf.set_priority(*cfg["priority"])
     buf.set_stream(sh)
     rng = rb.Rng(SEED).stream("buffer_sampling")
     K, Wm = args.steps, args.warmup
@@ -545,7 +554,10 @@ def parity_check(cfg, wl, nsteps, buf, rank, world, packed_tok, lpn, dlogp, stat
     t0 = time.perf_counter()
     ora = Oracle()
     T, N, B, G = world, cfg["capacity"], cfg["batch"], cfg["group"]
-    ob = ora.buffer(T, N, "uniform_with_replacement", cfg["retention"], cfg["delta"])
+    ob = ora.buffer(T, N, cfg.get("strategy", "uniform_with_replacement"), cfg["retention"],
+                    cfg["delta"])
+    if cfg.get("priority"):
+        ob.set_priority(*cfg["priority"])
     orng = ora.rng(SEED).stream("buffer_sampling")
     gmean_of = {}
 
@@ -637,7 +649,10 @@ def launches_per_step(cfg, world):
     k_insert_payload, k_sample_fused, k_gather, loss; + k_finalize_vec
     (rb_loss_finalize_vec / rb_allreduce_loss_stats, whose NCCL kernel is not
     ours) per step on more than one rank; + k_ring_lookahead above 8192 draws
-    per call."""
+    per call.  priority_with_replacement: k_sample_prio + k_sample_map in place
+    of k_sample_fused (and no ring lookahead)."""
+    if cfg.get("strategy") == "priority_with_replacement":
+        return 6 + (1 if world > 1 else 0)
     n = 5
     return n + (1 if world > 1 else 0) + (1 if cfg["batch"] > 8192 else 0)
 
@@ -1007,6 +1022,10 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
+        if cfg.get("strategy", "uniform_with_replacement") == "priority_with_replacement":
+            print(json.dumps({"impl": "reference", "unavailable": "the reference has no "
+                              "prioritised sampler (replay_buffer.cpp:135-182 is uniform)"}))
+            return
         # bounded sample of the same job's steps (at most ~90 s of timed
         # steps); N shards for an N-GPU job, like our arm
         r = cpu_reference(cfg, args.steps, args.warmup, shards=world)
@@ -1061,7 +1080,8 @@ def main():
     if emulated:
         res["emulated"] = (f"rank 0 of a {world}-GPU job alone on one GPU, no collective: "
                            "a prediction of the N-GPU step, not a measurement")
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if (rank == 0 and world == 1 and not args.no_cpu_baseline
+            and cfg.get("strategy", "uniform_with_replacement") != "priority_with_replacement"):
         try:
             r = cpu_reference(cfg, args.cpu_steps, 1)
             res["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": r["cores"],

@@ -1152,6 +1152,7 @@ struct SampleArgs {
     const long long* occ_dev;  // the same for more than 64 shards (device), else NULL
     const int* verdict;       // the pending insert's whole-batch verdict (1 valid, 2 rejected)
     int own_only;             // owned-metadata buffer: map (use counts, lengths, totals) only [lo, hi)
+    int chk_frozen;           // k_sample_map after k_sample_prio: a sticky error freezes it too
 };
 
 // A rejected insert leaves a sticky error and freezes the buffer until
@@ -1459,7 +1460,7 @@ __device__ void map_cta(const BufView& v, const SampleArgs& a, GridCtl* gc, int 
     }
     __syncthreads();
     RB_GCLOCK(44 + 8 * (t & 1), t < 2);
-    if (DRAW) {
+    if (DRAW || a.chk_frozen) {
         __shared__ int s_frozen;
         if (tid == 0) s_frozen = sampler_frozen(v, a);
         __syncthreads();
@@ -1611,7 +1612,7 @@ __device__ void map_finalize(const BufView& v, const SampleArgs& a, GridCtl* gc,
     const long long D = a.nsel;
     const long long nloc = a.hi - a.lo;
     __shared__ int s_frozen;
-    if (threadIdx.x == 0) s_frozen = DRAW ? sampler_frozen(v, a) : 0;  // final: a map CTA waited for it
+    if (threadIdx.x == 0) s_frozen = (DRAW || a.chk_frozen) ? sampler_frozen(v, a) : 0;  // final: a map CTA waited for it
     __syncthreads();
     const bool frozen = s_frozen != 0;
     if (frozen) {  // a rejected insert before this sampler: empty batch, ring position unchanged
@@ -1937,7 +1938,7 @@ __global__ void k_sample_without(BufView v, MtRing* r, SampleArgs a, int strateg
 // draws take one MT word per thread (a block scan of the accept flags ranks
 // them, so a rejected word shifts the later draws exactly as the serial
 // loop does), then one binary search per draw over the CDF (L2-resident).
-constexpr int PR_THREADS = 512;
+constexpr int PR_THREADS = 1024;
 __device__ __forceinline__ unsigned long long prio_weight(const BufView& v, size_t g,
                                                           const PrioParams& p) {
     double a = fabs(v.adv[g]);
@@ -1948,21 +1949,45 @@ __device__ __forceinline__ unsigned long long prio_weight(const BufView& v, size
     return w;
 }
 // CDF of up to PR_SMEM_CDF records in dynamic shared memory (the searches
-// are then shared-memory round trips), else in global scratch.
+// are then shared-memory round trips), else in global scratch.  The draws
+// read MT words from the stream's ring (the Rng's twisted-ahead blocks);
+// missing blocks are twisted into the ring by the whole CTA a chunk ahead
+// (ring_extend: a one-warp twist chain was 3/4 of the kernel at 14 blocks).  A chunk is PR_R consecutive words per
+// thread: the accept flags (x < below_limit(W)) are ranked by one block
+// scan, so a rejected word shifts the later draws exactly as rng.cpp:40-51's
+// loop does.
 constexpr int PR_SMEM_CDF = 24576;  // 192 KB
+constexpr int PR_R = 4;
+constexpr long long PR_CH = (long long)PR_THREADS * PR_R;  // words per chunk
+template <bool SM>
 __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r, SampleArgs a,
                                                             PrioParams p,
-                                                            unsigned long long* g_cdf /* >= C */,
-                                                            int cdf_in_smem) {
+                                                            unsigned long long* g_cdf /* >= C */) {
     extern __shared__ unsigned long long s_cdf[];
-    __shared__ uint64_t mt[MT_N];
-    __shared__ int s_consumed;
-    unsigned long long* cdf = cdf_in_smem ? s_cdf : g_cdf;
+    __shared__ uint64_t s_mt[MT_N];
+    __shared__ long long s_consumed;
+    unsigned long long* cdf = SM ? s_cdf : g_cdf;
+    // a rejected asynchronous insert before this call (sticky error): no
+    // draws, the stream position unchanged; k_sample_map (chk_frozen) maps
+    // an empty batch, as the fused uniform sampler does
+    if (*(volatile const int*)&v.ctl->err_code != 0) {
+        for (long long i = threadIdx.x; i < a.nsel; i += PR_THREADS) {  // in-range, never mapped
+            a.sel_shard[i] = 0;
+            a.sel_index[i] = 0;
+        }
+        return;
+    }
     const long long q0 = r->q_state;
-    ring_load_block(r, q0, mt);
-    uint32_t idx = r->idx;  // block-uniform copies
-    uint64_t draws = r->draws;
-    long long tw = 0, pos = 0;
+    const uint32_t idx0 = r->idx;
+    const uint64_t draws0 = r->draws;
+    long long qhi = r->q_hi;  // block-uniform: twisted blocks are [q0, qhi]
+    long long o = 0, pos = 0;  // words consumed past (q0, idx0); selections written
+    // ring block holding word o + d (d < PR_CH), capped to what the ring holds
+    auto chunk_target = [&](long long oo) {
+        const long long first = q0 + ((long long)idx0 + oo) / MT_N;
+        const long long last = q0 + ((long long)idx0 + oo + PR_CH - 1) / MT_N;
+        return last < first + MT_KR - 1 ? last : first + MT_KR - 1;
+    };
     for (int s = 0; s < a.nsh; ++s) {
         const long long n = occupancy(v, s), k = a.per;
         const int head = shard_head(v, s);
@@ -1986,43 +2011,76 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
         const uint64_t lim = below_limit((uint64_t)W);
         long long got = 0;
         while (got < k) {
-            if (idx >= MT_N) {
-                mt_twist_block(mt);
-                __syncthreads();
-                idx = 0;
-                ++tw;
+            const long long tgt = chunk_target(o);
+            if (tgt > qhi) {
+                ring_extend(r, s_mt, qhi, tgt);  // ends with a CTA barrier
+                qhi = tgt;
             }
-            const int avail = MT_N - (int)idx;
-            const int t = threadIdx.x;
-            uint64_t x = 0;
-            const bool ok = t < avail && (x = mt_temper(mt[idx + t])) < lim;
+            const long long ow = o + (long long)threadIdx.x * PR_R;
+            uint64_t x[PR_R];
+            unsigned okm = 0;
+#pragma unroll
+            for (int j = 0; j < PR_R; ++j) {
+                const long long gw = (long long)idx0 + ow + j;
+                const long long q = q0 + gw / MT_N;
+                x[j] = mt_temper(__ldcg(&r->blk[q % MT_KR][gw % MT_N]));
+                if (x[j] < lim) okm |= 1u << j;
+            }
+            const int cnt = __popc(okm);
             long long nacc;
-            const long long rank = block_exclusive_scan(ok ? 1 : 0, &nacc);
+            long long rank = block_exclusive_scan(cnt, &nacc);
             const long long need = k - got;
-            if (threadIdx.x == 0) s_consumed = avail;
+            if (threadIdx.x == 0) s_consumed = PR_CH;
             __syncthreads();
-            if (ok && rank == need - 1) s_consumed = t + 1;  // the last word this shard needs
-            if (ok && rank < need) {
-                const uint64_t xr = x % (uint64_t)W;
-                long long lo = 0, hi = n;
-                while (lo < hi) {  // upper_bound: first i with cdf[i] > xr
-                    const long long mid = (lo + hi) >> 1;
-                    if (cdf[mid] > xr) hi = mid;
-                    else lo = mid + 1;
+            // the PR_R searches advance level by level together (ILP)
+            long long lo[PR_R], hi[PR_R];
+            uint64_t xr[PR_R];
+#pragma unroll
+            for (int j = 0; j < PR_R; ++j) {
+                const bool ok = (okm >> j) & 1u;
+                if (ok && rank == need - 1) s_consumed = (long long)threadIdx.x * PR_R + j + 1;
+                const bool take = ok && rank < need;
+                lo[j] = 0;
+                hi[j] = take ? n : 0;
+                xr[j] = take ? x[j] % (uint64_t)W : 0;
+                rank += ok ? 1 : 0;
+            }
+            for (long long span = n; span > 0; span >>= 1) {  // ceil(log2(n + 1)) levels
+#pragma unroll
+                for (int j = 0; j < PR_R; ++j) {
+                    if (lo[j] < hi[j]) {  // upper_bound: first i with cdf[i] > xr
+                        const long long mid = (lo[j] + hi[j]) >> 1;
+                        if (cdf[mid] > xr[j]) hi[j] = mid;
+                        else lo[j] = mid + 1;
+                    }
                 }
-                a.sel_shard[pos + got + rank] = s;
-                a.sel_index[pos + got + rank] = lo;
+            }
+            rank -= cnt;
+#pragma unroll
+            for (int j = 0; j < PR_R; ++j) {
+                const bool ok = (okm >> j) & 1u;
+                if (ok && rank < need) {
+                    a.sel_shard[pos + got + rank] = s;
+                    a.sel_index[pos + got + rank] = lo[j];
+                }
+                rank += ok ? 1 : 0;
             }
             __syncthreads();
-            const int used = s_consumed;
-            idx += (uint32_t)used;
-            draws += (uint64_t)used;
+            o += s_consumed;
             got += nacc < need ? nacc : need;
             __syncthreads();
         }
         pos += k;
     }
-    ring_store_state(r, mt, q0, tw, idx, draws);
+    if (threadIdx.x == 0) {
+        long long q = q0;
+        uint32_t idx = idx0;
+        ring_advance(q, idx, (unsigned long long)o);
+        r->q_state = q;
+        r->q_hi = qhi > q ? qhi : q;
+        r->idx = idx;
+        r->draws = draws0 + (uint64_t)o;
+    }
 }
 
 // ---------------------------------------------------------------- FIFO route
@@ -4158,7 +4216,9 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         // error): the fused sampler checks that itself (it freezes, applying
         // nothing); the serial without-replacement path, which sizes its
         // draws from the host mirrors, checks first.
-        if (b->strategy != RB_UNIFORM_WITH_REPLACEMENT && b->async_unchecked) check_sticky(b);
+        if (b->strategy != RB_UNIFORM_WITH_REPLACEMENT &&
+            b->strategy != RB_PRIORITY_WITH_REPLACEMENT && b->async_unchecked)
+            check_sticky(b);
         // The reference fails at the first empty (197-199) or too-small
         // (148-150, without replacement) shard after mutating earlier shards.
         size_t nsh = T;
@@ -4200,6 +4260,7 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         a.n_units = b->n_units_sel;
         a.verdict = b->pay_sync;
         a.own_only = b->owned_meta ? 1 : 0;
+        a.chk_frozen = b->strategy == RB_PRIORITY_WITH_REPLACEMENT ? 1 : 0;
         if (b->owned_meta && b->strategy != RB_UNIFORM_WITH_REPLACEMENT)
             throw Error(RB_ELOGIC, "owned-metadata buffers sample uniformly with replacement");
         const unsigned nmap = (unsigned)std::max<size_t>(1, (nsel + MAP_SPC - 1) / MAP_SPC);
@@ -4276,11 +4337,14 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                                : (unsigned long long*)b->scratch(b->C * sizeof(unsigned long long) + 16);
                 static bool attr_set = false;  // per process; the attribute is per function
                 if (!attr_set) {
-                    RB_CUDA(cudaFuncSetAttribute(k_sample_prio, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    RB_CUDA(cudaFuncSetAttribute(k_sample_prio<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)(PR_SMEM_CDF * sizeof(unsigned long long))));
                     attr_set = true;
                 }
-                k_sample_prio<<<1, PR_THREADS, smem, b->stream>>>(b->v, ring, a, b->prio, cdf, sm ? 1 : 0);
+                if (sm)
+                    k_sample_prio<true><<<1, PR_THREADS, smem, b->stream>>>(b->v, ring, a, b->prio, cdf);
+                else
+                    k_sample_prio<false><<<1, PR_THREADS, 0, b->stream>>>(b->v, ring, a, b->prio, cdf);
                 RB_CUDA(cudaGetLastError());
             } else if (nsh > 0) {
                 int64_t* scr = (int64_t*)b->scratch(2 * b->C * sizeof(int64_t) + 16);

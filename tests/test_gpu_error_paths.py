@@ -1,7 +1,7 @@
 """Error and normalisation paths (round-2 advisor findings):
 
 * an asynchronous (RB_INSERT_ASSUME_UNIQUE) insert rejected on the device
-  freezes the fused sampler enqueued behind it — no use counts, no RNG
+  freezes the fused sampler (and the prioritised one) enqueued behind it — no use counts, no RNG
   consumption — and the next synchronising call reports the error; the
   buffer then continues exactly like the reference, which never applied the
   rejected push (replay_buffer.cpp:85-88);
@@ -41,14 +41,15 @@ def _fill(cfg, oracle):
     return buf, ob, prod
 
 
+@pytest.mark.parametrize("strategy", ["uniform_with_replacement", "priority_with_replacement"])
 @pytest.mark.parametrize("shards", [1, 3])
-def test_rejected_async_insert_freezes_sampler(oracle, shards):
+def test_rejected_async_insert_freezes_sampler(oracle, shards, strategy):
     _need_gpu()
     from oracle.pyoracle import same_records
     from paper_2604_08706_b200 import Rng
 
     cfg = StepConfig(capacity=48 * shards, shards=shards, batch=12 * shards, group=4, lmax=40,
-                     ragged=True, seed=7)
+                     ragged=True, seed=7, strategy=strategy)
     buf, ob, prod = _fill(cfg, oracle)
     grng = Rng(cfg.seed).stream("buffer_sampling")
     orng = oracle.rng(cfg.seed).stream("buffer_sampling")
@@ -73,11 +74,13 @@ def test_rejected_async_insert_freezes_sampler(oracle, shards):
         assert same_records(grec, orec)
 
 
-def test_rejected_async_insert_reported_by_host_sample(oracle):
+@pytest.mark.parametrize("strategy", ["uniform_with_replacement", "priority_with_replacement"])
+def test_rejected_async_insert_reported_by_host_sample(oracle, strategy):
     _need_gpu()
     from paper_2604_08706_b200 import Rng
 
-    cfg = StepConfig(capacity=32, shards=1, batch=8, group=4, lmax=16, ragged=False, seed=3)
+    cfg = StepConfig(capacity=32, shards=1, batch=8, group=4, lmax=16, ragged=False, seed=3,
+                     strategy=strategy)
     buf, ob, prod = _fill(cfg, oracle)
     rec, length, tok, lpo, toff, _ = prod.groups(2, 1)
     bad = rec.copy()
