@@ -1957,16 +1957,19 @@ __device__ __forceinline__ unsigned long long prio_weight(const BufView& v, size
 // scan, so a rejected word shifts the later draws exactly as rng.cpp:40-51's
 // loop does.
 constexpr int PR_SMEM_CDF = 24576;  // 192 KB
+constexpr int PR_G = 4096;          // guide-table buckets (16 KB)
 constexpr int PR_R = 4;
 constexpr long long PR_CH = (long long)PR_THREADS * PR_R;  // words per chunk
 template <bool SM>
 __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r, SampleArgs a,
                                                             PrioParams p,
-                                                            unsigned long long* g_cdf /* >= C */) {
-    extern __shared__ unsigned long long s_cdf[];
+                                                            unsigned long long* g_cdf /* >= C + G/2 */) {
+    extern __shared__ unsigned long long s_cdf[];  // [C] cdf, then [PR_G] int32 guide
     __shared__ uint64_t s_mt[MT_N];
     __shared__ long long s_consumed;
     unsigned long long* cdf = SM ? s_cdf : g_cdf;
+    int* guide = reinterpret_cast<int*>(cdf + v.C);
+    RB_GCLOCK(8, true);
     // a rejected asynchronous insert before this call (sticky error): no
     // draws, the stream position unchanged; k_sample_map (chk_frozen) maps
     // an empty batch, as the fused uniform sampler does
@@ -1996,18 +1999,45 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
         for (long long i = threadIdx.x; i < n; i += PR_THREADS)
             cdf[i] = prio_weight(v, (size_t)s * v.C + arrival_slot_h(v, s, i, head), p);
         __syncthreads();
-        // inclusive scan: a contiguous run per thread, one block scan of the run sums
-        const long long per = (n + PR_THREADS - 1) / PR_THREADS;
-        const long long i0 = threadIdx.x * per, i1 = i0 + per < n ? i0 + per : n;
-        long long run = 0;
-        for (long long i = i0; i < i1; ++i) run += (long long)cdf[i];
+        RB_GCLOCK(9, s == 0);
+        // inclusive scan: a contiguous segment per warp, read 32 consecutive
+        // words at a time (conflict-free; a run per thread was a 32-way bank
+        // conflict, 26 us at 16384 records), then one block scan of the warp sums
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        const long long seg = ((n + PR_THREADS / 32 - 1) / (PR_THREADS / 32) + 31) & ~31LL;
+        const long long w0 = wid * seg, w1 = w0 + seg < n ? w0 + seg : n;
+        unsigned long long carry = 0;
+        for (long long c = w0; c < w1; c += 32) {
+            const long long i = c + lane;
+            unsigned long long x = i < w1 ? cdf[i] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (i < w1) cdf[i] = carry + x;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
         long long W;
-        long long acc = block_exclusive_scan(run, &W);
-        for (long long i = i0; i < i1; ++i) {
-            acc += (long long)cdf[i];
-            cdf[i] = (unsigned long long)acc;
+        const long long wbase = block_exclusive_scan(lane == 0 ? (long long)carry : 0, &W);
+        const unsigned long long off = __shfl_sync(0xffffffffu, (unsigned long long)wbase, 0);
+        if (off)
+            for (long long i = w0 + lane; i < w1; i += 32) cdf[i] += off;
+        __syncthreads();
+        // guide table: bucket b of values [b << sh, (b + 1) << sh) starts at the
+        // record holding value b << sh (each record writes the buckets whose
+        // first value it holds: they partition [0, W)), so a search is over
+        // [guide[b], guide[b + 1]] — usually one or two records
+        const int sh = max(0, 64 - __clzll((long long)W) - 12);  // W >> sh < PR_G
+        const int G = (int)(((uint64_t)W - 1) >> sh) + 1;
+        const unsigned long long msk = (1ULL << sh) - 1;
+        for (long long i = threadIdx.x; i < n; i += PR_THREADS) {
+            const unsigned long long prev = i ? cdf[i - 1] : 0;
+            const int b0 = (int)((prev + msk) >> sh), b1 = (int)((cdf[i] + msk) >> sh);
+            for (int b = b0; b < b1 && b < G; ++b) guide[b] = (int)i;
         }
         __syncthreads();
+        RB_GCLOCK(10, s == 0);
         const uint64_t lim = below_limit((uint64_t)W);
         long long got = 0;
         while (got < k) {
@@ -2016,6 +2046,7 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
                 ring_extend(r, s_mt, qhi, tgt);  // ends with a CTA barrier
                 qhi = tgt;
             }
+            RB_GCLOCK(11, s == 0 && got == 0);
             const long long ow = o + (long long)threadIdx.x * PR_R;
             uint64_t x[PR_R];
             unsigned okm = 0;
@@ -2032,29 +2063,36 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
             const long long need = k - got;
             if (threadIdx.x == 0) s_consumed = PR_CH;
             __syncthreads();
-            // the PR_R searches advance level by level together (ILP)
-            long long lo[PR_R], hi[PR_R];
+            RB_GCLOCK(12, s == 0 && got == 0);
+            // the PR_R searches advance together (ILP): upper_bound over the
+            // guide bucket's records [guide[b], guide[b + 1]]
+            int lo[PR_R], hi[PR_R];
             uint64_t xr[PR_R];
 #pragma unroll
             for (int j = 0; j < PR_R; ++j) {
                 const bool ok = (okm >> j) & 1u;
                 if (ok && rank == need - 1) s_consumed = (long long)threadIdx.x * PR_R + j + 1;
                 const bool take = ok && rank < need;
-                lo[j] = 0;
-                hi[j] = take ? n : 0;
                 xr[j] = take ? x[j] % (uint64_t)W : 0;
+                const int b = (int)(xr[j] >> sh);
+                lo[j] = take ? guide[b] : 0;
+                hi[j] = !take ? 0 : (b + 1 < G ? guide[b + 1] : (int)n);
                 rank += ok ? 1 : 0;
             }
-            for (long long span = n; span > 0; span >>= 1) {  // ceil(log2(n + 1)) levels
+            RB_GCLOCK(13, s == 0 && got == 0);
+            for (bool more = true; more;) {
+                more = false;
 #pragma unroll
                 for (int j = 0; j < PR_R; ++j) {
-                    if (lo[j] < hi[j]) {  // upper_bound: first i with cdf[i] > xr
-                        const long long mid = (lo[j] + hi[j]) >> 1;
+                    if (lo[j] < hi[j]) {
+                        const int mid = (lo[j] + hi[j]) >> 1;
                         if (cdf[mid] > xr[j]) hi[j] = mid;
                         else lo[j] = mid + 1;
+                        more |= lo[j] < hi[j];
                     }
                 }
             }
+            RB_GCLOCK(15, s == 0 && got == 0);
             rank -= cnt;
 #pragma unroll
             for (int j = 0; j < PR_R; ++j) {
@@ -2071,6 +2109,7 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
             __syncthreads();
         }
         pos += k;
+        RB_GCLOCK(14, s == 0);
     }
     if (threadIdx.x == 0) {
         long long q = q0;
@@ -3355,6 +3394,12 @@ void rb_buffer::host_stage_issued() {
 }
 void rb_buffer::join_lookahead() {
     if (!look_pending) return;
+    if (!look_captured && cudaEventQuery(look_ev) == cudaSuccess) {  // complete, uncaptured
+        look_pending = false;
+        joined_uid = look_uid;
+        joined_seq = look_seq;
+        return;
+    }
     RB_CUDA(cudaStreamWaitEvent(stream, look_ev, 0));
     look_pending = false;
     joined_uid = look_uid;
@@ -4323,6 +4368,7 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
             if (rng->gen_pending) {
                 if (!b->look_ev) RB_CUDA(cudaEventCreateWithFlags(&b->look_ev, cudaEventDisableTiming));
                 RB_CUDA(cudaEventRecord(b->look_ev, rng->gen_stream));
+                b->look_captured = rng->gen_captured;
                 b->look_pending = true;
                 b->look_uid = rng->uid;
                 b->look_seq = rng->gen_seq;
@@ -4332,13 +4378,14 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
             MtRing* ring = rng->to_device(b->stream);
             if (nsh > 0 && b->strategy == RB_PRIORITY_WITH_REPLACEMENT) {
                 const bool sm = b->C <= (size_t)PR_SMEM_CDF;
-                const size_t smem = sm ? b->C * sizeof(unsigned long long) : 0;
-                auto* cdf = sm ? nullptr
-                               : (unsigned long long*)b->scratch(b->C * sizeof(unsigned long long) + 16);
+                const size_t need_b = b->C * sizeof(unsigned long long) + PR_G * sizeof(int);
+                const size_t smem = sm ? need_b : 0;
+                auto* cdf = sm ? nullptr : (unsigned long long*)b->scratch(need_b + 16);
                 static bool attr_set = false;  // per process; the attribute is per function
                 if (!attr_set) {
                     RB_CUDA(cudaFuncSetAttribute(k_sample_prio<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)(PR_SMEM_CDF * sizeof(unsigned long long))));
+                                                 (int)(PR_SMEM_CDF * sizeof(unsigned long long) +
+                                                       PR_G * sizeof(int))));
                     attr_set = true;
                 }
                 if (sm)
@@ -4346,6 +4393,18 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                 else
                     k_sample_prio<false><<<1, PR_THREADS, 0, b->stream>>>(b->v, ring, a, b->prio, cdf);
                 RB_CUDA(cudaGetLastError());
+                // the next call's MT blocks, twisted on the Rng's side stream
+                // beside the rest of the step (joined by the next to_device)
+                if (b->lookahead) {
+                    rng->used_on(b->stream);
+                    rng->launch_lookahead(b->stream, (unsigned long long)nsel);
+                    if (!b->look_ev) RB_CUDA(cudaEventCreateWithFlags(&b->look_ev, cudaEventDisableTiming));
+                    RB_CUDA(cudaEventRecord(b->look_ev, rng->gen_stream));
+                    b->look_captured = rng->gen_captured;
+                    b->look_pending = true;
+                    b->look_uid = rng->uid;
+                    b->look_seq = rng->gen_seq;
+                }
             } else if (nsh > 0) {
                 int64_t* scr = (int64_t*)b->scratch(2 * b->C * sizeof(int64_t) + 16);
                 k_sample_without<<<1, 32, 0, b->stream>>>(b->v, ring, a, b->strategy, scr);

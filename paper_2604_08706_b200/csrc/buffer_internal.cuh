@@ -161,6 +161,7 @@ struct rb_buffer {
     bool lookahead = true;              // RB_NO_LOOKAHEAD unset
     long long lookahead_min_draws = 8192;  // side-stream lookahead above this batch
     unsigned long long look_uid = 0, look_seq = 0;  // the lookahead recorded in look_ev
+    bool look_captured = false;  // look_ev recorded inside a stream capture
     unsigned long long joined_uid = 0, joined_seq = 0;  // the last one joined on `stream`
     void join_lookahead();
     bool gather_early = false;          // the last kernel on the stream is the fused sampler

@@ -120,6 +120,12 @@ void rb_rng::wait_lookahead() {
 }
 void rb_rng::join(cudaStream_t s) {
     if (!gen_pending) return;
+    // a lookahead launched outside any capture and already complete needs no
+    // wait (and a capture must not wait on uncaptured work)
+    if (!gen_captured && cudaEventQuery(gen_done) == cudaSuccess) {
+        gen_pending = false;
+        return;
+    }
     RB_CUDA(cudaStreamWaitEvent(s, gen_done, 0));
     gen_pending = false;
 }
@@ -228,6 +234,9 @@ void rb_rng::launch_lookahead(cudaStream_t s, unsigned long long draws) {
     join(s);  // at most one lookahead in flight
     RB_CUDA(cudaEventRecord(gen_fork, s));
     RB_CUDA(cudaStreamWaitEvent(gen_stream, gen_fork, 0));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    RB_CUDA(cudaStreamIsCapturing(s, &cs));
+    gen_captured = cs != cudaStreamCaptureStatusNone;
     k_ring_lookahead<<<1, 32, 0, gen_stream>>>(dev, draws);
     RB_CUDA(cudaGetLastError());
     RB_CUDA(cudaEventRecord(gen_done, gen_stream));

@@ -36,6 +36,7 @@ struct rb_rng {
     cudaStream_t gen_stream = nullptr;   // lookahead stream (non-blocking)
     cudaEvent_t gen_fork = nullptr, gen_done = nullptr;
     bool gen_pending = false;            // a lookahead not yet joined by a device user
+    bool gen_captured = false;           // that lookahead was launched inside a stream capture
     unsigned long long gen_seq = 0;      // lookaheads launched (pairs with the joiner's record)
     unsigned long long uid = 0;          // process-unique id (buffers remember who they joined)
 };
