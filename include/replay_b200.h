@@ -321,6 +321,17 @@ int rb_retention(const rb_buffer* b, int* kind, double* delta);
  * record stays reachable), adv_scale <= 65536. */
 int rb_set_priority(rb_buffer* b, uint32_t base, uint32_t adv_scale, uint32_t pos_bonus);
 int rb_get_priority(const rb_buffer* b, uint32_t* base, uint32_t* adv_scale, uint32_t* pos_bonus);
+/* Priority mass per shard: out[s] = W_s = sum of the weights of shard s's
+ * records for the shards this process holds ([shard_begin, shard_end) of
+ * rb_create), 0 for the others (uint64, exact).  Host or device out[num_shards]. */
+int rb_priority_mass(rb_buffer* b, uint64_t* out);
+/* The priority-mass all-reduce (north star): rb_priority_mass into the
+ * device vector masses[num_shards], then ncclAllReduce(sum, uint64) in place
+ * on the buffer's stream through the caller's communicator (ncclComm_t, as
+ * rb_allreduce_loss_stats), so every rank holds every shard's mass.  The
+ * sampler itself needs no collective: it draws B/T per shard from the
+ * shard's own CDF (replay_buffer.cpp:193-204). */
+int rb_allreduce_priority_mass(rb_buffer* b, void* nccl_comm, uint64_t* masses);
 int rb_route_cursor(rb_buffer* b, size_t* out);
 
 /* dump/load (replay_buffer.cpp:238-324): byte-identical text format.

@@ -125,6 +125,8 @@ def _load():
         "rb_retention": (ip, [vp, vp, vp]),
         "rb_set_priority": (ip, [vp, C.c_uint32, C.c_uint32, C.c_uint32]),
         "rb_get_priority": (ip, [vp, vp, vp, vp]),
+        "rb_priority_mass": (ip, [vp, vp]),
+        "rb_allreduce_priority_mass": (ip, [vp, vp, vp]),
         "rb_route_cursor": (ip, [vp, vp]),
         "rb_dump": (ip, [vp, C.c_char_p, sz, vp]),
         "rb_load": (ip, [C.c_char_p, i32, ip, vp]),

@@ -2122,6 +2122,29 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
     }
 }
 
+// Per-shard priority mass W_s (uint64, exact, order-free): one CTA per owned
+// shard.  The all-reduce of these T-vectors over the ranks is the global
+// priority mass (rb_allreduce_priority_mass).
+__global__ void __launch_bounds__(256) k_prio_mass(BufView v, PrioParams p,
+                                                   unsigned long long* out) {
+    const int s = v.sb + (int)blockIdx.x;
+    const long long n = occupancy(v, s);
+    const int head = shard_head(v, s);
+    unsigned long long w = 0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x)
+        w += prio_weight(v, (size_t)s * v.C + arrival_slot_h(v, s, i, head), p);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    __shared__ unsigned long long s_w[8];
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += s_w[k];
+        out[s] = t;
+    }
+}
+
 // ---------------------------------------------------------------- FIFO route
 // FIFO routing + eviction + group advantages + metadata scatter for ids
 // promised new and increasing (replay_buffer.cpp:83-133 in closed form;
@@ -4776,6 +4799,35 @@ int rb_strategy(const rb_buffer* b, int* out) {
     *out = b->strategy;
     return RB_OK;
 }
+extern "C++" {
+namespace rb {
+void prio_mass_launch(rb_buffer* b, unsigned long long* out) {
+    RB_CUDA(cudaMemsetAsync(out, 0, b->T * sizeof(unsigned long long), b->stream));
+    k_prio_mass<<<(unsigned)(b->se - b->sb), 256, 0, b->stream>>>(b->v, b->prio, out);
+    RB_CUDA(cudaGetLastError());
+}
+}  // namespace rb
+}  // extern "C++"
+
+int rb_priority_mass(rb_buffer* b, uint64_t* out) {
+    return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);
+        DeviceScope ds(b->device);
+        if (!out) invalid("rb_priority_mass: NULL output");
+        if (b->async_unchecked) check_sticky(b);
+        b->other_work();
+        const bool host = !is_device_ptr(out);
+        auto* d = host ? (unsigned long long*)b->scratch(b->T * sizeof(uint64_t))
+                       : (unsigned long long*)out;
+        rb::prio_mass_launch(b, d);
+        if (host) {
+            RB_CUDA(cudaMemcpyAsync(out, d, b->T * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                    b->stream));
+            b->sync();
+        }
+    });
+}
+
 // priority_with_replacement weights (builder extension; k_sample_prio).
 int rb_set_priority(rb_buffer* b, uint32_t base, uint32_t adv_scale, uint32_t pos_bonus) {
     return guard([&] {

@@ -73,6 +73,10 @@ struct PrioParams {
 };
 
 int loss_grid(int sms);
+// priority_with_replacement: enqueue this buffer's per-shard priority mass
+// (sum of the record weights of owned shards [sb, se), 0 elsewhere) into
+// out[T] (device) on the buffer's stream (buffer.cu).
+void prio_mass_launch(struct ::rb_buffer* b, unsigned long long* out);
 struct GridCtl;  // buffer.cu: multi-CTA bookkeeping
 struct PendingIns {
     int pending;          // 1: the last insert (closed-form FIFO, <= 64 shards) may be running

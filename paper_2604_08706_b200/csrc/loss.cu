@@ -1349,6 +1349,27 @@ int rb_allreduce_loss_stats(rb_buffer* b, void* nccl_comm, float* dlogp, rb_loss
     });
 }
 
+// The north star's priority-mass all-reduce: this rank's per-shard masses
+// (owned shards, zeros elsewhere) summed in place over the communicator, so
+// every rank holds every shard's W_s (e.g. for importance weights w_i / W).
+int rb_allreduce_priority_mass(rb_buffer* b, void* nccl_comm, uint64_t* masses) {
+    return guard([&] {
+        std::lock_guard<std::recursive_mutex> lk(b->mu);
+        if (!nccl_comm) invalid("rb_allreduce_priority_mass: NULL communicator");
+        if (!masses || !is_device_ptr(masses))
+            invalid("rb_allreduce_priority_mass: device vector of num_shards uint64 required");
+        const NcclSyms& nc = nccl_syms();
+        if (!nc.allreduce) throw Error(RB_ECUDA, "rb_allreduce_priority_mass: libnccl.so.2 not found");
+        b->other_work();
+        rb::prio_mass_launch(b, (unsigned long long*)masses);
+        const ncclResult_t r = nc.allreduce(masses, masses, b->T, ncclUint64, ncclSum,
+                                            (ncclComm_t)nccl_comm, b->stream);
+        if (r != ncclSuccess)
+            throw Error(RB_ECUDA, std::string("ncclAllReduce: ") +
+                                      (nc.errstr ? nc.errstr(r) : std::to_string((int)r)));
+    });
+}
+
 int rb_loss_finalize_vec(rb_buffer* b, float* dlogp, const double* vec3, rb_loss_stats* stats) {
     return guard([&] {
         std::lock_guard<std::recursive_mutex> lk(b->mu);  // one total order (replay_buffer.cpp:84, 188)

@@ -237,6 +237,22 @@ class ShardedReplayBuffer:
         check(lib.rb_get_priority(self._h, C.byref(b), C.byref(a), C.byref(p)))
         return b.value, a.value, p.value
 
+    def priority_mass(self, out=None):
+        """Per-shard priority mass (rb_priority_mass): W_s for the shards this
+        buffer holds, 0 for the others.  out: a device uint64/int64 tensor of
+        num_shards (asynchronous) or None (returns a numpy uint64 array)."""
+        if out is None:
+            host = np.zeros(self.num_shards(), np.uint64)
+            check(lib.rb_priority_mass(self._h, host.ctypes.data))
+            return host
+        check(lib.rb_priority_mass(self._h, _ptr(out)))
+        return out
+
+    def allreduce_priority_mass(self, nccl_comm: int, masses) -> None:
+        """rb_allreduce_priority_mass: masses (device, num_shards x 64-bit) <-
+        the sum over the communicator's ranks of each rank's priority_mass."""
+        check(lib.rb_allreduce_priority_mass(self._h, C.c_void_p(nccl_comm), _ptr(masses)))
+
     def set_stream(self, stream) -> None:
         """Enqueue on an external stream (int handle, e.g. torch.cuda.current_stream().cuda_stream)."""
         check(lib.rb_set_stream(self._h, C.c_void_p(stream)))

@@ -93,3 +93,24 @@ def test_allreduce_loss_stats_needs_a_registered_vector(comm, oracle):
         buf.allreduce_loss_stats(comm, dl)
     with pytest.raises(ValueError, match="NULL communicator"):
         buf.allreduce_loss_stats(0, dl)
+
+
+def test_allreduce_priority_mass(comm):
+    """rb_allreduce_priority_mass at world size 1: the identity over
+    rb_priority_mass, which equals the numpy sum of the record weights."""
+    import paper_2604_08706_b200 as rb
+    from tests.test_priority import random_records, weights_np
+
+    buf = rb.ShardedReplayBuffer(3, 60, strategy="priority_with_replacement")
+    buf.set_priority(2, 4096, 777)
+    for r in random_records(np.random.default_rng(3), 50):
+        buf.push(r)
+    want = np.array([weights_np(buf.shard_contents(s), 2, 4096, 777).sum(dtype=np.uint64)
+                     for s in range(3)], np.uint64)
+    assert np.array_equal(buf.priority_mass(), want)
+    dev = torch.full((3,), -1, dtype=torch.int64, device="cuda:0")
+    buf.allreduce_priority_mass(comm, dev)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.cpu().numpy().view(np.uint64), want)
+    with pytest.raises(ValueError, match="device vector"):
+        buf.allreduce_priority_mass(comm, np.zeros(3, np.uint64))

@@ -203,3 +203,23 @@ def test_priority_gpu_api():
         heavy |= {(s, i) for i in range(len(c)) if abs(c[i]["advantage"]) > 30000}
     frac = np.mean([(int(s), int(i)) in heavy for s, i in zip(sh, ix)])
     assert heavy and frac > 0.9, frac
+
+
+@pytest.mark.gpu
+def test_priority_mass_owned_shards():
+    """rb_priority_mass: exact per-shard sums; a process holding shard 1 of 3
+    reports zeros for the others (its contribution to the all-reduce)."""
+    import paper_2604_08706_b200 as rb
+
+    recs = random_records(np.random.default_rng(4), 40)
+    full = rb.ShardedReplayBuffer(3, 30, strategy="priority_with_replacement")
+    part = rb.ShardedReplayBuffer(3, 30, strategy="priority_with_replacement",
+                                  shard_range=(1, 2))
+    for b in (full, part):
+        b.set_priority(1, 65536, 12345)
+        for r in recs:
+            b.push(r)
+    want = np.array([weights_np(full.shard_contents(s), 1, 65536, 12345).sum(dtype=np.uint64)
+                     for s in range(3)], np.uint64)
+    assert np.array_equal(full.priority_mass(), want)
+    assert np.array_equal(part.priority_mass(), np.array([0, want[1], 0], np.uint64))
