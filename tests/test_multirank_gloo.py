@@ -161,3 +161,62 @@ def test_two_rank_decomposition_matches_single_process():
         assert o0 == pytest.approx(obj, rel=1e-12) and o1 == pytest.approx(obj, rel=1e-12)
         np.testing.assert_allclose(np.concatenate([d0, d1]), d, rtol=1e-6, atol=1e-12)
         assert len(d0) == split
+
+
+# ---------------------------------------------------------------- priority mass
+def _prio_run(rank, world, port, q):
+    """Each rank: the replicated oracle buffer, its own shard's mass only
+    (rb_priority_mass's contribution), then the all-reduce."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.pyoracle import Oracle
+    from tests.test_priority import random_records, weights_np
+
+    ora = Oracle()
+    buf = ora.buffer(world, 40 * world, "priority_with_replacement", "plain_fifo", 0.0)
+    buf.set_priority(3, 2048, 99)
+    for r in random_records(np.random.default_rng(8), 70 * world):
+        buf.push(r)
+    mass = torch.zeros(world, dtype=torch.int64)
+    mass[rank] = int(weights_np(buf.shard_contents(rank), 3, 2048, 99).sum(dtype=np.uint64))
+    dist.all_reduce(mass)
+    # the prioritised draws of this rank's shard from the shared stream
+    rng = ora.rng(5).stream("buffer_sampling")
+    _, sh, ix = buf.sample(world * 16, rng)
+    q.put((rank, (mass.numpy().copy(), ix[sh == rank].copy())))
+    dist.destroy_process_group()
+
+
+def test_two_rank_priority_mass_allreduce():
+    """World size 2 (gloo): the all-reduced per-shard masses equal the
+    single-process masses, and each rank's slice of the prioritised draws
+    equals the single-process draws of its shard (B/T per shard)."""
+    import socket
+
+    from oracle.pyoracle import Oracle
+    from tests.test_priority import random_records, weights_np
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_prio_run, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ora = Oracle()
+    buf = ora.buffer(2, 80, "priority_with_replacement", "plain_fifo", 0.0)
+    buf.set_priority(3, 2048, 99)
+    for r in random_records(np.random.default_rng(8), 140):
+        buf.push(r)
+    want = [int(weights_np(buf.shard_contents(s), 3, 2048, 99).sum(dtype=np.uint64))
+            for s in range(2)]
+    _, sh, ix = buf.sample(32, ora.rng(5).stream("buffer_sampling"))
+    for rank in range(2):
+        mass, own = got[rank]
+        assert mass.tolist() == want
+        assert np.array_equal(own, ix[sh == rank])
