@@ -39,7 +39,7 @@ def _bench(config, *extra):
     return line
 
 
-@pytest.mark.parametrize("config", ["c4", "c1", "c2", "c3"])
+@pytest.mark.parametrize("config", ["c4", "c1", "c2", "c3", "c4prio"])
 def test_bench_step_matches_oracle_at_full_shape(config):
     line = _bench(config)
     chk = line["parity_check"]
