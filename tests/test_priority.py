@@ -143,6 +143,10 @@ PRIO_CASES = {
                                 ragged=True, seed=63, assume_unique=True, priority=(1, 0, 0)),
     "many_shards": dict(capacity=70 * 2, shards=70, batch=140, group=10, lmax=9, ragged=True,
                         seed=64, priority=(2, 65536, 7)),
+    # shards above 24576 records: CDF and guide table in global scratch (k_sample_prio<false>)
+    "cdf_in_global_memory": dict(capacity=2 * 25600, shards=2, batch=1024, group=16, lmax=4,
+                                 ragged=True, seed=66, assume_unique=True, prompts=64,
+                                 priority=(1, 30000, 2048)),
 }
 
 
