@@ -22,6 +22,9 @@ enum class SamplingStrategy {
     uniform_with_replacement,
     uniform_without_replacement,
     unused_first_without_replacement,
+    // builder extension (include/replay_b200.h RB_PRIORITY_WITH_REPLACEMENT):
+    // weighted draws over an integer CDF; set_priority() sets the weights
+    priority_with_replacement,
 };
 
 inline std::string to_string(SamplingStrategy s) {  // replay_buffer.cpp:11-21
@@ -30,6 +33,7 @@ inline std::string to_string(SamplingStrategy s) {  // replay_buffer.cpp:11-21
         case SamplingStrategy::uniform_without_replacement: return "uniform_without_replacement";
         case SamplingStrategy::unused_first_without_replacement:
             return "unused_first_without_replacement";
+        case SamplingStrategy::priority_with_replacement: return "priority_with_replacement";
     }
     throw std::logic_error("bad SamplingStrategy");
 }
@@ -39,6 +43,7 @@ inline SamplingStrategy sampling_strategy_from_string(std::string_view s) {  // 
     if (s == "uniform_without_replacement") return SamplingStrategy::uniform_without_replacement;
     if (s == "unused_first_without_replacement")
         return SamplingStrategy::unused_first_without_replacement;
+    if (s == "priority_with_replacement") return SamplingStrategy::priority_with_replacement;
     throw std::invalid_argument("unknown sampling strategy: '" + std::string(s) + "'");
 }
 
@@ -152,6 +157,18 @@ public:
         v.reserve(n);
         for (std::size_t i = 0; i < n; ++i) v.push_back(RolloutRecord::from_rb(out[i]));
         return v;
+    }
+
+    // priority_with_replacement weights: w = base + floor(min(|advantage|, 2^15)
+    // * adv_scale) + pos_bonus * [reward > 0] (rb_set_priority)
+    void set_priority(std::uint32_t base, std::uint32_t adv_scale, std::uint32_t pos_bonus) {
+        detail::rb_check(rb_set_priority(h_.get(), base, adv_scale, pos_bonus));
+    }
+    // per-shard priority mass of the shards this process holds (rb_priority_mass)
+    std::vector<std::uint64_t> priority_mass() const {
+        std::vector<std::uint64_t> m(num_shards());
+        detail::rb_check(rb_priority_mass(h_.get(), m.data()));
+        return m;
     }
 
     SamplingStrategy strategy() const {
