@@ -1956,19 +1956,22 @@ __device__ __forceinline__ unsigned long long prio_weight(const BufView& v, size
 // thread: the accept flags (x < below_limit(W)) are ranked by one block
 // scan, so a rejected word shifts the later draws exactly as rng.cpp:40-51's
 // loop does.
-constexpr int PR_SMEM_CDF = 24576;  // 192 KB
+constexpr int PR_SMEM_CDF = 22528;  // 187 KB padded
 constexpr int PR_G = 4096;          // guide-table buckets (16 KB)
+// CDF word i lives at i + i / 16 (one pad word per 16: per-thread runs of 16
+// read distinct banks)
+__host__ __device__ __forceinline__ long long pr_pad(long long i) { return i + (i >> 4); }
 constexpr int PR_R = 4;
 constexpr long long PR_CH = (long long)PR_THREADS * PR_R;  // words per chunk
 template <bool SM>
 __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r, SampleArgs a,
                                                             PrioParams p,
                                                             unsigned long long* g_cdf /* >= C + G/2 */) {
-    extern __shared__ unsigned long long s_cdf[];  // [C] cdf, then [PR_G] int32 guide
+    extern __shared__ unsigned long long s_cdf[];  // [pr_pad(C)] cdf, then [PR_G] int32 guide
     __shared__ uint64_t s_mt[MT_N];
     __shared__ long long s_consumed;
     unsigned long long* cdf = SM ? s_cdf : g_cdf;
-    int* guide = reinterpret_cast<int*>(cdf + v.C);
+    int* guide = reinterpret_cast<int*>(cdf + pr_pad(v.C));
     RB_GCLOCK(8, true);
     // a rejected asynchronous insert before this call (sticky error): no
     // draws, the stream position unchanged; k_sample_map (chk_frozen) maps
@@ -1999,32 +2002,23 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
         // shuffles: 12.6 vs 5.4 us at 16384 records)
 #pragma unroll 8
         for (long long i = threadIdx.x; i < n; i += PR_THREADS)
-            cdf[i] = prio_weight(v, (size_t)s * v.C + arrival_slot_h(v, s, i, head), p);
+            cdf[pr_pad(i)] = prio_weight(v, (size_t)s * v.C + arrival_slot_h(v, s, i, head), p);
         __syncthreads();
         RB_GCLOCK(9, s == 0);
-        // inclusive scan: a contiguous segment per warp, read 32 consecutive
-        // words at a time (conflict-free; a run per thread was a 32-way bank
-        // conflict, 26 us at 16384 records), then one block scan of the warp sums
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        const long long seg = ((n + PR_THREADS / 32 - 1) / (PR_THREADS / 32) + 31) & ~31LL;
-        const long long w0 = wid * seg, w1 = w0 + seg < n ? w0 + seg : n;
-        unsigned long long carry = 0;
-        for (long long c = w0; c < w1; c += 32) {
-            const long long i = c + lane;
-            unsigned long long x = i < w1 ? cdf[i] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (i < w1) cdf[i] = carry + x;
-            carry += __shfl_sync(0xffffffffu, x, 31);
-        }
+        // inclusive scan: a contiguous run per thread in registers (the CDF is
+        // padded one word per 16, so the runs' strided reads are free of bank
+        // conflicts — unpadded they were 32-way, 26 us at 16384 records; a
+        // warp-segment shuffle scan took 10 us), one block scan of the run sums
+        const long long per = (n + PR_THREADS - 1) / PR_THREADS;
+        const long long i0 = threadIdx.x * per, i1 = i0 + per < n ? i0 + per : n;
+        long long run = 0;
+        for (long long i = i0; i < i1; ++i) run += (long long)cdf[pr_pad(i)];
         long long W;
-        const long long wbase = block_exclusive_scan(lane == 0 ? (long long)carry : 0, &W);
-        const unsigned long long off = __shfl_sync(0xffffffffu, (unsigned long long)wbase, 0);
-        if (off)
-            for (long long i = w0 + lane; i < w1; i += 32) cdf[i] += off;
+        long long acc = block_exclusive_scan(run, &W);
+        for (long long i = i0; i < i1; ++i) {
+            acc += (long long)cdf[pr_pad(i)];
+            cdf[pr_pad(i)] = (unsigned long long)acc;
+        }
         __syncthreads();
         // guide table: bucket b of values [b << sh, (b + 1) << sh) starts at the
         // record holding value b << sh (each record writes the buckets whose
@@ -2034,8 +2028,8 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
         const int G = (int)(((uint64_t)W - 1) >> sh) + 1;
         const unsigned long long msk = (1ULL << sh) - 1;
         for (long long i = threadIdx.x; i < n; i += PR_THREADS) {
-            const unsigned long long prev = i ? cdf[i - 1] : 0;
-            const int b0 = (int)((prev + msk) >> sh), b1 = (int)((cdf[i] + msk) >> sh);
+            const unsigned long long prev = i ? cdf[pr_pad(i - 1)] : 0;
+            const int b0 = (int)((prev + msk) >> sh), b1 = (int)((cdf[pr_pad(i)] + msk) >> sh);
             for (int b = b0; b < b1 && b < G; ++b) guide[b] = (int)i;
         }
         __syncthreads();
@@ -2088,7 +2082,7 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
                 for (int j = 0; j < PR_R; ++j) {
                     if (lo[j] < hi[j]) {
                         const int mid = (lo[j] + hi[j]) >> 1;
-                        if (cdf[mid] > xr[j]) hi[j] = mid;
+                        if (cdf[pr_pad(mid)] > xr[j]) hi[j] = mid;
                         else lo[j] = mid + 1;
                         more |= lo[j] < hi[j];
                     }
@@ -4403,13 +4397,14 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
             MtRing* ring = rng->to_device(b->stream);
             if (nsh > 0 && b->strategy == RB_PRIORITY_WITH_REPLACEMENT) {
                 const bool sm = b->C <= (size_t)PR_SMEM_CDF;
-                const size_t need_b = b->C * sizeof(unsigned long long) + PR_G * sizeof(int);
+                const size_t need_b = (size_t)pr_pad((long long)b->C) * sizeof(unsigned long long) +
+                                      PR_G * sizeof(int);
                 const size_t smem = sm ? need_b : 0;
                 auto* cdf = sm ? nullptr : (unsigned long long*)b->scratch(need_b + 16);
                 static bool attr_set = false;  // per process; the attribute is per function
                 if (!attr_set) {
                     RB_CUDA(cudaFuncSetAttribute(k_sample_prio<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)(PR_SMEM_CDF * sizeof(unsigned long long) +
+                                                 (int)(pr_pad(PR_SMEM_CDF) * sizeof(unsigned long long) +
                                                        PR_G * sizeof(int))));
                     attr_set = true;
                 }
