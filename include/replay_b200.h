@@ -318,7 +318,9 @@ int rb_retention(const rb_buffer* b, int* kind, double* delta);
  * draw is index = upper_bound(cdf, rng.below(W)) over the shard's arrival
  * order, shards in order, B/T draws each as rb_sample.  Defaults (1, 0, 0)
  * reproduce uniform_with_replacement draw for draw.  base >= 1 (every
- * record stays reachable), adv_scale <= 65536. */
+ * record stays reachable), adv_scale <= 65536.  The weights are a setting
+ * of the buffer object, not of its contents: rb_dump / rb_snapshot do not
+ * carry them (set them again after rb_load / rb_restore). */
 int rb_set_priority(rb_buffer* b, uint32_t base, uint32_t adv_scale, uint32_t pos_bonus);
 int rb_get_priority(const rb_buffer* b, uint32_t* base, uint32_t* adv_scale, uint32_t* pos_bonus);
 /* Priority mass per shard: out[s] = W_s = sum of the weights of shard s's
