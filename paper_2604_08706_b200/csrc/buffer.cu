@@ -1963,15 +1963,17 @@ constexpr int PR_G = 4096;          // guide-table buckets (16 KB)
 __host__ __device__ __forceinline__ long long pr_pad(long long i) { return i + (i >> 4); }
 constexpr int PR_R = 4;
 constexpr long long PR_CH = (long long)PR_THREADS * PR_R;  // words per chunk
+constexpr int PR_MS = 64;  // all-shards-at-once path: at most this many shards
 template <bool SM>
 __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r, SampleArgs a,
                                                             PrioParams p,
-                                                            unsigned long long* g_cdf /* >= C + G/2 */) {
-    extern __shared__ unsigned long long s_cdf[];  // [pr_pad(C)] cdf, then [PR_G] int32 guide
+                                                            unsigned long long* g_cdf,
+                                                            long long cdf_cap /* >= C */) {
+    extern __shared__ unsigned long long s_cdf[];  // [pr_pad(cap)] cdf, then [PR_G] int32 guide
     __shared__ uint64_t s_mt[MT_N];
     __shared__ long long s_consumed;
     unsigned long long* cdf = SM ? s_cdf : g_cdf;
-    int* guide = reinterpret_cast<int*>(cdf + pr_pad(v.C));
+    int* guide = reinterpret_cast<int*>(cdf + pr_pad(cdf_cap));
     RB_GCLOCK(8, true);
     // a rejected asynchronous insert before this call (sticky error): no
     // draws, the stream position unchanged; k_sample_map (chk_frozen) maps
@@ -1994,6 +1996,129 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
         const long long last = q0 + ((long long)idx0 + oo + PR_CH - 1) / MT_N;
         return last < first + MT_KR - 1 ? last : first + MT_KR - 1;
     };
+    // ---- several shards at once: one CDF over all their records (each
+    // shard's values are differences from the prefix before it), per-shard
+    // guide segments, and the draws taken as if no below() rejection occurs
+    // (probability < W / 2^64 per draw), which the same pass verifies; any
+    // rejection falls back to the shard-by-shard loop below (same ring).
+    __shared__ long long s_base[PR_MS + 1];
+    __shared__ unsigned long long s_pre[PR_MS], s_W[PR_MS], s_lim[PR_MS];
+    __shared__ int s_head[PR_MS], s_sh[PR_MS], s_G[PR_MS], s_flag;
+    const long long D = (long long)a.nsh * a.per;
+    if (SM && a.nsh > 1 && a.nsh <= PR_MS && D <= 60000) {
+        const int T = a.nsh;
+        if (threadIdx.x < T) {
+            s_base[threadIdx.x + 1] = occupancy(v, threadIdx.x);
+            s_head[threadIdx.x] = shard_head(v, threadIdx.x);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_base[0] = 0;
+            for (int t = 0; t < T; ++t) s_base[t + 1] += s_base[t];
+            s_flag = 0;
+        }
+        __syncthreads();
+        const long long M = s_base[T], k = a.per;
+        auto shard_of = [&](long long g) {  // last t with s_base[t] <= g
+            int lo = 0, hi = T;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_base[mid] <= g) lo = mid;
+                else hi = mid;
+            }
+            return lo;
+        };
+        if (M <= cdf_cap) {
+#pragma unroll 4
+            for (long long g = threadIdx.x; g < M; g += PR_THREADS) {
+                const int t = shard_of(g);
+                const long long i = g - s_base[t];
+                cdf[pr_pad(g)] = prio_weight(
+                    v, (size_t)t * v.C + arrival_slot_h(v, t, i, s_head[t]), p);
+            }
+            __syncthreads();
+            const long long per = (M + PR_THREADS - 1) / PR_THREADS;
+            const long long i0 = threadIdx.x * per, i1 = i0 + per < M ? i0 + per : M;
+            long long run = 0;
+            for (long long i = i0; i < i1; ++i) run += (long long)cdf[pr_pad(i)];
+            long long tot;
+            long long acc = block_exclusive_scan(run, &tot);
+            for (long long i = i0; i < i1; ++i) {
+                acc += (long long)cdf[pr_pad(i)];
+                cdf[pr_pad(i)] = (unsigned long long)acc;
+            }
+            __syncthreads();
+            const int gbits = 31 - __clz(PR_G / T);  // guide buckets per shard: 2^gbits
+            if (threadIdx.x < T) {
+                const int t = threadIdx.x;
+                const unsigned long long pre = s_base[t] ? cdf[pr_pad(s_base[t] - 1)] : 0;
+                const unsigned long long W = cdf[pr_pad(s_base[t + 1] - 1)] - pre;
+                s_pre[t] = pre;
+                s_W[t] = W;
+                s_lim[t] = below_limit(W);
+                s_sh[t] = max(0, 64 - __clzll((long long)W) - gbits);
+                s_G[t] = (int)((W - 1) >> s_sh[t]) + 1;
+            }
+            __syncthreads();
+            for (long long g = threadIdx.x; g < M; g += PR_THREADS) {
+                const int t = shard_of(g);
+                const long long i = g - s_base[t];
+                const unsigned long long prev = (i ? cdf[pr_pad(g - 1)] : s_pre[t]) - s_pre[t];
+                const unsigned long long cur = cdf[pr_pad(g)] - s_pre[t];
+                const int sh = s_sh[t];
+                const unsigned long long msk = (1ULL << sh) - 1;
+                const int b0 = (int)((prev + msk) >> sh), b1 = (int)((cur + msk) >> sh);
+                for (int b = b0; b < b1 && b < s_G[t]; ++b) guide[(t << gbits) + b] = (int)i;
+            }
+            __syncthreads();
+            for (long long c = 0; c < D; c += PR_CH) {
+                const long long tgt = chunk_target(c);
+                if (tgt > qhi) {
+                    ring_extend(r, s_mt, qhi, tgt);  // ends with a CTA barrier
+                    qhi = tgt;
+                }
+#pragma unroll
+                for (int j = 0; j < PR_R; ++j) {
+                    const long long d = c + (long long)threadIdx.x * PR_R + j;
+                    if (d >= D) continue;
+                    const long long gw = (long long)idx0 + d;
+                    const uint64_t x = mt_temper(__ldcg(&r->blk[(q0 + gw / MT_N) % MT_KR][gw % MT_N]));
+                    const int t = (int)(d / k);
+                    if (x >= s_lim[t]) {
+                        s_flag = 1;
+                        continue;
+                    }
+                    const unsigned long long xr = x % s_W[t], pre = s_pre[t];
+                    const int b = (int)(xr >> s_sh[t]);
+                    int lo = guide[(t << gbits) + b];
+                    int hi = b + 1 < s_G[t] ? guide[(t << gbits) + b + 1]
+                                            : (int)(s_base[t + 1] - s_base[t]);
+                    const long long bt = s_base[t];
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (cdf[pr_pad(bt + mid)] - pre > xr) hi = mid;
+                        else lo = mid + 1;
+                    }
+                    a.sel_shard[d] = t;
+                    a.sel_index[d] = lo;
+                }
+            }
+            __syncthreads();
+            if (!s_flag && !v.dbg_replay) {  // (tests: RB_DEBUG_FORCE_DRAW_REPLAY takes the fallback)
+                if (threadIdx.x == 0) {
+                    long long q = q0;
+                    uint32_t idx = idx0;
+                    ring_advance(q, idx, (unsigned long long)D);
+                    r->q_state = q;
+                    r->q_hi = qhi > q ? qhi : q;
+                    r->idx = idx;
+                    r->draws = draws0 + (uint64_t)D;
+                }
+                return;
+            }
+            // a rejection: the exact shard-by-shard loop (the ring blocks stay)
+        }
+    }
     for (int s = 0; s < a.nsh; ++s) {
         const long long n = occupancy(v, s), k = a.per;
         const int head = shard_head(v, s);
@@ -4396,8 +4521,10 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
         } else {
             MtRing* ring = rng->to_device(b->stream);
             if (nsh > 0 && b->strategy == RB_PRIORITY_WITH_REPLACEMENT) {
-                const bool sm = b->C <= (size_t)PR_SMEM_CDF;
-                const size_t need_b = (size_t)pr_pad((long long)b->C) * sizeof(unsigned long long) +
+                // several shards' records at once when they all fit in shared memory
+                const size_t cap = (b->T > 1 && b->N <= (size_t)PR_SMEM_CDF) ? b->N : b->C;
+                const bool sm = cap <= (size_t)PR_SMEM_CDF;
+                const size_t need_b = (size_t)pr_pad((long long)cap) * sizeof(unsigned long long) +
                                       PR_G * sizeof(int);
                 const size_t smem = sm ? need_b : 0;
                 auto* cdf = sm ? nullptr : (unsigned long long*)b->scratch(need_b + 16);
@@ -4409,9 +4536,11 @@ int rb_sample(rb_buffer* b, size_t batch_size, rb_rng* rng, rb_record* out_recor
                     attr_set = true;
                 }
                 if (sm)
-                    k_sample_prio<true><<<1, PR_THREADS, smem, b->stream>>>(b->v, ring, a, b->prio, cdf);
+                    k_sample_prio<true><<<1, PR_THREADS, smem, b->stream>>>(b->v, ring, a, b->prio, cdf,
+                                                                            (long long)cap);
                 else
-                    k_sample_prio<false><<<1, PR_THREADS, 0, b->stream>>>(b->v, ring, a, b->prio, cdf);
+                    k_sample_prio<false><<<1, PR_THREADS, 0, b->stream>>>(b->v, ring, a, b->prio, cdf,
+                                                                         (long long)cap);
                 RB_CUDA(cudaGetLastError());
             } else if (nsh > 0) {
                 int64_t* scr = (int64_t*)b->scratch(2 * b->C * sizeof(int64_t) + 16);

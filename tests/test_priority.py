@@ -227,3 +227,31 @@ def test_priority_mass_owned_shards():
                      for s in range(3)], np.uint64)
     assert np.array_equal(full.priority_mass(), want)
     assert np.array_equal(part.priority_mass(), np.array([0, want[1], 0], np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["adv_two_shards", "bonus_posbias"])
+def test_priority_multi_shard_fallback(name, monkeypatch):
+    """Several shards are drawn in one pass that assumes no below() rejection;
+    a rejection (probability < W/2^64 per draw) falls back to the exact
+    shard-by-shard loop over the same ring.  RB_DEBUG_FORCE_DRAW_REPLAY forces
+    that fallback after every optimistic pass: still bit-exact."""
+    from oracle.pyoracle import Oracle
+    from tests.harness import StepConfig, run_step_parity
+
+    monkeypatch.setenv("RB_DEBUG_FORCE_DRAW_REPLAY", "1")
+    cfg = StepConfig(strategy="priority_with_replacement", **PRIO_CASES[name])
+    run_step_parity(cfg, steps=4, ora=Oracle())
+
+
+@pytest.mark.gpu
+def test_priority_eight_shards_c4_shape():
+    """C4 split into 8 shards (16384 records, 512 draws each): the
+    all-shards-at-once pass, bit-exact vs the oracle."""
+    from oracle.pyoracle import Oracle
+    from tests.harness import StepConfig, run_step_parity
+
+    cfg = StepConfig(capacity=16384, shards=8, batch=4096, group=16, lmax=4, ragged=True,
+                     seed=67, prompts=256, assume_unique=True,
+                     strategy="priority_with_replacement", priority=(1, 65536, 4096))
+    run_step_parity(cfg, steps=3, ora=Oracle(), check_every=3)

@@ -16,12 +16,12 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def run(cap, batch, strategy, prio, iters=50):
+def run(cap, batch, strategy, prio, iters=50, shards=1):
     import torch
 
     import paper_2604_08706_b200 as rb
 
-    b = rb.ShardedReplayBuffer(1, cap, strategy=strategy)
+    b = rb.ShardedReplayBuffer(shards, cap, strategy=strategy)
     b.set_stream(torch.cuda.current_stream().cuda_stream)
     if prio is not None:
         b.set_priority(*prio)
@@ -45,12 +45,13 @@ def run(cap, batch, strategy, prio, iters=50):
 
 
 def main():
-    for cap, batch, shape in [(16384, 4096, "C4"), (1024, 1024, "C3")]:
+    for cap, batch, shape, shards in [(16384, 4096, "C4", 1), (1024, 1024, "C3", 1),
+                                      (16384, 4096, "C4 in 8 shards", 8)]:
         for strategy, prio in [("uniform_with_replacement", None),
                                ("priority_with_replacement", (1, 0, 0)),
                                ("priority_with_replacement", (1, 65536, 4096))]:
-            us = run(cap, batch, strategy, prio)
-            print(json.dumps({"shape": shape, "capacity": cap, "batch": batch,
+            us = run(cap, batch, strategy, prio, shards=shards)
+            print(json.dumps({"shape": shape, "capacity": cap, "batch": batch, "shards": shards,
                               "strategy": strategy, "priority": prio,
                               "us_per_sample_call": round(us, 2)}), flush=True)
 
