@@ -2002,7 +2002,7 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
     // (probability < W / 2^64 per draw), which the same pass verifies; any
     // rejection falls back to the shard-by-shard loop below (same ring).
     __shared__ long long s_base[PR_MS + 1];
-    __shared__ unsigned long long s_pre[PR_MS], s_W[PR_MS], s_lim[PR_MS];
+    __shared__ unsigned long long s_pre[PR_MS], s_W[PR_MS], s_lim[PR_MS], s_mag[PR_MS];
     __shared__ int s_head[PR_MS], s_sh[PR_MS], s_G[PR_MS], s_flag;
     const long long D = (long long)a.nsh * a.per;
     if (SM && a.nsh > 1 && a.nsh <= PR_MS && D <= 60000) {
@@ -2056,6 +2056,7 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
                 s_pre[t] = pre;
                 s_W[t] = W;
                 s_lim[t] = below_limit(W);
+                s_mag[t] = UINT64_MAX / W;  // fast_mod's reciprocal (one division per shard)
                 s_sh[t] = max(0, 64 - __clzll((long long)W) - gbits);
                 s_G[t] = (int)((W - 1) >> s_sh[t]) + 1;
             }
@@ -2088,7 +2089,7 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
                         s_flag = 1;
                         continue;
                     }
-                    const unsigned long long xr = x % s_W[t], pre = s_pre[t];
+                    const unsigned long long xr = fast_mod(x, s_W[t], s_mag[t]), pre = s_pre[t];
                     const int b = (int)(xr >> s_sh[t]);
                     int lo = guide[(t << gbits) + b];
                     int hi = b + 1 < s_G[t] ? guide[(t << gbits) + b + 1]
@@ -2160,6 +2161,7 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
         __syncthreads();
         RB_GCLOCK(10, s == 0);
         const uint64_t lim = below_limit((uint64_t)W);
+        const uint64_t mag = UINT64_MAX / (uint64_t)W;  // x % W by multiply-high (fast_mod)
         long long got = 0;
         while (got < k) {
             const long long tgt = chunk_target(o);
@@ -2194,7 +2196,7 @@ __global__ void __launch_bounds__(PR_THREADS) k_sample_prio(BufView v, MtRing* r
                 const bool ok = (okm >> j) & 1u;
                 if (ok && rank == need - 1) s_consumed = (long long)threadIdx.x * PR_R + j + 1;
                 const bool take = ok && rank < need;
-                xr[j] = take ? x[j] % (uint64_t)W : 0;
+                xr[j] = take ? fast_mod(x[j], (uint64_t)W, mag) : 0;
                 const int b = (int)(xr[j] >> sh);
                 lo[j] = take ? guide[b] : 0;
                 hi[j] = !take ? 0 : (b + 1 < G ? guide[b + 1] : (int)n);
