@@ -13,7 +13,7 @@ from paper_2604_08706_b200 import _lib  # noqa: E402
 from tools.prio_probe import run  # noqa: E402
 
 _lib.lib.rb_debug_phase_clocks.argtypes = [C.c_void_p]
-for cap, batch in [(16384, 4096), (16384, 512), (1024, 4096), (1024, 1024)]:
+for cap, batch in [(16384, 4096), (16384, 512), (1024, 4096), (1024, 1024)]:  # one shard
     us = run(cap, batch, "priority_with_replacement", (1, 65536, 4096), iters=5)
     torch.cuda.synchronize()
     out = (C.c_longlong * 64)()
