@@ -1,6 +1,7 @@
 """Time one sampling call (rb_sample, device outputs only) of the
 priority_with_replacement strategy against uniform_with_replacement on the
-C4 (16384 / B = 4096) and C3 (1024 / B = 1024) buffer shapes, metadata only.
+C4 (16384 / B = 4096, one shard and 8 shards) and C3 (1024 / B = 1024) buffer
+shapes, metadata only.  Back-to-back eager calls: host launch overhead included.
 CUDA events on the buffer's stream (torch's current stream), after warm-up.
 
     python tools/prio_probe.py  ->  one JSON line per (shape, strategy)
