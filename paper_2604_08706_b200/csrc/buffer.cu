@@ -3847,6 +3847,7 @@ rb_buffer* create(size_t T, size_t N, int strategy, int retention, double delta,
         b->loss_dyn = std::getenv("RB_LOSS_CHUNK_MAJOR") == nullptr;
         b->tma_long = std::getenv("RB_PAYLOAD_TMA_LONG") != nullptr;
         b->chunk_major = std::getenv("RB_NO_CHUNK_MAJOR") == nullptr;
+        b->tma_ctas = PB_CTAS;  // the build default (RB_PB_CTAS), overridable per process
         if (const char* e = std::getenv("RB_TMA_CTAS")) b->tma_ctas = std::max(1, std::atoi(e));
         b->sms = sms;
         RB_CUDA(cudaFuncSetAttribute(k_insert_payload_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
